@@ -1,0 +1,126 @@
+/*
+ * tetmf_b200 -- C ABI of the B200 matrix-free operator apply.
+ *
+ * This is the drop-in boundary for the reference's operator layer
+ * (/root/reference/pkg/src/tetmf/operator.py).  One plan replaces one operator
+ * object of the reference:
+ *
+ *   tmf_plan_create   <- CgPoissonOperator.__init__   operator.py:314-318
+ *                        DgSipgOperator.__init__      operator.py:449-454
+ *                        HelmholtzOperator.__init__   operator.py:473-479
+ *                        (+ _OperatorBase.__init__ operator.py:190-223 and
+ *                           _DgFaceMixin._setup_faces operator.py:337-385)
+ *   tmf_apply         <- <Operator>.apply(u) -> y      operator.py:320-331,
+ *                        456-466, 481-493 (device pointers, stream-ordered)
+ *   tmf_apply_host    <- the same with host buffers (copies inside; the call the
+ *                        Python shim makes for NumPy inputs)
+ *   tmf_diagonal      <- sparse.assemble(...).diagonal()   sparse.py:237-243
+ *                        (matrix-free, used by the Jacobi preconditioner)
+ *   tmf_pcg           <- SPEC.md:509-517 cg_solve with point-Jacobi (absent
+ *                        from the reference package; fixed iteration count)
+ *   tmf_last_error    <- the ValueError / RuntimeError messages of the
+ *                        reference (operator.py:305-308 etc.)
+ *
+ * All pointers in tmf_plan_desc are HOST pointers; the plan copies what it
+ * needs to the device and the caller keeps ownership.  Status codes: 0 = ok,
+ * TMF_EINVAL = invalid argument (Python: ValueError), TMF_ECUDA = CUDA
+ * failure / no device (Python: RuntimeError).  The library has no CPU
+ * fallback: every apply runs on the GPU or fails.
+ */
+#ifndef TETMF_B200_H
+#define TETMF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TMF_OK 0
+#define TMF_EINVAL 1
+#define TMF_ECUDA 2
+
+/* operator kinds */
+#define TMF_CG_LAPLACE 0     /* CgPoissonOperator                                   */
+#define TMF_DG_SIPG 1        /* DgSipgOperator                                      */
+#define TMF_DG_HELMHOLTZ 2   /* mass_scale*M + diffusivity*(kappa-)SIPG; n_comp 1|3  */
+
+typedef struct tmf_plan tmf_plan;
+
+typedef struct tmf_plan_desc {
+  int32_t operator_kind;
+  int32_t degree;              /* 1..4                                              */
+  int32_t n_dofs_per_cell;     /* (p+1)(p+2)(p+3)/6                                 */
+  int32_t n_components;        /* 1, or 3 interleaved (index = scalar*3 + c)        */
+  int64_t n_vertices;
+  int64_t n_cells;
+  int64_t n_scalar_dofs;
+  const double* vertices;      /* (n_vertices, 3)                                    */
+  const int32_t* cells;        /* (n_cells, 4), positively oriented                  */
+  const int32_t* cell_dofs;    /* (n_cells, n_dpc) CG numbering; NULL for DG         */
+  const uint8_t* dirichlet_mask; /* (n_scalar_dofs,) CG strong Dirichlet, or NULL   */
+  int32_t n_q;
+  int32_t n_qf;
+  const double* cell_weights;  /* (n_q,)                                             */
+  const double* value_matrix;  /* (n_q, n_dpc)                                       */
+  const double* grad_matrix;   /* (3 n_q, n_dpc), row 3*i + k                        */
+  const double* face_weights;  /* (n_qf,)                         DG only            */
+  const double* face_values;   /* (4, 6, n_qf, n_dpc)             DG only            */
+  const double* face_grads;    /* (4, 6, 3 n_qf, n_dpc)           DG only            */
+  int64_t n_interior_faces;
+  const int32_t* interior_faces; /* (n_if, 5): c-, lf-, c+, lf+, code                */
+  const double* tau_interior;  /* (n_if,)                                            */
+  int64_t n_boundary_faces;
+  const int32_t* boundary_faces; /* (n_bf, 3): cell, lf, boundary id                 */
+  const double* tau_boundary;  /* (n_bf,)                                            */
+  const uint8_t* boundary_dirichlet; /* (n_bf,) 1 = weak Dirichlet (SIPG) face       */
+  const double* kappa;         /* (n_cells,) per-cell Laplace coefficient, or NULL   */
+  double mass_scale;           /* Helmholtz mass coefficient                          */
+  double diffusivity;          /* Laplace/SIPG scale (nu)                             */
+  int32_t device;              /* CUDA device ordinal                                 */
+  int32_t flags;               /* reserved, 0                                         */
+} tmf_plan_desc;
+
+typedef struct tmf_plan_info {
+  int64_t n_global_dofs;       /* n_scalar_dofs * n_components                       */
+  double flops_alg;            /* reference counter flops per apply     */
+  double bytes_alg;            /* compulsory HBM bytes per apply         */
+  double flops_issued;         /* FP64 FMA*2 the kernels actually issue (padding incl.) */
+  int32_t kernels_per_apply;   /* kernel launches per tmf_apply                       */
+  int32_t n_face_batches;      /* signature-uniform 8-face batches (DG)               */
+  int64_t device_bytes;        /* device memory held by the plan                      */
+} tmf_plan_info;
+
+int tmf_plan_create(const tmf_plan_desc* desc, tmf_plan** out);
+int tmf_plan_destroy(tmf_plan* plan);
+int tmf_plan_get_info(const tmf_plan* plan, tmf_plan_info* info);
+
+/* y = A u on device pointers (length n_global_dofs), ordered on `stream`
+ * (a cudaStream_t, NULL = legacy default stream).  y is overwritten. */
+int tmf_apply(tmf_plan* plan, const double* u, double* y, void* stream);
+
+/* Same with host buffers: H2D(u), apply, D2H(y), synchronous. */
+int tmf_apply_host(tmf_plan* plan, const double* u_host, double* y_host);
+
+/* Per-stage timing of `reps` back-to-back applies (device pointers), CUDA
+ * events on `stream`: out_ms[0] = total, out_ms[1..] = per kernel class
+ * (cell, face, fixup).  For the bench only. */
+int tmf_apply_timed(tmf_plan* plan, const double* u, double* y, void* stream, int reps,
+                    double* out_ms, int n_out);
+
+/* diag(A) on device (identity rows on strong Dirichlet DoFs). CG only. */
+int tmf_diagonal(tmf_plan* plan, double* diag, void* stream);
+
+/* Point-Jacobi PCG, x0 = 0, exactly `iters` iterations (no early exit).
+ * b, x device pointers; res_norms (host, length iters+1) receives ||r_k||_2,
+ * or NULL.  All scalars stay on the device; one host sync at the end. */
+int tmf_pcg(tmf_plan* plan, const double* b, double* x, int iters, double* res_norms,
+            void* stream);
+
+const char* tmf_last_error(void);
+const char* tmf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TETMF_B200_H */

@@ -1,0 +1,93 @@
+"""ctypes binding of libtetmf_b200.so (the C-ABI declared in include/tetmf_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is present, every operator call raises RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtetmf_b200.so")
+
+TMF_OK, TMF_EINVAL, TMF_ECUDA = 0, 1, 2
+TMF_CG_LAPLACE, TMF_DG_SIPG, TMF_DG_HELMHOLTZ = 0, 1, 2
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_bp = C.POINTER(C.c_uint8)
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("operator_kind", C.c_int32), ("degree", C.c_int32), ("n_dofs_per_cell", C.c_int32),
+        ("n_components", C.c_int32), ("n_vertices", C.c_int64), ("n_cells", C.c_int64),
+        ("n_scalar_dofs", C.c_int64), ("vertices", _dp), ("cells", _ip), ("cell_dofs", _ip),
+        ("dirichlet_mask", _bp), ("n_q", C.c_int32), ("n_qf", C.c_int32),
+        ("cell_weights", _dp), ("value_matrix", _dp), ("grad_matrix", _dp),
+        ("face_weights", _dp), ("face_values", _dp), ("face_grads", _dp),
+        ("n_interior_faces", C.c_int64), ("interior_faces", _ip), ("tau_interior", _dp),
+        ("n_boundary_faces", C.c_int64), ("boundary_faces", _ip), ("tau_boundary", _dp),
+        ("boundary_dirichlet", _bp), ("kappa", _dp), ("mass_scale", C.c_double),
+        ("diffusivity", C.c_double), ("device", C.c_int32), ("flags", C.c_int32),
+    ]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("n_global_dofs", C.c_int64), ("flops_alg", C.c_double), ("bytes_alg", C.c_double),
+        ("flops_issued", C.c_double), ("kernels_per_apply", C.c_int32),
+        ("n_face_batches", C.c_int32), ("device_bytes", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load the library (once); raises RuntimeError if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with "
+                               "`python -m paper_2509_10226_b200._build` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.tmf_plan_create.argtypes = [C.POINTER(PlanDesc), C.POINTER(C.c_void_p)]
+        L.tmf_plan_destroy.argtypes = [C.c_void_p]
+        L.tmf_plan_get_info.argtypes = [C.c_void_p, C.POINTER(PlanInfo)]
+        L.tmf_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.tmf_apply_host.argtypes = [C.c_void_p, _dp, _dp]
+        L.tmf_apply_timed.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int]
+        L.tmf_diagonal.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.tmf_pcg.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_void_p]
+        L.tmf_last_error.restype = C.c_char_p
+        L.tmf_version.restype = C.c_char_p
+        for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
+                     "tmf_apply_host", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
+            "tmf_apply_host", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_last_error",
+            "tmf_version")
+
+
+def check(rc: int) -> None:
+    if rc == TMF_OK:
+        return
+    msg = lib().tmf_last_error().decode()
+    if rc == TMF_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def ptr(a: np.ndarray | None, ctype):
+    if a is None:
+        return C.cast(None, C.POINTER(ctype))
+    return a.ctypes.data_as(C.POINTER(ctype))

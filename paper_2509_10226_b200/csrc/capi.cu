@@ -1,0 +1,557 @@
+// C-ABI of tetmf_b200: plan creation (host-side setup of device data and
+// pre-swizzled DMMA table fragments), apply, diagonal, PCG.
+// See include/tetmf_b200.h for the mapping onto the reference interface.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/tetmf_b200.h"
+#include "cell_kernel.cuh"
+#include "face_kernel.cuh"
+#include "launch.h"
+#include "solver_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define TMF_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(TMF_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+template <typename T>
+int upload(T** dst, const T* src, size_t n, size_t* total) {
+  *dst = nullptr;
+  if (n == 0) return TMF_OK;
+  TMF_CUDA(cudaMalloc(dst, n * sizeof(T)));
+  TMF_CUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  *total += n * sizeof(T);
+  return TMF_OK;
+}
+
+// Lane-major DMMA B fragments for one table family (see cell_kernel.cuh):
+//   B1[t][c][kk][lane] = E_c(8t + (lane>>2), 4kk + (lane&3))
+//   B2[t][c][i][nj][lane] = w_q E_c(q = 8t + 2(lane&3) + i, 8nj + (lane>>2))
+template <typename F>
+void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<double>& out) {
+  const int T = (Q + 7) / 8, KK = (N + 3) / 4, NJ = (N + 7) / 8;
+  for (int t = 0; t < T; ++t)
+    for (int c = 0; c < NC; ++c)
+      for (int kk = 0; kk < KK; ++kk)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int q = 8 * t + (lane >> 2), j = 4 * kk + (lane & 3);
+          out.push_back(q < Q && j < N ? E(c, q, j) : 0.0);
+        }
+  for (int t = 0; t < T; ++t)
+    for (int c = 0; c < NC; ++c)
+      for (int i = 0; i < 2; ++i)
+        for (int nj = 0; nj < NJ; ++nj)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int q = 8 * t + 2 * (lane & 3) + i, j = 8 * nj + (lane >> 2);
+            out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
+          }
+}
+
+}  // namespace
+
+struct tmf_plan {
+  int dev = 0, n_sm = 0;
+  int kind = 0, degree = 0, N = 0, Q = 0, QF = 0, nc = 1;
+  bool dg = false, mass = false, faces = false;
+  int64_t n_cells = 0, n_verts = 0, n_scalar = 0, n_global = 0;
+  double mass_scale = 0.0, stiff_scale = 1.0;
+  size_t dev_bytes = 0;
+  // device data
+  double* verts = nullptr;
+  double* kappa = nullptr;
+  double* cell_frags = nullptr;
+  double* face_frags = nullptr;
+  int* cells = nullptr;
+  int* dofs = nullptr;
+  int* fix_list = nullptr;
+  int64_t n_fix = 0;
+  int2* if_combo = nullptr;
+  int* if_cm = nullptr;
+  int* if_cp = nullptr;
+  double* if_tau = nullptr;
+  int64_t n_if_batches = 0;
+  int2* bf_combo = nullptr;
+  int* bf_cm = nullptr;
+  double* bf_tau = nullptr;
+  int64_t n_bf_batches = 0;
+  // staging for host applies / solver scratch
+  double* stage_u = nullptr;
+  double* stage_y = nullptr;
+  double* pcg_buf = nullptr;
+  double* diag = nullptr;
+  double* diag_S = nullptr;
+  tmf_plan_info info{};
+  tmf::CellArgs cell_args(const double* u, double* y) const {
+    tmf::CellArgs a{};
+    a.u = u;
+    a.y = y;
+    a.dofs = dg ? nullptr : dofs;
+    a.cells = cells;
+    a.verts = verts;
+    a.kappa = kappa;
+    a.frags = cell_frags;
+    a.n_cells = n_cells;
+    a.nc = nc;
+    a.mass_scale = mass_scale;
+    a.stiff_scale = stiff_scale;
+    return a;
+  }
+  tmf::FaceArgs face_args(const double* u, double* y, bool boundary) const {
+    tmf::FaceArgs a{};
+    a.u = u;
+    a.y = y;
+    a.cells = cells;
+    a.verts = verts;
+    a.kappa = kappa;
+    a.frags = face_frags;
+    a.batch_combo = boundary ? bf_combo : if_combo;
+    a.cm = boundary ? bf_cm : if_cm;
+    a.cp = boundary ? nullptr : if_cp;
+    a.tau = boundary ? bf_tau : if_tau;
+    a.n_batches = boundary ? n_bf_batches : n_if_batches;
+    a.n_dpc = N;
+    a.nc = nc;
+    a.scale = stiff_scale;
+    return a;
+  }
+  ~tmf_plan() {
+    for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
+                    (void*)dofs, (void*)fix_list, (void*)if_combo, (void*)if_cm, (void*)if_cp,
+                    (void*)if_tau, (void*)bf_combo, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
+                    (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S})
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+
+int n_dofs_per_cell(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
+
+int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, size_t* total) {
+  const int64_t nif = d->n_interior_faces, nbf = d->n_boundary_faces;
+  // interior: stable sort by signature (minus combo, plus combo); faces keep their
+  // owning-cell order inside a signature (mesh.py:117)
+  std::vector<int64_t> order(nif);
+  std::iota(order.begin(), order.end(), 0);
+  auto sig = [&](int64_t f) {
+    const int32_t* r = d->interior_faces + 5 * f;
+    return r[1] * 24 + r[3] * 6 + r[4];
+  };
+  for (int64_t f = 0; f < nif; ++f) {
+    const int32_t* r = d->interior_faces + 5 * f;
+    if (r[0] < 0 || r[0] >= d->n_cells || r[2] < 0 || r[2] >= d->n_cells || r[1] < 0 || r[1] > 3 ||
+        r[3] < 0 || r[3] > 3 || r[4] < 0 || r[4] > 5)
+      return fail(TMF_EINVAL, "interior face " + std::to_string(f) + " out of range");
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sig(a) < sig(b); });
+  std::vector<int2> combo;
+  std::vector<int> cm, cp;
+  std::vector<double> tau;
+  for (int64_t s = 0; s < nif;) {
+    const int key = sig(order[s]);
+    int64_t e = s;
+    while (e < nif && sig(order[e]) == key) ++e;
+    for (int64_t b = s; b < e; b += 8) {
+      const int32_t* r0 = d->interior_faces + 5 * order[b];
+      combo.push_back(make_int2(r0[1] * 6, r0[3] * 6 + r0[4]));
+      for (int k = 0; k < 8; ++k) {
+        if (b + k < e) {
+          const int64_t f = order[b + k];
+          const int32_t* r = d->interior_faces + 5 * f;
+          cm.push_back(r[0]);
+          cp.push_back(r[2]);
+          tau.push_back(d->tau_interior[f]);
+        } else {
+          cm.push_back(-1);
+          cp.push_back(-1);
+          tau.push_back(0.0);
+        }
+      }
+    }
+    s = e;
+  }
+  P->n_if_batches = (int64_t)combo.size();
+  int rc;
+  if ((rc = upload(&P->if_combo, combo.data(), combo.size(), total))) return rc;
+  if ((rc = upload(&P->if_cm, cm.data(), cm.size(), total))) return rc;
+  if ((rc = upload(&P->if_cp, cp.data(), cp.size(), total))) return rc;
+  if ((rc = upload(&P->if_tau, tau.data(), tau.size(), total))) return rc;
+
+  // Dirichlet boundary faces grouped by local face (operator.py:365-366, 378-385)
+  std::vector<int2> bcombo;
+  std::vector<int> bcm;
+  std::vector<double> btau;
+  for (int lf = 0; lf < 4; ++lf) {
+    std::vector<int64_t> sel;
+    for (int64_t f = 0; f < nbf; ++f) {
+      const int32_t* r = d->boundary_faces + 3 * f;
+      if (r[1] == lf && d->boundary_dirichlet && d->boundary_dirichlet[f]) sel.push_back(f);
+    }
+    for (size_t b = 0; b < sel.size(); b += 8) {
+      bcombo.push_back(make_int2(lf * 6, -1));
+      for (int k = 0; k < 8; ++k) {
+        if (b + k < sel.size()) {
+          const int64_t f = sel[b + k];
+          const int32_t c = d->boundary_faces[3 * f];
+          if (c < 0 || c >= d->n_cells) return fail(TMF_EINVAL, "boundary face cell out of range");
+          bcm.push_back(c);
+          btau.push_back(d->tau_boundary ? d->tau_boundary[f] : 0.0);
+        } else {
+          bcm.push_back(-1);
+          btau.push_back(0.0);
+        }
+      }
+    }
+  }
+  P->n_bf_batches = (int64_t)bcombo.size();
+  if ((rc = upload(&P->bf_combo, bcombo.data(), bcombo.size(), total))) return rc;
+  if ((rc = upload(&P->bf_cm, bcm.data(), bcm.size(), total))) return rc;
+  if ((rc = upload(&P->bf_tau, btau.data(), btau.size(), total))) return rc;
+  return TMF_OK;
+}
+
+int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaEvent_t* ev) {
+  bool ok = true;
+  if (ev) TMF_CUDA(cudaEventRecord(ev[0], st));
+  if (!P->dg) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
+  TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y), P->n_sm, st, nullptr, &ok));
+  if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
+  if (P->faces) {
+    TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok));
+    TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok));
+  }
+  if (ev) TMF_CUDA(cudaEventRecord(ev[2], st));
+  if (!P->dg && P->n_fix) TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st));
+  if (ev) TMF_CUDA(cudaEventRecord(ev[3], st));
+  return TMF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tmf_last_error(void) { return g_err.c_str(); }
+const char* tmf_version(void) { return "tetmf_b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
+  if (!d || !out) return fail(TMF_EINVAL, "null descriptor/output");
+  *out = nullptr;
+  if (d->operator_kind < TMF_CG_LAPLACE || d->operator_kind > TMF_DG_HELMHOLTZ)
+    return fail(TMF_EINVAL, "unknown operator kind " + std::to_string(d->operator_kind));
+  if (d->degree < 1 || d->degree > 4)
+    return fail(TMF_EINVAL, "unsupported polynomial degree " + std::to_string(d->degree));
+  if (d->n_dofs_per_cell != n_dofs_per_cell(d->degree))
+    return fail(TMF_EINVAL, "n_dofs_per_cell does not match the degree");
+  if (d->n_components != 1 && d->n_components != 3)
+    return fail(TMF_EINVAL, "n_components must be 1 or 3");
+  if (d->n_cells <= 0 || d->n_vertices <= 0 || !d->vertices || !d->cells)
+    return fail(TMF_EINVAL, "empty mesh");
+  if (!d->grad_matrix || !d->cell_weights || d->n_q <= 0) return fail(TMF_EINVAL, "missing cell tables");
+  const bool dg = d->operator_kind != TMF_CG_LAPLACE;
+  if (!dg && !d->cell_dofs) return fail(TMF_EINVAL, "CG operator needs a CG dof map");
+  if (dg && d->n_scalar_dofs != d->n_cells * d->n_dofs_per_cell)
+    return fail(TMF_EINVAL, "DG operator needs a DG dof map");
+  if (d->n_scalar_dofs * d->n_components >= (int64_t)1 << 40) return fail(TMF_EINVAL, "too many dofs");
+  if (d->operator_kind == TMF_DG_HELMHOLTZ && !d->value_matrix)
+    return fail(TMF_EINVAL, "Helmholtz needs the value table");
+  const bool faces = dg && !(d->operator_kind == TMF_DG_HELMHOLTZ && d->diffusivity == 0.0);
+  if (faces && (!d->face_values || !d->face_grads || !d->face_weights || d->n_qf <= 0))
+    return fail(TMF_EINVAL, "geometry was built without face data");
+  if (faces && d->n_interior_faces > 0 && (!d->interior_faces || !d->tau_interior))
+    return fail(TMF_EINVAL, "missing interior faces / penalty");
+  for (int64_t f = 0; faces && f < d->n_interior_faces; ++f)
+    if (!(d->tau_interior[f] > 0)) return fail(TMF_EINVAL, "non-positive interior penalty");
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(TMF_ECUDA, "no CUDA device available (tetmf_b200 has no CPU path)");
+  if (d->device < 0 || d->device >= ndev) return fail(TMF_EINVAL, "bad device ordinal");
+  TMF_CUDA(cudaSetDevice(d->device));
+
+  auto P = new tmf_plan();
+  auto bail = [&](int rc) {
+    delete P;
+    return rc;
+  };
+  P->dev = d->device;
+  {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+    P->n_sm = sms;
+  }
+  P->kind = d->operator_kind;
+  P->degree = d->degree;
+  P->N = d->n_dofs_per_cell;
+  P->Q = d->n_q;
+  P->QF = d->n_qf;
+  P->nc = d->n_components;
+  P->dg = dg;
+  P->mass = d->operator_kind == TMF_DG_HELMHOLTZ;
+  P->faces = faces;
+  P->n_cells = d->n_cells;
+  P->n_verts = d->n_vertices;
+  P->n_scalar = d->n_scalar_dofs;
+  P->n_global = d->n_scalar_dofs * d->n_components;
+  P->mass_scale = P->mass ? d->mass_scale : 0.0;
+  P->stiff_scale = d->operator_kind == TMF_CG_LAPLACE ? 1.0 : d->diffusivity;
+
+  // validate mesh connectivity
+  for (int64_t i = 0; i < 4 * d->n_cells; ++i)
+    if (d->cells[i] < 0 || d->cells[i] >= d->n_vertices)
+      return bail(fail(TMF_EINVAL, "cell vertex id out of range"));
+
+  size_t total = 0;
+  int rc;
+  if ((rc = upload(&P->verts, d->vertices, 3 * d->n_vertices, &total))) return bail(rc);
+  if ((rc = upload(&P->cells, d->cells, 4 * d->n_cells, &total))) return bail(rc);
+  if (d->kappa && (rc = upload(&P->kappa, d->kappa, d->n_cells, &total))) return bail(rc);
+
+  // cell tables -> fragments
+  {
+    const int N = P->N, Q = P->Q;
+    const double* V = d->value_matrix;
+    const double* Gm = d->grad_matrix;
+    std::vector<double> fr;
+    if (P->mass) {
+      build_fragments(N, Q, 4, [&](int c, int q, int j) {
+        return c == 0 ? V[q * N + j] : Gm[(3 * q + c - 1) * N + j]; }, d->cell_weights, fr);
+    } else {
+      build_fragments(N, Q, 3, [&](int c, int q, int j) { return Gm[(3 * q + c) * N + j]; },
+                      d->cell_weights, fr);
+    }
+    tmf::CellLaunchInfo ci;
+    bool ok = true;
+    tmf::CellArgs dummy{};
+    dummy.n_cells = P->n_cells;
+    dummy.nc = P->nc;
+    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok));
+    if (!ok) return bail(fail(TMF_EINVAL, "unsupported (n_dofs_per_cell, n_q) = (" +
+                                              std::to_string(N) + ", " + std::to_string(Q) + ")"));
+    if ((int)fr.size() != ci.frag_doubles) return bail(fail(TMF_EINVAL, "internal: fragment size"));
+    if ((rc = upload(&P->cell_frags, fr.data(), fr.size(), &total))) return bail(rc);
+    P->info.flops_issued = (double)ci.tiles * ci.dmma_per_tile * 512.0;
+  }
+
+  // CG dof map (masked = ~idx) and the Dirichlet fix-up list
+  if (!dg) {
+    std::vector<int> enc((size_t)d->n_cells * P->N);
+    for (int64_t i = 0; i < (int64_t)enc.size(); ++i) {
+      const int g = d->cell_dofs[i];
+      if (g < 0 || g >= d->n_scalar_dofs) return bail(fail(TMF_EINVAL, "cell dof out of range"));
+      enc[i] = (d->dirichlet_mask && d->dirichlet_mask[g]) ? ~g : g;
+    }
+    if ((rc = upload(&P->dofs, enc.data(), enc.size(), &total))) return bail(rc);
+    std::vector<int> fix;
+    if (d->dirichlet_mask)
+      for (int64_t g = 0; g < d->n_scalar_dofs; ++g)
+        if (d->dirichlet_mask[g])
+          for (int c = 0; c < P->nc; ++c) fix.push_back((int)(g * P->nc + c));
+    P->n_fix = (int64_t)fix.size();
+    if ((rc = upload(&P->fix_list, fix.data(), fix.size(), &total))) return bail(rc);
+    // S_kl[j] = sum_q w_q E_k(q,j) E_l(q,j) for the matrix-free diagonal
+    const int N = P->N, Q = P->Q;
+    std::vector<double> S(6 * N, 0.0);
+    const int kl[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+    for (int m = 0; m < 6; ++m)
+      for (int j = 0; j < N; ++j)
+        for (int q = 0; q < Q; ++q)
+          S[m * N + j] += d->cell_weights[q] * d->grad_matrix[(3 * q + kl[m][0]) * N + j] *
+                          d->grad_matrix[(3 * q + kl[m][1]) * N + j];
+    if ((rc = upload(&P->diag_S, S.data(), S.size(), &total))) return bail(rc);
+  }
+
+  // face tables -> fragments per (lf, code), face batches
+  if (faces) {
+    const int N = P->N, QF = P->QF;
+    std::vector<double> fr;
+    for (int lf = 0; lf < 4; ++lf)
+      for (int code = 0; code < 6; ++code) {
+        const double* Fv = d->face_values + (size_t)(lf * 6 + code) * QF * N;
+        const double* Fg = d->face_grads + (size_t)(lf * 6 + code) * 3 * QF * N;
+        build_fragments(N, QF, 4, [&](int c, int q, int j) {
+          return c == 0 ? Fv[q * N + j] : Fg[(3 * q + c - 1) * N + j]; }, d->face_weights, fr);
+      }
+    tmf::FaceLaunchInfo fi;
+    bool ok = true;
+    tmf::FaceArgs dummy{};
+    dummy.nc = P->nc;
+    TMF_CUDA(tmf::launch_face(N, QF, false, dummy, P->n_sm, 0, &fi, &ok));
+    if (!ok) return bail(fail(TMF_EINVAL, "unsupported (n_dofs_per_cell, n_qf) = (" +
+                                              std::to_string(N) + ", " + std::to_string(QF) + ")"));
+    if ((int64_t)fr.size() != 24LL * fi.nfrag * 32) return bail(fail(TMF_EINVAL, "internal: face fragments"));
+    if ((rc = upload(&P->face_frags, fr.data(), fr.size(), &total))) return bail(rc);
+    if ((rc = build_face_batches(P, d, &total))) return bail(rc);
+    P->info.n_face_batches = (int32_t)(P->n_if_batches + P->n_bf_batches);
+    P->info.flops_issued += (double)P->nc * (P->n_if_batches * fi.dmma_per_batch +
+                                             P->n_bf_batches * fi.dmma_per_batch / 2) * 512.0;
+  }
+
+  // algorithmic flops / bytes (reference counters)
+  {
+    const double nd = P->N, nq = P->Q, nqf = P->QF, nce = (double)P->n_cells;
+    double n_scatter = nce * nd;
+    if (!dg && d->dirichlet_mask) {
+      int64_t masked = 0;
+      for (int64_t i = 0; i < (int64_t)d->n_cells * P->N; ++i) masked += d->dirichlet_mask[d->cell_dofs[i]] ? 1 : 0;
+      n_scatter -= (double)masked;
+    }
+    double f = nce * (12.0 * nq * nd + 33.0 * nq) + n_scatter;
+    if (P->mass) f += nce * (4.0 * nq * nd + 5.0 * nq + nd);
+    int64_t nbf_dir = 0;
+    if (faces) {
+      for (int64_t i = 0; i < d->n_boundary_faces; ++i) nbf_dir += (d->boundary_dirichlet && d->boundary_dirichlet[i]) ? 1 : 0;
+      f += (double)d->n_interior_faces * (32.0 * nqf * nd + 26.0 * nqf) +
+           (double)nbf_dir * (16.0 * nqf * nd + 13.0 * nqf);
+    }
+    P->info.flops_alg = f * P->nc;
+    double b = 16.0 * (double)P->n_global + 24.0 * (double)P->n_verts;
+    if (!dg)
+      b += 4.0 * nd * nce;
+    else
+      b += 16.0 * nce + 8.0 * (double)d->n_interior_faces + 4.0 * (double)d->n_boundary_faces;
+    if (d->kappa) b += 8.0 * nce;
+    P->info.bytes_alg = b;
+  }
+  P->info.n_global_dofs = P->n_global;
+  P->info.kernels_per_apply = 1 + (faces ? ((P->n_if_batches ? 1 : 0) + (P->n_bf_batches ? 1 : 0)) : 0) +
+                              ((!dg && P->n_fix) ? 1 : 0);
+  P->dev_bytes = total;
+  P->info.device_bytes = (int64_t)total;
+  TMF_CUDA(cudaDeviceSynchronize());
+  *out = P;
+  return TMF_OK;
+}
+
+int tmf_plan_destroy(tmf_plan* plan) {
+  if (!plan) return TMF_OK;
+  cudaSetDevice(plan->dev);
+  delete plan;
+  return TMF_OK;
+}
+
+int tmf_plan_get_info(const tmf_plan* plan, tmf_plan_info* info) {
+  if (!plan || !info) return fail(TMF_EINVAL, "null plan/info");
+  *info = plan->info;
+  return TMF_OK;
+}
+
+int tmf_apply(tmf_plan* P, const double* u, double* y, void* stream) {
+  if (!P || !u || !y) return fail(TMF_EINVAL, "null argument");
+  if (u == y) return fail(TMF_EINVAL, "u and y must not alias");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  return launch_apply(P, u, y, (cudaStream_t)stream, nullptr);
+}
+
+int tmf_apply_host(tmf_plan* P, const double* u_host, double* y_host) {
+  if (!P || !u_host || !y_host) return fail(TMF_EINVAL, "null argument");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  const size_t bytes = sizeof(double) * P->n_global;
+  if (!P->stage_u) {
+    TMF_CUDA(cudaMalloc(&P->stage_u, bytes));
+    TMF_CUDA(cudaMalloc(&P->stage_y, bytes));
+  }
+  TMF_CUDA(cudaMemcpyAsync(P->stage_u, u_host, bytes, cudaMemcpyHostToDevice, 0));
+  int rc = launch_apply(P, P->stage_u, P->stage_y, 0, nullptr);
+  if (rc) return rc;
+  TMF_CUDA(cudaMemcpyAsync(y_host, P->stage_y, bytes, cudaMemcpyDeviceToHost, 0));
+  TMF_CUDA(cudaStreamSynchronize(0));
+  return TMF_OK;
+}
+
+int tmf_apply_timed(tmf_plan* P, const double* u, double* y, void* stream, int reps, double* out_ms,
+                    int n_out) {
+  if (!P || !u || !y || !out_ms || reps < 1) return fail(TMF_EINVAL, "bad argument");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t ev[4];
+  for (auto& e : ev) TMF_CUDA(cudaEventCreate(&e));
+  double acc[4] = {0, 0, 0, 0};
+  for (int r = 0; r < reps; ++r) {
+    int rc = launch_apply(P, u, y, st, ev);
+    if (rc) return rc;
+    TMF_CUDA(cudaEventSynchronize(ev[3]));
+    float a, b, c, t;
+    cudaEventElapsedTime(&t, ev[0], ev[3]);
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    acc[0] += t;
+    acc[1] += a;
+    acc[2] += b;
+    acc[3] += c;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int i = 0; i < n_out && i < 4; ++i) out_ms[i] = acc[i] / reps;
+  return TMF_OK;
+}
+
+int tmf_diagonal(tmf_plan* P, double* diag, void* stream) {
+  if (!P || !diag) return fail(TMF_EINVAL, "null argument");
+  if (P->dg) return fail(TMF_EINVAL, "matrix-free diagonal is implemented for the CG operator");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  TMF_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * P->n_global, st));
+  tmf::DiagArgs a{diag, P->dofs, P->cells, P->verts, P->diag_S, P->n_cells, P->N, P->nc};
+  tmf::diag_kernel<<<P->n_sm * 8, 256, 0, st>>>(a);
+  TMF_CUDA(cudaGetLastError());
+  if (P->n_fix) {
+    tmf::set_list_kernel<<<P->n_sm * 4, 256, 0, st>>>(diag, P->fix_list, P->n_fix, 1.0);
+    TMF_CUDA(cudaGetLastError());
+  }
+  return TMF_OK;
+}
+
+int tmf_pcg(tmf_plan* P, const double* b, double* x, int iters, double* res_norms, void* stream) {
+  if (!P || !b || !x || iters < 0) return fail(TMF_EINVAL, "bad argument");
+  if (P->dg) return fail(TMF_EINVAL, "PCG is implemented for the CG operator");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = P->n_global;
+  if (!P->pcg_buf) TMF_CUDA(cudaMalloc(&P->pcg_buf, sizeof(double) * (5 * n)));
+  double *r = P->pcg_buf, *z = r + n, *p = z + n, *q = p + n, *dg = q + n;
+  double* sc = nullptr;  // rz[iters+1], pq[iters+1], rr[iters+1]
+  TMF_CUDA(cudaMallocAsync(&sc, sizeof(double) * 3 * (iters + 1), st));
+  double *rz = sc, *pq = sc + (iters + 1), *rr = sc + 2 * (iters + 1);
+  TMF_CUDA(cudaMemsetAsync(sc, 0, sizeof(double) * 3 * (iters + 1), st));
+  int rc = tmf_diagonal(P, dg, stream);
+  if (rc) return rc;
+  const int grid = P->n_sm * 4, blk = 512;
+  tmf::pcg_init_kernel<<<grid, blk, 0, st>>>(b, dg, x, r, z, p, n, rz, rr);
+  TMF_CUDA(cudaGetLastError());
+  for (int k = 0; k < iters; ++k) {
+    if ((rc = launch_apply(P, p, q, st, nullptr))) return rc;
+    tmf::dot_kernel<<<grid, blk, 0, st>>>(p, q, n, pq + k);
+    tmf::pcg_update_kernel<<<grid, blk, 0, st>>>(p, q, dg, x, r, z, n, rz + k, pq + k, rz + k + 1, rr + k + 1);
+    tmf::pcg_direction_kernel<<<grid, blk, 0, st>>>(z, p, n, rz + k, rz + k + 1);
+  }
+  TMF_CUDA(cudaGetLastError());
+  if (res_norms) {
+    std::vector<double> h(iters + 1);
+    TMF_CUDA(cudaMemcpyAsync(h.data(), rr, sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, st));
+    TMF_CUDA(cudaStreamSynchronize(st));
+    for (int k = 0; k <= iters; ++k) res_norms[k] = std::sqrt(h[k]);
+  }
+  TMF_CUDA(cudaFreeAsync(sc, st));
+  return TMF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// Shared device helpers for the tetmf_b200 kernels (sm_100a, FP64).
+//
+// FP64 tensor-core tile: mma.sync m8n8k4 .f64 (SASS DMMA.8x8x4), measured at
+// 37.1 TFLOP/s on B200 vs 34 TFLOP/s for register DFMA (tools/microbench,
+// profiles/r01_fp64_peak.json).  Fragment ownership (PTX ISA, m8n8k4 .f64):
+//   A (8x4, row):  lane holds A[lane>>2][lane&3]
+//   B (4x8, col):  lane holds B[lane&3][lane>>2]
+//   C (8x8):       lane holds C[lane>>2][2*(lane&3) + {0,1}]
+#pragma once
+#include <cstdint>
+
+namespace tmf {
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+struct Vec3 {
+  double x, y, z;
+};
+
+__device__ __forceinline__ Vec3 load_vertex(const double* __restrict__ v, int id) {
+  const double* p = v + 3 * (int64_t)id;
+  return Vec3{__ldg(p), __ldg(p + 1), __ldg(p + 2)};
+}
+
+// Affine cell map x = x0 + J xi with J = [x1-x0 | x2-x0 | x3-x0] (mesh.py:64-67).
+struct Affine {
+  double J[3][3];
+  double adj[3][3];  // adjugate: J^{-1} = adj / det
+  double det;
+};
+
+__device__ __forceinline__ void affine_from_vertices(const Vec3& a, const Vec3& b, const Vec3& c,
+                                                     const Vec3& d, Affine& g) {
+  const double e1[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
+  const double e2[3] = {c.x - a.x, c.y - a.y, c.z - a.z};
+  const double e3[3] = {d.x - a.x, d.y - a.y, d.z - a.z};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    g.J[i][0] = e1[i];
+    g.J[i][1] = e2[i];
+    g.J[i][2] = e3[i];
+  }
+  const double(&J)[3][3] = g.J;
+  g.adj[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  g.adj[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+  g.adj[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+  g.adj[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  g.adj[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+  g.adj[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+  g.adj[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  g.adj[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+  g.adj[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  g.det = J[0][0] * g.adj[0][0] + J[0][1] * g.adj[1][0] + J[0][2] * g.adj[2][0];
+}
+
+// Symmetric G = det * J^{-1} J^{-T} = adj adj^T / det, packed (00,01,02,11,12,22):
+// the reference D action J^{-1} (jxw J^{-T} g) equals w_q * G g (numpy_backend.py:68-76).
+__device__ __forceinline__ void stiffness_metric(const Affine& g, double scale, double (&G)[6]) {
+  const double s = scale / g.det;
+  const double(&A)[3][3] = g.adj;
+  G[0] = s * (A[0][0] * A[0][0] + A[0][1] * A[0][1] + A[0][2] * A[0][2]);
+  G[1] = s * (A[0][0] * A[1][0] + A[0][1] * A[1][1] + A[0][2] * A[1][2]);
+  G[2] = s * (A[0][0] * A[2][0] + A[0][1] * A[2][1] + A[0][2] * A[2][2]);
+  G[3] = s * (A[1][0] * A[1][0] + A[1][1] * A[1][1] + A[1][2] * A[1][2]);
+  G[4] = s * (A[1][0] * A[2][0] + A[1][1] * A[2][1] + A[1][2] * A[2][2]);
+  G[5] = s * (A[2][0] * A[2][0] + A[2][1] * A[2][1] + A[2][2] * A[2][2]);
+}
+
+// Reference-cell tangents of local face lf (corners FACE_VERTICES[lf], reference.py:25-26):
+// ds = xi(c1) - xi(c0), dt = xi(c2) - xi(c0) with xi(v0)=0, xi(v_k)=e_{k-1}.
+__device__ __forceinline__ void face_tangents_ref(int lf, double (&ds)[3], double (&dt)[3]) {
+  // lf 0: (1,2,3) -> ds = e1-e0, dt = e2-e0;  lf 1: (0,2,3) -> ds = e1, dt = e2
+  // lf 2: (0,1,3) -> ds = e0, dt = e2;        lf 3: (0,1,2) -> ds = e0, dt = e1
+  ds[0] = (lf == 0) ? -1.0 : (lf >= 2 ? 1.0 : 0.0);
+  ds[1] = (lf <= 1) ? 1.0 : 0.0;
+  ds[2] = 0.0;
+  dt[0] = (lf == 0) ? -1.0 : 0.0;
+  dt[1] = (lf == 3) ? 1.0 : 0.0;
+  dt[2] = (lf == 3) ? 0.0 : 1.0;
+}
+
+}  // namespace tmf

@@ -1,0 +1,120 @@
+// Kernel instantiations and launchers for tetmf_b200 (sm_100a).
+#include <cuda_runtime.h>
+
+#include "cell_kernel.cuh"
+#include "face_kernel.cuh"
+#include "launch.h"
+
+namespace tmf {
+
+template <int N, int Q, bool MASS, bool DG>
+static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
+  using S = CellShape<N, Q, MASS>;
+  constexpr int BLOCK = S::SMEM > 96 * 1024 ? 512 : 256;
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK>;
+  static int configured = 0;  // per instantiation, per process
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = 1;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t tiles = ((a.n_cells + 7) / 8) * a.nc;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  const int64_t need = (tiles + BLOCK / 32 - 1) / (BLOCK / 32);
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  if (info) {
+    info->dmma_per_tile = S::DMMA_PER_TILE;
+    info->tiles = tiles;
+    info->block = BLOCK;
+    info->grid = (int)blocks;
+    info->smem = S::SMEM;
+    info->frag_doubles = S::NFRAG * 32;
+    return cudaSuccess;
+  }
+  kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N, int Q>
+static cudaError_t cell_variant(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
+                                CellLaunchInfo* info) {
+  if (!dg) return launch_cell_t<N, Q, false, false>(a, n_sm, st, info);
+  if (mass) return launch_cell_t<N, Q, true, true>(a, n_sm, st, info);
+  return launch_cell_t<N, Q, false, true>(a, n_sm, st, info);
+}
+
+cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& a, int n_sm,
+                        cudaStream_t st, CellLaunchInfo* info, bool* supported) {
+  *supported = true;
+#define TMF_CELL(NN, QQ) \
+  if (n_dpc == NN && n_q == QQ) return cell_variant<NN, QQ>(mass, dg, a, n_sm, st, info);
+  TMF_CELL(4, 4)
+  TMF_CELL(4, 5)
+  TMF_CELL(10, 14)
+  TMF_CELL(10, 15)
+  TMF_CELL(20, 35)
+  TMF_CELL(35, 70)
+#undef TMF_CELL
+  *supported = false;
+  return cudaSuccess;
+}
+
+template <int N, int QF, bool BND>
+static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
+  using S = FaceShape<N, QF>;
+  auto kern = face_apply_kernel<N, QF, BND>;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t work = a.n_batches * a.nc;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  const int64_t need = (work + 7) / 8;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  if (info) {
+    info->nfrag = S::NFRAG;
+    info->dmma_per_batch = BND ? (S::NB1 + S::NB2) : 2 * (S::NB1 + S::NB2);
+    info->grid = (int)blocks;
+    return cudaSuccess;
+  }
+  if (work == 0) return cudaSuccess;
+  kern<<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
+                        cudaStream_t st, FaceLaunchInfo* info, bool* supported) {
+  *supported = true;
+#define TMF_FACE(NN, QQ)                                                          \
+  if (n_dpc == NN && n_qf == QQ) {                                                \
+    if (boundary) return launch_face_t<NN, QQ, true>(a, n_sm, st, info);          \
+    return launch_face_t<NN, QQ, false>(a, n_sm, st, info);                       \
+  }
+  TMF_FACE(4, 3)
+  TMF_FACE(4, 4)
+  TMF_FACE(10, 6)
+  TMF_FACE(10, 10)
+  TMF_FACE(20, 12)
+  TMF_FACE(20, 20)
+  TMF_FACE(35, 35)
+#undef TMF_FACE
+  *supported = false;
+  return cudaSuccess;
+}
+
+cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
+                         cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 4 * n_sm) blocks = 4 * n_sm;
+  dirichlet_fixup_kernel<<<(unsigned)blocks, 256, 0, st>>>(u, y, list, n);
+  return cudaGetLastError();
+}
+
+}  // namespace tmf

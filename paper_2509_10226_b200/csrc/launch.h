@@ -1,0 +1,34 @@
+// Internal launcher interface between the C-ABI (capi.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tmf {
+
+struct CellArgs;
+struct FaceArgs;
+
+struct CellLaunchInfo {
+  int dmma_per_tile = 0;
+  int64_t tiles = 0;
+  int block = 0;
+  int grid = 0;
+  int smem = 0;
+  int frag_doubles = 0;
+};
+
+struct FaceLaunchInfo {
+  int nfrag = 0;            // fragments per (lf, code) combo
+  int dmma_per_batch = 0;
+  int grid = 0;
+};
+
+// info != nullptr: only fill the launch description (no launch).
+cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& a, int n_sm,
+                        cudaStream_t st, CellLaunchInfo* info, bool* supported);
+cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
+                        cudaStream_t st, FaceLaunchInfo* info, bool* supported);
+cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
+                         cudaStream_t st);
+
+}  // namespace tmf

@@ -1,0 +1,30 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the reference's
+golden outputs and the CPU oracle.  Tolerance: relative L2 <= 1e-12 (north_star)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden, rel_l2
+from helpers import operator_from_fixture
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_gpu_matches_reference_golden(name):
+    g = load_golden(name)
+    A = operator_from_fixture(g)
+    y = A.apply(g["u"])
+    err = rel_l2(y, g["y"])
+    assert err <= TOL, f"{name}: rel L2 {err:.3e}"
+    assert A.n_applies == 1
+
+
+@pytest.mark.parametrize("name", ["cg_p2_n8_gm", "dg_p3_n3_gm_dir", "helmk_p2_n3_gm_dir"])
+def test_gpu_repeatable(name):
+    g = load_golden(name)
+    A = operator_from_fixture(g)
+    y1 = A.apply(g["u"])
+    y2 = A.apply(g["u"])
+    assert rel_l2(y1, y2) <= 1e-15

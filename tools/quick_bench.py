@@ -1,0 +1,42 @@
+"""Developer timing of single applies (not the official bench.py)."""
+import sys, time, os, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2509_10226_b200 import mesh as M, dofmap as D, basis as B, quadrature as Q, geometry as G, operator as op
+
+def run(kind, p, n, reps=20):
+    t0 = time.time()
+    m = M.kuhn_cube_mesh(n, seed=0)
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    geo = G.GeometryData("affine", cr, fr, None, None, None, None)
+    if kind == "cg":
+        dm = D.build_dof_map(m, p, "cg")
+        A = op.CgPoissonOperator(m, dm, geo, bas)
+    elif kind == "dg":
+        dm = D.build_dof_map(m, p, "dg")
+        A = op.DgSipgOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n), dirichlet_ids=range(6))
+    else:
+        dm = D.build_dof_map(m, p, "dg")
+        kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
+        A = op.KappaHelmholtzOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n), kap, 1.0, dirichlet_ids=range(6))
+    setup = time.time() - t0
+    nd = A.n_global_dofs
+    u = torch.rand(nd, dtype=torch.float64, device="cuda") * 2 - 1
+    y = torch.empty_like(u)
+    st = torch.cuda.current_stream().cuda_stream
+    A.timed(u.data_ptr(), y.data_ptr(), st, 3)
+    ms = A.timed(u.data_ptr(), y.data_ptr(), st, reps)
+    info = A.info
+    gdofs = nd / (ms[0] * 1e-3) / 1e9
+    tf_alg = info["flops_alg"] / (ms[0] * 1e-3) / 1e12
+    tf_iss = info["flops_issued"] / (ms[0] * 1e-3) / 1e12
+    print(json.dumps(dict(kind=kind, p=p, n=n, ndof=nd, setup_s=round(setup, 1), ms=[round(x, 4) for x in ms],
+                          gdofs=round(gdofs, 3), tflops_alg=round(tf_alg, 2), tflops_issued=round(tf_iss, 2),
+                          frac_fp64=round(tf_alg / 37.1, 3))), flush=True)
+
+if __name__ == "__main__":
+    for spec in sys.argv[1:]:
+        kind, p, n = spec.split(":")
+        run(kind, int(p), int(n))
