@@ -1,0 +1,358 @@
+"""Benchmark of the B200 matrix-free operator apply (driver contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2]
+
+Workload (BASELINE.json configs[1], "C2"): CG Laplace operator apply, degree
+sweep P1..P4, fp64, on the 48^3 x 6 = 663,552-cell jittered, randomly permuted
+Kuhn mesh (seed 0), Grundmann-Moller quadrature exact to 2p, u ~ U[-1,1]
+(seed 1).  One *step* = one apply at each degree, on the unordered mesh and on
+the hierarchically reordered mesh (8 applies); ``value`` = DoFs processed /
+device time (GDoF/s).  Inputs and plans are resident in HBM before timing;
+L2 is flushed (256 MiB write) before every apply, outside the timed events.
+
+``e2e`` times the same step through the public API with host buffers
+(``Operator.apply(numpy)`` -> ``tmf_apply_host``: pinned H2D of u, apply, D2H
+of y), wall clock.  ``--impl reference`` times the CPU oracle port of the
+reference's batched NumPy loop (oracle/ref_apply.py; the reference package
+itself cannot travel to the GPU box) with one worker process per host core
+on a bounded sample of batches of the same workload, extrapolated per DoF.
+
+Multi-GPU (torchrun, N>1): ``scaling: "weak"``, each rank applies the full
+operator (replicas; the partitioned NCCL-halo path is measured separately).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")   # CPU arm: one BLAS thread per worker
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.1   # measured: DMMA m8n8k4 on this pool's B200 (profiles/r01_fp64_peak.json)
+FP64_PEAK_SOURCE = "profiles/r01_fp64_peak.json (mma.sync m8n8k4 f64 microbench on B200, 1965 MHz)"
+DEGREES = (1, 2, 3, 4)
+N_MESH = 48
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2"])
+    ap.add_argument("--n", type=int, default=N_MESH)
+    ap.add_argument("--no-reorder", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=2.5)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- workload
+def build_problem(n, p, reorder):
+    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+
+    m = M.kuhn_cube_mesh(n, seed=0)
+    if reorder:
+        from paper_2509_10226_b200.reorder import hierarchical_reorder
+
+        m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    dm = D.build_dof_map(m, p, "cg")
+    geo = GeometryData("affine", cr, fr, None, None, None, None)
+    return m, dm, geo, bas
+
+
+def variants(args):
+    vs = [False]
+    if not args.no_reorder:
+        try:
+            import paper_2509_10226_b200.reorder  # noqa: F401
+            vs.append(True)
+        except ImportError:
+            pass
+    return vs
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    NAMES = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, dev=0, period=0.005):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.period, self._stop = period, threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max,
+                "reasons": [v for k, v in self.NAMES.items() if self.reasons & k], "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- reference arm / cpu baseline
+def _cpu_worker(args):
+    p, n, b0, b1, reorder = args
+    from oracle import ref_apply
+
+    m, dm, geo, bas, jit, jxw = _CPU_CACHE[(p, reorder)]
+    gidx = dm.cell_dofs.astype(np.int64)
+    u = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
+    y = np.zeros_like(u)
+    ids, act = ref_apply._cell_batches(m.n_cells, 4, 4)
+    t0 = time.perf_counter()
+    for b in range(b0, b1):
+        sub = ids[b]
+        idx = gidx[sub].T.copy()
+        idx[:, ~act[b]] = -1
+        U = ref_apply.gather(u, idx)
+        G = (bas.grad_matrix @ U).reshape(-1, 3, U.shape[1])
+        Dd = ref_apply.d_action_affine(G, jit[sub], jxw[sub])
+        R = bas.grad_matrix.T @ Dd.reshape(-1, U.shape[1])
+        ref_apply.scatter_add(y, idx, R)
+    return time.perf_counter() - t0, b1 - b0
+
+
+_CPU_CACHE = {}
+
+
+def cpu_reference(args, sample_s, workers=None):
+    """Time the oracle port of the reference's batched NumPy loop (kernel_stage "mm":
+    W=4 lanes x 4 cells per batch, operator.py:77-87) on all host cores; returns the
+    aggregate GDoF/s over the P1..P4 sweep, extrapolated from a bounded sample."""
+    import multiprocessing as mp
+
+    workers = workers or os.cpu_count() or 1
+    tot_dofs, tot_time, detail = 0.0, 0.0, {}
+    for reorder in variants(args):
+        for p in DEGREES:
+            from oracle import ref_apply
+
+            m, dm, geo, bas = build_problem(args.n, p, reorder)
+            jit, jxw, _ = ref_apply.affine_cell_geometry(m.vertices, m.cells, geo.cell_rule.weights)
+            _CPU_CACHE[(p, reorder)] = (m, dm, geo, bas, jit, jxw)
+            n_batches = (m.n_cells + 15) // 16
+            # calibrate batches/second on one worker, then give each worker ~sample_s
+            dt, nb = _cpu_worker((p, args.n, 0, 20, reorder))
+            per = max(1, int(sample_s * nb / dt))
+            chunks = [(p, args.n, (w * per) % n_batches, min(n_batches, (w * per) % n_batches + per), reorder)
+                      for w in range(workers)]
+            ctx = mp.get_context("fork")
+            with ctx.Pool(workers) as pool:
+                res = pool.map(_cpu_worker, chunks)
+            wall = max(r[0] for r in res)                # concurrent loops: slowest worker
+            done = sum(r[1] for r in res)
+            t_full = wall * n_batches / done            # extrapolated apply time, all cores
+            tot_dofs += dm.n_global_dofs
+            tot_time += t_full
+            detail[f"p{p}{'_reordered' if reorder else ''}"] = {
+                "gdofs": dm.n_global_dofs / t_full / 1e9, "batches_sampled": done, "n_batches": n_batches}
+    return tot_dofs / tot_time / 1e9, workers, detail
+
+
+# ----------------------------------------------------------------- GPU arm
+def gpu_bench(args, rank, world):
+    import torch
+
+    from paper_2509_10226_b200 import operator as op
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    cfg = op.OperatorConfig(device=dev)
+    problems = []
+    for reorder in variants(args):
+        for p in DEGREES:
+            m, dm, geo, bas = build_problem(args.n, p, reorder)
+            A = op.CgPoissonOperator(m, dm, geo, bas, cfg)
+            u_host = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
+            u = torch.from_numpy(u_host).cuda()
+            y = torch.empty_like(u)
+            u_pin = torch.from_numpy(u_host).pin_memory()
+            y_pin = torch.empty_like(u_pin).pin_memory()
+            problems.append(dict(p=p, reorder=reorder, A=A, u=u, y=y, u_pin=u_pin, y_pin=y_pin,
+                                 ndof=dm.n_global_dofs))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+
+    def step(record):
+        for pr in problems:
+            flush.fill_(1.0)
+            ms = pr["A"].timed(pr["u"].data_ptr(), pr["y"].data_ptr(), st, 1)
+            if record is not None:
+                record.append((pr, ms))
+
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    rec = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            step(rec)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    total_ms = sum(ms[0] for _, ms in rec)
+    dofs = sum(pr["ndof"] for pr, _ in rec)
+
+    # e2e through the public API with host (pinned) buffers
+    def e2e_step():
+        for pr in problems:
+            pr["A"].apply(pr["u_pin"].numpy(), out=pr["y_pin"].numpy())
+    e2e_step()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_s = time.perf_counter() - t0
+
+    # parity spot check of the timed path against the e2e path (P2, unordered)
+    pr0 = problems[1]
+    err = float(torch.linalg.vector_norm(pr0["y"].cpu() - pr0["y_pin"]) / torch.linalg.vector_norm(pr0["y_pin"]))
+
+    per = {}
+    for pr in problems:
+        key = f"p{pr['p']}{'_reordered' if pr['reorder'] else ''}"
+        ms = np.array([m for q, m in rec if q is pr])
+        t = ms[:, 0].mean()
+        tc = ms[:, 1].mean()
+        info = pr["A"].info
+        per[key] = {"ndof": pr["ndof"], "ms": round(float(t), 4), "gdofs": round(pr["ndof"] / t / 1e6, 3),
+                    "cell_kernel_ms": round(float(tc), 4),
+                    "tflops_alg": round(info["flops_alg"] / tc / 1e9, 2),
+                    "frac_fp64": round(info["flops_alg"] / tc / 1e9 / FP64_PEAK_TFLOPS, 3)}
+    # dominant kernel = the cell kernel of the slowest apply
+    dom = max(problems, key=lambda q: per[f"p{q['p']}{'_reordered' if q['reorder'] else ''}"]["cell_kernel_ms"])
+    dk = f"p{dom['p']}{'_reordered' if dom['reorder'] else ''}"
+    tc = per[dk]["cell_kernel_ms"]
+    achieved = dom["A"].info["flops_alg"] / tc / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("cell_kernel_p4", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    n_kern = sum(pr["A"].info["kernels_per_apply"] for pr in problems) * args.steps
+    return dict(total_ms=total_ms, dofs=dofs, e2e_s=e2e_s, per=per, clocks=clk.summary(),
+                roofline={"bound": "tensor", "kernel": f"cell_apply_kernel ({dk})", "achieved": round(achieved, 3),
+                          "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE, "unit": "TFLOP/s",
+                          "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
+                          "algorithmic": "reference counter flops (operator.py:227-242) per launch / CUDA-event kernel time"},
+                gpu_launches=n_kern, parity_rel_l2=err,
+                h2d=sum(8 * pr["ndof"] for pr in problems), d2h=sum(8 * pr["ndof"] for pr in problems))
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    workload = (f"CG Laplace apply, P1-P4 sweep, {args.n}^3x6 jittered permuted Kuhn tets, GM quadrature 2p, "
+                f"fp64, unordered{'' if args.no_reorder else ' + hierarchically reordered'}")
+    metric, unit = "operator-apply GDoF/s (fp64), CG Laplace P1-P4 sweep", "GDoF/s"
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        val, cores, detail = cpu_reference(args, args.cpu_sample_s)
+        line = {"impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": workload},
+                "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "port",
+                                 "sample": f"oracle port of the reference batched NumPy loop (16-cell batches), "
+                                           f"~{args.cpu_sample_s}s per worker per degree, extrapolated per DoF",
+                                 "detail": detail},
+                "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    r = gpu_bench(args, rank, world)
+    total_ms = r["total_ms"]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms, r["e2e_s"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_s = float(t[0]), float(t[1])
+    else:
+        e2e_s = r["e2e_s"]
+    value = r["dofs"] * world / (total_ms * 1e-3) / 1e9
+    e2e_val = r["dofs"] * world / e2e_s / 1e9
+    cpu = None
+    if rank == 0 and world == 1:
+        try:
+            v, cores, detail = cpu_reference(args, min(args.cpu_sample_s, 1.5))
+            cpu = {"value": v, "unit": unit, "cores": cores, "kind": "port",
+                   "sample": "oracle port of the reference batched NumPy loop, ~1.5 s per worker per degree, "
+                             "extrapolated per DoF", "detail": detail}
+        except Exception as e:  # the CPU baseline is reported, not required for the GPU number
+            cpu = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        line = {"metric": metric, "value": round(value, 4), "unit": unit, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload, "l2": "flushed (256 MiB write) before every apply",
+                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                "per_degree": r["per"], "roofline": r["roofline"], "cpu_baseline": cpu,
+                "e2e": {"value": round(e2e_val, 4), "unit": unit, "h2d_bytes_per_step": r["h2d"],
+                        "d2h_bytes_per_step": r["d2h"], "path": "Operator.apply(numpy, pinned) -> tmf_apply_host"},
+                "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "parity_e2e_vs_timed_rel_l2": r["parity_rel_l2"]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

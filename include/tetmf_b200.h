@@ -117,6 +117,14 @@ int tmf_diagonal(tmf_plan* plan, double* diag, void* stream);
 int tmf_pcg(tmf_plan* plan, const double* b, double* x, int iters, double* res_norms,
             void* stream);
 
+/* Hierarchical cell reordering (host-side setup; no GPU needed).  Writes the
+ * permutation new_of_old (cell e moves to position new_of_old[e]), to be
+ * applied like mesh.apply_cell_permutation (mesh.py:291-293).  Replaces the
+ * reorder module the reference only specifies. */
+int tmf_hierarchical_reorder(int64_t n_cells, int64_t n_interior_faces,
+                             const int32_t* interior_faces, int32_t group_size,
+                             int64_t* new_of_old);
+
 const char* tmf_last_error(void);
 const char* tmf_version(void);
 

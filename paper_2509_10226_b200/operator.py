@@ -206,8 +206,9 @@ class _B200Operator:
         self.n_applies += 1
 
     # -- apply
-    def apply(self, u):
-        """y = A u.  NumPy in -> fresh NumPy out; CUDA tensor in -> CUDA tensor out."""
+    def apply(self, u, out=None):
+        """y = A u.  NumPy in -> fresh NumPy out (or ``out``, e.g. a pinned buffer);
+        CUDA tensor in -> CUDA tensor out."""
         self._check_length(u)
         if type(u).__module__.startswith("torch"):
             import torch
@@ -220,7 +221,9 @@ class _B200Operator:
                 self.apply_into(u.data_ptr(), y.data_ptr(), torch.cuda.current_stream(u.device).cuda_stream)
                 return y
         u = np.ascontiguousarray(u, dtype=np.float64)
-        y = np.empty_like(u)
+        y = np.empty_like(u) if out is None else out
+        if y.dtype != np.float64 or not y.flags.c_contiguous or y.shape != u.shape:
+            raise ValueError("out must be a contiguous float64 vector of the operator size")
         _lib.check(_lib.lib().tmf_apply_host(self._plan, _lib.ptr(u, C.c_double), _lib.ptr(y, C.c_double)))
         self._count()
         return y

@@ -1,0 +1,170 @@
+"""CPU tests: host setup vs the oracle restatements, the C-ABI library surface,
+quadrature/basis properties.  No GPU needed."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_names, load_golden
+from oracle import ref_reorder, ref_setup
+from paper_2509_10226_b200 import _lib, basis as B, dofmap as D, mesh as M, quadrature as Q, reorder as R
+from paper_2509_10226_b200.reference import PERMS
+
+
+# ------------------------------------------------------------------ C-ABI surface
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "tetmf_b200.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(tmf_\w+)\s*\(", hdr, re.M))
+    assert declared == set(_lib.EXPORTED)
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert b"sm_100a" in _lib.lib().tmf_version()
+
+
+def test_plan_create_rejects_bad_descriptors():
+    d = _lib.PlanDesc()
+    d.operator_kind = 7
+    plan = ctypes.c_void_p()
+    with pytest.raises(ValueError, match="unknown operator kind"):
+        _lib.check(_lib.lib().tmf_plan_create(ctypes.byref(d), ctypes.byref(plan)))
+    d.operator_kind = _lib.TMF_CG_LAPLACE
+    d.degree = 5
+    with pytest.raises(ValueError, match="unsupported polynomial degree"):
+        _lib.check(_lib.lib().tmf_plan_create(ctypes.byref(d), ctypes.byref(plan)))
+
+
+# ------------------------------------------------------------------ mesh / faces
+@pytest.mark.parametrize("n,seed", [(1, 0), (2, 5), (3, 1)])
+def test_build_faces_matches_oracle(n, seed):
+    m = M.kuhn_cube_mesh(n, seed=seed)
+    ifc, bfc = ref_setup.build_faces(m.cells, lambda c: int(M.cube_boundary_ids(c[None])[0]), m.vertices)
+    assert np.array_equal(ifc, m.interior_faces)
+    assert np.array_equal(bfc, m.boundary_faces)
+    m.validate()
+    assert len(m.interior_faces) == 12 * n ** 3 - 6 * n ** 2
+    assert len(m.boundary_faces) == 12 * n ** 2
+
+
+def test_mesh_generator_deterministic_and_positive():
+    a, b = M.kuhn_cube_mesh(4, seed=7), M.kuhn_cube_mesh(4, seed=7)
+    assert np.array_equal(a.cells, b.cells) and np.array_equal(a.vertices, b.vertices)
+    assert np.all(a.cell_volumes() > 0)
+    assert abs(a.cell_volumes().sum() - 1.0) < 1e-12
+    assert sorted(set(a.boundary_faces[:, 2].tolist())) == [0, 1, 2, 3, 4, 5]
+
+
+def test_golden_meshes_rebuild_identically():
+    for name in golden_names("cg_p2_n8"):
+        g = load_golden(name)
+        ifc, bfc = M.build_faces(g["cells"], g["vertices"], M.cube_boundary_ids)
+        assert np.array_equal(ifc, g["interior_faces"])
+        assert np.array_equal(bfc, g["boundary_faces"])
+
+
+# ------------------------------------------------------------------ DoF maps
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("dids", [(), (0, 1, 2, 3, 4, 5), (2, 5)])
+def test_cg_dofmap_matches_oracle(p, dids):
+    m = M.kuhn_cube_mesh(3, seed=2)
+    dm = D.build_dof_map(m, p, "cg", 1, dids)
+    cd, mask, n = ref_setup.build_cg_dofs(m.cells, m.n_vertices, p, m.boundary_faces, dids)
+    assert dm.n_scalar_dofs == n == (3 * p + 1) ** 3
+    assert np.array_equal(dm.cell_dofs, cd)
+    assert np.array_equal(dm.dirichlet_mask, mask)
+
+
+def test_dofmap_errors():
+    m = M.kuhn_cube_mesh(2)
+    with pytest.raises(ValueError):
+        D.build_dof_map(m, 2, "xx")
+    with pytest.raises(ValueError):
+        D.build_dof_map(m, 2, "cg", dirichlet_boundary_ids=(9,))
+    with pytest.raises(ValueError):
+        D.build_dof_map(m, 2, "cg", n_components=2)
+
+
+def test_golden_dofmaps_rebuild_identically():
+    for name in golden_names("cg_"):
+        g = load_golden(name)
+        m = M.TetMesh(g["vertices"], g["cells"], g["interior_faces"], g["boundary_faces"])
+        dm = D.build_dof_map(m, int(g["p"]), "cg", 1, tuple(g["dirichlet_ids"].tolist()))
+        assert np.array_equal(dm.cell_dofs, g["cell_dofs"]), name
+        assert np.array_equal(dm.dirichlet_mask, g["dirichlet_mask"]), name
+
+
+def test_colouring_oracle_smoke():
+    m = M.kuhn_cube_mesh(2, seed=0)
+    dm = D.build_dof_map(m, 1, "cg")
+    ids = np.arange(m.n_cells).reshape(-1, 16)
+    col = ref_setup.color_batches(dm.cell_dofs, ids, np.ones_like(ids, bool))
+    for b in range(len(ids)):
+        for c in range(b):
+            if col[b] == col[c]:
+                assert not set(dm.cell_dofs[ids[b]].ravel()) & set(dm.cell_dofs[ids[c]].ravel())
+
+
+# ------------------------------------------------------------------ quadrature / basis
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_gm_rules(p):
+    c, f = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    assert (c.n_points, f.n_points) == ({1: 5, 2: 15, 3: 35, 4: 70}[p], {1: 4, 2: 10, 3: 20, 4: 35}[p])
+    assert Q.monomial_exactness(c) >= 2 * p and Q.monomial_exactness(f) >= 2 * p
+    for perm in PERMS:
+        assert Q.symmetric_point_permutation(f.points, perm) is not None
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_basis_nodal_and_partition_of_unity(p):
+    nodes, tags = B.reference_nodes(p)
+    assert len(nodes) == B.n_dofs_per_cell(p) == len(tags)
+    assert np.allclose(B.lagrange_values(p, nodes), np.eye(len(nodes)), atol=1e-10)
+    b = B.tabulate_basis(p, Q.make_cell_quadrature(p), Q.make_face_quadrature(p))
+    assert np.allclose(b.value_matrix.sum(axis=1), 1.0)
+    assert np.allclose(b.grad_matrix.sum(axis=1), 0.0, atol=1e-10)
+    assert b.face_values.shape == (4, 6, b.n_qf, len(nodes))
+
+
+def test_basis_tables_match_reference_fixtures():
+    for name in golden_names("cg_p"):
+        g = load_golden(name)
+        p = int(g["p"])
+        cr = Q.QuadratureRule(g["cell_points"], g["cell_weights"], 2 * p, 3)
+        fr = Q.QuadratureRule(g["face_points"], g["face_weights"], 2 * p, 2)
+        b = B.tabulate_basis(p, cr, fr)
+        assert np.allclose(b.grad_matrix, g["grad_matrix"], atol=1e-11), name
+        assert np.allclose(b.face_grads, g["face_grads"], atol=1e-11), name
+
+
+# ------------------------------------------------------------------ reordering
+@pytest.mark.parametrize("n,seed", [(2, 0), (3, 4), (5, 1)])
+def test_reorder_bit_exact_vs_oracle(n, seed):
+    m = M.kuhn_cube_mesh(n, seed=seed)
+    a = R.hierarchical_reorder(m)
+    b = ref_reorder.hierarchical_reorder(m.n_cells, m.interior_faces)
+    assert np.array_equal(a, b)
+    assert np.array_equal(np.sort(a), np.arange(m.n_cells))
+
+
+def test_reorder_improves_locality_spec_acceptance():
+    m = M.kuhn_cube_mesh(8, seed=0)
+    m2 = M.apply_cell_permutation(m, R.hierarchical_reorder(m))
+    before, after = R.locality_metrics(m), R.locality_metrics(m2)
+    assert after["mean_neighbor_index_distance"] * 2 <= before["mean_neighbor_index_distance"]
+    m2.validate()
+
+
+def test_reorder_chain_and_determinism():
+    # shuffled chain of 256 cells as a face graph: bandwidth must collapse
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(256)
+    faces = np.array([[perm[i], 0, perm[i + 1], 0, 0] for i in range(255)], dtype=np.int32)
+    faces[:, [0, 2]] = np.sort(faces[:, [0, 2]], axis=1)
+    nb = ref_reorder.hierarchical_reorder(256, faces)
+    nb2 = ref_reorder.hierarchical_reorder(256, faces)
+    assert np.array_equal(nb, nb2)
+    d = np.abs(nb[faces[:, 0]] - nb[faces[:, 2]])
+    assert d.max() <= 16
