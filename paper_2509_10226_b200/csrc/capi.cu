@@ -66,6 +66,28 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
           }
 }
 
+// Face tables (4 components per point), point groups of 4 (see face_kernel.cuh):
+//   B1[g][h][kk][lane] = E_{2h + (n&1)}(4g + (n>>1), 4kk + (lane&3)),  n = lane>>2
+//   B2[g][c][nj][lane] = w_q E_c(q = 4g + (lane&3), 8nj + (lane>>2))
+template <typename F>
+void build_face_fragments(int N, int Q, F E, const double* w, std::vector<double>& out) {
+  const int G = (Q + 3) / 4, KK = (N + 3) / 4, NJ = (N + 7) / 8;
+  for (int g = 0; g < G; ++g)
+    for (int h = 0; h < 2; ++h)
+      for (int kk = 0; kk < KK; ++kk)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int n = lane >> 2, q = 4 * g + (n >> 1), c = 2 * h + (n & 1), j = 4 * kk + (lane & 3);
+          out.push_back(q < Q && j < N ? E(c, q, j) : 0.0);
+        }
+  for (int g = 0; g < G; ++g)
+    for (int c = 0; c < 4; ++c)
+      for (int nj = 0; nj < NJ; ++nj)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int q = 4 * g + (lane & 3), j = 8 * nj + (lane >> 2);
+          out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
+        }
+}
+
 }  // namespace
 
 struct tmf_plan {
@@ -84,15 +106,15 @@ struct tmf_plan {
   int* dofs = nullptr;
   int* fix_list = nullptr;
   int64_t n_fix = 0;
-  int2* if_combo = nullptr;
+  int4* if_chunks = nullptr;
   int* if_cm = nullptr;
   int* if_cp = nullptr;
   double* if_tau = nullptr;
-  int64_t n_if_batches = 0;
-  int2* bf_combo = nullptr;
+  int64_t n_if_batches = 0, n_if_chunks = 0;
+  int4* bf_chunks = nullptr;
   int* bf_cm = nullptr;
   double* bf_tau = nullptr;
-  int64_t n_bf_batches = 0;
+  int64_t n_bf_batches = 0, n_bf_chunks = 0;
   // staging for host applies / solver scratch
   double* stage_u = nullptr;
   double* stage_y = nullptr;
@@ -123,11 +145,11 @@ struct tmf_plan {
     a.verts = verts;
     a.kappa = kappa;
     a.frags = face_frags;
-    a.batch_combo = boundary ? bf_combo : if_combo;
+    a.chunks = boundary ? bf_chunks : if_chunks;
     a.cm = boundary ? bf_cm : if_cm;
     a.cp = boundary ? nullptr : if_cp;
     a.tau = boundary ? bf_tau : if_tau;
-    a.n_batches = boundary ? n_bf_batches : n_if_batches;
+    a.n_chunks = boundary ? n_bf_chunks : n_if_chunks;
     a.n_dpc = N;
     a.nc = nc;
     a.scale = stiff_scale;
@@ -135,8 +157,8 @@ struct tmf_plan {
   }
   ~tmf_plan() {
     for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
-                    (void*)dofs, (void*)fix_list, (void*)if_combo, (void*)if_cm, (void*)if_cp,
-                    (void*)if_tau, (void*)bf_combo, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
+                    (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
+                    (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S})
       if (p) cudaFree(p);
   }
@@ -146,9 +168,15 @@ namespace {
 
 int n_dofs_per_cell(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
 
-int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, size_t* total) {
+// Split [first, first+count) batches of one signature into CTA chunks.
+void push_chunks(std::vector<int4>& out, int cm, int cp, int64_t first, int64_t count, int chunk) {
+  for (int64_t b = 0; b < count; b += chunk)
+    out.push_back(make_int4(cm, cp, (int)(first + b), (int)std::min<int64_t>(chunk, count - b)));
+}
+
+int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* total) {
   const int64_t nif = d->n_interior_faces, nbf = d->n_boundary_faces;
-  // interior: stable sort by signature (minus combo, plus combo); faces keep their
+  // interior: stable sort by signature (lf-, lf+, code); faces keep their
   // owning-cell order inside a signature (mesh.py:117)
   std::vector<int64_t> order(nif);
   std::iota(order.begin(), order.end(), 0);
@@ -163,67 +191,71 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, size_t* total) {
       return fail(TMF_EINVAL, "interior face " + std::to_string(f) + " out of range");
   }
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sig(a) < sig(b); });
-  std::vector<int2> combo;
+  std::vector<int4> chunks;
   std::vector<int> cm, cp;
   std::vector<double> tau;
+  int64_t nb = 0;
   for (int64_t s = 0; s < nif;) {
     const int key = sig(order[s]);
     int64_t e = s;
     while (e < nif && sig(order[e]) == key) ++e;
-    for (int64_t b = s; b < e; b += 8) {
-      const int32_t* r0 = d->interior_faces + 5 * order[b];
-      combo.push_back(make_int2(r0[1] * 6, r0[3] * 6 + r0[4]));
-      for (int k = 0; k < 8; ++k) {
-        if (b + k < e) {
-          const int64_t f = order[b + k];
-          const int32_t* r = d->interior_faces + 5 * f;
-          cm.push_back(r[0]);
-          cp.push_back(r[2]);
-          tau.push_back(d->tau_interior[f]);
-        } else {
-          cm.push_back(-1);
-          cp.push_back(-1);
-          tau.push_back(0.0);
-        }
+    const int32_t* r0 = d->interior_faces + 5 * order[s];
+    const int64_t nbatch = (e - s + 7) / 8;
+    push_chunks(chunks, r0[1] * 6, r0[3] * 6 + r0[4], nb, nbatch, chunk);
+    for (int64_t k = 0; k < nbatch * 8; ++k) {
+      if (s + k < e) {
+        const int64_t f = order[s + k];
+        const int32_t* r = d->interior_faces + 5 * f;
+        cm.push_back(r[0]);
+        cp.push_back(r[2]);
+        tau.push_back(d->tau_interior[f]);
+      } else {
+        cm.push_back(-1);
+        cp.push_back(-1);
+        tau.push_back(0.0);
       }
     }
+    nb += nbatch;
     s = e;
   }
-  P->n_if_batches = (int64_t)combo.size();
+  P->n_if_batches = nb;
+  P->n_if_chunks = (int64_t)chunks.size();
   int rc;
-  if ((rc = upload(&P->if_combo, combo.data(), combo.size(), total))) return rc;
+  if ((rc = upload(&P->if_chunks, chunks.data(), chunks.size(), total))) return rc;
   if ((rc = upload(&P->if_cm, cm.data(), cm.size(), total))) return rc;
   if ((rc = upload(&P->if_cp, cp.data(), cp.size(), total))) return rc;
   if ((rc = upload(&P->if_tau, tau.data(), tau.size(), total))) return rc;
 
   // Dirichlet boundary faces grouped by local face (operator.py:365-366, 378-385)
-  std::vector<int2> bcombo;
+  std::vector<int4> bchunks;
   std::vector<int> bcm;
   std::vector<double> btau;
+  nb = 0;
   for (int lf = 0; lf < 4; ++lf) {
     std::vector<int64_t> sel;
     for (int64_t f = 0; f < nbf; ++f) {
       const int32_t* r = d->boundary_faces + 3 * f;
       if (r[1] == lf && d->boundary_dirichlet && d->boundary_dirichlet[f]) sel.push_back(f);
     }
-    for (size_t b = 0; b < sel.size(); b += 8) {
-      bcombo.push_back(make_int2(lf * 6, -1));
-      for (int k = 0; k < 8; ++k) {
-        if (b + k < sel.size()) {
-          const int64_t f = sel[b + k];
-          const int32_t c = d->boundary_faces[3 * f];
-          if (c < 0 || c >= d->n_cells) return fail(TMF_EINVAL, "boundary face cell out of range");
-          bcm.push_back(c);
-          btau.push_back(d->tau_boundary ? d->tau_boundary[f] : 0.0);
-        } else {
-          bcm.push_back(-1);
-          btau.push_back(0.0);
-        }
+    const int64_t nbatch = ((int64_t)sel.size() + 7) / 8;
+    push_chunks(bchunks, lf * 6, -1, nb, nbatch, chunk);
+    for (int64_t k = 0; k < nbatch * 8; ++k) {
+      if (k < (int64_t)sel.size()) {
+        const int64_t f = sel[k];
+        const int32_t c = d->boundary_faces[3 * f];
+        if (c < 0 || c >= d->n_cells) return fail(TMF_EINVAL, "boundary face cell out of range");
+        bcm.push_back(c);
+        btau.push_back(d->tau_boundary ? d->tau_boundary[f] : 0.0);
+      } else {
+        bcm.push_back(-1);
+        btau.push_back(0.0);
       }
     }
+    nb += nbatch;
   }
-  P->n_bf_batches = (int64_t)bcombo.size();
-  if ((rc = upload(&P->bf_combo, bcombo.data(), bcombo.size(), total))) return rc;
+  P->n_bf_batches = nb;
+  P->n_bf_chunks = (int64_t)bchunks.size();
+  if ((rc = upload(&P->bf_chunks, bchunks.data(), bchunks.size(), total))) return rc;
   if ((rc = upload(&P->bf_cm, bcm.data(), bcm.size(), total))) return rc;
   if ((rc = upload(&P->bf_tau, btau.data(), btau.size(), total))) return rc;
   return TMF_OK;
@@ -387,7 +419,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       for (int code = 0; code < 6; ++code) {
         const double* Fv = d->face_values + (size_t)(lf * 6 + code) * QF * N;
         const double* Fg = d->face_grads + (size_t)(lf * 6 + code) * 3 * QF * N;
-        build_fragments(N, QF, 4, [&](int c, int q, int j) {
+        build_face_fragments(N, QF, [&](int c, int q, int j) {
           return c == 0 ? Fv[q * N + j] : Fg[(3 * q + c - 1) * N + j]; }, d->face_weights, fr);
       }
     tmf::FaceLaunchInfo fi;
@@ -399,7 +431,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
                                               std::to_string(N) + ", " + std::to_string(QF) + ")"));
     if ((int64_t)fr.size() != 24LL * fi.nfrag * 32) return bail(fail(TMF_EINVAL, "internal: face fragments"));
     if ((rc = upload(&P->face_frags, fr.data(), fr.size(), &total))) return bail(rc);
-    if ((rc = build_face_batches(P, d, &total))) return bail(rc);
+    if ((rc = build_face_batches(P, d, fi.chunk, &total))) return bail(rc);
     P->info.n_face_batches = (int32_t)(P->n_if_batches + P->n_bf_batches);
     P->info.flops_issued += (double)P->nc * (P->n_if_batches * fi.dmma_per_batch +
                                              P->n_bf_batches * fi.dmma_per_batch / 2) * 512.0;

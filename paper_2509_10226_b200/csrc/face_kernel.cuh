@@ -7,12 +7,22 @@
 //     qv = w (tau jump - avg),   qg± = -w jump m± / 2
 //     R- = Fv-^T qv + Fg-^T qg-,   R+ = -Fv+^T qv + Fg+^T qg+
 //   boundary (Dirichlet): qv = w (tau V - m.G),  qg = -w V m
-// One warp handles 8 faces that share the signature (lf-, lf+, code), so the
-// face tables (lf-, 0) and (lf+, code) are common B operands, exactly the
-// reference's grouping of faces by signature (operator.py:152-170); the host
-// sorts faces by signature and pads each group to a multiple of 8.
-// Tables are pre-swizzled DMMA fragments (4 components per point: value and 3
-// reference gradients; GEMM2 tables carry w_q) read through L1 (__ldg).
+//
+// Work decomposition.  One warp handles a batch of 8 faces (M = faces) that
+// share the signature (lf-, lf+, code), so the tables (lf-, 0) and
+// (lf+, code) are common B operands -- the reference's grouping of faces by
+// signature (operator.py:152-170).  The host sorts faces by signature, pads
+// each group to a multiple of 8 and cuts it into chunks of <= CHUNK batches;
+// one CTA per chunk stages the two tables' DMMA fragments in shared memory
+// once and its warps stream over the chunk's batches.
+//
+// Point layout (4 components per point: value + 3 reference gradients):
+// points are taken in groups of 4; GEMM1 n-tile (g, h) holds columns
+// 2*q + i = (point 4g + q, component 2h + i), so lane (q = lane&3) owns all
+// four components of point 4g + q after the two tiles of group g, and those
+// four values are directly the A fragments of the four GEMM2 k-steps
+// (g, c), k = lane&3 <-> point 4g + k.  Points pad to a multiple of 4
+// (n_qf 20 -> 20, 10 -> 12), not 8.
 // Geometry (unit normal outward from the minus cell, |t_s x t_t|,
 // m = J^-1 n on each side) is recomputed from vertex coordinates
 // (geometry.py:202-236).  Contributions are added to y with fp64 RED.
@@ -28,11 +38,11 @@ struct FaceArgs {
   const double* __restrict__ verts;
   const double* __restrict__ kappa;
   const double* __restrict__ frags;   // per (lf, code) combo: B1 then B2 fragments
-  const int2* __restrict__ batch_combo;  // (minus combo, plus combo); plus = -1 for boundary
+  const int4* __restrict__ chunks;    // (combo-, combo+ or -1, first batch, n batches)
   const int* __restrict__ cm;         // (n_batches*8) minus cell, -1 = padding
   const int* __restrict__ cp;         // (n_batches*8) plus cell (interior)
   const double* __restrict__ tau;     // (n_batches*8)
-  int64_t n_batches;
+  int64_t n_chunks;
   int n_dpc;
   int nc;
   double scale;
@@ -41,16 +51,12 @@ struct FaceArgs {
 template <int N, int QF>
 struct FaceShape {
   static constexpr int KK = (N + 3) / 4;
-  static constexpr int T = (QF + 7) / 8;
+  static constexpr int G = (QF + 3) / 4;       // point groups of 4
   static constexpr int NJ = (N + 7) / 8;
-  static constexpr int NB1 = T * 4 * KK;
-  static constexpr int NB2 = T * 4 * 2 * NJ;
+  static constexpr int NB1 = G * 2 * KK;       // GEMM1 fragments: (g, h, kk)
+  static constexpr int NB2 = G * 4 * NJ;       // GEMM2 fragments: (g, c, nj)
   static constexpr int NFRAG = NB1 + NB2;      // per (lf, code) combo
-};
-
-struct FaceGeo {
-  double m[3];  // J^-1 n (times kappa)
-  double s;     // |t_s x t_t| * scale
+  static constexpr int CHUNK = 32;             // batches per CTA chunk
 };
 
 __device__ __forceinline__ void cell_affine(const FaceArgs& a, int c, Affine& g, Vec3& opp_base,
@@ -73,152 +79,158 @@ __device__ __forceinline__ void apply_inv(const Affine& g, const double (&n)[3],
 }
 
 template <int N, int QF, bool BOUNDARY>
-__global__ void __launch_bounds__(256) face_apply_kernel(FaceArgs a) {
+__global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
+  constexpr int SIDES = BOUNDARY ? 1 : 2;
+  extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
   const int fs = lane >> 2;
   const int q4 = lane & 3;
-  const int64_t nw = (int64_t)gridDim.x * 8;
-  const int64_t nwork = a.n_batches * a.nc;
+  const int warp = threadIdx.x >> 5;
 
-  for (int64_t w = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); w < nwork; w += nw) {
-    const int comp = (int)(w / a.n_batches);
-    const int64_t b = w - (int64_t)comp * a.n_batches;
-    const int2 combo = __ldg(a.batch_combo + b);
-    const int lfm = combo.x / 6;
-    const int c_m = __ldg(a.cm + b * 8 + fs);
-    const bool valid = c_m >= 0;
-    const int c_p = BOUNDARY ? -1 : __ldg(a.cp + b * 8 + fs);
-
-    // ---- gather both sides
-    double am[S::KK], ap[S::KK];
-#pragma unroll
-    for (int kk = 0; kk < S::KK; ++kk) {
-      const int j = 4 * kk + q4;
-      am[kk] = 0.0;
-      ap[kk] = 0.0;
-      if (valid && j < N) {
-        am[kk] = __ldg(a.u + ((int64_t)c_m * N + j) * a.nc + comp);
-        if (!BOUNDARY) ap[kk] = __ldg(a.u + ((int64_t)c_p * N + j) * a.nc + comp);
+  for (int64_t w = blockIdx.x; w < a.n_chunks * a.nc; w += gridDim.x) {
+    const int comp = (int)(w / a.n_chunks);
+    const int4 ch = __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
+    __syncthreads();  // previous chunk's warps are done with the staged tables
+    {
+      const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.x * S::NFRAG * 32);
+      double2* d = reinterpret_cast<double2*>(smem);
+      for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[i] = __ldg(s0 + i);
+      if (!BOUNDARY) {
+        const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.y * S::NFRAG * 32);
+        for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[S::NFRAG * 16 + i] = __ldg(s1 + i);
       }
     }
+    __syncthreads();
+    const double* Fm = smem;
+    const double* Fp = smem + S::NFRAG * 32;
+    const int lfm = ch.x / 6;
 
-    // ---- face geometry
-    FaceGeo gm, gp;
-    double tau = 0.0;
-    {
-      const int cmm = valid ? c_m : 0;
-      Affine Jm;
-      Vec3 opp, fv0;
-      cell_affine(a, cmm, Jm, opp, lfm, fv0);
-      double ds[3], dt[3];
-      face_tangents_ref(lfm, ds, dt);
-      double ts[3], tt[3];
+    for (int bi = warp; bi < ch.w; bi += blockDim.x / 32) {
+      const int64_t b = (int64_t)ch.z + bi;
+      const int c_m = __ldg(a.cm + b * 8 + fs);
+      const bool valid = c_m >= 0;
+      const int c_p = BOUNDARY ? -1 : __ldg(a.cp + b * 8 + fs);
+
+      double am[S::KK], ap[S::KK];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        ts[i] = Jm.J[i][0] * ds[0] + Jm.J[i][1] * ds[1] + Jm.J[i][2] * ds[2];
-        tt[i] = Jm.J[i][0] * dt[0] + Jm.J[i][1] * dt[1] + Jm.J[i][2] * dt[2];
+      for (int kk = 0; kk < S::KK; ++kk) {
+        const int j = 4 * kk + q4;
+        am[kk] = 0.0;
+        ap[kk] = 0.0;
+        if (valid && j < N) {
+          am[kk] = __ldg(a.u + ((int64_t)c_m * N + j) * a.nc + comp);
+          if (!BOUNDARY) ap[kk] = __ldg(a.u + ((int64_t)c_p * N + j) * a.nc + comp);
+        }
       }
-      double n[3] = {ts[1] * tt[2] - ts[2] * tt[1], ts[2] * tt[0] - ts[0] * tt[2],
-                     ts[0] * tt[1] - ts[1] * tt[0]};
-      const double area2 = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
-      // outward from the minus cell: away from the vertex opposite the face
-      const double side = n[0] * (fv0.x - opp.x) + n[1] * (fv0.y - opp.y) + n[2] * (fv0.z - opp.z);
-      const double inv = (side < 0 ? -1.0 : 1.0) / area2;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) n[i] *= inv;
-      apply_inv(Jm, n, gm.m);
-      gm.s = area2 * a.scale;
-      tau = valid ? __ldg(a.tau + b * 8 + fs) : 0.0;
-      double km = 1.0;
-      if (a.kappa) km = __ldg(a.kappa + cmm);
-      if (!BOUNDARY) {
-        const int cpp = valid ? c_p : 0;
-        Affine Jp;
-        Vec3 o2, f2;
-        cell_affine(a, cpp, Jp, o2, 0, f2);
-        apply_inv(Jp, n, gp.m);
-        double kp = 1.0;
-        if (a.kappa) kp = __ldg(a.kappa + cpp);
+
+      // ---- face geometry
+      double mm[3], mp[3] = {0.0, 0.0, 0.0}, s, tau;
+      {
+        const int cmm = valid ? c_m : 0;
+        Affine Jm;
+        Vec3 opp, fv0;
+        cell_affine(a, cmm, Jm, opp, lfm, fv0);
+        double ds[3], dt[3];
+        face_tangents_ref(lfm, ds, dt);
+        double ts[3], tt[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          gm.m[i] *= km;
-          gp.m[i] *= kp;
+          ts[i] = Jm.J[i][0] * ds[0] + Jm.J[i][1] * ds[1] + Jm.J[i][2] * ds[2];
+          tt[i] = Jm.J[i][0] * dt[0] + Jm.J[i][1] * dt[1] + Jm.J[i][2] * dt[2];
         }
-        tau *= fmax(km, kp);
-      } else {
+        double n[3] = {ts[1] * tt[2] - ts[2] * tt[1], ts[2] * tt[0] - ts[0] * tt[2],
+                       ts[0] * tt[1] - ts[1] * tt[0]};
+        const double area2 = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        const double side = n[0] * (fv0.x - opp.x) + n[1] * (fv0.y - opp.y) + n[2] * (fv0.z - opp.z);
+        const double inv = (side < 0 ? -1.0 : 1.0) / area2;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) gm.m[i] *= km;
-        tau *= km;
-      }
-    }
-
-    const double* Fm = a.frags + (int64_t)combo.x * S::NFRAG * 32;
-    const double* Fp = a.frags + (int64_t)(BOUNDARY ? 0 : combo.y) * S::NFRAG * 32;
-    double ym[S::NJ][2], yp[S::NJ][2];
+        for (int i = 0; i < 3; ++i) n[i] *= inv;
+        apply_inv(Jm, n, mm);
+        s = area2 * a.scale;
+        tau = valid ? __ldg(a.tau + b * 8 + fs) : 0.0;
+        const double km = a.kappa ? __ldg(a.kappa + cmm) : 1.0;
+        if (!BOUNDARY) {
+          const int cpp = valid ? c_p : 0;
+          Affine Jp;
+          Vec3 o2, f2;
+          cell_affine(a, cpp, Jp, o2, 0, f2);
+          apply_inv(Jp, n, mp);
+          const double kp = a.kappa ? __ldg(a.kappa + cpp) : 1.0;
 #pragma unroll
-    for (int nj = 0; nj < S::NJ; ++nj) ym[nj][0] = ym[nj][1] = yp[nj][0] = yp[nj][1] = 0.0;
-
-#pragma unroll
-    for (int t = 0; t < S::T; ++t) {
-      double vm[4][2], vp[4][2];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) vm[c][0] = vm[c][1] = vp[c][0] = vp[c][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < S::KK; ++kk)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int f = ((t * 4 + c) * S::KK + kk) * 32 + lane;
-          dmma(vm[c], am[kk], __ldg(Fm + f));
-          if (!BOUNDARY) dmma(vp[c], ap[kk], __ldg(Fp + f));
-        }
-      double qm[4][2], qp[4][2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const double dnm = gm.m[0] * vm[1][i] + gm.m[1] * vm[2][i] + gm.m[2] * vm[3][i];
-        if (BOUNDARY) {
-          qm[0][i] = gm.s * (tau * vm[0][i] - dnm);
-          const double wj = -gm.s * vm[0][i];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) qm[1 + k][i] = wj * gm.m[k];
+          for (int i = 0; i < 3; ++i) {
+            mm[i] *= km;
+            mp[i] *= kp;
+          }
+          tau *= fmax(km, kp);
         } else {
-          const double dnp = gp.m[0] * vp[1][i] + gp.m[1] * vp[2][i] + gp.m[2] * vp[3][i];
-          const double jump = vm[0][i] - vp[0][i];
-          const double qv = gm.s * (tau * jump - 0.5 * (dnm + dnp));
-          const double hw = -0.5 * gm.s * jump;
-          qm[0][i] = qv;
-          qp[0][i] = -qv;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) mm[i] *= km;
+          tau *= km;
+        }
+      }
+
+      double ym[S::NJ][2], yp[S::NJ][2];
+#pragma unroll
+      for (int nj = 0; nj < S::NJ; ++nj) ym[nj][0] = ym[nj][1] = yp[nj][0] = yp[nj][1] = 0.0;
+
+#pragma unroll
+      for (int g = 0; g < S::G; ++g) {
+        double vm[2][2], vp[2][2];  // [h][i] = component 2h+i of point 4g+q4
+#pragma unroll
+        for (int h = 0; h < 2; ++h) vm[h][0] = vm[h][1] = vp[h][0] = vp[h][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < S::KK; ++kk)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int f = ((g * 2 + h) * S::KK + kk) * 32 + lane;
+            dmma(vm[h], am[kk], Fm[f]);
+            if (!BOUNDARY) dmma(vp[h], ap[kk], Fp[f]);
+          }
+        double qm[4], qp[4];
+        const double dnm = mm[0] * vm[0][1] + mm[1] * vm[1][0] + mm[2] * vm[1][1];
+        if (BOUNDARY) {
+          qm[0] = s * (tau * vm[0][0] - dnm);
+          const double wj = -s * vm[0][0];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) qm[1 + k] = wj * mm[k];
+        } else {
+          const double dnp = mp[0] * vp[0][1] + mp[1] * vp[1][0] + mp[2] * vp[1][1];
+          const double jump = vm[0][0] - vp[0][0];
+          const double qv = s * (tau * jump - 0.5 * (dnm + dnp));
+          const double hw = -0.5 * s * jump;
+          qm[0] = qv;
+          qp[0] = -qv;
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
-            qm[1 + k][i] = hw * gm.m[k];
-            qp[1 + k][i] = hw * gp.m[k];
+            qm[1 + k] = hw * mm[k];
+            qp[1 + k] = hw * mp[k];
           }
         }
-      }
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int nj = 0; nj < S::NJ; ++nj) {
-            const int f = (S::NB1 + (((t * 4 + c) * 2 + i) * S::NJ + nj)) * 32 + lane;
-            dmma(ym[nj], qm[c][i], __ldg(Fm + f));
-            if (!BOUNDARY) dmma(yp[nj], qp[c][i], __ldg(Fp + f));
+            const int f = (S::NB1 + (g * 4 + c) * S::NJ + nj) * 32 + lane;
+            dmma(ym[nj], qm[c], Fm[f]);
+            if (!BOUNDARY) dmma(yp[nj], qp[c], Fp[f]);
           }
-    }
+      }
 
-    if (valid) {
+      if (valid) {
 #pragma unroll
-      for (int nj = 0; nj < S::NJ; ++nj)
+        for (int nj = 0; nj < S::NJ; ++nj)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int j = 8 * nj + 2 * q4 + i;
-          if (j < N) {
-            atomicAdd(a.y + ((int64_t)c_m * N + j) * a.nc + comp, ym[nj][i]);
-            if (!BOUNDARY) atomicAdd(a.y + ((int64_t)c_p * N + j) * a.nc + comp, yp[nj][i]);
+          for (int i = 0; i < 2; ++i) {
+            const int j = 8 * nj + 2 * q4 + i;
+            if (j < N) {
+              atomicAdd(a.y + ((int64_t)c_m * N + j) * a.nc + comp, ym[nj][i]);
+              if (!BOUNDARY) atomicAdd(a.y + ((int64_t)c_p * N + j) * a.nc + comp, yp[nj][i]);
+            }
           }
-        }
+      }
     }
+    (void)SIDES;
   }
 }
 

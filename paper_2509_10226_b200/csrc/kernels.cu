@@ -67,24 +67,29 @@ cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& 
 template <int N, int QF, bool BND>
 static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShape<N, QF>;
+  constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
   auto kern = face_apply_kernel<N, QF, BND>;
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  const int64_t work = a.n_batches * a.nc;
-  int64_t blocks = (int64_t)n_sm * per_sm;
-  const int64_t need = (work + 7) / 8;
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
+  static int configured = 0;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    configured = 1;
+  }
   if (info) {
     info->nfrag = S::NFRAG;
+    info->chunk = S::CHUNK;
     info->dmma_per_batch = BND ? (S::NB1 + S::NB2) : 2 * (S::NB1 + S::NB2);
-    info->grid = (int)blocks;
     return cudaSuccess;
   }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, SMEM);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t work = a.n_chunks * a.nc;
   if (work == 0) return cudaSuccess;
-  kern<<<(unsigned)blocks, 256, 0, st>>>(a);
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  if (blocks > work) blocks = work;
+  kern<<<(unsigned)blocks, 256, SMEM, st>>>(a);
   return cudaGetLastError();
 }
 

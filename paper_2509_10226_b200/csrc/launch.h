@@ -19,6 +19,7 @@ struct CellLaunchInfo {
 
 struct FaceLaunchInfo {
   int nfrag = 0;            // fragments per (lf, code) combo
+  int chunk = 0;            // batches per CTA chunk
   int dmma_per_batch = 0;
   int grid = 0;
 };
