@@ -125,6 +125,17 @@ int tmf_hierarchical_reorder(int64_t n_cells, int64_t n_interior_faces,
                              const int32_t* interior_faces, int32_t group_size,
                              int64_t* new_of_old);
 
+/* Host-side setup at scale (no GPU needed), bit-identical to the reference:
+ * face pairing <- mesh._build_faces (mesh.py:84-120); interior_out needs room
+ * for 2*n_cells rows of 5, boundary_out for 4*n_cells rows of 3 (boundary ids
+ * are left 0 for the caller).  CG DoF numbering <- build_dof_map
+ * (dofmap.py:67-123, + the P4 convention of SURVEY Appendix B6). */
+int tmf_build_faces(int64_t n_cells, const int32_t* cells, int64_t n_vertices,
+                    int32_t* interior_out, int64_t* n_interior, int32_t* boundary_out,
+                    int64_t* n_boundary);
+int tmf_build_cg_dofs(int64_t n_cells, const int32_t* cells, int64_t n_vertices, int32_t degree,
+                      int32_t* cell_dofs, int64_t* n_scalar_dofs);
+
 const char* tmf_last_error(void);
 const char* tmf_version(void);
 

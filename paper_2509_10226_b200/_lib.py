@@ -65,11 +65,14 @@ def lib():
         L.tmf_diagonal.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.tmf_pcg.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_void_p]
         L.tmf_hierarchical_reorder.argtypes = [C.c_int64, C.c_int64, _ip, C.c_int32, C.POINTER(C.c_int64)]
+        _lp = C.POINTER(C.c_int64)
+        L.tmf_build_faces.argtypes = [C.c_int64, _ip, C.c_int64, _ip, _lp, _ip, _lp]
+        L.tmf_build_cg_dofs.argtypes = [C.c_int64, _ip, C.c_int64, C.c_int32, _ip, _lp]
         L.tmf_last_error.restype = C.c_char_p
         L.tmf_version.restype = C.c_char_p
         for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
                      "tmf_apply_host", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg",
-                     "tmf_hierarchical_reorder"):
+                     "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -77,7 +80,7 @@ def lib():
 
 EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
             "tmf_apply_host", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
-            "tmf_last_error", "tmf_version")
+            "tmf_build_faces", "tmf_build_cg_dofs", "tmf_last_error", "tmf_version")
 
 
 def check(rc: int) -> None:

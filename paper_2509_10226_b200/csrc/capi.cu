@@ -168,6 +168,8 @@ namespace {
 
 int n_dofs_per_cell(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
 
+constexpr int64_t kFaceWindow = 8192;
+
 // Split [first, first+count) batches of one signature into CTA chunks.
 void push_chunks(std::vector<int4>& out, int cm, int cp, int64_t first, int64_t count, int chunk) {
   for (int64_t b = 0; b < count; b += chunk)
@@ -180,9 +182,12 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   // owning-cell order inside a signature (mesh.py:117)
   std::vector<int64_t> order(nif);
   std::iota(order.begin(), order.end(), 0);
+  // faces are grouped by signature inside windows of kFaceWindow consecutive minus
+  // cells, so the GPU sweeps the cell range once (u/y stay L2-resident) instead of
+  // once per signature
   auto sig = [&](int64_t f) {
     const int32_t* r = d->interior_faces + 5 * f;
-    return r[1] * 24 + r[3] * 6 + r[4];
+    return (int64_t)(r[0] / kFaceWindow) * 96 + r[1] * 24 + r[3] * 6 + r[4];
   };
   for (int64_t f = 0; f < nif; ++f) {
     const int32_t* r = d->interior_faces + 5 * f;
@@ -196,7 +201,7 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   std::vector<double> tau;
   int64_t nb = 0;
   for (int64_t s = 0; s < nif;) {
-    const int key = sig(order[s]);
+    const int64_t key = sig(order[s]);
     int64_t e = s;
     while (e < nif && sig(order[e]) == key) ++e;
     const int32_t* r0 = d->interior_faces + 5 * order[s];
@@ -231,12 +236,25 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   std::vector<int> bcm;
   std::vector<double> btau;
   nb = 0;
-  for (int lf = 0; lf < 4; ++lf) {
-    std::vector<int64_t> sel;
-    for (int64_t f = 0; f < nbf; ++f) {
+  std::vector<std::vector<int64_t>> groups;
+  {
+    std::vector<int64_t> bord;
+    for (int64_t f = 0; f < nbf; ++f)
+      if (d->boundary_dirichlet && d->boundary_dirichlet[f]) bord.push_back(f);
+    auto bsig = [&](int64_t f) {
       const int32_t* r = d->boundary_faces + 3 * f;
-      if (r[1] == lf && d->boundary_dirichlet && d->boundary_dirichlet[f]) sel.push_back(f);
+      return (int64_t)(r[0] / kFaceWindow) * 4 + r[1];
+    };
+    std::stable_sort(bord.begin(), bord.end(), [&](int64_t a, int64_t b) { return bsig(a) < bsig(b); });
+    for (size_t s = 0; s < bord.size();) {
+      size_t e = s;
+      while (e < bord.size() && bsig(bord[e]) == bsig(bord[s])) ++e;
+      groups.emplace_back(bord.begin() + s, bord.begin() + e);
+      s = e;
     }
+  }
+  for (const auto& sel : groups) {
+    const int lf = d->boundary_faces[3 * sel[0] + 1];
     const int64_t nbatch = ((int64_t)sel.size() + 7) / 8;
     push_chunks(bchunks, lf * 6, -1, nb, nbatch, chunk);
     for (int64_t k = 0; k < nbatch * 8; ++k) {
@@ -302,7 +320,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   if (!dg && !d->cell_dofs) return fail(TMF_EINVAL, "CG operator needs a CG dof map");
   if (dg && d->n_scalar_dofs != d->n_cells * d->n_dofs_per_cell)
     return fail(TMF_EINVAL, "DG operator needs a DG dof map");
-  if (d->n_scalar_dofs * d->n_components >= (int64_t)1 << 40) return fail(TMF_EINVAL, "too many dofs");
+  if (d->n_scalar_dofs >= ((int64_t)1 << 31)) return fail(TMF_EINVAL, "too many dofs for int32 indexing");
   if (d->operator_kind == TMF_DG_HELMHOLTZ && !d->value_matrix)
     return fail(TMF_EINVAL, "Helmholtz needs the value table");
   const bool faces = dg && !(d->operator_kind == TMF_DG_HELMHOLTZ && d->diffusivity == 0.0);

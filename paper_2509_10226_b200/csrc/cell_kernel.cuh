@@ -79,37 +79,50 @@ __global__ void __launch_bounds__(BLOCK) cell_apply_kernel(CellArgs a) {
   const int64_t ntiles = ctiles * a.nc;
   const int64_t nwarps = (int64_t)gridDim.x * (BLOCK / 32);
 
-  for (int64_t tile = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); tile < ntiles;
-       tile += nwarps) {
+  // Index prefetch: the DoF indices and vertex ids of the warp's next tile are
+  // loaded while the current tile computes, so each tile start pays one memory
+  // round trip (u, coordinates) instead of two (indices, then data).
+  int64_t tile = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+  int nidx[S::KK];
+  int nvid[4];
+  auto load_indices = [&](int64_t t) {
+    const int cmp = (int)(t / ctiles);
+    const int64_t c = (t - (int64_t)cmp * ctiles) * 8 + cs;
+    const bool ok = t < ntiles && c < a.n_cells;
+#pragma unroll
+    for (int kk = 0; kk < S::KK; ++kk) {
+      const int j = 4 * kk + q4;
+      nidx[kk] = -1;
+      if (ok && j < N) nidx[kk] = DG ? (int)(c * N + j) : __ldg(a.dofs + c * N + j);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) nvid[i] = ok ? __ldg(a.cells + 4 * c + i) : 0;
+  };
+  load_indices(tile);
+
+  for (; tile < ntiles; tile += nwarps) {
     const int comp = (int)(tile / ctiles);
     const int64_t cell = (tile - (int64_t)comp * ctiles) * 8 + cs;
     const bool valid = cell < a.n_cells;
+    int vid[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) vid[i] = nvid[i];
 
     // ---- gather: A fragments of GEMM1 (lane owns DoFs 4kk + q4 of its cell)
     double av[S::KK];
 #pragma unroll
     for (int kk = 0; kk < S::KK; ++kk) {
-      const int j = 4 * kk + q4;
-      av[kk] = 0.0;
-      if (valid && j < N) {
-        int64_t g;
-        if (DG) {
-          g = cell * N + j;
-        } else {
-          g = __ldg(a.dofs + cell * N + j);
-        }
-        if (g >= 0) av[kk] = __ldg(a.u + g * a.nc + comp);
-      }
+      const int g = nidx[kk];
+      av[kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + comp) : 0.0;
     }
+    // DG indices are (cell*N + j) and may exceed int range only beyond 2^31 DoFs
+    // (rejected at plan creation).
 
     // ---- geometry: G = scale * adj adj^T / det, mass factor det
     double G[6];
     double mdet = 0.0;
     {
-      int vid[4];
       const int64_t c = valid ? cell : 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) vid[i] = __ldg(a.cells + 4 * c + i);
       Affine g;
       affine_from_vertices(load_vertex(a.verts, vid[0]), load_vertex(a.verts, vid[1]),
                            load_vertex(a.verts, vid[2]), load_vertex(a.verts, vid[3]), g);
@@ -118,6 +131,7 @@ __global__ void __launch_bounds__(BLOCK) cell_apply_kernel(CellArgs a) {
       stiffness_metric(g, sc, G);
       if (MASS) mdet = a.mass_scale * g.det;
     }
+    load_indices(tile + nwarps);
 
     double yacc[S::NJ][2];
 #pragma unroll

@@ -106,11 +106,28 @@ __global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
     const double* Fp = smem + S::NFRAG * 32;
     const int lfm = ch.x / 6;
 
-    for (int bi = warp; bi < ch.w; bi += blockDim.x / 32) {
+    // prefetch the next batch's face records while the current one computes
+    const int nwb = blockDim.x / 32;
+    int n_cm = -1, n_cp = -1;
+    double n_tau = 0.0;
+    if (warp < ch.w) {
+      const int64_t b0 = (int64_t)ch.z + warp;
+      n_cm = __ldg(a.cm + b0 * 8 + fs);
+      if (!BOUNDARY) n_cp = __ldg(a.cp + b0 * 8 + fs);
+      n_tau = __ldg(a.tau + b0 * 8 + fs);
+    }
+    for (int bi = warp; bi < ch.w; bi += nwb) {
       const int64_t b = (int64_t)ch.z + bi;
-      const int c_m = __ldg(a.cm + b * 8 + fs);
+      const int c_m = n_cm;
       const bool valid = c_m >= 0;
-      const int c_p = BOUNDARY ? -1 : __ldg(a.cp + b * 8 + fs);
+      const int c_p = n_cp;
+      const double tau_f = n_tau;
+      if (bi + nwb < ch.w) {
+        const int64_t bn = b + nwb;
+        n_cm = __ldg(a.cm + bn * 8 + fs);
+        if (!BOUNDARY) n_cp = __ldg(a.cp + bn * 8 + fs);
+        n_tau = __ldg(a.tau + bn * 8 + fs);
+      }
 
       double am[S::KK], ap[S::KK];
 #pragma unroll
@@ -148,7 +165,7 @@ __global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
         for (int i = 0; i < 3; ++i) n[i] *= inv;
         apply_inv(Jm, n, mm);
         s = area2 * a.scale;
-        tau = valid ? __ldg(a.tau + b * 8 + fs) : 0.0;
+        tau = valid ? tau_f : 0.0;
         const double km = a.kappa ? __ldg(a.kappa + cmm) : 1.0;
         if (!BOUNDARY) {
           const int cpp = valid ? c_p : 0;

@@ -95,8 +95,23 @@ def face_local_dofs(p: int) -> list[np.ndarray]:
     return out
 
 
+def _cg_dofs_native(cells: np.ndarray, n_vertices: int, p: int):
+    import ctypes as C
+
+    from . import _lib
+
+    c = np.ascontiguousarray(cells, dtype=np.int32)
+    out = np.empty((len(c), n_dofs_per_cell(p)), dtype=np.int32)
+    ns = C.c_int64()
+    _lib.check(_lib.lib().tmf_build_cg_dofs(len(c), _lib.ptr(c, C.c_int32), int(n_vertices), int(p),
+                                            _lib.ptr(out, C.c_int32), C.byref(ns)))
+    return out, int(ns.value)
+
+
 def build_dof_map(mesh: TetMesh, p: int, space: str, n_components: int = 1,
-                  dirichlet_boundary_ids=()) -> DoFMap:
+                  dirichlet_boundary_ids=(), method: str = "native") -> DoFMap:
+    """``method``: "native" (C++ bucket sort, csrc/setup.cpp) or "numpy" (vectorised);
+    both bit-identical to the reference numbering."""
     if space not in (CG, DG):
         raise ValueError(f"unknown space {space!r}")
     if n_components not in (1, 3):
@@ -111,6 +126,12 @@ def build_dof_map(mesh: TetMesh, p: int, space: str, n_components: int = 1,
         cell_dofs = np.arange(n * nd, dtype=np.int32).reshape(n, nd)
         return DoFMap(DG, p, n_components, n * nd, cell_dofs, np.zeros(n * nd, dtype=bool))
 
+    if method == "native":
+        cell_dofs, n_scalar = _cg_dofs_native(mesh.cells, mesh.n_vertices, p)
+        return DoFMap(CG, p, n_components, n_scalar, cell_dofs,
+                      _dirichlet_mask(mesh, p, cell_dofs, n_scalar, dirichlet_boundary_ids))
+    if method != "numpy":
+        raise ValueError(f"unknown method {method!r}")
     cells = mesh.cells.astype(np.int64)
     _, tags = reference_nodes(p)
     per_edge = p - 1
@@ -151,6 +172,13 @@ def build_dof_map(mesh: TetMesh, p: int, space: str, n_components: int = 1,
     if n_scalar >= 2 ** 31:
         raise ValueError("DoF count exceeds int32 indexing")
 
+    cell_dofs = cell_dofs.astype(np.int32)
+    return DoFMap(CG, p, n_components, int(n_scalar), cell_dofs,
+                  _dirichlet_mask(mesh, p, cell_dofs, n_scalar, dirichlet_boundary_ids))
+
+
+def _dirichlet_mask(mesh, p, cell_dofs, n_scalar, dirichlet_boundary_ids):
+    """Closure of the selected boundary faces (dofmap.py:125-142)."""
     mask = np.zeros(n_scalar, dtype=bool)
     if len(dirichlet_boundary_ids) and len(mesh.boundary_faces):
         bf = mesh.boundary_faces
@@ -159,4 +187,4 @@ def build_dof_map(mesh: TetMesh, p: int, space: str, n_components: int = 1,
         for lf in range(4):
             rows = bf[sel & (bf[:, 1] == lf), 0]
             mask[cell_dofs[rows[:, None], fl[lf][None, :]].reshape(-1)] = True
-    return DoFMap(CG, p, n_components, int(n_scalar), cell_dofs.astype(np.int32), mask)
+    return mask

@@ -168,3 +168,24 @@ def test_reorder_chain_and_determinism():
     assert np.array_equal(nb, nb2)
     d = np.abs(nb[faces[:, 0]] - nb[faces[:, 2]])
     assert d.max() <= 16
+
+
+# ------------------------------------------------------------------ native (C++) vs numpy setup
+@pytest.mark.parametrize("n,seed", [(2, 0), (4, 3)])
+def test_native_setup_matches_numpy_path(n, seed):
+    m = M.kuhn_cube_mesh(n, seed=seed)
+    a = M.build_faces(m.cells, m.vertices, M.cube_boundary_ids, method="native")
+    b = M.build_faces(m.cells, m.vertices, M.cube_boundary_ids, method="numpy")
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for p in (1, 2, 3, 4):
+        x = D.build_dof_map(m, p, "cg", 1, (0, 3), method="native")
+        y = D.build_dof_map(m, p, "cg", 1, (0, 3), method="numpy")
+        assert x.n_scalar_dofs == y.n_scalar_dofs
+        assert np.array_equal(x.cell_dofs, y.cell_dofs)
+        assert np.array_equal(x.dirichlet_mask, y.dirichlet_mask)
+
+
+def test_native_faces_reject_nonmanifold():
+    cells = np.array([[0, 1, 2, 3], [0, 1, 2, 4], [0, 1, 2, 5]], dtype=np.int32)
+    with pytest.raises(ValueError):
+        M.build_faces(cells)
