@@ -110,10 +110,12 @@ struct tmf_plan {
   int* if_cm = nullptr;
   int* if_cp = nullptr;
   double* if_tau = nullptr;
+  double* if_geo = nullptr;
   int64_t n_if_batches = 0, n_if_chunks = 0;
   int4* bf_chunks = nullptr;
   int* bf_cm = nullptr;
   double* bf_tau = nullptr;
+  double* bf_geo = nullptr;
   int64_t n_bf_batches = 0, n_bf_chunks = 0;
   // staging for host applies / solver scratch
   double* stage_u = nullptr;
@@ -141,17 +143,27 @@ struct tmf_plan {
     tmf::FaceArgs a{};
     a.u = u;
     a.y = y;
-    a.cells = cells;
-    a.verts = verts;
-    a.kappa = kappa;
     a.frags = face_frags;
     a.chunks = boundary ? bf_chunks : if_chunks;
     a.cm = boundary ? bf_cm : if_cm;
     a.cp = boundary ? nullptr : if_cp;
-    a.tau = boundary ? bf_tau : if_tau;
+    a.geo = boundary ? bf_geo : if_geo;
     a.n_chunks = boundary ? n_bf_chunks : n_if_chunks;
     a.n_dpc = N;
     a.nc = nc;
+    return a;
+  }
+  tmf::FaceGeoArgs face_geo_args(bool boundary) const {
+    tmf::FaceGeoArgs a{};
+    a.cells = cells;
+    a.verts = verts;
+    a.kappa = kappa;
+    a.chunks = boundary ? bf_chunks : if_chunks;
+    a.cm = boundary ? bf_cm : if_cm;
+    a.cp = boundary ? nullptr : if_cp;
+    a.tau = boundary ? bf_tau : if_tau;
+    a.geo = boundary ? bf_geo : if_geo;
+    a.n_chunks = boundary ? n_bf_chunks : n_if_chunks;
     a.scale = stiff_scale;
     return a;
   }
@@ -159,7 +171,7 @@ struct tmf_plan {
     for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
-                    (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S})
+                    (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo})
       if (p) cudaFree(p);
   }
 };
@@ -450,6 +462,15 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     if ((int64_t)fr.size() != 24LL * fi.nfrag * 32) return bail(fail(TMF_EINVAL, "internal: face fragments"));
     if ((rc = upload(&P->face_frags, fr.data(), fr.size(), &total))) return bail(rc);
     if ((rc = build_face_batches(P, d, fi.chunk, &total))) return bail(rc);
+    // per-face geometry, computed once on the device (64 B per face slot)
+    for (int bnd = 0; bnd < 2; ++bnd) {
+      const int64_t slots = (bnd ? P->n_bf_batches : P->n_if_batches) * 8;
+      if (!slots) continue;
+      double** g = bnd ? &P->bf_geo : &P->if_geo;
+      TMF_CUDA(cudaMalloc(g, sizeof(double) * 8 * slots));
+      total += sizeof(double) * 8 * slots;
+      TMF_CUDA(tmf::launch_face_geometry(bnd != 0, P->face_geo_args(bnd != 0), P->n_sm, 0));
+    }
     P->info.n_face_batches = (int32_t)(P->n_if_batches + P->n_bf_batches);
     P->info.flops_issued += (double)P->nc * (P->n_if_batches * fi.dmma_per_batch +
                                              P->n_bf_batches * fi.dmma_per_batch / 2) * 512.0;

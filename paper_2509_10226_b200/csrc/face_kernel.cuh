@@ -24,8 +24,8 @@
 // (g, c), k = lane&3 <-> point 4g + k.  Points pad to a multiple of 4
 // (n_qf 20 -> 20, 10 -> 12), not 8.
 // Geometry (unit normal outward from the minus cell, |t_s x t_t|,
-// m = J^-1 n on each side) is recomputed from vertex coordinates
-// (geometry.py:202-236).  Contributions are added to y with fp64 RED.
+// m = J^-1 n on each side, geometry.py:202-236) is computed once per plan by
+// face_geometry_kernel.  Contributions are added to y with fp64 RED.
 #pragma once
 #include "common.cuh"
 
@@ -34,17 +34,30 @@ namespace tmf {
 struct FaceArgs {
   const double* __restrict__ u;
   double* __restrict__ y;
-  const int* __restrict__ cells;
-  const double* __restrict__ verts;
-  const double* __restrict__ kappa;
   const double* __restrict__ frags;   // per (lf, code) combo: B1 then B2 fragments
   const int4* __restrict__ chunks;    // (combo-, combo+ or -1, first batch, n batches)
   const int* __restrict__ cm;         // (n_batches*8) minus cell, -1 = padding
   const int* __restrict__ cp;         // (n_batches*8) plus cell (interior)
-  const double* __restrict__ tau;     // (n_batches*8)
+  const double* __restrict__ geo;     // (n_batches*8, 8): m-[3], m+[3], s, tau (see below)
   int64_t n_chunks;
   int n_dpc;
   int nc;
+};
+
+// Per-face geometry, computed once at plan creation by face_geometry_kernel and
+// streamed (64 B per face, coalesced) by the apply -- the reference stores the
+// same factors in GeometryData (face_jxw, face_m_minus/plus, geometry.py:44-53):
+//   m± = kappa± J±^-1 n,  s = |t_s x t_t| * scale,  tau_eff = tau * max(kappa-, kappa+)
+struct FaceGeoArgs {
+  const int* __restrict__ cells;
+  const double* __restrict__ verts;
+  const double* __restrict__ kappa;
+  const int4* __restrict__ chunks;
+  const int* __restrict__ cm;
+  const int* __restrict__ cp;
+  const double* __restrict__ tau;     // raw penalty per slot
+  double* __restrict__ geo;
+  int64_t n_chunks;
   double scale;
 };
 
@@ -59,13 +72,13 @@ struct FaceShape {
   static constexpr int CHUNK = 32;             // batches per CTA chunk
 };
 
-__device__ __forceinline__ void cell_affine(const FaceArgs& a, int c, Affine& g, Vec3& opp_base,
-                                            int lf, Vec3& face_v0) {
+__device__ __forceinline__ void cell_affine(const int* __restrict__ cells, const double* __restrict__ verts,
+                                            int c, Affine& g, Vec3& opp_base, int lf, Vec3& face_v0) {
   int vid[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) vid[i] = __ldg(a.cells + 4 * (int64_t)c + i);
-  const Vec3 x0 = load_vertex(a.verts, vid[0]), x1 = load_vertex(a.verts, vid[1]),
-             x2 = load_vertex(a.verts, vid[2]), x3 = load_vertex(a.verts, vid[3]);
+  for (int i = 0; i < 4; ++i) vid[i] = __ldg(cells + 4 * (int64_t)c + i);
+  const Vec3 x0 = load_vertex(verts, vid[0]), x1 = load_vertex(verts, vid[1]),
+             x2 = load_vertex(verts, vid[2]), x3 = load_vertex(verts, vid[3]);
   affine_from_vertices(x0, x1, x2, x3, g);
   // local face lf is opposite local vertex lf; its first corner is v1 (lf 0) or v0
   opp_base = lf == 0 ? x0 : (lf == 1 ? x1 : (lf == 2 ? x2 : x3));
@@ -78,15 +91,77 @@ __device__ __forceinline__ void apply_inv(const Affine& g, const double (&n)[3],
   for (int i = 0; i < 3; ++i) m[i] = inv * (g.adj[i][0] * n[0] + g.adj[i][1] * n[1] + g.adj[i][2] * n[2]);
 }
 
+// One thread per face slot: unit normal outward from the minus cell
+// (geometry.py:207-225), surface JxW factor and m = J^-1 n on each side.
+template <bool BOUNDARY>
+__global__ void face_geometry_kernel(FaceGeoArgs a) {
+  for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
+    const int4 ch = __ldg(a.chunks + ci);
+    const int lfm = ch.x / 6;
+    for (int k = threadIdx.x; k < ch.w * 8; k += blockDim.x) {
+      const int64_t slot = (int64_t)ch.z * 8 + k;
+      double* out = a.geo + slot * 8;
+      const int c_m = a.cm[slot];
+      if (c_m < 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) out[i] = 0.0;
+        continue;
+      }
+      Affine Jm;
+      Vec3 opp, fv0;
+      cell_affine(a.cells, a.verts, c_m, Jm, opp, lfm, fv0);
+      double ds[3], dt[3];
+      face_tangents_ref(lfm, ds, dt);
+      double ts[3], tt[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        ts[i] = Jm.J[i][0] * ds[0] + Jm.J[i][1] * ds[1] + Jm.J[i][2] * ds[2];
+        tt[i] = Jm.J[i][0] * dt[0] + Jm.J[i][1] * dt[1] + Jm.J[i][2] * dt[2];
+      }
+      double n[3] = {ts[1] * tt[2] - ts[2] * tt[1], ts[2] * tt[0] - ts[0] * tt[2],
+                     ts[0] * tt[1] - ts[1] * tt[0]};
+      const double area2 = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+      const double side = n[0] * (fv0.x - opp.x) + n[1] * (fv0.y - opp.y) + n[2] * (fv0.z - opp.z);
+      const double inv = (side < 0 ? -1.0 : 1.0) / area2;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) n[i] *= inv;
+      double mm[3], mp[3] = {0.0, 0.0, 0.0};
+      apply_inv(Jm, n, mm);
+      double tau = a.tau[slot];
+      const double km = a.kappa ? a.kappa[c_m] : 1.0;
+      if (!BOUNDARY) {
+        const int c_p = a.cp[slot];
+        Affine Jp;
+        Vec3 o2, f2;
+        cell_affine(a.cells, a.verts, c_p, Jp, o2, 0, f2);
+        apply_inv(Jp, n, mp);
+        const double kp = a.kappa ? a.kappa[c_p] : 1.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) mp[i] *= kp;
+        tau *= fmax(km, kp);
+      } else {
+        tau *= km;
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        out[i] = mm[i] * km;
+        out[3 + i] = mp[i];
+      }
+      out[6] = area2 * a.scale;
+      out[7] = tau;
+    }
+  }
+}
+
 template <int N, int QF, bool BOUNDARY>
 __global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
-  constexpr int SIDES = BOUNDARY ? 1 : 2;
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
   const int fs = lane >> 2;
   const int q4 = lane & 3;
   const int warp = threadIdx.x >> 5;
+  const int nwb = blockDim.x >> 5;
 
   for (int64_t w = blockIdx.x; w < a.n_chunks * a.nc; w += gridDim.x) {
     const int comp = (int)(w / a.n_chunks);
@@ -104,88 +179,51 @@ __global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
     __syncthreads();
     const double* Fm = smem;
     const double* Fp = smem + S::NFRAG * 32;
-    const int lfm = ch.x / 6;
 
-    // prefetch the next batch's face records while the current one computes
-    const int nwb = blockDim.x / 32;
+    // Software pipeline over the warp's batches: the next batch's face record,
+    // geometry and gathered u values are loaded while the current batch computes.
+    double nam[S::KK], nap[S::KK], ng[8];
     int n_cm = -1, n_cp = -1;
-    double n_tau = 0.0;
-    if (warp < ch.w) {
-      const int64_t b0 = (int64_t)ch.z + warp;
-      n_cm = __ldg(a.cm + b0 * 8 + fs);
-      if (!BOUNDARY) n_cp = __ldg(a.cp + b0 * 8 + fs);
-      n_tau = __ldg(a.tau + b0 * 8 + fs);
-    }
-    for (int bi = warp; bi < ch.w; bi += nwb) {
-      const int64_t b = (int64_t)ch.z + bi;
-      const int c_m = n_cm;
-      const bool valid = c_m >= 0;
-      const int c_p = n_cp;
-      const double tau_f = n_tau;
-      if (bi + nwb < ch.w) {
-        const int64_t bn = b + nwb;
-        n_cm = __ldg(a.cm + bn * 8 + fs);
-        if (!BOUNDARY) n_cp = __ldg(a.cp + bn * 8 + fs);
-        n_tau = __ldg(a.tau + bn * 8 + fs);
+    auto fetch = [&](int bi) {
+      n_cm = -1;
+      n_cp = -1;
+      if (bi < ch.w) {
+        const int64_t slot = ((int64_t)ch.z + bi) * 8 + fs;
+        n_cm = __ldg(a.cm + slot);
+        if (!BOUNDARY) n_cp = __ldg(a.cp + slot);
+        const double2* gp = reinterpret_cast<const double2*>(a.geo + slot * 8);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double2 v = __ldg(gp + i);
+          ng[2 * i] = v.x;
+          ng[2 * i + 1] = v.y;
+        }
       }
-
-      double am[S::KK], ap[S::KK];
 #pragma unroll
       for (int kk = 0; kk < S::KK; ++kk) {
         const int j = 4 * kk + q4;
-        am[kk] = 0.0;
-        ap[kk] = 0.0;
-        if (valid && j < N) {
-          am[kk] = __ldg(a.u + ((int64_t)c_m * N + j) * a.nc + comp);
-          if (!BOUNDARY) ap[kk] = __ldg(a.u + ((int64_t)c_p * N + j) * a.nc + comp);
+        nam[kk] = 0.0;
+        nap[kk] = 0.0;
+        if (n_cm >= 0 && j < N) {
+          nam[kk] = __ldg(a.u + ((int64_t)n_cm * N + j) * a.nc + comp);
+          if (!BOUNDARY) nap[kk] = __ldg(a.u + ((int64_t)n_cp * N + j) * a.nc + comp);
         }
       }
+    };
+    fetch(warp);
 
-      // ---- face geometry
-      double mm[3], mp[3] = {0.0, 0.0, 0.0}, s, tau;
-      {
-        const int cmm = valid ? c_m : 0;
-        Affine Jm;
-        Vec3 opp, fv0;
-        cell_affine(a, cmm, Jm, opp, lfm, fv0);
-        double ds[3], dt[3];
-        face_tangents_ref(lfm, ds, dt);
-        double ts[3], tt[3];
+    for (int bi = warp; bi < ch.w; bi += nwb) {
+      const int c_m = n_cm, c_p = n_cp;
+      double am[S::KK], ap[S::KK];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          ts[i] = Jm.J[i][0] * ds[0] + Jm.J[i][1] * ds[1] + Jm.J[i][2] * ds[2];
-          tt[i] = Jm.J[i][0] * dt[0] + Jm.J[i][1] * dt[1] + Jm.J[i][2] * dt[2];
-        }
-        double n[3] = {ts[1] * tt[2] - ts[2] * tt[1], ts[2] * tt[0] - ts[0] * tt[2],
-                       ts[0] * tt[1] - ts[1] * tt[0]};
-        const double area2 = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
-        const double side = n[0] * (fv0.x - opp.x) + n[1] * (fv0.y - opp.y) + n[2] * (fv0.z - opp.z);
-        const double inv = (side < 0 ? -1.0 : 1.0) / area2;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) n[i] *= inv;
-        apply_inv(Jm, n, mm);
-        s = area2 * a.scale;
-        tau = valid ? tau_f : 0.0;
-        const double km = a.kappa ? __ldg(a.kappa + cmm) : 1.0;
-        if (!BOUNDARY) {
-          const int cpp = valid ? c_p : 0;
-          Affine Jp;
-          Vec3 o2, f2;
-          cell_affine(a, cpp, Jp, o2, 0, f2);
-          apply_inv(Jp, n, mp);
-          const double kp = a.kappa ? __ldg(a.kappa + cpp) : 1.0;
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            mm[i] *= km;
-            mp[i] *= kp;
-          }
-          tau *= fmax(km, kp);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 3; ++i) mm[i] *= km;
-          tau *= km;
-        }
+      for (int kk = 0; kk < S::KK; ++kk) {
+        am[kk] = nam[kk];
+        ap[kk] = nap[kk];
       }
+      const double mm[3] = {ng[0], ng[1], ng[2]};
+      const double mp[3] = {ng[3], ng[4], ng[5]};
+      const double s = ng[6], tau = ng[7];
+      fetch(bi + nwb);
 
       double ym[S::NJ][2], yp[S::NJ][2];
 #pragma unroll
@@ -234,7 +272,7 @@ __global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
           }
       }
 
-      if (valid) {
+      if (c_m >= 0) {
 #pragma unroll
         for (int nj = 0; nj < S::NJ; ++nj)
 #pragma unroll
@@ -247,7 +285,6 @@ __global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
           }
       }
     }
-    (void)SIDES;
   }
 }
 

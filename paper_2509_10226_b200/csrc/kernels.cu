@@ -1,6 +1,8 @@
 // Kernel instantiations and launchers for tetmf_b200 (sm_100a).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "cell_kernel.cuh"
 #include "face_kernel.cuh"
 #include "launch.h"
@@ -111,6 +113,16 @@ cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, i
 #undef TMF_FACE
   *supported = false;
   return cudaSuccess;
+}
+
+cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st) {
+  if (a.n_chunks == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)std::min<int64_t>(a.n_chunks, (int64_t)n_sm * 8);
+  if (boundary)
+    face_geometry_kernel<true><<<blocks, 256, 0, st>>>(a);
+  else
+    face_geometry_kernel<false><<<blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,

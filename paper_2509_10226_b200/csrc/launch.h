@@ -7,6 +7,7 @@ namespace tmf {
 
 struct CellArgs;
 struct FaceArgs;
+struct FaceGeoArgs;
 
 struct CellLaunchInfo {
   int dmma_per_tile = 0;
@@ -29,6 +30,7 @@ cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& 
                         cudaStream_t st, CellLaunchInfo* info, bool* supported);
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
                         cudaStream_t st, FaceLaunchInfo* info, bool* supported);
+cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
                          cudaStream_t st);
 
