@@ -101,6 +101,7 @@ struct tmf_plan {
   double* verts = nullptr;
   double* kappa = nullptr;
   double* cell_frags = nullptr;
+  double* cell_geo = nullptr;
   double* face_frags = nullptr;
   int* cells = nullptr;
   int* dofs = nullptr;
@@ -129,14 +130,10 @@ struct tmf_plan {
     a.u = u;
     a.y = y;
     a.dofs = dg ? nullptr : dofs;
-    a.cells = cells;
-    a.verts = verts;
-    a.kappa = kappa;
+    a.cgeo = cell_geo;
     a.frags = cell_frags;
     a.n_cells = n_cells;
     a.nc = nc;
-    a.mass_scale = mass_scale;
-    a.stiff_scale = stiff_scale;
     return a;
   }
   tmf::FaceArgs face_args(const double* u, double* y, bool boundary) const {
@@ -171,7 +168,7 @@ struct tmf_plan {
     for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
-                    (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo})
+                    (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo})
       if (p) cudaFree(p);
   }
 };
@@ -411,6 +408,14 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     if ((int)fr.size() != ci.frag_doubles) return bail(fail(TMF_EINVAL, "internal: fragment size"));
     if ((rc = upload(&P->cell_frags, fr.data(), fr.size(), &total))) return bail(rc);
     P->info.flops_issued = (double)ci.tiles * ci.dmma_per_tile * 512.0;
+  }
+
+  // per-cell geometry (G, mass factor), computed once on the device
+  {
+    TMF_CUDA(cudaMalloc(&P->cell_geo, sizeof(double) * 8 * P->n_cells));
+    total += sizeof(double) * 8 * P->n_cells;
+    tmf::CellGeoArgs g{P->cells, P->verts, P->kappa, P->cell_geo, P->n_cells, P->stiff_scale, P->mass_scale};
+    TMF_CUDA(tmf::launch_cell_geometry(g, P->n_sm, 0));
   }
 
   // CG dof map (masked = ~idx) and the Dirichlet fix-up list

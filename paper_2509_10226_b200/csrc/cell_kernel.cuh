@@ -36,15 +36,46 @@ struct CellArgs {
   const double* __restrict__ u;
   double* __restrict__ y;
   const int* __restrict__ dofs;    // CG: (n_cells, N) encoded; DG: nullptr (contiguous)
-  const int* __restrict__ cells;   // (n_cells, 4)
-  const double* __restrict__ verts;
-  const double* __restrict__ kappa;  // per-cell Laplace coefficient or nullptr
+  const double* __restrict__ cgeo; // (n_cells, 8): G[6] (scaled), mass factor, 0
   const double* __restrict__ frags;  // B1 then B2 fragments (global; staged to smem)
   int64_t n_cells;
   int nc;                          // interleaved components
-  double mass_scale;
-  double stiff_scale;
 };
+
+// Per-cell geometry, computed once per plan by cell_geometry_kernel (the
+// reference stores J^-T and JxW per cell, geometry.py:145-151; 8 doubles here):
+//   G = stiff_scale * kappa_e * det J * J^-1 J^-T  (packed 00,01,02,11,12,22)
+//   m = mass_scale * det J
+struct CellGeoArgs {
+  const int* __restrict__ cells;
+  const double* __restrict__ verts;
+  const double* __restrict__ kappa;
+  double* __restrict__ cgeo;
+  int64_t n_cells;
+  double stiff_scale;
+  double mass_scale;
+};
+
+static __global__ void cell_geometry_kernel(CellGeoArgs a) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.n_cells;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int vid[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) vid[i] = __ldg(a.cells + 4 * e + i);
+    Affine g;
+    affine_from_vertices(load_vertex(a.verts, vid[0]), load_vertex(a.verts, vid[1]),
+                         load_vertex(a.verts, vid[2]), load_vertex(a.verts, vid[3]), g);
+    double sc = a.stiff_scale;
+    if (a.kappa) sc *= a.kappa[e];
+    double G[6];
+    stiffness_metric(g, sc, G);
+    double* o = a.cgeo + 8 * e;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) o[i] = G[i];
+    o[6] = a.mass_scale * g.det;
+    o[7] = 0.0;
+  }
+}
 
 template <int N, int Q, bool MASS>
 struct CellShape {
@@ -57,11 +88,15 @@ struct CellShape {
   static constexpr int NFRAG = NB1 + NB2;
   static constexpr int SMEM = NFRAG * 32 * 8;
   static constexpr int DMMA_PER_TILE = NB1 + NB2;
+  // tiles per warp iteration: two independent 8-cell tiles share every B
+  // fragment load (half the LDS traffic) and double the DMMA chains in flight
+  static constexpr int MT = (KK + 2 * NJ) <= 7 ? 2 : 1;
 };
 
 template <int N, int Q, bool MASS, bool DG, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) cell_apply_kernel(CellArgs a) {
   using S = CellShape<N, Q, MASS>;
+  constexpr int MT = S::MT;
   extern __shared__ __align__(16) double smem[];
   {
     const double2* src = reinterpret_cast<const double2*>(a.frags);
@@ -76,100 +111,108 @@ __global__ void __launch_bounds__(BLOCK) cell_apply_kernel(CellArgs a) {
   const int cs = lane >> 2;  // cell slot in the tile
   const int q4 = lane & 3;
   const int64_t ctiles = (a.n_cells + 7) / 8;
-  const int64_t ntiles = ctiles * a.nc;
+  const int64_t cst = (ctiles + MT - 1) / MT;       // super-tiles per component
+  const int64_t nst = cst * a.nc;
   const int64_t nwarps = (int64_t)gridDim.x * (BLOCK / 32);
 
-  // Index prefetch: the DoF indices and vertex ids of the warp's next tile are
-  // loaded while the current tile computes, so each tile start pays one memory
-  // round trip (u, coordinates) instead of two (indices, then data).
-  int64_t tile = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
-  int nidx[S::KK];
-  int nvid[4];
+  // Index prefetch: the DoF indices of the warp's next super-tile are loaded
+  // while the current one computes, so each start pays one memory round trip
+  // (u and the per-cell geometry, issued together) instead of two.
+  int64_t st = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+  int nidx[MT][S::KK];
   auto load_indices = [&](int64_t t) {
-    const int cmp = (int)(t / ctiles);
-    const int64_t c = (t - (int64_t)cmp * ctiles) * 8 + cs;
-    const bool ok = t < ntiles && c < a.n_cells;
+    const int cmp = (int)(t / cst);
 #pragma unroll
-    for (int kk = 0; kk < S::KK; ++kk) {
-      const int j = 4 * kk + q4;
-      nidx[kk] = -1;
-      if (ok && j < N) nidx[kk] = DG ? (int)(c * N + j) : __ldg(a.dofs + c * N + j);
+    for (int m = 0; m < MT; ++m) {
+      const int64_t c = ((t - (int64_t)cmp * cst) * MT + m) * 8 + cs;
+      const bool ok = t < nst && c < a.n_cells;
+#pragma unroll
+      for (int kk = 0; kk < S::KK; ++kk) {
+        const int j = 4 * kk + q4;
+        nidx[m][kk] = -1;
+        if (ok && j < N) nidx[m][kk] = DG ? (int)(c * N + j) : __ldg(a.dofs + c * N + j);
+      }
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) nvid[i] = ok ? __ldg(a.cells + 4 * c + i) : 0;
   };
-  load_indices(tile);
+  load_indices(st);
 
-  for (; tile < ntiles; tile += nwarps) {
-    const int comp = (int)(tile / ctiles);
-    const int64_t cell = (tile - (int64_t)comp * ctiles) * 8 + cs;
-    const bool valid = cell < a.n_cells;
-    int vid[4];
+  for (; st < nst; st += nwarps) {
+    const int comp = (int)(st / cst);
+    int64_t cell[MT];
+    bool valid[MT];
+    double av[MT][S::KK];
+    double G[MT][6];
+    double mdet[MT];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) vid[i] = nvid[i];
-
-    // ---- gather: A fragments of GEMM1 (lane owns DoFs 4kk + q4 of its cell)
-    double av[S::KK];
+    for (int m = 0; m < MT; ++m) {
+      cell[m] = ((st - (int64_t)comp * cst) * MT + m) * 8 + cs;
+      valid[m] = cell[m] < a.n_cells;
+      // ---- gather: A fragments of GEMM1 (lane owns DoFs 4kk + q4 of its cell)
 #pragma unroll
-    for (int kk = 0; kk < S::KK; ++kk) {
-      const int g = nidx[kk];
-      av[kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + comp) : 0.0;
+      for (int kk = 0; kk < S::KK; ++kk) {
+        const int g = nidx[m][kk];
+        av[m][kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + comp) : 0.0;
+      }
+      // ---- geometry (precomputed per plan)
+      const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * (valid[m] ? cell[m] : 0));
+      const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
+      G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
+      G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
+      mdet[m] = MASS ? __ldg(a.cgeo + 8 * (valid[m] ? cell[m] : 0) + 6) : 0.0;
     }
-    // DG indices are (cell*N + j) and may exceed int range only beyond 2^31 DoFs
-    // (rejected at plan creation).
+    load_indices(st + nwarps);
 
-    // ---- geometry: G = scale * adj adj^T / det, mass factor det
-    double G[6];
-    double mdet = 0.0;
-    {
-      const int64_t c = valid ? cell : 0;
-      Affine g;
-      affine_from_vertices(load_vertex(a.verts, vid[0]), load_vertex(a.verts, vid[1]),
-                           load_vertex(a.verts, vid[2]), load_vertex(a.verts, vid[3]), g);
-      double sc = a.stiff_scale;
-      if (a.kappa) sc *= __ldg(a.kappa + c);
-      stiffness_metric(g, sc, G);
-      if (MASS) mdet = a.mass_scale * g.det;
-    }
-    load_indices(tile + nwarps);
-
-    double yacc[S::NJ][2];
+    double yacc[MT][S::NJ][2];
 #pragma unroll
-    for (int nj = 0; nj < S::NJ; ++nj) yacc[nj][0] = yacc[nj][1] = 0.0;
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int nj = 0; nj < S::NJ; ++nj) yacc[m][nj][0] = yacc[m][nj][1] = 0.0;
 
 #pragma unroll
     for (int t = 0; t < S::T; ++t) {
-      double v[S::NC][2];
+      double v[MT][S::NC][2];
 #pragma unroll
-      for (int c = 0; c < S::NC; ++c) v[c][0] = v[c][1] = 0.0;
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int c = 0; c < S::NC; ++c) v[m][c][0] = v[m][c][1] = 0.0;
 #pragma unroll
       for (int kk = 0; kk < S::KK; ++kk) {
 #pragma unroll
-        for (int c = 0; c < S::NC; ++c)
-          dmma(v[c], av[kk], sB1[((t * S::NC + c) * S::KK + kk) * 32 + lane]);
+        for (int c = 0; c < S::NC; ++c) {
+          const double b = sB1[((t * S::NC + c) * S::KK + kk) * 32 + lane];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(v[m][c], av[m][kk], b);
+        }
       }
       // D action at the lane's two points (w_q lives in the GEMM2 table)
-      double d[S::NC][2];
+      double d[MT][S::NC][2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        constexpr int o = MASS ? 1 : 0;
-        const double g0 = v[o][i], g1 = v[o + 1][i], g2 = v[o + 2][i];
-        d[o][i] = G[0] * g0 + G[1] * g1 + G[2] * g2;
-        d[o + 1][i] = G[1] * g0 + G[3] * g1 + G[4] * g2;
-        d[o + 2][i] = G[2] * g0 + G[4] * g1 + G[5] * g2;
-        if (MASS) d[0][i] = mdet * v[0][i];
-      }
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          constexpr int o = MASS ? 1 : 0;
+          const double g0 = v[m][o][i], g1 = v[m][o + 1][i], g2 = v[m][o + 2][i];
+          d[m][o][i] = G[m][0] * g0 + G[m][1] * g1 + G[m][2] * g2;
+          d[m][o + 1][i] = G[m][1] * g0 + G[m][3] * g1 + G[m][4] * g2;
+          d[m][o + 2][i] = G[m][2] * g0 + G[m][4] * g1 + G[m][5] * g2;
+          if (MASS) d[m][0][i] = mdet[m] * v[m][0][i];
+        }
 #pragma unroll
       for (int c = 0; c < S::NC; ++c)
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int nj = 0; nj < S::NJ; ++nj)
-            dmma(yacc[nj], d[c][i], sB2[(((t * S::NC + c) * 2 + i) * S::NJ + nj) * 32 + lane]);
+          for (int nj = 0; nj < S::NJ; ++nj) {
+            const double b = sB2[(((t * S::NC + c) * 2 + i) * S::NJ + nj) * 32 + lane];
+#pragma unroll
+            for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][c][i], b);
+          }
     }
 
     // ---- scatter / store: lane owns DoFs 8nj + 2q4 + {0,1}
-    if (valid) {
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (!valid[m]) continue;
 #pragma unroll
       for (int nj = 0; nj < S::NJ; ++nj)
 #pragma unroll
@@ -177,10 +220,10 @@ __global__ void __launch_bounds__(BLOCK) cell_apply_kernel(CellArgs a) {
           const int j = 8 * nj + 2 * q4 + i;
           if (j < N) {
             if (DG) {
-              a.y[(cell * N + j) * a.nc + comp] = yacc[nj][i];
+              a.y[(cell[m] * N + j) * a.nc + comp] = yacc[m][nj][i];
             } else {
-              const int64_t g = __ldg(a.dofs + cell * N + j);
-              if (g >= 0) atomicAdd(a.y + g * a.nc + comp, yacc[nj][i]);
+              const int64_t g = __ldg(a.dofs + cell[m] * N + j);
+              if (g >= 0) atomicAdd(a.y + g * a.nc + comp, yacc[m][nj][i]);
             }
           }
         }

@@ -25,13 +25,14 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t tiles = ((a.n_cells + 7) / 8) * a.nc;
+  const int64_t supertiles = ((a.n_cells + 8 * S::MT - 1) / (8 * S::MT)) * a.nc;
   int64_t blocks = (int64_t)n_sm * per_sm;
-  const int64_t need = (tiles + BLOCK / 32 - 1) / (BLOCK / 32);
+  const int64_t need = (supertiles + BLOCK / 32 - 1) / (BLOCK / 32);
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   if (info) {
     info->dmma_per_tile = S::DMMA_PER_TILE;
-    info->tiles = tiles;
+    info->tiles = supertiles * S::MT;
     info->block = BLOCK;
     info->grid = (int)blocks;
     info->smem = S::SMEM;
@@ -113,6 +114,11 @@ cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, i
 #undef TMF_FACE
   *supported = false;
   return cudaSuccess;
+}
+
+cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st) {
+  cell_geometry_kernel<<<n_sm * 8, 256, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st) {
