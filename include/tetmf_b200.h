@@ -117,6 +117,24 @@ int tmf_diagonal(tmf_plan* plan, double* diag, void* stream);
 int tmf_pcg(tmf_plan* plan, const double* b, double* x, int iters, double* res_norms,
             void* stream);
 
+/* Fused point-Jacobi PCG vector kernels for callers that drive the iteration
+ * themselves (the multi-GPU solver: local partial sums are all-reduced between
+ * the calls).  All pointers are device pointers on the current device; the
+ * scalar outputs are device doubles that are ACCUMULATED (caller zeroes them).
+ *   tmf_vec_dot:       *out += a.b
+ *   tmf_pcg_init:      x = 0, r = b, z = r/d, p = z;  *rz += r.z, *rr += r.r
+ *   tmf_pcg_update:    alpha = *rz_k / *pq_k; x += alpha p; r -= alpha q; z = r/d;
+ *                      *rz_next += r.z, *rr_next += r.r
+ *   tmf_pcg_direction: p = z + (*rz_next / *rz_k) p                              */
+int tmf_vec_dot(const double* a, const double* b, int64_t n, double* out, void* stream);
+int tmf_pcg_init(const double* b, const double* d, double* x, double* r, double* z, double* p,
+                 int64_t n, double* rz, double* rr, void* stream);
+int tmf_pcg_update(const double* p, const double* q, const double* d, double* x, double* r,
+                   double* z, int64_t n, const double* rz_k, const double* pq_k, double* rz_next,
+                   double* rr_next, void* stream);
+int tmf_pcg_direction(const double* z, double* p, int64_t n, const double* rz_k,
+                      const double* rz_next, void* stream);
+
 /* Hierarchical cell reordering (host-side setup; no GPU needed).  Writes the
  * permutation new_of_old (cell e moves to position new_of_old[e]), to be
  * applied like mesh.apply_cell_permutation (mesh.py:291-293).  Replaces the

@@ -68,11 +68,17 @@ def lib():
         _lp = C.POINTER(C.c_int64)
         L.tmf_build_faces.argtypes = [C.c_int64, _ip, C.c_int64, _ip, _lp, _ip, _lp]
         L.tmf_build_cg_dofs.argtypes = [C.c_int64, _ip, C.c_int64, C.c_int32, _ip, _lp]
+        _v = C.c_void_p
+        L.tmf_vec_dot.argtypes = [_v, _v, C.c_int64, _v, _v]
+        L.tmf_pcg_init.argtypes = [_v, _v, _v, _v, _v, _v, C.c_int64, _v, _v, _v]
+        L.tmf_pcg_update.argtypes = [_v, _v, _v, _v, _v, _v, C.c_int64, _v, _v, _v, _v, _v]
+        L.tmf_pcg_direction.argtypes = [_v, _v, C.c_int64, _v, _v, _v]
         L.tmf_last_error.restype = C.c_char_p
         L.tmf_version.restype = C.c_char_p
         for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
                      "tmf_apply_host", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg",
-                     "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs"):
+                     "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs",
+                     "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -80,7 +86,8 @@ def lib():
 
 EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
             "tmf_apply_host", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
-            "tmf_build_faces", "tmf_build_cg_dofs", "tmf_last_error", "tmf_version")
+            "tmf_build_faces", "tmf_build_cg_dofs", "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update",
+            "tmf_pcg_direction", "tmf_last_error", "tmf_version")
 
 
 def check(rc: int) -> None:

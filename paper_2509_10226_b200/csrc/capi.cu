@@ -630,4 +630,50 @@ int tmf_pcg(tmf_plan* P, const double* b, double* x, int iters, double* res_norm
   return TMF_OK;
 }
 
+// ---- fused PCG vector kernels (device pointers; scalars are device doubles) --
+int tmf_vec_dot(const double* a, const double* b, int64_t n, double* out, void* stream) {
+  if (!a || !b || !out || n < 0) return fail(TMF_EINVAL, "bad argument");
+  int dev = 0, sms = 0;
+  TMF_CUDA(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  tmf::dot_kernel<<<sms * 4, 512, 0, (cudaStream_t)stream>>>(a, b, n, out);
+  TMF_CUDA(cudaGetLastError());
+  return TMF_OK;
+}
+
+int tmf_pcg_init(const double* b, const double* d, double* x, double* r, double* z, double* p, int64_t n,
+                 double* rz, double* rr, void* stream) {
+  if (!b || !d || !x || !r || !z || !p || !rz || !rr || n < 0) return fail(TMF_EINVAL, "bad argument");
+  int dev = 0, sms = 0;
+  TMF_CUDA(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  tmf::pcg_init_kernel<<<sms * 4, 512, 0, (cudaStream_t)stream>>>(b, d, x, r, z, p, n, rz, rr);
+  TMF_CUDA(cudaGetLastError());
+  return TMF_OK;
+}
+
+int tmf_pcg_update(const double* p, const double* q, const double* d, double* x, double* r, double* z,
+                   int64_t n, const double* rz_k, const double* pq_k, double* rz_next, double* rr_next,
+                   void* stream) {
+  if (!p || !q || !d || !x || !r || !z || n < 0) return fail(TMF_EINVAL, "bad argument");
+  int dev = 0, sms = 0;
+  TMF_CUDA(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  tmf::pcg_update_kernel<<<sms * 4, 512, 0, (cudaStream_t)stream>>>(p, q, d, x, r, z, n, rz_k, pq_k, rz_next,
+                                                                      rr_next);
+  TMF_CUDA(cudaGetLastError());
+  return TMF_OK;
+}
+
+int tmf_pcg_direction(const double* z, double* p, int64_t n, const double* rz_k, const double* rz_next,
+                      void* stream) {
+  if (!z || !p || n < 0) return fail(TMF_EINVAL, "bad argument");
+  int dev = 0, sms = 0;
+  TMF_CUDA(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  tmf::pcg_direction_kernel<<<sms * 4, 512, 0, (cudaStream_t)stream>>>(z, p, n, rz_k, rz_next);
+  TMF_CUDA(cudaGetLastError());
+  return TMF_OK;
+}
+
 }  // extern "C"

@@ -1,0 +1,420 @@
+"""Domain decomposition for multi-GPU applies (the reference is
+single-process, SPEC.md:17 -- the paper scales with MPI + METIS).
+
+One process per GPU.  The mesh is split into k subdomains by recursive
+coordinate bisection of cell centroids (deterministic; k = 2^L gives the
+2x2x2 blocks at k = 8).  Each rank runs the B200 plan of its local problem
+and exchanges ghost data over NCCL (``torch.distributed`` P2P, grouped):
+
+CG (identity Dirichlet rows kept):
+    owner(d) = lowest rank whose cells touch DoF d; local vector = owned DoFs
+    (ascending global id) then ghosts (by owner, then global id).
+    apply: forward halo (owners -> ghost copies of u), local cell kernel,
+    reverse halo (ghost partial y -> owner, added; constrained DoFs excluded,
+    their rows are fixed by the owner), result = owned slice.
+DG (SIPG / Helmholtz):
+    local cells = owned cells (global order) + face-neighbour ghost cells;
+    forward halo of the ghosts' u blocks only; partition faces are evaluated
+    on both sides and each rank keeps its own cells' rows.  Artificial
+    boundary faces of the ghost layer are never Dirichlet.
+Krylov dot products: local partial sums over owned DoFs + all_reduce (sum).
+
+The exchange lists are pure host data built identically on every rank.
+``HaloExchange`` works with any torch.distributed backend: NCCL for GPU
+tensors, gloo for the CPU tests (tests/test_distributed.py), where the local
+apply is the CPU oracle; the GPU path plugs in the B200 plan.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .mesh import TetMesh, build_faces
+from .reference import FACE_VERTICES_ARR
+
+__all__ = ["partition_cells", "CgSubdomain", "DgSubdomain", "build_cg_subdomain",
+           "build_dg_subdomain", "HaloExchange"]
+
+
+def partition_cells(mesh: TetMesh, k: int) -> np.ndarray:
+    """Recursive coordinate bisection of cell centroids into k parts (k a power of 2).
+
+    Each split sorts by (coordinate along the widest axis, cell id) and cuts at
+    the middle, so the partition is deterministic."""
+    if k < 1 or (k & (k - 1)):
+        raise ValueError("k must be a power of two")
+    cen = mesh.vertices[mesh.cells].mean(axis=1)
+    part = np.zeros(mesh.n_cells, dtype=np.int64)
+
+    def split(ids, lo, nparts):
+        if nparts == 1:
+            part[ids] = lo
+            return
+        c = cen[ids]
+        axis = int(np.argmax(c.max(axis=0) - c.min(axis=0)))
+        order = np.lexsort((ids, c[:, axis]))
+        half = len(ids) // 2
+        split(ids[order[:half]], lo, nparts // 2)
+        split(ids[order[half:]], lo + nparts // 2, nparts // 2)
+
+    split(np.arange(mesh.n_cells), 0, k)
+    return part
+
+
+@dataclass
+class Exchange:
+    """Per-rank halo plan: for each peer, local indices to pack and to unpack."""
+
+    peers: list = field(default_factory=list)
+    send: dict = field(default_factory=dict)    # peer -> local indices (pack)
+    recv: dict = field(default_factory=dict)    # peer -> local indices (unpack)
+
+
+@dataclass
+class CgSubdomain:
+    rank: int
+    mesh: TetMesh                 # local cells, local vertex numbering
+    cell_dofs: np.ndarray         # (n_local_cells, n_dpc) local DoF ids
+    dirichlet_mask: np.ndarray    # (n_local,) bool
+    l2g: np.ndarray               # local -> global DoF
+    n_owned: int
+    forward: Exchange             # u: owners -> ghosts
+    reverse: Exchange             # y: ghosts -> owners (added)
+
+
+@dataclass
+class DgSubdomain:
+    rank: int
+    mesh: TetMesh                 # owned + ghost cells, local numbering
+    cell_l2g: np.ndarray          # local -> global cell
+    n_owned_cells: int
+    dirichlet_faces: np.ndarray   # (n_bf_local,) bool
+    interior_face_g: np.ndarray   # local interior face -> global interior face
+    boundary_face_g: np.ndarray   # local boundary face -> global boundary face (-1 = artificial)
+    forward: Exchange             # cell blocks of u: owners -> ghosts (cell indices)
+
+
+def _local_mesh(mesh: TetMesh, cells_g: np.ndarray) -> tuple[TetMesh, np.ndarray]:
+    verts_g, cells_l = np.unique(mesh.cells[cells_g], return_inverse=True)
+    cells_l = cells_l.reshape(-1, 4).astype(np.int32)
+    ifc, bfc = build_faces(cells_l)
+    return TetMesh(mesh.vertices[verts_g], cells_l, ifc, bfc), verts_g
+
+
+def build_cg_subdomain(mesh: TetMesh, cell_dofs: np.ndarray, dirichlet_mask: np.ndarray,
+                       part: np.ndarray, rank: int, k: int) -> CgSubdomain:
+    nd = cell_dofs.shape[1]
+    n_dofs = len(dirichlet_mask)
+    owner = np.full(n_dofs, k, dtype=np.int64)
+    np.minimum.at(owner, cell_dofs.ravel().astype(np.int64), np.repeat(part, nd))
+    touched = []                                           # DoFs touched by each rank
+    for r in range(k):
+        touched.append(np.unique(cell_dofs[part == r]))
+    l2g_all = []
+    for r in range(k):
+        d = touched[r]
+        own = d[owner[d] == r]
+        gh = d[owner[d] != r]
+        gh = gh[np.lexsort((gh, owner[gh]))]
+        l2g_all.append(np.concatenate([own, gh]))
+
+    def g2l(r, g):
+        l2g = l2g_all[r]
+        n_own = int(np.sum(owner[l2g] == r))
+        own = l2g[:n_own]
+        pos = np.searchsorted(own, g)
+        out = np.empty(len(g), dtype=np.int64)
+        hit = (pos < n_own) & (own[np.minimum(pos, n_own - 1)] == g) if n_own else np.zeros(len(g), bool)
+        out[hit] = pos[hit]
+        if np.any(~hit):
+            gh = l2g[n_own:]
+            idx = {int(v): i for i, v in enumerate(gh)}
+            out[~hit] = [n_own + idx[int(v)] for v in g[~hit]]
+        return out
+
+    fwd, rev = Exchange(), Exchange()
+    for s in range(k):
+        if s == rank:
+            continue
+        # ghosts on s owned by rank -> rank sends u, receives y partials
+        ls = l2g_all[s]
+        gh_s = ls[owner[ls] == rank]
+        gh_s = np.sort(gh_s)
+        # ghosts on rank owned by s
+        lr = l2g_all[rank]
+        gh_r = np.sort(lr[owner[lr] == s])
+        if len(gh_s) == 0 and len(gh_r) == 0:
+            continue
+        fwd.peers.append(s)
+        rev.peers.append(s)
+        fwd.send[s] = g2l(rank, gh_s)
+        fwd.recv[s] = g2l(rank, gh_r)
+        # reverse: constrained DoFs are never scattered -> excluded
+        rev_send = gh_r[~dirichlet_mask[gh_r]]
+        rev_recv = gh_s[~dirichlet_mask[gh_s]]
+        rev.send[s] = g2l(rank, rev_send)
+        rev.recv[s] = g2l(rank, rev_recv)
+    cells_g = np.flatnonzero(part == rank)
+    lmesh, _ = _local_mesh(mesh, cells_g)
+    l2g = l2g_all[rank]
+    lcd = g2l(rank, cell_dofs[cells_g].ravel().astype(np.int64)).reshape(-1, nd).astype(np.int32)
+    n_owned = int(np.sum(owner[l2g] == rank))
+    return CgSubdomain(rank, lmesh, lcd, dirichlet_mask[l2g], l2g, n_owned, fwd, rev)
+
+
+def build_dg_subdomain(mesh: TetMesh, part: np.ndarray, rank: int, k: int,
+                       dirichlet_ids=()) -> DgSubdomain:
+    ifc = mesh.interior_faces.astype(np.int64)
+    cm, cp = ifc[:, 0], ifc[:, 2]
+
+    def ghosts_of(r):
+        a = (part[cm] == r) & (part[cp] != r)
+        b = (part[cp] == r) & (part[cm] != r)
+        g = np.unique(np.concatenate([cp[a], cm[b]]))
+        return g[np.lexsort((g, part[g]))]
+
+    owned = np.flatnonzero(part == rank)
+    ghosts = ghosts_of(rank)
+    cells_g = np.concatenate([owned, ghosts])
+    lmesh, _ = _local_mesh(mesh, cells_g)
+    # map local faces back to global faces (sorted vertex triples)
+    g_tri_i = np.sort(mesh.cells[ifc[:, 0, None], FACE_VERTICES_ARR[ifc[:, 1]]], axis=1)
+    bfc = mesh.boundary_faces.astype(np.int64)
+    g_tri_b = np.sort(mesh.cells[bfc[:, 0, None], FACE_VERTICES_ARR[bfc[:, 1]]], axis=1)
+    lc_g = cells_g                                     # local cell -> global cell
+    li, lb = lmesh.interior_faces.astype(np.int64), lmesh.boundary_faces.astype(np.int64)
+    l_tri_i = np.sort(mesh.cells[lc_g[li[:, 0]][:, None], FACE_VERTICES_ARR[li[:, 1]]], axis=1)
+    l_tri_b = np.sort(mesh.cells[lc_g[lb[:, 0]][:, None], FACE_VERTICES_ARR[lb[:, 1]]], axis=1)
+
+    def match(q, ref):
+        keys = {tuple(t): i for i, t in enumerate(ref.tolist())}
+        return np.array([keys.get(tuple(t), -1) for t in q.tolist()], dtype=np.int64)
+
+    if_g = match(l_tri_i, g_tri_i)
+    bf_g = match(l_tri_b, g_tri_b)
+    bids = np.where(bf_g >= 0, bfc[np.maximum(bf_g, 0), 2], -1)
+    lb_out = lb.copy()
+    lb_out[:, 2] = bids
+    lmesh.boundary_faces = lb_out.astype(np.int32)
+    dset = np.array(sorted(dirichlet_ids), dtype=np.int64)
+    dfaces = np.isin(bids, dset) & (bids >= 0)
+
+    fwd = Exchange()
+    n_own = len(owned)
+    for s in range(k):
+        if s == rank:
+            continue
+        gh_r = ghosts[part[ghosts] == s]                       # my ghosts owned by s
+        gh_s = ghosts_of(s)
+        gh_s = gh_s[part[gh_s] == rank]                         # s's ghosts owned by me
+        if len(gh_r) == 0 and len(gh_s) == 0:
+            continue
+        fwd.peers.append(s)
+        fwd.send[s] = np.searchsorted(owned, gh_s)             # local owned cell index
+        fwd.recv[s] = n_own + np.flatnonzero(part[ghosts] == s)
+    return DgSubdomain(rank, lmesh, cells_g, n_own, dfaces, if_g, bf_g, fwd)
+
+
+class HaloExchange:
+    """Grouped P2P exchange over torch.distributed (NCCL on GPUs, gloo on CPU).
+
+    ``block`` = entries per index (1 for CG DoFs, n_dpc*n_comp for DG cells).
+    Pack/unpack are device gathers/scatters on the vector's own device."""
+
+    def __init__(self, ex: Exchange, block: int, device):
+        import torch
+
+        self.peers = list(ex.peers)
+        self.block = block
+        self.send = {p: torch.as_tensor(self._expand(ex.send[p], block), device=device) for p in self.peers}
+        self.recv = {p: torch.as_tensor(self._expand(ex.recv[p], block), device=device) for p in self.peers}
+        self.sbuf = {p: None for p in self.peers}
+        self.rbuf = {p: None for p in self.peers}
+
+    @staticmethod
+    def _expand(idx, block):
+        idx = np.asarray(idx, dtype=np.int64)
+        if block == 1:
+            return idx
+        return (idx[:, None] * block + np.arange(block)[None, :]).ravel()
+
+    def _exchange(self, vec, add: bool):
+        import torch
+        import torch.distributed as dist
+
+        ops = []
+        for p in self.peers:
+            self.sbuf[p] = vec.index_select(0, self.send[p])
+            self.rbuf[p] = torch.empty(len(self.recv[p]), dtype=vec.dtype, device=vec.device)
+            if len(self.sbuf[p]):
+                ops.append(dist.P2POp(dist.isend, self.sbuf[p], p))
+            if len(self.rbuf[p]):
+                ops.append(dist.P2POp(dist.irecv, self.rbuf[p], p))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for p in self.peers:
+            if len(self.rbuf[p]):
+                if add:
+                    vec.index_add_(0, self.recv[p], self.rbuf[p])
+                else:
+                    vec.index_copy_(0, self.recv[p], self.rbuf[p])
+
+    def forward(self, vec):
+        """Owners -> ghost copies (overwrite)."""
+        self._exchange(vec, add=False)
+
+    def reverse_add(self, vec):
+        """Ghost partials -> owners (accumulate)."""
+        self._exchange(vec, add=True)
+
+
+# --------------------------------------------------------------------------- operators
+def _stream_of(t):
+    import torch
+
+    return torch.cuda.current_stream(t.device).cuda_stream if t.is_cuda else 0
+
+
+class DistributedCgOperator:
+    """CG Laplace apply on a k-way partition: y_owned = A u_owned.
+
+    ``local_factory(mesh, dofmap, geometry, basis)`` may supply the local apply
+    (a callable on local vectors); by default it is the rank's B200 plan, whose
+    kernels run on the rank's current CUDA device."""
+
+    def __init__(self, mesh, dofmap, geometry, basis, rank: int, world: int, part=None,
+                 device=None, local_factory=None):
+        import torch
+
+        from .dofmap import DoFMap
+        from .operator import CgPoissonOperator, OperatorConfig
+
+        self.rank, self.world = rank, world
+        self.part = partition_cells(mesh, world) if part is None else part
+        self.sub = build_cg_subdomain(mesh, dofmap.cell_dofs, dofmap.dirichlet_mask, self.part, rank, world)
+        n_local = len(self.sub.l2g)
+        ldm = DoFMap("cg", dofmap.degree, 1, n_local, self.sub.cell_dofs, self.sub.dirichlet_mask)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if local_factory is None:
+            op = CgPoissonOperator(self.sub.mesh, ldm, geometry, basis,
+                                   OperatorConfig(device=self.device.index or 0))
+            self.local_op = op
+
+            def local(u, y):
+                op.apply_into(u.data_ptr(), y.data_ptr(), _stream_of(u))
+        else:
+            self.local_op = None
+            fn = local_factory(self.sub.mesh, ldm, geometry, basis)
+
+            def local(u, y):
+                y.copy_(fn(u))
+        self._local = local
+        self.fwd = HaloExchange(self.sub.forward, 1, self.device)
+        self.rev = HaloExchange(self.sub.reverse, 1, self.device)
+        self.u_loc = torch.zeros(n_local, dtype=torch.float64, device=self.device)
+        self.y_loc = torch.zeros(n_local, dtype=torch.float64, device=self.device)
+
+    @property
+    def n_owned(self) -> int:
+        return self.sub.n_owned
+
+    @property
+    def owned_global_ids(self) -> np.ndarray:
+        return self.sub.l2g[: self.sub.n_owned]
+
+    def apply(self, u_owned, out=None):
+        n = self.sub.n_owned
+        self.u_loc[:n].copy_(u_owned)
+        self.fwd.forward(self.u_loc)
+        self._local(self.u_loc, self.y_loc)
+        self.rev.reverse_add(self.y_loc)
+        if out is None:
+            return self.y_loc[:n].clone()
+        out.copy_(self.y_loc[:n])
+        return out
+
+    def diagonal(self):
+        """Owned slice of diag(A): local matrix-free diagonal + reverse halo."""
+        import torch
+
+        from . import _lib
+        import ctypes as C
+
+        d = torch.zeros(len(self.sub.l2g), dtype=torch.float64, device=self.device)
+        _lib.check(_lib.lib().tmf_diagonal(self.local_op._plan, C.c_void_p(d.data_ptr()),
+                                            C.c_void_p(_stream_of(d))))
+        self.rev.reverse_add(d)
+        return d[: self.sub.n_owned].clone()
+
+
+class DistributedDgOperator:
+    """DG-SIPG / Helmholtz apply on a k-way partition (forward halo of ghost cells only).
+
+    ``kind`` = "sipg" or "helmholtz" (scalar mass + per-cell kappa, KappaHelmholtzOperator)."""
+
+    def __init__(self, mesh, dofmap, geometry, basis, sipg, rank: int, world: int, kind="sipg",
+                 dirichlet_ids=(), kappa=None, mass_scale=1.0, part=None, device=None, local_factory=None):
+        import torch
+
+        from .dofmap import DoFMap
+        from .operator import DgSipgOperator, KappaHelmholtzOperator, OperatorConfig, SipgConfig
+
+        self.rank, self.world = rank, world
+        self.part = partition_cells(mesh, world) if part is None else part
+        sub = self.sub = build_dg_subdomain(mesh, self.part, rank, world, dirichlet_ids)
+        nd = dofmap.cell_dofs.shape[1]
+        nc = dofmap.n_components
+        self.block = nd * nc
+        n_loc_cells = len(sub.cell_l2g)
+        ldm = DoFMap("dg", dofmap.degree, nc, n_loc_cells * nd,
+                     np.arange(n_loc_cells * nd, dtype=np.int32).reshape(n_loc_cells, nd),
+                     np.zeros(n_loc_cells * nd, dtype=bool))
+        tau_i = np.asarray(sipg.tau_interior)[sub.interior_face_g]
+        tau_b = np.where(sub.boundary_face_g >= 0,
+                         np.asarray(sipg.tau_boundary)[np.maximum(sub.boundary_face_g, 0)], 0.0)
+        lsipg = SipgConfig(sipg.penalty_constant, tau_i, tau_b)
+        lkappa = None if kappa is None else np.asarray(kappa)[sub.cell_l2g]
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        cfg = OperatorConfig(device=self.device.index or 0) if self.device.type == "cuda" else None
+        if local_factory is None:
+            if kind == "sipg":
+                op = DgSipgOperator(sub.mesh, ldm, geometry, basis, lsipg, cfg, dirichlet_ids)
+            else:
+                op = KappaHelmholtzOperator(sub.mesh, ldm, geometry, basis, lsipg, lkappa, mass_scale, cfg,
+                                            dirichlet_ids)
+            self.local_op = op
+
+            def local(u, y):
+                op.apply_into(u.data_ptr(), y.data_ptr(), _stream_of(u))
+        else:
+            self.local_op = None
+            fn = local_factory(sub.mesh, ldm, geometry, basis, lsipg, lkappa, dirichlet_ids)
+
+            def local(u, y):
+                y.copy_(fn(u))
+        self._local = local
+        self.fwd = HaloExchange(sub.forward, self.block, self.device)
+        n_local = n_loc_cells * self.block
+        self.u_loc = torch.zeros(n_local, dtype=torch.float64, device=self.device)
+        self.y_loc = torch.zeros(n_local, dtype=torch.float64, device=self.device)
+
+    @property
+    def n_owned(self) -> int:
+        return self.sub.n_owned_cells * self.block
+
+    def owned_global_ids(self) -> np.ndarray:
+        c = self.sub.cell_l2g[: self.sub.n_owned_cells]
+        return (c[:, None] * self.block + np.arange(self.block)[None, :]).ravel()
+
+    def apply(self, u_owned, out=None):
+        n = self.n_owned
+        self.u_loc[:n].copy_(u_owned)
+        self.fwd.forward(self.u_loc)
+        self._local(self.u_loc, self.y_loc)
+        if out is None:
+            return self.y_loc[:n].clone()
+        out.copy_(self.y_loc[:n])
+        return out
