@@ -17,8 +17,11 @@ reference's batched NumPy loop (oracle/ref_apply.py; the reference package
 itself cannot travel to the GPU box) with one worker process per host core
 on a bounded sample of batches of the same workload, extrapolated per DoF.
 
-Multi-GPU (torchrun, N>1): ``scaling: "weak"``, each rank applies the full
-operator (replicas; the partitioned NCCL-halo path is measured separately).
+Multi-GPU (torchrun, N>1): ``scaling: "weak"``.  The global mesh grows to
+round(48 N^(1/3))^3 x 6 cells, is split by recursive coordinate bisection into
+N subdomains (paper_2509_10226_b200.distributed), and every apply runs the
+forward NCCL halo, the local B200 kernel and the reverse (additive) halo;
+``value`` = global DoFs per step / max-over-ranks step time.
 """
 
 from __future__ import annotations
@@ -53,6 +56,7 @@ def parse():
     ap.add_argument("--n", type=int, default=N_MESH)
     ap.add_argument("--no-reorder", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=2.5)
+    ap.add_argument("--dist", action="store_true", help="use the partitioned (NCCL) path even at world size 1")
     return ap.parse_args()
 
 
@@ -201,25 +205,52 @@ def gpu_bench(args, rank, world):
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
     cfg = op.OperatorConfig(device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    # weak scaling: each rank keeps ~n^3 x 6 cells (global mesh grows with the world size)
+    n_glob = args.n if world == 1 else int(round(args.n * world ** (1.0 / 3.0)))
     problems = []
     for reorder in variants(args):
         for p in DEGREES:
-            m, dm, geo, bas = build_problem(args.n, p, reorder)
-            A = op.CgPoissonOperator(m, dm, geo, bas, cfg)
-            u_host = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
-            u = torch.from_numpy(u_host).cuda()
+            m, dm, geo, bas = build_problem(n_glob, p, reorder)
+            u_glob = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
+            if world == 1 and not args.dist:
+                A = op.CgPoissonOperator(m, dm, geo, bas, cfg)
+                ids = None
+                local = A
+            else:
+                from paper_2509_10226_b200.distributed import DistributedCgOperator
+
+                A = DistributedCgOperator(m, dm, geo, bas, rank, world)
+                ids = A.owned_global_ids
+                local = A.local_op
+            u_host = u_glob if ids is None else u_glob[ids]
+            u = torch.from_numpy(np.ascontiguousarray(u_host)).cuda()
             y = torch.empty_like(u)
-            u_pin = torch.from_numpy(u_host).pin_memory()
+            u_pin = torch.from_numpy(np.ascontiguousarray(u_host)).pin_memory()
             y_pin = torch.empty_like(u_pin).pin_memory()
-            problems.append(dict(p=p, reorder=reorder, A=A, u=u, y=y, u_pin=u_pin, y_pin=y_pin,
-                                 ndof=dm.n_global_dofs))
+            problems.append(dict(p=p, reorder=reorder, A=A, local=local, u=u, y=y, u_pin=u_pin, y_pin=y_pin,
+                                 ndof=len(u_host), ndof_global=dm.n_global_dofs))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    st = torch.cuda.current_stream().cuda_stream
+
+    def timed_apply(pr):
+        """(total, cell-kernel) ms of one apply, CUDA events on the launch stream."""
+        if world == 1 and not args.dist:
+            ms = pr["A"].timed(pr["u"].data_ptr(), pr["y"].data_ptr(), st, 1)
+            return float(ms[0]), float(ms[1])
+        A = pr["A"]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        A.kernel_events = []
+        e0.record()
+        A.apply(pr["u"], out=pr["y"])
+        e1.record()
+        e1.synchronize()
+        k0, k1 = A.kernel_events[0]
+        return e0.elapsed_time(e1), k0.elapsed_time(k1)
 
     def step(record):
         for pr in problems:
             flush.fill_(1.0)
-            ms = pr["A"].timed(pr["u"].data_ptr(), pr["y"].data_ptr(), st, 1)
+            ms = timed_apply(pr)
             if record is not None:
                 record.append((pr, ms))
 
@@ -238,12 +269,17 @@ def gpu_bench(args, rank, world):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     total_ms = sum(ms[0] for _, ms in rec)
-    dofs = sum(pr["ndof"] for pr, _ in rec)
+    dofs = sum(pr["ndof"] for pr, _ in rec)   # owned DoFs of this rank
 
     # e2e through the public API with host (pinned) buffers
     def e2e_step():
         for pr in problems:
-            pr["A"].apply(pr["u_pin"].numpy(), out=pr["y_pin"].numpy())
+            if world == 1 and not args.dist:
+                pr["A"].apply(pr["u_pin"].numpy(), out=pr["y_pin"].numpy())
+            else:   # host -> device, partitioned apply (NCCL halo), device -> host
+                u = pr["u_pin"].cuda(non_blocking=True)
+                pr["y_pin"].copy_(pr["A"].apply(u), non_blocking=True)
+                torch.cuda.synchronize()
     e2e_step()
     if world > 1:
         torch.distributed.barrier()
@@ -262,7 +298,7 @@ def gpu_bench(args, rank, world):
         ms = np.array([m for q, m in rec if q is pr])
         t = ms[:, 0].mean()
         tc = ms[:, 1].mean()
-        info = pr["A"].info
+        info = pr["local"].info
         per[key] = {"ndof": pr["ndof"], "ms": round(float(t), 4), "gdofs": round(pr["ndof"] / t / 1e6, 3),
                     "cell_kernel_ms": round(float(tc), 4),
                     "tflops_alg": round(info["flops_alg"] / tc / 1e9, 2),
@@ -271,7 +307,7 @@ def gpu_bench(args, rank, world):
     dom = max(problems, key=lambda q: per[f"p{q['p']}{'_reordered' if q['reorder'] else ''}"]["cell_kernel_ms"])
     dk = f"p{dom['p']}{'_reordered' if dom['reorder'] else ''}"
     tc = per[dk]["cell_kernel_ms"]
-    achieved = dom["A"].info["flops_alg"] / tc / 1e9
+    achieved = dom["local"].info["flops_alg"] / tc / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
@@ -279,8 +315,9 @@ def gpu_bench(args, rank, world):
             traffic = json.load(open(prof)).get("cell_kernel_p4", {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    n_kern = sum(pr["A"].info["kernels_per_apply"] for pr in problems) * args.steps
-    return dict(total_ms=total_ms, dofs=dofs, e2e_s=e2e_s, per=per, clocks=clk.summary(),
+    n_kern = sum(pr["local"].info["kernels_per_apply"] for pr in problems) * args.steps
+    dofs_global = sum(pr["ndof_global"] for pr, _ in rec)
+    return dict(total_ms=total_ms, dofs=dofs, dofs_global=dofs_global, n_glob=n_glob, e2e_s=e2e_s, per=per, clocks=clk.summary(),
                 roofline={"bound": "tensor", "kernel": f"cell_apply_kernel ({dk})", "achieved": round(achieved, 3),
                           "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE, "unit": "TFLOP/s",
                           "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
@@ -311,10 +348,14 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
-    if world > 1:
+    if world > 1 or args.dist:
+        import torch
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl", rank=rank, world_size=world)
     r = gpu_bench(args, rank, world)
     total_ms = r["total_ms"]
     if world > 1:
@@ -326,8 +367,8 @@ def main():
         total_ms, e2e_s = float(t[0]), float(t[1])
     else:
         e2e_s = r["e2e_s"]
-    value = r["dofs"] * world / (total_ms * 1e-3) / 1e9
-    e2e_val = r["dofs"] * world / e2e_s / 1e9
+    value = r["dofs_global"] / (total_ms * 1e-3) / 1e9
+    e2e_val = r["dofs_global"] / e2e_s / 1e9
     cpu = None
     if rank == 0 and world == 1:
         try:
@@ -342,13 +383,15 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload, "l2": "flushed (256 MiB write) before every apply",
-                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                           "global_mesh": f"{r['n_glob']}^3 x 6",
+                           "parallelism": (f"{world}-way RCB domain decomposition, NCCL halo (weak scaling: "
+                                           f"~{args.n}^3 x 6 cells per GPU)") if world > 1 else "single GPU"},
                 "per_degree": r["per"], "roofline": r["roofline"], "cpu_baseline": cpu,
                 "e2e": {"value": round(e2e_val, 4), "unit": unit, "h2d_bytes_per_step": r["h2d"],
                         "d2h_bytes_per_step": r["d2h"], "path": "Operator.apply(numpy, pinned) -> tmf_apply_host"},
                 "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "parity_e2e_vs_timed_rel_l2": r["parity_rel_l2"]}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
 
         dist.destroy_process_group()

@@ -325,11 +325,25 @@ class DistributedCgOperator:
     def owned_global_ids(self) -> np.ndarray:
         return self.sub.l2g[: self.sub.n_owned]
 
+    kernel_events = None   # set to a list to record (start, end) CUDA events of the local apply
+
+    def _timed_local(self):
+        if self.kernel_events is None:
+            self._local(self.u_loc, self.y_loc)
+            return
+        import torch
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        self._local(self.u_loc, self.y_loc)
+        e1.record()
+        self.kernel_events.append((e0, e1))
+
     def apply(self, u_owned, out=None):
         n = self.sub.n_owned
         self.u_loc[:n].copy_(u_owned)
         self.fwd.forward(self.u_loc)
-        self._local(self.u_loc, self.y_loc)
+        self._timed_local()
         self.rev.reverse_add(self.y_loc)
         if out is None:
             return self.y_loc[:n].clone()
