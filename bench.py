@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--n", type=int, default=N_MESH)
     ap.add_argument("--no-reorder", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=2.5)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (e.g. under ncu)")
     ap.add_argument("--dist", action="store_true", help="use the partitioned (NCCL) path even at world size 1")
     return ap.parse_args()
 
@@ -370,7 +371,7 @@ def main():
     value = r["dofs_global"] / (total_ms * 1e-3) / 1e9
     e2e_val = r["dofs_global"] / e2e_s / 1e9
     cpu = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.no_cpu:
         try:
             v, cores, detail = cpu_reference(args, min(args.cpu_sample_s, 1.5))
             cpu = {"value": v, "unit": unit, "cores": cores, "kind": "port",

@@ -115,6 +115,32 @@ __global__ void dfma_smem(double* out, int iters) {
   if (blockIdx.x == 0 && threadIdx.x == 0) { g_clk[0] = c1 - c0; g_clk[1] = t1 - t0; }
 }
 
+// DMMA and DFMA issued together: are the tensor FP64 pipe and the vector FP64
+// pipe independent?  RATIO DFMA per DMMA per warp.
+template <int RATIO>
+__global__ void mix_kernel(double* out, int iters, double a, double b) {
+  double acc[8][2];
+  double f[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) { acc[c][0] = c; acc[c][1] = -c; f[c] = threadIdx.x * 1e-3 + c; }
+  double av = a + threadIdx.x * 1e-9, bv = b - threadIdx.x * 1e-9;
+  uint64_t c0 = clock64(), t0 = gtimer();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      dmma(acc[c], av, bv);
+#pragma unroll
+      for (int r = 0; r < RATIO; ++r) f[(c + r) & 7] = fma(f[(c + r) & 7], a, b);
+    }
+  }
+  uint64_t c1 = clock64(), t1 = gtimer();
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c][0] + acc[c][1] + f[c];
+  if (s == 1234.5678) out[threadIdx.x] = s;  // keeps the chains live
+  if (blockIdx.x == 0 && threadIdx.x == 0) { g_clk[0] = c1 - c0; g_clk[1] = t1 - t0; }
+}
+
 template <typename F>
 static int timeit(const char* name, F launch, double fma_per_launch, int n_sm) {
   cudaEvent_t e0, e1;
@@ -167,6 +193,18 @@ int main() {
     char nm[64]; snprintf(nm, 64, "dfma_const_%dblk", bps);
     timeit(nm, [&] { dfma_const<<<blocks, threads>>>(out, iters); },
            (double)blocks * threads * NCONST, n_sm);
+  }
+  {
+    int blocks = n_sm * 4; int iters = 1024;
+    // FMA counted: DMMA 256 per warp-instr; DFMA 32 per warp-instr
+    timeit("mix_dmma_only(ratio0)", [&] { mix_kernel<0><<<blocks, threads>>>(out, iters, 1.0000001, 1e-9); },
+           (double)blocks * (threads / 32) * iters * 8 * 256, n_sm);
+    timeit("mix_ratio2_dmma_fma_only", [&] { mix_kernel<2><<<blocks, threads>>>(out, iters, 1.0000001, 1e-9); },
+           (double)blocks * (threads / 32) * iters * 8 * 256, n_sm);
+    timeit("mix_ratio4_dmma_fma_only", [&] { mix_kernel<4><<<blocks, threads>>>(out, iters, 1.0000001, 1e-9); },
+           (double)blocks * (threads / 32) * iters * 8 * 256, n_sm);
+    timeit("mix_ratio8_dmma_fma_only", [&] { mix_kernel<8><<<blocks, threads>>>(out, iters, 1.0000001, 1e-9); },
+           (double)blocks * (threads / 32) * iters * 8 * 256, n_sm);
   }
   for (int bps : {4, 8}) {
     int blocks = n_sm * bps; int iters = 64;
