@@ -78,7 +78,7 @@ typedef struct tmf_plan_desc {
   double mass_scale;           /* Helmholtz mass coefficient                          */
   double diffusivity;          /* Laplace/SIPG scale (nu)                             */
   int32_t device;              /* CUDA device ordinal                                 */
-  int32_t flags;               /* reserved, 0                                         */
+  int32_t flags;               /* bits 0-3: kernel tuning variant (0 = default)       */
 } tmf_plan_desc;
 
 typedef struct tmf_plan_info {

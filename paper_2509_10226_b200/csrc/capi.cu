@@ -93,6 +93,7 @@ void build_face_fragments(int N, int Q, F E, const double* w, std::vector<double
 struct tmf_plan {
   int dev = 0, n_sm = 0;
   int kind = 0, degree = 0, N = 0, Q = 0, QF = 0, nc = 1;
+  int variant = 0;  // desc.flags & 0xF: kernel tuning variant (0 = default)
   bool dg = false, mass = false, faces = false;
   int64_t n_cells = 0, n_verts = 0, n_scalar = 0, n_global = 0;
   double mass_scale = 0.0, stiff_scale = 1.0;
@@ -292,7 +293,8 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
   bool ok = true;
   if (ev) TMF_CUDA(cudaEventRecord(ev[0], st));
   if (!P->dg) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
-  TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y), P->n_sm, st, nullptr, &ok));
+  TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y), P->n_sm, st, nullptr, &ok,
+                            P->variant));
   if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
   if (P->faces) {
     TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok));
@@ -358,6 +360,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     P->n_sm = sms;
   }
   P->kind = d->operator_kind;
+  P->variant = d->flags & 0xF;
   P->degree = d->degree;
   P->N = d->n_dofs_per_cell;
   P->Q = d->n_q;
@@ -402,7 +405,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     tmf::CellArgs dummy{};
     dummy.n_cells = P->n_cells;
     dummy.nc = P->nc;
-    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok));
+    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok, P->variant));
     if (!ok) return bail(fail(TMF_EINVAL, "unsupported (n_dofs_per_cell, n_q) = (" +
                                               std::to_string(N) + ", " + std::to_string(Q) + ")"));
     if ((int)fr.size() != ci.frag_doubles) return bail(fail(TMF_EINVAL, "internal: fragment size"));

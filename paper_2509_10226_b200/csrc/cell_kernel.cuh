@@ -93,10 +93,12 @@ struct CellShape {
   static constexpr int MT = (KK + 2 * NJ) <= 7 ? 2 : 1;
 };
 
-template <int N, int Q, bool MASS, bool DG, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) cell_apply_kernel(CellArgs a) {
+// MT_: tiles per warp iteration (0 = CellShape default); MINB: min CTAs/SM hint;
+// PF: software-prefetch the next super-tile's gathered u and geometry (indices 2 ahead)
+template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT_ = 0, int MINB = 1, bool PF = false>
+__global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   using S = CellShape<N, Q, MASS>;
-  constexpr int MT = S::MT;
+  constexpr int MT = MT_ ? MT_ : S::MT;
   extern __shared__ __align__(16) double smem[];
   {
     const double2* src = reinterpret_cast<const double2*>(a.frags);
@@ -134,7 +136,31 @@ __global__ void __launch_bounds__(BLOCK) cell_apply_kernel(CellArgs a) {
       }
     }
   };
+  // gathered u (A fragments) and geometry of one super-tile, from the indices in nidx
+  auto load_data = [&](int64_t t, double (&av)[MT][S::KK], double (&G)[MT][6], double (&mdet)[MT]) {
+    const int cmp = (int)(t / cst);
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const int64_t c = ((t - (int64_t)cmp * cst) * MT + m) * 8 + cs;
+      const bool ok = t < nst && c < a.n_cells;
+#pragma unroll
+      for (int kk = 0; kk < S::KK; ++kk) {
+        const int g = nidx[m][kk];
+        av[m][kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + cmp) : 0.0;
+      }
+      const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * (ok ? c : 0));
+      const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
+      G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
+      G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
+      mdet[m] = MASS ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
+    }
+  };
   load_indices(st);
+  double pav[MT][S::KK], pG[MT][6], pmdet[MT];
+  if (PF) {
+    load_data(st, pav, pG, pmdet);
+    load_indices(st + nwarps);
+  }
 
   for (; st < nst; st += nwarps) {
     const int comp = (int)(st / cst);
@@ -147,20 +173,22 @@ __global__ void __launch_bounds__(BLOCK) cell_apply_kernel(CellArgs a) {
     for (int m = 0; m < MT; ++m) {
       cell[m] = ((st - (int64_t)comp * cst) * MT + m) * 8 + cs;
       valid[m] = cell[m] < a.n_cells;
-      // ---- gather: A fragments of GEMM1 (lane owns DoFs 4kk + q4 of its cell)
-#pragma unroll
-      for (int kk = 0; kk < S::KK; ++kk) {
-        const int g = nidx[m][kk];
-        av[m][kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + comp) : 0.0;
-      }
-      // ---- geometry (precomputed per plan)
-      const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * (valid[m] ? cell[m] : 0));
-      const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
-      G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
-      G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
-      mdet[m] = MASS ? __ldg(a.cgeo + 8 * (valid[m] ? cell[m] : 0) + 6) : 0.0;
     }
-    load_indices(st + nwarps);
+    if (PF) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+#pragma unroll
+        for (int kk = 0; kk < S::KK; ++kk) av[m][kk] = pav[m][kk];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) G[m][i] = pG[m][i];
+        mdet[m] = pmdet[m];
+      }
+      load_data(st + nwarps, pav, pG, pmdet);
+      load_indices(st + 2 * nwarps);
+    } else {
+      load_data(st, av, G, mdet);
+      load_indices(st + nwarps);
+    }
 
     double yacc[MT][S::NJ][2];
 #pragma unroll

@@ -9,11 +9,11 @@
 
 namespace tmf {
 
-template <int N, int Q, bool MASS, bool DG>
-static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
+template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PF = false>
+static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = CellShape<N, Q, MASS>;
-  constexpr int BLOCK = S::SMEM > 96 * 1024 ? 512 : 256;
-  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK>;
+  constexpr int MTE = MT ? MT : S::MT;
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF>;
   static int configured = 0;  // per instantiation, per process
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
@@ -24,15 +24,14 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const int64_t tiles = ((a.n_cells + 7) / 8) * a.nc;
-  const int64_t supertiles = ((a.n_cells + 8 * S::MT - 1) / (8 * S::MT)) * a.nc;
+  const int64_t supertiles = ((a.n_cells + 8 * MTE - 1) / (8 * MTE)) * a.nc;
   int64_t blocks = (int64_t)n_sm * per_sm;
   const int64_t need = (supertiles + BLOCK / 32 - 1) / (BLOCK / 32);
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   if (info) {
     info->dmma_per_tile = S::DMMA_PER_TILE;
-    info->tiles = supertiles * S::MT;
+    info->tiles = supertiles * MTE;
     info->block = BLOCK;
     info->grid = (int)blocks;
     info->smem = S::SMEM;
@@ -43,19 +42,35 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   return cudaGetLastError();
 }
 
+// variant: 0 = default; 1..3 = tuning variants of the CG kernel (bench sweeps only)
+template <int N, int Q, bool MASS, bool DG>
+static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info,
+                                 int variant) {
+  using S = CellShape<N, Q, MASS>;
+  constexpr int BLOCK = S::SMEM > 96 * 1024 ? 512 : 256;
+  if (!DG && !MASS) {
+    if (variant == 1) return launch_cell_v<N, Q, MASS, DG, BLOCK, 2, 1>(a, n_sm, st, info);
+    if (variant == 2) return launch_cell_v<N, Q, MASS, DG, BLOCK, 1, (BLOCK == 256 ? 3 : 1)>(a, n_sm, st, info);
+    if (variant == 3) return launch_cell_v<N, Q, MASS, DG, 128, 1, 4>(a, n_sm, st, info);
+    if (variant == 4) return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, true>(a, n_sm, st, info);
+    if (variant == 5) return launch_cell_v<N, Q, MASS, DG, BLOCK, 1, 1, true>(a, n_sm, st, info);
+  }
+  return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1>(a, n_sm, st, info);
+}
+
 template <int N, int Q>
 static cudaError_t cell_variant(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                                CellLaunchInfo* info) {
-  if (!dg) return launch_cell_t<N, Q, false, false>(a, n_sm, st, info);
-  if (mass) return launch_cell_t<N, Q, true, true>(a, n_sm, st, info);
-  return launch_cell_t<N, Q, false, true>(a, n_sm, st, info);
+                                CellLaunchInfo* info, int variant) {
+  if (!dg) return launch_cell_t<N, Q, false, false>(a, n_sm, st, info, variant);
+  if (mass) return launch_cell_t<N, Q, true, true>(a, n_sm, st, info, variant);
+  return launch_cell_t<N, Q, false, true>(a, n_sm, st, info, variant);
 }
 
 cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& a, int n_sm,
-                        cudaStream_t st, CellLaunchInfo* info, bool* supported) {
+                        cudaStream_t st, CellLaunchInfo* info, bool* supported, int variant) {
   *supported = true;
 #define TMF_CELL(NN, QQ) \
-  if (n_dpc == NN && n_q == QQ) return cell_variant<NN, QQ>(mass, dg, a, n_sm, st, info);
+  if (n_dpc == NN && n_q == QQ) return cell_variant<NN, QQ>(mass, dg, a, n_sm, st, info, variant);
   TMF_CELL(4, 4)
   TMF_CELL(4, 5)
   TMF_CELL(10, 14)

@@ -28,7 +28,7 @@ struct FaceLaunchInfo {
 
 // info != nullptr: only fill the launch description (no launch).
 cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& a, int n_sm,
-                        cudaStream_t st, CellLaunchInfo* info, bool* supported);
+                        cudaStream_t st, CellLaunchInfo* info, bool* supported, int variant = 0);
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
                         cudaStream_t st, FaceLaunchInfo* info, bool* supported);
 cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st);

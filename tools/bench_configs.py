@@ -1,0 +1,156 @@
+"""Measure every BASELINE.json config on one GPU (developer tool; bench.py is the contract).
+
+    python tools/bench_configs.py [c1 c2 c3 c4 c5] [--n4 128] [--n5 128]
+
+Prints one JSON line per config: GDoF/s (fp64), per-kernel CUDA-event times, the
+roofline fraction against the measured FP64 DMMA peak, and for C1 the parity vs
+the CPU oracle.  Reordering (hierarchical) is applied as setup for C3-C5.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+PEAK = 37.1
+
+
+def setup(n, p, space, reorder, dids=()):
+    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+
+    t = time.time()
+    m = M.kuhn_cube_mesh(n, seed=0)
+    if reorder:
+        from paper_2509_10226_b200.reorder import hierarchical_reorder
+
+        m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    dm = D.build_dof_map(m, p, space, 1, dids)
+    geo = GeometryData("affine", cr, fr, None, None, None, None)
+    return m, dm, geo, bas, time.time() - t
+
+
+def timed(A, nd, reps=10):
+    import torch
+
+    u = torch.rand(nd, dtype=torch.float64, device="cuda") * 2 - 1
+    y = torch.empty_like(u)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    A.timed(u.data_ptr(), y.data_ptr(), st, 3)
+    acc = np.zeros(4)
+    for _ in range(reps):
+        flush.fill_(1.0)
+        acc += A.timed(u.data_ptr(), y.data_ptr(), st, 1)
+    return acc / reps
+
+
+def line(name, A, nd, ms, extra=None):
+    info = A.info
+    d = {"config": name, "ndof": nd, "ms": round(float(ms[0]), 4), "cell_ms": round(float(ms[1]), 4),
+         "face_ms": round(float(ms[2]), 4), "gdofs": round(nd / ms[0] / 1e6, 3),
+         "tflops_alg": round(info["flops_alg"] / ms[0] / 1e9, 2),
+         "frac_fp64_roofline": round(info["flops_alg"] / ms[0] / 1e9 / PEAK, 3),
+         "flops_alg_per_dof": round(info["flops_alg"] / nd, 1), "bytes_alg_per_dof": round(info["bytes_alg"] / nd, 1),
+         "issued_over_alg": round(info["flops_issued"] / info["flops_alg"], 3)}
+    if extra:
+        d.update(extra)
+    print(json.dumps(d), flush=True)
+
+
+def c1():
+    from oracle import ref_apply
+    from paper_2509_10226_b200 import operator as op
+
+    m, dm, geo, bas, ts = setup(8, 2, "cg", False)
+    A = op.CgPoissonOperator(m, dm, geo, bas)
+    u = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
+    y = A.apply(u)
+    yr = ref_apply.cg_apply(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask, bas.grad_matrix,
+                            geo.cell_rule.weights, u)
+    ms = timed(A, dm.n_global_dofs, 50)
+    line("C1 CG P2 8^3x6", A, dm.n_global_dofs, ms,
+         {"rel_l2_vs_oracle": float(np.linalg.norm(y - yr) / np.linalg.norm(yr)), "setup_s": round(ts, 1)})
+
+
+def c2():
+    from paper_2509_10226_b200 import operator as op
+
+    for reorder in (False, True):
+        for p in (1, 2, 3, 4):
+            m, dm, geo, bas, ts = setup(48, p, "cg", reorder)
+            A = op.CgPoissonOperator(m, dm, geo, bas)
+            ms = timed(A, dm.n_global_dofs)
+            line(f"C2 CG P{p} 48^3x6{' reordered' if reorder else ''}", A, dm.n_global_dofs, ms,
+                 {"setup_s": round(ts, 1)})
+
+
+def c3(n=64):
+    from paper_2509_10226_b200 import operator as op
+
+    for reorder in (False, True):
+        m, dm, geo, bas, ts = setup(n, 3, "dg", reorder)
+        A = op.DgSipgOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, 3, 1.0 / n), dirichlet_ids=range(6))
+        ms = timed(A, dm.n_global_dofs)
+        line(f"C3 DG-SIPG P3 {n}^3x6{' reordered' if reorder else ''}", A, dm.n_global_dofs, ms,
+             {"setup_s": round(ts, 1)})
+
+
+def c4(n=128):
+    from paper_2509_10226_b200 import operator as op
+
+    m, dm, geo, bas, ts = setup(n, 2, "dg", True)
+    kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
+    A = op.KappaHelmholtzOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, 2, 1.0 / n), kap, 1.0,
+                                  dirichlet_ids=range(6))
+    ms = timed(A, dm.n_global_dofs, 5)
+    line(f"C4 DG Helmholtz (mass + kappa-Laplace) P2 {n}^3x6 reordered, 1 GPU", A, dm.n_global_dofs, ms,
+         {"setup_s": round(ts, 1)})
+
+
+def c5(n=128, iters=100):
+    import torch
+
+    from paper_2509_10226_b200 import operator as op
+    from paper_2509_10226_b200.solvers import jacobi_pcg
+
+    m, dm, geo, bas, ts = setup(n, 3, "cg", True, tuple(range(6)))
+    A = op.CgPoissonOperator(m, dm, geo, bas)
+    b = np.where(dm.dirichlet_mask, 0.0, np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs))
+    bt = torch.from_numpy(b).cuda()
+    jacobi_pcg(A, bt, 3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, hist = jacobi_pcg(A, bt, iters)
+    e1.record()
+    e1.synchronize()
+    t = e0.elapsed_time(e1)
+    ms = timed(A, dm.n_global_dofs, 5)
+    nd = dm.n_global_dofs
+    print(json.dumps({"config": f"C5 Jacobi-PCG CG P3 {n}^3x6 reordered, {iters} iterations, 1 GPU", "ndof": nd,
+                      "solve_ms": round(t, 2), "ms_per_iteration": round(t / iters, 4),
+                      "apply_ms": round(float(ms[0]), 4),
+                      "apply_gdofs": round(nd / ms[0] / 1e6, 3),
+                      "solver_gdofs_per_iteration": round(nd * iters / t / 1e6, 3),
+                      "apply_frac_fp64_roofline": round(A.info["flops_alg"] / ms[0] / 1e9 / PEAK, 3),
+                      "residual_first_last": [float(hist[0]), float(hist[-1])], "setup_s": round(ts, 1)}),
+          flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--n3", type=int, default=64)
+    ap.add_argument("--n4", type=int, default=128)
+    ap.add_argument("--n5", type=int, default=128)
+    a = ap.parse_args()
+    for c in a.configs:
+        {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5)}[c]()

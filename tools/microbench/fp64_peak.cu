@@ -141,6 +141,26 @@ __global__ void mix_kernel(double* out, int iters, double a, double b) {
   if (blockIdx.x == 0 && threadIdx.x == 0) { g_clk[0] = c1 - c0; g_clk[1] = t1 - t0; }
 }
 
+// DMMA dependent-chain latency: one warp per SMSP, CH independent chains.
+template <int CH>
+__global__ void dmma_chain(double* out, int iters, double a, double b) {
+  double acc[CH][2];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) { acc[c][0] = c; acc[c][1] = -c; }
+  double av = a + threadIdx.x * 1e-9, bv = b - threadIdx.x * 1e-9;
+  uint64_t c0 = clock64(), t0 = gtimer();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) dmma(acc[c], av, bv);
+  }
+  uint64_t c1 = clock64(), t1 = gtimer();
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 1234.5678) out[threadIdx.x] = s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { g_clk[0] = c1 - c0; g_clk[1] = t1 - t0; }
+}
+
 template <typename F>
 static int timeit(const char* name, F launch, double fma_per_launch, int n_sm) {
   cudaEvent_t e0, e1;
@@ -205,6 +225,22 @@ int main() {
            (double)blocks * (threads / 32) * iters * 8 * 256, n_sm);
     timeit("mix_ratio8_dmma_fma_only", [&] { mix_kernel<8><<<blocks, threads>>>(out, iters, 1.0000001, 1e-9); },
            (double)blocks * (threads / 32) * iters * 8 * 256, n_sm);
+  }
+  {
+    // 1 block of 128 threads (one warp per SMSP) per SM; cycles per DMMA per warp = latency / CH
+    int blocks = n_sm; int iters = 4096;
+    auto run = [&](const char* nm, auto kern, int ch) {
+      timeit(nm, [&] { kern<<<blocks, 128>>>(out, iters, 1.0000001, 1e-9); },
+             (double)blocks * 4 * iters * ch * 256, n_sm);
+      unsigned long long clk[2];
+      cudaMemcpyFromSymbol(clk, g_clk, sizeof(clk));
+      printf("{\"kernel\": \"%s_cycles_per_dmma_per_warp\", \"value\": %.2f}\n", nm, (double)clk[0] / (iters * ch));
+    };
+    run("chain1", dmma_chain<1>, 1);
+    run("chain2", dmma_chain<2>, 2);
+    run("chain3", dmma_chain<3>, 3);
+    run("chain4", dmma_chain<4>, 4);
+    run("chain8", dmma_chain<8>, 8);
   }
   for (int bps : {4, 8}) {
     int blocks = n_sm * bps; int iters = 64;
