@@ -78,7 +78,7 @@ typedef struct tmf_plan_desc {
   double mass_scale;           /* Helmholtz mass coefficient                          */
   double diffusivity;          /* Laplace/SIPG scale (nu)                             */
   int32_t device;              /* CUDA device ordinal                                 */
-  int32_t flags;               /* bits 0-3: kernel tuning variant (0 = default)       */
+  int32_t flags;               /* bits 0-3 / 4-7: cell / face kernel tuning variant    */
 } tmf_plan_desc;
 
 typedef struct tmf_plan_info {

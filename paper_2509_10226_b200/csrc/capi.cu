@@ -93,7 +93,8 @@ void build_face_fragments(int N, int Q, F E, const double* w, std::vector<double
 struct tmf_plan {
   int dev = 0, n_sm = 0;
   int kind = 0, degree = 0, N = 0, Q = 0, QF = 0, nc = 1;
-  int variant = 0;  // desc.flags & 0xF: kernel tuning variant (0 = default)
+  int variant = 0;       // desc.flags & 0xF: cell-kernel tuning variant (0 = default)
+  int face_variant = 0;  // (desc.flags >> 4) & 0xF: face-kernel tuning variant
   bool dg = false, mass = false, faces = false;
   int64_t n_cells = 0, n_verts = 0, n_scalar = 0, n_global = 0;
   double mass_scale = 0.0, stiff_scale = 1.0;
@@ -297,8 +298,10 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
                             P->variant));
   if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
   if (P->faces) {
-    TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok));
-    TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok));
+    TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
+                              P->face_variant));
+    TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
+                              P->face_variant));
   }
   if (ev) TMF_CUDA(cudaEventRecord(ev[2], st));
   if (!P->dg && P->n_fix) TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st));
@@ -361,6 +364,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   }
   P->kind = d->operator_kind;
   P->variant = d->flags & 0xF;
+  P->face_variant = (d->flags >> 4) & 0xF;
   P->degree = d->degree;
   P->N = d->n_dofs_per_cell;
   P->Q = d->n_q;

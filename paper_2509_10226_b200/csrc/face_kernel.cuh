@@ -153,8 +153,9 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
   }
 }
 
-template <int N, int QF, bool BOUNDARY>
-__global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
+// PF: software-prefetch the next batch (record, geometry, gathered u); MINB: CTAs/SM hint
+template <int N, int QF, bool BOUNDARY, bool PF = true, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
@@ -210,9 +211,10 @@ __global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
         }
       }
     };
-    fetch(warp);
+    if (PF) fetch(warp);
 
     for (int bi = warp; bi < ch.w; bi += nwb) {
+      if (!PF) fetch(bi);
       const int c_m = n_cm, c_p = n_cp;
       double am[S::KK], ap[S::KK];
 #pragma unroll
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(256, 2) face_apply_kernel(FaceArgs a) {
       const double mm[3] = {ng[0], ng[1], ng[2]};
       const double mp[3] = {ng[3], ng[4], ng[5]};
       const double s = ng[6], tau = ng[7];
-      fetch(bi + nwb);
+      if (PF) fetch(bi + nwb);
 
       double ym[S::NJ][2], yp[S::NJ][2];
 #pragma unroll

@@ -82,11 +82,11 @@ cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& 
   return cudaSuccess;
 }
 
-template <int N, int QF, bool BND>
-static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
+template <int N, int QF, bool BND, bool PF = true, int MINB = 2>
+static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShape<N, QF>;
   constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
-  auto kern = face_apply_kernel<N, QF, BND>;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB>;
   static int configured = 0;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -111,13 +111,28 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   return cudaGetLastError();
 }
 
+// variant: 0 = default (by degree, below); 1 = no prefetch, 3 CTAs/SM;
+// 2 = no prefetch, 2 CTAs/SM; 3 = prefetch, 1 CTA/SM; 4 = prefetch, 2 CTAs/SM
+template <int N, int QF, bool BND>
+static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info,
+                                 int variant) {
+  if (variant == 1) return launch_face_v<N, QF, BND, false, 3>(a, n_sm, st, info);
+  if (variant == 2) return launch_face_v<N, QF, BND, false, 2>(a, n_sm, st, info);
+  if (variant == 3) return launch_face_v<N, QF, BND, true, 1>(a, n_sm, st, info);
+  if (variant == 4) return launch_face_v<N, QF, BND, true, 2>(a, n_sm, st, info);
+  // default: low degrees have short batches -> occupancy beats prefetch depth (measured
+  // at P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the prefetching 2-CTA kernel
+  if (N <= 10) return launch_face_v<N, QF, BND, false, 3>(a, n_sm, st, info);
+  return launch_face_v<N, QF, BND, true, 2>(a, n_sm, st, info);
+}
+
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
-                        cudaStream_t st, FaceLaunchInfo* info, bool* supported) {
+                        cudaStream_t st, FaceLaunchInfo* info, bool* supported, int variant) {
   *supported = true;
 #define TMF_FACE(NN, QQ)                                                          \
   if (n_dpc == NN && n_qf == QQ) {                                                \
-    if (boundary) return launch_face_t<NN, QQ, true>(a, n_sm, st, info);          \
-    return launch_face_t<NN, QQ, false>(a, n_sm, st, info);                       \
+    if (boundary) return launch_face_t<NN, QQ, true>(a, n_sm, st, info, variant); \
+    return launch_face_t<NN, QQ, false>(a, n_sm, st, info, variant);              \
   }
   TMF_FACE(4, 3)
   TMF_FACE(4, 4)

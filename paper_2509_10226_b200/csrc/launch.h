@@ -30,7 +30,7 @@ struct FaceLaunchInfo {
 cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& a, int n_sm,
                         cudaStream_t st, CellLaunchInfo* info, bool* supported, int variant = 0);
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
-                        cudaStream_t st, FaceLaunchInfo* info, bool* supported);
+                        cudaStream_t st, FaceLaunchInfo* info, bool* supported, int variant = 0);
 cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,

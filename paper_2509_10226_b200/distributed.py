@@ -103,97 +103,95 @@ def _local_mesh(mesh: TetMesh, cells_g: np.ndarray) -> tuple[TetMesh, np.ndarray
     return TetMesh(mesh.vertices[verts_g], cells_l, ifc, bfc), verts_g
 
 
+def _touch_masks(cell_dofs: np.ndarray, part: np.ndarray, n_dofs: int, k: int) -> np.ndarray:
+    """Bit r of mask[d] is set iff a cell of rank r touches DoF d (k <= 64)."""
+    dt = np.uint8 if k <= 8 else (np.uint16 if k <= 16 else np.uint64)
+    mask = np.zeros(n_dofs, dtype=dt)
+    for r in range(k):
+        mask[cell_dofs[part == r].ravel()] |= dt(1 << r)
+    return mask
+
+
+def _lowest_bit(mask: np.ndarray, k: int) -> np.ndarray:
+    owner = np.full(len(mask), k, dtype=np.int64)
+    for r in range(k - 1, -1, -1):
+        owner[(mask >> r) & 1 == 1] = r
+    return owner
+
+
 def build_cg_subdomain(mesh: TetMesh, cell_dofs: np.ndarray, dirichlet_mask: np.ndarray,
                        part: np.ndarray, rank: int, k: int) -> CgSubdomain:
+    """O(n) vectorised: touch bitmasks per DoF give owners (lowest touching rank),
+    the rank's local numbering and every peer list."""
     nd = cell_dofs.shape[1]
     n_dofs = len(dirichlet_mask)
-    owner = np.full(n_dofs, k, dtype=np.int64)
-    np.minimum.at(owner, cell_dofs.ravel().astype(np.int64), np.repeat(part, nd))
-    touched = []                                           # DoFs touched by each rank
-    for r in range(k):
-        touched.append(np.unique(cell_dofs[part == r]))
-    l2g_all = []
-    for r in range(k):
-        d = touched[r]
-        own = d[owner[d] == r]
-        gh = d[owner[d] != r]
-        gh = gh[np.lexsort((gh, owner[gh]))]
-        l2g_all.append(np.concatenate([own, gh]))
-
-    def g2l(r, g):
-        l2g = l2g_all[r]
-        n_own = int(np.sum(owner[l2g] == r))
-        own = l2g[:n_own]
-        pos = np.searchsorted(own, g)
-        out = np.empty(len(g), dtype=np.int64)
-        hit = (pos < n_own) & (own[np.minimum(pos, n_own - 1)] == g) if n_own else np.zeros(len(g), bool)
-        out[hit] = pos[hit]
-        if np.any(~hit):
-            gh = l2g[n_own:]
-            idx = {int(v): i for i, v in enumerate(gh)}
-            out[~hit] = [n_own + idx[int(v)] for v in g[~hit]]
-        return out
-
+    mask = _touch_masks(cell_dofs, part, n_dofs, k)
+    owner = _lowest_bit(mask, k)
+    mine = ((mask >> rank) & 1).astype(bool)
+    own = np.flatnonzero(mine & (owner == rank))
+    gh = np.flatnonzero(mine & (owner != rank))
+    gh = gh[np.argsort(owner[gh], kind="stable")]          # by (owner, global id)
+    l2g = np.concatenate([own, gh])
+    g2l = np.full(n_dofs, -1, dtype=np.int64)
+    g2l[l2g] = np.arange(len(l2g))
     fwd, rev = Exchange(), Exchange()
     for s in range(k):
         if s == rank:
             continue
-        # ghosts on s owned by rank -> rank sends u, receives y partials
-        ls = l2g_all[s]
-        gh_s = ls[owner[ls] == rank]
-        gh_s = np.sort(gh_s)
-        # ghosts on rank owned by s
-        lr = l2g_all[rank]
-        gh_r = np.sort(lr[owner[lr] == s])
+        on_s = ((mask >> s) & 1).astype(bool)
+        gh_s = np.flatnonzero(on_s & (owner == rank))      # s's ghosts that I own (ascending)
+        gh_r = np.flatnonzero(mine & (owner == s))         # my ghosts owned by s (ascending)
         if len(gh_s) == 0 and len(gh_r) == 0:
             continue
         fwd.peers.append(s)
         rev.peers.append(s)
-        fwd.send[s] = g2l(rank, gh_s)
-        fwd.recv[s] = g2l(rank, gh_r)
+        fwd.send[s] = g2l[gh_s]
+        fwd.recv[s] = g2l[gh_r]
         # reverse: constrained DoFs are never scattered -> excluded
-        rev_send = gh_r[~dirichlet_mask[gh_r]]
-        rev_recv = gh_s[~dirichlet_mask[gh_s]]
-        rev.send[s] = g2l(rank, rev_send)
-        rev.recv[s] = g2l(rank, rev_recv)
+        rev.send[s] = g2l[gh_r[~dirichlet_mask[gh_r]]]
+        rev.recv[s] = g2l[gh_s[~dirichlet_mask[gh_s]]]
     cells_g = np.flatnonzero(part == rank)
     lmesh, _ = _local_mesh(mesh, cells_g)
-    l2g = l2g_all[rank]
-    lcd = g2l(rank, cell_dofs[cells_g].ravel().astype(np.int64)).reshape(-1, nd).astype(np.int32)
-    n_owned = int(np.sum(owner[l2g] == rank))
-    return CgSubdomain(rank, lmesh, lcd, dirichlet_mask[l2g], l2g, n_owned, fwd, rev)
+    lcd = g2l[cell_dofs[cells_g].astype(np.int64)].astype(np.int32).reshape(-1, nd)
+    return CgSubdomain(rank, lmesh, lcd, dirichlet_mask[l2g], l2g, len(own), fwd, rev)
+
+
+def _face_index_tables(mesh: TetMesh):
+    """(4*cell + lf) -> interior face index / boundary face index (or -1)."""
+    n4 = 4 * mesh.n_cells
+    fi = np.full(n4, -1, dtype=np.int64)
+    ifc = mesh.interior_faces.astype(np.int64)
+    idx = np.arange(len(ifc))
+    fi[4 * ifc[:, 0] + ifc[:, 1]] = idx
+    fi[4 * ifc[:, 2] + ifc[:, 3]] = idx
+    bi = np.full(n4, -1, dtype=np.int64)
+    bfc = mesh.boundary_faces.astype(np.int64)
+    bi[4 * bfc[:, 0] + bfc[:, 1]] = np.arange(len(bfc))
+    return fi, bi
 
 
 def build_dg_subdomain(mesh: TetMesh, part: np.ndarray, rank: int, k: int,
                        dirichlet_ids=()) -> DgSubdomain:
     ifc = mesh.interior_faces.astype(np.int64)
     cm, cp = ifc[:, 0], ifc[:, 2]
+    cross = part[cm] != part[cp]
 
     def ghosts_of(r):
-        a = (part[cm] == r) & (part[cp] != r)
-        b = (part[cp] == r) & (part[cm] != r)
+        a = cross & (part[cm] == r)
+        b = cross & (part[cp] == r)
         g = np.unique(np.concatenate([cp[a], cm[b]]))
-        return g[np.lexsort((g, part[g]))]
+        return g[np.argsort(part[g], kind="stable")]       # by (owner, global id)
 
     owned = np.flatnonzero(part == rank)
     ghosts = ghosts_of(rank)
     cells_g = np.concatenate([owned, ghosts])
     lmesh, _ = _local_mesh(mesh, cells_g)
-    # map local faces back to global faces (sorted vertex triples)
-    g_tri_i = np.sort(mesh.cells[ifc[:, 0, None], FACE_VERTICES_ARR[ifc[:, 1]]], axis=1)
-    bfc = mesh.boundary_faces.astype(np.int64)
-    g_tri_b = np.sort(mesh.cells[bfc[:, 0, None], FACE_VERTICES_ARR[bfc[:, 1]]], axis=1)
-    lc_g = cells_g                                     # local cell -> global cell
+    # local faces -> global faces through (global cell, local face) (same local face numbering)
+    fi, bi = _face_index_tables(mesh)
     li, lb = lmesh.interior_faces.astype(np.int64), lmesh.boundary_faces.astype(np.int64)
-    l_tri_i = np.sort(mesh.cells[lc_g[li[:, 0]][:, None], FACE_VERTICES_ARR[li[:, 1]]], axis=1)
-    l_tri_b = np.sort(mesh.cells[lc_g[lb[:, 0]][:, None], FACE_VERTICES_ARR[lb[:, 1]]], axis=1)
-
-    def match(q, ref):
-        keys = {tuple(t): i for i, t in enumerate(ref.tolist())}
-        return np.array([keys.get(tuple(t), -1) for t in q.tolist()], dtype=np.int64)
-
-    if_g = match(l_tri_i, g_tri_i)
-    bf_g = match(l_tri_b, g_tri_b)
+    if_g = fi[4 * cells_g[li[:, 0]] + li[:, 1]]
+    bf_g = bi[4 * cells_g[lb[:, 0]] + lb[:, 1]]            # -1: artificial (ghost-layer) face
+    bfc = mesh.boundary_faces.astype(np.int64)
     bids = np.where(bf_g >= 0, bfc[np.maximum(bf_g, 0), 2], -1)
     lb_out = lb.copy()
     lb_out[:, 2] = bids

@@ -52,6 +52,7 @@ class OperatorConfig:
     backend: str = "auto"
     device: int = 0
     kernel_variant: int = 0     # B200 cell-kernel tuning variant (0 = default)
+    face_variant: int = 0       # B200 face-kernel tuning variant (0 = default)
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -176,7 +177,8 @@ class _B200Operator:
         d.mass_scale = float(mass_scale)
         d.diffusivity = float(diffusivity)
         d.device = int(self.config.device)
-        d.flags = int(getattr(self.config, "kernel_variant", 0)) & 0xF
+        d.flags = (int(getattr(self.config, "kernel_variant", 0)) & 0xF) | \
+            ((int(getattr(self.config, "face_variant", 0)) & 0xF) << 4)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))
