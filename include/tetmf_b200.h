@@ -102,6 +102,12 @@ int tmf_apply(tmf_plan* plan, const double* u, double* y, void* stream);
 /* Same with host buffers: H2D(u), apply, D2H(y), synchronous. */
 int tmf_apply_host(tmf_plan* plan, const double* u_host, double* y_host);
 
+/* Same, asynchronous on `stream`: H2D(u), apply, D2H(y) are enqueued and the
+ * call returns; u_host/y_host should be pinned and must stay valid until the
+ * stream reaches that point.  Lets a caller pipeline several plans' copies
+ * against each other's kernels. */
+int tmf_apply_host_async(tmf_plan* plan, const double* u_host, double* y_host, void* stream);
+
 /* Per-stage timing of `reps` back-to-back applies (device pointers), CUDA
  * events on `stream`: out_ms[0] = total, out_ms[1..] = per kernel class
  * (cell, face, fixup).  For the bench only. */

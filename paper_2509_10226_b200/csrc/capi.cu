@@ -560,6 +560,22 @@ int tmf_apply_host(tmf_plan* P, const double* u_host, double* y_host) {
   return TMF_OK;
 }
 
+int tmf_apply_host_async(tmf_plan* P, const double* u_host, double* y_host, void* stream) {
+  if (!P || !u_host || !y_host) return fail(TMF_EINVAL, "null argument");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  const size_t bytes = sizeof(double) * P->n_global;
+  if (!P->stage_u) {
+    TMF_CUDA(cudaMalloc(&P->stage_u, bytes));
+    TMF_CUDA(cudaMalloc(&P->stage_y, bytes));
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  TMF_CUDA(cudaMemcpyAsync(P->stage_u, u_host, bytes, cudaMemcpyHostToDevice, st));
+  int rc = launch_apply(P, P->stage_u, P->stage_y, st, nullptr);
+  if (rc) return rc;
+  TMF_CUDA(cudaMemcpyAsync(y_host, P->stage_y, bytes, cudaMemcpyDeviceToHost, st));
+  return TMF_OK;
+}
+
 int tmf_apply_timed(tmf_plan* P, const double* u, double* y, void* stream, int reps, double* out_ms,
                     int n_out) {
   if (!P || !u || !y || !out_ms || reps < 1) return fail(TMF_EINVAL, "bad argument");

@@ -232,6 +232,18 @@ class _B200Operator:
         self._count()
         return y
 
+    def apply_host_async(self, u_host, y_host, stream: int = 0):
+        """Enqueue H2D(u), apply, D2H(y) on ``stream`` and return (pinned host arrays
+        or tensors; they must outlive the stream work)."""
+        for t in (u_host, y_host):
+            n = t.numel() if hasattr(t, "numel") else len(t)
+            if n != self.n_global_dofs:
+                raise ValueError("host buffer length does not match the operator size")
+        up = u_host.data_ptr() if hasattr(u_host, "data_ptr") else u_host.ctypes.data
+        yp = y_host.data_ptr() if hasattr(y_host, "data_ptr") else y_host.ctypes.data
+        _lib.check(_lib.lib().tmf_apply_host_async(self._plan, C.c_void_p(up), C.c_void_p(yp), C.c_void_p(stream)))
+        self._count()
+
     def apply_into(self, u_ptr: int, y_ptr: int, stream: int = 0):
         """Raw device-pointer apply (y overwritten), ordered on ``stream``."""
         _lib.check(_lib.lib().tmf_apply(self._plan, C.c_void_p(u_ptr), C.c_void_p(y_ptr), C.c_void_p(stream)))
