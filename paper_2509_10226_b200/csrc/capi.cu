@@ -473,7 +473,8 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
                                               std::to_string(N) + ", " + std::to_string(QF) + ")"));
     if ((int64_t)fr.size() != 24LL * fi.nfrag * 32) return bail(fail(TMF_EINVAL, "internal: face fragments"));
     if ((rc = upload(&P->face_frags, fr.data(), fr.size(), &total))) return bail(rc);
-    if ((rc = build_face_batches(P, d, fi.chunk, &total))) return bail(rc);
+    const int chunk = ((d->flags >> 8) & 0xF) ? 8 * ((d->flags >> 8) & 0xF) : fi.chunk;
+    if ((rc = build_face_batches(P, d, chunk, &total))) return bail(rc);
     // per-face geometry, computed once on the device (64 B per face slot)
     for (int bnd = 0; bnd < 2; ++bnd) {
       const int64_t slots = (bnd ? P->n_bf_batches : P->n_if_batches) * 8;

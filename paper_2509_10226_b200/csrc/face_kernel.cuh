@@ -69,7 +69,7 @@ struct FaceShape {
   static constexpr int NB1 = G * 2 * KK;       // GEMM1 fragments: (g, h, kk)
   static constexpr int NB2 = G * 4 * NJ;       // GEMM2 fragments: (g, c, nj)
   static constexpr int NFRAG = NB1 + NB2;      // per (lf, code) combo
-  static constexpr int CHUNK = 32;             // batches per CTA chunk
+  static constexpr int CHUNK = 32;             // default batches per CTA chunk
 };
 
 __device__ __forceinline__ void cell_affine(const int* __restrict__ cells, const double* __restrict__ verts,
@@ -153,8 +153,8 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
   }
 }
 
-// PF: software-prefetch the next batch (record, geometry, gathered u); MINB: CTAs/SM hint
-template <int N, int QF, bool BOUNDARY, bool PF = true, int MINB = 2>
+// PF: prefetch depth (0 none, 1 face record, 2 record + geometry + gathered u); MINB: CTAs/SM hint
+template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2>
 __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
   extern __shared__ __align__(16) double smem[];
@@ -181,17 +181,25 @@ __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
     const double* Fm = smem;
     const double* Fp = smem + S::NFRAG * 32;
 
-    // Software pipeline over the warp's batches: the next batch's face record,
-    // geometry and gathered u values are loaded while the current batch computes.
+    // Software pipeline over the warp's batches.  PF 2: the next batch's face
+    // record, geometry and gathered u are loaded while the current batch
+    // computes; PF 1: only the record (cell ids) is prefetched, so the u and
+    // geometry loads of a batch are issued together (one memory round trip);
+    // PF 0: no prefetch.
     double nam[S::KK], nap[S::KK], ng[8];
     int n_cm = -1, n_cp = -1;
-    auto fetch = [&](int bi) {
+    auto fetch_rec = [&](int bi) {
       n_cm = -1;
       n_cp = -1;
       if (bi < ch.w) {
         const int64_t slot = ((int64_t)ch.z + bi) * 8 + fs;
         n_cm = __ldg(a.cm + slot);
         if (!BOUNDARY) n_cp = __ldg(a.cp + slot);
+      }
+    };
+    auto fetch_data = [&](int bi) {
+      if (bi < ch.w) {
+        const int64_t slot = ((int64_t)ch.z + bi) * 8 + fs;
         const double2* gp = reinterpret_cast<const double2*>(a.geo + slot * 8);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -211,10 +219,12 @@ __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
         }
       }
     };
-    if (PF) fetch(warp);
+    if (PF >= 1) fetch_rec(warp);
+    if (PF == 2) fetch_data(warp);
 
     for (int bi = warp; bi < ch.w; bi += nwb) {
-      if (!PF) fetch(bi);
+      if (PF == 0) fetch_rec(bi);
+      if (PF <= 1) fetch_data(bi);
       const int c_m = n_cm, c_p = n_cp;
       double am[S::KK], ap[S::KK];
 #pragma unroll
@@ -225,7 +235,8 @@ __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
       const double mm[3] = {ng[0], ng[1], ng[2]};
       const double mp[3] = {ng[3], ng[4], ng[5]};
       const double s = ng[6], tau = ng[7];
-      if (PF) fetch(bi + nwb);
+      if (PF >= 1) fetch_rec(bi + nwb);
+      if (PF == 2) fetch_data(bi + nwb);
 
       double ym[S::NJ][2], yp[S::NJ][2];
 #pragma unroll

@@ -82,7 +82,7 @@ cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& 
   return cudaSuccess;
 }
 
-template <int N, int QF, bool BND, bool PF = true, int MINB = 2>
+template <int N, int QF, bool BND, int PF = 2, int MINB = 2>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShape<N, QF>;
   constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
@@ -112,18 +112,18 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
 }
 
 // variant: 0 = default (by degree, below); 1 = no prefetch, 3 CTAs/SM;
-// 2 = no prefetch, 2 CTAs/SM; 3 = prefetch, 1 CTA/SM; 4 = prefetch, 2 CTAs/SM
+// 2 = record prefetch, 3 CTAs/SM; 3 = record prefetch, 2 CTAs/SM; 4 = full prefetch, 2 CTAs/SM
 template <int N, int QF, bool BND>
 static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info,
                                  int variant) {
-  if (variant == 1) return launch_face_v<N, QF, BND, false, 3>(a, n_sm, st, info);
-  if (variant == 2) return launch_face_v<N, QF, BND, false, 2>(a, n_sm, st, info);
-  if (variant == 3) return launch_face_v<N, QF, BND, true, 1>(a, n_sm, st, info);
-  if (variant == 4) return launch_face_v<N, QF, BND, true, 2>(a, n_sm, st, info);
+  if (variant == 1) return launch_face_v<N, QF, BND, 0, 3>(a, n_sm, st, info);
+  if (variant == 2) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
+  if (variant == 3) return launch_face_v<N, QF, BND, 1, 2>(a, n_sm, st, info);
+  if (variant == 4) return launch_face_v<N, QF, BND, 2, 2>(a, n_sm, st, info);
   // default: low degrees have short batches -> occupancy beats prefetch depth (measured
-  // at P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the prefetching 2-CTA kernel
-  if (N <= 10) return launch_face_v<N, QF, BND, false, 3>(a, n_sm, st, info);
-  return launch_face_v<N, QF, BND, true, 2>(a, n_sm, st, info);
+  // at P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the fully prefetching 2-CTA kernel
+  if (N <= 10) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
+  return launch_face_v<N, QF, BND, 2, 2>(a, n_sm, st, info);
 }
 
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,

@@ -100,17 +100,17 @@ def base_record(tm, p, rule_kind, cr, fr, basis, dm):
         face_values=basis.face_values, face_grads=basis.face_grads)
 
 
-def cg_case(n, p, rule_kind, dids, seed=0):
+def cg_case(n, p, rule_kind, dids, seed=0, nc=1):
     tm = ref_mesh(n, seed)
     cr, fr = rules(p, rule_kind)
     basis = ref_basis(p, cr, fr)
-    dm = ref_dofmap(tm, p, "cg", 1, dids)
+    dm = ref_dofmap(tm, p, "cg", nc, dids)
     geo = rgeo.build_geometry(tm, cr, "affine")
     u = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
     y = rop.CgPoissonOperator(tm, dm, geo, basis).apply(u)
     A = rsparse.assemble(dm, tm, geo, basis)
     rec = base_record(tm, p, rule_kind, cr, fr, basis, dm)
-    rec.update(kind="cg", n=n, dirichlet_ids=np.array(dids, dtype=np.int64), u=u, y=y,
+    rec.update(kind="cg", n=n, n_components=nc, dirichlet_ids=np.array(dids, dtype=np.int64), u=u, y=y,
                y_csr=A.matvec(u), diag=A.to_scipy().diagonal())
     return rec
 
@@ -196,6 +196,7 @@ def cases():
         yield f"cg_p{p}_n4_ref", lambda p=p: cg_case(4, p, "ref", ())
         yield f"cg_p{p}_n4_ref_dir", lambda p=p: cg_case(4, p, "ref", ALL)
         yield f"cg_p{p}_n3_gm_dir2", lambda p=p: cg_case(3, p, "gm", (1, 4))
+    yield "cg3_p2_n3_ref_dir", lambda: cg_case(3, 2, "ref", (0, 2, 5), nc=3)
     yield "cg_p4_n3_gm", lambda: cg_case(3, 4, "gm", ())
     yield "cg_p4_n3_gm_dir", lambda: cg_case(3, 4, "gm", ALL)
     for p in (1, 2, 3):

@@ -10,7 +10,7 @@ from paper_2509_10226_b200 import operator as op
 def fixture_objects(g):
     nd = g["cell_dofs"].shape[1]
     kind = str(g["kind"])
-    nc = 3 if kind == "helm3" else 1
+    nc = 3 if kind == "helm3" else int(g["n_components"]) if "n_components" in g else 1
     space = "cg" if kind == "cg" else "dg"
     n_scalar = len(g["u"]) // nc
     mesh = NS(vertices=g["vertices"], cells=g["cells"], interior_faces=g["interior_faces"],

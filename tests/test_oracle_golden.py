@@ -12,8 +12,14 @@ TOL = 1e-12   # north_star: relative L2 <= 1e-12 in fp64
 def _oracle_y(g):
     kind = str(g["kind"])
     if kind == "cg":
-        return ref_apply.cg_apply(g["vertices"], g["cells"], g["cell_dofs"], g["dirichlet_mask"],
-                                  g["grad_matrix"], g["cell_weights"], g["u"])
+        nc = int(g["n_components"]) if "n_components" in g else 1
+        if nc == 1:
+            return ref_apply.cg_apply(g["vertices"], g["cells"], g["cell_dofs"], g["dirichlet_mask"],
+                                      g["grad_matrix"], g["cell_weights"], g["u"])
+        u = g["u"].reshape(-1, nc)
+        return np.stack([ref_apply.cg_apply(g["vertices"], g["cells"], g["cell_dofs"], g["dirichlet_mask"],
+                                            g["grad_matrix"], g["cell_weights"], u[:, c])
+                         for c in range(nc)], axis=1).ravel()
     nd = g["cell_dofs"].shape[1]
     common = (g["vertices"], g["cells"], nd, g["interior_faces"], g["boundary_faces"],
               set(g["dirichlet_ids"].tolist()), g["value_matrix"], g["grad_matrix"], g["cell_weights"],
