@@ -99,3 +99,13 @@ def test_reordered_mesh_gives_same_operator(p):
     y1 = op.CgPoissonOperator(m, d1, geo, bas).apply(u1)
     y2 = op.CgPoissonOperator(m2, d2, geo, bas).apply(u1[perm])
     assert rel_l2(y2, y1[perm]) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["cg_p2_n8_gm", "cg_p3_n4_ref_dir", "cg_p4_n3_gm_dir"])
+def test_gpu_csr_baseline_matches_reference_csr(name):
+    from paper_2509_10226_b200.sparse import CsrOperator
+
+    g = load_golden(name)
+    mesh, dofmap, geo, basis = fixture_objects(g)
+    A = CsrOperator(mesh, dofmap, geo, basis)
+    assert rel_l2(A.apply(g["u"]), g["y_csr"]) <= 1e-12

@@ -145,6 +145,45 @@ def c5(n=128, iters=100):
           flush=True)
 
 
+def csr(n=48):
+    """Matrix-free vs assembled CSR (cuSPARSE) on the C2 meshes: the paper's comparison on B200."""
+    import torch
+
+    from paper_2509_10226_b200 import operator as op
+    from paper_2509_10226_b200.sparse import CsrOperator
+
+    for p in (1, 2, 3, 4):
+        m, dm, geo, bas, ts = setup(n, p, "cg", True)
+        A = op.CgPoissonOperator(m, dm, geo, bas)
+        ms_mf = timed(A, dm.n_global_dofs)
+        t0 = time.time()
+        S = CsrOperator(m, dm, geo, bas)
+        torch.cuda.synchronize()
+        t_asm = time.time() - t0
+        u = torch.rand(dm.n_global_dofs, dtype=torch.float64, device="cuda")
+        flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+        for _ in range(3):
+            S.apply(u)
+        tt = []
+        for _ in range(10):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            S.apply(u)
+            e1.record()
+            e1.synchronize()
+            tt.append(e0.elapsed_time(e1))
+        ms = float(np.mean(tt))
+        print(json.dumps({"config": f"C2 P{p} {n}^3x6 reordered: matrix-free vs CSR SpMV (cuSPARSE)",
+                          "ndof": dm.n_global_dofs, "nnz": S.nnz, "csr_bytes": S.nbytes,
+                          "mf_ms": round(float(ms_mf[0]), 4), "csr_spmv_ms": round(ms, 4),
+                          "csr_assembly_s": round(t_asm, 2),
+                          "csr_spmv_gbps": round(S.nbytes / ms / 1e6, 1),
+                          "mf_speedup_over_csr": round(ms / float(ms_mf[0]), 3)}), flush=True)
+        del S
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["c1", "c2", "c3", "c4", "c5"])
@@ -153,4 +192,5 @@ if __name__ == "__main__":
     ap.add_argument("--n5", type=int, default=128)
     a = ap.parse_args()
     for c in a.configs:
-        {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5)}[c]()
+        {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5),
+         "csr": csr}[c]()
