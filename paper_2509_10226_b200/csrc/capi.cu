@@ -66,22 +66,25 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
           }
 }
 
-// Face tables (4 components per point), point groups of 4 (see face_kernel.cuh):
-//   B1[g][h][kk][lane] = E_{2h + (n&1)}(4g + (n>>1), 4kk + (lane&3)),  n = lane>>2
-//   B2[g][c][nj][lane] = w_q E_c(q = 4g + (lane&3), 8nj + (lane>>2))
+// Face tables in the face frame (see face_kernel.cuh), for one (lf, code) combo.
+// Components c: 0 = value, 1..3 = D_i = a_i . grad (a_0, a_1 tangent, a_2 transversal);
+// columns are DoFs in the gather order perm (face DoFs first).  Point groups of 4:
+//   B1[g][h=0][kk < KKF] / [h=1][kk < KK][lane] = E_{2h + (n&1)}(4g + (n>>1), 4kk + (lane&3)), n = lane>>2
+//   B2[g][c<3][nj < NJF] / [c=3][nj < NJ][lane] = w_q E_c(q = 4g + (lane&3), 8nj + (lane>>2))
 template <typename F>
-void build_face_fragments(int N, int Q, F E, const double* w, std::vector<double>& out) {
-  const int G = (Q + 3) / 4, KK = (N + 3) / 4, NJ = (N + 7) / 8;
+void build_face_fragments(int N, int NF, int Q, F E, const double* w, std::vector<double>& out) {
+  const int G = (Q + 3) / 4, KK = (N + 3) / 4, NJ = (N + 7) / 8, KKF = (NF + 3) / 4, NJF = (NF + 7) / 8;
+  auto Ev = [&](int c, int q, int j) { return (q < Q && j < N) ? E(c, q, j) : 0.0; };
   for (int g = 0; g < G; ++g)
     for (int h = 0; h < 2; ++h)
-      for (int kk = 0; kk < KK; ++kk)
+      for (int kk = 0; kk < (h == 0 ? KKF : KK); ++kk)
         for (int lane = 0; lane < 32; ++lane) {
-          const int n = lane >> 2, q = 4 * g + (n >> 1), c = 2 * h + (n & 1), j = 4 * kk + (lane & 3);
-          out.push_back(q < Q && j < N ? E(c, q, j) : 0.0);
+          const int n = lane >> 2;
+          out.push_back(Ev(2 * h + (n & 1), 4 * g + (n >> 1), 4 * kk + (lane & 3)));
         }
   for (int g = 0; g < G; ++g)
     for (int c = 0; c < 4; ++c)
-      for (int nj = 0; nj < NJ; ++nj)
+      for (int nj = 0; nj < (c < 3 ? NJF : NJ); ++nj)
         for (int lane = 0; lane < 32; ++lane) {
           const int q = 4 * g + (lane & 3), j = 8 * nj + (lane >> 2);
           out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
@@ -105,6 +108,7 @@ struct tmf_plan {
   double* cell_frags = nullptr;
   double* cell_geo = nullptr;
   double* face_frags = nullptr;
+  int* face_perm = nullptr;
   int* cells = nullptr;
   int* dofs = nullptr;
   int* fix_list = nullptr;
@@ -147,6 +151,7 @@ struct tmf_plan {
     a.cm = boundary ? bf_cm : if_cm;
     a.cp = boundary ? nullptr : if_cp;
     a.geo = boundary ? bf_geo : if_geo;
+    a.perm = face_perm;
     a.n_chunks = boundary ? n_bf_chunks : n_if_chunks;
     a.n_dpc = N;
     a.nc = nc;
@@ -170,7 +175,7 @@ struct tmf_plan {
     for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
-                    (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo})
+                    (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm})
       if (p) cudaFree(p);
   }
 };
@@ -453,17 +458,48 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     if ((rc = upload(&P->diag_S, S.data(), S.size(), &total))) return bail(rc);
   }
 
-  // face tables -> fragments per (lf, code), face batches
+  // face tables -> fragments per (lf, code) in the face frame, face batches
   if (faces) {
     const int N = P->N, QF = P->QF;
+    const int NF = (P->degree + 1) * (P->degree + 2) / 2;
+    // gather order per local face: the DoFs whose basis function does not vanish
+    // on the face (nodal basis: exactly the face's NF nodes), then the rest
+    std::vector<int> perm(4 * N);
+    for (int lf = 0; lf < 4; ++lf) {
+      const double* Fv = d->face_values + (size_t)(lf * 6) * QF * N;
+      std::vector<int> on, off;
+      for (int j = 0; j < N; ++j) {
+        double mx = 0.0;
+        for (int q = 0; q < QF; ++q) mx = std::max(mx, std::fabs(Fv[q * N + j]));
+        (mx > 1e-10 ? on : off).push_back(j);
+      }
+      if ((int)on.size() != NF) return bail(fail(TMF_EINVAL, "face tables are not those of a nodal basis"));
+      on.insert(on.end(), off.begin(), off.end());
+      std::copy(on.begin(), on.end(), perm.begin() + lf * N);
+    }
+    if ((rc = upload(&P->face_perm, perm.data(), perm.size(), &total))) return bail(rc);
     std::vector<double> fr;
-    for (int lf = 0; lf < 4; ++lf)
+    for (int lf = 0; lf < 4; ++lf) {
+      const double R[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+      const int fvv[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+      double a[3][3];  // a[i] = frame vector i
+      for (int k = 0; k < 3; ++k) {
+        a[0][k] = R[fvv[lf][1]][k] - R[fvv[lf][0]][k];
+        a[1][k] = R[fvv[lf][2]][k] - R[fvv[lf][0]][k];
+        a[2][k] = R[lf][k] - R[fvv[lf][0]][k];
+      }
+      const int* pm = perm.data() + lf * N;
       for (int code = 0; code < 6; ++code) {
         const double* Fv = d->face_values + (size_t)(lf * 6 + code) * QF * N;
         const double* Fg = d->face_grads + (size_t)(lf * 6 + code) * 3 * QF * N;
-        build_face_fragments(N, QF, [&](int c, int q, int j) {
-          return c == 0 ? Fv[q * N + j] : Fg[(3 * q + c - 1) * N + j]; }, d->face_weights, fr);
+        build_face_fragments(N, NF, QF, [&](int c, int q, int j) {
+          const int jj = pm[j];
+          if (c == 0) return Fv[q * N + jj];
+          const double* av = a[c - 1];
+          return av[0] * Fg[(3 * q) * N + jj] + av[1] * Fg[(3 * q + 1) * N + jj] + av[2] * Fg[(3 * q + 2) * N + jj];
+        }, d->face_weights, fr);
       }
+    }
     tmf::FaceLaunchInfo fi;
     bool ok = true;
     tmf::FaceArgs dummy{};

@@ -16,13 +16,23 @@
 // one CTA per chunk stages the two tables' DMMA fragments in shared memory
 // once and its warps stream over the chunk's batches.
 //
-// Point layout (4 components per point: value + 3 reference gradients):
-// points are taken in groups of 4; GEMM1 n-tile (g, h) holds columns
-// 2*q + i = (point 4g + q, component 2h + i), so lane (q = lane&3) owns all
-// four components of point 4g + q after the two tiles of group g, and those
-// four values are directly the A fragments of the four GEMM2 k-steps
-// (g, c), k = lane&3 <-> point 4g + k.  Points pad to a multiple of 4
-// (n_qf 20 -> 20, 10 -> 12), not 8.
+// Face frame.  Each side's reference gradient is rotated into the frame of
+// its local face lf: D = A_lf^T grad, A_lf = [c1-c0, c2-c0, v_lf-c0] (two
+// tangent directions of the reference face and one transversal), and
+// m.grad = (A_lf^-1 m).D, so the geometry record stores m~ = A^-1 m.  With
+// a nodal (Lagrange) basis the value and the two tangential derivatives on a
+// face only involve the NF = (p+1)(p+2)/2 DoFs on that face; DoFs are gathered
+// in the order perm_lf = (face DoFs, other DoFs) so those three components
+// only need ceil(NF/4) GEMM1 k-steps and ceil(NF/8) GEMM2 n-tiles (the
+// transversal component keeps all of them): 29 % (P2), 23 % (P3) and 37 % (P4)
+// fewer DMMAs than the plain 4-component layout, same quadrature.
+//
+// Point layout (4 components per point: value, D0, D1 | D2): points are taken
+// in groups of 4; GEMM1 n-tile (g, h) holds columns 2*q + i = (point 4g + q,
+// component 2h + i), so lane (q = lane&3) owns all four components of point
+// 4g + q after the two tiles of group g, and those four values are directly
+// the A fragments of the four GEMM2 k-steps (g, c), k = lane&3 <-> point
+// 4g + k.  Points pad to a multiple of 4 (n_qf 20 -> 20, 10 -> 12), not 8.
 // Geometry (unit normal outward from the minus cell, |t_s x t_t|,
 // m = J^-1 n on each side, geometry.py:202-236) is computed once per plan by
 // face_geometry_kernel.  Contributions are added to y with fp64 RED.
@@ -38,7 +48,8 @@ struct FaceArgs {
   const int4* __restrict__ chunks;    // (combo-, combo+ or -1, first batch, n batches)
   const int* __restrict__ cm;         // (n_batches*8) minus cell, -1 = padding
   const int* __restrict__ cp;         // (n_batches*8) plus cell (interior)
-  const double* __restrict__ geo;     // (n_batches*8, 8): m-[3], m+[3], s, tau (see below)
+  const double* __restrict__ geo;     // (n_batches*8, 8): m~-[3], m~+[3], s, tau (see below)
+  const int* __restrict__ perm;       // (4, n_dpc): gather order per local face (face DoFs first)
   int64_t n_chunks;
   int n_dpc;
   int nc;
@@ -63,14 +74,55 @@ struct FaceGeoArgs {
 
 template <int N, int QF>
 struct FaceShape {
+  static constexpr int NF = N == 4 ? 3 : N == 10 ? 6 : N == 20 ? 10 : 15;  // DoFs on a face
   static constexpr int KK = (N + 3) / 4;
+  static constexpr int KKF = (NF + 3) / 4;
   static constexpr int G = (QF + 3) / 4;       // point groups of 4
   static constexpr int NJ = (N + 7) / 8;
-  static constexpr int NB1 = G * 2 * KK;       // GEMM1 fragments: (g, h, kk)
-  static constexpr int NB2 = G * 4 * NJ;       // GEMM2 fragments: (g, c, nj)
+  static constexpr int NJF = (NF + 7) / 8;
+  static constexpr int B1G = KKF + KK;         // GEMM1 fragments per group: h=0 (V,D0) | h=1 (D1,D2)
+  static constexpr int B2G = 3 * NJF + NJ;     // GEMM2 fragments per group: V, D0, D1 face-only | D2
+  static constexpr int NB1 = G * B1G;
+  static constexpr int NB2 = G * B2G;
   static constexpr int NFRAG = NB1 + NB2;      // per (lf, code) combo
   static constexpr int CHUNK = 32;             // default batches per CTA chunk
+  __host__ __device__ static constexpr int b1(int g, int h, int kk) { return g * B1G + (h ? KKF + kk : kk); }
+  __host__ __device__ static constexpr int b2(int g, int c, int nj) {
+    return NB1 + g * B2G + (c < 3 ? c * NJF + nj : 3 * NJF + nj);
+  }
 };
+
+// A_lf^-1 for the face frame (reference vertices (0,0,0),(1,0,0),(0,1,0),(0,0,1)).
+__host__ __device__ inline void face_frame_inverse(int lf, double (&Ai)[3][3]) {
+  const double R[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  const int fv[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+  double A[3][3];
+  for (int k = 0; k < 3; ++k) {
+    A[k][0] = R[fv[lf][1]][k] - R[fv[lf][0]][k];
+    A[k][1] = R[fv[lf][2]][k] - R[fv[lf][0]][k];
+    A[k][2] = R[lf][k] - R[fv[lf][0]][k];
+  }
+  const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1], c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2],
+               c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+  const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
+  Ai[0][0] = c00 / det;
+  Ai[1][0] = c01 / det;
+  Ai[2][0] = c02 / det;
+  Ai[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) / det;
+  Ai[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) / det;
+  Ai[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) / det;
+  Ai[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) / det;
+  Ai[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) / det;
+  Ai[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) / det;
+}
+
+__device__ __forceinline__ void to_face_frame(int lf, double (&m)[3]) {
+  double Ai[3][3];
+  face_frame_inverse(lf, Ai);
+  const double x = m[0], y = m[1], z = m[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) m[i] = Ai[i][0] * x + Ai[i][1] * y + Ai[i][2] * z;
+}
 
 __device__ __forceinline__ void cell_affine(const int* __restrict__ cells, const double* __restrict__ verts,
                                             int c, Affine& g, Vec3& opp_base, int lf, Vec3& face_v0) {
@@ -92,7 +144,8 @@ __device__ __forceinline__ void apply_inv(const Affine& g, const double (&n)[3],
 }
 
 // One thread per face slot: unit normal outward from the minus cell
-// (geometry.py:207-225), surface JxW factor and m = J^-1 n on each side.
+// (geometry.py:207-225), surface JxW factor and m = J^-1 n on each side, the
+// latter expressed in the side's face frame (m~ = A_lf^-1 m).
 template <bool BOUNDARY>
 __global__ void face_geometry_kernel(FaceGeoArgs a) {
   for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
@@ -127,6 +180,7 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
       for (int i = 0; i < 3; ++i) n[i] *= inv;
       double mm[3], mp[3] = {0.0, 0.0, 0.0};
       apply_inv(Jm, n, mm);
+      to_face_frame(lfm, mm);
       double tau = a.tau[slot];
       const double km = a.kappa ? a.kappa[c_m] : 1.0;
       if (!BOUNDARY) {
@@ -135,6 +189,7 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
         Vec3 o2, f2;
         cell_affine(a.cells, a.verts, c_p, Jp, o2, 0, f2);
         apply_inv(Jp, n, mp);
+        to_face_frame(ch.y / 6, mp);
         const double kp = a.kappa ? a.kappa[c_p] : 1.0;
 #pragma unroll
         for (int i = 0; i < 3; ++i) mp[i] *= kp;
@@ -180,6 +235,8 @@ __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
     __syncthreads();
     const double* Fm = smem;
     const double* Fp = smem + S::NFRAG * 32;
+    const int* perm_m = a.perm + (ch.x / 6) * N;                  // gather order, minus side
+    const int* perm_p = a.perm + (BOUNDARY ? 0 : ch.y / 6) * N;   // plus side
 
     // Software pipeline over the warp's batches.  PF 2: the next batch's face
     // record, geometry and gathered u are loaded while the current batch
@@ -214,8 +271,8 @@ __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
         nam[kk] = 0.0;
         nap[kk] = 0.0;
         if (n_cm >= 0 && j < N) {
-          nam[kk] = __ldg(a.u + ((int64_t)n_cm * N + j) * a.nc + comp);
-          if (!BOUNDARY) nap[kk] = __ldg(a.u + ((int64_t)n_cp * N + j) * a.nc + comp);
+          nam[kk] = __ldg(a.u + ((int64_t)n_cm * N + __ldg(perm_m + j)) * a.nc + comp);
+          if (!BOUNDARY) nap[kk] = __ldg(a.u + ((int64_t)n_cp * N + __ldg(perm_p + j)) * a.nc + comp);
         }
       }
     };
@@ -251,7 +308,8 @@ __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
         for (int kk = 0; kk < S::KK; ++kk)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int f = ((g * 2 + h) * S::KK + kk) * 32 + lane;
+            if (h == 0 && kk >= S::KKF) continue;   // value and D0 live on the face DoFs
+            const int f = S::b1(g, h, kk) * 32 + lane;
             dmma(vm[h], am[kk], Fm[f]);
             if (!BOUNDARY) dmma(vp[h], ap[kk], Fp[f]);
           }
@@ -279,7 +337,8 @@ __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int nj = 0; nj < S::NJ; ++nj) {
-            const int f = (S::NB1 + (g * 4 + c) * S::NJ + nj) * 32 + lane;
+            if (c < 3 && nj >= S::NJF) continue;     // V, D0, D1 integrate onto face DoFs only
+            const int f = S::b2(g, c, nj) * 32 + lane;
             dmma(ym[nj], qm[c], Fm[f]);
             if (!BOUNDARY) dmma(yp[nj], qp[c], Fp[f]);
           }
@@ -292,8 +351,8 @@ __global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
           for (int i = 0; i < 2; ++i) {
             const int j = 8 * nj + 2 * q4 + i;
             if (j < N) {
-              atomicAdd(a.y + ((int64_t)c_m * N + j) * a.nc + comp, ym[nj][i]);
-              if (!BOUNDARY) atomicAdd(a.y + ((int64_t)c_p * N + j) * a.nc + comp, yp[nj][i]);
+              atomicAdd(a.y + ((int64_t)c_m * N + __ldg(perm_m + j)) * a.nc + comp, ym[nj][i]);
+              if (!BOUNDARY) atomicAdd(a.y + ((int64_t)c_p * N + __ldg(perm_p + j)) * a.nc + comp, yp[nj][i]);
             }
           }
       }

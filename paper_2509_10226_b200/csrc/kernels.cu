@@ -54,6 +54,8 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
     if (variant == 3) return launch_cell_v<N, Q, MASS, DG, 128, 1, 4>(a, n_sm, st, info);
     if (variant == 4) return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, true>(a, n_sm, st, info);
     if (variant == 5) return launch_cell_v<N, Q, MASS, DG, BLOCK, 1, 1, true>(a, n_sm, st, info);
+    if (variant == 6) return launch_cell_v<N, Q, MASS, DG, BLOCK, 3, 1>(a, n_sm, st, info);
+    if (variant == 7) return launch_cell_v<N, Q, MASS, DG, 128, 2, 1>(a, n_sm, st, info);
   }
   return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1>(a, n_sm, st, info);
 }
