@@ -28,7 +28,7 @@ from .basis import n_dofs_per_cell, reference_nodes
 from .mesh import TetMesh
 from .reference import EDGE_VERTICES_ARR, FACE_VERTICES_ARR
 
-__all__ = ["DoFMap", "build_dof_map", "face_local_dofs", "first_encounter_ids"]
+__all__ = ["DoFMap", "build_dof_map", "face_local_dofs", "first_encounter_ids", "dof_coordinates"]
 
 CG = "cg"
 DG = "dg"
@@ -188,3 +188,13 @@ def _dirichlet_mask(mesh, p, cell_dofs, n_scalar, dirichlet_boundary_ids):
             rows = bf[sel & (bf[:, 1] == lf), 0]
             mask[cell_dofs[rows[:, None], fl[lf][None, :]].reshape(-1)] = True
     return mask
+
+
+def dof_coordinates(mesh: TetMesh, dofmap: DoFMap, ref_nodes: np.ndarray) -> np.ndarray:
+    """Physical coordinates of the scalar DoFs (dofmap.py:295-303, vectorised)."""
+    v = mesh.vertices[mesh.cells]
+    jac = np.stack([v[:, 1] - v[:, 0], v[:, 2] - v[:, 0], v[:, 3] - v[:, 0]], axis=2)
+    phys = v[:, 0][:, None, :] + np.einsum("eij,aj->eai", jac, ref_nodes)
+    coords = np.empty((dofmap.n_scalar_dofs, 3))
+    coords[dofmap.cell_dofs.reshape(-1)] = phys.reshape(-1, 3)
+    return coords
