@@ -99,6 +99,17 @@ int tmf_plan_get_info(const tmf_plan* plan, tmf_plan_info* info);
  * (a cudaStream_t, NULL = legacy default stream).  y is overwritten. */
 int tmf_apply(tmf_plan* plan, const double* u, double* y, void* stream);
 
+/* The apply in stages, for callers that overlap communication with compute
+ * (the multi-GPU operators): ZERO clears y (CG), CELLS runs the cell kernel on
+ * cells [cell_begin, cell_end), FACES runs the face kernels (DG), FIXUP writes
+ * the identity Dirichlet rows (CG).  tmf_apply == all four on every cell. */
+#define TMF_STAGE_ZERO 1
+#define TMF_STAGE_CELLS 2
+#define TMF_STAGE_FACES 4
+#define TMF_STAGE_FIXUP 8
+int tmf_apply_stages(tmf_plan* plan, const double* u, double* y, int stages, int64_t cell_begin,
+                     int64_t cell_end, void* stream);
+
 /* Same with host buffers: H2D(u), apply, D2H(y), synchronous. */
 int tmf_apply_host(tmf_plan* plan, const double* u_host, double* y_host);
 

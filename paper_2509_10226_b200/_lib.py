@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libtetmf_b200.so")
 
 TMF_OK, TMF_EINVAL, TMF_ECUDA = 0, 1, 2
 TMF_CG_LAPLACE, TMF_DG_SIPG, TMF_DG_HELMHOLTZ = 0, 1, 2
+STAGE_ZERO, STAGE_CELLS, STAGE_FACES, STAGE_FIXUP = 1, 2, 4, 8
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -61,6 +62,8 @@ def lib():
         L.tmf_plan_get_info.argtypes = [C.c_void_p, C.POINTER(PlanInfo)]
         L.tmf_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.tmf_apply_host.argtypes = [C.c_void_p, _dp, _dp]
+        L.tmf_apply_stages.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int64,
+                                       C.c_void_p]
         L.tmf_apply_host_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.tmf_apply_timed.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int]
         L.tmf_diagonal.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -77,7 +80,7 @@ def lib():
         L.tmf_last_error.restype = C.c_char_p
         L.tmf_version.restype = C.c_char_p
         for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
-                     "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg",
+                     "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg",
                      "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs",
                      "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction"):
             getattr(L, name).restype = C.c_int
@@ -86,7 +89,7 @@ def lib():
 
 
 EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
-            "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
+            "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
             "tmf_build_faces", "tmf_build_cg_dofs", "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update",
             "tmf_pcg_direction", "tmf_last_error", "tmf_version")
 

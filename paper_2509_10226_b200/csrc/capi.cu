@@ -131,14 +131,18 @@ struct tmf_plan {
   double* diag = nullptr;
   double* diag_S = nullptr;
   tmf_plan_info info{};
-  tmf::CellArgs cell_args(const double* u, double* y) const {
+  // cell range [c0, c1): per-cell arrays are offset; CG u/y are global, DG u/y
+  // are cell-contiguous and offset with the cells
+  tmf::CellArgs cell_args(const double* u, double* y, int64_t c0 = 0, int64_t c1 = -1) const {
+    if (c1 < 0) c1 = n_cells;
     tmf::CellArgs a{};
-    a.u = u;
-    a.y = y;
-    a.dofs = dg ? nullptr : dofs;
-    a.cgeo = cell_geo;
+    const int64_t off = dg ? c0 * N * nc : 0;
+    a.u = u + off;
+    a.y = y + off;
+    a.dofs = dg ? nullptr : dofs + c0 * N;
+    a.cgeo = cell_geo + 8 * c0;
     a.frags = cell_frags;
-    a.n_cells = n_cells;
+    a.n_cells = c1 - c0;
     a.nc = nc;
     return a;
   }
@@ -317,6 +321,30 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
 }  // namespace
 
 extern "C" {
+
+int tmf_apply_stages(tmf_plan* P, const double* u, double* y, int stages, int64_t cell_begin,
+                     int64_t cell_end, void* stream) {
+  if (!P || !u || !y) return fail(TMF_EINVAL, "null argument");
+  if (cell_begin < 0 || cell_end > P->n_cells || cell_begin > cell_end)
+    return fail(TMF_EINVAL, "bad cell range");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  bool ok = true;
+  if ((stages & TMF_STAGE_ZERO) && !P->dg)
+    TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
+  if ((stages & TMF_STAGE_CELLS) && cell_end > cell_begin)
+    TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, cell_begin, cell_end), P->n_sm,
+                              st, nullptr, &ok, P->variant));
+  if ((stages & TMF_STAGE_FACES) && P->faces) {
+    TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
+                              P->face_variant));
+    TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
+                              P->face_variant));
+  }
+  if ((stages & TMF_STAGE_FIXUP) && !P->dg && P->n_fix)
+    TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st));
+  return TMF_OK;
+}
 
 const char* tmf_last_error(void) { return g_err.c_str(); }
 const char* tmf_version(void) { return "tetmf_b200 0.1 (sm_100a, fp64 DMMA)"; }

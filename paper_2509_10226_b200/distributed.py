@@ -82,6 +82,8 @@ class CgSubdomain:
     n_owned: int
     forward: Exchange             # u: owners -> ghosts
     reverse: Exchange             # y: ghosts -> owners (added)
+    n_interior_cells: int = 0     # local cells [0, n) touch no ghost DoF (overlap the forward halo)
+    cells_global: np.ndarray = None   # local cell -> global cell
 
 
 @dataclass
@@ -151,9 +153,12 @@ def build_cg_subdomain(mesh: TetMesh, cell_dofs: np.ndarray, dirichlet_mask: np.
         rev.send[s] = g2l[gh_r[~dirichlet_mask[gh_r]]]
         rev.recv[s] = g2l[gh_s[~dirichlet_mask[gh_s]]]
     cells_g = np.flatnonzero(part == rank)
+    touches_ghost = np.any(g2l[cell_dofs[cells_g].astype(np.int64)] >= len(own), axis=1)
+    cells_g = np.concatenate([cells_g[~touches_ghost], cells_g[touches_ghost]])  # interior first
     lmesh, _ = _local_mesh(mesh, cells_g)
     lcd = g2l[cell_dofs[cells_g].astype(np.int64)].astype(np.int32).reshape(-1, nd)
-    return CgSubdomain(rank, lmesh, lcd, dirichlet_mask[l2g], l2g, len(own), fwd, rev)
+    return CgSubdomain(rank, lmesh, lcd, dirichlet_mask[l2g], l2g, len(own), fwd, rev,
+                       int(np.count_nonzero(~touches_ghost)), cells_g)
 
 
 def _face_index_tables(mesh: TetMesh):
@@ -238,7 +243,8 @@ class HaloExchange:
             return idx
         return (idx[:, None] * block + np.arange(block)[None, :]).ravel()
 
-    def _exchange(self, vec, add: bool):
+    def start(self, vec):
+        """Pack the send buffers and post the grouped P2P operations (non-blocking)."""
         import torch
         import torch.distributed as dist
 
@@ -250,9 +256,12 @@ class HaloExchange:
                 ops.append(dist.P2POp(dist.isend, self.sbuf[p], p))
             if len(self.rbuf[p]):
                 ops.append(dist.P2POp(dist.irecv, self.rbuf[p], p))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def finish(self, reqs, vec, add: bool):
+        """Wait for the posted operations and unpack into ``vec`` (overwrite or accumulate)."""
+        for req in reqs:
+            req.wait()
         for p in self.peers:
             if len(self.rbuf[p]):
                 if add:
@@ -262,11 +271,11 @@ class HaloExchange:
 
     def forward(self, vec):
         """Owners -> ghost copies (overwrite)."""
-        self._exchange(vec, add=False)
+        self.finish(self.start(vec), vec, add=False)
 
     def reverse_add(self, vec):
         """Ghost partials -> owners (accumulate)."""
-        self._exchange(vec, add=True)
+        self.finish(self.start(vec), vec, add=True)
 
 
 # --------------------------------------------------------------------------- operators
@@ -325,6 +334,20 @@ class DistributedCgOperator:
 
     kernel_events = None   # set to a list to record (start, end) CUDA events of the local apply
 
+    def _event_pair(self):
+        if self.kernel_events is None:
+            return None
+        import torch
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        return (e0, e1)
+
+    def _close_events(self, ev):
+        if ev is not None:
+            ev[1].record()
+            self.kernel_events.append(ev)
+
     def _timed_local(self):
         if self.kernel_events is None:
             self._local(self.u_loc, self.y_loc)
@@ -338,10 +361,26 @@ class DistributedCgOperator:
         self.kernel_events.append((e0, e1))
 
     def apply(self, u_owned, out=None):
+        """Forward halo overlapped with the interior cells (no ghost DoF), then the
+        boundary cells, the identity rows and the additive reverse halo."""
+        from . import _lib
+
         n = self.sub.n_owned
         self.u_loc[:n].copy_(u_owned)
-        self.fwd.forward(self.u_loc)
-        self._timed_local()
+        reqs = self.fwd.start(self.u_loc)
+        if self.local_op is None:           # external local apply (tests): no stages
+            self.fwd.finish(reqs, self.u_loc, add=False)
+            self._timed_local()
+        else:
+            op, st = self.local_op, _stream_of(self.u_loc)
+            up, yp = self.u_loc.data_ptr(), self.y_loc.data_ptr()
+            ev = self._event_pair()
+            op.apply_stages(up, yp, _lib.STAGE_ZERO | _lib.STAGE_CELLS, 0, self.sub.n_interior_cells, st)
+            self._close_events(ev)
+            self.fwd.finish(reqs, self.u_loc, add=False)
+            ev = self._event_pair()
+            op.apply_stages(up, yp, _lib.STAGE_CELLS | _lib.STAGE_FIXUP, self.sub.n_interior_cells, None, st)
+            self._close_events(ev)
         self.rev.reverse_add(self.y_loc)
         if out is None:
             return self.y_loc[:n].clone()
@@ -422,10 +461,22 @@ class DistributedDgOperator:
         return (c[:, None] * self.block + np.arange(self.block)[None, :]).ravel()
 
     def apply(self, u_owned, out=None):
+        """Forward halo overlapped with the owned cells' volume terms (ghost cells'
+        volume terms are never needed), then all face terms."""
+        from . import _lib
+
         n = self.n_owned
         self.u_loc[:n].copy_(u_owned)
-        self.fwd.forward(self.u_loc)
-        self._local(self.u_loc, self.y_loc)
+        reqs = self.fwd.start(self.u_loc)
+        if self.local_op is None:
+            self.fwd.finish(reqs, self.u_loc, add=False)
+            self._local(self.u_loc, self.y_loc)
+        else:
+            op, st = self.local_op, _stream_of(self.u_loc)
+            up, yp = self.u_loc.data_ptr(), self.y_loc.data_ptr()
+            op.apply_stages(up, yp, _lib.STAGE_CELLS, 0, self.sub.n_owned_cells, st)
+            self.fwd.finish(reqs, self.u_loc, add=False)
+            op.apply_stages(up, yp, _lib.STAGE_FACES, 0, 0, st)
         if out is None:
             return self.y_loc[:n].clone()
         out.copy_(self.y_loc[:n])

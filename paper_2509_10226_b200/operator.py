@@ -246,6 +246,13 @@ class _B200Operator:
         _lib.check(_lib.lib().tmf_apply_host_async(self._plan, C.c_void_p(up), C.c_void_p(yp), C.c_void_p(stream)))
         self._count()
 
+    def apply_stages(self, u_ptr: int, y_ptr: int, stages: int, cell_begin: int = 0, cell_end: int | None = None,
+                     stream: int = 0):
+        """Part of the apply (``_lib.STAGE_*`` bits) on cells [cell_begin, cell_end)."""
+        end = len(self.mesh.cells) if cell_end is None else cell_end
+        _lib.check(_lib.lib().tmf_apply_stages(self._plan, C.c_void_p(u_ptr), C.c_void_p(y_ptr), int(stages),
+                                                int(cell_begin), int(end), C.c_void_p(stream)))
+
     def apply_into(self, u_ptr: int, y_ptr: int, stream: int = 0):
         """Raw device-pointer apply (y overwritten), ordered on ``stream``."""
         _lib.check(_lib.lib().tmf_apply(self._plan, C.c_void_p(u_ptr), C.c_void_p(y_ptr), C.c_void_p(stream)))

@@ -198,3 +198,23 @@ def test_partition_is_balanced_and_deterministic():
         assert counts.max() - counts.min() <= 1
     with pytest.raises(ValueError):
         DD.partition_cells(m, 3)
+
+
+def test_cg_subdomain_interior_cells_touch_no_ghosts():
+    """Cells [0, n_interior) are applied while the forward halo is in flight, so they
+    must not read any ghost DoF; together the subdomains cover every cell once."""
+    from paper_2509_10226_b200 import distributed as DD, dofmap as D, mesh as M
+
+    m = M.kuhn_cube_mesh(5, seed=2)
+    dm = D.build_dof_map(m, 2, "cg", 1, (0, 1))
+    part = DD.partition_cells(m, 4)
+    seen = []
+    for r in range(4):
+        sub = DD.build_cg_subdomain(m, dm.cell_dofs, dm.dirichlet_mask, part, r, 4)
+        ni = sub.n_interior_cells
+        assert 0 < ni < len(sub.cell_dofs)
+        assert np.all(sub.cell_dofs[:ni] < sub.n_owned)
+        assert np.any(sub.cell_dofs[ni:] >= sub.n_owned, axis=1).all()
+        assert np.array_equal(dm.cell_dofs[sub.cells_global], sub.l2g[sub.cell_dofs])
+        seen.append(sub.cells_global)
+    assert np.array_equal(np.sort(np.concatenate(seen)), np.arange(m.n_cells))
