@@ -97,6 +97,9 @@ struct tmf_plan {
   int dev = 0, n_sm = 0;
   int kind = 0, degree = 0, N = 0, Q = 0, QF = 0, nc = 1;
   int variant = 0;       // desc.flags & 0xF: cell-kernel tuning variant (0 = default)
+  bool concurrent = false;  // DG: cell and face kernels run concurrently (flags bit 12)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int face_variant = 0;  // (desc.flags >> 4) & 0xF: face-kernel tuning variant
   bool dg = false, mass = false, faces = false;
   int64_t n_cells = 0, n_verts = 0, n_scalar = 0, n_global = 0;
@@ -176,6 +179,9 @@ struct tmf_plan {
     return a;
   }
   ~tmf_plan() {
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
@@ -302,6 +308,31 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
 int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaEvent_t* ev) {
   bool ok = true;
   if (ev) TMF_CUDA(cudaEventRecord(ev[0], st));
+  if (P->dg && P->faces && P->concurrent) {
+    // DG with concurrent kernels: y = 0, then the face kernels (stream st) and the cell
+    // kernel (side stream) both accumulate with RED and fill each other's idle pipe slots
+    if (!P->side) {
+      TMF_CUDA(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+      TMF_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+      TMF_CUDA(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
+    }
+    TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
+    TMF_CUDA(cudaEventRecord(P->ev_fork, st));
+    TMF_CUDA(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
+    tmf::CellArgs ca = P->cell_args(u, y);
+    ca.accumulate = 1;
+    TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, ca, P->n_sm, P->side, nullptr, &ok, P->variant));
+    if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
+    TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
+                              P->face_variant));
+    TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
+                              P->face_variant));
+    TMF_CUDA(cudaEventRecord(P->ev_join, P->side));
+    TMF_CUDA(cudaStreamWaitEvent(st, P->ev_join, 0));
+    if (ev) TMF_CUDA(cudaEventRecord(ev[2], st));
+    if (ev) TMF_CUDA(cudaEventRecord(ev[3], st));
+    return TMF_OK;
+  }
   if (!P->dg) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
   TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y), P->n_sm, st, nullptr, &ok,
                             P->variant));
@@ -398,6 +429,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   P->kind = d->operator_kind;
   P->variant = d->flags & 0xF;
   P->face_variant = (d->flags >> 4) & 0xF;
+  P->concurrent = (d->flags >> 12) & 1;
   P->degree = d->degree;
   P->N = d->n_dofs_per_cell;
   P->Q = d->n_q;

@@ -40,6 +40,7 @@ struct CellArgs {
   const double* __restrict__ frags;  // B1 then B2 fragments (global; staged to smem)
   int64_t n_cells;
   int nc;                          // interleaved components
+  int accumulate;                  // DG: add into y (concurrent face kernel) instead of storing
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the
@@ -248,7 +249,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
           const int j = 8 * nj + 2 * q4 + i;
           if (j < N) {
             if (DG) {
-              a.y[(cell[m] * N + j) * a.nc + comp] = yacc[m][nj][i];
+              double* dst = a.y + (cell[m] * N + j) * a.nc + comp;
+              if (a.accumulate)
+                atomicAdd(dst, yacc[m][nj][i]);
+              else
+                *dst = yacc[m][nj][i];
             } else {
               const int64_t g = __ldg(a.dofs + cell[m] * N + j);
               if (g >= 0) atomicAdd(a.y + g * a.nc + comp, yacc[m][nj][i]);

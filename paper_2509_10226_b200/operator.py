@@ -54,6 +54,7 @@ class OperatorConfig:
     kernel_variant: int = 0     # B200 cell-kernel tuning variant (0 = default)
     face_variant: int = 0       # B200 face-kernel tuning variant (0 = default)
     face_chunk: int = 0         # 8-face batches per CTA chunk, multiple of 8 up to 120 (0 = default 32)
+    concurrent_dg: bool = False  # DG: run the cell and face kernels concurrently (accumulating)
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -180,7 +181,8 @@ class _B200Operator:
         d.device = int(self.config.device)
         d.flags = (int(getattr(self.config, "kernel_variant", 0)) & 0xF) | \
             ((int(getattr(self.config, "face_variant", 0)) & 0xF) << 4) | \
-            ((int(getattr(self.config, "face_chunk", 0)) // 8 & 0xF) << 8)
+            ((int(getattr(self.config, "face_chunk", 0)) // 8 & 0xF) << 8) | \
+            ((1 if getattr(self.config, "concurrent_dg", False) else 0) << 12)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))

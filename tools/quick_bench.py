@@ -22,13 +22,13 @@ def run(kind, p, n, reps=20, variant=0):
     elif kind == "dg":
         dm = D.build_dof_map(m, p, "dg")
         A = op.DgSipgOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n),
-                              op.OperatorConfig(kernel_variant=variant & 0xF, face_variant=(variant >> 4) & 0xF, face_chunk=(variant >> 8) * 8),
+                              op.OperatorConfig(kernel_variant=variant & 0xF, face_variant=(variant >> 4) & 0xF, face_chunk=((variant >> 8) & 0xF) * 8, concurrent_dg=bool(variant >> 12)),
                               dirichlet_ids=range(6))
     else:
         dm = D.build_dof_map(m, p, "dg")
         kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
         A = op.KappaHelmholtzOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n), kap, 1.0,
-                                      op.OperatorConfig(kernel_variant=variant & 0xF, face_variant=(variant >> 4) & 0xF, face_chunk=(variant >> 8) * 8),
+                                      op.OperatorConfig(kernel_variant=variant & 0xF, face_variant=(variant >> 4) & 0xF, face_chunk=((variant >> 8) & 0xF) * 8, concurrent_dg=bool(variant >> 12)),
                                       dirichlet_ids=range(6))
     setup = time.time() - t0
     nd = A.n_global_dofs
