@@ -56,16 +56,20 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
     if (variant == 5) return launch_cell_v<N, Q, MASS, DG, BLOCK, 1, 1, true>(a, n_sm, st, info);
     if (variant == 6) return launch_cell_v<N, Q, MASS, DG, BLOCK, 3, 1>(a, n_sm, st, info);
     if (variant == 7) return launch_cell_v<N, Q, MASS, DG, 128, 2, 1>(a, n_sm, st, info);
-    if (variant == 8) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
     if (variant == 9) return launch_cell_v<N, Q, MASS, DG, 384, 0, 1>(a, n_sm, st, info);
-    if (variant == 10) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
-    if (variant == 11) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
     if (variant == 12) return launch_cell_v<N, Q, MASS, DG, 768, 1, 1>(a, n_sm, st, info);
   }
-  // CG P3 / P4: one large CTA per SM (one staged table copy, 24 / 20 warps) measured
-  // 5.6 % / 1.4 % faster than the smem-limited default (tools/quick_bench.py variants 8, 10)
-  if (!DG && !MASS && N == 20) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
-  if (!DG && !MASS && N == 35) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
+  // block-size variants for every kernel family (registers are capped by the bounds)
+  if (variant == 8) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
+  if (variant == 10) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
+  if (variant == 11) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
+  // One large CTA per SM (a single staged table copy, more warps than the smem-limited
+  // default allows), measured with tools/quick_bench.py variants 8/10/11:
+  //   P3 (CG and DG) 768 threads: -5.6 % / -5 %;  CG P4 640: -1.4 %;
+  //   DG P2 512: -26 %, Helmholtz P2 512: -17 %;  CG P2 keeps 2 tiles per warp at 256.
+  if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
+  if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
+  if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
   return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1>(a, n_sm, st, info);
 }
 
