@@ -209,8 +209,8 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 }
 
 // PF: prefetch depth (0 none, 1 face record, 2 record + geometry + gathered u); MINB: CTAs/SM hint
-template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2>
-__global__ void __launch_bounds__(256, MINB) face_apply_kernel(FaceArgs a) {
+template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256>
+__global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;

@@ -97,11 +97,11 @@ cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& 
   return cudaSuccess;
 }
 
-template <int N, int QF, bool BND, int PF = 2, int MINB = 2>
+template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShape<N, QF>;
   constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
-  auto kern = face_apply_kernel<N, QF, BND, PF, MINB>;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK>;
   static int configured = 0;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -115,14 +115,14 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
     return cudaSuccess;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, SMEM);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, SMEM);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t work = a.n_chunks * a.nc;
   if (work == 0) return cudaSuccess;
   int64_t blocks = (int64_t)n_sm * per_sm;
   if (blocks > work) blocks = work;
-  kern<<<(unsigned)blocks, 256, SMEM, st>>>(a);
+  kern<<<(unsigned)blocks, BLOCK, SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -135,6 +135,10 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   if (variant == 2) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
   if (variant == 3) return launch_face_v<N, QF, BND, 1, 2>(a, n_sm, st, info);
   if (variant == 4) return launch_face_v<N, QF, BND, 2, 2>(a, n_sm, st, info);
+  if (variant == 5) return launch_face_v<N, QF, BND, 1, 1, 512>(a, n_sm, st, info);
+  if (variant == 6) return launch_face_v<N, QF, BND, 2, 1, 512>(a, n_sm, st, info);
+  if (variant == 7) return launch_face_v<N, QF, BND, 1, 1, 768>(a, n_sm, st, info);
+  if (variant == 8) return launch_face_v<N, QF, BND, 1, 2, 384>(a, n_sm, st, info);
   // default: low degrees have short batches -> occupancy beats prefetch depth (measured
   // at P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the fully prefetching 2-CTA kernel
   if (N <= 10) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);

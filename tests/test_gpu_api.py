@@ -109,3 +109,75 @@ def test_gpu_csr_baseline_matches_reference_csr(name):
     mesh, dofmap, geo, basis = fixture_objects(g)
     A = CsrOperator(mesh, dofmap, geo, basis)
     assert rel_l2(A.apply(g["u"]), g["y_csr"]) <= 1e-12
+
+
+def _single_tet_problem(p, space):
+    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+
+    v = np.array([[0.1, 0.0, 0.0], [1.0, 0.2, 0.0], [0.0, 1.1, 0.1], [0.2, 0.1, 0.9]])
+    cells = np.array([[0, 1, 2, 3]], dtype=np.int32)
+    ifc, bfc = M.build_faces(cells, v, lambda c: np.arange(len(c)) % 6)
+    m = M.TetMesh(v, cells, ifc, bfc)
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    geo = GeometryData("affine", cr, fr, None, None, None, None)
+    return m, D.build_dof_map(m, p, space), geo, bas
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_single_cell_edge_case(p):
+    """One cell: 1 tile with 7 padded slots, no interior faces, 4 boundary faces."""
+    from oracle import ref_apply
+    from paper_2509_10226_b200 import operator as op
+
+    m, dm, geo, bas = _single_tet_problem(p, "cg")
+    u = np.random.default_rng(p).uniform(-1, 1, dm.n_global_dofs)
+    y = op.CgPoissonOperator(m, dm, geo, bas).apply(u)
+    ref = ref_apply.cg_apply(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask, bas.grad_matrix,
+                             geo.cell_rule.weights, u)
+    assert rel_l2(y, ref) <= 1e-12
+    m, dm, geo, bas = _single_tet_problem(p, "dg")
+    sipg = op.SipgConfig(1.0, np.zeros(0), np.full(4, 10.0))
+    y = op.DgSipgOperator(m, dm, geo, bas, sipg, dirichlet_ids=(1, 3)).apply(u)
+    ref = ref_apply.dg_apply(m.vertices, m.cells, dm.n_dofs_per_cell, m.interior_faces, m.boundary_faces, {1, 3},
+                             bas.value_matrix, bas.grad_matrix, geo.cell_rule.weights, bas.face_values,
+                             bas.face_grads, geo.face_rule.weights, np.zeros(0), np.full(4, 10.0), u)
+    assert rel_l2(y, ref) <= 1e-12
+
+
+def test_all_dofs_constrained_is_identity():
+    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, operator as op, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+
+    m = M.kuhn_cube_mesh(1, seed=0)   # every vertex is on the boundary
+    cr, fr = Q.make_cell_quadrature(1), Q.make_face_quadrature(1)
+    dm = D.build_dof_map(m, 1, "cg", 1, tuple(range(6)))
+    assert dm.dirichlet_mask.all()
+    A = op.CgPoissonOperator(m, dm, GeometryData("affine", cr, fr, None, None, None, None),
+                             B.tabulate_basis(1, cr, fr))
+    u = np.arange(dm.n_global_dofs, dtype=np.float64)
+    assert np.array_equal(A.apply(u), u)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5])
+def test_ragged_tile_counts(n):
+    """Cell counts that are not multiples of the 8-cell tile / 2-tile super-tile."""
+    from oracle import ref_apply
+    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, operator as op, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+
+    m = M.kuhn_cube_mesh(n, seed=9)
+    m = M.TetMesh(m.vertices, m.cells[:-3], *M.build_faces(m.cells[:-3], m.vertices, M.cube_boundary_ids))
+    for p in (1, 2, 3):
+        cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+        bas = B.tabulate_basis(p, cr, fr)
+        geo = GeometryData("affine", cr, fr, None, None, None, None)
+        dm = D.build_dof_map(m, p, "cg")
+        used = np.zeros(dm.n_scalar_dofs, bool)
+        used[dm.cell_dofs.ravel()] = True
+        u = np.random.default_rng(p).uniform(-1, 1, dm.n_global_dofs) * used
+        y = op.CgPoissonOperator(m, dm, geo, bas).apply(u)
+        ref = ref_apply.cg_apply(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask, bas.grad_matrix,
+                                 geo.cell_rule.weights, u)
+        assert rel_l2(y, ref) <= 1e-12
