@@ -197,13 +197,16 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
       } else {
         tau *= km;
       }
+      // pre-scaled record: interior h+- = s m~+- / 2, boundary h = s m~;  out[6] = s tau
+      const double sc = area2 * a.scale;
+      const double hs = BOUNDARY ? sc : 0.5 * sc;
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        out[i] = mm[i] * km;
-        out[3 + i] = mp[i];
+        out[i] = hs * mm[i] * km;
+        out[3 + i] = hs * mp[i];
       }
-      out[6] = area2 * a.scale;
-      out[7] = tau;
+      out[6] = sc * tau;
+      out[7] = 0.0;
     }
   }
 }
@@ -289,9 +292,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
         am[kk] = nam[kk];
         ap[kk] = nap[kk];
       }
-      const double mm[3] = {ng[0], ng[1], ng[2]};
-      const double mp[3] = {ng[3], ng[4], ng[5]};
-      const double s = ng[6], tau = ng[7];
+      const double hm[3] = {ng[0], ng[1], ng[2]};   // s m~- / 2   (boundary: s m~)
+      const double hp[3] = {ng[3], ng[4], ng[5]};   // s m~+ / 2
+      const double stau = ng[6];                     // s tau
       if (PF >= 1) fetch_rec(bi + nwb);
       if (PF == 2) fetch_data(bi + nwb);
 
@@ -313,24 +316,29 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
             dmma(vm[h], am[kk], Fm[f]);
             if (!BOUNDARY) dmma(vp[h], ap[kk], Fp[f]);
           }
+        // face_qpoint / boundary_qpoint (numpy_backend.py:91-119) with s, 1/2 and m~
+        // folded into the per-face record: 14 (interior) / 7 (boundary) FP64 ops per point
         double qm[4], qp[4];
-        const double dnm = mm[0] * vm[0][1] + mm[1] * vm[1][0] + mm[2] * vm[1][1];
         if (BOUNDARY) {
-          qm[0] = s * (tau * vm[0][0] - dnm);
-          const double wj = -s * vm[0][0];
+          const double v = vm[0][0];
+          qm[0] = fma(stau, v, -(hm[0] * vm[0][1] + hm[1] * vm[1][0] + hm[2] * vm[1][1]));
 #pragma unroll
-          for (int k = 0; k < 3; ++k) qm[1 + k] = wj * mm[k];
+          for (int k = 0; k < 3; ++k) qm[1 + k] = -v * hm[k];
         } else {
-          const double dnp = mp[0] * vp[0][1] + mp[1] * vp[1][0] + mp[2] * vp[1][1];
-          const double jump = vm[0][0] - vp[0][0];
-          const double qv = s * (tau * jump - 0.5 * (dnm + dnp));
-          const double hw = -0.5 * s * jump;
+          const double nj = vp[0][0] - vm[0][0];   // -[[u]]
+          double qv = -stau * nj;
+          qv = fma(-hm[0], vm[0][1], qv);
+          qv = fma(-hm[1], vm[1][0], qv);
+          qv = fma(-hm[2], vm[1][1], qv);
+          qv = fma(-hp[0], vp[0][1], qv);
+          qv = fma(-hp[1], vp[1][0], qv);
+          qv = fma(-hp[2], vp[1][1], qv);
           qm[0] = qv;
           qp[0] = -qv;
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
-            qm[1 + k] = hw * mm[k];
-            qp[1 + k] = hw * mp[k];
+            qm[1 + k] = nj * hm[k];
+            qp[1 + k] = nj * hp[k];
           }
         }
 #pragma unroll
