@@ -212,7 +212,10 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 }
 
 // PF: prefetch depth (0 none, 1 face record, 2 record + geometry + gathered u); MINB: CTAs/SM hint
-template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256>
+// BLOCKED: each CTA takes a contiguous run of chunks (consecutive chunks of one
+// (window, signature) group share their tables, so restaging and both barriers are
+// skipped); otherwise chunks are dealt round-robin.
+template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
   extern __shared__ __align__(16) double smem[];
@@ -222,9 +225,19 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   const int warp = threadIdx.x >> 5;
   const int nwb = blockDim.x >> 5;
 
-  for (int64_t w = blockIdx.x; w < a.n_chunks * a.nc; w += gridDim.x) {
+  const int64_t nwork = a.n_chunks * a.nc;
+  const int64_t per = (nwork + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = BLOCKED ? blockIdx.x * per : blockIdx.x;
+  const int64_t w1 = BLOCKED ? (w0 + per < nwork ? w0 + per : nwork) : nwork;
+  const int64_t wstep = BLOCKED ? 1 : gridDim.x;
+  int cur_x = -1, cur_y = -2;
+  for (int64_t w = w0; w < w1; w += wstep) {
     const int comp = (int)(w / a.n_chunks);
     const int4 ch = __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
+    const bool restage = ch.x != cur_x || ch.y != cur_y;
+    cur_x = ch.x;
+    cur_y = ch.y;
+    if (restage) {
     __syncthreads();  // previous chunk's warps are done with the staged tables
     {
       const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.x * S::NFRAG * 32);
@@ -236,6 +249,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
       }
     }
     __syncthreads();
+    }
     const double* Fm = smem;
     const double* Fp = smem + S::NFRAG * 32;
     const int* perm_m = a.perm + (ch.x / 6) * N;                  // gather order, minus side

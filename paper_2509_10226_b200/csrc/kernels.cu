@@ -97,11 +97,11 @@ cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& 
   return cudaSuccess;
 }
 
-template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256>
+template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShape<N, QF>;
   constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
-  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK>;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED>;
   static int configured = 0;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -126,7 +126,7 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
   return cudaGetLastError();
 }
 
-// variant: 0 = default (by degree, below); 1 = no prefetch, 3 CTAs/SM;
+// variant: 0 = default (by degree, below, blocked chunk runs); 1 = no prefetch, 3 CTAs/SM;
 // 2 = record prefetch, 3 CTAs/SM; 3 = record prefetch, 2 CTAs/SM; 4 = full prefetch, 2 CTAs/SM
 template <int N, int QF, bool BND>
 static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info,
@@ -139,10 +139,14 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   if (variant == 6) return launch_face_v<N, QF, BND, 2, 1, 512>(a, n_sm, st, info);
   if (variant == 7) return launch_face_v<N, QF, BND, 1, 1, 768>(a, n_sm, st, info);
   if (variant == 8) return launch_face_v<N, QF, BND, 1, 2, 384>(a, n_sm, st, info);
-  // default: low degrees have short batches -> occupancy beats prefetch depth (measured
-  // at P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the fully prefetching 2-CTA kernel
-  if (N <= 10) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
-  return launch_face_v<N, QF, BND, 2, 2>(a, n_sm, st, info);
+  if (variant == 9) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
+  if (variant == 10) return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
+  // default: contiguous chunk runs per CTA (tables restaged only when the signature
+  // changes: -7 % / -8 % at P3 / P2); low degrees have short batches, so occupancy
+  // beats prefetch depth (P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the fully
+  // prefetching 2-CTA kernel
+  if (N <= 10) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
+  return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
 }
 
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
