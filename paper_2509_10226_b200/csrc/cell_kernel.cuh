@@ -96,7 +96,9 @@ struct CellShape {
 
 // MT_: tiles per warp iteration (0 = CellShape default); MINB: min CTAs/SM hint;
 // PF: software-prefetch the next super-tile's gathered u and geometry (indices 2 ahead)
-template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT_ = 0, int MINB = 1, bool PF = false>
+// BLK: each warp takes a contiguous run of super-tiles instead of a grid-strided set
+template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT_ = 0, int MINB = 1, bool PF = false,
+          bool BLK = false>
 __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   using S = CellShape<N, Q, MASS>;
   constexpr int MT = MT_ ? MT_ : S::MT;
@@ -121,7 +123,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   // Index prefetch: the DoF indices of the warp's next super-tile are loaded
   // while the current one computes, so each start pays one memory round trip
   // (u and the per-cell geometry, issued together) instead of two.
-  int64_t st = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+  const int64_t per = (nst + nwarps - 1) / nwarps;
+  int64_t st = BLK ? gw * per : gw;
+  const int64_t st_end = BLK ? (st + per < nst ? st + per : nst) : nst;
+  const int64_t step = BLK ? 1 : nwarps;
   int nidx[MT][S::KK];
   auto load_indices = [&](int64_t t) {
     const int cmp = (int)(t / cst);
@@ -160,10 +166,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   double pav[MT][S::KK], pG[MT][6], pmdet[MT];
   if (PF) {
     load_data(st, pav, pG, pmdet);
-    load_indices(st + nwarps);
+    load_indices(st + step);
   }
 
-  for (; st < nst; st += nwarps) {
+  for (; st < st_end; st += step) {
     const int comp = (int)(st / cst);
     int64_t cell[MT];
     bool valid[MT];
@@ -184,11 +190,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
         for (int i = 0; i < 6; ++i) G[m][i] = pG[m][i];
         mdet[m] = pmdet[m];
       }
-      load_data(st + nwarps, pav, pG, pmdet);
-      load_indices(st + 2 * nwarps);
+      load_data(st + step, pav, pG, pmdet);
+      load_indices(st + 2 * step);
     } else {
       load_data(st, av, G, mdet);
-      load_indices(st + nwarps);
+      load_indices(st + step);
     }
 
     double yacc[MT][S::NJ][2];
