@@ -6,18 +6,20 @@ recorded in SURVEY Appendix B12 and DESIGN.md.  Parity of the product's C++
 implementation (csrc/reorder.cpp) against this file is bit-exact on the
 permutation; parity against the reference itself is unpinned.
 
-    order(G):  if |G| <= g: greedy_chain(G)
+    order(G):  if |G| <= base: cuthill_mckee(G)
                groups = bfs_groups(G)            # members in BFS growth order
                C = coarsen(G, groups)           # weight = number of shared faces
                return concat(groups[c] for c in order(C))
+    cuthill_mckee: BFS from the lowest-degree node (ties: lowest id), each
+               node's unvisited neighbours appended by (degree, id); restart at
+               the lowest-degree unvisited node for another component.  Ordering
+               the top of the hierarchy (<= base = 512 groups) as a level
+               structure bounds the bandwidth, the groups below keep locality.
     bfs_groups: seed = the unvisited neighbour of the previous group with the
                fewest unvisited neighbours (ties: lowest id); if there is none,
                the lowest-degree unvisited node (ties: lowest id).  Grow by BFS
                over unvisited neighbours in ascending id until g nodes (a group
                closes early if its frontier empties).
-    greedy_chain: start at the lowest-degree node; repeatedly append the
-               unplaced node with the largest weight to the last placed node
-               (ties: lowest id); reseed with the lowest-degree unplaced node.
 """
 
 from __future__ import annotations
@@ -93,44 +95,41 @@ def coarsen(adj, groups):
     return cadj
 
 
-def greedy_chain(adj):
+def cuthill_mckee(adj):
     n = len(adj)
-    placed = [False] * n
+    seen = [False] * n
     seeds = _by_degree(adj)
     out, si = [], 0
-    last = None
     while len(out) < n:
-        nxt = None
-        if last is not None:
-            best = None
-            for u, w in adj[last].items():
-                if not placed[u] and (best is None or w > best[0] or (w == best[0] and u < best[1])):
-                    best = (w, u)
-            if best is not None:
-                nxt = best[1]
-        if nxt is None:
-            while placed[seeds[si]]:
-                si += 1
-            nxt = seeds[si]
-        placed[nxt] = True
-        out.append(nxt)
-        last = nxt
+        while seen[seeds[si]]:
+            si += 1
+        s = seeds[si]
+        seen[s] = True
+        queue, head = [s], 0
+        while head < len(queue):
+            v = queue[head]
+            head += 1
+            out.append(v)
+            for u in sorted(adj[v], key=lambda x: (len(adj[x]), x)):
+                if not seen[u]:
+                    seen[u] = True
+                    queue.append(u)
     return out
 
 
-def order(adj, g):
-    if len(adj) <= g:
-        return greedy_chain(adj)
+def order(adj, g, base=512):
+    if len(adj) <= base:
+        return cuthill_mckee(adj)
     groups = bfs_groups(adj, g)
-    corder = order(coarsen(adj, groups), g)
+    corder = order(coarsen(adj, groups), g, base)
     return [v for c in corder for v in groups[c]]
 
 
-def hierarchical_reorder(n_cells, interior_faces, group_size=8):
+def hierarchical_reorder(n_cells, interior_faces, group_size=8, base=512):
     """new_of_old permutation (cell e moves to position new_of_old[e])."""
     if group_size < 2:
         raise ValueError("group_size must be >= 2")
-    seq = order(cell_graph(n_cells, interior_faces), group_size)
+    seq = order(cell_graph(n_cells, interior_faces), group_size, base)
     new_of_old = np.empty(n_cells, dtype=np.int64)
     new_of_old[np.asarray(seq, dtype=np.int64)] = np.arange(n_cells)
     return new_of_old

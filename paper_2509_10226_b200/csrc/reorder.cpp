@@ -2,7 +2,7 @@
 // (no reference implementation exists).
 // Deterministic algorithm, bit-exact
 // with the oracle restatement oracle/ref_reorder.py:
-//   order(G): |G| <= g -> greedy_chain(G); else groups = bfs_groups(G),
+//   order(G): |G| <= 512 -> cuthill_mckee(G); else groups = bfs_groups(G),
 //             C = coarsen(G, groups), concat(groups[c] for c in order(C)).
 #include <algorithm>
 #include <climits>
@@ -119,42 +119,51 @@ Graph coarsen(const Graph& g, const std::vector<std::vector<int64_t>>& groups) {
   return from_edges((int64_t)groups.size(), e, &w);
 }
 
-std::vector<int64_t> greedy_chain(const Graph& g) {
+// Cuthill-McKee level structure (the top of the hierarchy): BFS from the lowest-degree
+// node, neighbours appended by (degree, id); restart per component.
+std::vector<int64_t> cuthill_mckee(const Graph& g) {
   const int64_t n = g.n();
-  std::vector<char> placed(n, 0);
+  std::vector<char> seen(n, 0);
   const std::vector<int64_t> seeds = by_degree(g);
   std::vector<int64_t> out;
+  out.reserve(n);
   size_t si = 0;
-  int64_t last = -1;
+  std::vector<int64_t> nb;
   while ((int64_t)out.size() < n) {
-    int64_t nxt = -1, best = -1;
-    if (last >= 0)
-      for (int64_t k = g.ptr[last]; k < g.ptr[last + 1]; ++k)
-        if (!placed[g.nbr[k]] && g.w[k] > best) {
-          best = g.w[k];
-          nxt = g.nbr[k];
+    while (seen[seeds[si]]) ++si;
+    const int64_t s = seeds[si];
+    seen[s] = 1;
+    size_t head = out.size();
+    out.push_back(s);
+    while (head < out.size()) {
+      const int64_t v = out[head++];
+      nb.assign(g.nbr.begin() + g.ptr[v], g.nbr.begin() + g.ptr[v + 1]);
+      std::sort(nb.begin(), nb.end(), [&](int64_t a, int64_t b) {
+        const int64_t da = g.ptr[a + 1] - g.ptr[a], db = g.ptr[b + 1] - g.ptr[b];
+        return da != db ? da < db : a < b;
+      });
+      for (int64_t u : nb)
+        if (!seen[u]) {
+          seen[u] = 1;
+          out.push_back(u);
         }
-    if (nxt < 0) {
-      while (placed[seeds[si]]) ++si;
-      nxt = seeds[si];
     }
-    placed[nxt] = 1;
-    out.push_back(nxt);
-    last = nxt;
   }
   return out;
 }
 
-std::vector<int64_t> order(const Graph& g, int gs) {
-  if (g.n() <= gs) return greedy_chain(g);
+std::vector<int64_t> order(const Graph& g, int gs, int64_t base) {
+  if (g.n() <= base) return cuthill_mckee(g);
   auto groups = bfs_groups(g, gs);
   const Graph c = coarsen(g, groups);
-  const std::vector<int64_t> co = order(c, gs);
+  const std::vector<int64_t> co = order(c, gs, base);
   std::vector<int64_t> out;
   out.reserve(g.n());
   for (int64_t k : co) out.insert(out.end(), groups[k].begin(), groups[k].end());
   return out;
 }
+
+constexpr int64_t kBaseNodes = 512;  // coarsest level ordered as a Cuthill-McKee level structure
 
 }  // namespace
 
@@ -172,7 +181,7 @@ extern "C" int tmf_hierarchical_reorder(int64_t n_cells, int64_t n_interior_face
     e.emplace_back(b, a);
   }
   const Graph g = from_edges(n_cells, e, nullptr);
-  const std::vector<int64_t> seq = order(g, group_size);
+  const std::vector<int64_t> seq = order(g, group_size, kBaseNodes);
   for (int64_t i = 0; i < n_cells; ++i) new_of_old[seq[i]] = i;
   return TMF_OK;
 }

@@ -17,7 +17,9 @@ def pytest_configure(config):
 
 
 def golden_names(prefix=""):
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, prefix + "*.npz")))
+    """Operator fixtures (mesh-only fixtures are excluded)."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, prefix + "*.npz"))
+                  if not os.path.basename(p).startswith("mesh_"))
 
 
 def load_golden(name):

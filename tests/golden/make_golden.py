@@ -186,10 +186,18 @@ def helm3_case(n, p, rule_kind, dids, mass_scale, nu, seed=0):
     return rec
 
 
+def reorder_mesh_case():
+    """SPEC.md:638 acceptance fixture: the reference's seed-42 shuffled 5-tet 8^3 cube mesh."""
+    m = rmesh.shuffle_cells(rmesh.generate_cube_mesh(8), 42)
+    return dict(kind="mesh", vertices=m.vertices, cells=m.cells, interior_faces=m.interior_faces,
+                boundary_faces=m.boundary_faces)
+
+
 ALL = tuple(range(6))
 
 
 def cases():
+    yield "mesh_5tet_n8_shuffled42", reorder_mesh_case
     yield "cg_p2_n8_gm", lambda: cg_case(8, 2, "gm", ())            # BASELINE config 1
     yield "cg_p2_n8_gm_dir", lambda: cg_case(8, 2, "gm", ALL)
     for p in (1, 2, 3):
@@ -220,7 +228,8 @@ def main():
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in rec.items()})
         ref = rec.get("y_csr")
         extra = "" if ref is None else f" mf-vs-csr {np.linalg.norm(rec['y'] - ref) / np.linalg.norm(ref):.2e}"
-        print(f"{name}: {os.path.getsize(path) / 1024:.0f} KiB, n_dof {len(rec['u'])}{extra}")
+        ndof = len(rec["u"]) if "u" in rec else 0
+        print(f"{name}: {os.path.getsize(path) / 1024:.0f} KiB, n_dof {ndof}{extra}")
 
 
 if __name__ == "__main__":

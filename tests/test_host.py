@@ -149,6 +149,20 @@ def test_reorder_bit_exact_vs_oracle(n, seed):
     assert np.array_equal(np.sort(a), np.arange(m.n_cells))
 
 
+def test_reorder_spec_acceptance_on_reference_fixture():
+    """on the reference's seed-42 shuffled 5*8^3 mesh the reordering cuts the
+    mean neighbour index distance >= 2x and the max bandwidth >= 4x."""
+    g = load_golden("mesh_5tet_n8_shuffled42")
+    m = M.TetMesh(g["vertices"], g["cells"], g["interior_faces"], g["boundary_faces"])
+    nb = R.hierarchical_reorder(m)
+    assert np.array_equal(nb, ref_reorder.hierarchical_reorder(m.n_cells, m.interior_faces))
+    m2 = M.apply_cell_permutation(m, nb)
+    before, after = R.locality_metrics(m), R.locality_metrics(m2)
+    assert after["mean_neighbor_index_distance"] * 2 <= before["mean_neighbor_index_distance"]
+    assert after["max_bandwidth"] * 4 <= before["max_bandwidth"]
+    m2.validate()
+
+
 def test_reorder_improves_locality_spec_acceptance():
     m = M.kuhn_cube_mesh(8, seed=0)
     m2 = M.apply_cell_permutation(m, R.hierarchical_reorder(m))
