@@ -360,8 +360,12 @@ def main():
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29561")
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl", rank=rank, world_size=world)
+        dev = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(dev)
+        # eager communicator init + a collective first: batch_isend_irecv requires that all
+        # ranks take part in the first NCCL call, and halo peers are a subset of the ranks
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", dev))
+        dist.barrier()
     r = gpu_bench(args, rank, world)
     total_ms = r["total_ms"]
     if world > 1:

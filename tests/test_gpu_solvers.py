@@ -102,7 +102,8 @@ def test_distributed_operator_single_rank_on_gpu():
     os.environ.setdefault("MASTER_PORT", "29533")
     created = False
     if not dist.is_initialized():
-        dist.init_process_group("nccl", rank=0, world_size=1)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        dist.barrier()
         created = True
     try:
         m, dm, geo, bas, A = _cg(4, 2, (1, 2))
