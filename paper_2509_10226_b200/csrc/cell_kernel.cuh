@@ -97,8 +97,9 @@ struct CellShape {
 // MT_: tiles per warp iteration (0 = CellShape default); MINB: min CTAs/SM hint;
 // PF: software-prefetch the next super-tile's gathered u and geometry (indices 2 ahead)
 // BLK: each warp takes a contiguous run of super-tiles instead of a grid-strided set
+// SKEW: issue GEMM1 of the next point tile before the D action of the current one
 template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT_ = 0, int MINB = 1, bool PF = false,
-          bool BLK = false>
+          bool BLK = false, bool SKEW = false>
 __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   using S = CellShape<N, Q, MASS>;
   constexpr int MT = MT_ ? MT_ : S::MT;
@@ -203,9 +204,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
 #pragma unroll
       for (int nj = 0; nj < S::NJ; ++nj) yacc[m][nj][0] = yacc[m][nj][1] = 0.0;
 
-#pragma unroll
-    for (int t = 0; t < S::T; ++t) {
-      double v[MT][S::NC][2];
+    auto gemm1 = [&](int t, double (&v)[MT][S::NC][2]) {
 #pragma unroll
       for (int m = 0; m < MT; ++m)
 #pragma unroll
@@ -219,7 +218,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
           for (int m = 0; m < MT; ++m) dmma(v[m][c], av[m][kk], b);
         }
       }
-      // D action at the lane's two points (w_q lives in the GEMM2 table)
+    };
+    // D action at the lane's two points (w_q lives in the GEMM2 table), then GEMM2
+    auto daction_gemm2 = [&](int t, const double (&v)[MT][S::NC][2]) {
       double d[MT][S::NC][2];
 #pragma unroll
       for (int m = 0; m < MT; ++m)
@@ -242,6 +243,29 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
 #pragma unroll
             for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][c][i], b);
           }
+    };
+    if (SKEW) {
+      // skewed software pipeline: GEMM1 of point tile t+1 is issued before the D
+      // action of tile t, so the FP64-pipe D action overlaps tensor work in flight
+      double va[MT][S::NC][2], vb[MT][S::NC][2];
+      gemm1(0, va);
+#pragma unroll
+      for (int t = 0; t < S::T; ++t) {
+        if (t % 2 == 0) {
+          if (t + 1 < S::T) gemm1(t + 1, vb);
+          daction_gemm2(t, va);
+        } else {
+          if (t + 1 < S::T) gemm1(t + 1, va);
+          daction_gemm2(t, vb);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < S::T; ++t) {
+        double v[MT][S::NC][2];
+        gemm1(t, v);
+        daction_gemm2(t, v);
+      }
     }
 
     // ---- scatter / store: lane owns DoFs 8nj + 2q4 + {0,1}

@@ -9,11 +9,12 @@
 
 namespace tmf {
 
-template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PF = false, bool BLK = false>
+template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PF = false, bool BLK = false,
+          bool SKEW = false>
 static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = CellShape<N, Q, MASS>;
   constexpr int MTE = MT ? MT : S::MT;
-  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK>;
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK, SKEW>;
   static int configured = 0;  // per instantiation, per process
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
@@ -63,6 +64,12 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   if (variant == 8) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
   if (variant == 10) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
   if (variant == 11) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
+  if (variant == 14) {   // skewed GEMM1/D-action pipeline with the per-degree default CTA size
+    if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, false, true>(a, n_sm, st, info);
+    if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1, false, false, true>(a, n_sm, st, info);
+    if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1, false, false, true>(a, n_sm, st, info);
+    return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, false, false, true>(a, n_sm, st, info);
+  }
   if (variant == 13) {   // blocked tile runs with the per-degree default CTA size
     if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, true>(a, n_sm, st, info);
     if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1, false, true>(a, n_sm, st, info);
@@ -73,6 +80,9 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   // default allows), measured with tools/quick_bench.py variants 8/10/11:
   //   P3 (CG and DG) 768 threads: -5.6 % / -5 %;  CG P4 640: -1.4 %;
   //   DG P2 512: -26 %, Helmholtz P2 512: -17 %;  CG P2 keeps 2 tiles per warp at 256.
+  //   CG P3 additionally skews GEMM1(t+1) ahead of the D action of tile t (-2.7 %;
+  //   slower for the other families, variant 14)
+  if (N == 20 && !MASS && !DG) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, false, true>(a, n_sm, st, info);
   if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
   if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
   if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
