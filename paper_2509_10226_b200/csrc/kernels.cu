@@ -9,18 +9,29 @@
 
 namespace tmf {
 
+// Dynamic shared memory above 48 KB needs a per-kernel, per-DEVICE opt-in; remember
+// which devices each instantiation has been configured on.
+template <typename K>
+static cudaError_t opt_in_smem(K kern, int bytes) {
+  static unsigned long long configured = 0;   // bit d = done on device d (d < 64)
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (configured & bit) return cudaSuccess;
+  if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      e != cudaSuccess)
+    return e;
+  configured |= bit;
+  return cudaSuccess;
+}
+
 template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PF = false, bool BLK = false,
           bool SKEW = false>
 static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = CellShape<N, Q, MASS>;
   constexpr int MTE = MT ? MT : S::MT;
   auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK, SKEW>;
-  static int configured = 0;  // per instantiation, per process
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = 1;
-  }
+  if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
   if (e != cudaSuccess) return e;
@@ -118,12 +129,7 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
   using S = FaceShape<N, QF>;
   constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
   auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED>;
-  static int configured = 0;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    configured = 1;
-  }
+  if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   if (info) {
     info->nfrag = S::NFRAG;
     info->chunk = S::CHUNK;
