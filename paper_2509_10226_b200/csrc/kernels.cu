@@ -2,6 +2,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "cell_kernel.cuh"
 #include "face_kernel.cuh"
@@ -10,18 +12,22 @@
 namespace tmf {
 
 // Dynamic shared memory above 48 KB needs a per-kernel, per-DEVICE opt-in; remember
-// which devices each instantiation has been configured on.
+// which (kernel, device) pairs have been configured (kernels sharing a signature share
+// a function-pointer type, so the key is the pointer itself).
 template <typename K>
 static cudaError_t opt_in_smem(K kern, int bytes) {
-  static unsigned long long configured = 0;   // bit d = done on device d (d < 64)
+  static std::mutex mu;
+  static std::unordered_map<const void*, unsigned long long> done;  // bit d = device d (< 64)
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
   const unsigned long long bit = 1ull << (dev & 63);
-  if (configured & bit) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(mu);
+  unsigned long long& mask = done[reinterpret_cast<const void*>(kern)];
+  if (mask & bit) return cudaSuccess;
   if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       e != cudaSuccess)
     return e;
-  configured |= bit;
+  mask |= bit;
   return cudaSuccess;
 }
 
