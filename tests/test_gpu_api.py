@@ -181,3 +181,23 @@ def test_ragged_tile_counts(n):
         ref = ref_apply.cg_apply(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask, bas.grad_matrix,
                                  geo.cell_rule.weights, u)
         assert rel_l2(y, ref) <= 1e-12
+
+
+def test_c_abi_demo_runs():
+    """The plain-C demo (examples/c_abi_demo.c) passes on the GPU."""
+    import os
+    import shutil
+    import subprocess
+
+    from conftest import ROOT
+    from paper_2509_10226_b200 import _lib
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    out = os.path.join(ROOT, "examples", "c_abi_demo")
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "examples", "c_abi_demo.c"),
+                    "-L", os.path.dirname(_lib.LIB_PATH), "-ltetmf_b200",
+                    f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}", "-lm", "-o", out], check=True)
+    r = subprocess.run([out], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout

@@ -203,3 +203,18 @@ def test_native_faces_reject_nonmanifold():
     cells = np.array([[0, 1, 2, 3], [0, 1, 2, 4], [0, 1, 2, 5]], dtype=np.int32)
     with pytest.raises(ValueError):
         M.build_faces(cells)
+
+
+def test_c_abi_demo_compiles_against_header_and_library():
+    """A plain-C caller of include/tetmf_b200.h links against libtetmf_b200.so (gcc)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    out = os.path.join(ROOT, "examples", "c_abi_demo")
+    r = subprocess.run(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "c_abi_demo.c"), "-L", os.path.dirname(_lib.LIB_PATH),
+                        "-ltetmf_b200", f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}", "-lm", "-o", out],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
