@@ -78,7 +78,9 @@ typedef struct tmf_plan_desc {
   double mass_scale;           /* Helmholtz mass coefficient                          */
   double diffusivity;          /* Laplace/SIPG scale (nu)                             */
   int32_t device;              /* CUDA device ordinal                                 */
-  int32_t flags;               /* bits 0-3 / 4-7: cell / face kernel tuning variant    */
+  int32_t flags;               /* bits 0-3 / 4-7: cell / face kernel tuning variant;
+                                  8-11 face chunk/8; 12 concurrent DG; 13-14 cell engine
+                                  (0 by degree, 1 DMMA tensor cores, 2 DFMA)            */
 } tmf_plan_desc;
 
 typedef struct tmf_plan_info {

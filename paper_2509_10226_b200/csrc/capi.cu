@@ -66,6 +66,17 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
           }
 }
 
+// Point-major rows for the DFMA cell kernel (cell_dfma_kernel.cuh), row length
+// NP = N rounded up to even:  T1[q][c][j] = E_c(q, j),  T2[q][c][j] = w_q E_c(q, j)
+template <typename F>
+void build_point_rows(int N, int Q, int NC, F E, const double* w, std::vector<double>& out) {
+  const int NP = (N + 1) & ~1;
+  for (int t = 0; t < 2; ++t)
+    for (int q = 0; q < Q; ++q)
+      for (int c = 0; c < NC; ++c)
+        for (int j = 0; j < NP; ++j) out.push_back(j < N ? (t ? w[q] : 1.0) * E(c, q, j) : 0.0);
+}
+
 // Face tables in the face frame (see face_kernel.cuh), for one (lf, code) combo.
 // Components c: 0 = value, 1..3 = D_i = a_i . grad (a_0, a_1 tangent, a_2 transversal);
 // columns are DoFs in the gather order perm (face DoFs first).  Point groups of 4:
@@ -97,6 +108,7 @@ struct tmf_plan {
   int dev = 0, n_sm = 0;
   int kind = 0, degree = 0, N = 0, Q = 0, QF = 0, nc = 1;
   int variant = 0;       // desc.flags & 0xF: cell-kernel tuning variant (0 = default)
+  int engine = 0;        // (desc.flags >> 13) & 3: cell engine 0 = by degree, 1 = DMMA, 2 = DFMA
   bool concurrent = false;  // DG: cell and face kernels run concurrently (flags bit 12)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -321,7 +333,7 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
     TMF_CUDA(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     tmf::CellArgs ca = P->cell_args(u, y);
     ca.accumulate = 1;
-    TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, ca, P->n_sm, P->side, nullptr, &ok, P->variant));
+    TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, ca, P->n_sm, P->side, nullptr, &ok, P->variant, P->engine));
     if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
     TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
@@ -335,7 +347,7 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
   }
   if (!P->dg) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
   TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y), P->n_sm, st, nullptr, &ok,
-                            P->variant));
+                            P->variant, P->engine));
   if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
   if (P->faces) {
     TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
@@ -365,7 +377,7 @@ int tmf_apply_stages(tmf_plan* P, const double* u, double* y, int stages, int64_
     TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
   if ((stages & TMF_STAGE_CELLS) && cell_end > cell_begin)
     TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, cell_begin, cell_end), P->n_sm,
-                              st, nullptr, &ok, P->variant));
+                              st, nullptr, &ok, P->variant, P->engine));
   if ((stages & TMF_STAGE_FACES) && P->faces) {
     TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
@@ -428,6 +440,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   }
   P->kind = d->operator_kind;
   P->variant = d->flags & 0xF;
+  P->engine = (d->flags >> 13) & 3;
   P->face_variant = (d->flags >> 4) & 0xF;
   P->concurrent = (d->flags >> 12) & 1;
   P->degree = d->degree;
@@ -461,25 +474,27 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     const int N = P->N, Q = P->Q;
     const double* V = d->value_matrix;
     const double* Gm = d->grad_matrix;
-    std::vector<double> fr;
-    if (P->mass) {
-      build_fragments(N, Q, 4, [&](int c, int q, int j) {
-        return c == 0 ? V[q * N + j] : Gm[(3 * q + c - 1) * N + j]; }, d->cell_weights, fr);
-    } else {
-      build_fragments(N, Q, 3, [&](int c, int q, int j) { return Gm[(3 * q + c) * N + j]; },
-                      d->cell_weights, fr);
-    }
     tmf::CellLaunchInfo ci;
     bool ok = true;
     tmf::CellArgs dummy{};
     dummy.n_cells = P->n_cells;
     dummy.nc = P->nc;
-    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok, P->variant));
+    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok, P->variant, P->engine));
     if (!ok) return bail(fail(TMF_EINVAL, "unsupported (n_dofs_per_cell, n_q) = (" +
                                               std::to_string(N) + ", " + std::to_string(Q) + ")"));
+    const int NC = P->mass ? 4 : 3;
+    auto E = [&](int c, int q, int j) {
+      if (P->mass) return c == 0 ? V[q * N + j] : Gm[(3 * q + c - 1) * N + j];
+      return Gm[(3 * q + c) * N + j];
+    };
+    std::vector<double> fr;
+    if (ci.table == 0)
+      build_fragments(N, Q, NC, E, d->cell_weights, fr);
+    else
+      build_point_rows(N, Q, NC, E, d->cell_weights, fr);
     if ((int)fr.size() != ci.frag_doubles) return bail(fail(TMF_EINVAL, "internal: fragment size"));
     if ((rc = upload(&P->cell_frags, fr.data(), fr.size(), &total))) return bail(rc);
-    P->info.flops_issued = (double)ci.tiles * ci.dmma_per_tile * 512.0;
+    P->info.flops_issued = ci.flops_issued;
   }
 
   // per-cell geometry (G, mass factor), computed once on the device

@@ -1,0 +1,163 @@
+// Cell-kernel launchers: tuning variants and per-degree defaults of the DMMA
+// (cell_kernel.cuh) and DFMA (cell_dfma_kernel.cuh) engines.  Each degree is
+// instantiated in its own translation unit (cell_p*.cu) through TMF_CELL_TU so
+// the kernels compile in parallel; kernels.cu dispatches on (n_dpc, n_q).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "cell_dfma_kernel.cuh"
+#include "cell_kernel.cuh"
+#include "launch.h"
+#include "launch_common.cuh"
+
+namespace tmf {
+
+template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PF = false, bool BLK = false,
+          bool SKEW = false>
+static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
+  using S = CellShape<N, Q, MASS>;
+  constexpr int MTE = MT ? MT : S::MT;
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK, SKEW>;
+  if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t supertiles = ((a.n_cells + 8 * MTE - 1) / (8 * MTE)) * a.nc;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  const int64_t need = (supertiles + BLOCK / 32 - 1) / (BLOCK / 32);
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  if (info) {
+    info->dmma_per_tile = S::DMMA_PER_TILE;
+    info->tiles = supertiles * MTE;
+    info->block = BLOCK;
+    info->grid = (int)blocks;
+    info->smem = S::SMEM;
+    info->frag_doubles = S::NFRAG * 32;
+    info->table = 0;
+    info->flops_issued = (double)supertiles * MTE * S::DMMA_PER_TILE * 512.0;
+    return cudaSuccess;
+  }
+  kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// DFMA engine (cell_dfma_kernel.cuh): one thread per MC cells, point-major tables.
+// OVER: CTAs per SM slot launched (1 = persistent grid-stride; > 1 oversubscribes so
+// the block scheduler refills SMs as CTAs finish)
+template <int N, int Q, bool MASS, bool DG, int BLOCK, int MC, int MINB, int OVER = 1>
+static cudaError_t launch_cell_d(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
+  using S = DfmaShape<N, Q, MASS>;
+  auto kern = cell_dfma_kernel<N, Q, MASS, DG, BLOCK, MC, MINB>;
+  if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t chunks = ((a.n_cells + BLOCK * MC - 1) / (BLOCK * MC)) * a.nc;
+  int64_t blocks = (int64_t)n_sm * per_sm * OVER;
+  if (blocks > chunks) blocks = chunks;
+  if (blocks < 1) blocks = 1;
+  if (info) {
+    info->dmma_per_tile = 0;
+    info->tiles = (a.n_cells + 7) / 8 * a.nc;
+    info->block = BLOCK;
+    info->grid = (int)blocks;
+    info->smem = S::SMEM;
+    info->frag_doubles = 2 * S::TAB;
+    info->table = 1;
+    info->flops_issued = 2.0 * a.n_cells * a.nc * Q * (2.0 * S::NC * N + 9 + (MASS ? 1 : 0));
+    return cudaSuccess;
+  }
+  if (a.n_cells == 0) return cudaSuccess;
+  kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// DFMA variants (engine 2): 0 = per-degree default; 1..8 tuning (bench sweeps only)
+template <int N, int Q, bool MASS, bool DG>
+static cudaError_t launch_cell_dt(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info,
+                                  int variant) {
+  if (variant == 1) return launch_cell_d<N, Q, MASS, DG, 256, 1, 1>(a, n_sm, st, info);
+  if (variant == 2) return launch_cell_d<N, Q, MASS, DG, 256, 2, 1>(a, n_sm, st, info);
+  if (variant == 3) return launch_cell_d<N, Q, MASS, DG, 256, 1, 2>(a, n_sm, st, info);
+  if (variant == 4) return launch_cell_d<N, Q, MASS, DG, 256, 1, 3>(a, n_sm, st, info);
+  if (variant == 5) return launch_cell_d<N, Q, MASS, DG, 256, 1, 4>(a, n_sm, st, info);
+  if (variant == 6) return launch_cell_d<N, Q, MASS, DG, 256, 2, 2>(a, n_sm, st, info);
+  if (variant == 7) return launch_cell_d<N, Q, MASS, DG, 128, 1, 6>(a, n_sm, st, info);
+  if (variant == 8) return launch_cell_d<N, Q, MASS, DG, 256, 1, 4, 4>(a, n_sm, st, info);
+  if (N <= 4) return launch_cell_d<N, Q, MASS, DG, 256, 1, 4>(a, n_sm, st, info);
+  return launch_cell_d<N, Q, MASS, DG, 256, 1, 3>(a, n_sm, st, info);
+}
+
+// variant: 0 = default; 1..3 = tuning variants of the CG kernel (bench sweeps only)
+template <int N, int Q, bool MASS, bool DG>
+static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info,
+                                 int variant) {
+  using S = CellShape<N, Q, MASS>;
+  constexpr int BLOCK = S::SMEM > 96 * 1024 ? 512 : 256;
+  if (!DG && !MASS) {
+    if (variant == 1) return launch_cell_v<N, Q, MASS, DG, BLOCK, 2, 1>(a, n_sm, st, info);
+    if (variant == 2) return launch_cell_v<N, Q, MASS, DG, BLOCK, 1, (BLOCK == 256 ? 3 : 1)>(a, n_sm, st, info);
+    if (variant == 3) return launch_cell_v<N, Q, MASS, DG, 128, 1, 4>(a, n_sm, st, info);
+    if (variant == 4) return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, true>(a, n_sm, st, info);
+    if (variant == 5) return launch_cell_v<N, Q, MASS, DG, BLOCK, 1, 1, true>(a, n_sm, st, info);
+    if (variant == 6) return launch_cell_v<N, Q, MASS, DG, BLOCK, 3, 1>(a, n_sm, st, info);
+    if (variant == 7) return launch_cell_v<N, Q, MASS, DG, 128, 2, 1>(a, n_sm, st, info);
+    if (variant == 9) return launch_cell_v<N, Q, MASS, DG, 384, 0, 1>(a, n_sm, st, info);
+    if (variant == 12) return launch_cell_v<N, Q, MASS, DG, 768, 1, 1>(a, n_sm, st, info);
+  }
+  // block-size variants for every kernel family (registers are capped by the bounds)
+  if (variant == 8) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
+  if (variant == 10) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
+  if (variant == 11) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
+  if (variant == 14) {   // skewed GEMM1/D-action pipeline with the per-degree default CTA size
+    if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, false, true>(a, n_sm, st, info);
+    if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1, false, false, true>(a, n_sm, st, info);
+    if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1, false, false, true>(a, n_sm, st, info);
+    return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, false, false, true>(a, n_sm, st, info);
+  }
+  if (variant == 13) {   // blocked tile runs with the per-degree default CTA size
+    if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, true>(a, n_sm, st, info);
+    if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1, false, true>(a, n_sm, st, info);
+    if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1, false, true>(a, n_sm, st, info);
+    return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, false, true>(a, n_sm, st, info);
+  }
+  // One large CTA per SM (a single staged table copy, more warps than the smem-limited
+  // default allows), measured with tools/quick_bench.py variants 8/10/11:
+  //   P3 (CG and DG) 768 threads: -5.6 % / -5 %;  CG P4 640: -1.4 %;
+  //   DG P2 512: -26 %, Helmholtz P2 512: -17 %;  CG P2 keeps 2 tiles per warp at 256.
+  //   CG P3 additionally skews GEMM1(t+1) ahead of the D action of tile t (-2.7 %;
+  //   slower for the other families, variant 14)
+  if (N == 20 && !MASS && !DG) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, false, true>(a, n_sm, st, info);
+  if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
+  if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
+  if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
+  return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1>(a, n_sm, st, info);
+}
+
+// engine: 0 = per-degree default, 1 = DMMA (cell_kernel.cuh), 2 = DFMA (cell_dfma_kernel.cuh)
+template <int N, int Q>
+static cudaError_t cell_variant(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
+                                CellLaunchInfo* info, int variant, int engine) {
+  if (engine == 0) engine = 1;   // measured: DFMA P1 ~= DMMA, P2 +20 % (tools/gpu_dfma1.sh)
+  if constexpr (N <= 20) {   // P4 rows do not fit the DFMA register budget
+    if (engine == 2) {
+      if (!dg) return launch_cell_dt<N, Q, false, false>(a, n_sm, st, info, variant);
+      if (mass) return launch_cell_dt<N, Q, true, true>(a, n_sm, st, info, variant);
+      return launch_cell_dt<N, Q, false, true>(a, n_sm, st, info, variant);
+    }
+  }
+  if (!dg) return launch_cell_t<N, Q, false, false>(a, n_sm, st, info, variant);
+  if (mass) return launch_cell_t<N, Q, true, true>(a, n_sm, st, info, variant);
+  return launch_cell_t<N, Q, false, true>(a, n_sm, st, info, variant);
+}
+
+#define TMF_CELL_TU(NN, QQ)                                                                        \
+  cudaError_t cell_dispatch_##NN##_##QQ(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st, \
+                                        CellLaunchInfo* info, int variant, int engine) {             \
+    return cell_variant<NN, QQ>(mass, dg, a, n_sm, st, info, variant, engine);                        \
+  }
+
+}  // namespace tmf

@@ -1,0 +1,7 @@
+// Cell-kernel instantiations, degree 2.
+#include "cell_launch.cuh"
+
+namespace tmf {
+TMF_CELL_TU(10, 14)
+TMF_CELL_TU(10, 15)
+}  // namespace tmf

@@ -1,0 +1,89 @@
+// Face-kernel instantiations and launchers (sm_100a).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "face_kernel.cuh"
+#include "launch.h"
+#include "launch_common.cuh"
+
+namespace tmf {
+
+template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false>
+static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
+  using S = FaceShape<N, QF>;
+  constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED>;
+  if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
+  if (info) {
+    info->nfrag = S::NFRAG;
+    info->chunk = S::CHUNK;
+    info->dmma_per_batch = BND ? (S::NB1 + S::NB2) : 2 * (S::NB1 + S::NB2);
+    return cudaSuccess;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, SMEM);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t work = a.n_chunks * a.nc;
+  if (work == 0) return cudaSuccess;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  if (blocks > work) blocks = work;
+  kern<<<(unsigned)blocks, BLOCK, SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// variant: 0 = default (by degree, below, blocked chunk runs); 1 = no prefetch, 3 CTAs/SM;
+// 2 = record prefetch, 3 CTAs/SM; 3 = record prefetch, 2 CTAs/SM; 4 = full prefetch, 2 CTAs/SM
+template <int N, int QF, bool BND>
+static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info,
+                                 int variant) {
+  if (variant == 1) return launch_face_v<N, QF, BND, 0, 3>(a, n_sm, st, info);
+  if (variant == 2) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
+  if (variant == 3) return launch_face_v<N, QF, BND, 1, 2>(a, n_sm, st, info);
+  if (variant == 4) return launch_face_v<N, QF, BND, 2, 2>(a, n_sm, st, info);
+  if (variant == 5) return launch_face_v<N, QF, BND, 1, 1, 512>(a, n_sm, st, info);
+  if (variant == 6) return launch_face_v<N, QF, BND, 2, 1, 512>(a, n_sm, st, info);
+  if (variant == 7) return launch_face_v<N, QF, BND, 1, 1, 768>(a, n_sm, st, info);
+  if (variant == 8) return launch_face_v<N, QF, BND, 1, 2, 384>(a, n_sm, st, info);
+  if (variant == 9) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
+  if (variant == 10) return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
+  // default: contiguous chunk runs per CTA (tables restaged only when the signature
+  // changes: -7 % / -8 % at P3 / P2); low degrees have short batches, so occupancy
+  // beats prefetch depth (P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the fully
+  // prefetching 2-CTA kernel
+  if (N <= 10) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
+  return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
+}
+
+cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
+                        cudaStream_t st, FaceLaunchInfo* info, bool* supported, int variant) {
+  *supported = true;
+#define TMF_FACE(NN, QQ)                                                          \
+  if (n_dpc == NN && n_qf == QQ) {                                                \
+    if (boundary) return launch_face_t<NN, QQ, true>(a, n_sm, st, info, variant); \
+    return launch_face_t<NN, QQ, false>(a, n_sm, st, info, variant);              \
+  }
+  TMF_FACE(4, 3)
+  TMF_FACE(4, 4)
+  TMF_FACE(10, 6)
+  TMF_FACE(10, 10)
+  TMF_FACE(20, 12)
+  TMF_FACE(20, 20)
+  TMF_FACE(35, 35)
+#undef TMF_FACE
+  *supported = false;
+  return cudaSuccess;
+}
+
+cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st) {
+  if (a.n_chunks == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)std::min<int64_t>(a.n_chunks, (int64_t)n_sm * 8);
+  if (boundary)
+    face_geometry_kernel<true><<<blocks, 256, 0, st>>>(a);
+  else
+    face_geometry_kernel<false><<<blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace tmf

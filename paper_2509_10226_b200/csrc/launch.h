@@ -17,6 +17,8 @@ struct CellLaunchInfo {
   int grid = 0;
   int smem = 0;
   int frag_doubles = 0;
+  int table = 0;             // 0 = DMMA lane fragments, 1 = point-major DFMA rows
+  double flops_issued = 0;   // FP64 FMA*2 issued per launch (padding included)
 };
 
 struct FaceLaunchInfo {
@@ -28,7 +30,8 @@ struct FaceLaunchInfo {
 
 // info != nullptr: only fill the launch description (no launch).
 cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& a, int n_sm,
-                        cudaStream_t st, CellLaunchInfo* info, bool* supported, int variant = 0);
+                        cudaStream_t st, CellLaunchInfo* info, bool* supported, int variant = 0,
+                        int engine = 0);
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
                         cudaStream_t st, FaceLaunchInfo* info, bool* supported, int variant = 0);
 cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st);

@@ -24,10 +24,10 @@ def fixture_objects(g):
     return mesh, dofmap, geo, basis
 
 
-def operator_from_fixture(g, device=0):
+def operator_from_fixture(g, device=0, **config):
     mesh, dofmap, geo, basis = fixture_objects(g)
     kind = str(g["kind"])
-    cfg = op.OperatorConfig(device=device)
+    cfg = op.OperatorConfig(device=device, **config)
     dids = tuple(int(x) for x in g["dirichlet_ids"])
     if kind == "cg":
         return op.CgPoissonOperator(mesh, dofmap, geo, basis, cfg)

@@ -28,3 +28,23 @@ def test_gpu_repeatable(name):
     y1 = A.apply(g["u"])
     y2 = A.apply(g["u"])
     assert rel_l2(y1, y2) <= 1e-15
+
+
+@pytest.mark.parametrize("engine", ["dmma", "dfma"])
+@pytest.mark.parametrize("name", [n for n in golden_names() if "_p4_" not in n])
+def test_gpu_both_cell_engines_match_golden(name, engine):
+    """The tensor-core (DMMA) and vector-pipe (DFMA) cell kernels are both exact
+    restatements; the default picks one per degree (cell_dfma_kernel.cuh)."""
+    g = load_golden(name)
+    A = operator_from_fixture(g, cell_engine=engine)
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
+
+
+@pytest.mark.parametrize("variant", range(1, 9))
+@pytest.mark.parametrize("name", ["cg_p1_n3_gm_dir2", "cg_p2_n8_gm", "cg3_p2_n3_ref_dir", "helmk_p2_n3_gm_dir", "dg_p3_n3_gm_dir"])
+def test_gpu_dfma_variants_match_golden(name, variant):
+    g = load_golden(name)
+    A = operator_from_fixture(g, cell_engine="dfma", kernel_variant=variant)
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}/v{variant}: rel L2 {err:.3e}"
