@@ -80,7 +80,8 @@ typedef struct tmf_plan_desc {
   int32_t device;              /* CUDA device ordinal                                 */
   int32_t flags;               /* bits 0-3 / 4-7: cell / face kernel tuning variant;
                                   8-11 face chunk/8; 12 concurrent DG; 13-14 cell engine
-                                  (0 by degree, 1 DMMA tensor cores, 2 DFMA)            */
+                                  (0 by degree, 1 DMMA tensor cores, 2 DFMA); 15-16 CG
+                                  patch-local assembly (0 auto, 1 off, 2 on)            */
 } tmf_plan_desc;
 
 typedef struct tmf_plan_info {
@@ -91,6 +92,8 @@ typedef struct tmf_plan_info {
   int32_t kernels_per_apply;   /* kernel launches per tmf_apply                       */
   int32_t n_face_batches;      /* signature-uniform 8-face batches (DG)               */
   int64_t device_bytes;        /* device memory held by the plan                      */
+  int32_t patch_cells;         /* CG patch-local assembly: cells per patch (0 = off)  */
+  double patch_ratio;          /* unique patch DoFs / unmasked cell-DoF slots (CG)    */
 } tmf_plan_info;
 
 int tmf_plan_create(const tmf_plan_desc* desc, tmf_plan** out);

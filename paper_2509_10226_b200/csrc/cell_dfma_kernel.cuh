@@ -30,10 +30,69 @@ struct DfmaShape {
   static constexpr int SMEM = 2 * TAB * 8;
 };
 
+// The point loop of one thread's MC cells: uu (gathered u, padded to NP) ->
+// yy (cell residual), G / md the per-cell metric and mass factor, T1 / T2 the
+// point-major rows E and w_q E in shared memory.
+template <int N, int Q, bool MASS, int MC>
+__device__ __forceinline__ void dfma_cell_points(const double2* __restrict__ T1, const double2* __restrict__ T2,
+                                                 const double (&uu)[MC][DfmaShape<N, Q, MASS>::NP],
+                                                 const double (&G)[MC][6], const double (&md)[MC],
+                                                 double (&yy)[MC][DfmaShape<N, Q, MASS>::NP]) {
+  using S = DfmaShape<N, Q, MASS>;
+  constexpr int NP = S::NP, NC = S::NC;
+#pragma unroll
+  for (int m = 0; m < MC; ++m)
+#pragma unroll
+    for (int j = 0; j < NP; ++j) yy[m][j] = 0.0;
+#pragma unroll (Q <= 5 ? Q : 1)
+  for (int q = 0; q < Q; ++q) {
+    const double2* t1 = T1 + q * (NC * NP / 2);
+    const double2* t2 = T2 + q * (NC * NP / 2);
+    double g[MC][NC];
+#pragma unroll
+    for (int m = 0; m < MC; ++m)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) g[m][c] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NP; j += 2)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double2 e = t1[(c * NP + j) / 2];
+#pragma unroll
+        for (int m = 0; m < MC; ++m) {
+          g[m][c] = fma(e.x, uu[m][j], g[m][c]);
+          if (j + 1 < N) g[m][c] = fma(e.y, uu[m][j + 1], g[m][c]);
+        }
+      }
+    double d[MC][NC];
+#pragma unroll
+    for (int m = 0; m < MC; ++m) {
+      constexpr int o = MASS ? 1 : 0;
+      const double g0 = g[m][o], g1 = g[m][o + 1], g2 = g[m][o + 2];
+      d[m][o] = G[m][0] * g0 + G[m][1] * g1 + G[m][2] * g2;
+      d[m][o + 1] = G[m][1] * g0 + G[m][3] * g1 + G[m][4] * g2;
+      d[m][o + 2] = G[m][2] * g0 + G[m][4] * g1 + G[m][5] * g2;
+      if (MASS) d[m][0] = md[m] * g[m][0];
+    }
+#pragma unroll
+    for (int j = 0; j < NP; j += 2)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double2 e = t2[(c * NP + j) / 2];
+#pragma unroll
+        for (int m = 0; m < MC; ++m) {
+          yy[m][j] = fma(e.x, d[m][c], yy[m][j]);
+          if (j + 1 < N) yy[m][j + 1] = fma(e.y, d[m][c], yy[m][j + 1]);
+        }
+      }
+  }
+}
+
 template <int N, int Q, bool MASS, bool DG, int BLOCK, int MC, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB) cell_dfma_kernel(CellArgs a) {
   using S = DfmaShape<N, Q, MASS>;
-  constexpr int NP = S::NP, NC = S::NC;
+  constexpr int NP = S::NP;
+  constexpr int CH = BLOCK * MC;                     // cells per CTA iteration
   extern __shared__ __align__(16) double smem[];
   {
     const double2* src = reinterpret_cast<const double2*>(a.frags);
@@ -44,7 +103,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_dfma_kernel(CellArgs a) {
   const double2* T1 = reinterpret_cast<const double2*>(smem);
   const double2* T2 = reinterpret_cast<const double2*>(smem + S::TAB);
 
-  constexpr int CH = BLOCK * MC;                     // cells per CTA iteration
   const int64_t cpc = (a.n_cells + CH - 1) / CH;     // chunks per component
   const int64_t nch = cpc * a.nc;
   for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
@@ -87,53 +145,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_dfma_kernel(CellArgs a) {
       G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
       G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
       md[m] = MASS ? __ldg(a.cgeo + 8 * cc + 6) : 0.0;
-#pragma unroll
-      for (int j = 0; j < NP; ++j) yy[m][j] = 0.0;
     }
-
-#pragma unroll (Q <= 5 ? Q : 1)
-    for (int q = 0; q < Q; ++q) {
-      const double2* t1 = T1 + q * (NC * NP / 2);
-      const double2* t2 = T2 + q * (NC * NP / 2);
-      double g[MC][NC];
-#pragma unroll
-      for (int m = 0; m < MC; ++m)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) g[m][c] = 0.0;
-#pragma unroll
-      for (int j = 0; j < NP; j += 2)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const double2 e = t1[(c * NP + j) / 2];
-#pragma unroll
-          for (int m = 0; m < MC; ++m) {
-            g[m][c] = fma(e.x, uu[m][j], g[m][c]);
-            if (j + 1 < N) g[m][c] = fma(e.y, uu[m][j + 1], g[m][c]);
-          }
-        }
-      double d[MC][NC];
-#pragma unroll
-      for (int m = 0; m < MC; ++m) {
-        constexpr int o = MASS ? 1 : 0;
-        const double g0 = g[m][o], g1 = g[m][o + 1], g2 = g[m][o + 2];
-        d[m][o] = G[m][0] * g0 + G[m][1] * g1 + G[m][2] * g2;
-        d[m][o + 1] = G[m][1] * g0 + G[m][3] * g1 + G[m][4] * g2;
-        d[m][o + 2] = G[m][2] * g0 + G[m][4] * g1 + G[m][5] * g2;
-        if (MASS) d[m][0] = md[m] * g[m][0];
-      }
-#pragma unroll
-      for (int j = 0; j < NP; j += 2)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const double2 e = t2[(c * NP + j) / 2];
-#pragma unroll
-          for (int m = 0; m < MC; ++m) {
-            yy[m][j] = fma(e.x, d[m][c], yy[m][j]);
-            if (j + 1 < N) yy[m][j + 1] = fma(e.y, d[m][c], yy[m][j + 1]);
-          }
-        }
-    }
-
+    dfma_cell_points<N, Q, MASS, MC>(T1, T2, uu, G, md, yy);
 #pragma unroll
     for (int m = 0; m < MC; ++m) {
       const int64_t c = base + (int64_t)m * BLOCK;

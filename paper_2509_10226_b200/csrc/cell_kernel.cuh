@@ -19,9 +19,9 @@
 //
 // Both B operands are constant tables, pre-swizzled on the host into
 // lane-major fragments (frag[f][lane]) and staged once per CTA in shared
-// memory (one conflict-free LDS.64 per DMMA).  Geometry (J, det, adjugate)
-// is recomputed from the 4 vertex coordinates, so the only per-cell traffic
-// is the vertex ids, DoF indices and the gathered/scattered vector entries.
+// memory (one conflict-free LDS.64 per DMMA).  Per-cell geometry (6 entries
+// of G = det J^-1 J^-T, plus the mass factor) is precomputed once per plan by
+// cell_geometry_kernel and read as 64 B per cell.
 //
 // CG: masked (Dirichlet) DoFs are encoded as ~idx (< 0): gathered as 0 and
 // never scattered (operator.py:327-328 fixes y on them afterwards).  The
@@ -41,6 +41,19 @@ struct CellArgs {
   int64_t n_cells;
   int nc;                          // interleaved components
   int accumulate;                  // DG: add into y (concurrent face kernel) instead of storing
+  // CG patch-local assembly (cell_patch_kernel.cuh): the cells are cut into
+  // patches of consecutive cells; per patch p, pmeta[p] = {pdofs start, nu,
+  // pic start, pic length} (16-byte aligned segments), pdofs = the patch's
+  // unique unmasked DoFs (ascending), pic = [incidence offsets (nu+1)] [shared
+  // contribution offsets j*CHP + cl], plidw / pgeo = the cells' 16-bit local
+  // DoF indices and G in patch-SoA layout (word / component major).
+  const int4* __restrict__ pmeta = nullptr;
+  const int* __restrict__ pdofs = nullptr;
+  const uint16_t* __restrict__ pic = nullptr;
+  const uint32_t* __restrict__ plidw = nullptr;
+  const double* __restrict__ pgeo = nullptr;
+  int numax = 0;                   // max unique DoFs of a patch (multiple of 4)
+  int icmax = 0;                   // max pic segment length (multiple of 8)
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the

@@ -7,6 +7,7 @@
 
 #include "cell_dfma_kernel.cuh"
 #include "cell_kernel.cuh"
+#include "cell_patch_kernel.cuh"
 #include "launch.h"
 #include "launch_common.cuh"
 
@@ -49,21 +50,13 @@ static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, C
 template <int N, int Q, bool MASS, bool DG, int BLOCK, int MC, int MINB, int OVER = 1>
 static cudaError_t launch_cell_d(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = DfmaShape<N, Q, MASS>;
+  constexpr int CH = BLOCK * MC;
   auto kern = cell_dfma_kernel<N, Q, MASS, DG, BLOCK, MC, MINB>;
   if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  const int64_t chunks = ((a.n_cells + BLOCK * MC - 1) / (BLOCK * MC)) * a.nc;
-  int64_t blocks = (int64_t)n_sm * per_sm * OVER;
-  if (blocks > chunks) blocks = chunks;
-  if (blocks < 1) blocks = 1;
   if (info) {
     info->dmma_per_tile = 0;
     info->tiles = (a.n_cells + 7) / 8 * a.nc;
     info->block = BLOCK;
-    info->grid = (int)blocks;
     info->smem = S::SMEM;
     info->frag_doubles = 2 * S::TAB;
     info->table = 1;
@@ -71,7 +64,36 @@ static cudaError_t launch_cell_d(const CellArgs& a, int n_sm, cudaStream_t st, C
     return cudaSuccess;
   }
   if (a.n_cells == 0) return cudaSuccess;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t chunks = ((a.n_cells + CH - 1) / CH) * a.nc;
+  int64_t blocks = (int64_t)n_sm * per_sm * OVER;
+  if (blocks > chunks) blocks = chunks;
+  if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// CG patch-local assembly (cell_patch_kernel.cuh); runs when the plan built patch
+// tables (a.pmeta), whatever the engine; uses the DFMA point-major tables
+template <int N, int Q, int BLOCK, int STAGES, int MINB>
+static cudaError_t launch_cell_p(const CellArgs& a, int n_sm, cudaStream_t st) {
+  using S = PatchShape<N, Q, BLOCK>;
+  auto kern = cell_patch_kernel<N, Q, BLOCK, STAGES, MINB>;
+  const size_t smem = S::smem_bytes(a.numax, a.icmax, STAGES);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  if (cudaError_t e = opt_in_smem(kern, 227 * 1024); e != cudaSuccess) return e;
+  if (a.n_cells == 0) return cudaSuccess;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t chunks = ((a.n_cells + S::CH - 1) / S::CH) * a.nc;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  if (blocks > chunks) blocks = chunks;
+  kern<<<(unsigned)blocks, BLOCK, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -141,6 +163,13 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
 template <int N, int Q>
 static cudaError_t cell_variant(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
                                 CellLaunchInfo* info, int variant, int engine) {
+  if constexpr (N <= 20) {   // CG patch-local assembly: 256-cell patches, 3-stage ring
+    if (!dg && info) {
+      info->patch_cells = PatchShape<N, Q, 256>::CH;
+      info->patch_stride = PatchShape<N, Q, 256>::CHP;
+    }
+    if (!dg && !info && a.pmeta) return launch_cell_p<N, Q, 256, 3, 1>(a, n_sm, st);
+  }
   if (engine == 0) engine = 1;   // measured: DFMA P1 ~= DMMA, P2 +20 % (tools/gpu_dfma1.sh)
   if constexpr (N <= 20) {   // P4 rows do not fit the DFMA register budget
     if (engine == 2) {

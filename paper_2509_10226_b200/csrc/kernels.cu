@@ -42,6 +42,23 @@ cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st
   return cudaGetLastError();
 }
 
+// patch-SoA copy of G for cell_patch_kernel: pgeo[(p*6 + i)*CH + cl] = cgeo[(p*CH + cl)*8 + i]
+static __global__ void patch_geometry_kernel(const double* __restrict__ cgeo, double* __restrict__ pgeo,
+                                             int64_t n_cells, int CH) {
+  const int64_t n = (n_cells + CH - 1) / CH * CH;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = c / CH, cl = c - p * CH;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) pgeo[(p * 6 + i) * CH + cl] = c < n_cells ? cgeo[c * 8 + i] : 0.0;
+  }
+}
+
+cudaError_t launch_patch_geometry(const double* cgeo, double* pgeo, int64_t n_cells, int CH, int n_sm,
+                                  cudaStream_t st) {
+  patch_geometry_kernel<<<n_sm * 8, 256, 0, st>>>(cgeo, pgeo, n_cells, CH);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
                          cudaStream_t st) {
   if (n == 0) return cudaSuccess;

@@ -36,6 +36,7 @@ __all__ = ["OperatorConfig", "SipgConfig", "HelmholtzCoefficients", "CgPoissonOp
 
 _STAGES = ("ref", "data", "mm", "sched")
 _ENGINES = {"auto": 0, "dmma": 1, "dfma": 2}
+_PATCHES = {"auto": 0, "off": 1, "on": 2}
 
 
 @dataclass(frozen=True)
@@ -57,6 +58,7 @@ class OperatorConfig:
     face_chunk: int = 0         # 8-face batches per CTA chunk, multiple of 8 up to 120 (0 = default 32)
     concurrent_dg: bool = False  # DG: run the cell and face kernels concurrently (accumulating)
     cell_engine: str = "auto"    # B200 cell kernel: auto (by degree) | dmma (tensor cores) | dfma
+    cell_patches: str = "auto"   # B200 CG patch-local assembly: auto (by locality) | off | on
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -67,6 +69,8 @@ class OperatorConfig:
             raise ValueError(f"unknown precision {self.precision!r}")
         if self.cell_engine not in _ENGINES:
             raise ValueError(f"unknown cell engine {self.cell_engine!r}")
+        if self.cell_patches not in _PATCHES:
+            raise ValueError(f"unknown cell patch mode {self.cell_patches!r}")
         if self.backend not in ("auto", "compiled", "python", "b200"):
             raise ValueError(f"unknown backend {self.backend!r}")
 
@@ -187,7 +191,8 @@ class _B200Operator:
             ((int(getattr(self.config, "face_variant", 0)) & 0xF) << 4) | \
             ((int(getattr(self.config, "face_chunk", 0)) // 8 & 0xF) << 8) | \
             ((1 if getattr(self.config, "concurrent_dg", False) else 0) << 12) | \
-            (_ENGINES[getattr(self.config, "cell_engine", "auto")] << 13)
+            (_ENGINES[getattr(self.config, "cell_engine", "auto")] << 13) | \
+            (_PATCHES[getattr(self.config, "cell_patches", "auto")] << 15)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))

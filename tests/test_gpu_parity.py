@@ -48,3 +48,14 @@ def test_gpu_dfma_variants_match_golden(name, variant):
     A = operator_from_fixture(g, cell_engine="dfma", kernel_variant=variant)
     err = rel_l2(A.apply(g["u"]), g["y"])
     assert err <= TOL, f"{name}/v{variant}: rel L2 {err:.3e}"
+
+
+@pytest.mark.parametrize("variant", [0, 2, 3])
+@pytest.mark.parametrize("name", [n for n in golden_names() if n.startswith("cg") and "_p4_" not in n])
+def test_gpu_patch_local_assembly_matches_golden(name, variant):
+    """CG patch-local assembly (shared-memory gather/scatter per cell patch) forced on."""
+    g = load_golden(name)
+    A = operator_from_fixture(g, cell_engine="dfma", cell_patches="on", kernel_variant=variant)
+    assert A.info["patch_cells"] > 0
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}: rel L2 {err:.3e}"

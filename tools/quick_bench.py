@@ -5,7 +5,7 @@ import numpy as np
 import torch
 from paper_2509_10226_b200 import mesh as M, dofmap as D, basis as B, quadrature as Q, geometry as G, operator as op
 
-def run(kind, p, n, reps=20, variant=0, engine="auto"):
+def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto"):
     reordered = kind.endswith("r")
     t0 = time.time()
     m = M.kuhn_cube_mesh(n, seed=0)
@@ -18,7 +18,7 @@ def run(kind, p, n, reps=20, variant=0, engine="auto"):
     geo = G.GeometryData("affine", cr, fr, None, None, None, None)
     if kind == "cg":
         dm = D.build_dof_map(m, p, "cg")
-        A = op.CgPoissonOperator(m, dm, geo, bas, op.OperatorConfig(kernel_variant=variant, cell_engine=engine))
+        A = op.CgPoissonOperator(m, dm, geo, bas, op.OperatorConfig(kernel_variant=variant, cell_engine=engine, cell_patches=patches))
     elif kind == "dg":
         dm = D.build_dof_map(m, p, "dg")
         A = op.DgSipgOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n),
@@ -41,7 +41,7 @@ def run(kind, p, n, reps=20, variant=0, engine="auto"):
     gdofs = nd / (ms[0] * 1e-3) / 1e9
     tf_alg = info["flops_alg"] / (ms[0] * 1e-3) / 1e12
     tf_iss = info["flops_issued"] / (ms[0] * 1e-3) / 1e12
-    print(json.dumps(dict(kind=kind + ("r" if reordered else ""), p=p, n=n, variant=variant, engine=engine, ndof=nd, setup_s=round(setup, 1), ms=[round(x, 4) for x in ms],
+    print(json.dumps(dict(kind=kind + ("r" if reordered else ""), p=p, n=n, variant=variant, engine=engine, patch_cells=A.info['patch_cells'], patch_ratio=round(A.info['patch_ratio'], 3), ndof=nd, setup_s=round(setup, 1), ms=[round(x, 4) for x in ms],
                           gdofs=round(gdofs, 3), tflops_alg=round(tf_alg, 2), tflops_issued=round(tf_iss, 2),
                           frac_fp64=round(tf_alg / 37.1, 3))), flush=True)
 
@@ -49,4 +49,4 @@ if __name__ == "__main__":
     for spec in sys.argv[1:]:
         parts = spec.split(":")
         run(parts[0], int(parts[1]), int(parts[2]), variant=int(parts[3]) if len(parts) > 3 else 0,
-            engine=parts[4] if len(parts) > 4 else "auto")
+            engine=parts[4] if len(parts) > 4 else "auto", patches=parts[5] if len(parts) > 5 else "auto")
