@@ -67,87 +67,88 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
           }
 }
 
-// CG patch-local assembly tables (CellArgs / cell_patch_kernel.cuh) for patches of
-// CH consecutive cells; contribution offsets are j*CHP + cl.  Two parallel passes
-// over the patches (sizes, then fill at the prefix-summed offsets); per patch the
-// (DoF, offset) pairs are sorted, so unique DoFs are ascending (coalesced u loads
-// and REDs) and every DoF's incidences are contiguous.  Every per-patch segment is
-// padded to 16 bytes for the bulk copies.
+// CG warp-patch records (cell_patch_kernel.cuh) for patches of CH = 32 consecutive
+// cells; contribution slots are j*CH + cl.  Two parallel passes over the patches
+// (sizes, then fill at the prefix-summed offsets); per patch the (DoF, slot) pairs
+// are sorted, so unique DoFs are ascending (coalesced u gathers and REDs) and every
+// DoF's incidences are contiguous.  G is filled in on the device afterwards.
 struct PatchTables {
-  std::vector<int4> meta;         // {pd start, nu, ic start, ic length}
-  std::vector<int> pd;            // unique DoFs
-  std::vector<uint16_t> ic;       // [offsets (nu+1) | positions], each padded to 8
-  std::vector<uint32_t> lidw;     // [patch][word][cell] local indices (2 per word)
-  int numax = 0, icmax = 0;
+  std::vector<int4> meta;         // {record offset (16 B), nu, incidences, record size (16 B)}
+  std::vector<uint4> rec;         // records
+  int numax = 0, recmax = 0;
   int64_t slots = 0, unique = 0;
 };
 
-void build_patches(const int* enc, int64_t n_cells, int N, int CH, int CHP, PatchTables& T) {
+void build_patches(const int* enc, int64_t n_cells, int N, int CH, PatchTables& T) {
   const int NP = (N + 1) & ~1, NW = NP / 2;
+  const int geo_b = 6 * CH * 8, lid_b = NW * CH * 4;
   const int64_t np = (n_cells + CH - 1) / CH;
   std::vector<int> nu(np), ninc(np);
-  auto keys_of = [&](int64_t p, std::vector<uint64_t>& k) {
+  auto keys_of = [&](int64_t p, std::vector<uint32_t>& k) {
     k.clear();
     const int64_t c0 = p * CH, c1 = std::min<int64_t>(n_cells, c0 + CH);
     for (int64_t c = c0; c < c1; ++c)
       for (int j = 0; j < N; ++j) {
         const int g = enc[c * N + j];
-        if (g >= 0) k.push_back(((uint64_t)g << 16) | (uint64_t)(j * CHP + (c - c0)));
+        if (g >= 0) k.push_back((uint32_t)(j * CH + (c - c0)));
       }
-    std::sort(k.begin(), k.end());
+    std::sort(k.begin(), k.end(), [&](uint32_t x, uint32_t y) {
+      const int gx = enc[(p * CH + x % CH) * N + x / CH], gy = enc[(p * CH + y % CH) * N + y / CH];
+      return gx != gy ? gx < gy : x < y;
+    });
   };
+  auto dof = [&](int64_t p, uint32_t x) { return enc[(p * CH + x % CH) * N + x / CH]; };
   const int nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
   auto parallel = [&](auto&& body) {
     std::vector<std::thread> th;
     for (int t = 0; t < nt; ++t)
       th.emplace_back([&, t] {
-        std::vector<uint64_t> k;
+        std::vector<uint32_t> k;
         for (int64_t p = t; p < np; p += nt) body(p, k);
       });
     for (auto& x : th) x.join();
   };
-  parallel([&](int64_t p, std::vector<uint64_t>& k) {
+  parallel([&](int64_t p, std::vector<uint32_t>& k) {
     keys_of(p, k);
     int u = 0;
-    for (size_t i = 0; i < k.size(); ++i) u += (i == 0 || (k[i] >> 16) != (k[i - 1] >> 16));
+    for (size_t i = 0; i < k.size(); ++i) u += (i == 0 || dof(p, k[i]) != dof(p, k[i - 1]));
     nu[p] = u;
     ninc[p] = (int)k.size();
   });
   auto r4 = [](int64_t x) { return (x + 3) & ~(int64_t)3; };
   auto r8 = [](int64_t x) { return (x + 7) & ~(int64_t)7; };
   T.meta.resize(np);
-  int64_t pd_at = 0, ic_at = 0;
+  int64_t at = 0;   // 16-byte units
   for (int64_t p = 0; p < np; ++p) {
-    const int64_t icl = r8(nu[p] + 1) + r8(ninc[p]);
-    T.meta[p] = make_int4((int)pd_at, nu[p], (int)ic_at, (int)icl);
-    pd_at += r4(nu[p]);
-    ic_at += icl;
-    T.numax = std::max<int>(T.numax, (int)r4(nu[p]));
-    T.icmax = std::max<int>(T.icmax, (int)icl);
+    const int64_t bytes = geo_b + lid_b + 4 * r4(nu[p]) + 2 * r8(nu[p] + 1) + 2 * r8(ninc[p]);
+    T.meta[p] = make_int4((int)at, nu[p], ninc[p], (int)(bytes / 16));
+    at += bytes / 16;
+    T.numax = std::max(T.numax, (nu[p] + 1) & ~1);
+    T.recmax = std::max<int>(T.recmax, (int)bytes);
     T.slots += ninc[p];
     T.unique += nu[p];
   }
-  T.pd.assign(pd_at, 0);
-  T.ic.assign(ic_at, 0);
-  T.lidw.assign((size_t)np * NW * CH, 0xFFFFFFFFu);
-  parallel([&](int64_t p, std::vector<uint64_t>& k) {
+  T.rec.assign(at, make_uint4(0, 0, 0, 0));
+  parallel([&](int64_t p, std::vector<uint32_t>& k) {
     keys_of(p, k);
     const int4 m = T.meta[p];
-    uint16_t* off = T.ic.data() + m.z;
+    unsigned char* r = reinterpret_cast<unsigned char*>(T.rec.data() + m.x);
+    uint16_t* lid = reinterpret_cast<uint16_t*>(r + geo_b);
+    std::fill(lid, lid + 2 * NW * CH, (uint16_t)0xFFFF);
+    int* pd = reinterpret_cast<int*>(r + geo_b + lid_b);
+    uint16_t* off = reinterpret_cast<uint16_t*>(pd + r4(m.y));
     uint16_t* pos = off + r8(m.y + 1);
-    uint16_t* lid = reinterpret_cast<uint16_t*>(T.lidw.data() + (size_t)p * NW * CH);
     int u = -1;
     for (size_t i = 0; i < k.size(); ++i) {
-      const int g = (int)(k[i] >> 16);
-      const int ps = (int)(k[i] & 0xFFFF);
-      if (i == 0 || g != (int)(k[i - 1] >> 16)) {
+      const int g = dof(p, k[i]);
+      if (i == 0 || g != dof(p, k[i - 1])) {
         ++u;
-        T.pd[m.x + u] = g;
+        pd[u] = g;
         off[u] = (uint16_t)i;
       }
-      pos[i] = (uint16_t)ps;
-      const int j = ps / CHP, cl = ps % CHP;
-      lid[2 * ((size_t)(j / 2) * CH + cl) + (j & 1)] = (uint16_t)u;   // little-endian halves
+      pos[i] = (uint16_t)k[i];
+      const int j = k[i] / CH, cl = k[i] % CH;
+      lid[2 * ((j / 2) * CH + cl) + (j & 1)] = (uint16_t)u;   // little-endian halves of word j/2
     }
     off[m.y] = (uint16_t)k.size();
   });
@@ -218,13 +219,10 @@ struct tmf_plan {
   // CG patch-local assembly (CellArgs): built when the cell order has locality
   int patches = 0;       // (desc.flags >> 15) & 3: 0 = auto (locality ratio), 1 = off, 2 = on
   bool local = false;
-  int numax = 0, icmax = 0;
+  int numax = 0, recmax = 0;
   double patch_ratio = 1.0;   // unique patch DoFs / unmasked cell-DoF slots
   int4* pmeta = nullptr;
-  int* pdofs = nullptr;
-  uint16_t* pic = nullptr;
-  uint32_t* plidw = nullptr;
-  double* pgeo = nullptr;
+  uint4* prec = nullptr;
   int4* if_chunks = nullptr;
   int* if_cm = nullptr;
   int* if_cp = nullptr;
@@ -258,12 +256,9 @@ struct tmf_plan {
     a.nc = nc;
     if (local && c0 == 0 && c1 == n_cells) {
       a.pmeta = pmeta;
-      a.pdofs = pdofs;
-      a.pic = pic;
-      a.plidw = plidw;
-      a.pgeo = pgeo;
+      a.prec = prec;
       a.numax = numax;
-      a.icmax = icmax;
+      a.recmax = recmax;
     }
     return a;
   }
@@ -304,7 +299,7 @@ struct tmf_plan {
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
-                    (void*)pmeta, (void*)pdofs, (void*)pic, (void*)plidw, (void*)pgeo})
+                    (void*)pmeta, (void*)prec})
       if (p) cudaFree(p);
   }
 };
@@ -549,6 +544,8 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   P->variant = d->flags & 0xF;
   P->engine = (d->flags >> 13) & 3;
   P->patches = (d->flags >> 15) & 3;
+  // warp patches use the DFMA point-major tables (also for their global-kernel fallback)
+  if (P->patches == 2 && d->operator_kind == TMF_CG_LAPLACE && d->n_dofs_per_cell <= 20) P->engine = 2;
   P->face_variant = (d->flags >> 4) & 0xF;
   P->concurrent = (d->flags >> 12) & 1;
   P->degree = d->degree;
@@ -629,25 +626,20 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     dummy.n_cells = P->n_cells;
     dummy.nc = P->nc;
     TMF_CUDA(tmf::launch_cell(P->N, P->Q, false, false, dummy, P->n_sm, 0, &ci, &ok, P->variant, P->engine));
-    if (P->patches != 1 && ci.patch_cells > 0 && ci.patch_cells * P->N <= 65535 &&
-        P->N * ci.patch_stride <= 65535) {
+    if (P->patches == 2 && ci.patch_cells > 0) {
       PatchTables T;
-      build_patches(enc.data(), P->n_cells, P->N, ci.patch_cells, ci.patch_stride, T);
+      build_patches(enc.data(), P->n_cells, P->N, ci.patch_cells, T);
       P->patch_ratio = T.slots ? (double)T.unique / (double)T.slots : 1.0;
       P->info.patch_ratio = P->patch_ratio;
-      if (P->patches == 2 || P->patch_ratio < 0.5) {
-        const int64_t np = (int64_t)T.meta.size();
+      if (P->patches == 2) {   // opt-in: measured slower than the DMMA kernel
         P->local = true;
         P->numax = T.numax;
-        P->icmax = T.icmax;
+        P->recmax = T.recmax;
         P->info.patch_cells = ci.patch_cells;
         if ((rc = upload(&P->pmeta, T.meta.data(), T.meta.size(), &total))) return bail(rc);
-        if ((rc = upload(&P->pdofs, T.pd.data(), T.pd.size(), &total))) return bail(rc);
-        if ((rc = upload(&P->pic, T.ic.data(), T.ic.size(), &total))) return bail(rc);
-        if ((rc = upload(&P->plidw, T.lidw.data(), T.lidw.size(), &total))) return bail(rc);
-        TMF_CUDA(cudaMalloc(&P->pgeo, sizeof(double) * 6 * ci.patch_cells * np));
-        total += sizeof(double) * 6 * ci.patch_cells * np;
-        TMF_CUDA(tmf::launch_patch_geometry(P->cell_geo, P->pgeo, P->n_cells, ci.patch_cells, P->n_sm, 0));
+        if ((rc = upload(&P->prec, T.rec.data(), T.rec.size(), &total))) return bail(rc);
+        TMF_CUDA(tmf::launch_patch_geometry(P->cell_geo, P->pmeta, P->prec, P->n_cells, ci.patch_cells,
+                                            P->n_sm, 0));
       }
     }
     std::vector<int> fix;

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_dfma_kernel(CellArgs a) {
   const int64_t cpc = (a.n_cells + CH - 1) / CH;     // chunks per component
   const int64_t nch = cpc * a.nc;
   for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-    const int comp = (int)(ch / cpc);
+    const int comp = a.nc == 1 ? 0 : (int)(ch / cpc);
     const int64_t base = (ch - (int64_t)comp * cpc) * CH + threadIdx.x;
     double uu[MC][NP], yy[MC][NP], G[MC][6], md[MC];
 #pragma unroll

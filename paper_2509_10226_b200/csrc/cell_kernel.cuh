@@ -41,19 +41,13 @@ struct CellArgs {
   int64_t n_cells;
   int nc;                          // interleaved components
   int accumulate;                  // DG: add into y (concurrent face kernel) instead of storing
-  // CG patch-local assembly (cell_patch_kernel.cuh): the cells are cut into
-  // patches of consecutive cells; per patch p, pmeta[p] = {pdofs start, nu,
-  // pic start, pic length} (16-byte aligned segments), pdofs = the patch's
-  // unique unmasked DoFs (ascending), pic = [incidence offsets (nu+1)] [shared
-  // contribution offsets j*CHP + cl], plidw / pgeo = the cells' 16-bit local
-  // DoF indices and G in patch-SoA layout (word / component major).
+  // CG warp-patch-local assembly (cell_patch_kernel.cuh): patches of 32
+  // consecutive cells, one 16-byte aligned record each in prec; pmeta[p] =
+  // {record offset (16 B units), unique DoFs nu, incidences, record size (16 B)}
   const int4* __restrict__ pmeta = nullptr;
-  const int* __restrict__ pdofs = nullptr;
-  const uint16_t* __restrict__ pic = nullptr;
-  const uint32_t* __restrict__ plidw = nullptr;
-  const double* __restrict__ pgeo = nullptr;
-  int numax = 0;                   // max unique DoFs of a patch (multiple of 4)
-  int icmax = 0;                   // max pic segment length (multiple of 8)
+  const void* __restrict__ prec = nullptr;
+  int numax = 0;                   // max unique DoFs of a patch (even)
+  int recmax = 0;                  // max record bytes (multiple of 16)
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the
@@ -144,7 +138,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   const int64_t step = BLK ? 1 : nwarps;
   int nidx[MT][S::KK];
   auto load_indices = [&](int64_t t) {
-    const int cmp = (int)(t / cst);
+    const int cmp = a.nc == 1 ? 0 : (int)(t / cst);
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
       const int64_t c = ((t - (int64_t)cmp * cst) * MT + m) * 8 + cs;
@@ -159,7 +153,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   };
   // gathered u (A fragments) and geometry of one super-tile, from the indices in nidx
   auto load_data = [&](int64_t t, double (&av)[MT][S::KK], double (&G)[MT][6], double (&mdet)[MT]) {
-    const int cmp = (int)(t / cst);
+    const int cmp = a.nc == 1 ? 0 : (int)(t / cst);
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
       const int64_t c = ((t - (int64_t)cmp * cst) * MT + m) * 8 + cs;
@@ -184,7 +178,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   }
 
   for (; st < st_end; st += step) {
-    const int comp = (int)(st / cst);
+    const int comp = a.nc == 1 ? 0 : (int)(st / cst);
     int64_t cell[MT];
     bool valid[MT];
     double av[MT][S::KK];

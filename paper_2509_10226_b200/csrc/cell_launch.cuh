@@ -76,23 +76,24 @@ static cudaError_t launch_cell_d(const CellArgs& a, int n_sm, cudaStream_t st, C
   return cudaGetLastError();
 }
 
-// CG patch-local assembly (cell_patch_kernel.cuh); runs when the plan built patch
-// tables (a.pmeta), whatever the engine; uses the DFMA point-major tables
-template <int N, int Q, int BLOCK, int STAGES, int MINB>
+// CG warp-patch-local assembly (cell_patch_kernel.cuh); runs when the plan built
+// patch records (a.pmeta), whatever the engine; uses the DFMA point-major tables
+template <int N, int Q, int BLOCK, int MINB>
 static cudaError_t launch_cell_p(const CellArgs& a, int n_sm, cudaStream_t st) {
-  using S = PatchShape<N, Q, BLOCK>;
-  auto kern = cell_patch_kernel<N, Q, BLOCK, STAGES, MINB>;
-  const size_t smem = S::smem_bytes(a.numax, a.icmax, STAGES);
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  using S = PatchShape<N, Q>;
+  auto kern = cell_patch_kernel<N, Q, BLOCK, MINB>;
+  const size_t smem = S::smem_bytes(a.recmax, a.numax, BLOCK / 32);
+  if (smem > 227 * 1024) return cudaErrorNotSupported;   // caller falls back to the global kernel
   if (cudaError_t e = opt_in_smem(kern, 227 * 1024); e != cudaSuccess) return e;
   if (a.n_cells == 0) return cudaSuccess;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const int64_t chunks = ((a.n_cells + S::CH - 1) / S::CH) * a.nc;
+  const int64_t warps = ((a.n_cells + S::CH - 1) / S::CH) * a.nc;
   int64_t blocks = (int64_t)n_sm * per_sm;
-  if (blocks > chunks) blocks = chunks;
+  const int64_t need = (warps + BLOCK / 32 - 1) / (BLOCK / 32);
+  if (blocks > need) blocks = need;
   kern<<<(unsigned)blocks, BLOCK, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -163,12 +164,26 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
 template <int N, int Q>
 static cudaError_t cell_variant(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
                                 CellLaunchInfo* info, int variant, int engine) {
-  if constexpr (N <= 20) {   // CG patch-local assembly: 256-cell patches, 3-stage ring
-    if (!dg && info) {
-      info->patch_cells = PatchShape<N, Q, 256>::CH;
-      info->patch_stride = PatchShape<N, Q, 256>::CHP;
+  if constexpr (N <= 20) {   // CG warp-patch-local assembly (32-cell patches)
+    if (!dg && info) info->patch_cells = PatchShape<N, Q>::CH;
+    if (!dg && !info && a.pmeta) {
+      // variants (bench sweeps): CTA size / minimum CTAs per SM (register cap)
+      cudaError_t e;
+      if (variant == 1) e = launch_cell_p<N, Q, 128, 4>(a, n_sm, st);
+      else if (variant == 2) e = launch_cell_p<N, Q, 128, 8>(a, n_sm, st);
+      else if (variant == 3) e = launch_cell_p<N, Q, 256, 2>(a, n_sm, st);
+      else if (variant == 4) e = launch_cell_p<N, Q, 256, 3>(a, n_sm, st);
+      else if (variant == 5) e = launch_cell_p<N, Q, 64, 12>(a, n_sm, st);
+      else if (variant == 6) e = launch_cell_p<N, Q, 128, 2>(a, n_sm, st);
+      else if (N <= 4) e = launch_cell_p<N, Q, 128, 6>(a, n_sm, st);
+      else if (N <= 10) e = launch_cell_p<N, Q, 128, 4>(a, n_sm, st);
+      else e = launch_cell_p<N, Q, 128, 2>(a, n_sm, st);
+      if (e != cudaErrorNotSupported) return e;
+      // patch records too large for shared memory (tiny or unordered meshes)
+      CellArgs g = a;
+      g.pmeta = nullptr;
+      return cell_variant<N, Q>(mass, dg, g, n_sm, st, info, 0, engine);
     }
-    if (!dg && !info && a.pmeta) return launch_cell_p<N, Q, 256, 3, 1>(a, n_sm, st);
   }
   if (engine == 0) engine = 1;   // measured: DFMA P1 ~= DMMA, P2 +20 % (tools/gpu_dfma1.sh)
   if constexpr (N <= 20) {   // P4 rows do not fit the DFMA register budget

@@ -42,20 +42,22 @@ cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st
   return cudaGetLastError();
 }
 
-// patch-SoA copy of G for cell_patch_kernel: pgeo[(p*6 + i)*CH + cl] = cgeo[(p*CH + cl)*8 + i]
-static __global__ void patch_geometry_kernel(const double* __restrict__ cgeo, double* __restrict__ pgeo,
-                                             int64_t n_cells, int CH) {
+// G into the warp-patch records (cell_patch_kernel.cuh): record p starts with
+// G component-major, geo[i*CH + cl] = cgeo[(p*CH + cl)*8 + i] (0 past the last cell)
+static __global__ void patch_geometry_kernel(const double* __restrict__ cgeo, const int4* __restrict__ pmeta,
+                                             double* __restrict__ prec, int64_t n_cells, int CH) {
   const int64_t n = (n_cells + CH - 1) / CH * CH;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = c / CH, cl = c - p * CH;
+    double* geo = prec + (int64_t)pmeta[p].x * 2;   // 16-byte units
 #pragma unroll
-    for (int i = 0; i < 6; ++i) pgeo[(p * 6 + i) * CH + cl] = c < n_cells ? cgeo[c * 8 + i] : 0.0;
+    for (int i = 0; i < 6; ++i) geo[i * CH + cl] = c < n_cells ? cgeo[c * 8 + i] : 0.0;
   }
 }
 
-cudaError_t launch_patch_geometry(const double* cgeo, double* pgeo, int64_t n_cells, int CH, int n_sm,
-                                  cudaStream_t st) {
-  patch_geometry_kernel<<<n_sm * 8, 256, 0, st>>>(cgeo, pgeo, n_cells, CH);
+cudaError_t launch_patch_geometry(const double* cgeo, const int4* pmeta, void* prec, int64_t n_cells,
+                                  int CH, int n_sm, cudaStream_t st) {
+  patch_geometry_kernel<<<n_sm * 8, 256, 0, st>>>(cgeo, pmeta, static_cast<double*>(prec), n_cells, CH);
   return cudaGetLastError();
 }
 

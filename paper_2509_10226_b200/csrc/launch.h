@@ -20,7 +20,6 @@ struct CellLaunchInfo {
   int table = 0;             // 0 = DMMA lane fragments, 1 = point-major DFMA rows
   double flops_issued = 0;   // FP64 FMA*2 issued per launch (padding included)
   int patch_cells = 0;       // CG patch-local assembly: cells per patch (0 = not supported)
-  int patch_stride = 0;      // row stride of the shared contribution array
 };
 
 struct FaceLaunchInfo {
@@ -38,8 +37,8 @@ cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, i
                         cudaStream_t st, FaceLaunchInfo* info, bool* supported, int variant = 0);
 cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st);
-cudaError_t launch_patch_geometry(const double* cgeo, double* pgeo, int64_t n_cells, int CH, int n_sm,
-                                  cudaStream_t st);
+cudaError_t launch_patch_geometry(const double* cgeo, const int4* pmeta, void* prec, int64_t n_cells,
+                                  int CH, int n_sm, cudaStream_t st);
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
                          cudaStream_t st);
 

@@ -58,7 +58,7 @@ class OperatorConfig:
     face_chunk: int = 0         # 8-face batches per CTA chunk, multiple of 8 up to 120 (0 = default 32)
     concurrent_dg: bool = False  # DG: run the cell and face kernels concurrently (accumulating)
     cell_engine: str = "auto"    # B200 cell kernel: auto (by degree) | dmma (tensor cores) | dfma
-    cell_patches: str = "auto"   # B200 CG patch-local assembly: auto (by locality) | off | on
+    cell_patches: str = "auto"   # B200 CG warp-patch assembly: auto (= off, measured slower) | off | on
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:

@@ -8,5 +8,6 @@ cap() {  # name spec [source]
   [ -n "$3" ] && ncu -i /tmp/$1.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_$1_sass.csv 2>/dev/null
   rm -f /tmp/$1.ncu-rep
 }
-cap cg1r_patch cgr:1:48:0:dmma:on --import-source=on
+cap cg1r_wpatch cgr:1:48:0:dmma:on --import-source=on
+cap cg2r_wpatch cgr:2:48:0:dmma:on --import-source=on
 echo done
