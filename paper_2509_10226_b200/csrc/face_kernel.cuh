@@ -215,9 +215,15 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 // BLOCKED: each CTA takes a contiguous run of chunks (consecutive chunks of one
 // (window, signature) group share their tables, so restaging and both barriers are
 // skipped); otherwise chunks are dealt round-robin.
-template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false>
+// TPF (with !BLOCKED): chunks are dealt round-robin, so all CTAs march through the
+// (window, signature)-sorted chunk list together and the live set of u / y stays in
+// L2; the next chunk's tables are prefetched with cp.async into a second shared
+// buffer while the current chunk computes (one barrier per chunk, no load latency).
+template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
+          bool TPF = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
+  constexpr int TAB = (BOUNDARY ? 1 : 2) * S::NFRAG * 32;   // doubles per staged table set
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
   const int fs = lane >> 2;
@@ -230,28 +236,61 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   const int64_t w0 = BLOCKED ? blockIdx.x * per : blockIdx.x;
   const int64_t w1 = BLOCKED ? (w0 + per < nwork ? w0 + per : nwork) : nwork;
   const int64_t wstep = BLOCKED ? 1 : gridDim.x;
+  auto chunk_at = [&](int64_t w) {
+    const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
+    return __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
+  };
+  auto stage_async = [&](int4 c, double* d) {
+    const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)c.x * S::NFRAG * 32);
+    for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(d + 2 * i)),
+                   "l"(s0 + i) : "memory");
+    if (!BOUNDARY) {
+      const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)c.y * S::NFRAG * 32);
+      for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(d + S::NFRAG * 32 + 2 * i)), "l"(s1 + i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
   int cur_x = -1, cur_y = -2;
+  int buf = 0;   // TPF: staged table set in use
+  if (TPF && w0 < w1) {
+    stage_async(chunk_at(w0), smem);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
   for (int64_t w = w0; w < w1; w += wstep) {
-    const int comp = (int)(w / a.n_chunks);
-    const int4 ch = __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
-    const bool restage = ch.x != cur_x || ch.y != cur_y;
-    cur_x = ch.x;
-    cur_y = ch.y;
-    if (restage) {
-    __syncthreads();  // previous chunk's warps are done with the staged tables
-    {
-      const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.x * S::NFRAG * 32);
-      double2* d = reinterpret_cast<double2*>(smem);
-      for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[i] = __ldg(s0 + i);
-      if (!BOUNDARY) {
-        const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.y * S::NFRAG * 32);
-        for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[S::NFRAG * 16 + i] = __ldg(s1 + i);
+    const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
+    const int4 ch = chunk_at(w);
+    bool next_restage = false;
+    if (TPF) {
+      // prefetch the next chunk's tables when its signature differs
+      if (w + wstep < w1) {
+        const int4 nx = chunk_at(w + wstep);
+        next_restage = nx.x != ch.x || nx.y != ch.y;
+        if (next_restage) stage_async(nx, smem + (buf ^ 1) * TAB);
+      }
+    } else {
+      const bool restage = ch.x != cur_x || ch.y != cur_y;
+      cur_x = ch.x;
+      cur_y = ch.y;
+      if (restage) {
+        __syncthreads();  // previous chunk's warps are done with the staged tables
+        {
+          const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.x * S::NFRAG * 32);
+          double2* d = reinterpret_cast<double2*>(smem);
+          for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[i] = __ldg(s0 + i);
+          if (!BOUNDARY) {
+            const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.y * S::NFRAG * 32);
+            for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[S::NFRAG * 16 + i] = __ldg(s1 + i);
+          }
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
-    }
-    const double* Fm = smem;
-    const double* Fp = smem + S::NFRAG * 32;
+    const double* Fm = smem + (TPF ? buf * TAB : 0);
+    const double* Fp = Fm + S::NFRAG * 32;
     const int* perm_m = a.perm + (ch.x / 6) * N;                  // gather order, minus side
     const int* perm_p = a.perm + (BOUNDARY ? 0 : ch.y / 6) * N;   // plus side
 
@@ -378,6 +417,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
             }
           }
       }
+    }
+    if (TPF) {
+      if (next_restage) asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncthreads();   // the chunk's warps are done with buffer buf; the next tables landed
+      if (next_restage) buf ^= 1;
     }
   }
 }

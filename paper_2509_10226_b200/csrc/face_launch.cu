@@ -9,11 +9,12 @@
 
 namespace tmf {
 
-template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false>
+template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
+          bool TPF = false>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShape<N, QF>;
-  constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
-  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED>;
+  constexpr int SMEM = (TPF ? 2 : 1) * (BND ? 1 : 2) * S::NFRAG * 32 * 8;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, TPF>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   if (info) {
     info->nfrag = S::NFRAG;
@@ -48,6 +49,13 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   if (variant == 8) return launch_face_v<N, QF, BND, 1, 2, 384>(a, n_sm, st, info);
   if (variant == 9) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
   if (variant == 10) return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
+  // round-robin chunks (all CTAs march through the chunk list together, keeping the
+  // live u / y in L2) + cp.async prefetch of the next chunk's tables: measured
+  // 5-15 % slower than the blocked default at C3 / C4 sizes (barrier per chunk)
+  if (variant == 11) return launch_face_v<N, QF, BND, 1, 3, 256, false, true>(a, n_sm, st, info);
+  if (variant == 12) return launch_face_v<N, QF, BND, 2, 2, 256, false, true>(a, n_sm, st, info);
+  if (variant == 13) return launch_face_v<N, QF, BND, 1, 2, 256, false, true>(a, n_sm, st, info);
+  if (variant == 14) return launch_face_v<N, QF, BND, 2, 1, 512, false, true>(a, n_sm, st, info);
   // default: contiguous chunk runs per CTA (tables restaged only when the signature
   // changes: -7 % / -8 % at P3 / P2); low degrees have short batches, so occupancy
   // beats prefetch depth (P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the fully

@@ -59,3 +59,14 @@ def test_gpu_patch_local_assembly_matches_golden(name, variant):
     assert A.info["patch_cells"] > 0
     err = rel_l2(A.apply(g["u"]), g["y"])
     assert err <= TOL, f"{name}: rel L2 {err:.3e}"
+
+
+@pytest.mark.parametrize("face_variant", [11, 12, 13, 14])
+@pytest.mark.parametrize("name", ["dg_p1_n3_gm_dir", "dg_p2_n3_gm_dir", "dg_p3_n3_gm_dir", "helmk_p2_n3_gm_dir",
+                                  "helm3_p2_n2_gm_none", "dg_p4_n2_gm_dir"])
+def test_gpu_face_variants_match_golden(name, face_variant):
+    """Face-kernel scheduling variants (round-robin chunks + table prefetch)."""
+    g = load_golden(name)
+    A = operator_from_fixture(g, face_variant=face_variant, face_chunk=8)
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}/f{face_variant}: rel L2 {err:.3e}"
