@@ -47,15 +47,28 @@ int upload(T** dst, const T* src, size_t n, size_t* total) {
 // Lane-major DMMA B fragments for one table family (see cell_kernel.cuh):
 //   B1[t][c][kk][lane] = E_c(8t + (lane>>2), 4kk + (lane&3))
 //   B2[t][c][i][nj][lane] = w_q E_c(q = 8t + 2(lane&3) + i, 8nj + (lane>>2))
+// for the T full 8-point tiles; a remainder of 1..4 points is one 4-point group
+// (CellShape::GRP) with components padded to 4:
+//   B1g[h][kk][lane] = E_{2h + (n&1)}(8T + (n>>1), 4kk + (lane&3)),  n = lane>>2
+//   B2g[c][nj][lane] = w_q E_c(q = 8T + (lane&3), 8nj + (lane>>2))
 template <typename F>
 void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<double>& out) {
-  const int T = (Q + 7) / 8, KK = (N + 3) / 4, NJ = (N + 7) / 8;
+  const int KK = (N + 3) / 4, NJ = (N + 7) / 8, R = Q % 8;
+  const bool grp = R >= 1 && R <= 4;
+  const int T = grp ? Q / 8 : (Q + 7) / 8;
   for (int t = 0; t < T; ++t)
     for (int c = 0; c < NC; ++c)
       for (int kk = 0; kk < KK; ++kk)
         for (int lane = 0; lane < 32; ++lane) {
           const int q = 8 * t + (lane >> 2), j = 4 * kk + (lane & 3);
           out.push_back(q < Q && j < N ? E(c, q, j) : 0.0);
+        }
+  if (grp)
+    for (int h = 0; h < 2; ++h)
+      for (int kk = 0; kk < KK; ++kk)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int n = lane >> 2, c = 2 * h + (n & 1), q = 8 * T + (n >> 1), j = 4 * kk + (lane & 3);
+          out.push_back(q < Q && j < N && c < NC ? E(c, q, j) : 0.0);
         }
   for (int t = 0; t < T; ++t)
     for (int c = 0; c < NC; ++c)
@@ -65,6 +78,13 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
             const int q = 8 * t + 2 * (lane & 3) + i, j = 8 * nj + (lane >> 2);
             out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
           }
+  if (grp)
+    for (int c = 0; c < NC; ++c)
+      for (int nj = 0; nj < NJ; ++nj)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int q = 8 * T + (lane & 3), j = 8 * nj + (lane >> 2);
+          out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
+        }
 }
 
 // CG warp-patch records (cell_patch_kernel.cuh) for patches of CH = 32 consecutive

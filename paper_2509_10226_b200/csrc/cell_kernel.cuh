@@ -88,11 +88,19 @@ static __global__ void cell_geometry_kernel(CellGeoArgs a) {
 template <int N, int Q, bool MASS>
 struct CellShape {
   static constexpr int KK = (N + 3) / 4;     // GEMM1 k-steps (DoFs)
-  static constexpr int T = (Q + 7) / 8;      // point tiles
   static constexpr int NJ = (N + 7) / 8;     // GEMM2 n-tiles (DoFs)
   static constexpr int NC = MASS ? 4 : 3;    // value (mass) + 3 reference gradients
-  static constexpr int NB1 = T * NC * KK;
-  static constexpr int NB2 = T * NC * 2 * NJ;
+  // Points: T full 8-point tiles; a remainder of 1..4 points goes to one 4-point
+  // group (GEMM1 columns (point, component) with components padded to 4, the
+  // face-kernel layout), which takes 2 KK + NC NJ DMMAs instead of the
+  // NC KK + 2 NC NJ of an 8-point tile (P3, n_q 35: 165 -> 151 per tile).
+  static constexpr int R = Q % 8;
+  static constexpr bool GRP = R >= 1 && R <= 4;
+  static constexpr int T = GRP ? Q / 8 : (Q + 7) / 8;
+  static constexpr int NB1T = T * NC * KK;   // GEMM1 fragments of the 8-point tiles
+  static constexpr int NB2T = T * NC * 2 * NJ;
+  static constexpr int NB1 = NB1T + (GRP ? 2 * KK : 0);
+  static constexpr int NB2 = NB2T + (GRP ? NC * NJ : 0);
   static constexpr int NFRAG = NB1 + NB2;
   static constexpr int SMEM = NFRAG * 32 * 8;
   static constexpr int DMMA_PER_TILE = NB1 + NB2;
@@ -251,27 +259,70 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
             for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][c][i], b);
           }
     };
+    // remainder 4-point group: lane owns point 8T + q4 (components 2h + i)
+    auto gemm1g = [&](double (&v)[MT][2][2]) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m) v[m][0][0] = v[m][0][1] = v[m][1][0] = v[m][1][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < S::KK; ++kk)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double b = sB1[(S::NB1T + h * S::KK + kk) * 32 + lane];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(v[m][h], av[m][kk], b);
+        }
+    };
+    auto dgemm2g = [&](const double (&v)[MT][2][2]) {
+      double d[MT][S::NC];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        constexpr int o = MASS ? 1 : 0;
+        const double c[4] = {v[m][0][0], v[m][0][1], v[m][1][0], v[m][1][1]};
+        const double g0 = c[o], g1 = c[o + 1], g2 = c[o + 2];
+        d[m][o] = G[m][0] * g0 + G[m][1] * g1 + G[m][2] * g2;
+        d[m][o + 1] = G[m][1] * g0 + G[m][3] * g1 + G[m][4] * g2;
+        d[m][o + 2] = G[m][2] * g0 + G[m][4] * g1 + G[m][5] * g2;
+        if (MASS) d[m][0] = mdet[m] * c[0];
+      }
+#pragma unroll
+      for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+        for (int nj = 0; nj < S::NJ; ++nj) {
+          const double b = sB2[(S::NB2T + c * S::NJ + nj) * 32 + lane];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][c], b);
+        }
+    };
+    double vg[MT][2][2];
     if (SKEW) {
       // skewed software pipeline: GEMM1 of point tile t+1 is issued before the D
       // action of tile t, so the FP64-pipe D action overlaps tensor work in flight
       double va[MT][S::NC][2], vb[MT][S::NC][2];
-      gemm1(0, va);
+      if (S::T > 0) gemm1(0, va);
+      else if (S::GRP) gemm1g(vg);
 #pragma unroll
       for (int t = 0; t < S::T; ++t) {
         if (t % 2 == 0) {
           if (t + 1 < S::T) gemm1(t + 1, vb);
+          else if (S::GRP) gemm1g(vg);
           daction_gemm2(t, va);
         } else {
           if (t + 1 < S::T) gemm1(t + 1, va);
+          else if (S::GRP) gemm1g(vg);
           daction_gemm2(t, vb);
         }
       }
+      if (S::GRP) dgemm2g(vg);
     } else {
 #pragma unroll
       for (int t = 0; t < S::T; ++t) {
         double v[MT][S::NC][2];
         gemm1(t, v);
         daction_gemm2(t, v);
+      }
+      if (S::GRP) {
+        gemm1g(vg);
+        dgemm2g(vg);
       }
     }
 

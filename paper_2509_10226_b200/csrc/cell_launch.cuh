@@ -151,9 +151,8 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   // default allows), measured with tools/quick_bench.py variants 8/10/11:
   //   P3 (CG and DG) 768 threads: -5.6 % / -5 %;  CG P4 640: -1.4 %;
   //   DG P2 512: -26 %, Helmholtz P2 512: -17 %;  CG P2 keeps 2 tiles per warp at 256.
-  //   CG P3 additionally skews GEMM1(t+1) ahead of the D action of tile t (-2.7 %;
-  //   slower for the other families, variant 14)
-  if (N == 20 && !MASS && !DG) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, false, true>(a, n_sm, st, info);
+  //   (the skewed GEMM1/D-action pipeline, variant 14, helped CG P3 by 2.7 % before
+  //   the remainder-point group; with it the plain loop is 5 % faster)
   if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
   if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
   if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
