@@ -62,20 +62,41 @@ def parse():
 
 
 # ----------------------------------------------------------------- workload
+_MESHES = {}
+
+
 def build_problem(n, p, reorder):
+    """Mesh (cached per (n, reorder): the reordering and the partition are shared by
+    all degrees), DoF map, tables."""
     from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, quadrature as Q
     from paper_2509_10226_b200.geometry import GeometryData
 
-    m = M.kuhn_cube_mesh(n, seed=0)
-    if reorder:
-        from paper_2509_10226_b200.reorder import hierarchical_reorder
+    key = (n, reorder)
+    if key not in _MESHES:
+        m = M.kuhn_cube_mesh(n, seed=0)
+        if reorder:
+            from paper_2509_10226_b200.reorder import hierarchical_reorder
 
-        m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+            m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+        _MESHES[key] = m
+    m = _MESHES[key]
     cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
     bas = B.tabulate_basis(p, cr, fr)
     dm = D.build_dof_map(m, p, "cg")
     geo = GeometryData("affine", cr, fr, None, None, None, None)
     return m, dm, geo, bas
+
+
+_PARTS = {}
+
+
+def partition_of(m, world):
+    from paper_2509_10226_b200.distributed import partition_cells
+
+    key = (id(m), world)
+    if key not in _PARTS:
+        _PARTS[key] = partition_cells(m, world)
+    return _PARTS[key]
 
 
 def variants(args):
@@ -221,7 +242,7 @@ def gpu_bench(args, rank, world):
             else:
                 from paper_2509_10226_b200.distributed import DistributedCgOperator
 
-                A = DistributedCgOperator(m, dm, geo, bas, rank, world)
+                A = DistributedCgOperator(m, dm, geo, bas, rank, world, part=partition_of(m, world))
                 ids = A.owned_global_ids
                 local = A.local_op
             u_host = u_glob if ids is None else u_glob[ids]
@@ -337,7 +358,20 @@ def gpu_bench(args, rank, world):
                 h2d=sum(8 * pr["ndof"] for pr in problems), d2h=sum(8 * pr["ndof"] for pr in problems))
 
 
+_STDOUT_FD = None
+
+
+def emit(line):
+    """The one JSON line, on the real stdout (everything else -- e.g. the NCCL version
+    banner that libnccl prints on fd 1 -- was redirected to stderr)."""
+    os.write(_STDOUT_FD if _STDOUT_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _STDOUT_FD
+    sys.stdout.flush()
+    _STDOUT_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -356,7 +390,7 @@ def main():
                                            f"~{args.cpu_sample_s}s per worker per degree, extrapolated per DoF",
                                  "detail": detail},
                 "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        emit(line)
         return
 
     if world > 1 or args.dist:
@@ -405,7 +439,7 @@ def main():
                 "e2e": {"value": round(e2e_val, 4), "unit": unit, "h2d_bytes_per_step": r["h2d"],
                         "d2h_bytes_per_step": r["d2h"], "path": "Operator.apply_host_async(pinned host u, y) -> tmf_apply_host_async, one stream per plan, largest first"},
                 "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "parity_e2e_vs_timed_rel_l2": r["parity_rel_l2"]}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1 or args.dist:
         import torch.distributed as dist
 
