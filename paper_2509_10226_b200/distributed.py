@@ -285,6 +285,29 @@ def _stream_of(t):
     return torch.cuda.current_stream(t.device).cuda_stream if t.is_cuda else 0
 
 
+def _local_buffers(op, u, out, n):
+    """(u_loc, y_loc) for one apply: caller tensors of the local length are used in
+    place; owned-length input is copied into the operator's local buffer."""
+    nl = op.u_loc.numel()
+    if u.numel() == nl:      # local layout (or a rank without ghosts): in place
+        u_loc = u
+    elif u.numel() == n:
+        op.u_loc[:n].copy_(u)
+        u_loc = op.u_loc
+    else:
+        raise ValueError(f"vector length {u.numel()} is neither the owned ({n}) nor the local ({nl}) size")
+    y_loc = out if (out is not None and out.numel() == nl) else op.y_loc
+    return u_loc, y_loc
+
+
+def _local_result(y_loc, out, n):
+    if out is None:
+        return y_loc[:n].clone()
+    if out.data_ptr() != y_loc.data_ptr():
+        out.copy_(y_loc[:n])
+    return out
+
+
 class DistributedCgOperator:
     """CG Laplace apply on a k-way partition: y_owned = A u_owned.
 
@@ -348,44 +371,50 @@ class DistributedCgOperator:
             ev[1].record()
             self.kernel_events.append(ev)
 
-    def _timed_local(self):
-        if self.kernel_events is None:
-            self._local(self.u_loc, self.y_loc)
-            return
+    def _timed_local_on(self, u_loc, y_loc):
         import torch
 
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        self._local(self.u_loc, self.y_loc)
+        self._local(u_loc, y_loc)
         e1.record()
         self.kernel_events.append((e0, e1))
 
+    @property
+    def n_local(self) -> int:
+        """Length of the rank-local layout (owned DoFs first, then ghost slots)."""
+        return len(self.sub.l2g)
+
     def apply(self, u_owned, out=None):
         """Forward halo overlapped with the interior cells (no ghost DoF), then the
-        boundary cells, the identity rows and the additive reverse halo."""
+        boundary cells, the identity rows and the additive reverse halo.
+
+        ``u_owned`` / ``out`` have the owned length (copied through internal local
+        buffers) or the local length ``n_local`` (used in place, no copies: the ghost
+        slots of ``u`` are overwritten by the halo, ``out[:n_owned]`` is the result)."""
         from . import _lib
 
         n = self.sub.n_owned
-        self.u_loc[:n].copy_(u_owned)
-        reqs = self.fwd.start(self.u_loc)
+        u_loc, y_loc = _local_buffers(self, u_owned, out, n)
+        reqs = self.fwd.start(u_loc)
         if self.local_op is None:           # external local apply (tests): no stages
-            self.fwd.finish(reqs, self.u_loc, add=False)
-            self._timed_local()
+            self.fwd.finish(reqs, u_loc, add=False)
+            if self.kernel_events is None:
+                self._local(u_loc, y_loc)
+            else:
+                self._timed_local_on(u_loc, y_loc)
         else:
-            op, st = self.local_op, _stream_of(self.u_loc)
-            up, yp = self.u_loc.data_ptr(), self.y_loc.data_ptr()
+            op, st = self.local_op, _stream_of(u_loc)
+            up, yp = u_loc.data_ptr(), y_loc.data_ptr()
             ev = self._event_pair()
             op.apply_stages(up, yp, _lib.STAGE_ZERO | _lib.STAGE_CELLS, 0, self.sub.n_interior_cells, st)
             self._close_events(ev)
-            self.fwd.finish(reqs, self.u_loc, add=False)
+            self.fwd.finish(reqs, u_loc, add=False)
             ev = self._event_pair()
             op.apply_stages(up, yp, _lib.STAGE_CELLS | _lib.STAGE_FIXUP, self.sub.n_interior_cells, None, st)
             self._close_events(ev)
-        self.rev.reverse_add(self.y_loc)
-        if out is None:
-            return self.y_loc[:n].clone()
-        out.copy_(self.y_loc[:n])
-        return out
+        self.rev.reverse_add(y_loc)
+        return _local_result(y_loc, out, n)
 
     def diagonal(self):
         """Owned slice of diag(A): local matrix-free diagonal + reverse halo."""
@@ -456,6 +485,11 @@ class DistributedDgOperator:
     def n_owned(self) -> int:
         return self.sub.n_owned_cells * self.block
 
+    @property
+    def n_local(self) -> int:
+        """Length of the rank-local layout (owned cells' DoFs first, then ghost cells')."""
+        return self.u_loc.numel()
+
     def owned_global_ids(self) -> np.ndarray:
         c = self.sub.cell_l2g[: self.sub.n_owned_cells]
         return (c[:, None] * self.block + np.arange(self.block)[None, :]).ravel()
@@ -466,18 +500,15 @@ class DistributedDgOperator:
         from . import _lib
 
         n = self.n_owned
-        self.u_loc[:n].copy_(u_owned)
-        reqs = self.fwd.start(self.u_loc)
+        u_loc, y_loc = _local_buffers(self, u_owned, out, n)
+        reqs = self.fwd.start(u_loc)
         if self.local_op is None:
-            self.fwd.finish(reqs, self.u_loc, add=False)
-            self._local(self.u_loc, self.y_loc)
+            self.fwd.finish(reqs, u_loc, add=False)
+            self._local(u_loc, y_loc)
         else:
-            op, st = self.local_op, _stream_of(self.u_loc)
-            up, yp = self.u_loc.data_ptr(), self.y_loc.data_ptr()
+            op, st = self.local_op, _stream_of(u_loc)
+            up, yp = u_loc.data_ptr(), y_loc.data_ptr()
             op.apply_stages(up, yp, _lib.STAGE_CELLS, 0, self.sub.n_owned_cells, st)
-            self.fwd.finish(reqs, self.u_loc, add=False)
+            self.fwd.finish(reqs, u_loc, add=False)
             op.apply_stages(up, yp, _lib.STAGE_FACES, 0, 0, st)
-        if out is None:
-            return self.y_loc[:n].clone()
-        out.copy_(self.y_loc[:n])
-        return out
+        return _local_result(y_loc, out, n)

@@ -106,6 +106,12 @@ def _worker(rank, world, port, kind, n, p, q):
             ids = A.owned_global_ids
             y = A.apply(torch.from_numpy(u[ids])).numpy()
             out["apply"] = (ids, y)
+            # local layout (owned + ghost slots), used in place
+            ul = torch.zeros(A.n_local, dtype=torch.float64)
+            ul[: A.n_owned] = torch.from_numpy(u[ids])
+            yl = torch.empty_like(ul)
+            assert A.apply(ul, out=yl) is yl
+            assert np.array_equal(yl[: A.n_owned].numpy(), y)
             if kind == "cg_dir":
                 from oracle import ref_apply
 
@@ -123,6 +129,11 @@ def _worker(rank, world, port, kind, n, p, q):
             ids = A.owned_global_ids()
             y = A.apply(torch.from_numpy(u[ids])).numpy()
             out["apply"] = (ids, y)
+            ul = torch.zeros(A.n_local, dtype=torch.float64)
+            ul[: A.n_owned] = torch.from_numpy(u[ids])
+            yl = torch.empty_like(ul)
+            assert A.apply(ul, out=yl) is yl
+            assert np.array_equal(yl[: A.n_owned].numpy(), y)
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
         if rank == 0:
