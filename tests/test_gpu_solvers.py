@@ -113,6 +113,23 @@ def test_distributed_operator_single_rank_on_gpu():
         y = D.apply(torch.from_numpy(u[ids]).cuda()).cpu().numpy()
         ref = A.apply(u)
         assert rel_l2(y, ref[ids]) <= 1e-14
+        # DG-SIPG through the partitioned class (owned cells' volume terms, then faces)
+        from paper_2509_10226_b200 import basis as B, dofmap as Dm, operator as op, quadrature as Q
+        from paper_2509_10226_b200.geometry import GeometryData
+
+        p = 2
+        cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+        bas2 = B.tabulate_basis(p, cr, fr)
+        geo2 = GeometryData("affine", cr, fr, None, None, None, None)
+        dm2 = Dm.build_dof_map(m, p, "dg")
+        sipg = op.baseline_sipg_tau(m, p, 0.25)
+        Dg = DD.DistributedDgOperator(m, dm2, geo2, bas2, sipg, 0, 1, dirichlet_ids=range(6))
+        Ag = op.DgSipgOperator(m, dm2, geo2, bas2, sipg, dirichlet_ids=range(6))
+        ug = np.random.default_rng(2).uniform(-1, 1, dm2.n_global_dofs)
+        gids = Dg.owned_global_ids()
+        yg = torch.empty(Dg.n_local, dtype=torch.float64, device="cuda")
+        Dg.apply(torch.from_numpy(ug[gids]).cuda(), out=yg)
+        assert rel_l2(yg.cpu().numpy()[: Dg.n_owned], Ag.apply(ug)[gids]) <= 1e-14
     finally:
         if created:
             dist.destroy_process_group()
