@@ -70,22 +70,33 @@ class DeviceVecOps:
                                             self._st(p)))
 
 
-def pcg_loop(apply, diag, b, iters: int, allreduce=None, ops=None):
+def pcg_loop(apply, diag, b, iters: int, allreduce=None, ops=None, n_local=None):
     """Jacobi-PCG on (possibly partitioned) vectors.
 
     ``apply(p, out=q)`` computes the owned slice of A p; ``allreduce(t)`` sums a
-    small contiguous tensor across ranks in place (None: single process)."""
+    small contiguous tensor across ranks in place (None: single process).  With
+    ``n_local`` (a partitioned operator's local length) the search direction and
+    A p live in rank-local buffers that the operator uses in place; the vector
+    updates and dot products run on their owned prefix."""
     import torch
 
     ops = ops or DeviceVecOps()
     red = allreduce or (lambda t: None)
     n = b.numel()
-    x, r, z, p, q = (torch.empty_like(b) for _ in range(5))
+    x, r, z = (torch.empty_like(b) for _ in range(3))
+    if n_local is not None and n_local > n:
+        p_buf = torch.zeros(n_local, dtype=b.dtype, device=b.device)
+        q_buf = torch.empty(n_local, dtype=b.dtype, device=b.device)
+        p, q = p_buf[:n], q_buf[:n]
+        apply_pq = lambda: apply(p_buf, out=q_buf)  # noqa: E731
+    else:
+        p, q = torch.empty_like(b), torch.empty_like(b)
+        apply_pq = lambda: apply(p, out=q)  # noqa: E731
     sc = torch.zeros(iters + 1, 3, dtype=torch.float64, device=b.device)   # [rz, rr, pq] per iteration
     ops.init(b, diag, x, r, z, p, sc[0, 0], sc[0, 1])
     red(sc[0, 0:2])
     for k in range(iters):
-        apply(p, out=q)
+        apply_pq()
         ops.dot(p, q, sc[k, 2])
         red(sc[k, 2:3])
         ops.update(p, q, diag, x, r, z, sc[k, 0], sc[k, 2], sc[k + 1, 0], sc[k + 1, 1])

@@ -121,6 +121,10 @@ def _worker(rank, world, port, kind, n, p, q):
                 x, hist = pcg_loop(A.apply, torch.from_numpy(diag_g[ids]), b, 12,
                                    allreduce=lambda t: dist.all_reduce(t), ops=CpuVecOps())
                 out["pcg"] = (ids, x.numpy(), hist)
+                # the same solve with the direction / A p in rank-local buffers (in place)
+                x2, hist2 = pcg_loop(A.apply, torch.from_numpy(diag_g[ids]), b, 12,
+                                     allreduce=lambda t: dist.all_reduce(t), ops=CpuVecOps(), n_local=A.n_local)
+                assert np.array_equal(x2.numpy(), x.numpy()) and np.array_equal(hist2, hist)
         else:
             kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells) if kind == "helm" else None
             A = DD.DistributedDgOperator(m, dm, geo, bas, sipg, rank, world,

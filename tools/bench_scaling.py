@@ -105,12 +105,12 @@ def main():
     if a.config == "c5":
         b = torch.from_numpy(np.ascontiguousarray(np.where(dm.dirichlet_mask, 0.0, rng)[ids])).cuda()
         diag = A.diagonal()
-        pcg_loop(A.apply, diag, b, 2, allreduce=lambda t: dist.all_reduce(t))
+        pcg_loop(A.apply, diag, b, 2, allreduce=lambda t: dist.all_reduce(t), n_local=A.n_local)
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        x, hist = pcg_loop(A.apply, diag, b, a.iters, allreduce=lambda t: dist.all_reduce(t))
+        x, hist = pcg_loop(A.apply, diag, b, a.iters, allreduce=lambda t: dist.all_reduce(t), n_local=A.n_local)
         e1.record()
         e1.synchronize()
         solve = maxr(e0.elapsed_time(e1))
