@@ -230,6 +230,9 @@ def gpu_bench(args, rank, world):
     st = torch.cuda.current_stream().cuda_stream
     # weak scaling: each rank keeps ~n^3 x 6 cells (global mesh grows with the world size)
     n_glob = args.n if world == 1 else int(round(args.n * world ** (1.0 / 3.0)))
+    # multi-GPU transport: "p2p" = ghost DoFs read / RED-scattered by the cell kernel in
+    # the owner's buffers over NVLink (CUDA IPC), "nccl" = NCCL halo exchange
+    transport = os.environ.get("TMF_TRANSPORT", "p2p")
     problems = []
     for reorder in variants(args):
         for p in DEGREES:
@@ -242,23 +245,52 @@ def gpu_bench(args, rank, world):
             else:
                 from paper_2509_10226_b200.distributed import DistributedCgOperator
 
-                A = DistributedCgOperator(m, dm, geo, bas, rank, world, part=partition_of(m, world))
+                A = DistributedCgOperator(m, dm, geo, bas, rank, world, part=partition_of(m, world),
+                                          transport=transport)
+                if transport == "p2p":
+                    A.connect_ipc()
                 ids = A.owned_global_ids
                 local = A.local_op
             u_host = u_glob if ids is None else u_glob[ids]
             u = torch.from_numpy(np.ascontiguousarray(u_host)).cuda()
-            if ids is not None:
+            if ids is not None and transport == "p2p":
+                # the registered (peer-visible) local buffers, used in place
+                A.bufs.u[: len(u_host)].copy_(u)
+                u, y = A.bufs.u, A.bufs.y
+            elif ids is not None:
                 # rank-local layout (owned DoFs, then ghost slots): the partitioned apply
                 # works on these vectors in place (no owned <-> local copies)
                 ul = torch.zeros(A.n_local, dtype=torch.float64, device="cuda")
                 ul[: len(u_host)] = u
                 u = ul
-            y = torch.empty_like(u)
+                y = torch.empty_like(u)
+            else:
+                y = torch.empty_like(u)
             u_pin = torch.from_numpy(np.ascontiguousarray(u_host)).pin_memory()
             y_pin = torch.empty_like(u_pin).pin_memory()
             problems.append(dict(p=p, reorder=reorder, A=A, local=local, u=u, y=y, u_pin=u_pin, y_pin=y_pin,
                                  ndof=len(u_host), ndof_global=dm.n_global_dofs))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    # self-check of the peer-memory transport against the NCCL halo path (same plans)
+    p2p_check = None
+    if (world > 1 or args.dist) and transport == "p2p":
+        err = 0.0
+        for pr in problems:
+            A, n = pr["A"], pr["ndof"]
+            y1 = A.apply(pr["u"])
+            A.set_transport("nccl")
+            y2 = A.apply(pr["u"])
+            A.set_transport("p2p")
+            err = max(err, float(torch.linalg.vector_norm(y1[:n] - y2[:n]) / torch.linalg.vector_norm(y2[:n])))
+        t = torch.tensor([err], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        p2p_check = float(t[0])
+        if not p2p_check <= 1e-12:
+            for pr in problems:
+                pr["A"].set_transport("nccl")
+            transport = "nccl"
 
     def timed_apply(pr):
         """(total, cell-kernel) ms of one apply, CUDA events on the launch stream."""
@@ -357,6 +389,7 @@ def gpu_bench(args, rank, world):
     n_kern = sum(pr["local"].info["kernels_per_apply"] for pr in problems) * args.steps
     dofs_global = sum(pr["ndof_global"] for pr, _ in rec)
     return dict(total_ms=total_ms, dofs=dofs, dofs_global=dofs_global, n_glob=n_glob, e2e_s=e2e_s, per=per, clocks=clk.summary(),
+                transport=transport, p2p_check=p2p_check,
                 roofline={"bound": "tensor", "kernel": f"cell_apply_kernel ({dk})", "achieved": round(achieved, 3),
                           "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE, "unit": "TFLOP/s",
                           "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
@@ -440,8 +473,13 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload, "l2": "flushed (256 MiB write) before every apply",
                            "global_mesh": f"{r['n_glob']}^3 x 6",
-                           "parallelism": (f"{world}-way RCB domain decomposition, NCCL halo (weak scaling: "
-                                           f"~{args.n}^3 x 6 cells per GPU)") if world > 1 else "single GPU"},
+                           "parallelism": (f"{world}-way RCB domain decomposition, "
+                                           + ("ghost DoFs gathered / RED-scattered by the cell kernel in peer "
+                                              "memory (NVLink, CUDA IPC)" if r["transport"] == "p2p" else "NCCL halo")
+                                           + f" (weak scaling: ~{args.n}^3 x 6 cells per GPU)")
+                           if (world > 1 or args.dist) else "single GPU",
+                           "transport": r["transport"] if (world > 1 or args.dist) else None,
+                           "p2p_vs_nccl_rel_l2": r["p2p_check"]},
                 "per_degree": r["per"], "roofline": r["roofline"], "cpu_baseline": cpu,
                 "e2e": {"value": round(e2e_val, 4), "unit": unit, "h2d_bytes_per_step": r["h2d"],
                         "d2h_bytes_per_step": r["d2h"], "path": "Operator.apply_host_async(pinned host u, y) -> tmf_apply_host_async, one stream per plan, largest first"},

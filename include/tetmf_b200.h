@@ -157,6 +157,28 @@ int tmf_pcg_update(const double* p, const double* q, const double* d, double* x,
 int tmf_pcg_direction(const double* z, double* p, int64_t n, const double* rz_k,
                       const double* rz_next, void* stream);
 
+/* Multi-GPU without a halo exchange (SURVEY §8e "fused peer-store halo").  The
+ * plan's local layout is owned entries [0, n_own) then ghosts [n_own, n_own+n_ghost)
+ * (CG: DoFs, DG: cells); ghost e lives at element ghost_index[e] of rank
+ * ghost_rank[e]'s local vector.  peer_u / peer_y hold every rank's registered
+ * u / y device buffers as mapped on THIS device (tmf_ipc_open_handle for other
+ * processes; plain pointers when ranks share a device).  The cell kernel (CG)
+ * gathers ghost u with peer loads and scatters ghost y with peer REDs; the face
+ * kernel (DG) gathers ghost cells' u from the owner -- compute and exchange in one
+ * kernel over NVLink.  Applies must then pass the registered buffers; CG uses
+ * tmf_apply_stages: ZERO, cross-rank barrier, CELLS|FIXUP, cross-rank barrier.
+ * n_ranks = 0 switches peers off.  Needs the default DMMA cell engine. */
+int tmf_plan_set_peers(tmf_plan* plan, int32_t n_ranks, const uint64_t* peer_u, const uint64_t* peer_y,
+                       int32_t self_rank, int64_t n_own, int64_t n_ghost, const int32_t* ghost_rank,
+                       const int32_t* ghost_index);
+/* Dedicated device allocations (IPC-exportable at offset 0) and CUDA IPC handles
+ * (64 bytes) for mapping another process's buffers. */
+int tmf_alloc(int64_t bytes, int32_t device, void** dev_ptr);
+int tmf_free(void* dev_ptr);
+int tmf_ipc_get_handle(const void* dev_ptr, uint8_t handle[64]);
+int tmf_ipc_open_handle(const uint8_t handle[64], int32_t device, void** dev_ptr);
+int tmf_ipc_close_handle(void* dev_ptr);
+
 /* Hierarchical cell reordering (host-side setup; no GPU needed).  Writes the
  * permutation new_of_old (cell e moves to position new_of_old[e]), to be
  * applied like mesh.apply_cell_permutation (mesh.py:291-293).  Replaces the

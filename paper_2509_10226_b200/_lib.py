@@ -78,12 +78,22 @@ def lib():
         L.tmf_pcg_init.argtypes = [_v, _v, _v, _v, _v, _v, C.c_int64, _v, _v, _v]
         L.tmf_pcg_update.argtypes = [_v, _v, _v, _v, _v, _v, C.c_int64, _v, _v, _v, _v, _v]
         L.tmf_pcg_direction.argtypes = [_v, _v, C.c_int64, _v, _v, _v]
+        _u64p = C.POINTER(C.c_uint64)
+        L.tmf_plan_set_peers.argtypes = [C.c_void_p, C.c_int32, _u64p, _u64p, C.c_int32, C.c_int64, C.c_int64,
+                                         _ip, _ip]
+        L.tmf_alloc.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_void_p)]
+        L.tmf_free.argtypes = [C.c_void_p]
+        L.tmf_ipc_get_handle.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]
+        L.tmf_ipc_open_handle.argtypes = [C.POINTER(C.c_uint8), C.c_int32, C.POINTER(C.c_void_p)]
+        L.tmf_ipc_close_handle.argtypes = [C.c_void_p]
         L.tmf_last_error.restype = C.c_char_p
         L.tmf_version.restype = C.c_char_p
         for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
                      "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg",
                      "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs",
-                     "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction"):
+                     "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction",
+                     "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle", "tmf_ipc_open_handle",
+                     "tmf_ipc_close_handle"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -92,7 +102,8 @@ def lib():
 EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
             "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
             "tmf_build_faces", "tmf_build_cg_dofs", "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update",
-            "tmf_pcg_direction", "tmf_last_error", "tmf_version")
+            "tmf_pcg_direction", "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle",
+            "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_last_error", "tmf_version")
 
 
 def check(rc: int) -> None:

@@ -243,6 +243,14 @@ struct tmf_plan {
   double patch_ratio = 1.0;   // unique patch DoFs / unmasked cell-DoF slots
   int4* pmeta = nullptr;
   uint4* prec = nullptr;
+  // multi-GPU peer-memory ghost access (tmf_plan_set_peers)
+  tmf::PeerArgs peer{};
+  const double** peer_u_tab = nullptr;   // device arrays of device pointers
+  double** peer_y_tab = nullptr;
+  int* ghost_rank = nullptr;
+  int* ghost_index = nullptr;
+  const double* peer_self_u = nullptr;   // this rank's registered buffers
+  double* peer_self_y = nullptr;
   int4* if_chunks = nullptr;
   int* if_cm = nullptr;
   int* if_cp = nullptr;
@@ -274,6 +282,7 @@ struct tmf_plan {
     a.frags = cell_frags;
     a.n_cells = c1 - c0;
     a.nc = nc;
+    if (!dg) a.peer = peer;   // CG ghost DoFs over peer memory (DG: the face kernel's ghost cells)
     if (local && c0 == 0 && c1 == n_cells) {
       a.pmeta = pmeta;
       a.prec = prec;
@@ -295,6 +304,7 @@ struct tmf_plan {
     a.n_chunks = boundary ? n_bf_chunks : n_if_chunks;
     a.n_dpc = N;
     a.nc = nc;
+    a.peer = peer;
     return a;
   }
   tmf::FaceGeoArgs face_geo_args(bool boundary) const {
@@ -319,7 +329,8 @@ struct tmf_plan {
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
-                    (void*)pmeta, (void*)prec})
+                    (void*)pmeta, (void*)prec,
+                    (void*)peer_u_tab, (void*)peer_y_tab, (void*)ghost_rank, (void*)ghost_index})
       if (p) cudaFree(p);
   }
 };
@@ -492,6 +503,8 @@ int tmf_apply_stages(tmf_plan* P, const double* u, double* y, int stages, int64_
   if (!P || !u || !y) return fail(TMF_EINVAL, "null argument");
   if (cell_begin < 0 || cell_end > P->n_cells || cell_begin > cell_end)
     return fail(TMF_EINVAL, "bad cell range");
+  if (P->peer.u && (u != P->peer_self_u || (!P->dg && y != P->peer_self_y)))
+    return fail(TMF_EINVAL, "with peers, u (and y for CG) must be this rank's registered buffers");
   TMF_CUDA(cudaSetDevice(P->dev));
   cudaStream_t st = (cudaStream_t)stream;
   bool ok = true;
@@ -784,6 +797,90 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   return TMF_OK;
 }
 
+int tmf_plan_set_peers(tmf_plan* P, int32_t n_ranks, const uint64_t* peer_u, const uint64_t* peer_y,
+                       int32_t self_rank, int64_t n_own, int64_t n_ghost, const int32_t* ghost_rank,
+                       const int32_t* ghost_index) {
+  if (!P) return fail(TMF_EINVAL, "null plan");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  for (void* q : {(void*)P->peer_u_tab, (void*)P->peer_y_tab, (void*)P->ghost_rank, (void*)P->ghost_index})
+    if (q) cudaFree(q);
+  P->peer_u_tab = nullptr;
+  P->peer_y_tab = nullptr;
+  P->ghost_rank = nullptr;
+  P->ghost_index = nullptr;
+  P->peer = tmf::PeerArgs{};
+  P->peer_self_u = nullptr;
+  P->peer_self_y = nullptr;
+  if (n_ranks == 0) return TMF_OK;
+  if (n_ranks < 0 || !peer_u || self_rank < 0 || self_rank >= n_ranks || n_own < 0 || n_ghost < 0 ||
+      (n_ghost && (!ghost_rank || !ghost_index)))
+    return fail(TMF_EINVAL, "bad peer description");
+  if (!P->dg && !peer_y) return fail(TMF_EINVAL, "a CG plan needs the peers' y buffers (ghost RED)");
+  if (P->engine == 2 || P->local)
+    return fail(TMF_EINVAL, "peer-memory ghosts need the DMMA cell engine (no DFMA engine / patches)");
+  const int64_t n_entries = P->dg ? P->n_cells : P->n_scalar;
+  if (n_own + n_ghost != n_entries)
+    return fail(TMF_EINVAL, "n_own + n_ghost must equal the plan's local " +
+                                std::string(P->dg ? "cells" : "DoFs"));
+  for (int64_t i = 0; i < n_ghost; ++i)
+    if (ghost_rank[i] < 0 || ghost_rank[i] >= n_ranks || ghost_rank[i] == self_rank || ghost_index[i] < 0)
+      return fail(TMF_EINVAL, "ghost owner rank / index out of range");
+  size_t total = 0;
+  int rc;
+  if ((rc = upload(reinterpret_cast<uint64_t**>(&P->peer_u_tab), peer_u, (size_t)n_ranks, &total))) return rc;
+  if (peer_y && (rc = upload(reinterpret_cast<uint64_t**>(&P->peer_y_tab), peer_y, (size_t)n_ranks, &total)))
+    return rc;
+  if (n_ghost) {
+    if ((rc = upload(&P->ghost_rank, ghost_rank, (size_t)n_ghost, &total))) return rc;
+    if ((rc = upload(&P->ghost_index, ghost_index, (size_t)n_ghost, &total))) return rc;
+  }
+  P->peer.u = P->peer_u_tab;
+  P->peer.y = peer_y ? P->peer_y_tab : nullptr;
+  P->peer.rank = P->ghost_rank;
+  P->peer.idx = P->ghost_index;
+  P->peer.n_own = n_own;
+  P->peer_self_u = reinterpret_cast<const double*>(peer_u[self_rank]);
+  P->peer_self_y = peer_y ? reinterpret_cast<double*>(peer_y[self_rank]) : nullptr;
+  return TMF_OK;
+}
+
+int tmf_alloc(int64_t bytes, int32_t device, void** out) {
+  if (!out || bytes < 0) return fail(TMF_EINVAL, "bad argument");
+  *out = nullptr;
+  TMF_CUDA(cudaSetDevice(device));
+  TMF_CUDA(cudaMalloc(out, bytes > 0 ? (size_t)bytes : 1));
+  return TMF_OK;
+}
+
+int tmf_free(void* p) {
+  if (p) TMF_CUDA(cudaFree(p));
+  return TMF_OK;
+}
+
+int tmf_ipc_get_handle(const void* dev_ptr, uint8_t handle[64]) {
+  if (!dev_ptr || !handle) return fail(TMF_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  TMF_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  return TMF_OK;
+}
+
+int tmf_ipc_open_handle(const uint8_t handle[64], int32_t device, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(TMF_EINVAL, "null argument");
+  *dev_ptr = nullptr;
+  TMF_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  TMF_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return TMF_OK;
+}
+
+int tmf_ipc_close_handle(void* dev_ptr) {
+  if (dev_ptr) TMF_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return TMF_OK;
+}
+
 int tmf_plan_destroy(tmf_plan* plan) {
   if (!plan) return TMF_OK;
   cudaSetDevice(plan->dev);
@@ -800,6 +897,10 @@ int tmf_plan_get_info(const tmf_plan* plan, tmf_plan_info* info) {
 int tmf_apply(tmf_plan* P, const double* u, double* y, void* stream) {
   if (!P || !u || !y) return fail(TMF_EINVAL, "null argument");
   if (u == y) return fail(TMF_EINVAL, "u and y must not alias");
+  if (P->peer.u && !P->dg)
+    return fail(TMF_EINVAL, "a CG plan with peers needs tmf_apply_stages with cross-rank barriers "
+                            "(ZERO | barrier | CELLS | FIXUP | barrier)");
+  if (P->peer.u && u != P->peer_self_u) return fail(TMF_EINVAL, "u must be this rank's registered buffer");
   TMF_CUDA(cudaSetDevice(P->dev));
   return launch_apply(P, u, y, (cudaStream_t)stream, nullptr);
 }

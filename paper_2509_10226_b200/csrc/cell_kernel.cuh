@@ -48,6 +48,7 @@ struct CellArgs {
   const void* __restrict__ prec = nullptr;
   int numax = 0;                   // max unique DoFs of a patch (even)
   int recmax = 0;                  // max record bytes (multiple of 16)
+  PeerArgs peer;                   // multi-GPU: ghost DoFs read / scattered over peer memory
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the
@@ -113,8 +114,10 @@ struct CellShape {
 // PF: software-prefetch the next super-tile's gathered u and geometry (indices 2 ahead)
 // BLK: each warp takes a contiguous run of super-tiles instead of a grid-strided set
 // SKEW: issue GEMM1 of the next point tile before the D action of the current one
+// PEER: ghost DoFs through peer memory (multi-GPU, CellArgs::peer); a separate
+// instantiation so the single-GPU kernel carries no ghost test (it costs 10-20 %)
 template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT_ = 0, int MINB = 1, bool PF = false,
-          bool BLK = false, bool SKEW = false>
+          bool BLK = false, bool SKEW = false, bool PEER = false>
 __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   using S = CellShape<N, Q, MASS>;
   constexpr int MT = MT_ ? MT_ : S::MT;
@@ -169,7 +172,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
 #pragma unroll
       for (int kk = 0; kk < S::KK; ++kk) {
         const int g = nidx[m][kk];
-        av[m][kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + cmp) : 0.0;
+        if (PEER)
+          av[m][kk] = (g >= 0) ? __ldg(peer_src(a.peer, a.u, g, a.nc, cmp)) : 0.0;
+        else
+          av[m][kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + cmp) : 0.0;
       }
       const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * (ok ? c : 0));
       const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
@@ -344,12 +350,19 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
                 *dst = yacc[m][nj][i];
             } else {
               const int64_t g = __ldg(a.dofs + cell[m] * N + j);
-              if (g >= 0) atomicAdd(a.y + g * a.nc + comp, yacc[m][nj][i]);
+              if (g >= 0) {
+                if (PEER)
+                  atomicAdd(peer_dst(a.peer, a.y, g, a.nc, comp), yacc[m][nj][i]);
+                else
+                  atomicAdd(a.y + g * a.nc + comp, yacc[m][nj][i]);
+              }
             }
           }
         }
     }
   }
+  // peer REDs must be visible system-wide before the caller's cross-rank barrier
+  if (PEER && a.peer.y != nullptr) __threadfence_system();
 }
 
 // y[c] = u[c] on strongly constrained DoFs (identity rows, operator.py:327-328)

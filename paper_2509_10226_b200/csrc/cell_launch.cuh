@@ -14,11 +14,11 @@
 namespace tmf {
 
 template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PF = false, bool BLK = false,
-          bool SKEW = false>
+          bool SKEW = false, bool PEER = false>
 static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = CellShape<N, Q, MASS>;
   constexpr int MTE = MT ? MT : S::MT;
-  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK, SKEW>;
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK, SKEW, PEER>;
   if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
@@ -120,6 +120,11 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
                                  int variant) {
   using S = CellShape<N, Q, MASS>;
   constexpr int BLOCK = S::SMEM > 96 * 1024 ? 512 : 256;
+  if (!DG && a.peer.u != nullptr && !info) {   // multi-GPU peer ghosts: the default CTA shape
+    if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, false, false, true>(a, n_sm, st, info);
+    if (N == 35) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1, false, false, false, true>(a, n_sm, st, info);
+    return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, false, false, false, true>(a, n_sm, st, info);
+  }
   if (!DG && !MASS) {
     if (variant == 1) return launch_cell_v<N, Q, MASS, DG, BLOCK, 2, 1>(a, n_sm, st, info);
     if (variant == 2) return launch_cell_v<N, Q, MASS, DG, BLOCK, 1, (BLOCK == 256 ? 3 : 1)>(a, n_sm, st, info);

@@ -17,6 +17,36 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Multi-GPU without a halo exchange: entries of the rank-local layout at or beyond
+// n_own (ghost DoFs for CG, ghost cells for DG) live on their owner rank; ghost
+// entry e is element idx[e] of owner rank[e]'s local vector, reached through the
+// owner's mapped device pointers u[rank] / y[rank] (NVLink peer memory, or this
+// device's own buffers when ranks are emulated on one GPU).  The gather is a peer
+// load, the CG scatter a peer RED, fused into the cell / face kernels.
+struct PeerArgs {
+  const double* const* __restrict__ u = nullptr;   // nullptr: off
+  double* const* __restrict__ y = nullptr;
+  const int* __restrict__ rank = nullptr;
+  const int* __restrict__ idx = nullptr;
+  int64_t n_own = 0;
+};
+
+__device__ __forceinline__ const double* peer_src(const PeerArgs& p, const double* u, int64_t e, int nc,
+                                                  int comp) {
+  if (p.u != nullptr && e >= p.n_own) {
+    const int64_t g = e - p.n_own;
+    return p.u[__ldg(p.rank + g)] + (int64_t)__ldg(p.idx + g) * nc + comp;
+  }
+  return u + e * nc + comp;
+}
+__device__ __forceinline__ double* peer_dst(const PeerArgs& p, double* y, int64_t e, int nc, int comp) {
+  if (p.y != nullptr && e >= p.n_own) {
+    const int64_t g = e - p.n_own;
+    return p.y[__ldg(p.rank + g)] + (int64_t)__ldg(p.idx + g) * nc + comp;
+  }
+  return y + e * nc + comp;
+}
+
 struct Vec3 {
   double x, y, z;
 };

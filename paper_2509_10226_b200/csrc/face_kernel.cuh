@@ -53,6 +53,7 @@ struct FaceArgs {
   int64_t n_chunks;
   int n_dpc;
   int nc;
+  PeerArgs peer;                      // multi-GPU: ghost cells' u read from their owner (n_own = cells)
 };
 
 // Per-face geometry, computed once at plan creation by face_geometry_kernel and
@@ -220,7 +221,7 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 // L2; the next chunk's tables are prefetched with cp.async into a second shared
 // buffer while the current chunk computes (one barrier per chunk, no load latency).
 template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool TPF = false>
+          bool TPF = false, bool PEER = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
   constexpr int TAB = (BOUNDARY ? 1 : 2) * S::NFRAG * 32;   // doubles per staged table set
@@ -328,7 +329,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
         nap[kk] = 0.0;
         if (n_cm >= 0 && j < N) {
           nam[kk] = __ldg(a.u + ((int64_t)n_cm * N + __ldg(perm_m + j)) * a.nc + comp);
-          if (!BOUNDARY) nap[kk] = __ldg(a.u + ((int64_t)n_cp * N + __ldg(perm_p + j)) * a.nc + comp);
+          if (!BOUNDARY) {
+            // DG ghost cell (partitioned apply): its u is read from the owner rank
+            if (PEER && n_cp >= a.peer.n_own) {
+              const int64_t gc = n_cp - a.peer.n_own;
+              nap[kk] = __ldg(a.peer.u[__ldg(a.peer.rank + gc)] +
+                              ((int64_t)__ldg(a.peer.idx + gc) * N + __ldg(perm_p + j)) * a.nc + comp);
+            } else {
+              nap[kk] = __ldg(a.u + ((int64_t)n_cp * N + __ldg(perm_p + j)) * a.nc + comp);
+            }
+          }
         }
       }
     };

@@ -10,11 +10,11 @@
 namespace tmf {
 
 template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool TPF = false>
+          bool TPF = false, bool PEER = false>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShape<N, QF>;
   constexpr int SMEM = (TPF ? 2 : 1) * (BND ? 1 : 2) * S::NFRAG * 32 * 8;
-  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, TPF>;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, TPF, PEER>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   if (info) {
     info->nfrag = S::NFRAG;
@@ -39,6 +39,10 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
 template <int N, int QF, bool BND>
 static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info,
                                  int variant) {
+  if (!BND && a.peer.u != nullptr && !info) {   // multi-GPU: plus-side ghost cells from peer memory
+    if (N <= 10) return launch_face_v<N, QF, BND, 1, 3, 256, true, false, true>(a, n_sm, st, info);
+    return launch_face_v<N, QF, BND, 2, 2, 256, true, false, true>(a, n_sm, st, info);
+  }
   if (variant == 1) return launch_face_v<N, QF, BND, 0, 3>(a, n_sm, st, info);
   if (variant == 2) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
   if (variant == 3) return launch_face_v<N, QF, BND, 1, 2>(a, n_sm, st, info);

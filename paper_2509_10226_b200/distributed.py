@@ -84,6 +84,8 @@ class CgSubdomain:
     reverse: Exchange             # y: ghosts -> owners (added)
     n_interior_cells: int = 0     # local cells [0, n) touch no ghost DoF (overlap the forward halo)
     cells_global: np.ndarray = None   # local cell -> global cell
+    ghost_owner: np.ndarray = None    # (n_local - n_owned,) owner rank of each ghost DoF
+    ghost_index: np.ndarray = None    # its index in the owner's local layout
 
 
 @dataclass
@@ -96,6 +98,19 @@ class DgSubdomain:
     interior_face_g: np.ndarray   # local interior face -> global interior face
     boundary_face_g: np.ndarray   # local boundary face -> global boundary face (-1 = artificial)
     forward: Exchange             # cell blocks of u: owners -> ghosts (cell indices)
+    ghost_owner: np.ndarray = None    # (n_ghost_cells,) owner rank of each ghost cell
+    ghost_index: np.ndarray = None    # its cell index in the owner's local layout
+
+
+def _index_in_owner(owner: np.ndarray, k: int) -> np.ndarray:
+    """Position of every entry among the entries of the same owner, ascending ids:
+    the owner's local index of an owned DoF / cell (owned entries come first, in
+    ascending global order, in every subdomain layout)."""
+    order = np.argsort(owner, kind="stable")
+    starts = np.concatenate([[0], np.cumsum(np.bincount(owner, minlength=k))[:-1]])
+    idx = np.empty(len(owner), dtype=np.int64)
+    idx[order] = np.arange(len(owner)) - starts[owner[order]]
+    return idx
 
 
 def _local_mesh(mesh: TetMesh, cells_g: np.ndarray) -> tuple[TetMesh, np.ndarray]:
@@ -157,8 +172,10 @@ def build_cg_subdomain(mesh: TetMesh, cell_dofs: np.ndarray, dirichlet_mask: np.
     cells_g = np.concatenate([cells_g[~touches_ghost], cells_g[touches_ghost]])  # interior first
     lmesh, _ = _local_mesh(mesh, cells_g)
     lcd = g2l[cell_dofs[cells_g].astype(np.int64)].astype(np.int32).reshape(-1, nd)
+    in_owner = _index_in_owner(owner, k)
     return CgSubdomain(rank, lmesh, lcd, dirichlet_mask[l2g], l2g, len(own), fwd, rev,
-                       int(np.count_nonzero(~touches_ghost)), cells_g)
+                       int(np.count_nonzero(~touches_ghost)), cells_g,
+                       owner[gh].astype(np.int32), in_owner[gh].astype(np.int32))
 
 
 def _face_index_tables(mesh: TetMesh):
@@ -217,7 +234,9 @@ def build_dg_subdomain(mesh: TetMesh, part: np.ndarray, rank: int, k: int,
         fwd.peers.append(s)
         fwd.send[s] = np.searchsorted(owned, gh_s)             # local owned cell index
         fwd.recv[s] = n_own + np.flatnonzero(part[ghosts] == s)
-    return DgSubdomain(rank, lmesh, cells_g, n_own, dfaces, if_g, bf_g, fwd)
+    in_owner = _index_in_owner(part.astype(np.int64), k)
+    return DgSubdomain(rank, lmesh, cells_g, n_own, dfaces, if_g, bf_g, fwd,
+                       part[ghosts].astype(np.int32), in_owner[ghosts].astype(np.int32))
 
 
 class HaloExchange:
@@ -285,6 +304,202 @@ def _stream_of(t):
     return torch.cuda.current_stream(t.device).cuda_stream if t.is_cuda else 0
 
 
+# --------------------------------------------------------------------------- peer memory
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device allocation (zero-copy tensor)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+
+class PeerBuffers:
+    """This rank's registered local u / y vectors for the peer-memory transport:
+    dedicated device allocations (CUDA-IPC exportable at offset 0) wrapped as
+    tensors.  Peers read ghost u from them and RED ghost y into them."""
+
+    def __init__(self, n_local: int, device):
+        import ctypes as C
+
+        import torch
+
+        from . import _lib
+
+        self.n, self.device = int(n_local), device
+        self.ptrs = []
+        for _ in range(2):
+            p = C.c_void_p()
+            _lib.check(_lib.lib().tmf_alloc(C.c_int64(8 * max(self.n, 1)), int(device.index or 0), C.byref(p)))
+            self.ptrs.append(p.value)
+        self.u = torch.as_tensor(_CudaArray(self.ptrs[0], self.n), device=device)
+        self.y = torch.as_tensor(_CudaArray(self.ptrs[1], self.n), device=device)
+        self.u.zero_()
+        self.y.zero_()
+        self.opened = []
+
+    def handles(self):
+        import ctypes as C
+
+        from . import _lib
+
+        out = []
+        for p in self.ptrs:
+            h = (C.c_uint8 * 64)()
+            _lib.check(_lib.lib().tmf_ipc_get_handle(C.c_void_p(p), h))
+            out.append(bytes(h))
+        return out
+
+    def open(self, handle: bytes) -> int:
+        import ctypes as C
+
+        from . import _lib
+
+        h = (C.c_uint8 * 64).from_buffer_copy(handle)
+        p = C.c_void_p()
+        _lib.check(_lib.lib().tmf_ipc_open_handle(h, int(self.device.index or 0), C.byref(p)))
+        self.opened.append(p.value)
+        return p.value
+
+    def close(self):
+        import ctypes as C
+
+        from . import _lib
+
+        if _lib is None or not hasattr(self, "ptrs"):
+            return
+        for p in self.opened:
+            _lib.lib().tmf_ipc_close_handle(C.c_void_p(p))
+        self.opened = []
+        for p in self.ptrs:
+            _lib.lib().tmf_free(C.c_void_p(p))
+        self.ptrs = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
+
+class _PeerTransport:
+    """Multi-GPU apply without a halo exchange (transport="p2p"): ghost entries are
+    read (and, for CG, RED-scattered) by the cell / face kernels directly in the
+    owner's registered buffers over NVLink peer memory (tmf_plan_set_peers), with
+    two cross-rank barriers per apply.  ``connect_ipc`` maps the peers' buffers of
+    other processes (CUDA IPC); ``connect_local`` links operators that share one
+    process (ranks emulated on one device: same kernels, same peer tables)."""
+
+    def _peer_init(self, n_local, ghost_owner, ghost_index, n_own):
+        self.bufs = PeerBuffers(n_local, self.device)
+        self._ghost_owner = np.ascontiguousarray(ghost_owner, dtype=np.int32)
+        self._ghost_index = np.ascontiguousarray(ghost_index, dtype=np.int32)
+        self._peer_n_own = int(n_own)
+        self._bar = None
+        self.connected = False
+
+    def connect_peers(self, ptrs_u, ptrs_y):
+        import ctypes as C
+
+        from . import _lib
+
+        assert len(ptrs_u) == self.world
+        u64 = (C.c_uint64 * self.world)(*[int(p) for p in ptrs_u])
+        y64 = (C.c_uint64 * self.world)(*[int(p) for p in ptrs_y]) if ptrs_y is not None else None
+        gr, gi = self._ghost_owner, self._ghost_index
+        _lib.check(_lib.lib().tmf_plan_set_peers(
+            self.local_op._plan, self.world, u64, y64, self.rank, self._peer_n_own, len(gr),
+            _lib.ptr(gr, C.c_int32), _lib.ptr(gi, C.c_int32)))
+        self._peer_ptrs = (list(ptrs_u), None if ptrs_y is None else list(ptrs_y))
+        self.connected = True
+
+    def set_transport(self, transport: str):
+        """Switch a connected operator between the peer-memory path and the NCCL halo
+        path (e.g. to cross-check them); the plan's peer tables follow."""
+        import ctypes as C
+
+        from . import _lib
+
+        if transport == "nccl":
+            if getattr(self, "connected", False):
+                _lib.check(_lib.lib().tmf_plan_set_peers(self.local_op._plan, 0, None, None, 0, 0, 0, None, None))
+        elif transport == "p2p":
+            if not getattr(self, "_peer_ptrs", None):
+                raise RuntimeError("peer transport: connect first")
+            self.connect_peers(*self._peer_ptrs)
+        else:
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
+        del C
+
+    def connect_ipc(self, group=None):
+        """Exchange CUDA-IPC handles of every rank's registered buffers (collective)."""
+        import torch.distributed as dist
+
+        mine = self.bufs.handles()
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        pu, py = [], []
+        for r in range(self.world):
+            if r == self.rank:
+                pu.append(self.bufs.ptrs[0])
+                py.append(self.bufs.ptrs[1])
+            else:
+                pu.append(self.bufs.open(allh[r][0]))
+                py.append(self.bufs.open(allh[r][1]))
+        self._group = group
+        self.connect_peers(pu, py if self._peer_writes_y else None)
+
+    @staticmethod
+    def connect_local(ops):
+        """Link the rank operators of one process (emulated ranks on one device)."""
+        pu = [op.bufs.ptrs[0] for op in ops]
+        py = [op.bufs.ptrs[1] for op in ops]
+        for op in ops:
+            op.connect_peers(pu, py if op._peer_writes_y else None)
+
+    def barrier(self):
+        """Cross-rank barrier ordered on the current stream (NCCL: a 1-element
+        all_reduce; other backends: device sync + host barrier)."""
+        import torch
+        import torch.distributed as dist
+
+        if not dist.is_initialized() or self.world == 1:
+            return
+        group = getattr(self, "_group", None)
+        if dist.get_backend(group) == "nccl":
+            if self._bar is None:
+                self._bar = torch.zeros(1, dtype=torch.float64, device=self.device)
+            dist.all_reduce(self._bar, group=group)
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=group)
+
+    # phases (apply = stage_in | barrier | compute | barrier | result)
+    def p2p_stage_in(self, u):
+        from . import _lib
+
+        n = self.n_owned
+        if u.data_ptr() != self.bufs.u.data_ptr():
+            self.bufs.u[:n].copy_(u[:n])
+        if self._peer_writes_y:   # CG: zero y before any peer can RED into it
+            self.local_op.apply_stages(self.bufs.u.data_ptr(), self.bufs.y.data_ptr(), _lib.STAGE_ZERO, 0, 0,
+                                       _stream_of(self.bufs.u))
+
+    def p2p_result(self, out):
+        return _local_result(self.bufs.y, out, self.n_owned)
+
+    def _apply_p2p(self, u, out):
+        if not self.connected:
+            raise RuntimeError("peer transport: call connect_ipc() (or connect_local) first")
+        self.p2p_stage_in(u)
+        self.barrier()
+        ev = self._event_pair() if hasattr(self, "_event_pair") else None
+        self.p2p_compute()
+        if ev is not None:
+            self._close_events(ev)
+        self.barrier()
+        return self.p2p_result(out)
+
+
 def _local_buffers(op, u, out, n):
     """(u_loc, y_loc) for one apply: caller tensors of the local length are used in
     place; owned-length input is copied into the operator's local buffer."""
@@ -308,7 +523,7 @@ def _local_result(y_loc, out, n):
     return out
 
 
-class DistributedCgOperator:
+class DistributedCgOperator(_PeerTransport):
     """CG Laplace apply on a k-way partition: y_owned = A u_owned.
 
     ``local_factory(mesh, dofmap, geometry, basis)`` may supply the local apply
@@ -316,12 +531,15 @@ class DistributedCgOperator:
     kernels run on the rank's current CUDA device."""
 
     def __init__(self, mesh, dofmap, geometry, basis, rank: int, world: int, part=None,
-                 device=None, local_factory=None):
+                 device=None, local_factory=None, transport: str = "nccl"):
         import torch
 
         from .dofmap import DoFMap
         from .operator import CgPoissonOperator, OperatorConfig
 
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
         self.rank, self.world = rank, world
         self.part = partition_cells(mesh, world) if part is None else part
         self.sub = build_cg_subdomain(mesh, dofmap.cell_dofs, dofmap.dirichlet_mask, self.part, rank, world)
@@ -346,6 +564,11 @@ class DistributedCgOperator:
         self.rev = HaloExchange(self.sub.reverse, 1, self.device)
         self.u_loc = torch.zeros(n_local, dtype=torch.float64, device=self.device)
         self.y_loc = torch.zeros(n_local, dtype=torch.float64, device=self.device)
+        self._peer_writes_y = True
+        if transport == "p2p":
+            if self.local_op is None:
+                raise ValueError("the p2p transport needs the B200 local plan")
+            self._peer_init(n_local, self.sub.ghost_owner, self.sub.ghost_index, self.sub.n_owned)
 
     @property
     def n_owned(self) -> int:
@@ -394,6 +617,8 @@ class DistributedCgOperator:
         slots of ``u`` are overwritten by the halo, ``out[:n_owned]`` is the result)."""
         from . import _lib
 
+        if self.transport == "p2p":
+            return self._apply_p2p(u_owned, out)
         n = self.sub.n_owned
         u_loc, y_loc = _local_buffers(self, u_owned, out, n)
         reqs = self.fwd.start(u_loc)
@@ -416,6 +641,14 @@ class DistributedCgOperator:
         self.rev.reverse_add(y_loc)
         return _local_result(y_loc, out, n)
 
+    def p2p_compute(self):
+        """All local cells in one kernel: ghost u by peer loads, ghost y by peer REDs."""
+        from . import _lib
+
+        b = self.bufs
+        self.local_op.apply_stages(b.u.data_ptr(), b.y.data_ptr(), _lib.STAGE_CELLS | _lib.STAGE_FIXUP, 0, None,
+                                   _stream_of(b.u))
+
     def diagonal(self):
         """Owned slice of diag(A): local matrix-free diagonal + reverse halo."""
         import torch
@@ -430,14 +663,19 @@ class DistributedCgOperator:
         return d[: self.sub.n_owned].clone()
 
 
-class DistributedDgOperator:
+class DistributedDgOperator(_PeerTransport):
     """DG-SIPG / Helmholtz apply on a k-way partition (forward halo of ghost cells only).
 
     ``kind`` = "sipg" or "helmholtz" (scalar mass + per-cell kappa, KappaHelmholtzOperator)."""
 
     def __init__(self, mesh, dofmap, geometry, basis, sipg, rank: int, world: int, kind="sipg",
-                 dirichlet_ids=(), kappa=None, mass_scale=1.0, part=None, device=None, local_factory=None):
+                 dirichlet_ids=(), kappa=None, mass_scale=1.0, part=None, device=None, local_factory=None,
+                 transport: str = "nccl"):
         import torch
+
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
 
         from .dofmap import DoFMap
         from .operator import DgSipgOperator, KappaHelmholtzOperator, OperatorConfig, SipgConfig
@@ -480,6 +718,13 @@ class DistributedDgOperator:
         n_local = n_loc_cells * self.block
         self.u_loc = torch.zeros(n_local, dtype=torch.float64, device=self.device)
         self.y_loc = torch.zeros(n_local, dtype=torch.float64, device=self.device)
+        self._peer_writes_y = False   # DG: ghost cells' u is read from the owner, nothing is written back
+        if transport == "p2p":
+            if self.local_op is None:
+                raise ValueError("the p2p transport needs the B200 local plan")
+            if nc != 1:
+                raise ValueError("the p2p transport supports scalar DG (n_components = 1)")
+            self._peer_init(n_local, sub.ghost_owner, sub.ghost_index, sub.n_owned_cells)
 
     @property
     def n_owned(self) -> int:
@@ -499,6 +744,8 @@ class DistributedDgOperator:
         volume terms are never needed), then all face terms."""
         from . import _lib
 
+        if self.transport == "p2p":
+            return self._apply_p2p(u_owned, out)
         n = self.n_owned
         u_loc, y_loc = _local_buffers(self, u_owned, out, n)
         reqs = self.fwd.start(u_loc)
@@ -512,3 +759,12 @@ class DistributedDgOperator:
             self.fwd.finish(reqs, u_loc, add=False)
             op.apply_stages(up, yp, _lib.STAGE_FACES, 0, 0, st)
         return _local_result(y_loc, out, n)
+
+    def p2p_compute(self):
+        """Owned cells' volume terms, then every face (plus-side ghost cells' u by peer loads)."""
+        from . import _lib
+
+        b = self.bufs
+        st = _stream_of(b.u)
+        self.local_op.apply_stages(b.u.data_ptr(), b.y.data_ptr(), _lib.STAGE_CELLS, 0, self.sub.n_owned_cells, st)
+        self.local_op.apply_stages(b.u.data_ptr(), b.y.data_ptr(), _lib.STAGE_FACES, 0, 0, st)

@@ -235,3 +235,31 @@ def test_cg_subdomain_interior_cells_touch_no_ghosts():
         assert np.array_equal(dm.cell_dofs[sub.cells_global], sub.l2g[sub.cell_dofs])
         seen.append(sub.cells_global)
     assert np.array_equal(np.sort(np.concatenate(seen)), np.arange(m.n_cells))
+
+
+def test_ghost_owner_maps_point_at_the_owners_entries():
+    """Peer-memory transport tables: ghost e of rank r is entry ghost_index[e] of rank
+    ghost_owner[e]'s local layout, which holds the same global DoF / cell, owned there."""
+    from paper_2509_10226_b200 import distributed as DD, dofmap as D, mesh as M
+
+    m = M.kuhn_cube_mesh(5, seed=1)
+    dm = D.build_dof_map(m, 2, "cg", 1, (0, 4))
+    for k in (2, 4, 8):
+        part = DD.partition_cells(m, k)
+        subs = [DD.build_cg_subdomain(m, dm.cell_dofs, dm.dirichlet_mask, part, r, k) for r in range(k)]
+        for r, s in enumerate(subs):
+            gh = s.l2g[s.n_owned:]
+            assert len(gh) == len(s.ghost_owner) == len(s.ghost_index)
+            assert np.all(s.ghost_owner != r)
+            for o in np.unique(s.ghost_owner):
+                sel = s.ghost_owner == o
+                assert np.all(s.ghost_index[sel] < subs[o].n_owned)
+                assert np.array_equal(subs[o].l2g[s.ghost_index[sel]], gh[sel])
+        dsubs = [DD.build_dg_subdomain(m, part, r, k) for r in range(k)]
+        for r, s in enumerate(dsubs):
+            gh = s.cell_l2g[s.n_owned_cells:]
+            assert np.all(s.ghost_owner != r)
+            for o in np.unique(s.ghost_owner):
+                sel = s.ghost_owner == o
+                assert np.all(s.ghost_index[sel] < dsubs[o].n_owned_cells)
+                assert np.array_equal(dsubs[o].cell_l2g[s.ghost_index[sel]], gh[sel])

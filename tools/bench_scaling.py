@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     a = ap.parse_args()
 
     import torch
@@ -66,12 +67,15 @@ def main():
         dm = D.build_dof_map(m, p, "dg")
         kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
         A = DD.DistributedDgOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n), rank, world,
-                                     kind="helmholtz", dirichlet_ids=range(6), kappa=kap, part=part)
+                                     kind="helmholtz", dirichlet_ids=range(6), kappa=kap, part=part,
+                                     transport=a.transport)
         ids = A.owned_global_ids()
     else:
         dm = D.build_dof_map(m, p, "cg", 1, tuple(range(6)))
-        A = DD.DistributedCgOperator(m, dm, geo, bas, rank, world, part=part)
+        A = DD.DistributedCgOperator(m, dm, geo, bas, rank, world, part=part, transport=a.transport)
         ids = A.owned_global_ids
+    if a.transport == "p2p":
+        A.connect_ipc()
     setup_s = time.time() - t0
     ng = dm.n_global_dofs
     rng = np.random.default_rng(1).uniform(-1, 1, ng)
@@ -99,7 +103,7 @@ def main():
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     apply_ms = maxr(float(np.mean(ts)))
-    out = {"config": a.config, "n_gpus": world, "mesh": f"{n}^3 x 6", "ndof": ng,
+    out = {"config": a.config, "n_gpus": world, "transport": a.transport, "mesh": f"{n}^3 x 6", "ndof": ng,
            "apply_ms_max_over_ranks": round(apply_ms, 4), "apply_gdofs": round(ng / apply_ms / 1e6, 3),
            "setup_s_rank0": round(setup_s, 1), "scaling": "strong"}
     if a.config == "c5":
