@@ -167,10 +167,11 @@ int tmf_pcg_direction(const double* z, double* p, int64_t n, const double* rz_k,
  * kernel (DG) gathers ghost cells' u from the owner -- compute and exchange in one
  * kernel over NVLink.  Applies must then pass the registered buffers; CG uses
  * tmf_apply_stages: ZERO, cross-rank barrier, CELLS|FIXUP, cross-rank barrier.
+ * CG cells [0, n_peer_free_cells) touch no ghost DoF and run the plain kernel.
  * n_ranks = 0 switches peers off.  Needs the default DMMA cell engine. */
 int tmf_plan_set_peers(tmf_plan* plan, int32_t n_ranks, const uint64_t* peer_u, const uint64_t* peer_y,
                        int32_t self_rank, int64_t n_own, int64_t n_ghost, const int32_t* ghost_rank,
-                       const int32_t* ghost_index);
+                       const int32_t* ghost_index, int64_t n_peer_free_cells);
 /* Dedicated device allocations (IPC-exportable at offset 0) and CUDA IPC handles
  * (64 bytes) for mapping another process's buffers. */
 int tmf_alloc(int64_t bytes, int32_t device, void** dev_ptr);

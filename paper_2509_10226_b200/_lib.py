@@ -80,7 +80,7 @@ def lib():
         L.tmf_pcg_direction.argtypes = [_v, _v, C.c_int64, _v, _v, _v]
         _u64p = C.POINTER(C.c_uint64)
         L.tmf_plan_set_peers.argtypes = [C.c_void_p, C.c_int32, _u64p, _u64p, C.c_int32, C.c_int64, C.c_int64,
-                                         _ip, _ip]
+                                         _ip, _ip, C.c_int64]
         L.tmf_alloc.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_void_p)]
         L.tmf_free.argtypes = [C.c_void_p]
         L.tmf_ipc_get_handle.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]

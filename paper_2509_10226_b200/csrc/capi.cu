@@ -251,6 +251,7 @@ struct tmf_plan {
   int* ghost_index = nullptr;
   const double* peer_self_u = nullptr;   // this rank's registered buffers
   double* peer_self_y = nullptr;
+  int64_t n_peer_free = 0;               // CG: cells [0, n) touch no ghost DoF (plain kernel)
   int4* if_chunks = nullptr;
   int* if_cm = nullptr;
   int* if_cp = nullptr;
@@ -271,7 +272,7 @@ struct tmf_plan {
   tmf_plan_info info{};
   // cell range [c0, c1): per-cell arrays are offset; CG u/y are global, DG u/y
   // are cell-contiguous and offset with the cells
-  tmf::CellArgs cell_args(const double* u, double* y, int64_t c0 = 0, int64_t c1 = -1) const {
+  tmf::CellArgs cell_args(const double* u, double* y, int64_t c0 = 0, int64_t c1 = -1, bool with_peer = true) const {
     if (c1 < 0) c1 = n_cells;
     tmf::CellArgs a{};
     const int64_t off = dg ? c0 * N * nc : 0;
@@ -282,7 +283,7 @@ struct tmf_plan {
     a.frags = cell_frags;
     a.n_cells = c1 - c0;
     a.nc = nc;
-    if (!dg) a.peer = peer;   // CG ghost DoFs over peer memory (DG: the face kernel's ghost cells)
+    if (!dg && with_peer) a.peer = peer;   // CG ghost DoFs over peer memory (DG: the face kernel's ghost cells)
     if (local && c0 == 0 && c1 == n_cells) {
       a.pmeta = pmeta;
       a.prec = prec;
@@ -510,9 +511,21 @@ int tmf_apply_stages(tmf_plan* P, const double* u, double* y, int stages, int64_
   bool ok = true;
   if ((stages & TMF_STAGE_ZERO) && !P->dg)
     TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
-  if ((stages & TMF_STAGE_CELLS) && cell_end > cell_begin)
-    TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, cell_begin, cell_end), P->n_sm,
-                              st, nullptr, &ok, P->variant, P->engine));
+  if ((stages & TMF_STAGE_CELLS) && cell_end > cell_begin) {
+    if (P->peer.u && !P->dg) {
+      // cells touching no ghost DoF run the plain kernel, the rest the peer-memory one
+      const int64_t m = std::min(std::max(P->n_peer_free, cell_begin), cell_end);
+      if (m > cell_begin)
+        TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, cell_begin, m, false), P->n_sm,
+                                  st, nullptr, &ok, P->variant, P->engine));
+      if (cell_end > m)
+        TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, m, cell_end), P->n_sm, st,
+                                  nullptr, &ok, P->variant, P->engine));
+    } else {
+      TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, cell_begin, cell_end), P->n_sm,
+                                st, nullptr, &ok, P->variant, P->engine));
+    }
+  }
   if ((stages & TMF_STAGE_FACES) && P->faces) {
     TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
@@ -799,7 +812,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
 
 int tmf_plan_set_peers(tmf_plan* P, int32_t n_ranks, const uint64_t* peer_u, const uint64_t* peer_y,
                        int32_t self_rank, int64_t n_own, int64_t n_ghost, const int32_t* ghost_rank,
-                       const int32_t* ghost_index) {
+                       const int32_t* ghost_index, int64_t n_peer_free_cells) {
   if (!P) return fail(TMF_EINVAL, "null plan");
   TMF_CUDA(cudaSetDevice(P->dev));
   for (void* q : {(void*)P->peer_u_tab, (void*)P->peer_y_tab, (void*)P->ghost_rank, (void*)P->ghost_index})
@@ -811,9 +824,10 @@ int tmf_plan_set_peers(tmf_plan* P, int32_t n_ranks, const uint64_t* peer_u, con
   P->peer = tmf::PeerArgs{};
   P->peer_self_u = nullptr;
   P->peer_self_y = nullptr;
+  P->n_peer_free = 0;
   if (n_ranks == 0) return TMF_OK;
   if (n_ranks < 0 || !peer_u || self_rank < 0 || self_rank >= n_ranks || n_own < 0 || n_ghost < 0 ||
-      (n_ghost && (!ghost_rank || !ghost_index)))
+      (n_ghost && (!ghost_rank || !ghost_index)) || n_peer_free_cells < 0 || n_peer_free_cells > P->n_cells)
     return fail(TMF_EINVAL, "bad peer description");
   if (!P->dg && !peer_y) return fail(TMF_EINVAL, "a CG plan needs the peers' y buffers (ghost RED)");
   if (P->engine == 2 || P->local)
@@ -841,6 +855,11 @@ int tmf_plan_set_peers(tmf_plan* P, int32_t n_ranks, const uint64_t* peer_u, con
   P->peer.n_own = n_own;
   P->peer_self_u = reinterpret_cast<const double*>(peer_u[self_rank]);
   P->peer_self_y = peer_y ? reinterpret_cast<double*>(peer_y[self_rank]) : nullptr;
+  P->n_peer_free = P->dg ? 0 : n_peer_free_cells;
+  if (n_ghost == 0) {   // nothing lives elsewhere: the plain kernels (buffers stay registered)
+    P->peer.u = nullptr;
+    P->peer.y = nullptr;
+  }
   return TMF_OK;
 }
 

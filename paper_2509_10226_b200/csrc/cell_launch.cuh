@@ -21,7 +21,7 @@ static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, C
   auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK, SKEW, PEER>;
   if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
+  cudaError_t e = blocks_per_sm(kern, BLOCK, S::SMEM, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t supertiles = ((a.n_cells + 8 * MTE - 1) / (8 * MTE)) * a.nc;
@@ -65,7 +65,7 @@ static cudaError_t launch_cell_d(const CellArgs& a, int n_sm, cudaStream_t st, C
   }
   if (a.n_cells == 0) return cudaSuccess;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, S::SMEM);
+  cudaError_t e = blocks_per_sm(kern, BLOCK, S::SMEM, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t chunks = ((a.n_cells + CH - 1) / CH) * a.nc;
@@ -87,7 +87,7 @@ static cudaError_t launch_cell_p(const CellArgs& a, int n_sm, cudaStream_t st) {
   if (cudaError_t e = opt_in_smem(kern, 227 * 1024); e != cudaSuccess) return e;
   if (a.n_cells == 0) return cudaSuccess;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem);
+  cudaError_t e = blocks_per_sm(kern, BLOCK, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t warps = ((a.n_cells + S::CH - 1) / S::CH) * a.nc;

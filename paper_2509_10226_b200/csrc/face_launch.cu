@@ -23,7 +23,7 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
     return cudaSuccess;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, SMEM);
+  cudaError_t e = blocks_per_sm(kern, BLOCK, SMEM, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t work = a.n_chunks * a.nc;

@@ -27,4 +27,44 @@ static cudaError_t opt_in_smem(K kern, int bytes) {
   return cudaSuccess;
 }
 
+// Resident CTAs per SM of (kernel, block, dynamic smem) on the current device, computed
+// once (cudaOccupancyMaxActiveBlocksPerMultiprocessor costs microseconds of host time
+// per launch, which small applies and the multi-GPU stages would pay every call).
+template <typename K>
+static cudaError_t blocks_per_sm(K kern, int block, size_t smem, int* out) {
+  struct Key {
+    const void* k;
+    int dev, block;
+    size_t smem;
+    bool operator==(const Key& o) const { return k == o.k && dev == o.dev && block == o.block && smem == o.smem; }
+  };
+  struct Hash {
+    size_t operator()(const Key& x) const {
+      return std::hash<const void*>()(x.k) ^ (std::hash<size_t>()(x.smem) * 31u) ^ ((size_t)x.dev << 20) ^
+             ((size_t)x.block << 40);
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, int, Hash> cache;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  const Key key{reinterpret_cast<const void*>(kern), dev, block, smem};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return cudaSuccess;
+    }
+  }
+  int per_sm = 0;
+  if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, block, smem); e != cudaSuccess)
+    return e;
+  if (per_sm < 1) per_sm = 1;
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = per_sm;
+  *out = per_sm;
+  return cudaSuccess;
+}
+
 }  // namespace tmf

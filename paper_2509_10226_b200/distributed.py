@@ -407,7 +407,7 @@ class _PeerTransport:
         gr, gi = self._ghost_owner, self._ghost_index
         _lib.check(_lib.lib().tmf_plan_set_peers(
             self.local_op._plan, self.world, u64, y64, self.rank, self._peer_n_own, len(gr),
-            _lib.ptr(gr, C.c_int32), _lib.ptr(gi, C.c_int32)))
+            _lib.ptr(gr, C.c_int32), _lib.ptr(gi, C.c_int32), int(getattr(self, "_peer_free_cells", 0))))
         self._peer_ptrs = (list(ptrs_u), None if ptrs_y is None else list(ptrs_y))
         self.connected = True
 
@@ -420,7 +420,7 @@ class _PeerTransport:
 
         if transport == "nccl":
             if getattr(self, "connected", False):
-                _lib.check(_lib.lib().tmf_plan_set_peers(self.local_op._plan, 0, None, None, 0, 0, 0, None, None))
+                _lib.check(_lib.lib().tmf_plan_set_peers(self.local_op._plan, 0, None, None, 0, 0, 0, None, None, 0))
         elif transport == "p2p":
             if not getattr(self, "_peer_ptrs", None):
                 raise RuntimeError("peer transport: connect first")
@@ -569,6 +569,7 @@ class DistributedCgOperator(_PeerTransport):
             if self.local_op is None:
                 raise ValueError("the p2p transport needs the B200 local plan")
             self._peer_init(n_local, self.sub.ghost_owner, self.sub.ghost_index, self.sub.n_owned)
+            self._peer_free_cells = self.sub.n_interior_cells
 
     @property
     def n_owned(self) -> int:
