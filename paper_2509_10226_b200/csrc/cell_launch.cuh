@@ -146,6 +146,12 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
     if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1, false, false, true>(a, n_sm, st, info);
     return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, false, false, true>(a, n_sm, st, info);
   }
+  if (variant == 15) {   // data prefetch (next tile's u and G) with a CTA size that leaves the registers
+    if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1, true>(a, n_sm, st, info);
+    if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1, true>(a, n_sm, st, info);
+    if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 384, 0, 1, true>(a, n_sm, st, info);
+    return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, true>(a, n_sm, st, info);
+  }
   if (variant == 13) {   // blocked tile runs with the per-degree default CTA size
     if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1, false, true>(a, n_sm, st, info);
     if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1, false, true>(a, n_sm, st, info);
