@@ -80,7 +80,8 @@ typedef struct tmf_plan_desc {
   int32_t device;              /* CUDA device ordinal                                 */
   int32_t flags;               /* bits 0-3 / 4-7: cell / face kernel tuning variant;
                                   8-11 face chunk/8; 12 concurrent DG; 13-14 cell engine
-                                  (0 by degree, 1 DMMA tensor cores, 2 DFMA); 15-16 CG
+                                  (0 by degree, 1 DMMA quadrature points, 2 DFMA,
+                                  3 DMMA reference tensor); 15-16 CG
                                   patch-local assembly (0 auto, 1 off, 2 on)            */
 } tmf_plan_desc;
 
@@ -94,6 +95,10 @@ typedef struct tmf_plan_info {
   int64_t device_bytes;        /* device memory held by the plan                      */
   int32_t patch_cells;         /* CG patch-local assembly: cells per patch (0 = off)  */
   double patch_ratio;          /* unique patch DoFs / unmasked cell-DoF slots (CG)    */
+  int32_t cell_engine;         /* cell kernel in use: 1 DMMA quadrature points, 2 DFMA,
+                                  3 DMMA reference tensor (affine precontraction)      */
+  double flops_engine;         /* useful flops per apply of the algorithm the engines
+                                  run (= flops_alg except for the tensor cell engine)  */
 } tmf_plan_info;
 
 int tmf_plan_create(const tmf_plan_desc* desc, tmf_plan** out);

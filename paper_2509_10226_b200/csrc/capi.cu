@@ -87,6 +87,43 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
         }
 }
 
+// Reference-tensor fragments (cell_tensor_kernel.cuh): the quadrature sum of the
+// reference's cell loop taken once, in extended precision, from the same tables:
+//   S_0..5 (packed kl = 00,01,02,11,12,22)
+//     S_kl(i, j) = sum_q w_q (G_k(q,i) G_l(q,j) + [k != l] G_l(q,i) G_k(q,j)),
+//   S_6(i, j) = sum_q w_q V(q,i) V(q,j) (mass),  S_7 = 0;
+//   B[ib][p][kk][lane] = S_{2p + (n&1)}(4ib + (n>>1), 4kk + (lane&3)),  n = lane>>2
+template <typename FG, typename FV>
+void build_tensor_fragments(int N, int Q, bool mass, FG Eg, FV Ev, const double* w, std::vector<double>& out) {
+  static const int KL[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+  const int KK = (N + 3) / 4, NP = mass ? 4 : 3, NM = mass ? 7 : 6;
+  std::vector<double> S((size_t)NM * N * N);
+  for (int m = 0; m < NM; ++m)
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        long double s = 0.0L;
+        for (int q = 0; q < Q; ++q) {
+          long double t;
+          if (m == 6) {
+            t = (long double)Ev(q, i) * Ev(q, j);
+          } else {
+            const int k = KL[m][0], l = KL[m][1];
+            t = (long double)Eg(k, q, i) * Eg(l, q, j);
+            if (k != l) t += (long double)Eg(l, q, i) * Eg(k, q, j);
+          }
+          s += (long double)w[q] * t;
+        }
+        S[((size_t)m * N + i) * N + j] = (double)s;
+      }
+  for (int ib = 0; ib < KK; ++ib)
+    for (int p = 0; p < NP; ++p)
+      for (int kk = 0; kk < KK; ++kk)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int n = lane >> 2, i = 4 * ib + (n >> 1), m = 2 * p + (n & 1), j = 4 * kk + (lane & 3);
+          out.push_back(i < N && j < N && m < NM ? S[((size_t)m * N + i) * N + j] : 0.0);
+        }
+}
+
 // CG warp-patch records (cell_patch_kernel.cuh) for patches of CH = 32 consecutive
 // cells; contribution slots are j*CH + cl.  Two parallel passes over the patches
 // (sizes, then fill at the prefix-summed offsets); per patch the (DoF, slot) pairs
@@ -639,13 +676,18 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       return Gm[(3 * q + c) * N + j];
     };
     std::vector<double> fr;
-    if (ci.table == 0)
+    if (ci.table == 2)
+      build_tensor_fragments(
+          N, Q, P->mass, [&](int k, int q, int j) { return Gm[(3 * q + k) * N + j]; },
+          [&](int q, int j) { return V[q * N + j]; }, d->cell_weights, fr);
+    else if (ci.table == 0)
       build_fragments(N, Q, NC, E, d->cell_weights, fr);
     else
       build_point_rows(N, Q, NC, E, d->cell_weights, fr);
     if ((int)fr.size() != ci.frag_doubles) return bail(fail(TMF_EINVAL, "internal: fragment size"));
     if ((rc = upload(&P->cell_frags, fr.data(), fr.size(), &total))) return bail(rc);
     P->info.flops_issued = ci.flops_issued;
+    P->info.cell_engine = ci.table == 2 ? 3 : ci.table == 1 ? 2 : 1;
   }
 
   // per-cell geometry (G, mass factor), computed once on the device
@@ -792,6 +834,15 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
            (double)nbf_dir * (16.0 * nqf * nd + 13.0 * nqf);
     }
     P->info.flops_alg = f * P->nc;
+    // the same apply's useful flops in the algorithm the cell engine runs: the reference
+    // tensor form replaces the cell term's 12 n_q N + 33 n_q by 12 N^2 + 12 N (+ 4 N^2 + 2 N mass)
+    double fe = f;
+    if (P->info.cell_engine == 3) {
+      fe -= nce * (12.0 * nq * nd + 33.0 * nq);
+      fe += nce * (12.0 * nd * nd + 12.0 * nd);
+      if (P->mass) fe += nce * (2.0 * nd * nd + 2.0 * nd) - nce * (4.0 * nq * nd + 5.0 * nq + nd);
+    }
+    P->info.flops_engine = fe * P->nc;
     double b = 16.0 * (double)P->n_global + 24.0 * (double)P->n_verts;
     if (!dg)
       b += 4.0 * nd * nce;

@@ -8,6 +8,7 @@
 #include "cell_dfma_kernel.cuh"
 #include "cell_kernel.cuh"
 #include "cell_patch_kernel.cuh"
+#include "cell_tensor_kernel.cuh"
 #include "launch.h"
 #include "launch_common.cuh"
 
@@ -42,6 +43,64 @@ static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, C
   }
   kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
   return cudaGetLastError();
+}
+
+// Reference-tensor engine (cell_tensor_kernel.cuh)
+template <int N, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PEER = false>
+static cudaError_t launch_cell_x(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
+  using S = TensorShape<N, MASS>;
+  auto kern = cell_tensor_kernel<N, MASS, DG, BLOCK, MT, MINB, PEER>;
+  if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaError_t e = blocks_per_sm(kern, BLOCK, S::SMEM, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t supertiles = ((a.n_cells + 8 * MT - 1) / (8 * MT)) * a.nc;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  const int64_t need = (supertiles + BLOCK / 32 - 1) / (BLOCK / 32);
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  if (info) {
+    info->dmma_per_tile = S::DMMA_PER_TILE;
+    info->tiles = supertiles * MT;
+    info->block = BLOCK;
+    info->grid = (int)blocks;
+    info->smem = S::SMEM;
+    info->frag_doubles = S::NFRAG * 32;
+    info->table = 2;
+    // DMMAs + the (6 | 7)-term contraction per output DoF
+    info->flops_issued = (double)supertiles * MT * (S::DMMA_PER_TILE * 512.0 + 8.0 * S::KK * 4 * 2 * (MASS ? 7 : 6));
+    return cudaSuccess;
+  }
+  if (a.n_cells == 0) return cudaSuccess;
+  kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// variants: 0 = per-degree default; 1..7 = tuning (bench sweeps only)
+template <int N, bool MASS, bool DG>
+static cudaError_t launch_cell_xt(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info,
+                                  int variant) {
+  if (!DG && a.peer.u != nullptr && !info) {   // multi-GPU peer ghosts: the default shapes
+    if (N <= 4) return launch_cell_x<N, MASS, DG, 768, 2, 1, true>(a, n_sm, st, info);
+    if (N <= 20) return launch_cell_x<N, MASS, DG, 1024, 1, 1, true>(a, n_sm, st, info);
+    return launch_cell_x<N, MASS, DG, 512, 2, 1, true>(a, n_sm, st, info);
+  }
+  if (variant == 1) return launch_cell_x<N, MASS, DG, 256, 1, 1>(a, n_sm, st, info);
+  if (variant == 2) return launch_cell_x<N, MASS, DG, 512, 2, 1>(a, n_sm, st, info);
+  if (variant == 3) return launch_cell_x<N, MASS, DG, 128, 2, 4>(a, n_sm, st, info);
+  if (variant == 4) return launch_cell_x<N, MASS, DG, 256, 4, 1>(a, n_sm, st, info);
+  if (variant == 5) return launch_cell_x<N, MASS, DG, 768, 2, 1>(a, n_sm, st, info);
+  if (variant == 6) return launch_cell_x<N, MASS, DG, 1024, 1, 1>(a, n_sm, st, info);
+  if (variant == 7) return launch_cell_x<N, MASS, DG, 256, 3, 1>(a, n_sm, st, info);
+  // per-degree defaults, measured on CG 48^3 reordered (tools/gpu_tensor1.sh, variants 0-7):
+  //   P1 768 threads x 2 tiles 31.5 us (256 x 2: 34.6), P2 1024 x 1 65.0 us (67.8),
+  //   P3 1024 x 1 132 us (135), P4 512 x 2 350 us (375)
+  if (N <= 4) return launch_cell_x<N, MASS, DG, 768, 2, 1>(a, n_sm, st, info);
+  if (N <= 10 && !MASS) return launch_cell_x<N, MASS, DG, 1024, 1, 1>(a, n_sm, st, info);
+  if (N <= 10) return launch_cell_x<N, MASS, DG, 512, 2, 1>(a, n_sm, st, info);
+  if (N <= 20) return launch_cell_x<N, MASS, DG, 1024, 1, 1>(a, n_sm, st, info);
+  return launch_cell_x<N, MASS, DG, 512, 2, 1>(a, n_sm, st, info);
 }
 
 // DFMA engine (cell_dfma_kernel.cuh): one thread per MC cells, point-major tables.
@@ -170,7 +229,8 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1>(a, n_sm, st, info);
 }
 
-// engine: 0 = per-degree default, 1 = DMMA (cell_kernel.cuh), 2 = DFMA (cell_dfma_kernel.cuh)
+// engine: 0 = per-degree default, 1 = DMMA quadrature points (cell_kernel.cuh), 2 = DFMA
+// (cell_dfma_kernel.cuh), 3 = DMMA reference tensor (cell_tensor_kernel.cuh)
 template <int N, int Q>
 static cudaError_t cell_variant(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
                                 CellLaunchInfo* info, int variant, int engine) {
@@ -195,7 +255,14 @@ static cudaError_t cell_variant(bool mass, bool dg, const CellArgs& a, int n_sm,
       return cell_variant<N, Q>(mass, dg, g, n_sm, st, info, 0, engine);
     }
   }
-  if (engine == 0) engine = 1;   // measured: DFMA P1 ~= DMMA, P2 +20 % (tools/gpu_dfma1.sh)
+  // default: the reference-tensor engine (measured 1.2-2.0x faster than the quadrature-point
+  // DMMA engine at P1-P4, tools/gpu_tensor1.sh; DFMA was P1 ~= DMMA, P2 +20 %, tools/gpu_dfma1.sh)
+  if (engine == 0) engine = 3;
+  if (engine == 3) {
+    if (!dg) return launch_cell_xt<N, false, false>(a, n_sm, st, info, variant);
+    if (mass) return launch_cell_xt<N, true, true>(a, n_sm, st, info, variant);
+    return launch_cell_xt<N, false, true>(a, n_sm, st, info, variant);
+  }
   if constexpr (N <= 20) {   // P4 rows do not fit the DFMA register budget
     if (engine == 2) {
       if (!dg) return launch_cell_dt<N, Q, false, false>(a, n_sm, st, info, variant);

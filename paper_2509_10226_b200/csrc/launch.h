@@ -17,7 +17,8 @@ struct CellLaunchInfo {
   int grid = 0;
   int smem = 0;
   int frag_doubles = 0;
-  int table = 0;             // 0 = DMMA lane fragments, 1 = point-major DFMA rows
+  int table = 0;             // 0 = DMMA lane fragments, 1 = point-major DFMA rows,
+                             // 2 = reference-tensor fragments (cell_tensor_kernel.cuh)
   double flops_issued = 0;   // FP64 FMA*2 issued per launch (padding included)
   int patch_cells = 0;       // CG patch-local assembly: cells per patch (0 = not supported)
 };

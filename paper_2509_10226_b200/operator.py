@@ -35,7 +35,7 @@ __all__ = ["OperatorConfig", "SipgConfig", "HelmholtzCoefficients", "CgPoissonOp
            "baseline_sipg_tau", "apply_cg_poisson", "apply_dg_sipg", "apply_helmholtz"]
 
 _STAGES = ("ref", "data", "mm", "sched")
-_ENGINES = {"auto": 0, "dmma": 1, "dfma": 2}
+_ENGINES = {"auto": 0, "dmma": 1, "dfma": 2, "tensor": 3}
 _PATCHES = {"auto": 0, "off": 1, "on": 2}
 
 
@@ -57,7 +57,7 @@ class OperatorConfig:
     face_variant: int = 0       # B200 face-kernel tuning variant (0 = default)
     face_chunk: int = 0         # 8-face batches per CTA chunk, multiple of 8 up to 120 (0 = default 32)
     concurrent_dg: bool = False  # DG: run the cell and face kernels concurrently (accumulating)
-    cell_engine: str = "auto"    # B200 cell kernel: auto (by degree) | dmma (tensor cores) | dfma
+    cell_engine: str = "auto"    # B200 cell kernel: auto | dmma (quadrature points) | dfma | tensor (affine reference tensor)
     cell_patches: str = "auto"   # B200 CG warp-patch assembly: auto (= off, measured slower) | off | on
 
     def __post_init__(self):

@@ -41,6 +41,28 @@ def test_gpu_both_cell_engines_match_golden(name, engine):
     assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
 
 
+@pytest.mark.parametrize("engine", ["dmma", "tensor"])
+@pytest.mark.parametrize("name", golden_names())
+def test_gpu_quadrature_and_tensor_engines_match_golden(name, engine):
+    """The quadrature-point DMMA engine (the reference's point loop) and the reference-
+    tensor engine (the point sum precontracted per plan) against every golden, P4 included."""
+    g = load_golden(name)
+    A = operator_from_fixture(g, cell_engine=engine)
+    assert A.info["cell_engine"] == (3 if engine == "tensor" else 1)
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
+
+
+@pytest.mark.parametrize("variant", range(1, 8))
+@pytest.mark.parametrize("name", ["cg_p1_n3_gm_dir2", "cg_p2_n8_gm", "cg3_p2_n3_ref_dir", "cg_p4_n3_gm_dir",
+                                  "helmk_p2_n3_gm_dir", "dg_p3_n3_gm_dir"])
+def test_gpu_tensor_variants_match_golden(name, variant):
+    g = load_golden(name)
+    A = operator_from_fixture(g, cell_engine="tensor", kernel_variant=variant)
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}/v{variant}: rel L2 {err:.3e}"
+
+
 @pytest.mark.parametrize("variant", range(1, 9))
 @pytest.mark.parametrize("name", ["cg_p1_n3_gm_dir2", "cg_p2_n8_gm", "cg3_p2_n3_ref_dir", "helmk_p2_n3_gm_dir", "dg_p3_n3_gm_dir"])
 def test_gpu_dfma_variants_match_golden(name, variant):
