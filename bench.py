@@ -77,9 +77,9 @@ def build_problem(n, p, reorder):
     if key not in _MESHES:
         m = M.kuhn_cube_mesh(n, seed=0)
         if reorder:
-            from paper_2509_10226_b200.reorder import hierarchical_reorder
+            from paper_2509_10226_b200.reorder import reorder_mesh
 
-            m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+            m = reorder_mesh(m)   # hierarchical cell order + first-touch vertex numbering
         _MESHES[key] = m
     m = _MESHES[key]
     cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)

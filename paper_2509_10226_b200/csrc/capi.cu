@@ -519,15 +519,18 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
   if (!P->dg) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
   TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y), P->n_sm, st, nullptr, &ok,
                             P->variant, P->engine));
-  if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
+  // stage events only between kernels that exist (an event record between two empty
+  // stages still costs ~3 us of GPU time, which would inflate the measured apply)
+  const bool fix = !P->dg && P->n_fix;
+  if (ev && (P->faces || fix)) TMF_CUDA(cudaEventRecord(ev[1], st));
   if (P->faces) {
     TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
     TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
   }
-  if (ev) TMF_CUDA(cudaEventRecord(ev[2], st));
-  if (!P->dg && P->n_fix) TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st));
+  if (ev && P->faces && fix) TMF_CUDA(cudaEventRecord(ev[2], st));
+  if (fix) TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st));
   if (ev) TMF_CUDA(cudaEventRecord(ev[3], st));
   return TMF_OK;
 }
@@ -1015,15 +1018,20 @@ int tmf_apply_timed(tmf_plan* P, const double* u, double* y, void* stream, int r
   cudaEvent_t ev[4];
   for (auto& e : ev) TMF_CUDA(cudaEventCreate(&e));
   double acc[4] = {0, 0, 0, 0};
+  // which stage events launch_apply records (see there): ev[0] and ev[3] always
+  const bool fix = !P->dg && P->n_fix, conc = P->dg && P->faces && P->concurrent;
+  const bool e1 = conc || P->faces || fix, e2 = conc || (P->faces && fix);
   for (int r = 0; r < reps; ++r) {
     int rc = launch_apply(P, u, y, st, ev);
     if (rc) return rc;
     TMF_CUDA(cudaEventSynchronize(ev[3]));
-    float a, b, c, t;
+    float t = 0, a = 0, b = 0, c = 0;
     cudaEventElapsedTime(&t, ev[0], ev[3]);
-    cudaEventElapsedTime(&a, ev[0], ev[1]);
-    cudaEventElapsedTime(&b, ev[1], ev[2]);
-    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    // cell | faces | fixup; a stage without its closing event ends at ev[3]
+    const cudaEvent_t end_cell = e1 ? ev[1] : ev[3];
+    cudaEventElapsedTime(&a, ev[0], end_cell);
+    if (P->faces || conc) cudaEventElapsedTime(&b, end_cell, e2 ? ev[2] : ev[3]);
+    if (fix) cudaEventElapsedTime(&c, e2 ? ev[2] : end_cell, ev[3]);
     acc[0] += t;
     acc[1] += a;
     acc[2] += b;

@@ -46,10 +46,10 @@ static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, C
 }
 
 // Reference-tensor engine (cell_tensor_kernel.cuh)
-template <int N, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PEER = false>
+template <int N, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PEER = false, bool PF = false>
 static cudaError_t launch_cell_x(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = TensorShape<N, MASS>;
-  auto kern = cell_tensor_kernel<N, MASS, DG, BLOCK, MT, MINB, PEER>;
+  auto kern = cell_tensor_kernel<N, MASS, DG, BLOCK, MT, MINB, PEER, PF>;
   if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
   int per_sm = 0;
   cudaError_t e = blocks_per_sm(kern, BLOCK, S::SMEM, &per_sm);
@@ -93,6 +93,15 @@ static cudaError_t launch_cell_xt(const CellArgs& a, int n_sm, cudaStream_t st, 
   if (variant == 5) return launch_cell_x<N, MASS, DG, 768, 2, 1>(a, n_sm, st, info);
   if (variant == 6) return launch_cell_x<N, MASS, DG, 1024, 1, 1>(a, n_sm, st, info);
   if (variant == 7) return launch_cell_x<N, MASS, DG, 256, 3, 1>(a, n_sm, st, info);
+  if constexpr (N <= 10) {   // data prefetch (low degrees: latency-bound gathers)
+    if (variant == 8) return launch_cell_x<N, MASS, DG, 768, 2, 1, false, true>(a, n_sm, st, info);
+    if (variant == 9) return launch_cell_x<N, MASS, DG, 1024, 1, 1, false, true>(a, n_sm, st, info);
+    if (variant == 10) return launch_cell_x<N, MASS, DG, 512, 2, 2, false, true>(a, n_sm, st, info);
+    if (variant == 11) return launch_cell_x<N, MASS, DG, 256, 1, 6, false, true>(a, n_sm, st, info);
+    if (variant == 12) return launch_cell_x<N, MASS, DG, 512, 1, 3, false, true>(a, n_sm, st, info);
+    if (variant == 13) return launch_cell_x<N, MASS, DG, 256, 1, 8, false, false>(a, n_sm, st, info);
+    if (variant == 14) return launch_cell_x<N, MASS, DG, 256, 2, 4, false, true>(a, n_sm, st, info);
+  }
   // per-degree defaults, measured on CG 48^3 reordered (tools/gpu_tensor1.sh, variants 0-7):
   //   P1 768 threads x 2 tiles 31.5 us (256 x 2: 34.6), P2 1024 x 1 65.0 us (67.8),
   //   P3 1024 x 1 132 us (135), P4 512 x 2 350 us (375)

@@ -41,7 +41,10 @@ struct TensorShape {
 };
 
 // MT: 8-cell tiles per warp iteration (they share every B-fragment load)
-template <int N, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PEER = false>
+// PF: software pipeline one super-tile deeper -- the next super-tile's gathered u and
+// geometry are loaded while this one computes (indices two ahead); for the low degrees,
+// whose few DMMAs cannot hide a memory round trip per tile
+template <int N, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PEER = false, bool PF = false>
 __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
   using S = TensorShape<N, MASS>;
   constexpr int KK = S::KK, NP = S::NP;
@@ -81,30 +84,61 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
   };
   load_indices(st);
 
+  // gathered u, indices (kept for the scatter) and geometry of super-tile t
+  auto load_data = [&](int64_t t, int (&ix)[MT][KK], double (&av)[MT][KK], double (&G)[MT][6],
+                       double (&mdet)[MT]) {
+    const int cmp = a.nc == 1 ? 0 : (int)(t / cst);
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const int64_t c = ((t - (int64_t)cmp * cst) * MT + m) * 8 + cs;
+      const bool ok = t < nst && c < a.n_cells;
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk) {
+        const int g = ix[m][kk] = nidx[m][kk];
+        if (PEER)
+          av[m][kk] = (g >= 0) ? __ldg(peer_src(a.peer, a.u, g, a.nc, cmp)) : 0.0;
+        else
+          av[m][kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + cmp) : 0.0;
+      }
+      const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * (ok ? c : 0));
+      const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
+      G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
+      G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
+      mdet[m] = MASS ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
+    }
+  };
+  int pidx[MT][KK];
+  double pav[MT][KK], pG[MT][6], pmdet[MT];
+  if (PF) {
+    load_data(st, pidx, pav, pG, pmdet);
+    load_indices(st + step);
+  }
+
   for (; st < nst; st += step) {
     const int comp = a.nc == 1 ? 0 : (int)(st / cst);
     int64_t cell[MT];
     int idx[MT][KK];
     double av[MT][KK], G[MT][6], mdet[MT];
 #pragma unroll
-    for (int m = 0; m < MT; ++m) {
-      cell[m] = ((st - (int64_t)comp * cst) * MT + m) * 8 + cs;
-      const bool ok = cell[m] < a.n_cells;
+    for (int m = 0; m < MT; ++m) cell[m] = ((st - (int64_t)comp * cst) * MT + m) * 8 + cs;
+    if (PF) {
 #pragma unroll
-      for (int kk = 0; kk < KK; ++kk) {
-        const int g = idx[m][kk] = nidx[m][kk];
-        if (PEER)
-          av[m][kk] = (g >= 0) ? __ldg(peer_src(a.peer, a.u, g, a.nc, comp)) : 0.0;
-        else
-          av[m][kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + comp) : 0.0;
+      for (int m = 0; m < MT; ++m) {
+#pragma unroll
+        for (int kk = 0; kk < KK; ++kk) {
+          idx[m][kk] = pidx[m][kk];
+          av[m][kk] = pav[m][kk];
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i) G[m][i] = pG[m][i];
+        mdet[m] = pmdet[m];
       }
-      const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * (ok ? cell[m] : 0));
-      const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
-      G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
-      G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
-      mdet[m] = MASS ? __ldg(a.cgeo + 8 * (ok ? cell[m] : 0) + 6) : 0.0;
+      load_data(st + step, pidx, pav, pG, pmdet);
+      load_indices(st + 2 * step);
+    } else {
+      load_data(st, idx, av, G, mdet);
+      load_indices(st + step);
     }
-    load_indices(st + step);
 
     // one i-block at a time: GEMM columns (ib, kl), contraction, then its scatter/store
     // (the lane owns DoF 4 ib + q4 of cell cs, whose index it gathered for k-step ib)

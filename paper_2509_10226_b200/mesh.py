@@ -210,3 +210,43 @@ def apply_cell_permutation(mesh: TetMesh, new_of_old: np.ndarray) -> TetMesh:
     geom = mesh.geometry_nodes[order] if mesh.geometry_nodes is not None else None
     par = mesh.parent_cells[order] if mesh.parent_cells is not None else None
     return TetMesh(mesh.vertices.copy(), cells, interior, bnd, geom, par)
+
+
+def apply_vertex_permutation(mesh: TetMesh, new_of_old: np.ndarray) -> TetMesh:
+    """Vertex v is renumbered new_of_old[v] (cells keep their order and local vertex
+    order, so orientation is unchanged); faces are rebuilt because their orientation
+    codes follow global vertex ids (reference.py orientation_code), boundary ids are
+    carried over by vertex triple.  The reference has no vertex renumbering; the CG DoF
+    map of the result (vertex DoF = vertex id, dofmap.py:113-114) follows the new ids."""
+    new_of_old = np.asarray(new_of_old, dtype=np.int64)
+    nv = len(mesh.vertices)
+    if new_of_old.shape != (nv,) or not np.array_equal(np.sort(new_of_old), np.arange(nv)):
+        raise ValueError("new_of_old must be a permutation of the vertex ids")
+    verts = np.empty_like(mesh.vertices)
+    verts[new_of_old] = mesh.vertices
+    cells = new_of_old[mesh.cells].astype(mesh.cells.dtype)
+    interior, bnd = build_faces(cells)
+    if len(bnd):
+        old_tri = np.sort(new_of_old[mesh.cells[mesh.boundary_faces[:, 0, None],
+                                                FACE_VERTICES_ARR[mesh.boundary_faces[:, 1]]]], axis=1)
+        new_tri = np.sort(cells[bnd[:, 0, None], FACE_VERTICES_ARR[bnd[:, 1]]], axis=1)
+        lookup = {tuple(t): int(b) for t, b in zip(old_tri.tolist(), mesh.boundary_faces[:, 2].tolist())}
+        bnd = bnd.copy()
+        bnd[:, 2] = [lookup.get(tuple(t), 0) for t in new_tri.tolist()]
+    # curved geometry nodes are per-cell coordinates: unaffected by vertex ids
+    return TetMesh(verts, cells, interior, bnd, mesh.geometry_nodes, mesh.parent_cells)
+
+
+def first_touch_vertex_order(mesh: TetMesh) -> np.ndarray:
+    """new_of_old for apply_vertex_permutation: vertices numbered in order of first
+    appearance in the cell list (cell order, then local vertex order), so the vertices
+    of consecutive cells get nearby ids.  Vertices no cell touches go last."""
+    flat = mesh.cells.ravel()
+    uniq, first = np.unique(flat, return_index=True)
+    order = uniq[np.argsort(first, kind="stable")]
+    nv = len(mesh.vertices)
+    rest = np.setdiff1d(np.arange(nv), order, assume_unique=True)
+    order = np.concatenate([order, rest])
+    new_of_old = np.empty(nv, dtype=np.int64)
+    new_of_old[order] = np.arange(nv)
+    return new_of_old

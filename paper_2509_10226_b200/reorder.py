@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["hierarchical_reorder", "locality_metrics"]
+__all__ = ["hierarchical_reorder", "reorder_mesh", "locality_metrics"]
 
 
 def hierarchical_reorder(mesh, group_size: int = 8) -> np.ndarray:
@@ -27,6 +27,19 @@ def hierarchical_reorder(mesh, group_size: int = 8) -> np.ndarray:
     _lib.check(_lib.lib().tmf_hierarchical_reorder(len(mesh.cells), len(f), _lib.ptr(f, C.c_int32),
                                                    int(group_size), _lib.ptr(out, C.c_int64)))
     return out
+
+
+def reorder_mesh(mesh, group_size: int = 8, renumber_vertices: bool = True):
+    """The reordered mesh: cells in hierarchical order (``hierarchical_reorder``), then,
+    optionally, vertices renumbered by first touch in that cell order so that the vertex
+    DoFs of consecutive cells (P1: all of them) are close in memory -- a gathered or
+    RED-scattered warp of 8 cells then touches a few cache lines instead of ~30."""
+    from . import mesh as M
+
+    m = M.apply_cell_permutation(mesh, hierarchical_reorder(mesh, group_size))
+    if renumber_vertices:
+        m = M.apply_vertex_permutation(m, M.first_touch_vertex_order(m))
+    return m
 
 
 def locality_metrics(mesh) -> dict:

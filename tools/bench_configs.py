@@ -27,9 +27,9 @@ def setup(n, p, space, reorder, dids=()):
     t = time.time()
     m = M.kuhn_cube_mesh(n, seed=0)
     if reorder:
-        from paper_2509_10226_b200.reorder import hierarchical_reorder
+        from paper_2509_10226_b200.reorder import reorder_mesh
 
-        m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+        m = reorder_mesh(m)
     cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
     bas = B.tabulate_basis(p, cr, fr)
     dm = D.build_dof_map(m, p, space, 1, dids)
@@ -56,10 +56,11 @@ def line(name, A, nd, ms, extra=None):
     info = A.info
     d = {"config": name, "ndof": nd, "ms": round(float(ms[0]), 4), "cell_ms": round(float(ms[1]), 4),
          "face_ms": round(float(ms[2]), 4), "gdofs": round(nd / ms[0] / 1e6, 3),
-         "tflops_alg": round(info["flops_alg"] / ms[0] / 1e9, 2),
-         "frac_fp64_roofline": round(info["flops_alg"] / ms[0] / 1e9 / PEAK, 3),
+         "tflops_engine": round(info["flops_engine"] / ms[0] / 1e9, 2),
+         "frac_fp64_roofline": round(info["flops_engine"] / ms[0] / 1e9 / PEAK, 3),
+         "tflops_ref_formula": round(info["flops_alg"] / ms[0] / 1e9, 2), "cell_engine": int(info["cell_engine"]),
          "flops_alg_per_dof": round(info["flops_alg"] / nd, 1), "bytes_alg_per_dof": round(info["bytes_alg"] / nd, 1),
-         "issued_over_alg": round(info["flops_issued"] / info["flops_alg"], 3)}
+         "issued_over_engine": round(info["flops_issued"] / info["flops_engine"], 3)}
     if extra:
         d.update(extra)
     print(json.dumps(d), flush=True)
@@ -140,7 +141,7 @@ def c5(n=128, iters=100):
                       "apply_ms": round(float(ms[0]), 4),
                       "apply_gdofs": round(nd / ms[0] / 1e6, 3),
                       "solver_gdofs_per_iteration": round(nd * iters / t / 1e6, 3),
-                      "apply_frac_fp64_roofline": round(A.info["flops_alg"] / ms[0] / 1e9 / PEAK, 3),
+                      "apply_frac_fp64_roofline": round(A.info["flops_engine"] / ms[0] / 1e9 / PEAK, 3),
                       "residual_first_last": [float(hist[0]), float(hist[-1])], "setup_s": round(ts, 1)}),
           flush=True)
 

@@ -6,12 +6,13 @@ import torch
 from paper_2509_10226_b200 import mesh as M, dofmap as D, basis as B, quadrature as Q, geometry as G, operator as op
 
 def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto"):
-    reordered = kind.endswith("r")
+    reordered = kind[-1] in "rv"
+    suffix = kind[-1] if reordered else ""
     t0 = time.time()
     m = M.kuhn_cube_mesh(n, seed=0)
-    if kind.endswith("r"):
-        from paper_2509_10226_b200.reorder import hierarchical_reorder
-        m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+    if reordered:   # r: cells only, v: cells + first-touch vertex renumbering
+        from paper_2509_10226_b200.reorder import reorder_mesh
+        m = reorder_mesh(m, renumber_vertices=suffix == "v")
         kind = kind[:-1]
     cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
     bas = B.tabulate_basis(p, cr, fr)
@@ -41,7 +42,7 @@ def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto"):
     gdofs = nd / (ms[0] * 1e-3) / 1e9
     tf_alg = info["flops_alg"] / (ms[0] * 1e-3) / 1e12
     tf_iss = info["flops_issued"] / (ms[0] * 1e-3) / 1e12
-    print(json.dumps(dict(kind=kind + ("r" if reordered else ""), p=p, n=n, variant=variant, engine=engine, patch_cells=A.info['patch_cells'], patch_ratio=round(A.info['patch_ratio'], 3), ndof=nd, setup_s=round(setup, 1), ms=[round(x, 4) for x in ms],
+    print(json.dumps(dict(kind=kind + suffix, p=p, n=n, variant=variant, engine=engine, patch_cells=A.info['patch_cells'], patch_ratio=round(A.info['patch_ratio'], 3), ndof=nd, setup_s=round(setup, 1), ms=[round(x, 4) for x in ms],
                           gdofs=round(gdofs, 3), tflops_alg=round(tf_alg, 2), tflops_issued=round(tf_iss, 2),
                           frac_fp64=round(tf_alg / 37.1, 3))), flush=True)
 
