@@ -218,3 +218,35 @@ def test_c_abi_demo_compiles_against_header_and_library():
                         "-ltetmf_b200", f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}", "-lm", "-o", out],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_vertex_renumbering_is_a_permutation_of_the_operator(p):
+    """reorder_mesh's first-touch vertex numbering relabels vertices only: the mesh stays
+    valid and positive, boundary ids survive, and the CG operator (oracle) on the new mesh
+    equals the old one up to the DoF relabelling (P1: DoF = vertex id)."""
+    from oracle import ref_apply
+
+    m = M.apply_cell_permutation(M.kuhn_cube_mesh(4, seed=3), R.hierarchical_reorder(M.kuhn_cube_mesh(4, seed=3)))
+    nov = M.first_touch_vertex_order(m)
+    m2 = M.apply_vertex_permutation(m, nov)
+    m2.validate()
+    assert np.all(np.linalg.det(m2.cell_jacobians()) > 0)
+    assert np.array_equal(np.sort(nov), np.arange(m.n_vertices))
+    assert np.array_equal(np.bincount(m2.boundary_faces[:, 2]), np.bincount(m.boundary_faces[:, 2]))
+    # first touch: the vertices of the first cell are 0..3
+    assert sorted(m2.cells[0].tolist()) == [0, 1, 2, 3]
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    d1, d2 = D.build_dof_map(m, p, "cg"), D.build_dof_map(m2, p, "cg")
+    u1 = np.random.default_rng(1).uniform(-1, 1, d1.n_global_dofs)
+    y1 = ref_apply.cg_apply(m.vertices, m.cells, d1.cell_dofs, d1.dirichlet_mask, bas.grad_matrix, cr.weights, u1)
+    # DoF relabelling old -> new through the cell-local DoF lists (same cells, same local order)
+    new_of_old = np.empty(d1.n_global_dofs, dtype=np.int64)
+    new_of_old[d1.cell_dofs.ravel()] = d2.cell_dofs.ravel()
+    u2 = np.empty_like(u1)
+    u2[new_of_old] = u1
+    y2 = ref_apply.cg_apply(m2.vertices, m2.cells, d2.cell_dofs, d2.dirichlet_mask, bas.grad_matrix, cr.weights, u2)
+    assert np.linalg.norm(y2[new_of_old] - y1) <= 1e-13 * np.linalg.norm(y1)
+    with pytest.raises(ValueError):
+        M.apply_vertex_permutation(m, np.zeros(m.n_vertices, dtype=np.int64))
