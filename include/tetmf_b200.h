@@ -82,7 +82,9 @@ typedef struct tmf_plan_desc {
                                   8-11 face chunk/8; 12 concurrent DG; 13-14 cell engine
                                   (0 by degree, 1 DMMA quadrature points, 2 DFMA,
                                   3 DMMA reference tensor); 15-16 CG
-                                  patch-local assembly (0 auto, 1 off, 2 on)            */
+                                  patch-local assembly (0 auto, 1 off, 2 on); 17-18
+                                  interior-face engine (0 by degree, 1 quadrature
+                                  points, 2 reference tensor)                          */
 } tmf_plan_desc;
 
 typedef struct tmf_plan_info {
@@ -98,7 +100,9 @@ typedef struct tmf_plan_info {
   int32_t cell_engine;         /* cell kernel in use: 1 DMMA quadrature points, 2 DFMA,
                                   3 DMMA reference tensor (affine precontraction)      */
   double flops_engine;         /* useful flops per apply of the algorithm the engines
-                                  run (= flops_alg except for the tensor cell engine)  */
+                                  run (= flops_alg except for the tensor engines)      */
+  int32_t face_engine;         /* interior faces: 1 quadrature points, 2 reference
+                                  tensor (0: no faces)                                 */
 } tmf_plan_info;
 
 int tmf_plan_create(const tmf_plan_desc* desc, tmf_plan** out);

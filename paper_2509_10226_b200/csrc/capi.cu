@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -122,6 +123,92 @@ void build_tensor_fragments(int N, int Q, bool mass, FG Eg, FV Ev, const double*
           const int n = lane >> 2, i = 4 * ib + (n >> 1), m = 2 * p + (n & 1), j = 4 * kk + (lane & 3);
           out.push_back(i < N && j < N && m < NM ? S[((size_t)m * N + i) * N + j] : 0.0);
         }
+}
+
+// Reference-tensor interior-face tables (face_tensor_kernel.cuh), one per signature
+// sig = lf- * 24 + lf+ * 6 + code.  Tables of one side: Ev(lf, code, c, q, a) = component
+// c (0 value, 1..3 face-frame derivative) at point q of the DoF at gather position a
+// (face DoFs first).  With <x, y> = sum_q w_q x(q) y(q) and slots (0 s tau, 1 hm0,
+// 2 hm1, 3 hp0, 4 hp1, 5 zero, 6 hm2, 7 hp2), the point loop of face_kernel.cuh is
+//   s tau: [m,m] <m0,m0>  [m,p] -<m0,p0>  [p,m] -<p0,m0>  [p,p] <p0,p0>
+//   hm_k:  [m,m] -<m0,mk'> - <mk',m0>  [m,p] <mk',p0>  [p,m] <p0,mk'>
+//   hp_k:  [m,p] -<m0,pk'>  [p,m] -<pk',m0>  [p,p] <p0,pk'> + <pk',p0>      (k' = k + 1)
+// ([out side, in side]).  Inputs/outputs are ordered [-F | +F] (region F) and
+// [-I | +I] (region I); the fragments hold the blocks the kernel multiplies, and every
+// dropped block is checked to vanish (nodal basis).
+template <typename F>
+int build_face_tensor_fragments(int N, int NF, int QF, F Ev, const double* w, std::vector<double>& out) {
+  const int NI = N - NF, KF = (2 * NF + 3) / 4, KI = (2 * NI + 3) / 4;
+  double dropped = 0.0, kept = 0.0;
+  for (int lfm = 0; lfm < 4; ++lfm)
+    for (int lfp = 0; lfp < 4; ++lfp)
+      for (int code = 0; code < 6; ++code) {
+        // side 0 = minus (lf-, code 0), side 1 = plus (lf+, code)
+        const int lf[2] = {lfm, lfp}, cd[2] = {0, code};
+        auto E = [&](int side, int c, int q, int a) { return Ev(lf[side], cd[side], c, q, a); };
+        auto IP = [&](int so, int co, int ao, int si, int ci, int ai) {
+          long double acc = 0.0L;
+          for (int q = 0; q < QF; ++q) acc += (long double)w[q] * E(so, co, q, ao) * E(si, ci, q, ai);
+          return (double)acc;
+        };
+        auto T = [&](int slot, int so, int ao, int si, int ai) -> double {
+          if (slot == 5) return 0.0;
+          if (slot == 0) return (so == si ? 1.0 : -1.0) * IP(so, 0, ao, si, 0, ai);
+          const bool hm = slot == 1 || slot == 2 || slot == 6;
+          const int k1 = (slot == 1 || slot == 3) ? 1 : (slot == 2 || slot == 4) ? 2 : 3;
+          if (hm) {
+            if (so == 0 && si == 0) return -IP(0, 0, ao, 0, k1, ai) - IP(0, k1, ao, 0, 0, ai);
+            if (so == 0 && si == 1) return IP(0, k1, ao, 1, 0, ai);
+            if (so == 1 && si == 0) return IP(1, 0, ao, 0, k1, ai);
+            return 0.0;
+          }
+          if (so == 1 && si == 1) return IP(1, 0, ao, 1, k1, ai) + IP(1, k1, ao, 1, 0, ai);
+          if (so == 0 && si == 1) return -IP(0, 0, ao, 1, k1, ai);
+          if (so == 1 && si == 0) return -IP(1, k1, ao, 0, 0, ai);
+          return 0.0;
+        };
+        // region index -> (side, gather position); -1 = padding
+        auto regF = [&](int x, int& side, int& a) {
+          if (x >= 2 * NF) return false;
+          side = x >= NF;
+          a = x - side * NF;
+          return true;
+        };
+        auto regI = [&](int x, int& side, int& a) {
+          if (x >= 2 * NI) return false;
+          side = x >= NI;
+          a = NF + x - side * NI;
+          return true;
+        };
+        auto frag = [&](bool outF, int ib, int p, bool inF, int kk) {
+          for (int lane = 0; lane < 32; ++lane) {
+            const int n = lane >> 2, slot = 2 * p + (n & 1);
+            int so, ao, si, ai;
+            const bool ok = (outF ? regF(4 * ib + (n >> 1), so, ao) : regI(4 * ib + (n >> 1), so, ao)) &&
+                            (inF ? regF(4 * kk + (lane & 3), si, ai) : regI(4 * kk + (lane & 3), si, ai));
+            out.push_back(ok ? T(slot, so, ao, si, ai) : 0.0);
+          }
+        };
+        for (int ib = 0; ib < KF; ++ib) {
+          for (int p = 0; p < 4; ++p)
+            for (int kk = 0; kk < KF; ++kk) frag(true, ib, p, true, kk);
+          for (int kk = 0; kk < KI; ++kk) frag(true, ib, 3, false, kk);
+        }
+        for (int ib = 0; ib < KI; ++ib)
+          for (int kk = 0; kk < KF; ++kk) frag(false, ib, 3, true, kk);
+        // the dropped blocks must vanish: slots 0-5 between F and I, everything I x I
+        for (int so = 0; so < 2; ++so)
+          for (int si = 0; si < 2; ++si)
+            for (int slot = 0; slot < 8; ++slot)
+              for (int ao = 0; ao < N; ++ao)
+                for (int ai = 0; ai < N; ++ai) {
+                  const bool fo = ao < NF, fi = ai < NF;
+                  const double v = std::fabs(T(slot, so, ao, si, ai));
+                  const bool keep = (fo && fi) || ((fo != fi) && slot >= 6);
+                  (keep ? kept : dropped) = std::max(keep ? kept : dropped, v);
+                }
+      }
+  return dropped <= 1e-12 * std::max(kept, 1.0) ? TMF_OK : TMF_EINVAL;
 }
 
 // CG warp-patch records (cell_patch_kernel.cuh) for patches of CH = 32 consecutive
@@ -268,6 +355,8 @@ struct tmf_plan {
   double* cell_frags = nullptr;
   double* cell_geo = nullptr;
   double* face_frags = nullptr;
+  double* face_tfrags = nullptr;   // reference-tensor interior-face tables (96 signatures)
+  int face_engine = 0;             // (desc.flags >> 17) & 3: 0 by degree, 1 quadrature points, 2 tensor
   int* face_perm = nullptr;
   int* cells = nullptr;
   int* dofs = nullptr;
@@ -343,6 +432,7 @@ struct tmf_plan {
     a.n_dpc = N;
     a.nc = nc;
     a.peer = peer;
+    a.tfrags = face_tfrags;   // the launcher uses the tensor kernel for interior faces when set
     return a;
   }
   tmf::FaceGeoArgs face_geo_args(bool boundary) const {
@@ -363,7 +453,7 @@ struct tmf_plan {
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
-    for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
+    for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)face_tfrags, (void*)cells,
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
@@ -633,6 +723,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   // warp patches use the DFMA point-major tables (also for their global-kernel fallback)
   if (P->patches == 2 && d->operator_kind == TMF_CG_LAPLACE && d->n_dofs_per_cell <= 20) P->engine = 2;
   P->face_variant = (d->flags >> 4) & 0xF;
+  P->face_engine = (d->flags >> 17) & 3;
   P->concurrent = (d->flags >> 12) & 1;
   P->degree = d->degree;
   P->N = d->n_dofs_per_cell;
@@ -803,6 +894,41 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
                                               std::to_string(N) + ", " + std::to_string(QF) + ")"));
     if ((int64_t)fr.size() != 24LL * fi.nfrag * 32) return bail(fail(TMF_EINVAL, "internal: face fragments"));
     if ((rc = upload(&P->face_frags, fr.data(), fr.size(), &total))) return bail(rc);
+    // reference-tensor interior-face tables: by default at P2-P4 (DMMAs per 8 faces 48 / 150
+    // / 416 vs 60 / 170 / 432 for the point loop, no per-point arithmetic; measured faces
+    // P2 96^3 Helmholtz 1.89 -> 1.77 ms, P3 64^3 1.34 -> 1.14 ms, P4 48^3 1.71 -> 1.31 ms);
+    // P1 keeps the point loop (20 vs 12 DMMAs: 0.91 vs 1.00 ms at 96^3)
+    int fe = P->face_engine;
+    if (fe == 0) fe = N >= 10 ? 2 : 1;
+    P->face_engine = fe;
+    if (fe == 2 && d->n_interior_faces > 0) {
+      std::vector<double> tf;
+      tf.reserve((size_t)96 * fi.tnfrag * 32);
+      const double* Fv = d->face_values;
+      const double* Fg = d->face_grads;
+      std::vector<std::array<std::array<double, 3>, 3>> frame(4);
+      for (int lf = 0; lf < 4; ++lf) {
+        const double R[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+        const int fvv[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+        for (int k = 0; k < 3; ++k) {
+          frame[lf][0][k] = R[fvv[lf][1]][k] - R[fvv[lf][0]][k];
+          frame[lf][1][k] = R[fvv[lf][2]][k] - R[fvv[lf][0]][k];
+          frame[lf][2][k] = R[lf][k] - R[fvv[lf][0]][k];
+        }
+      }
+      auto Ev = [&](int lf, int code, int c, int q, int a) -> double {
+        const int jj = perm[lf * N + a];
+        const size_t t = (size_t)(lf * 6 + code);
+        if (c == 0) return Fv[(t * QF + q) * N + jj];
+        const auto& av = frame[lf][c - 1];
+        const double* g = Fg + t * 3 * QF * N;
+        return av[0] * g[(3 * q) * N + jj] + av[1] * g[(3 * q + 1) * N + jj] + av[2] * g[(3 * q + 2) * N + jj];
+      };
+      if (build_face_tensor_fragments(N, NF, QF, Ev, d->face_weights, tf) != TMF_OK)
+        return bail(fail(TMF_EINVAL, "face tables are not those of a nodal basis (tensor face form)"));
+      if ((int64_t)tf.size() != 96LL * fi.tnfrag * 32) return bail(fail(TMF_EINVAL, "internal: tensor face fragments"));
+      if ((rc = upload(&P->face_tfrags, tf.data(), tf.size(), &total))) return bail(rc);
+    }
     const int chunk = ((d->flags >> 8) & 0xF) ? 8 * ((d->flags >> 8) & 0xF) : fi.chunk;
     if ((rc = build_face_batches(P, d, chunk, &total))) return bail(rc);
     // per-face geometry, computed once on the device (64 B per face slot)
@@ -815,7 +941,8 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       TMF_CUDA(tmf::launch_face_geometry(bnd != 0, P->face_geo_args(bnd != 0), P->n_sm, 0));
     }
     P->info.n_face_batches = (int32_t)(P->n_if_batches + P->n_bf_batches);
-    P->info.flops_issued += (double)P->nc * (P->n_if_batches * fi.dmma_per_batch +
+    P->info.face_engine = P->face_tfrags ? 2 : 1;
+    P->info.flops_issued += (double)P->nc * (P->n_if_batches * (P->face_tfrags ? fi.tdmma_per_batch : fi.dmma_per_batch) +
                                              P->n_bf_batches * fi.dmma_per_batch / 2) * 512.0;
   }
 
@@ -844,6 +971,13 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       fe -= nce * (12.0 * nq * nd + 33.0 * nq);
       fe += nce * (12.0 * nd * nd + 12.0 * nd);
       if (P->mass) fe += nce * (2.0 * nd * nd + 2.0 * nd) - nce * (4.0 * nq * nd + 5.0 * nq + nd);
+    }
+    if (faces && P->face_tfrags) {
+      // tensor face form: the nonzero blocks (F x F: s tau full, each m~ coefficient 3/4 of
+      // it; F x I and I x F: the transversal pair) plus the per-output contraction
+      const double NF = (P->degree + 1) * (P->degree + 2) / 2, NI = nd - NF;
+      fe -= (double)d->n_interior_faces * (32.0 * nqf * nd + 26.0 * nqf);
+      fe += (double)d->n_interior_faces * (2.0 * (22.0 * NF * NF + 8.0 * NF * NI) + 2.0 * (14.0 * NF + 4.0 * NI));
     }
     P->info.flops_engine = fe * P->nc;
     double b = 16.0 * (double)P->n_global + 24.0 * (double)P->n_verts;

@@ -54,6 +54,8 @@ struct FaceArgs {
   int n_dpc;
   int nc;
   PeerArgs peer;                      // multi-GPU: ghost cells' u read from their owner (n_own = cells)
+  const double* __restrict__ tfrags = nullptr;   // interior faces, reference-tensor form
+                                                 // (face_tensor_kernel.cuh): 96 signature tables
 };
 
 // Per-face geometry, computed once at plan creation by face_geometry_kernel and

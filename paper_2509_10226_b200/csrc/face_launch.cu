@@ -4,6 +4,7 @@
 #include <algorithm>
 
 #include "face_kernel.cuh"
+#include "face_tensor_kernel.cuh"
 #include "launch.h"
 #include "launch_common.cuh"
 
@@ -34,11 +35,49 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
   return cudaGetLastError();
 }
 
+// Reference-tensor interior-face kernel (face_tensor_kernel.cuh)
+template <int N, int BLOCK, int MINB, bool PF>
+static cudaError_t launch_face_x(const FaceArgs& a, int n_sm, cudaStream_t st) {
+  using S = FaceTensorShape<N>;
+  auto kern = face_tensor_kernel<N, BLOCK, MINB, PF>;
+  if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaError_t e = blocks_per_sm(kern, BLOCK, S::SMEM, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t work = a.n_chunks * a.nc;
+  if (work == 0) return cudaSuccess;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  if (blocks > work) blocks = work;
+  kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// variants of the tensor face kernel: 0 = by degree; 1..6 tuning (bench sweeps)
+template <int N>
+static cudaError_t launch_face_xt(const FaceArgs& a, int n_sm, cudaStream_t st, int variant) {
+  if (variant == 1) return launch_face_x<N, 256, 3, false>(a, n_sm, st);
+  if (variant == 2) return launch_face_x<N, 256, 2, true>(a, n_sm, st);
+  if (variant == 3) return launch_face_x<N, 256, 2, false>(a, n_sm, st);
+  if (variant == 4) return launch_face_x<N, 512, 1, true>(a, n_sm, st);
+  if (variant == 5) return launch_face_x<N, 128, 4, true>(a, n_sm, st);
+  if (variant == 6) return launch_face_x<N, 256, 3, true>(a, n_sm, st);
+  // measured (tools/gpu_face3.sh): P2 Helmholtz 96^3 128 x 4 CTAs with prefetch 1.77 ms
+  // (256 x 3 without: 1.80); P3 64^3 256 x 2 with prefetch 1.14 ms (best of 7)
+  if (N <= 10) return launch_face_x<N, 128, 4, true>(a, n_sm, st);
+  return launch_face_x<N, 256, 2, true>(a, n_sm, st);
+}
+
 // variant: 0 = default (by degree, below, blocked chunk runs); 1 = no prefetch, 3 CTAs/SM;
 // 2 = record prefetch, 3 CTAs/SM; 3 = record prefetch, 2 CTAs/SM; 4 = full prefetch, 2 CTAs/SM
 template <int N, int QF, bool BND>
 static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info,
                                  int variant) {
+  if (!BND && info) {
+    info->tnfrag = FaceTensorShape<N>::NFRAG;
+    info->tdmma_per_batch = FaceTensorShape<N>::DMMA_PER_BATCH;
+  }
+  if (!BND && !info && a.tfrags != nullptr && a.peer.u == nullptr) return launch_face_xt<N>(a, n_sm, st, variant);
   if (!BND && a.peer.u != nullptr && !info) {   // multi-GPU: plus-side ghost cells from peer memory
     if (N <= 10) return launch_face_v<N, QF, BND, 1, 3, 256, true, false, true>(a, n_sm, st, info);
     return launch_face_v<N, QF, BND, 2, 2, 256, true, false, true>(a, n_sm, st, info);

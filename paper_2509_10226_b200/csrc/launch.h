@@ -28,6 +28,8 @@ struct FaceLaunchInfo {
   int chunk = 0;            // batches per CTA chunk
   int dmma_per_batch = 0;
   int grid = 0;
+  int tnfrag = 0;           // reference-tensor interior-face kernel: fragments per signature
+  int tdmma_per_batch = 0;  //   and its DMMAs per 8-face batch (0: no tensor kernel)
 };
 
 // info != nullptr: only fill the launch description (no launch).

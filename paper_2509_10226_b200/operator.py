@@ -37,6 +37,7 @@ __all__ = ["OperatorConfig", "SipgConfig", "HelmholtzCoefficients", "CgPoissonOp
 _STAGES = ("ref", "data", "mm", "sched")
 _ENGINES = {"auto": 0, "dmma": 1, "dfma": 2, "tensor": 3}
 _PATCHES = {"auto": 0, "off": 1, "on": 2}
+_FACE_ENGINES = {"auto": 0, "quadrature": 1, "tensor": 2}
 
 
 @dataclass(frozen=True)
@@ -59,6 +60,7 @@ class OperatorConfig:
     concurrent_dg: bool = False  # DG: run the cell and face kernels concurrently (accumulating)
     cell_engine: str = "auto"    # B200 cell kernel: auto | dmma (quadrature points) | dfma | tensor (affine reference tensor)
     cell_patches: str = "auto"   # B200 CG warp-patch assembly: auto (= off, measured slower) | off | on
+    face_engine: str = "auto"    # B200 interior faces: auto (tensor at P2/P3) | quadrature (points) | tensor
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -71,6 +73,8 @@ class OperatorConfig:
             raise ValueError(f"unknown cell engine {self.cell_engine!r}")
         if self.cell_patches not in _PATCHES:
             raise ValueError(f"unknown cell patch mode {self.cell_patches!r}")
+        if self.face_engine not in _FACE_ENGINES:
+            raise ValueError(f"unknown face engine {self.face_engine!r}")
         if self.backend not in ("auto", "compiled", "python", "b200"):
             raise ValueError(f"unknown backend {self.backend!r}")
 
@@ -192,7 +196,8 @@ class _B200Operator:
             ((int(getattr(self.config, "face_chunk", 0)) // 8 & 0xF) << 8) | \
             ((1 if getattr(self.config, "concurrent_dg", False) else 0) << 12) | \
             (_ENGINES[getattr(self.config, "cell_engine", "auto")] << 13) | \
-            (_PATCHES[getattr(self.config, "cell_patches", "auto")] << 15)
+            (_PATCHES[getattr(self.config, "cell_patches", "auto")] << 15) | \
+            (_FACE_ENGINES[getattr(self.config, "face_engine", "auto")] << 17)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))

@@ -53,6 +53,28 @@ def test_gpu_quadrature_and_tensor_engines_match_golden(name, engine):
     assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
 
 
+@pytest.mark.parametrize("engine", ["quadrature", "tensor"])
+@pytest.mark.parametrize("name", [n for n in golden_names() if n.startswith(("dg", "helm"))])
+def test_gpu_face_engines_match_golden(name, engine):
+    """Interior faces: the point loop (face_kernel.cuh) and the reference-tensor form
+    (face_tensor_kernel.cuh, per-signature precontracted tables) against every DG golden."""
+    g = load_golden(name)
+    A = operator_from_fixture(g, face_engine=engine)
+    if A.info["n_face_batches"]:
+        assert A.info["face_engine"] == (2 if engine == "tensor" else 1)
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
+
+
+@pytest.mark.parametrize("variant", range(1, 7))
+@pytest.mark.parametrize("name", ["dg_p2_n3_gm_dir", "dg_p3_n3_gm_dir", "helmk_p2_n3_gm_dir", "helm3_p2_n2_gm_none"])
+def test_gpu_face_tensor_variants_match_golden(name, variant):
+    g = load_golden(name)
+    A = operator_from_fixture(g, face_engine="tensor", face_variant=variant)
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}/v{variant}: rel L2 {err:.3e}"
+
+
 @pytest.mark.parametrize("variant", range(1, 8))
 @pytest.mark.parametrize("name", ["cg_p1_n3_gm_dir2", "cg_p2_n8_gm", "cg3_p2_n3_ref_dir", "cg_p4_n3_gm_dir",
                                   "helmk_p2_n3_gm_dir", "dg_p3_n3_gm_dir"])
