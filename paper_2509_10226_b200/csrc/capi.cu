@@ -578,7 +578,10 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   return TMF_OK;
 }
 
-int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaEvent_t* ev) {
+// y_zeroed: the caller already cleared y (CG); energy: += sum_e u_e^T A_e u_e + the identity
+// rows' u_i^2 (= u.Au when the tensor cell engine runs; PCG's fused p.Ap)
+int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaEvent_t* ev,
+                 bool y_zeroed = false, double* energy = nullptr) {
   bool ok = true;
   if (ev) TMF_CUDA(cudaEventRecord(ev[0], st));
   if (P->dg && P->faces && P->concurrent) {
@@ -606,9 +609,12 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
     if (ev) TMF_CUDA(cudaEventRecord(ev[3], st));
     return TMF_OK;
   }
-  if (!P->dg) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
-  TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y), P->n_sm, st, nullptr, &ok,
-                            P->variant, P->engine));
+  if (!P->dg && !y_zeroed) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
+  {
+    tmf::CellArgs ca = P->cell_args(u, y);
+    ca.energy = energy;
+    TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, ca, P->n_sm, st, nullptr, &ok, P->variant, P->engine));
+  }
   // stage events only between kernels that exist (an event record between two empty
   // stages still costs ~3 us of GPU time, which would inflate the measured apply)
   const bool fix = !P->dg && P->n_fix;
@@ -620,7 +626,7 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
                               P->face_variant));
   }
   if (ev && P->faces && fix) TMF_CUDA(cudaEventRecord(ev[2], st));
-  if (fix) TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st));
+  if (fix) TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st, energy));
   if (ev) TMF_CUDA(cudaEventRecord(ev[3], st));
   return TMF_OK;
 }
@@ -1207,6 +1213,18 @@ int tmf_pcg(tmf_plan* P, const double* b, double* x, int iters, double* res_norm
   int rc = tmf_diagonal(P, dg, stream);
   if (rc) return rc;
   const int grid = P->n_sm * 4, blk = 512;
+  // fused iteration when the element energies are available (tensor cell engine, plain
+  // single-GPU plan): apply(+p.Ap) -> residual -> step (x, p, q = 0)
+  const bool fused = P->info.cell_engine == 3 && !P->local && !P->peer.u && !P->dg;
+  if (fused) {
+    tmf::pcg_init_fused_kernel<<<grid, blk, 0, st>>>(b, dg, x, r, z, p, q, n, rz, rr);
+    TMF_CUDA(cudaGetLastError());
+    for (int k = 0; k < iters; ++k) {
+      if ((rc = launch_apply(P, p, q, st, nullptr, true, pq + k))) return rc;
+      tmf::pcg_residual_kernel<<<grid, blk, 0, st>>>(q, dg, r, z, n, rz + k, pq + k, rz + k + 1, rr + k + 1);
+      tmf::pcg_step_kernel<<<grid, blk, 0, st>>>(z, p, x, q, n, rz + k, pq + k, rz + k + 1);
+    }
+  } else {
   tmf::pcg_init_kernel<<<grid, blk, 0, st>>>(b, dg, x, r, z, p, n, rz, rr);
   TMF_CUDA(cudaGetLastError());
   for (int k = 0; k < iters; ++k) {
@@ -1214,6 +1232,7 @@ int tmf_pcg(tmf_plan* P, const double* b, double* x, int iters, double* res_norm
     tmf::dot_kernel<<<grid, blk, 0, st>>>(p, q, n, pq + k);
     tmf::pcg_update_kernel<<<grid, blk, 0, st>>>(p, q, dg, x, r, z, n, rz + k, pq + k, rz + k + 1, rr + k + 1);
     tmf::pcg_direction_kernel<<<grid, blk, 0, st>>>(z, p, n, rz + k, rz + k + 1);
+  }
   }
   TMF_CUDA(cudaGetLastError());
   if (res_norms) {

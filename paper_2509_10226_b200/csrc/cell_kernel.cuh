@@ -49,6 +49,7 @@ struct CellArgs {
   int numax = 0;                   // max unique DoFs of a patch (even)
   int recmax = 0;                  // max record bytes (multiple of 16)
   PeerArgs peer;                   // multi-GPU: ghost DoFs read / scattered over peer memory
+  double* energy = nullptr;        // CG tensor engine: += sum_e u_e^T A_e u_e (PCG's p.Ap)
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the
@@ -366,12 +367,22 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
 }
 
 // y[c] = u[c] on strongly constrained DoFs (identity rows, operator.py:327-328)
+// energy != nullptr: also += sum over the list of u[g] y[g] = u[g]^2 (the identity rows'
+// share of u.Au, which the cell kernels' element energies leave out)
 static __global__ void dirichlet_fixup_kernel(const double* __restrict__ u, double* __restrict__ y,
-                                       const int* __restrict__ list, int64_t n) {
+                                       const int* __restrict__ list, int64_t n, double* energy) {
+  double e = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t g = list[i];
-    y[g] = u[g];
+    const double v = u[g];
+    y[g] = v;
+    e += v * v;
+  }
+  if (energy) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    if ((threadIdx.x & 31) == 0 && e != 0.0) atomicAdd(energy, e);
   }
 }
 

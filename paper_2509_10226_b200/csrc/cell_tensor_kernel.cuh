@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
   };
   int pidx[MT][KK];
   double pav[MT][KK], pG[MT][6], pmdet[MT];
+  double en = 0.0;   // sum of u_i y_i over the lane's outputs (element energies, CG)
   if (PF) {
     load_data(st, pidx, pav, pG, pmdet);
     load_indices(st + step);
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
             *dst = yv[m];
         } else {
           const int g = idx[m][ib];
+          en = fma(av[m][ib], yv[m], en);   // av = u at this DoF (0 when masked)
           if (g >= 0) {
             if (PEER)
               atomicAdd(peer_dst(a.peer, a.y, g, a.nc, comp), yv[m]);
@@ -189,6 +191,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
         }
       }
     }
+  }
+  if (!DG && a.energy != nullptr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) en += __shfl_xor_sync(0xffffffffu, en, o);
+    if (lane == 0) atomicAdd(a.energy, en);
   }
   if (PEER && a.peer.y != nullptr) __threadfence_system();
 }

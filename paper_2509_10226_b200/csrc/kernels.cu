@@ -62,11 +62,11 @@ cudaError_t launch_patch_geometry(const double* cgeo, const int4* pmeta, void* p
 }
 
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
-                         cudaStream_t st) {
+                         cudaStream_t st, double* energy) {
   if (n == 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 4 * n_sm) blocks = 4 * n_sm;
-  dirichlet_fixup_kernel<<<(unsigned)blocks, 256, 0, st>>>(u, y, list, n);
+  dirichlet_fixup_kernel<<<(unsigned)blocks, 256, 0, st>>>(u, y, list, n, energy);
   return cudaGetLastError();
 }
 

@@ -43,6 +43,6 @@ cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st
 cudaError_t launch_patch_geometry(const double* cgeo, const int4* pmeta, void* prec, int64_t n_cells,
                                   int CH, int n_sm, cudaStream_t st);
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
-                         cudaStream_t st);
+                         cudaStream_t st, double* energy = nullptr);
 
 }  // namespace tmf

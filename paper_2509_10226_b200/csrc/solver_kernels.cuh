@@ -135,4 +135,72 @@ __global__ void pcg_direction_kernel(const double* __restrict__ z, double* __res
     p[i] = z[i] + beta * p[i];
 }
 
+// ---- fused iteration (single GPU, tensor cell engine): p.Ap comes out of the cell kernel as
+// the sum of element energies (CellArgs::energy) and the x update and the zeroing of the
+// next A p ride along with the search-direction update -- 11 vector passes per iteration
+// instead of 14 (memset, dot, update, direction).
+
+// r = b, z = r / d, p = z, x = 0, q = 0; rz0 += r.z, rr0 += r.r
+__global__ void pcg_init_fused_kernel(const double* __restrict__ b, const double* __restrict__ d,
+                                      double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                                      double* __restrict__ p, double* __restrict__ q, int64_t n, double* rz,
+                                      double* rr) {
+  __shared__ double sh[32];
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = b[i], zi = ri / d[i];
+    x[i] = 0.0;
+    q[i] = 0.0;
+    r[i] = ri;
+    z[i] = zi;
+    p[i] = zi;
+    s1 += ri * zi;
+    s2 += ri * ri;
+  }
+  s1 = block_sum(s1, sh);
+  __syncthreads();
+  s2 = block_sum(s2, sh);
+  if (threadIdx.x == 0) {
+    atomicAdd(rz, s1);
+    atomicAdd(rr, s2);
+  }
+}
+
+// alpha = rz[k] / pq[k]; r -= alpha q; z = r / d; rz[k+1] += r.z; rr[k+1] += r.r
+__global__ void pcg_residual_kernel(const double* __restrict__ q, const double* __restrict__ d,
+                                    double* __restrict__ r, double* __restrict__ z, int64_t n, const double* rz_k,
+                                    const double* pq_k, double* rz_next, double* rr_next) {
+  __shared__ double sh[32];
+  const double alpha = *rz_k / *pq_k;
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = r[i] - alpha * q[i];
+    const double zi = ri / d[i];
+    r[i] = ri;
+    z[i] = zi;
+    s1 += ri * zi;
+    s2 += ri * ri;
+  }
+  s1 = block_sum(s1, sh);
+  __syncthreads();
+  s2 = block_sum(s2, sh);
+  if (threadIdx.x == 0) {
+    atomicAdd(rz_next, s1);
+    atomicAdd(rr_next, s2);
+  }
+}
+
+// x += alpha p (the old p), p = z + beta p, q = 0 (the next apply scatters into it)
+__global__ void pcg_step_kernel(const double* __restrict__ z, double* __restrict__ p, double* __restrict__ x,
+                                double* __restrict__ q, int64_t n, const double* rz_k, const double* pq_k,
+                                const double* rz_next) {
+  const double alpha = *rz_k / *pq_k, beta = *rz_next / *rz_k;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double pi = p[i];
+    x[i] += alpha * pi;
+    p[i] = z[i] + beta * pi;
+    q[i] = 0.0;
+  }
+}
+
 }  // namespace tmf
