@@ -39,7 +39,7 @@ struct FaceTensorShape {
   static constexpr int KI = (2 * NI + 3) / 4;   // over [-I | +I]
   static constexpr int RF = 4 * KF + KI;         // fragments per out-F block
   static constexpr int NFRAG = KF * RF + KI * KF;
-  static constexpr int SMEM = NFRAG * 32 * 8;
+  static constexpr int SMEM = NFRAG * 32 * 8 + 4 * N * 4;   // tables + the 4 gather orders
   static constexpr int DMMA_PER_BATCH = NFRAG;
 };
 
@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_tensor_kernel(FaceArgs a) {
   using S = FaceTensorShape<N>;
   constexpr int NF = S::NF, NI = S::NI, KF = S::KF, KI = S::KI, RF = S::RF;
   extern __shared__ __align__(16) double smem[];
+  int* sperm = reinterpret_cast<int*>(smem + S::NFRAG * 32);   // (4, N) gather orders
+  for (int i = threadIdx.x; i < 4 * N; i += BLOCK) sperm[i] = __ldg(a.perm + i);
   const int lane = threadIdx.x & 31;
   const int fs = lane >> 2;
   const int q4 = lane & 3;
@@ -62,13 +64,19 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_tensor_kernel(FaceArgs a) {
   const int64_t w0 = blockIdx.x * per;
   const int64_t w1 = w0 + per < nwork ? w0 + per : nwork;
   int cur_sig = -1;
+  auto chunk_at = [&](int64_t w) {
+    const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
+    return __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
+  };
+  int4 nch = w0 < w1 ? chunk_at(w0) : make_int4(0, 0, 0, 0);
   for (int64_t w = w0; w < w1; ++w) {
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
-    const int4 ch = __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
+    const int4 ch = nch;
+    if (w + 1 < w1) nch = chunk_at(w + 1);   // the next chunk's record, one chunk ahead
     const int lfm = ch.x / 6, lfp = ch.y / 6;
     const int sig = lfm * 24 + ch.y;
-    if (sig != cur_sig) {
-      __syncthreads();   // the previous chunk's warps are done with the staged table
+    if (sig != cur_sig || cur_sig < 0) {
+      __syncthreads();   // the previous chunk's warps are done with the staged table (and sperm is set)
       const double2* src = reinterpret_cast<const double2*>(a.tfrags + (int64_t)sig * S::NFRAG * 32);
       double2* dst = reinterpret_cast<double2*>(smem);
       for (int i = threadIdx.x; i < S::NFRAG * 16; i += BLOCK) dst[i] = __ldg(src + i);
@@ -83,9 +91,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_tensor_kernel(FaceArgs a) {
       const int x = 4 * k + q4;
       offF[k] = -1;
       if (x < NF) {
-        offF[k] = __ldg(a.perm + lfm * N + x);
+        offF[k] = sperm[lfm * N + x];
       } else if (x < 2 * NF) {
-        offF[k] = __ldg(a.perm + lfp * N + x - NF);
+        offF[k] = sperm[lfp * N + x - NF];
         sideF |= 1u << k;
       }
     }
@@ -94,9 +102,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_tensor_kernel(FaceArgs a) {
       const int x = 4 * k + q4;
       offI[k] = -1;
       if (x < NI) {
-        offI[k] = __ldg(a.perm + lfm * N + NF + x);
+        offI[k] = sperm[lfm * N + NF + x];
       } else if (x < 2 * NI) {
-        offI[k] = __ldg(a.perm + lfp * N + NF + x - NI);
+        offI[k] = sperm[lfp * N + NF + x - NI];
         sideI |= 1u << k;
       }
     }
