@@ -250,12 +250,28 @@ def gpu_bench(args, rank, world):
                 A = DistributedCgOperator(m, dm, geo, bas, rank, world, part=partition_of(m, world),
                                           transport=transport)
                 if transport == "p2p":
-                    A.connect_ipc()
+                    # CUDA-IPC mapping of the peers' buffers; if any rank cannot map them,
+                    # every rank falls back to the NCCL halo transport
+                    ok = 1.0
+                    try:
+                        A.connect_ipc()
+                    except Exception as e:  # noqa: BLE001
+                        print(f"rank {rank}: peer mapping failed ({e}); NCCL halo instead", file=sys.stderr)
+                        ok = 0.0
+                    flag = torch.tensor([ok], dtype=torch.float64, device="cuda")
+                    if world > 1:
+                        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+                    if float(flag[0]) < 1.0:
+                        transport = "nccl"
+                        for q in problems:
+                            if q["ids"] is not None:
+                                q["A"].set_transport("nccl")
+                        A.set_transport("nccl")
                 ids = A.owned_global_ids
                 local = A.local_op
             u_host = u_glob if ids is None else u_glob[ids]
             u = torch.from_numpy(np.ascontiguousarray(u_host)).cuda()
-            if ids is not None and transport == "p2p":
+            if ids is not None and transport == "p2p" and A.transport == "p2p":
                 # the registered (peer-visible) local buffers, used in place
                 A.bufs.u[: len(u_host)].copy_(u)
                 u, y = A.bufs.u, A.bufs.y
@@ -271,7 +287,7 @@ def gpu_bench(args, rank, world):
             u_pin = torch.from_numpy(np.ascontiguousarray(u_host)).pin_memory()
             y_pin = torch.empty_like(u_pin).pin_memory()
             problems.append(dict(p=p, reorder=reorder, A=A, local=local, u=u, y=y, u_pin=u_pin, y_pin=y_pin,
-                                 ndof=len(u_host), ndof_global=dm.n_global_dofs))
+                                 ndof=len(u_host), ndof_global=dm.n_global_dofs, ids=ids))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     # self-check of the peer-memory transport against the NCCL halo path (same plans)

@@ -356,6 +356,7 @@ struct tmf_plan {
   double* cell_geo = nullptr;
   double* face_frags = nullptr;
   double* face_tfrags = nullptr;   // reference-tensor interior-face tables (96 signatures)
+  std::vector<double> p1_tab;      // P1: constant gradients a[3][4] + sum of weights (13)
   int face_engine = 0;             // (desc.flags >> 17) & 3: 0 by degree, 1 quadrature points, 2 tensor
   int* face_perm = nullptr;
   int* cells = nullptr;
@@ -407,6 +408,7 @@ struct tmf_plan {
     a.dofs = dg ? nullptr : dofs + c0 * N;
     a.cgeo = cell_geo + 8 * c0;
     a.frags = cell_frags;
+    a.hP1 = p1_tab.empty() ? nullptr : p1_tab.data();
     a.n_cells = c1 - c0;
     a.nc = nc;
     if (!dg && with_peer) a.peer = peer;   // CG ghost DoFs over peer memory (DG: the face kernel's ghost cells)
@@ -788,6 +790,21 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     if ((rc = upload(&P->cell_frags, fr.data(), fr.size(), &total))) return bail(rc);
     P->info.flops_issued = ci.flops_issued;
     P->info.cell_engine = ci.table == 2 ? 3 : ci.table == 1 ? 2 : 1;
+    if (N == 4 && ci.table == 2) {
+      // P1: point-independent gradients -> the one-point collapse of cell_p1_thread_kernel
+      bool constant = true;
+      for (int q = 1; q < Q && constant; ++q)
+        for (int r = 0; r < 12; ++r)
+          if (std::fabs(Gm[3 * q * N + r] - Gm[r]) > 1e-13) constant = false;
+      if (constant) {
+        P->p1_tab.assign(13, 0.0);
+        for (int k = 0; k < 3; ++k)
+          for (int i = 0; i < 4; ++i) P->p1_tab[4 * k + i] = Gm[k * N + i];
+        long double ws = 0.0L;
+        for (int q = 0; q < Q; ++q) ws += d->cell_weights[q];
+        P->p1_tab[12] = (double)ws;
+      }
+    }
   }
 
   // per-cell geometry (G, mass factor), computed once on the device

@@ -50,6 +50,8 @@ struct CellArgs {
   int recmax = 0;                  // max record bytes (multiple of 16)
   PeerArgs peer;                   // multi-GPU: ghost DoFs read / scattered over peer memory
   double* energy = nullptr;        // CG tensor engine: += sum_e u_e^T A_e u_e (PCG's p.Ap)
+  const double* hP1 = nullptr;     // HOST: P1 constant gradients a[3][4] and sum of weights (13
+                                   // doubles, launcher only: a kernel parameter of the P1 kernel)
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the

@@ -77,6 +77,27 @@ static cudaError_t launch_cell_x(const CellArgs& a, int n_sm, cudaStream_t st, C
   return cudaGetLastError();
 }
 
+// P1 thread-per-cell kernel (cell_p1_thread_kernel): needs the plan's constant-gradient
+// table (a.hP1, set when the P1 gradient tables are point-independent)
+template <bool DG, int BLOCK, int MINB>
+static cudaError_t launch_cell_p1(const CellArgs& a, int n_sm, cudaStream_t st) {
+  if (a.n_cells == 0) return cudaSuccess;
+  P1Tab T;
+  for (int k = 0; k < 3; ++k)
+    for (int i = 0; i < 4; ++i) T.a[k][i] = a.hP1[4 * k + i];
+  T.w = a.hP1[12];
+  auto kern = cell_p1_thread_kernel<DG, BLOCK, MINB>;
+  int per_sm = 0;
+  cudaError_t e = blocks_per_sm(kern, BLOCK, 0, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t need = (a.n_cells * a.nc + BLOCK - 1) / BLOCK;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  if (blocks > need) blocks = need;
+  kern<<<(unsigned)blocks, BLOCK, 0, st>>>(a, T);
+  return cudaGetLastError();
+}
+
 // variants: 0 = per-degree default; 1..7 = tuning (bench sweeps only)
 template <int N, bool MASS, bool DG>
 static cudaError_t launch_cell_xt(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info,
@@ -99,8 +120,11 @@ static cudaError_t launch_cell_xt(const CellArgs& a, int n_sm, cudaStream_t st, 
     if (variant == 10) return launch_cell_x<N, MASS, DG, 512, 2, 2, false, true>(a, n_sm, st, info);
     if (variant == 11) return launch_cell_x<N, MASS, DG, 256, 1, 6, false, true>(a, n_sm, st, info);
     if (variant == 12) return launch_cell_x<N, MASS, DG, 512, 1, 3, false, true>(a, n_sm, st, info);
-    if (variant == 13) return launch_cell_x<N, MASS, DG, 256, 1, 8, false, false>(a, n_sm, st, info);
     if (variant == 14) return launch_cell_x<N, MASS, DG, 256, 2, 4, false, true>(a, n_sm, st, info);
+    if (N == 4 && !MASS && a.peer.u == nullptr && a.hP1 != nullptr && !info) {   // P1 thread per cell
+      if (variant == 15) return launch_cell_p1<DG, 256, 4>(a, n_sm, st);
+      if (variant == 7) return launch_cell_p1<DG, 512, 2>(a, n_sm, st);
+    }
   }
   // per-degree defaults, measured on CG 48^3 reordered (tools/gpu_tensor1.sh, variants 0-7):
   //   P1 768 threads x 2 tiles 31.5 us (256 x 2: 34.6), P2 1024 x 1 65.0 us (67.8),
