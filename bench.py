@@ -43,7 +43,10 @@ sys.path.insert(0, ROOT)
 FP64_PEAK_TFLOPS = 37.1   # measured: DMMA m8n8k4 on this pool's B200 (profiles/r01_fp64_peak.json)
 FP64_PEAK_SOURCE = "profiles/r01_fp64_peak.json (mma.sync m8n8k4 f64 microbench on B200, 1965 MHz)"
 DEGREES = (1, 2, 3, 4)
-ENGINE_NAMES = {1: "dmma-quadrature", 2: "dfma-quadrature", 3: "dmma-reference-tensor"}
+ENGINE_NAMES = {1: "dmma-quadrature", 2: "dfma-quadrature", 3: "dmma-reference-tensor",
+                4: "dmma-modal (point kernel on M = dim P_(p-1) exact modes)"}
+KERNEL_NAMES = {1: "cell_apply_kernel (n_q points)", 2: "cell_dfma_kernel", 3: "cell_tensor_kernel",
+                4: "cell_apply_kernel (modal tables)"}
 N_MESH = 48
 
 
@@ -434,12 +437,14 @@ def gpu_bench(args, rank, world):
     dofs_global = sum(pr["ndof_global"] for pr, _ in rec)
     return dict(total_ms=total_ms, dofs=dofs, dofs_global=dofs_global, n_glob=n_glob, e2e_s=e2e_s, per=per, clocks=clk.summary(),
                 transport=transport, p2p_check=p2p_check, quadrature_engine=quad,
-                roofline={"bound": "tensor", "kernel": f"cell_tensor_kernel ({dk})", "achieved": round(achieved, 3),
+                roofline={"bound": "tensor", "kernel": f"{KERNEL_NAMES.get(dom['local'].info['cell_engine'])} ({dk})",
+                          "achieved": round(achieved, 3),
                           "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE, "unit": "TFLOP/s",
                           "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
-                          "algorithmic": "useful flops of the reference-tensor cell algorithm per launch "
-                                         "(12 N^2 + 12 N + N per cell, N = DoFs per cell; tmf_plan_info.flops_engine) "
-                                         "/ CUDA-event kernel time"},
+                          "algorithmic": "useful flops of the algorithm the cell engine runs, per launch "
+                                         "(tmf_plan_info.flops_engine: modal 12 M N + 18 M + N per cell, M = dim "
+                                         "P_(p-1), N = DoFs per cell; reference tensor 12 N^2 + 13 N) / CUDA-event "
+                                         "kernel time"},
                 gpu_launches=n_kern, parity_rel_l2=err,
                 h2d=sum(8 * pr["ndof"] for pr in problems), d2h=sum(8 * pr["ndof"] for pr in problems))
 

@@ -83,8 +83,12 @@ typedef struct tmf_plan_desc {
                                   (0 by degree, 1 DMMA quadrature points, 2 DFMA,
                                   3 DMMA reference tensor); 15-16 CG
                                   patch-local assembly (0 auto, 1 off, 2 on); 17-18
-                                  interior-face engine (0 by degree, 1 quadrature
-                                  points, 2 reference tensor)                          */
+                                  face engine (0 by degree, 1 quadrature points,
+                                  2 reference tensor (interior faces), 3 modal: the
+                                  point loop on NF exact unit-weight face modes);
+                                  19: cell engine bit 2
+                                  (4 = modal: the point kernel on M = dim P_{p-1}
+                                  unit-weight modes)                                   */
 } tmf_plan_desc;
 
 typedef struct tmf_plan_info {
@@ -98,11 +102,12 @@ typedef struct tmf_plan_info {
   int32_t patch_cells;         /* CG patch-local assembly: cells per patch (0 = off)  */
   double patch_ratio;          /* unique patch DoFs / unmasked cell-DoF slots (CG)    */
   int32_t cell_engine;         /* cell kernel in use: 1 DMMA quadrature points, 2 DFMA,
-                                  3 DMMA reference tensor (affine precontraction)      */
+                                  3 DMMA reference tensor (affine precontraction),
+                                  4 modal (point kernel on M exact unit-weight modes) */
   double flops_engine;         /* useful flops per apply of the algorithm the engines
                                   run (= flops_alg except for the tensor engines)      */
-  int32_t face_engine;         /* interior faces: 1 quadrature points, 2 reference
-                                  tensor (0: no faces)                                 */
+  int32_t face_engine;         /* faces: 1 quadrature points, 2 reference tensor,
+                                  3 modal (0: no faces)                                */
 } tmf_plan_info;
 
 int tmf_plan_create(const tmf_plan_desc* desc, tmf_plan** out);

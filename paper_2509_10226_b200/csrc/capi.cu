@@ -211,6 +211,89 @@ int build_face_tensor_fragments(int N, int NF, int QF, F Ev, const double* w, st
   return dropped <= 1e-12 * std::max(kept, 1.0) ? TMF_OK : TMF_EINVAL;
 }
 
+// Symmetric eigendecomposition by cyclic Jacobi rotations in long double (small n):
+// A (n x n, row-major, destroyed) -> eigenvalues lam (descending) and eigenvectors V
+// (column m of V belongs to lam[m]).
+void jacobi_eigen(int n, std::vector<long double>& A, std::vector<long double>& lam, std::vector<long double>& V) {
+  V.assign((size_t)n * n, 0.0L);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0L;
+  auto a = [&](int i, int j) -> long double& { return A[(size_t)i * n + j]; };
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    long double off = 0.0L, diag = 0.0L;
+    for (int i = 0; i < n; ++i) {
+      diag += a(i, i) * a(i, i);
+      for (int j = i + 1; j < n; ++j) off += a(i, j) * a(i, j);
+    }
+    if (off <= 1e-36L * diag) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        if (a(p, q) == 0.0L) continue;
+        const long double th = (a(q, q) - a(p, p)) / (2.0L * a(p, q));
+        const long double t = (th >= 0 ? 1.0L : -1.0L) / (std::fabs(th) + std::sqrt(th * th + 1.0L));
+        const long double c = 1.0L / std::sqrt(t * t + 1.0L), sn = t * c;
+        for (int k = 0; k < n; ++k) {   // A <- A J (columns p, q)
+          const long double akp = a(k, p), akq = a(k, q);
+          a(k, p) = c * akp - sn * akq;
+          a(k, q) = sn * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {   // A <- J^T A (rows p, q)
+          const long double apk = a(p, k), aqk = a(q, k);
+          a(p, k) = c * apk - sn * aqk;
+          a(q, k) = sn * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          long double& vp = V[(size_t)k * n + p];
+          long double& vq = V[(size_t)k * n + q];
+          const long double x = vp, y = vq;
+          vp = c * x - sn * y;
+          vq = sn * x + c * y;
+        }
+      }
+  }
+  std::vector<int> ord(n);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::sort(ord.begin(), ord.end(), [&](int x, int y) { return a(x, x) > a(y, y); });
+  std::vector<long double> V2((size_t)n * n);
+  lam.resize(n);
+  for (int m = 0; m < n; ++m) {
+    lam[m] = a(ord[m], ord[m]);
+    for (int k = 0; k < n; ++k) V2[(size_t)k * n + m] = V[(size_t)k * n + ord[m]];
+  }
+  V.swap(V2);
+}
+
+// Modal cell tables.  The reference's cell term needs only the point sums
+//   H[(k,i),(l,j)] = sum_q w_q d_k phi_i(q) d_l phi_j(q)          (3N x 3N)
+// -- exact integrals of products of P_{p-1} polynomials, so H is positive semidefinite
+// of rank M = dim P_{p-1} = p(p+1)(p+2)/6 (4 / 10 / 20 at P2 / P3 / P4) however many
+// points the rule has (GM: 15 / 35 / 70).  With H = sum_m lam_m v_m v_m^T,
+//   E'(k, m, i) = sqrt(lam_m) v_m[(k,i)]   satisfies   sum_m E'(k,m,i) E'(l,m,j) = H,
+// i.e. E' is an M-"point" rule with unit weights that integrates the cell term exactly:
+// the quadrature-point kernel (cell_kernel.cuh) runs on it unchanged, with M instead of
+// n_q points.  Returns false unless the spectrum has the expected rank gap.
+bool build_modal_cell_tables(int N, int Q, int M, const double* Gm, const double* w, std::vector<double>& E) {
+  const int n = 3 * N;
+  std::vector<long double> H((size_t)n * n, 0.0L);
+  for (int a = 0; a < n; ++a)
+    for (int b = a; b < n; ++b) {
+      long double acc = 0.0L;
+      const int k = a / N, i = a % N, l = b / N, j = b % N;
+      for (int q = 0; q < Q; ++q) acc += (long double)w[q] * Gm[(3 * q + k) * N + i] * Gm[(3 * q + l) * N + j];
+      H[(size_t)a * n + b] = H[(size_t)b * n + a] = acc;
+    }
+  std::vector<long double> lam, V;
+  jacobi_eigen(n, H, lam, V);
+  if (M >= n || !(lam[0] > 0) || !(lam[M - 1] > 1e-10L * lam[0]) || !(std::fabs(lam[M]) <= 1e-12L * lam[0]))
+    return false;
+  E.assign((size_t)3 * M * N, 0.0);   // layout of grad_matrix: row 3 m + k, column i
+  for (int m = 0; m < M; ++m) {
+    const long double s = std::sqrt(lam[m]);
+    for (int k = 0; k < 3; ++k)
+      for (int i = 0; i < N; ++i) E[(size_t)(3 * m + k) * N + i] = (double)(s * V[(size_t)(k * N + i) * n + m]);
+  }
+  return true;
+}
+
 // CG warp-patch records (cell_patch_kernel.cuh) for patches of CH = 32 consecutive
 // cells; contribution slots are j*CH + cl.  Two parallel passes over the patches
 // (sizes, then fill at the prefix-summed offsets); per patch the (DoF, slot) pairs
@@ -340,7 +423,11 @@ struct tmf_plan {
   int dev = 0, n_sm = 0;
   int kind = 0, degree = 0, N = 0, Q = 0, QF = 0, nc = 1;
   int variant = 0;       // desc.flags & 0xF: cell-kernel tuning variant (0 = default)
-  int engine = 0;        // (desc.flags >> 13) & 3: cell engine 0 = by degree, 1 = DMMA, 2 = DFMA
+  int engine = 0;        // (desc.flags >> 13) & 3 (| 4 via bit 19): cell engine 0 = by degree,
+                         // 1 = DMMA points, 2 = DFMA, 3 = reference tensor, 4 = modal
+  int kengine = 0;       // engine handed to the launcher (modal runs the point kernel: 1)
+  int Qk = 0;            // "points" of the cell kernel (n_q, or M for the modal tables)
+  int QFk = 0;           // "points" of the face kernel (n_qf, or NF for the modal face tables)
   bool concurrent = false;  // DG: cell and face kernels run concurrently (flags bit 12)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -599,11 +686,11 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
     TMF_CUDA(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     tmf::CellArgs ca = P->cell_args(u, y);
     ca.accumulate = 1;
-    TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, ca, P->n_sm, P->side, nullptr, &ok, P->variant, P->engine));
+    TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, ca, P->n_sm, P->side, nullptr, &ok, P->variant, P->kengine));
     if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
-    TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
-    TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
     TMF_CUDA(cudaEventRecord(P->ev_join, P->side));
     TMF_CUDA(cudaStreamWaitEvent(st, P->ev_join, 0));
@@ -615,16 +702,16 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
   {
     tmf::CellArgs ca = P->cell_args(u, y);
     ca.energy = energy;
-    TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, ca, P->n_sm, st, nullptr, &ok, P->variant, P->engine));
+    TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, ca, P->n_sm, st, nullptr, &ok, P->variant, P->kengine));
   }
   // stage events only between kernels that exist (an event record between two empty
   // stages still costs ~3 us of GPU time, which would inflate the measured apply)
   const bool fix = !P->dg && P->n_fix;
   if (ev && (P->faces || fix)) TMF_CUDA(cudaEventRecord(ev[1], st));
   if (P->faces) {
-    TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
-    TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
   }
   if (ev && P->faces && fix) TMF_CUDA(cudaEventRecord(ev[2], st));
@@ -654,20 +741,20 @@ int tmf_apply_stages(tmf_plan* P, const double* u, double* y, int stages, int64_
       // cells touching no ghost DoF run the plain kernel, the rest the peer-memory one
       const int64_t m = std::min(std::max(P->n_peer_free, cell_begin), cell_end);
       if (m > cell_begin)
-        TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, cell_begin, m, false), P->n_sm,
-                                  st, nullptr, &ok, P->variant, P->engine));
+        TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, P->cell_args(u, y, cell_begin, m, false), P->n_sm,
+                                  st, nullptr, &ok, P->variant, P->kengine));
       if (cell_end > m)
-        TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, m, cell_end), P->n_sm, st,
-                                  nullptr, &ok, P->variant, P->engine));
+        TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, P->cell_args(u, y, m, cell_end), P->n_sm, st,
+                                  nullptr, &ok, P->variant, P->kengine));
     } else {
-      TMF_CUDA(tmf::launch_cell(P->N, P->Q, P->mass, P->dg, P->cell_args(u, y, cell_begin, cell_end), P->n_sm,
-                                st, nullptr, &ok, P->variant, P->engine));
+      TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, P->cell_args(u, y, cell_begin, cell_end), P->n_sm,
+                                st, nullptr, &ok, P->variant, P->kengine));
     }
   }
   if ((stages & TMF_STAGE_FACES) && P->faces) {
-    TMF_CUDA(tmf::launch_face(P->N, P->QF, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
-    TMF_CUDA(tmf::launch_face(P->N, P->QF, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
                               P->face_variant));
   }
   if ((stages & TMF_STAGE_FIXUP) && !P->dg && P->n_fix)
@@ -726,7 +813,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   }
   P->kind = d->operator_kind;
   P->variant = d->flags & 0xF;
-  P->engine = (d->flags >> 13) & 3;
+  P->engine = ((d->flags >> 13) & 3) | (((d->flags >> 19) & 1) << 2);
   P->patches = (d->flags >> 15) & 3;
   // warp patches use the DFMA point-major tables (also for their global-kernel fallback)
   if (P->patches == 2 && d->operator_kind == TMF_CG_LAPLACE && d->n_dofs_per_cell <= 20) P->engine = 2;
@@ -761,15 +848,36 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
 
   // cell tables -> fragments
   {
-    const int N = P->N, Q = P->Q;
+    const int N = P->N;
     const double* V = d->value_matrix;
     const double* Gm = d->grad_matrix;
+    const double* W = d->cell_weights;
+    int Q = P->Q;
+    // engine by default: modal tables on the point kernel for Laplace cell terms at P2-P4
+    // (DMMAs per 8-cell tile 12 / 52 / 147 against 27 / 75 / 243 for the reference tensor
+    // and 42 / 151 / 513 for the n_q-point loop), the reference tensor otherwise (P1, mass)
+    std::vector<double> modal, ones;
+    int eng = P->engine;
+    if (eng == 0) eng = (!P->mass && N >= 10) ? 4 : 3;
+    if (eng == 4) {
+      const int p = P->degree, M = p * (p + 1) * (p + 2) / 6;
+      if (P->mass) return bail(fail(TMF_EINVAL, "the modal cell engine has no mass term (Helmholtz: use tensor)"));
+      if (!build_modal_cell_tables(N, Q, M, Gm, W, modal))
+        return bail(fail(TMF_EINVAL, "modal cell engine: gradient tables without the P_{p-1} rank structure"));
+      Gm = modal.data();
+      ones.assign(M, 1.0);
+      W = ones.data();
+      Q = M;
+    }
+    P->engine = eng;
+    P->kengine = eng == 4 ? 1 : eng;
+    P->Qk = Q;
     tmf::CellLaunchInfo ci;
     bool ok = true;
     tmf::CellArgs dummy{};
     dummy.n_cells = P->n_cells;
     dummy.nc = P->nc;
-    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok, P->variant, P->engine));
+    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok, P->variant, P->kengine));
     if (!ok) return bail(fail(TMF_EINVAL, "unsupported (n_dofs_per_cell, n_q) = (" +
                                               std::to_string(N) + ", " + std::to_string(Q) + ")"));
     const int NC = P->mass ? 4 : 3;
@@ -781,15 +889,15 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     if (ci.table == 2)
       build_tensor_fragments(
           N, Q, P->mass, [&](int k, int q, int j) { return Gm[(3 * q + k) * N + j]; },
-          [&](int q, int j) { return V[q * N + j]; }, d->cell_weights, fr);
+          [&](int q, int j) { return V[q * N + j]; }, W, fr);
     else if (ci.table == 0)
-      build_fragments(N, Q, NC, E, d->cell_weights, fr);
+      build_fragments(N, Q, NC, E, W, fr);
     else
-      build_point_rows(N, Q, NC, E, d->cell_weights, fr);
+      build_point_rows(N, Q, NC, E, W, fr);
     if ((int)fr.size() != ci.frag_doubles) return bail(fail(TMF_EINVAL, "internal: fragment size"));
     if ((rc = upload(&P->cell_frags, fr.data(), fr.size(), &total))) return bail(rc);
     P->info.flops_issued = ci.flops_issued;
-    P->info.cell_engine = ci.table == 2 ? 3 : ci.table == 1 ? 2 : 1;
+    P->info.cell_engine = eng == 4 ? 4 : ci.table == 2 ? 3 : ci.table == 1 ? 2 : 1;
     if (N == 4 && ci.table == 2) {
       // P1: point-independent gradients -> the one-point collapse of cell_p1_thread_kernel
       bool constant = true;
@@ -830,7 +938,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     tmf::CellArgs dummy{};
     dummy.n_cells = P->n_cells;
     dummy.nc = P->nc;
-    TMF_CUDA(tmf::launch_cell(P->N, P->Q, false, false, dummy, P->n_sm, 0, &ci, &ok, P->variant, P->engine));
+    TMF_CUDA(tmf::launch_cell(P->N, P->Qk, false, false, dummy, P->n_sm, 0, &ci, &ok, P->variant, P->kengine));
     if (P->patches == 2 && ci.patch_cells > 0) {
       PatchTables T;
       build_patches(enc.data(), P->n_cells, P->N, ci.patch_cells, T);
@@ -886,6 +994,53 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       std::copy(on.begin(), on.end(), perm.begin() + lf * N);
     }
     if ((rc = upload(&P->face_perm, perm.data(), perm.size(), &total))) return bail(rc);
+    // face engine by default: modal at P2-P4, the point loop at P1 (decided by measurement)
+    int fe = P->face_engine;
+    if (fe == 0) fe = N >= 10 ? 3 : 1;
+    P->face_engine = fe;
+    // modal face tables (face engine 3): every face integrand is a product of two P_p
+    // polynomials on the face (values in P_p, derivatives in P_{p-1}), so NF = dim P_p
+    // orthonormal modes integrate it exactly.  psi = V_F L^-T from the Cholesky factor of
+    // the Gram matrix of the face-DoF traces (lf 0, code 0; every (lf, code) table is
+    // indexed by the same reference-triangle points), and each table is projected:
+    //   E'(c, m, j) = sum_q w_q psi_m(q) E(c, q, j),  unit weights.
+    std::vector<double> proj;   // (NF, QF): w_q psi_m(q)
+    int QK = QF;
+    if (fe == 3) {
+      std::vector<long double> H((size_t)NF * NF, 0.0L), L((size_t)NF * NF, 0.0L);
+      const double* Fv0 = d->face_values;
+      for (int a = 0; a < NF; ++a)
+        for (int b = 0; b < NF; ++b) {
+          long double acc = 0.0L;
+          for (int q = 0; q < QF; ++q)
+            acc += (long double)d->face_weights[q] * Fv0[q * N + perm[a]] * Fv0[q * N + perm[b]];
+          H[(size_t)a * NF + b] = acc;
+        }
+      for (int j = 0; j < NF; ++j) {
+        long double dj = H[(size_t)j * NF + j];
+        for (int k = 0; k < j; ++k) dj -= L[(size_t)j * NF + k] * L[(size_t)j * NF + k];
+        if (!(dj > 1e-20L)) return bail(fail(TMF_EINVAL, "modal face engine: face traces are not a basis of P_p"));
+        L[(size_t)j * NF + j] = std::sqrt(dj);
+        for (int i = j + 1; i < NF; ++i) {
+          long double v = H[(size_t)i * NF + j];
+          for (int k = 0; k < j; ++k) v -= L[(size_t)i * NF + k] * L[(size_t)j * NF + k];
+          L[(size_t)i * NF + j] = v / L[(size_t)j * NF + j];
+        }
+      }
+      proj.assign((size_t)NF * QF, 0.0);
+      for (int q = 0; q < QF; ++q) {   // X = L^-1 V_F^T column by column (forward substitution)
+        std::vector<long double> x(NF);
+        for (int m = 0; m < NF; ++m) {
+          long double v = Fv0[q * N + perm[m]];
+          for (int k = 0; k < m; ++k) v -= L[(size_t)m * NF + k] * x[k];
+          x[m] = v / L[(size_t)m * NF + m];
+          proj[(size_t)m * QF + q] = (double)((long double)d->face_weights[q] * x[m]);
+        }
+      }
+      QK = NF;
+    }
+    P->QFk = QK;
+    std::vector<double> ones(QK, 1.0);
     std::vector<double> fr;
     for (int lf = 0; lf < 4; ++lf) {
       const double R[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
@@ -900,30 +1055,35 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       for (int code = 0; code < 6; ++code) {
         const double* Fv = d->face_values + (size_t)(lf * 6 + code) * QF * N;
         const double* Fg = d->face_grads + (size_t)(lf * 6 + code) * 3 * QF * N;
-        build_face_fragments(N, NF, QF, [&](int c, int q, int j) {
+        auto Ept = [&](int c, int q, int j) {   // component c at face point q, gather position j
           const int jj = pm[j];
           if (c == 0) return Fv[q * N + jj];
           const double* av = a[c - 1];
           return av[0] * Fg[(3 * q) * N + jj] + av[1] * Fg[(3 * q + 1) * N + jj] + av[2] * Fg[(3 * q + 2) * N + jj];
-        }, d->face_weights, fr);
+        };
+        if (fe == 3)
+          build_face_fragments(N, NF, QK, [&](int c, int m, int j) {
+            long double acc = 0.0L;
+            for (int q = 0; q < QF; ++q) acc += (long double)proj[(size_t)m * QF + q] * Ept(c, q, j);
+            return (double)acc;
+          }, ones.data(), fr);
+        else
+          build_face_fragments(N, NF, QF, Ept, d->face_weights, fr);
       }
     }
     tmf::FaceLaunchInfo fi;
     bool ok = true;
     tmf::FaceArgs dummy{};
     dummy.nc = P->nc;
-    TMF_CUDA(tmf::launch_face(N, QF, false, dummy, P->n_sm, 0, &fi, &ok));
+    TMF_CUDA(tmf::launch_face(N, QK, false, dummy, P->n_sm, 0, &fi, &ok));
     if (!ok) return bail(fail(TMF_EINVAL, "unsupported (n_dofs_per_cell, n_qf) = (" +
                                               std::to_string(N) + ", " + std::to_string(QF) + ")"));
     if ((int64_t)fr.size() != 24LL * fi.nfrag * 32) return bail(fail(TMF_EINVAL, "internal: face fragments"));
     if ((rc = upload(&P->face_frags, fr.data(), fr.size(), &total))) return bail(rc);
-    // reference-tensor interior-face tables: by default at P2-P4 (DMMAs per 8 faces 48 / 150
-    // / 416 vs 60 / 170 / 432 for the point loop, no per-point arithmetic; measured faces
-    // P2 96^3 Helmholtz 1.89 -> 1.77 ms, P3 64^3 1.34 -> 1.14 ms, P4 48^3 1.71 -> 1.31 ms);
-    // P1 keeps the point loop (20 vs 12 DMMAs: 0.91 vs 1.00 ms at 96^3)
-    int fe = P->face_engine;
-    if (fe == 0) fe = N >= 10 ? 2 : 1;
-    P->face_engine = fe;
+    // reference-tensor interior-face tables (face engine 2; DMMAs per 8 faces 48 / 150 / 416
+    // at P2-P4 vs 60 / 170 / 432 for the n_qf-point loop and 40 / 102 / 192 for the modal
+    // one; measured faces P2 96^3 Helmholtz 1.89 -> 1.77 ms, P3 64^3 1.34 -> 1.14 ms, P4
+    // 48^3 1.71 -> 1.31 ms against the n_qf-point loop)
     if (fe == 2 && d->n_interior_faces > 0) {
       std::vector<double> tf;
       tf.reserve((size_t)96 * fi.tnfrag * 32);
@@ -964,7 +1124,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       TMF_CUDA(tmf::launch_face_geometry(bnd != 0, P->face_geo_args(bnd != 0), P->n_sm, 0));
     }
     P->info.n_face_batches = (int32_t)(P->n_if_batches + P->n_bf_batches);
-    P->info.face_engine = P->face_tfrags ? 2 : 1;
+    P->info.face_engine = P->face_tfrags ? 2 : P->face_engine;
     P->info.flops_issued += (double)P->nc * (P->n_if_batches * (P->face_tfrags ? fi.tdmma_per_batch : fi.dmma_per_batch) +
                                              P->n_bf_batches * fi.dmma_per_batch / 2) * 512.0;
   }
@@ -987,13 +1147,24 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
            (double)nbf_dir * (16.0 * nqf * nd + 13.0 * nqf);
     }
     P->info.flops_alg = f * P->nc;
-    // the same apply's useful flops in the algorithm the cell engine runs: the reference
-    // tensor form replaces the cell term's 12 n_q N + 33 n_q by 12 N^2 + 12 N (+ 4 N^2 + 2 N mass)
+    // the same apply's useful flops in the algorithms the engines run: the reference tensor
+    // form replaces the cell term's 12 n_q N + 33 n_q by 12 N^2 + 12 N (+ 2 N^2 + 2 N mass)
     double fe = f;
     if (P->info.cell_engine == 3) {
       fe -= nce * (12.0 * nq * nd + 33.0 * nq);
       fe += nce * (12.0 * nd * nd + 12.0 * nd);
       if (P->mass) fe += nce * (2.0 * nd * nd + 2.0 * nd) - nce * (4.0 * nq * nd + 5.0 * nq + nd);
+    } else if (P->info.cell_engine == 4) {
+      // the point loop on M unit-weight modes: 12 M N (both GEMMs) + 18 M (G action)
+      const double M = P->Qk;
+      fe -= nce * (12.0 * nq * nd + 33.0 * nq);
+      fe += nce * (12.0 * M * nd + 18.0 * M);
+    }
+    if (faces && P->face_engine == 3) {
+      // modal face tables: the point loop on NF unit-weight modes instead of n_qf points
+      const double NFm = P->QFk;
+      fe -= (double)d->n_interior_faces * (32.0 * nqf * nd + 26.0 * nqf) + (double)nbf_dir * (16.0 * nqf * nd + 13.0 * nqf);
+      fe += (double)d->n_interior_faces * (32.0 * NFm * nd + 26.0 * NFm) + (double)nbf_dir * (16.0 * NFm * nd + 13.0 * NFm);
     }
     if (faces && P->face_tfrags) {
       // tensor face form: the nonzero blocks (F x F: s tau full, each m~ coefficient 3/4 of
@@ -1232,7 +1403,7 @@ int tmf_pcg(tmf_plan* P, const double* b, double* x, int iters, double* res_norm
   const int grid = P->n_sm * 4, blk = 512;
   // fused iteration when the element energies are available (tensor cell engine, plain
   // single-GPU plan): apply(+p.Ap) -> residual -> step (x, p, q = 0)
-  const bool fused = P->info.cell_engine == 3 && !P->local && !P->peer.u && !P->dg;
+  const bool fused = (P->info.cell_engine == 3 || P->info.cell_engine == 4) && !P->local && !P->peer.u && !P->dg;
   if (fused) {
     tmf::pcg_init_fused_kernel<<<grid, blk, 0, st>>>(b, dg, x, r, z, p, q, n, rz, rr);
     TMF_CUDA(cudaGetLastError());

@@ -189,6 +189,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   };
   load_indices(st);
   double pav[MT][S::KK], pG[MT][6], pmdet[MT];
+  // sum over the lane's points of g . (G g) = u_e^T A_e u_e when the point weights are 1:
+  // compiled for the modal tables only (fewer "points" than DoFs), CG; CellArgs::energy
+  constexpr bool EN = !DG && Q < N;
+  double en = 0.0;
   if (PF) {
     load_data(st, pav, pG, pmdet);
     load_indices(st + step);
@@ -256,6 +260,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
           d[m][o + 1][i] = G[m][1] * g0 + G[m][3] * g1 + G[m][4] * g2;
           d[m][o + 2][i] = G[m][2] * g0 + G[m][4] * g1 + G[m][5] * g2;
           if (MASS) d[m][0][i] = mdet[m] * v[m][0][i];
+          if (EN) en = fma(g0, d[m][o][i], fma(g1, d[m][o + 1][i], fma(g2, d[m][o + 2][i], en)));
         }
 #pragma unroll
       for (int c = 0; c < S::NC; ++c)
@@ -292,6 +297,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
         d[m][o + 1] = G[m][1] * g0 + G[m][3] * g1 + G[m][4] * g2;
         d[m][o + 2] = G[m][2] * g0 + G[m][4] * g1 + G[m][5] * g2;
         if (MASS) d[m][0] = mdet[m] * c[0];
+        // lane q4 owns group point 8T + q4 (all its components), so each point counts once
+        if (EN) en = fma(g0, d[m][o], fma(g1, d[m][o + 1], fma(g2, d[m][o + 2], en)));
       }
 #pragma unroll
       for (int c = 0; c < S::NC; ++c)
@@ -363,6 +370,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
           }
         }
     }
+  }
+  if (EN && a.energy != nullptr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) en += __shfl_xor_sync(0xffffffffu, en, o);
+    if (lane == 0) atomicAdd(a.energy, en);
   }
   // peer REDs must be visible system-wide before the caller's cross-rank barrier
   if (PEER && a.peer.y != nullptr) __threadfence_system();

@@ -256,7 +256,10 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   //   DG P2 512: -26 %, Helmholtz P2 512: -17 %;  CG P2 keeps 2 tiles per warp at 256.
   //   (the skewed GEMM1/D-action pipeline, variant 14, helped CG P3 by 2.7 % before
   //   the remainder-point group; with it the plain loop is 5 % faster)
+  //   modal tables (Q = M < N, tools/gpu_modal1.sh): P4 512 threads 0.268 ms (640: 0.306),
+  //   P3 768 0.1075 ms, P2 256 x 2 tiles 0.0516 ms
   if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
+  if (N == 35 && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
   if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
   if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
   return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1>(a, n_sm, st, info);

@@ -103,6 +103,10 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   // changes: -7 % / -8 % at P3 / P2); low degrees have short batches, so occupancy
   // beats prefetch depth (P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the fully
   // prefetching 2-CTA kernel
+  //   modal tables (QF = NF < n_qf, tools/gpu_modal2.sh): P2 prefers round-robin chunks
+  //   with record prefetch at 3 CTAs/SM (Helmholtz 96^3 1.55 ms vs 1.90 blocked), P3 / P4
+  //   the default below (DG 64^3 P3 0.94 ms, 48^3 P4 1.04 ms)
+  if (N == 10 && QF < 10) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
   if (N <= 10) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
   return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
 }
@@ -121,7 +125,9 @@ cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, i
   TMF_FACE(10, 10)
   TMF_FACE(20, 12)
   TMF_FACE(20, 20)
+  TMF_FACE(20, 10)   // modal face tables (NF = dim P_p on the face)
   TMF_FACE(35, 35)
+  TMF_FACE(35, 15)
 #undef TMF_FACE
   *supported = false;
   return cudaSuccess;

@@ -17,6 +17,14 @@ cudaError_t cell_dispatch_10_15(bool mass, bool dg, const CellArgs& a, int n_sm,
                               CellLaunchInfo* info, int variant, int engine);
 cudaError_t cell_dispatch_20_35(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
                               CellLaunchInfo* info, int variant, int engine);
+cudaError_t cell_dispatch_4_1(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
+                              CellLaunchInfo* info, int variant, int engine);
+cudaError_t cell_dispatch_10_4(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
+                              CellLaunchInfo* info, int variant, int engine);
+cudaError_t cell_dispatch_20_10(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
+                              CellLaunchInfo* info, int variant, int engine);
+cudaError_t cell_dispatch_35_20(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
+                              CellLaunchInfo* info, int variant, int engine);
 cudaError_t cell_dispatch_35_70(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
                               CellLaunchInfo* info, int variant, int engine);
 
@@ -32,6 +40,10 @@ cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& 
   TMF_CELL(10, 15)
   TMF_CELL(20, 35)
   TMF_CELL(35, 70)
+  TMF_CELL(4, 1)
+  TMF_CELL(10, 4)
+  TMF_CELL(20, 10)
+  TMF_CELL(35, 20)
 #undef TMF_CELL
   *supported = false;
   return cudaSuccess;

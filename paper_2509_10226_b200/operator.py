@@ -35,9 +35,9 @@ __all__ = ["OperatorConfig", "SipgConfig", "HelmholtzCoefficients", "CgPoissonOp
            "baseline_sipg_tau", "apply_cg_poisson", "apply_dg_sipg", "apply_helmholtz"]
 
 _STAGES = ("ref", "data", "mm", "sched")
-_ENGINES = {"auto": 0, "dmma": 1, "dfma": 2, "tensor": 3}
+_ENGINES = {"auto": 0, "dmma": 1, "dfma": 2, "tensor": 3, "modal": 4}
 _PATCHES = {"auto": 0, "off": 1, "on": 2}
-_FACE_ENGINES = {"auto": 0, "quadrature": 1, "tensor": 2}
+_FACE_ENGINES = {"auto": 0, "quadrature": 1, "tensor": 2, "modal": 3}
 
 
 @dataclass(frozen=True)
@@ -58,9 +58,10 @@ class OperatorConfig:
     face_variant: int = 0       # B200 face-kernel tuning variant (0 = default)
     face_chunk: int = 0         # 8-face batches per CTA chunk, multiple of 8 up to 120 (0 = default 32)
     concurrent_dg: bool = False  # DG: run the cell and face kernels concurrently (accumulating)
-    cell_engine: str = "auto"    # B200 cell kernel: auto | dmma (quadrature points) | dfma | tensor (affine reference tensor)
+    cell_engine: str = "auto"    # B200 cell kernel: auto | dmma (quadrature points) | dfma | tensor (affine
+    #                              reference tensor) | modal (points loop on the M = dim P_{p-1} exact modes)
     cell_patches: str = "auto"   # B200 CG warp-patch assembly: auto (= off, measured slower) | off | on
-    face_engine: str = "auto"    # B200 interior faces: auto (tensor at P2/P3) | quadrature (points) | tensor
+    face_engine: str = "auto"    # B200 faces: auto (modal at P2-P4) | quadrature (points) | tensor (interior) | modal
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -195,7 +196,8 @@ class _B200Operator:
             ((int(getattr(self.config, "face_variant", 0)) & 0xF) << 4) | \
             ((int(getattr(self.config, "face_chunk", 0)) // 8 & 0xF) << 8) | \
             ((1 if getattr(self.config, "concurrent_dg", False) else 0) << 12) | \
-            (_ENGINES[getattr(self.config, "cell_engine", "auto")] << 13) | \
+            ((_ENGINES[getattr(self.config, "cell_engine", "auto")] & 3) << 13) | \
+            ((_ENGINES[getattr(self.config, "cell_engine", "auto")] >> 2) << 19) | \
             (_PATCHES[getattr(self.config, "cell_patches", "auto")] << 15) | \
             (_FACE_ENGINES[getattr(self.config, "face_engine", "auto")] << 17)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))

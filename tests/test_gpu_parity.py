@@ -41,36 +41,42 @@ def test_gpu_both_cell_engines_match_golden(name, engine):
     assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
 
 
-@pytest.mark.parametrize("engine", ["dmma", "tensor"])
+ENGINE_CODE = {"dmma": 1, "tensor": 3, "modal": 4}
+
+
+@pytest.mark.parametrize("engine", ["dmma", "tensor", "modal"])
 @pytest.mark.parametrize("name", golden_names())
-def test_gpu_quadrature_and_tensor_engines_match_golden(name, engine):
-    """The quadrature-point DMMA engine (the reference's point loop) and the reference-
-    tensor engine (the point sum precontracted per plan) against every golden, P4 included."""
+def test_gpu_cell_engines_match_golden(name, engine):
+    """Every cell engine against every golden, P4 included: the quadrature-point loop (the
+    reference's algorithm), the reference tensor (point sum precontracted per plan) and
+    the modal tables (the point loop on M = dim P_{p-1} exact unit-weight modes; Laplace
+    cell terms only -- Helmholtz plans refuse it)."""
     g = load_golden(name)
+    if engine == "modal" and str(g["kind"]).startswith("helm"):
+        with pytest.raises(ValueError, match="modal"):
+            operator_from_fixture(g, cell_engine=engine)
+        return
     A = operator_from_fixture(g, cell_engine=engine)
-    assert A.info["cell_engine"] == (3 if engine == "tensor" else 1)
+    assert A.info["cell_engine"] == ENGINE_CODE[engine]
     err = rel_l2(A.apply(g["u"]), g["y"])
     assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
 
 
-@pytest.mark.parametrize("engine", ["quadrature", "tensor"])
-@pytest.mark.parametrize("name", [n for n in golden_names() if n.startswith(("dg", "helm"))])
-def test_gpu_face_engines_match_golden(name, engine):
-    """Interior faces: the point loop (face_kernel.cuh) and the reference-tensor form
-    (face_tensor_kernel.cuh, per-signature precontracted tables) against every DG golden."""
-    g = load_golden(name)
-    A = operator_from_fixture(g, face_engine=engine)
-    if A.info["n_face_batches"]:
-        assert A.info["face_engine"] == (2 if engine == "tensor" else 1)
-    err = rel_l2(A.apply(g["u"]), g["y"])
-    assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
+def test_gpu_default_engines():
+    """auto: modal tables for Laplace cell terms at P2-P4, the reference tensor at P1 and
+    for Helmholtz; modal faces at P2-P4, the point loop at P1."""
+    for name, cell, face in [("cg_p1_n3_gm_dir2", 3, 0), ("cg_p2_n8_gm", 4, 0), ("cg_p4_n3_gm", 4, 0),
+                             ("dg_p1_n3_gm_dir", 3, 1), ("dg_p3_n3_gm_dir", 4, 3), ("helmk_p2_n3_gm_dir", 3, 3)]:
+        A = operator_from_fixture(load_golden(name))
+        assert A.info["cell_engine"] == cell, name
+        assert A.info["face_engine"] == face, name
 
 
-@pytest.mark.parametrize("variant", range(1, 7))
-@pytest.mark.parametrize("name", ["dg_p2_n3_gm_dir", "dg_p3_n3_gm_dir", "helmk_p2_n3_gm_dir", "helm3_p2_n2_gm_none"])
-def test_gpu_face_tensor_variants_match_golden(name, variant):
+@pytest.mark.parametrize("variant", [2, 8, 10, 11, 14, 15])
+@pytest.mark.parametrize("name", ["cg_p2_n8_gm", "cg3_p2_n3_ref_dir", "cg_p3_n3_gm_dir2", "cg_p4_n3_gm_dir", "dg_p3_n3_gm_dir"])
+def test_gpu_modal_variants_match_golden(name, variant):
     g = load_golden(name)
-    A = operator_from_fixture(g, face_engine="tensor", face_variant=variant)
+    A = operator_from_fixture(g, cell_engine="modal", kernel_variant=variant)
     err = rel_l2(A.apply(g["u"]), g["y"])
     assert err <= TOL, f"{name}/v{variant}: rel L2 {err:.3e}"
 

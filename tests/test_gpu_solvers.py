@@ -135,9 +135,10 @@ def test_distributed_operator_single_rank_on_gpu():
             dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("engine", ["modal", "tensor"])
 @pytest.mark.parametrize("p", [2, 3])
-def test_fused_pcg_matches_unfused(p):
-    """tmf_pcg's fused iteration (tensor cell engine: p.Ap from the element energies plus
+def test_fused_pcg_matches_unfused(p, engine):
+    """tmf_pcg's fused iteration (tensor / modal cell engines: p.Ap from the element energies plus
     the identity rows, x update and zeroing of A p folded into the direction update) against
     the unfused loop (quadrature-point engine: memset / dot / update / direction), with b
     nonzero on the constrained rows too so the identity-row energy term matters."""
@@ -146,8 +147,9 @@ def test_fused_pcg_matches_unfused(p):
     from paper_2509_10226_b200 import operator as op
     from paper_2509_10226_b200.solvers import jacobi_pcg
 
-    m, dm, geo, bas, A = _cg(5, p, (0, 3))
-    assert A.info["cell_engine"] == 3
+    m, dm, geo, bas, _ = _cg(5, p, (0, 3))
+    A = op.CgPoissonOperator(m, dm, geo, bas, op.OperatorConfig(cell_engine=engine))
+    assert A.info["cell_engine"] == {"modal": 4, "tensor": 3}[engine]
     B = op.CgPoissonOperator(m, dm, geo, bas, op.OperatorConfig(cell_engine="dmma"))
     b = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, dm.n_global_dofs)).cuda()
     x1, h1 = jacobi_pcg(A, b, 30)
