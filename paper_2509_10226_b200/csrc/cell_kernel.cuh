@@ -119,11 +119,16 @@ struct CellShape {
 // SKEW: issue GEMM1 of the next point tile before the D action of the current one
 // PEER: ghost DoFs through peer memory (multi-GPU, CellArgs::peer); a separate
 // instantiation so the single-GPU kernel carries no ghost test (it costs 10-20 %)
+// AS: asynchronous gather pipeline with AS stages -- each warp cp.async's the gathered u
+// (8-byte copies, zero-filled for masked DoFs) and the 64-byte geometry records of the
+// super-tile AS-1 ahead into its own shared-memory ring, so AS-1 tiles' loads are in
+// flight without holding registers (the register-prefetch PF variant spills)
 template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT_ = 0, int MINB = 1, bool PF = false,
-          bool BLK = false, bool SKEW = false, bool PEER = false>
+          bool BLK = false, bool SKEW = false, bool PEER = false, int AS = 0>
 __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   using S = CellShape<N, Q, MASS>;
   constexpr int MT = MT_ ? MT_ : S::MT;
+  static_assert(AS == 0 || (!PF && !PEER), "the async ring replaces PF; no peer gathers");
   extern __shared__ __align__(16) double smem[];
   {
     const double2* src = reinterpret_cast<const double2*>(a.frags);
@@ -187,7 +192,41 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
       mdet[m] = MASS ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
     }
   };
+  // async ring: per stage MT x (KK x 32 gathered u, then 8 cells x 8 geometry doubles)
+  constexpr int STAGE = MT * (S::KK * 32 + 64);
+  double* ring = smem + S::NFRAG * 32 + (threadIdx.x >> 5) * (AS > 0 ? AS : 1) * STAGE;
+  auto issue = [&](int64_t t, int slot) {
+    double* r = ring + slot * STAGE;
+    const int cmp = a.nc == 1 ? 0 : (int)(t / cst);
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const int64_t c = ((t - (int64_t)cmp * cst) * MT + m) * 8 + cs;
+      const bool ok = t < nst && c < a.n_cells;
+#pragma unroll
+      for (int kk = 0; kk < S::KK; ++kk) {
+        const int g = nidx[m][kk];
+        const double* src = g >= 0 ? a.u + (int64_t)g * a.nc + cmp : a.u;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(r + (m * S::KK + kk) * 32 + lane)),
+                     "l"(src), "r"(g >= 0 ? 8 : 0) : "memory");
+      }
+      // lane copies 16-byte piece q4 of its cell's 64-byte geometry record
+      const double* gsrc = a.cgeo + 8 * (ok ? c : 0) + 2 * q4;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(r + MT * S::KK * 32 + m * 64 + cs * 8 + 2 * q4)),
+                   "l"(gsrc), "r"(ok ? 16 : 0) : "memory");
+    }
+  };
   load_indices(st);
+  int slot = 0;
+  if (AS > 0) {
+#pragma unroll
+    for (int s = 0; s < AS - 1; ++s) {
+      issue(st + s * step, s);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      load_indices(st + (s + 1) * step);
+    }
+  }
   double pav[MT][S::KK], pG[MT][6], pmdet[MT];
   // sum over the lane's points of g . (G g) = u_e^T A_e u_e when the point weights are 1:
   // compiled for the modal tables only (fewer "points" than DoFs), CG; CellArgs::energy
@@ -210,7 +249,27 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
       cell[m] = ((st - (int64_t)comp * cst) * MT + m) * 8 + cs;
       valid[m] = cell[m] < a.n_cells;
     }
-    if (PF) {
+    if (AS > 0) {
+      // refill the slot of tile st + (AS-1) step (the slot the previous tile was read
+      // from: every lane has its values in registers), then wait for this tile's group
+      __syncwarp();
+      issue(st + (AS - 1) * step, (slot + AS - 1) % AS);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      load_indices(st + AS * step);
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(AS > 0 ? AS - 1 : 0) : "memory");
+      __syncwarp();
+      const double* r = ring + slot * STAGE;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+#pragma unroll
+        for (int kk = 0; kk < S::KK; ++kk) av[m][kk] = r[(m * S::KK + kk) * 32 + lane];
+        const double* gg = r + MT * S::KK * 32 + m * 64 + cs * 8;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) G[m][i] = gg[i];
+        mdet[m] = MASS ? gg[6] : 0.0;
+      }
+      slot = slot + 1 == AS ? 0 : slot + 1;
+    } else if (PF) {
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
 #pragma unroll

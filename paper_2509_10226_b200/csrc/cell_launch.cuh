@@ -15,14 +15,17 @@
 namespace tmf {
 
 template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PF = false, bool BLK = false,
-          bool SKEW = false, bool PEER = false>
+          bool SKEW = false, bool PEER = false, int AS = 0>
 static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = CellShape<N, Q, MASS>;
   constexpr int MTE = MT ? MT : S::MT;
-  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK, SKEW, PEER>;
-  if (cudaError_t e = opt_in_smem(kern, S::SMEM); e != cudaSuccess) return e;
+  // tables + the per-warp async rings
+  constexpr int SMEM = S::SMEM + (AS > 0 ? AS * MTE * (S::KK * 32 + 64) * 8 * (BLOCK / 32) : 0);
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, MT, MINB, PF, BLK, SKEW, PEER, AS>;
+  if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   int per_sm = 0;
-  cudaError_t e = blocks_per_sm(kern, BLOCK, S::SMEM, &per_sm);
+  cudaError_t e = blocks_per_sm(kern, BLOCK, SMEM, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t supertiles = ((a.n_cells + 8 * MTE - 1) / (8 * MTE)) * a.nc;
@@ -35,13 +38,13 @@ static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, C
     info->tiles = supertiles * MTE;
     info->block = BLOCK;
     info->grid = (int)blocks;
-    info->smem = S::SMEM;
+    info->smem = SMEM;
     info->frag_doubles = S::NFRAG * 32;
     info->table = 0;
     info->flops_issued = (double)supertiles * MTE * S::DMMA_PER_TILE * 512.0;
     return cudaSuccess;
   }
-  kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
+  kern<<<(unsigned)blocks, BLOCK, SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -217,6 +220,12 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
     if (N == 35) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1, false, false, false, true>(a, n_sm, st, info);
     return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1, false, false, false, true>(a, n_sm, st, info);
   }
+  if constexpr (Q < N) {   // modal tables: asynchronous gather ring (AS stages), default CTA shapes
+    constexpr int DB = N == 20 ? 768 : N == 35 ? 512 : (N == 10 && DG) ? 512 : BLOCK;
+    if (variant == 5) return launch_cell_v<N, Q, MASS, DG, DB, 0, 1, false, false, false, false, 3>(a, n_sm, st, info);
+    if (variant == 6) return launch_cell_v<N, Q, MASS, DG, DB, 0, 1, false, false, false, false, 2>(a, n_sm, st, info);
+    if (variant == 7) return launch_cell_v<N, Q, MASS, DG, DB, 0, 1, false, false, false, false, 4>(a, n_sm, st, info);
+  }
   if (!DG && !MASS) {
     if (variant == 1) return launch_cell_v<N, Q, MASS, DG, BLOCK, 2, 1>(a, n_sm, st, info);
     if (variant == 2) return launch_cell_v<N, Q, MASS, DG, BLOCK, 1, (BLOCK == 256 ? 3 : 1)>(a, n_sm, st, info);
@@ -259,7 +268,9 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   //   modal tables (Q = M < N, tools/gpu_modal1.sh): P4 512 threads 0.268 ms (640: 0.306),
   //   P3 768 0.1075 ms, P2 256 x 2 tiles 0.0516 ms
   if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
-  if (N == 35 && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
+  //   P4 modal with the 2-stage async gather ring (variant 6): 48^3 0.276 -> 0.253 ms
+  //   (unordered), 0.267 -> 0.245 (reordered); P2 / P3 lose 5-8 % with any ring
+  if (N == 35 && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1, false, false, false, false, 2>(a, n_sm, st, info);
   if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
   if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
   return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1>(a, n_sm, st, info);

@@ -72,7 +72,7 @@ def test_gpu_default_engines():
         assert A.info["face_engine"] == face, name
 
 
-@pytest.mark.parametrize("variant", [2, 8, 10, 11, 14, 15])
+@pytest.mark.parametrize("variant", [2, 5, 6, 7, 8, 10, 11, 14, 15])
 @pytest.mark.parametrize("name", ["cg_p2_n8_gm", "cg3_p2_n3_ref_dir", "cg_p3_n3_gm_dir2", "cg_p4_n3_gm_dir", "dg_p3_n3_gm_dir"])
 def test_gpu_modal_variants_match_golden(name, variant):
     g = load_golden(name)
