@@ -270,7 +270,7 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
   if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768, 0, 1>(a, n_sm, st, info);
   //   P4 modal with the 2-stage async gather ring (variant 6): 48^3 0.276 -> 0.253 ms
   //   (unordered), 0.267 -> 0.245 (reordered); P2 / P3 lose 5-8 % with any ring
-  if (N == 35 && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1, false, false, false, false, 2>(a, n_sm, st, info);
+  if constexpr (N == 35 && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1, false, false, false, false, 2>(a, n_sm, st, info);
   if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640, 0, 1>(a, n_sm, st, info);
   if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512, 0, 1>(a, n_sm, st, info);
   return launch_cell_v<N, Q, MASS, DG, BLOCK, 0, 1>(a, n_sm, st, info);
