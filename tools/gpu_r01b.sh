@@ -6,7 +6,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 1 --no-cpu --no-quadrature > gpurun_out/b_ncu_bench.log 2>&1; echo "ncu list rc=$?"
 K='regex:cell_tensor'
 cap() {  # name spec
-  timeout 600 ncu --set full --clock-control none --import-source on -k "$K" -s 3 -c 1 -o /tmp/$1 python tools/quick_bench.py $2 > gpurun_out/ncu_$1.log 2>&1
+  timeout 600 ncu -f --set full --clock-control none --import-source on -k "$K" -s 3 -c 1 -o /tmp/$1 python tools/quick_bench.py $2 > gpurun_out/ncu_$1.log 2>&1
   ncu -i /tmp/$1.ncu-rep --page raw --csv > gpurun_out/ncu_$1_raw.csv 2>/dev/null
   ncu -i /tmp/$1.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_$1_sass.csv 2>/dev/null
   rm -f /tmp/$1.ncu-rep
