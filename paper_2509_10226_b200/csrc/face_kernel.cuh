@@ -439,3 +439,220 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
 }
 
 }  // namespace tmf
+
+namespace tmf {
+
+// Interior faces with an asynchronous gather ring (the face-kernel analogue of the cell
+// kernel's AS pipeline).  Each warp walks its batches of the CTA's chunks as one flat
+// sequence; the gathered u of both sides and the 64-byte geometry records of the batch
+// AS-1 ahead -- which may lie in a later chunk: its gather order comes from the chunk's
+// signature, all four orders sit in shared memory -- are cp.async'ed into a per-warp ring,
+// and the cell ids of the batch after that are loaded into registers, so AS-1 batches'
+// gathers are in flight while the DMMAs of the current one run.  The chunk loop (table
+// restaging and its barriers) is unchanged; round-robin or blocked chunk runs.
+template <int N, int QF, int AS, int MINB = 2, int BLOCK = 256, bool BLOCKED = false>
+__global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
+  using S = FaceShape<N, QF>;
+  constexpr int SLOT = 2 * S::KK * 32 + 64 + 16;   // am, ap, geometry (8 x 8), cell ids (8 x 2 ints)
+  extern __shared__ __align__(16) double smem[];
+  double* tabs = smem;                                        // two staged tables
+  int* sperm = reinterpret_cast<int*>(smem + 2 * S::NFRAG * 32);   // (4, N) gather orders
+  constexpr int NW = BLOCK / 32;
+  double* ring = smem + 2 * S::NFRAG * 32 + (4 * N + 1) / 2 + (threadIdx.x >> 5) * AS * SLOT;
+  for (int i = threadIdx.x; i < 4 * N; i += BLOCK) sperm[i] = __ldg(a.perm + i);
+  __syncthreads();   // the prologue's gathers read sperm
+  const int lane = threadIdx.x & 31;
+  const int fs = lane >> 2;
+  const int q4 = lane & 3;
+  const int warp = threadIdx.x >> 5;
+
+  const int64_t nwork = a.n_chunks * a.nc;
+  const int64_t per = (nwork + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = BLOCKED ? blockIdx.x * per : blockIdx.x;
+  const int64_t w1 = BLOCKED ? (w0 + per < nwork ? w0 + per : nwork) : nwork;
+  const int64_t wstep = BLOCKED ? 1 : gridDim.x;
+  auto chunk_at = [&](int64_t w) {
+    const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
+    return __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
+  };
+  // flat per-warp item sequence (chunk w, batch bi); w >= w1 = past the end
+  struct Item {
+    int64_t w;
+    int bi;
+    int4 ch;
+  };
+  auto first_from = [&](int64_t w) {
+    Item it{w, warp, make_int4(0, 0, 0, 0)};
+    for (; it.w < w1; it.w += wstep) {
+      it.ch = chunk_at(it.w);
+      if (warp < it.ch.w) break;
+    }
+    return it;
+  };
+  auto advance = [&](Item it) {
+    if (it.w >= w1) return it;
+    if (it.bi + NW < it.ch.w) {
+      it.bi += NW;
+      return it;
+    }
+    return first_from(it.w + wstep);
+  };
+  Item iss = first_from(w0);    // next item to issue
+  Item rec = iss;               // item whose cell ids are in (rcm, rcp)
+  int rcm = -1, rcp = -1;
+  auto load_rec = [&]() {
+    rcm = rcp = -1;
+    if (rec.w < w1) {
+      const int64_t slot = ((int64_t)rec.ch.z + rec.bi) * 8 + fs;
+      rcm = __ldg(a.cm + slot);
+      rcp = __ldg(a.cp + slot);
+    }
+  };
+  int islot = 0;
+  auto issue = [&]() {   // gathers of item iss (cell ids rcm / rcp) into ring slot islot
+    double* r = ring + islot * SLOT;
+    if (iss.w < w1) {
+      const int comp = a.nc == 1 ? 0 : (int)(iss.w / a.n_chunks);
+      const int* pm = sperm + (iss.ch.x / 6) * N;
+      const int* pp = sperm + (iss.ch.y / 6) * N;
+#pragma unroll
+      for (int kk = 0; kk < S::KK; ++kk) {
+        const int j = 4 * kk + q4;
+        const bool ok = rcm >= 0 && j < N;
+        const double* sm = ok ? a.u + ((int64_t)rcm * N + pm[j]) * a.nc + comp : a.u;
+        const double* sp = ok ? a.u + ((int64_t)rcp * N + pp[j]) * a.nc + comp : a.u;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(r + kk * 32 + lane)), "l"(sm), "r"(ok ? 8 : 0) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(r + (S::KK + kk) * 32 + lane)), "l"(sp), "r"(ok ? 8 : 0)
+                     : "memory");
+      }
+      const int64_t gslot = ((int64_t)iss.ch.z + iss.bi) * 8 + fs;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(r + 2 * S::KK * 32 + fs * 8 + 2 * q4)),
+                   "l"(a.geo + gslot * 8 + 2 * q4) : "memory");
+      if (q4 == 0) {
+        int* ids = reinterpret_cast<int*>(r + 2 * S::KK * 32 + 64);
+        ids[2 * fs] = rcm;
+        ids[2 * fs + 1] = rcp;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    islot = islot + 1 == AS ? 0 : islot + 1;
+  };
+  // prologue: AS-1 items in flight, the record of the next one in registers
+  load_rec();
+#pragma unroll
+  for (int s = 0; s < AS - 1; ++s) {
+    issue();
+    iss = advance(iss);
+    rec = iss;
+    load_rec();
+  }
+  int cslot = 0;
+  int cur_x = -1, cur_y = -2;
+  for (int64_t w = w0; w < w1; w += wstep) {
+    const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
+    const int4 ch = chunk_at(w);
+    if (ch.x != cur_x || ch.y != cur_y) {
+      __syncthreads();   // previous chunk's warps are done with the tables (and sperm is set)
+      const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.x * S::NFRAG * 32);
+      const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.y * S::NFRAG * 32);
+      double2* d = reinterpret_cast<double2*>(tabs);
+      for (int i = threadIdx.x; i < S::NFRAG * 16; i += BLOCK) {
+        d[i] = __ldg(s0 + i);
+        d[S::NFRAG * 16 + i] = __ldg(s1 + i);
+      }
+      __syncthreads();
+      cur_x = ch.x;
+      cur_y = ch.y;
+    }
+    const double* Fm = tabs;
+    const double* Fp = tabs + S::NFRAG * 32;
+    const int* perm_m = sperm + (ch.x / 6) * N;
+    const int* perm_p = sperm + (ch.y / 6) * N;
+    for (int bi = warp; bi < ch.w; bi += NW) {
+      // keep AS-1 items in flight: issue the next one, fetch the record after it
+      __syncwarp();   // every lane is done reading the slot the issue refills
+      issue();
+      iss = advance(iss);
+      rec = iss;
+      load_rec();
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(AS - 1) : "memory");
+      __syncwarp();
+      const double* r = ring + cslot * SLOT;
+      cslot = cslot + 1 == AS ? 0 : cslot + 1;
+      double am[S::KK], ap[S::KK];
+#pragma unroll
+      for (int kk = 0; kk < S::KK; ++kk) {
+        am[kk] = r[kk * 32 + lane];
+        ap[kk] = r[(S::KK + kk) * 32 + lane];
+      }
+      const double* ng = r + 2 * S::KK * 32 + fs * 8;
+      const double hm[3] = {ng[0], ng[1], ng[2]};
+      const double hp[3] = {ng[3], ng[4], ng[5]};
+      const double stau = ng[6];
+      const int* ids = reinterpret_cast<const int*>(r + 2 * S::KK * 32 + 64);
+      const int c_m = ids[2 * fs], c_p = ids[2 * fs + 1];
+
+      double ym[S::NJ][2], yp[S::NJ][2];
+#pragma unroll
+      for (int nj = 0; nj < S::NJ; ++nj) ym[nj][0] = ym[nj][1] = yp[nj][0] = yp[nj][1] = 0.0;
+#pragma unroll
+      for (int g = 0; g < S::G; ++g) {
+        double vm[2][2], vp[2][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) vm[h][0] = vm[h][1] = vp[h][0] = vp[h][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < S::KK; ++kk)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 0 && kk >= S::KKF) continue;
+            const int f = S::b1(g, h, kk) * 32 + lane;
+            dmma(vm[h], am[kk], Fm[f]);
+            dmma(vp[h], ap[kk], Fp[f]);
+          }
+        const double nj = vp[0][0] - vm[0][0];
+        double qv = -stau * nj;
+        qv = fma(-hm[0], vm[0][1], qv);
+        qv = fma(-hm[1], vm[1][0], qv);
+        qv = fma(-hm[2], vm[1][1], qv);
+        qv = fma(-hp[0], vp[0][1], qv);
+        qv = fma(-hp[1], vp[1][0], qv);
+        qv = fma(-hp[2], vp[1][1], qv);
+        double qm[4], qp[4];
+        qm[0] = qv;
+        qp[0] = -qv;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          qm[1 + k] = nj * hm[k];
+          qp[1 + k] = nj * hp[k];
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int nj2 = 0; nj2 < S::NJ; ++nj2) {
+            if (c < 3 && nj2 >= S::NJF) continue;
+            const int f = S::b2(g, c, nj2) * 32 + lane;
+            dmma(ym[nj2], qm[c], Fm[f]);
+            dmma(yp[nj2], qp[c], Fp[f]);
+          }
+      }
+      if (c_m >= 0) {
+#pragma unroll
+        for (int nj = 0; nj < S::NJ; ++nj)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int j = 8 * nj + 2 * q4 + i;
+            if (j < N) {
+              atomicAdd(a.y + ((int64_t)c_m * N + perm_m[j]) * a.nc + comp, ym[nj][i]);
+              atomicAdd(a.y + ((int64_t)c_p * N + perm_p[j]) * a.nc + comp, yp[nj][i]);
+            }
+          }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+}  // namespace tmf

@@ -68,6 +68,29 @@ static cudaError_t launch_face_xt(const FaceArgs& a, int n_sm, cudaStream_t st, 
   return launch_face_x<N, 256, 2, true>(a, n_sm, st);
 }
 
+// interior faces with the asynchronous gather ring (face_async_kernel)
+template <int N, int QF, int AS, int MINB, int BLOCK = 256, bool BLOCKED = false>
+static cudaError_t launch_face_a(const FaceArgs& a, int n_sm, cudaStream_t st) {
+  using S = FaceShape<N, QF>;
+  constexpr int SLOT = 2 * S::KK * 32 + 64 + 16;
+  constexpr int SMEM = (2 * S::NFRAG * 32 + (4 * N + 1) / 2 + (BLOCK / 32) * AS * SLOT) * 8;
+  if constexpr (SMEM > 227 * 1024) {
+    return cudaErrorNotSupported;   // tables + rings do not fit (n_qf-point P4): caller falls back
+  }
+  auto kern = face_async_kernel<N, QF, AS, MINB, BLOCK, BLOCKED>;
+  if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaError_t e = blocks_per_sm(kern, BLOCK, SMEM, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t work = a.n_chunks * a.nc;
+  if (work == 0) return cudaSuccess;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  if (blocks > work) blocks = work;
+  kern<<<(unsigned)blocks, BLOCK, SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
 // variant: 0 = default (by degree, below, blocked chunk runs); 1 = no prefetch, 3 CTAs/SM;
 // 2 = record prefetch, 3 CTAs/SM; 3 = record prefetch, 2 CTAs/SM; 4 = full prefetch, 2 CTAs/SM
 template <int N, int QF, bool BND>
@@ -88,8 +111,8 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   if (variant == 4) return launch_face_v<N, QF, BND, 2, 2>(a, n_sm, st, info);
   if (variant == 5) return launch_face_v<N, QF, BND, 1, 1, 512>(a, n_sm, st, info);
   if (variant == 6) return launch_face_v<N, QF, BND, 2, 1, 512>(a, n_sm, st, info);
-  if (variant == 7) return launch_face_v<N, QF, BND, 1, 1, 768>(a, n_sm, st, info);
-  if (variant == 8) return launch_face_v<N, QF, BND, 1, 2, 384>(a, n_sm, st, info);
+  if (variant == 7) return launch_face_v<N, QF, BND, 1, 4>(a, n_sm, st, info);          // 64 registers
+  if (variant == 8) return launch_face_v<N, QF, BND, 1, 6, 128>(a, n_sm, st, info);
   if (variant == 9) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
   if (variant == 10) return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
   // round-robin chunks (all CTAs march through the chunk list together, keeping the
@@ -97,8 +120,16 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   // 5-15 % slower than the blocked default at C3 / C4 sizes (barrier per chunk)
   if (variant == 11) return launch_face_v<N, QF, BND, 1, 3, 256, false, true>(a, n_sm, st, info);
   if (variant == 12) return launch_face_v<N, QF, BND, 2, 2, 256, false, true>(a, n_sm, st, info);
-  if (variant == 13) return launch_face_v<N, QF, BND, 1, 2, 256, false, true>(a, n_sm, st, info);
-  if (variant == 14) return launch_face_v<N, QF, BND, 2, 1, 512, false, true>(a, n_sm, st, info);
+  if constexpr (!BND) {   // asynchronous gather ring (no peers)
+    if (!info && a.peer.u == nullptr && variant >= 13) {
+      cudaError_t e = cudaErrorNotSupported;
+      if (variant == 13) e = launch_face_a<N, QF, 2, 3>(a, n_sm, st);
+      if (variant == 14) e = launch_face_a<N, QF, 3, 2>(a, n_sm, st);
+      if (variant == 15) e = launch_face_a<N, QF, 3, 2, 256, true>(a, n_sm, st);
+      if (e != cudaErrorNotSupported) return e;
+      variant = 0;   // does not fit in shared memory: the default kernel
+    }
+  }
   // default: contiguous chunk runs per CTA (tables restaged only when the signature
   // changes: -7 % / -8 % at P3 / P2); low degrees have short batches, so occupancy
   // beats prefetch depth (P2 96^3: 2.39 vs 2.48 ms); P >= 3 prefers the fully
@@ -106,6 +137,14 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   //   modal tables (QF = NF < n_qf, tools/gpu_modal2.sh): P2 prefers round-robin chunks
   //   with record prefetch at 3 CTAs/SM (Helmholtz 96^3 1.55 ms vs 1.90 blocked), P3 / P4
   //   the default below (DG 64^3 P3 0.94 ms, 48^3 P4 1.04 ms)
+  //   P4 interior faces (modal) with the 3-stage asynchronous gather ring, blocked chunk runs
+  //   (variant 15): DG 48^3 1.05 -> 0.85 ms; P2 / P3 gain nothing from the ring (-2 % / +7 %)
+  if constexpr (!BND && N == 35) {
+    if (!info && a.peer.u == nullptr && QF < N) {
+      cudaError_t e = launch_face_a<N, QF, 3, 2, 256, true>(a, n_sm, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
   if (N == 10 && QF < 10) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
   if (N <= 10) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
   return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
