@@ -213,6 +213,38 @@ int tmf_build_faces(int64_t n_cells, const int32_t* cells, int64_t n_vertices,
 int tmf_build_cg_dofs(int64_t n_cells, const int32_t* cells, int64_t n_vertices, int32_t degree,
                       int32_t* cell_dofs, int64_t* n_scalar_dofs);
 
+/* p-multigrid building blocks (the paper's solver layer, PAPER.md:423-436,
+ * SPEC.md:494-565; the reference has no implementation).  A transfer links two CG spaces of
+ * degrees pf > pc on the same mesh: prolongation x_f = P x_c interpolates the coarse
+ * function at the fine nodes (interp[i*n_coarse_dpc + j] = coarse basis j at fine node i,
+ * row-major n_fine_dpc x n_coarse_dpc); restriction r_c = P^T r_f is its exact transpose.
+ * Each fine DoF is written by one owner cell (the first cell containing it).  Dirichlet
+ * masks (uint8 per DoF, or NULL): fine Dirichlet DoFs are set to 0 by an overwriting
+ * prolongation (left alone when add != 0) and never restricted; coarse Dirichlet DoFs are
+ * read as 0 and never written by restriction.  Device vectors, stream-ordered. */
+typedef struct tmf_transfer tmf_transfer;
+typedef struct tmf_transfer_desc {
+  int64_t n_cells;
+  int32_t n_fine_dpc, n_coarse_dpc;          /* 10/20/35 over 4/10/20                  */
+  int64_t n_fine_dofs, n_coarse_dofs;
+  const int32_t* fine_cell_dofs;             /* host (n_cells, n_fine_dpc)              */
+  const int32_t* coarse_cell_dofs;           /* host (n_cells, n_coarse_dpc)            */
+  const uint8_t* fine_dirichlet;             /* host (n_fine_dofs) or NULL              */
+  const uint8_t* coarse_dirichlet;           /* host (n_coarse_dofs) or NULL            */
+  const double* interp;                      /* host (n_fine_dpc, n_coarse_dpc)         */
+  int32_t device;
+} tmf_transfer_desc;
+int tmf_transfer_create(const tmf_transfer_desc* desc, tmf_transfer** out);
+int tmf_transfer_destroy(tmf_transfer* t);
+int tmf_prolongate(tmf_transfer* t, const double* xc, double* xf, int add, void* stream);
+int tmf_restrict(tmf_transfer* t, const double* rf, double* rc, void* stream);
+/* Chebyshev-Jacobi smoother step (fused):  ax == NULL (x = 0 on entry): d = c2 D^-1 b, x = d;
+ * otherwise d = c1 d + c2 D^-1 (b - ax), x += d.   tmf_vec_axpby: out = alpha x + beta y. */
+int tmf_chebyshev_step(int64_t n, const double* ax, const double* b, const double* dinv, double* x,
+                       double* d, double c1, double c2, void* stream);
+int tmf_vec_axpby(int64_t n, double alpha, const double* x, double beta, const double* y, double* out,
+                  void* stream);
+
 const char* tmf_last_error(void);
 const char* tmf_version(void);
 

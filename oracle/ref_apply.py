@@ -279,12 +279,13 @@ def jacobi_pcg(apply, diag, b, iters):
     hist = [float(np.sqrt(r @ r))]
     for _ in range(iters):
         q = apply(p)
-        alpha = rz / float(p @ q)
+        pq = float(p @ q)
+        alpha = rz / pq if pq != 0.0 else 0.0   # exact breakdown (converged): stay put
         x += alpha * p
         r -= alpha * q
         z = r / diag
         rz_new = float(r @ z)
         hist.append(float(np.sqrt(r @ r)))
-        p = z + (rz_new / rz) * p
+        p = z + (rz_new / rz if rz != 0.0 else 0.0) * p
         rz = rz_new
     return x, np.array(hist)

@@ -38,6 +38,15 @@ class PlanDesc(C.Structure):
     ]
 
 
+class TransferDesc(C.Structure):
+    _fields_ = [
+        ("n_cells", C.c_int64), ("n_fine_dpc", C.c_int32), ("n_coarse_dpc", C.c_int32),
+        ("n_fine_dofs", C.c_int64), ("n_coarse_dofs", C.c_int64), ("fine_cell_dofs", _ip),
+        ("coarse_cell_dofs", _ip), ("fine_dirichlet", _bp), ("coarse_dirichlet", _bp),
+        ("interp", _dp), ("device", C.c_int32),
+    ]
+
+
 class PlanInfo(C.Structure):
     _fields_ = [
         ("n_global_dofs", C.c_int64), ("flops_alg", C.c_double), ("bytes_alg", C.c_double),
@@ -87,6 +96,12 @@ def lib():
         L.tmf_ipc_get_handle.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]
         L.tmf_ipc_open_handle.argtypes = [C.POINTER(C.c_uint8), C.c_int32, C.POINTER(C.c_void_p)]
         L.tmf_ipc_close_handle.argtypes = [C.c_void_p]
+        L.tmf_transfer_create.argtypes = [C.POINTER(TransferDesc), C.POINTER(C.c_void_p)]
+        L.tmf_transfer_destroy.argtypes = [_v]
+        L.tmf_prolongate.argtypes = [_v, _v, _v, C.c_int, _v]
+        L.tmf_restrict.argtypes = [_v, _v, _v, _v]
+        L.tmf_chebyshev_step.argtypes = [C.c_int64, _v, _v, _v, _v, _v, C.c_double, C.c_double, _v]
+        L.tmf_vec_axpby.argtypes = [C.c_int64, C.c_double, _v, C.c_double, _v, _v, _v]
         L.tmf_last_error.restype = C.c_char_p
         L.tmf_version.restype = C.c_char_p
         for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
@@ -94,7 +109,8 @@ def lib():
                      "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs",
                      "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction",
                      "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle", "tmf_ipc_open_handle",
-                     "tmf_ipc_close_handle"):
+                     "tmf_ipc_close_handle", "tmf_transfer_create", "tmf_transfer_destroy", "tmf_prolongate",
+                     "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -104,7 +120,9 @@ EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_app
             "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
             "tmf_build_faces", "tmf_build_cg_dofs", "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update",
             "tmf_pcg_direction", "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle",
-            "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_last_error", "tmf_version")
+            "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_transfer_create", "tmf_transfer_destroy",
+            "tmf_prolongate", "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby", "tmf_last_error",
+            "tmf_version")
 
 
 def check(rc: int) -> None:

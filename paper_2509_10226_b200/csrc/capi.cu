@@ -763,6 +763,9 @@ int tmf_apply_stages(tmf_plan* P, const double* u, double* y, int stages, int64_
 }
 
 const char* tmf_last_error(void) { return g_err.c_str(); }
+
+// error reporting for the other C-ABI translation units (multigrid.cu); not in the header
+int tmf_internal_set_error(int code, const char* msg) { return fail(code, msg); }
 const char* tmf_version(void) { return "tetmf_b200 0.1 (sm_100a, fp64 DMMA)"; }
 
 int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {

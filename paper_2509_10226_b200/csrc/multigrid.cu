@@ -1,0 +1,271 @@
+// p-multigrid building blocks (the paper's solver layer PAPER.md:423-436,
+// SPEC.md:494-565; the reference ships none of it): degree-transfer operators between
+// two CG spaces on the same mesh and the fused Chebyshev-Jacobi smoother update.
+//
+// Prolongation P: the coarse (degree pc) function interpolated at the fine (degree pf)
+// nodes, cell by cell: x_f[i] = sum_j P_loc[i, j] x_c[cdofs[j]], P_loc[i, j] =
+// phi^c_j(node^f_i).  A fine DoF shared by several cells is written by exactly ONE of
+// them (its owner = the first cell in cell order that contains it), so prolongation
+// needs no atomics, is deterministic, and restriction R = P^T (the exact transpose of
+// the global interpolation matrix) sums every fine row once:
+//   r_c[cdofs[j]] += sum_{i owned by e} P_loc[i, j] r_f[fdofs[i]]     (fp64 RED)
+// Dirichlet DoFs: fine ones are written as 0 (overwrite) / left alone (add) and never
+// restricted; coarse ones are gathered as 0 and never scattered (their rows are
+// identity rows of the coarse operator and stay zero in the correction).
+// All kernels are memory-bound thread-per-cell loops (a few % of one apply).
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tetmf_b200.h"
+
+extern "C" int tmf_internal_set_error(int code, const char* msg);
+
+namespace {
+
+constexpr int kNotOwned = INT_MIN;
+
+int mg_fail(int code, const std::string& m) { return tmf_internal_set_error(code, m.c_str()); }
+
+#define MG_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return mg_fail(TMF_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+// fdofs: fine DoF id (owned, free), ~id (owned, Dirichlet) or kNotOwned
+// cdofs: coarse DoF id, or ~id for a coarse Dirichlet DoF
+template <int NC>
+__global__ void prolongate_kernel(const int* __restrict__ fdofs, const int* __restrict__ cdofs,
+                                  const double* __restrict__ Pg, int nf, int64_t n_cells,
+                                  const double* __restrict__ xc, double* __restrict__ xf, int add) {
+  extern __shared__ double sP[];
+  for (int i = threadIdx.x; i < nf * NC; i += blockDim.x) sP[i] = Pg[i];
+  __syncthreads();
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double v[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int g = __ldg(cdofs + c * NC + j);
+      v[j] = g >= 0 ? __ldg(xc + g) : 0.0;
+    }
+    for (int i = 0; i < nf; ++i) {
+      const int f = __ldg(fdofs + c * nf + i);
+      if (f == kNotOwned) continue;
+      if (f < 0) {
+        if (!add) xf[~f] = 0.0;
+        continue;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) s = fma(sP[i * NC + j], v[j], s);
+      xf[f] = add ? xf[f] + s : s;
+    }
+  }
+}
+
+template <int NC>
+__global__ void restrict_kernel(const int* __restrict__ fdofs, const int* __restrict__ cdofs,
+                                const double* __restrict__ Pg, int nf, int64_t n_cells,
+                                const double* __restrict__ rf, double* __restrict__ rc) {
+  extern __shared__ double sP[];
+  for (int i = threadIdx.x; i < nf * NC; i += blockDim.x) sP[i] = Pg[i];
+  __syncthreads();
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double acc[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc[j] = 0.0;
+    for (int i = 0; i < nf; ++i) {
+      const int f = __ldg(fdofs + c * nf + i);
+      if (f < 0) continue;   // not owned, or Dirichlet
+      const double r = __ldg(rf + f);
+#pragma unroll
+      for (int j = 0; j < NC; ++j) acc[j] = fma(sP[i * NC + j], r, acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int g = __ldg(cdofs + c * NC + j);
+      if (g >= 0 && acc[j] != 0.0) atomicAdd(rc + g, acc[j]);
+    }
+  }
+}
+
+// first == 1 (x = 0 on entry, ax unused):  d = c2 D^-1 b;  x = d
+// otherwise:                               d = c1 d + c2 D^-1 (b - ax);  x += d
+__global__ void chebyshev_kernel(int64_t n, const double* __restrict__ ax, const double* __restrict__ b,
+                                 const double* __restrict__ dinv, double* __restrict__ x,
+                                 double* __restrict__ d, double c1, double c2, int first) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (first) {
+      const double di = c2 * dinv[i] * b[i];
+      d[i] = di;
+      x[i] = di;
+    } else {
+      const double di = c1 * d[i] + c2 * dinv[i] * (b[i] - ax[i]);
+      d[i] = di;
+      x[i] += di;
+    }
+  }
+}
+
+__global__ void axpby_kernel(int64_t n, double alpha, const double* __restrict__ x, double beta,
+                             const double* __restrict__ y, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = alpha * x[i] + beta * y[i];
+}
+
+int sm_count(int dev) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+}  // namespace
+
+struct tmf_transfer {
+  int device = 0;
+  int sms = 148;
+  int64_t n_cells = 0;
+  int nf = 0, nc = 0;
+  int64_t n_fine = 0, n_coarse = 0;
+  int* fdofs = nullptr;
+  int* cdofs = nullptr;
+  double* P = nullptr;
+};
+
+extern "C" {
+
+int tmf_transfer_create(const tmf_transfer_desc* d, tmf_transfer** out) {
+  if (!d || !out) return mg_fail(TMF_EINVAL, "null descriptor/output");
+  *out = nullptr;
+  if (d->n_cells <= 0) return mg_fail(TMF_EINVAL, "empty mesh");
+  if (!d->fine_cell_dofs || !d->coarse_cell_dofs || !d->interp)
+    return mg_fail(TMF_EINVAL, "missing dof maps / interpolation matrix");
+  if (d->n_coarse_dpc != 4 && d->n_coarse_dpc != 10 && d->n_coarse_dpc != 20)
+    return mg_fail(TMF_EINVAL, "coarse space must be P1, P2 or P3 (4/10/20 DoFs per cell)");
+  if (d->n_fine_dpc <= d->n_coarse_dpc || d->n_fine_dpc > 35)
+    return mg_fail(TMF_EINVAL, "fine space must have more DoFs per cell than the coarse one (<= 35)");
+  if (d->n_fine_dofs <= 0 || d->n_coarse_dofs <= 0 || d->n_fine_dofs >= INT_MAX)
+    return mg_fail(TMF_EINVAL, "bad DoF counts");
+  const int64_t n = d->n_cells;
+  const int nf = d->n_fine_dpc, nc = d->n_coarse_dpc;
+  // owners: first cell (in cell order) that contains the fine DoF
+  std::vector<int> f(n * nf), c(n * nc);
+  std::vector<char> seen(d->n_fine_dofs, 0);
+  for (int64_t e = 0; e < n; ++e)
+    for (int i = 0; i < nf; ++i) {
+      const int g = d->fine_cell_dofs[e * nf + i];
+      if (g < 0 || g >= d->n_fine_dofs) return mg_fail(TMF_EINVAL, "fine DoF index out of range");
+      if (seen[g]) {
+        f[e * nf + i] = kNotOwned;
+        continue;
+      }
+      seen[g] = 1;
+      f[e * nf + i] = (d->fine_dirichlet && d->fine_dirichlet[g]) ? ~g : g;
+    }
+  for (int64_t e = 0; e < n; ++e)
+    for (int j = 0; j < nc; ++j) {
+      const int g = d->coarse_cell_dofs[e * nc + j];
+      if (g < 0 || g >= d->n_coarse_dofs) return mg_fail(TMF_EINVAL, "coarse DoF index out of range");
+      c[e * nc + j] = (d->coarse_dirichlet && d->coarse_dirichlet[g]) ? ~g : g;
+    }
+  for (int64_t g = 0; g < d->n_fine_dofs; ++g)
+    if (!seen[g]) return mg_fail(TMF_EINVAL, "a fine DoF belongs to no cell");
+  MG_CUDA(cudaSetDevice(d->device));
+  auto* t = new tmf_transfer();
+  t->device = d->device;
+  t->sms = sm_count(d->device);
+  t->n_cells = n;
+  t->nf = nf;
+  t->nc = nc;
+  t->n_fine = d->n_fine_dofs;
+  t->n_coarse = d->n_coarse_dofs;
+  cudaError_t e = cudaMalloc(&t->fdofs, f.size() * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&t->cdofs, c.size() * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&t->P, (size_t)nf * nc * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(t->fdofs, f.data(), f.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(t->cdofs, c.data(), c.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(t->P, d->interp, (size_t)nf * nc * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    tmf_transfer_destroy(t);
+    return mg_fail(TMF_ECUDA, std::string("transfer upload: ") + cudaGetErrorString(e));
+  }
+  *out = t;
+  return TMF_OK;
+}
+
+int tmf_transfer_destroy(tmf_transfer* t) {
+  if (!t) return TMF_OK;
+  cudaSetDevice(t->device);
+  cudaFree(t->fdofs);
+  cudaFree(t->cdofs);
+  cudaFree(t->P);
+  delete t;
+  return TMF_OK;
+}
+
+int tmf_prolongate(tmf_transfer* t, const double* xc, double* xf, int add, void* stream) {
+  if (!t || !xc || !xf) return mg_fail(TMF_EINVAL, "null argument");
+  MG_CUDA(cudaSetDevice(t->device));
+  const cudaStream_t st = (cudaStream_t)stream;
+  const int block = 256;
+  int64_t grid = (t->n_cells + block - 1) / block;
+  if (grid > (int64_t)t->sms * 16) grid = (int64_t)t->sms * 16;
+  const size_t smem = (size_t)t->nf * t->nc * sizeof(double);
+  if (t->nc == 4)
+    prolongate_kernel<4><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
+  else if (t->nc == 10)
+    prolongate_kernel<10><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
+  else
+    prolongate_kernel<20><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
+  MG_CUDA(cudaGetLastError());
+  return TMF_OK;
+}
+
+int tmf_restrict(tmf_transfer* t, const double* rf, double* rc, void* stream) {
+  if (!t || !rf || !rc) return mg_fail(TMF_EINVAL, "null argument");
+  MG_CUDA(cudaSetDevice(t->device));
+  const cudaStream_t st = (cudaStream_t)stream;
+  MG_CUDA(cudaMemsetAsync(rc, 0, t->n_coarse * sizeof(double), st));
+  const int block = 256;
+  int64_t grid = (t->n_cells + block - 1) / block;
+  if (grid > (int64_t)t->sms * 16) grid = (int64_t)t->sms * 16;
+  const size_t smem = (size_t)t->nf * t->nc * sizeof(double);
+  if (t->nc == 4)
+    restrict_kernel<4><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
+  else if (t->nc == 10)
+    restrict_kernel<10><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
+  else
+    restrict_kernel<20><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
+  MG_CUDA(cudaGetLastError());
+  return TMF_OK;
+}
+
+int tmf_chebyshev_step(int64_t n, const double* ax, const double* b, const double* dinv, double* x,
+                       double* d, double c1, double c2, void* stream) {
+  if (n < 0 || !b || !dinv || !x || !d) return mg_fail(TMF_EINVAL, "bad argument");
+  int dev = 0;
+  MG_CUDA(cudaGetDevice(&dev));
+  chebyshev_kernel<<<sm_count(dev) * 4, 512, 0, (cudaStream_t)stream>>>(n, ax, b, dinv, x, d, c1, c2,
+                                                                         ax == nullptr ? 1 : 0);
+  MG_CUDA(cudaGetLastError());
+  return TMF_OK;
+}
+
+int tmf_vec_axpby(int64_t n, double alpha, const double* x, double beta, const double* y, double* out,
+                  void* stream) {
+  if (n < 0 || !x || !y || !out) return mg_fail(TMF_EINVAL, "bad argument");
+  int dev = 0;
+  MG_CUDA(cudaGetDevice(&dev));
+  axpby_kernel<<<sm_count(dev) * 4, 512, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y, out);
+  MG_CUDA(cudaGetLastError());
+  return TMF_OK;
+}
+
+}  // extern "C"

@@ -107,7 +107,7 @@ __global__ void pcg_update_kernel(const double* __restrict__ p, const double* __
                                   double* __restrict__ z, int64_t n, const double* rz_k, const double* pq_k,
                                   double* rz_next, double* rr_next) {
   __shared__ double sh[32];
-  const double alpha = *rz_k / *pq_k;
+  const double alpha = *pq_k != 0.0 ? *rz_k / *pq_k : 0.0;   // 0 at exact breakdown
   double s1 = 0.0, s2 = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     x[i] += alpha * p[i];
@@ -130,7 +130,7 @@ __global__ void pcg_update_kernel(const double* __restrict__ p, const double* __
 // p = z + (rz[k+1] / rz[k]) p
 __global__ void pcg_direction_kernel(const double* __restrict__ z, double* __restrict__ p, int64_t n,
                                      const double* rz_k, const double* rz_next) {
-  const double beta = *rz_next / *rz_k;
+  const double beta = *rz_k != 0.0 ? *rz_next / *rz_k : 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
 }
@@ -171,7 +171,7 @@ __global__ void pcg_residual_kernel(const double* __restrict__ q, const double* 
                                     double* __restrict__ r, double* __restrict__ z, int64_t n, const double* rz_k,
                                     const double* pq_k, double* rz_next, double* rr_next) {
   __shared__ double sh[32];
-  const double alpha = *rz_k / *pq_k;
+  const double alpha = *pq_k != 0.0 ? *rz_k / *pq_k : 0.0;   // 0 at exact breakdown
   double s1 = 0.0, s2 = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double ri = r[i] - alpha * q[i];
@@ -194,7 +194,7 @@ __global__ void pcg_residual_kernel(const double* __restrict__ q, const double* 
 __global__ void pcg_step_kernel(const double* __restrict__ z, double* __restrict__ p, double* __restrict__ x,
                                 double* __restrict__ q, int64_t n, const double* rz_k, const double* pq_k,
                                 const double* rz_next) {
-  const double alpha = *rz_k / *pq_k, beta = *rz_next / *rz_k;
+  const double alpha = *pq_k != 0.0 ? *rz_k / *pq_k : 0.0, beta = *rz_k != 0.0 ? *rz_next / *rz_k : 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double pi = p[i];
     x[i] += alpha * pi;

@@ -1,0 +1,292 @@
+"""p-multigrid preconditioned CG on the matrix-free operators.
+
+The paper's solver layer is the main consumer of
+the apply; the reference package specifies it but ships no implementation.  This is
+the fp64 p-multigrid part of it, built on the B200 operator apply:
+
+* levels: CG spaces of decreasing degree on the same mesh (default p, p-1, ..., 1),
+  each a :class:`CgPoissonOperator` with its matrix-free diagonal;
+* transfers: ``tmf_prolongate`` / ``tmf_restrict`` (interpolation of the coarse
+  function at the fine nodes and its exact transpose, csrc/multigrid.cu);
+* smoother: Chebyshev-accelerated point Jacobi of degree ``smoothing_degree`` on
+  [lambda_max / smoothing_range, lambda_max] (Saad, Iterative Methods, Alg. 12.1;
+  fused update ``tmf_chebyshev_step``); lambda_max of D^-1 A from a short Lanczos
+  (Jacobi-PCG coefficients) times 1.1;
+* coarse level (P1): ``coarse_iterations`` native Jacobi-PCG iterations (``tmf_pcg``);
+* outer loop: flexible (Polak-Ribiere) PCG, since a fixed-count inner CG makes the
+  V-cycle slightly nonlinear.
+
+Not built (out of scope this round): fp32 levels (mixed precision), h-coarsening
+below P1, Chebyshev on the coarse level.  No CPU fallback: every vector operation
+is a native kernel or a device tensor op; the CPU restatement is
+``oracle/ref_multigrid.py`` (tests only).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from . import basis as B
+from . import dofmap as D
+from . import quadrature as Q
+from .geometry import GeometryData
+
+__all__ = ["interpolation_matrix", "Transfer", "PMultigrid", "chebyshev_coefficients"]
+
+
+def interpolation_matrix(p_fine: int, p_coarse: int) -> np.ndarray:
+    """(n_fine_dpc, n_coarse_dpc): coarse Lagrange basis at the fine reference nodes;
+    entries below 1e-13 (where a coarse function vanishes at a fine node) are exact 0."""
+    if not 1 <= p_coarse < p_fine <= B.MAX_DEGREE:
+        raise ValueError(f"need 1 <= p_coarse < p_fine <= {B.MAX_DEGREE}")
+    nodes, _ = B.reference_nodes(p_fine)
+    P = B.lagrange_values(p_coarse, nodes)
+    P[np.abs(P) < 1e-13] = 0.0
+    return np.ascontiguousarray(P)
+
+
+def chebyshev_coefficients(lmax: float, smoothing_range: float, degree: int):
+    """[(c1, c2)] per step of the Chebyshev-Jacobi iteration on [lmax/range, lmax]:
+    step k: d = c1 d + c2 D^-1 (b - A x), x += d (step 0: c1 = 0)."""
+    a, b = lmax / smoothing_range, lmax
+    theta, delta = 0.5 * (b + a), 0.5 * (b - a)
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    out = [(0.0, 1.0 / theta)]
+    for _ in range(1, degree):
+        rho_new = 1.0 / (2.0 * sigma - rho)
+        out.append((rho_new * rho, 2.0 * rho_new / delta))
+        rho = rho_new
+    return out
+
+
+def _vp(t):
+    return C.c_void_p(t.data_ptr())
+
+
+class Transfer:
+    """Degree transfer between two CG dof maps on the same mesh (device resident)."""
+
+    def __init__(self, fine_dm, coarse_dm, device: int = 0):
+        if fine_dm.n_cells != coarse_dm.n_cells:
+            raise ValueError("fine and coarse dof maps must live on the same mesh")
+        self.P = interpolation_matrix(fine_dm.degree, coarse_dm.degree)
+        fd = np.ascontiguousarray(fine_dm.cell_dofs, dtype=np.int32)
+        cd = np.ascontiguousarray(coarse_dm.cell_dofs, dtype=np.int32)
+        fm = np.ascontiguousarray(fine_dm.dirichlet_mask, dtype=np.uint8)
+        cm = np.ascontiguousarray(coarse_dm.dirichlet_mask, dtype=np.uint8)
+        d = _lib.TransferDesc()
+        d.n_cells = fine_dm.n_cells
+        d.n_fine_dpc, d.n_coarse_dpc = fd.shape[1], cd.shape[1]
+        d.n_fine_dofs, d.n_coarse_dofs = fine_dm.n_scalar_dofs, coarse_dm.n_scalar_dofs
+        d.fine_cell_dofs = _lib.ptr(fd, C.c_int32)
+        d.coarse_cell_dofs = _lib.ptr(cd, C.c_int32)
+        d.fine_dirichlet = _lib.ptr(fm, C.c_uint8) if fm.any() else _lib.ptr(None, C.c_uint8)
+        d.coarse_dirichlet = _lib.ptr(cm, C.c_uint8) if cm.any() else _lib.ptr(None, C.c_uint8)
+        d.interp = _lib.ptr(self.P, C.c_double)
+        d.device = int(device)
+        self._t = C.c_void_p()
+        _lib.check(_lib.lib().tmf_transfer_create(C.byref(d), C.byref(self._t)))
+        self.n_fine, self.n_coarse = fine_dm.n_scalar_dofs, coarse_dm.n_scalar_dofs
+
+    def prolongate(self, xc, xf, add: bool = False, stream: int = 0):
+        """xf = P xc (add: xf += P xc), device tensors."""
+        _lib.check(_lib.lib().tmf_prolongate(self._t, _vp(xc), _vp(xf), int(bool(add)), C.c_void_p(stream)))
+
+    def restrict(self, rf, rc, stream: int = 0):
+        """rc = P^T rf, device tensors."""
+        _lib.check(_lib.lib().tmf_restrict(self._t, _vp(rf), _vp(rc), C.c_void_p(stream)))
+
+    def close(self):
+        if self._t:
+            _lib.lib().tmf_transfer_destroy(self._t)
+            self._t = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class _Level:
+    p: int
+    dm: object
+    A: object
+    dinv: object
+    lmax: float
+    coeffs: list
+    x: object = None
+    b: object = None
+    r: object = None
+    d: object = None
+    ax: object = None
+
+
+class PMultigrid:
+    """p-multigrid V-cycle on CG Laplace (homogeneous Dirichlet on ``dirichlet_ids``)."""
+
+    def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 3,
+                 smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
+                 lmax=None, config=None, seed: int = 0):
+        import torch
+
+        from . import operator as op
+
+        degrees = tuple(int(p) for p in degrees)
+        if len(degrees) < 2 or any(a <= b for a, b in zip(degrees, degrees[1:])):
+            raise ValueError("degrees must be strictly decreasing, at least two levels")
+        self.config = config or op.OperatorConfig()
+        dev = int(self.config.device)
+        self.device = torch.device(f"cuda:{dev}")
+        self.smoothing_degree, self.smoothing_range = int(smoothing_degree), float(smoothing_range)
+        self.coarse_iterations = int(coarse_iterations)
+        self.levels: list[_Level] = []
+        for i, p in enumerate(degrees):
+            cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+            bas = B.tabulate_basis(p, cr, fr)
+            geo = GeometryData("affine", cr, fr, None, None, None, None)
+            dm = D.build_dof_map(mesh, p, "cg", 1, tuple(dirichlet_ids))
+            A = op.CgPoissonOperator(mesh, dm, geo, bas, self.config)
+            dinv = 1.0 / A.diagonal()
+            lv = _Level(p, dm, A, dinv, 0.0, [])
+            n = dm.n_global_dofs
+            lv.x, lv.b, lv.r, lv.d, lv.ax = (torch.zeros(n, dtype=torch.float64, device=self.device)
+                                             for _ in range(5))
+            if i < len(degrees) - 1:
+                given = None if lmax is None else float(lmax[i])
+                lv.lmax = given if given is not None else 1.1 * self.estimate_lmax(lv, eig_iterations, seed)
+                lv.coeffs = chebyshev_coefficients(lv.lmax, self.smoothing_range, self.smoothing_degree)
+            self.levels.append(lv)
+        self.transfers = [Transfer(self.levels[i].dm, self.levels[i + 1].dm, dev)
+                          for i in range(len(self.levels) - 1)]
+        self.n_global_dofs = self.levels[0].dm.n_global_dofs
+
+    # ------------------------------------------------------------------ setup
+    def estimate_lmax(self, lv, iters: int, seed: int) -> float:
+        """Largest eigenvalue of D^-1 A from ``iters`` Jacobi-PCG (Lanczos) steps."""
+        import torch
+
+        n = lv.dm.n_global_dofs
+        g = np.random.default_rng(seed).uniform(-1, 1, n)
+        g[np.asarray(lv.dm.dirichlet_mask, dtype=bool)] = 0.0
+        r = torch.from_numpy(g).to(self.device)
+        z = r * lv.dinv
+        p = z.clone()
+        q = torch.empty_like(p)
+        rz = float(r @ z)
+        alphas, betas = [], []
+        for _ in range(iters):
+            lv.A.apply_into(p.data_ptr(), q.data_ptr(), self._st())
+            pq = float(p @ q)
+            if pq <= 0.0 or rz <= 0.0:
+                break
+            a = rz / pq
+            r -= a * q
+            z = r * lv.dinv
+            rz_new = float(r @ z)
+            alphas.append(a)
+            betas.append(rz_new / rz)
+            p = z + betas[-1] * p
+            rz = rz_new
+        k = len(alphas)
+        T = np.zeros((k, k))
+        for j in range(k):
+            T[j, j] = 1.0 / alphas[j] + (betas[j - 1] / alphas[j - 1] if j else 0.0)
+            if j + 1 < k:
+                T[j, j + 1] = T[j + 1, j] = np.sqrt(betas[j]) / alphas[j]
+        return float(np.linalg.eigvalsh(T)[-1])
+
+    @staticmethod
+    def _st():
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+
+    # ------------------------------------------------------------------ cycle
+    def _smooth(self, lv, first: bool):
+        """Chebyshev-Jacobi on A x = b (lv.x, lv.b); first: x = 0 on entry."""
+        L = _lib.lib()
+        st = C.c_void_p(self._st())
+        n = lv.dm.n_global_dofs
+        for k, (c1, c2) in enumerate(lv.coeffs):
+            if k == 0 and first:
+                _lib.check(L.tmf_chebyshev_step(n, None, _vp(lv.b), _vp(lv.dinv), _vp(lv.x), _vp(lv.d),
+                                                c1, c2, st))
+                continue
+            lv.A.apply_into(lv.x.data_ptr(), lv.ax.data_ptr(), self._st())
+            _lib.check(L.tmf_chebyshev_step(n, _vp(lv.ax), _vp(lv.b), _vp(lv.dinv), _vp(lv.x), _vp(lv.d),
+                                            c1, c2, st))
+
+    def _cycle(self, i: int):
+        from .solvers import jacobi_pcg
+
+        lv = self.levels[i]
+        if i == len(self.levels) - 1:
+            x, _ = jacobi_pcg(lv.A, lv.b, self.coarse_iterations)
+            lv.x.copy_(x)
+            return
+        st = self._st()
+        self._smooth(lv, first=True)
+        lv.A.apply_into(lv.x.data_ptr(), lv.ax.data_ptr(), st)
+        _lib.check(_lib.lib().tmf_vec_axpby(lv.dm.n_global_dofs, 1.0, _vp(lv.b), -1.0, _vp(lv.ax), _vp(lv.r),
+                                            C.c_void_p(st)))
+        nxt = self.levels[i + 1]
+        self.transfers[i].restrict(lv.r, nxt.b, st)
+        self._cycle(i + 1)
+        self.transfers[i].prolongate(nxt.x, lv.x, add=True, stream=st)
+        self._smooth(lv, first=False)
+
+    def vcycle(self, r, out=None):
+        """z = V r (one V-cycle from a zero initial guess); device tensors."""
+        import torch
+
+        lv = self.levels[0]
+        lv.b.copy_(r)
+        self._cycle(0)
+        if out is None:
+            return lv.x.clone()
+        out.copy_(lv.x)
+        return out
+
+    # ------------------------------------------------------------------ solve
+    def solve(self, b, tol: float = 1e-8, maxiter: int = 200):
+        """Flexible PCG with one V-cycle per iteration; stops when ||r|| <= tol ||b||.
+        Returns (x, residual norms)."""
+        import torch
+
+        A = self.levels[0].A
+        st = self._st()
+        x = torch.zeros_like(b)
+        r = b.clone()
+        z = self.vcycle(r)
+        p = z.clone()
+        q = torch.empty_like(b)
+        rz = float(r @ z)
+        hist = [float(torch.linalg.vector_norm(r))]
+        stop = tol * hist[0]
+        for _ in range(maxiter):
+            if hist[-1] <= stop:
+                break
+            A.apply_into(p.data_ptr(), q.data_ptr(), st)
+            alpha = rz / float(p @ q)
+            x.add_(p, alpha=alpha)
+            r.add_(q, alpha=-alpha)
+            hist.append(float(torch.linalg.vector_norm(r)))
+            z_new = self.vcycle(r)
+            beta = float(r @ (z_new - z)) / rz
+            rz = float(r @ z_new)
+            z = z_new
+            p = z + beta * p
+        return x, np.array(hist)
+
+    def close(self):
+        for t in self.transfers:
+            t.close()
+        for lv in self.levels:
+            lv.A.close()

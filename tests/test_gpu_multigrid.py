@@ -1,0 +1,131 @@
+"""GPU tests of the p-multigrid layer (paper_2509_10226_b200/multigrid.py, csrc/multigrid.cu)
+against the CPU restatement oracle/ref_multigrid.py."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from oracle import ref_apply, ref_multigrid as RM
+
+pytestmark = pytest.mark.gpu
+
+
+def _dm(m, p, dids):
+    from paper_2509_10226_b200 import dofmap as D
+
+    return D.build_dof_map(m, p, "cg", 1, dids)
+
+
+@pytest.mark.parametrize("pf,pc", [(2, 1), (3, 1), (3, 2), (4, 1), (4, 2), (4, 3)])
+@pytest.mark.parametrize("dirichlet", [False, True])
+def test_transfers_match_oracle(pf, pc, dirichlet):
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import Transfer, interpolation_matrix
+
+    m = M.kuhn_cube_mesh(4, seed=0)
+    dids = tuple(range(6)) if dirichlet else ()
+    dmf, dmc = _dm(m, pf, dids), _dm(m, pc, dids)
+    T = Transfer(dmf, dmc)
+    Pg = RM.prolongation_matrix(dmf.cell_dofs, dmc.cell_dofs, interpolation_matrix(pf, pc), dmf.n_scalar_dofs,
+                                dmc.n_scalar_dofs, dmf.dirichlet_mask if dirichlet else None,
+                                dmc.dirichlet_mask if dirichlet else None)
+    rng = np.random.default_rng(3)
+    xc = rng.uniform(-1, 1, dmc.n_scalar_dofs)
+    rf = rng.uniform(-1, 1, dmf.n_scalar_dofs)
+    xf0 = rng.uniform(-1, 1, dmf.n_scalar_dofs)
+    xc_t, rf_t = torch.from_numpy(xc).cuda(), torch.from_numpy(rf).cuda()
+    xf_t = torch.from_numpy(xf0).cuda()
+    T.prolongate(xc_t, xf_t)                      # overwrite
+    assert rel_l2(xf_t.cpu().numpy(), Pg @ xc) <= 1e-14
+    xf_t = torch.from_numpy(xf0).cuda()
+    T.prolongate(xc_t, xf_t, add=True)            # accumulate
+    assert rel_l2(xf_t.cpu().numpy(), xf0 + Pg @ xc) <= 1e-14
+    rc_t = torch.full((dmc.n_scalar_dofs,), 7.0, dtype=torch.float64, device="cuda")
+    T.restrict(rf_t, rc_t)
+    torch.cuda.synchronize()
+    assert rel_l2(rc_t.cpu().numpy(), Pg.T @ rf) <= 1e-14
+    if dirichlet:
+        assert np.all(rc_t.cpu().numpy()[dmc.dirichlet_mask] == 0.0)
+
+
+def test_transfer_rejects_bad_input():
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import Transfer
+
+    m = M.kuhn_cube_mesh(2, seed=0)
+    with pytest.raises(ValueError):
+        Transfer(_dm(m, 1, ()), _dm(m, 2, ()))        # coarse has more DoFs per cell
+    m2 = M.kuhn_cube_mesh(3, seed=0)
+    with pytest.raises(ValueError):
+        Transfer(_dm(m2, 2, ()), _dm(m, 1, ()))       # different meshes
+
+
+def _oracle_levels(m, mg):
+    from paper_2509_10226_b200 import basis as B, quadrature as Q
+
+    levels, transfers = [], []
+    for i, lv in enumerate(mg.levels):
+        p = lv.p
+        cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+        bas = B.tabulate_basis(p, cr, fr)
+        dm = lv.dm
+        A = (lambda dm, bas, w: lambda v: ref_apply.cg_apply(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask,
+                                                             bas.grad_matrix, w, v))(dm, bas, cr.weights)
+        diag = ref_apply.cg_diagonal(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask, bas.grad_matrix,
+                                     cr.weights, dm.n_global_dofs)
+        levels.append(dict(apply=A, diag=diag, coeffs=lv.coeffs))
+        if i + 1 < len(mg.levels):
+            nx = mg.levels[i + 1].dm
+            transfers.append(RM.prolongation_matrix(dm.cell_dofs, nx.cell_dofs, mg.transfers[i].P, dm.n_scalar_dofs,
+                                                    nx.n_scalar_dofs, dm.dirichlet_mask, nx.dirichlet_mask))
+    return levels, transfers
+
+
+@pytest.mark.parametrize("degrees", [(2, 1), (3, 2, 1), (4, 2, 1)])
+def test_vcycle_matches_oracle(degrees):
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import PMultigrid
+
+    m = M.kuhn_cube_mesh(4, seed=0)
+    mg = PMultigrid(m, degrees, coarse_iterations=12)
+    levels, transfers = _oracle_levels(m, mg)
+    # the Lanczos estimate agrees with the oracle's (same start vector, same iteration)
+    lv = mg.levels[0]
+    r0 = np.where(lv.dm.dirichlet_mask, 0.0, np.random.default_rng(0).uniform(-1, 1, lv.dm.n_global_dofs))
+    assert abs(lv.lmax - 1.1 * RM.lanczos_lmax(levels[0]["apply"], levels[0]["diag"], r0, 15)) <= 1e-10 * lv.lmax
+    b = np.where(lv.dm.dirichlet_mask, 0.0, np.random.default_rng(1).uniform(-1, 1, lv.dm.n_global_dofs))
+    z = mg.vcycle(torch.from_numpy(b).cuda()).cpu().numpy()
+    zr = RM.vcycle(levels, transfers, b, 12)
+    assert rel_l2(z, zr) <= 1e-11
+    assert np.all(z[lv.dm.dirichlet_mask] == 0.0)
+
+
+def test_multigrid_pcg_converges_and_matches_oracle():
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import PMultigrid
+    from paper_2509_10226_b200.solvers import jacobi_pcg
+
+    m = M.kuhn_cube_mesh(6, seed=0)
+    mg = PMultigrid(m, (3, 2, 1), coarse_iterations=30)
+    dm = mg.levels[0].dm
+    b = np.where(dm.dirichlet_mask, 0.0, np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs))
+    bt = torch.from_numpy(b).cuda()
+    x, hist = mg.solve(bt, tol=1e-10, maxiter=50)
+    assert hist[-1] <= 1e-10 * hist[0]
+    assert len(hist) - 1 <= 15
+    levels, transfers = _oracle_levels(m, mg)
+    xr, hr = RM.flexible_pcg(levels[0]["apply"], lambda r: RM.vcycle(levels, transfers, r, 30), b, 1e-10, 50)
+    assert len(hr) == len(hist)
+    assert rel_l2(x.cpu().numpy(), xr) <= 1e-9
+    # the true residual, and Jacobi-PCG with the same iteration count is far behind
+    Ax = mg.levels[0].A.apply(x)
+    assert rel_l2(Ax.cpu().numpy(), b) <= 1e-9
+    _, hj = jacobi_pcg(mg.levels[0].A, bt, len(hist) - 1)
+    assert hj[-1] > 1e3 * hist[-1]
+    mg.close()

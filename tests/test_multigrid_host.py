@@ -1,0 +1,95 @@
+"""CPU tests of the p-multigrid layer: interpolation tables, Chebyshev coefficients, and the
+oracle's transfer / V-cycle restatement (oracle/ref_multigrid.py) on small meshes."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from oracle import ref_apply, ref_multigrid as RM
+from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, quadrature as Q
+from paper_2509_10226_b200.multigrid import chebyshev_coefficients, interpolation_matrix
+
+PAIRS = [(2, 1), (3, 1), (3, 2), (4, 1), (4, 2), (4, 3)]
+
+
+@pytest.mark.parametrize("pf,pc", PAIRS)
+def test_interpolation_matrix_reproduces_coarse_polynomials(pf, pc):
+    P = interpolation_matrix(pf, pc)
+    nf, nc = B.n_dofs_per_cell(pf), B.n_dofs_per_cell(pc)
+    assert P.shape == (nf, nc)
+    assert np.allclose(P.sum(axis=1), 1.0, atol=1e-13)          # partition of unity
+    fine, _ = B.reference_nodes(pf)
+    coarse, _ = B.reference_nodes(pc)
+    rng = np.random.default_rng(0)
+    for _ in range(3):   # a random polynomial of degree pc, sampled at both node sets
+        c = rng.standard_normal(B.n_dofs_per_cell(pc))
+        f = lambda x: B._mono(x, B._exponents(pc)) @ c  # noqa: E731
+        assert np.allclose(P @ f(coarse), f(fine), atol=1e-12)
+    # vertex DoFs of the fine space are the coarse vertex DoFs
+    assert np.array_equal(P[:4, :4], np.eye(4))
+
+
+def test_interpolation_matrix_rejects_bad_degrees():
+    with pytest.raises(ValueError):
+        interpolation_matrix(2, 2)
+    with pytest.raises(ValueError):
+        interpolation_matrix(5, 1)
+
+
+def test_chebyshev_coefficients_match_oracle():
+    for deg in (1, 2, 3, 5):
+        a = chebyshev_coefficients(1.7, 15.0, deg)
+        b = RM.chebyshev_coefficients(1.7, 15.0, deg)
+        assert np.allclose(a, b, rtol=0, atol=0)
+
+
+def _space(m, p, dids=()):
+    dm = D.build_dof_map(m, p, "cg", 1, dids)
+    return dm
+
+
+@pytest.mark.parametrize("pf,pc", [(2, 1), (3, 2), (4, 2)])
+def test_oracle_prolongation_interpolates(pf, pc):
+    """The oracle's global prolongation maps the interpolant of a degree-pc polynomial on
+    the coarse space to its interpolant on the fine space (continuity across cells)."""
+    m = M.kuhn_cube_mesh(3, seed=0)
+    dmf, dmc = _space(m, pf), _space(m, pc)
+    Pg = RM.prolongation_matrix(dmf.cell_dofs, dmc.cell_dofs, interpolation_matrix(pf, pc),
+                                dmf.n_scalar_dofs, dmc.n_scalar_dofs)
+    xf = D.dof_coordinates(m, dmf, B.reference_nodes(pf)[0])
+    xc = D.dof_coordinates(m, dmc, B.reference_nodes(pc)[0])
+    f = lambda x: 1.0 + x[:, 0] - 2.0 * x[:, 1] * (pc >= 2) * x[:, 2] + 0.5 * x[:, 2] ** pc  # noqa: E731
+    assert rel_l2(Pg @ f(xc), f(xf)) <= 1e-13
+    # each fine row is a partition of unity
+    assert np.allclose(np.asarray(Pg.sum(axis=1)).ravel(), 1.0, atol=1e-13)
+
+
+def test_oracle_multigrid_pcg_converges_fast():
+    """p-MG (3 -> 2 -> 1) flexible PCG reaches 1e-8 in far fewer iterations than Jacobi-PCG."""
+    m = M.kuhn_cube_mesh(3, seed=0)
+    dids = tuple(range(6))
+    levels, dms = [], []
+    for p in (3, 2, 1):
+        cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+        bas = B.tabulate_basis(p, cr, fr)
+        dm = _space(m, p, dids)
+        A = (lambda dm, bas, w: lambda v: ref_apply.cg_apply(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask,
+                                                             bas.grad_matrix, w, v))(dm, bas, cr.weights)
+        diag = ref_apply.cg_diagonal(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask, bas.grad_matrix,
+                                     cr.weights, dm.n_global_dofs)
+        r0 = np.where(dm.dirichlet_mask, 0.0, np.random.default_rng(0).uniform(-1, 1, dm.n_global_dofs))
+        lmax = 1.1 * RM.lanczos_lmax(A, diag, r0, 15)
+        assert 1.0 < lmax < 5.0
+        levels.append(dict(apply=A, diag=diag, coeffs=RM.chebyshev_coefficients(lmax, 15.0, 3)))
+        dms.append(dm)
+    transfers = [RM.prolongation_matrix(dms[i].cell_dofs, dms[i + 1].cell_dofs,
+                                        interpolation_matrix(dms[i].degree, dms[i + 1].degree),
+                                        dms[i].n_scalar_dofs, dms[i + 1].n_scalar_dofs,
+                                        dms[i].dirichlet_mask, dms[i + 1].dirichlet_mask) for i in range(2)]
+    b = np.where(dms[0].dirichlet_mask, 0.0, np.random.default_rng(1).uniform(-1, 1, dms[0].n_global_dofs))
+    x, hist = RM.flexible_pcg(levels[0]["apply"], lambda r: RM.vcycle(levels, transfers, r, 40), b, 1e-8, 60)
+    assert hist[-1] <= 1e-8 * hist[0]
+    assert len(hist) - 1 <= 10
+    assert rel_l2(levels[0]["apply"](x), b) <= 1e-7
+    _, hj = ref_apply.jacobi_pcg(levels[0]["apply"], levels[0]["diag"], b, len(hist) - 1)
+    assert hj[-1] > 100 * hist[-1]

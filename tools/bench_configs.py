@@ -185,6 +185,64 @@ def csr(n=48):
         torch.cuda.empty_cache()
 
 
+def mg(n=128, degrees=(3, 2, 1), tol=1e-8):
+    """p-multigrid flexible PCG vs Jacobi-PCG on the C5 problem (CG P3, homogeneous
+    Dirichlet, RHS uniform[-1,1]): iterations and device time to ||r|| <= tol ||b||."""
+    import torch
+
+    from paper_2509_10226_b200.multigrid import PMultigrid
+    from paper_2509_10226_b200.solvers import jacobi_pcg
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.reorder import reorder_mesh
+
+    t0 = time.time()
+    m = reorder_mesh(M.kuhn_cube_mesh(n, seed=0))
+    mg_ = PMultigrid(m, degrees, coarse_iterations=30)
+    setup = time.time() - t0
+    dm = mg_.levels[0].dm
+    nd = dm.n_global_dofs
+    b = np.where(dm.dirichlet_mask, 0.0, np.random.default_rng(1).uniform(-1, 1, nd))
+    bt = torch.from_numpy(b).cuda()
+    mg_.solve(bt, tol=1e-2, maxiter=3)   # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, hist = mg_.solve(bt, tol=tol, maxiter=200)
+    e1.record()
+    e1.synchronize()
+    t_mg = e0.elapsed_time(e1)
+    # one V-cycle alone
+    r = bt.clone()
+    e0.record()
+    for _ in range(5):
+        mg_.vcycle(r)
+    e1.record()
+    e1.synchronize()
+    t_v = e0.elapsed_time(e1) / 5
+    true_res = float(torch.linalg.vector_norm(mg_.levels[0].A.apply(x) - bt) / torch.linalg.vector_norm(bt))
+    # Jacobi-PCG: iterations to the same tolerance (fixed-count native loop, residual history)
+    jit = 4000
+    e0.record()
+    _, hj = jacobi_pcg(mg_.levels[0].A, bt, jit)
+    e1.record()
+    e1.synchronize()
+    t_j = e0.elapsed_time(e1)
+    hit = np.nonzero(hj <= tol * hj[0])[0]
+    kj = int(hit[0]) if len(hit) else None
+    print(json.dumps({"config": f"p-multigrid PCG vs Jacobi-PCG, CG P3 {n}^3x6 reordered, Dirichlet, tol {tol}",
+                      "ndof": nd, "levels": list(degrees), "lmax": [round(lv.lmax, 4) for lv in mg_.levels[:-1]],
+                      "smoother": f"Chebyshev-Jacobi degree {mg_.smoothing_degree}, range {mg_.smoothing_range}",
+                      "coarse": f"P1 Jacobi-PCG {mg_.coarse_iterations} iterations",
+                      "mg_iterations": len(hist) - 1, "mg_solve_ms": round(t_mg, 2), "vcycle_ms": round(t_v, 3),
+                      "mg_true_rel_residual": true_res,
+                      "jacobi_iterations_to_tol": kj, "jacobi_ms_per_iteration": round(t_j / jit, 4),
+                      "jacobi_ms_to_tol": round(t_j / jit * kj, 2) if kj else None,
+                      "speedup_time_to_tol": round(t_j / jit * kj / t_mg, 2) if kj else None,
+                      "setup_s": round(setup, 1)}), flush=True)
+    mg_.close()
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["c1", "c2", "c3", "c4", "c5"])
@@ -194,4 +252,4 @@ if __name__ == "__main__":
     a = ap.parse_args()
     for c in a.configs:
         {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5),
-         "csr": csr}[c]()
+         "csr": csr, "mg": lambda: mg(a.n5)}[c]()
