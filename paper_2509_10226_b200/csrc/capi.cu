@@ -7,6 +7,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -556,7 +557,11 @@ namespace {
 
 int n_dofs_per_cell(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
 
+#ifdef TMF_EXP_FACE_WINDOW_ENV   // tuning experiment only (tools/gpu_window.sh)
+const int64_t kFaceWindow = getenv("TMF_FACE_WINDOW") ? atoll(getenv("TMF_FACE_WINDOW")) : 8192;
+#else
 constexpr int64_t kFaceWindow = 8192;
+#endif
 
 // Split [first, first+count) batches of one signature into CTA chunks.
 void push_chunks(std::vector<int4>& out, int cm, int cp, int64_t first, int64_t count, int chunk) {
