@@ -558,9 +558,12 @@ namespace {
 int n_dofs_per_cell(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
 
 #ifdef TMF_EXP_FACE_WINDOW_ENV   // tuning experiment only (tools/gpu_window.sh)
-const int64_t kFaceWindow = getenv("TMF_FACE_WINDOW") ? atoll(getenv("TMF_FACE_WINDOW")) : 8192;
+const int64_t kFaceWindow = getenv("TMF_FACE_WINDOW") ? atoll(getenv("TMF_FACE_WINDOW")) : 32768;
 #else
-constexpr int64_t kFaceWindow = 8192;
+// measured (tools/gpu_window.sh, profiles/r01/face_window_sweep.json): 512 / 2048 / 8192 / 32768 /
+// 131072 minus cells per window -> DG P3 64^3 faces 1.224 / 1.045 / 0.930 / 0.889 / 0.888 ms,
+// Helmholtz P2 96^3 1.576 / 1.459 / 1.406 / 1.392 / 1.412 ms (longer signature runs, fewer chunks)
+constexpr int64_t kFaceWindow = 32768;
 #endif
 
 // Split [first, first+count) batches of one signature into CTA chunks.

@@ -8,7 +8,8 @@ the fp64 p-multigrid part of it, built on the B200 operator apply:
   each a :class:`CgPoissonOperator` with its matrix-free diagonal;
 * transfers: ``tmf_prolongate`` / ``tmf_restrict`` (interpolation of the coarse
   function at the fine nodes and its exact transpose, csrc/multigrid.cu);
-* smoother: Chebyshev-accelerated point Jacobi of degree ``smoothing_degree`` on
+* smoother: Chebyshev-accelerated point Jacobi of degree ``smoothing_degree`` (default 2:
+  fastest to 1e-8 on the C5 problem among 2 / 3 / 4, tools/mg_sweep.py) on
   [lambda_max / smoothing_range, lambda_max] (Saad, Iterative Methods, Alg. 12.1;
   fused update ``tmf_chebyshev_step``); lambda_max of D^-1 A from a short Lanczos
   (Jacobi-PCG coefficients) times 1.1;
@@ -131,7 +132,7 @@ class _Level:
 class PMultigrid:
     """p-multigrid V-cycle on CG Laplace (homogeneous Dirichlet on ``dirichlet_ids``)."""
 
-    def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 3,
+    def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 2,
                  smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
                  lmax=None, config=None, seed: int = 0):
         import torch
