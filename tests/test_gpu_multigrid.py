@@ -118,7 +118,7 @@ def test_multigrid_pcg_converges_and_matches_oracle():
     bt = torch.from_numpy(b).cuda()
     x, hist = mg.solve(bt, tol=1e-10, maxiter=50)
     assert hist[-1] <= 1e-10 * hist[0]
-    assert len(hist) - 1 <= 15
+    assert len(hist) - 1 <= 20
     levels, transfers = _oracle_levels(m, mg)
     xr, hr = RM.flexible_pcg(levels[0]["apply"], lambda r: RM.vcycle(levels, transfers, r, 30), b, 1e-10, 50)
     assert len(hr) == len(hist)
