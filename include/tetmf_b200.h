@@ -213,9 +213,16 @@ int tmf_build_faces(int64_t n_cells, const int32_t* cells, int64_t n_vertices,
 int tmf_build_cg_dofs(int64_t n_cells, const int32_t* cells, int64_t n_vertices, int32_t degree,
                       int32_t* cell_dofs, int64_t* n_scalar_dofs);
 
+/* Greedy distance-1 colouring of the cells' face-adjacency graph (cells in order, smallest
+ * colour unused by a coloured face neighbour; <= 5 colours).  Host-side setup; used to probe
+ * the exact diagonal of DG operators (one apply per colour and local DoF). */
+int tmf_color_cells(int64_t n_cells, int64_t n_interior_faces, const int32_t* interior_faces,
+                    int32_t* colors, int32_t* n_colors);
+
 /* p-multigrid building blocks (the paper's solver layer, PAPER.md:423-436,
  * SPEC.md:494-565; the reference has no implementation).  A transfer links two CG spaces of
- * degrees pf > pc on the same mesh: prolongation x_f = P x_c interpolates the coarse
+ * degrees pf > pc on the same mesh (or a DG space over the CG space of the same degree: the
+ * c-transfer, interp = identity): prolongation x_f = P x_c interpolates the coarse
  * function at the fine nodes (interp[i*n_coarse_dpc + j] = coarse basis j at fine node i,
  * row-major n_fine_dpc x n_coarse_dpc); restriction r_c = P^T r_f is its exact transpose.
  * Each fine DoF is written by one owner cell (the first cell containing it).  Dirichlet
@@ -225,7 +232,7 @@ int tmf_build_cg_dofs(int64_t n_cells, const int32_t* cells, int64_t n_vertices,
 typedef struct tmf_transfer tmf_transfer;
 typedef struct tmf_transfer_desc {
   int64_t n_cells;
-  int32_t n_fine_dpc, n_coarse_dpc;          /* 10/20/35 over 4/10/20                  */
+  int32_t n_fine_dpc, n_coarse_dpc;          /* fine >= coarse; coarse 4/10/20/35      */
   int64_t n_fine_dofs, n_coarse_dofs;
   const int32_t* fine_cell_dofs;             /* host (n_cells, n_fine_dpc)              */
   const int32_t* coarse_cell_dofs;           /* host (n_cells, n_coarse_dpc)            */

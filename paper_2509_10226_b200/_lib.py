@@ -96,6 +96,7 @@ def lib():
         L.tmf_ipc_get_handle.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]
         L.tmf_ipc_open_handle.argtypes = [C.POINTER(C.c_uint8), C.c_int32, C.POINTER(C.c_void_p)]
         L.tmf_ipc_close_handle.argtypes = [C.c_void_p]
+        L.tmf_color_cells.argtypes = [C.c_int64, C.c_int64, _ip, _ip, _ip]
         L.tmf_transfer_create.argtypes = [C.POINTER(TransferDesc), C.POINTER(C.c_void_p)]
         L.tmf_transfer_destroy.argtypes = [_v]
         L.tmf_prolongate.argtypes = [_v, _v, _v, C.c_int, _v]
@@ -109,7 +110,7 @@ def lib():
                      "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs",
                      "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction",
                      "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle", "tmf_ipc_open_handle",
-                     "tmf_ipc_close_handle", "tmf_transfer_create", "tmf_transfer_destroy", "tmf_prolongate",
+                     "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create", "tmf_transfer_destroy", "tmf_prolongate",
                      "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby"):
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -120,7 +121,7 @@ EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_app
             "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
             "tmf_build_faces", "tmf_build_cg_dofs", "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update",
             "tmf_pcg_direction", "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle",
-            "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_transfer_create", "tmf_transfer_destroy",
+            "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create", "tmf_transfer_destroy",
             "tmf_prolongate", "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby", "tmf_last_error",
             "tmf_version")
 

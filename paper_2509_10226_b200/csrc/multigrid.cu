@@ -1,6 +1,7 @@
-// p-multigrid building blocks (the paper's solver layer PAPER.md:423-436,
+// p- and c-multigrid building blocks (the paper's solver layer PAPER.md:423-436,
 // SPEC.md:494-565; the reference ships none of it): degree-transfer operators between
-// two CG spaces on the same mesh and the fused Chebyshev-Jacobi smoother update.
+// two CG spaces (or a DG and a CG space) on the same mesh and the fused Chebyshev-Jacobi
+// smoother update.
 //
 // Prolongation P: the coarse (degree pc) function interpolated at the fine (degree pf)
 // nodes, cell by cell: x_f[i] = sum_j P_loc[i, j] x_c[cdofs[j]], P_loc[i, j] =
@@ -9,6 +10,9 @@
 // needs no atomics, is deterministic, and restriction R = P^T (the exact transpose of
 // the global interpolation matrix) sums every fine row once:
 //   r_c[cdofs[j]] += sum_{i owned by e} P_loc[i, j] r_f[fdofs[i]]     (fp64 RED)
+// c-transfer (DG fine space over the CG space of the same degree, P_loc = I): every DG
+// DoF belongs to one cell, prolongation copies the CG value of a node into each cell's
+// DG DoF and restriction sums the DG values of a node into its CG DoF.
 // Dirichlet DoFs: fine ones are written as 0 (overwrite) / left alone (add) and never
 // restricted; coarse ones are gathered as 0 and never scattered (their rows are
 // identity rows of the coarse operator and stay zero in the correction).
@@ -147,10 +151,10 @@ int tmf_transfer_create(const tmf_transfer_desc* d, tmf_transfer** out) {
   if (d->n_cells <= 0) return mg_fail(TMF_EINVAL, "empty mesh");
   if (!d->fine_cell_dofs || !d->coarse_cell_dofs || !d->interp)
     return mg_fail(TMF_EINVAL, "missing dof maps / interpolation matrix");
-  if (d->n_coarse_dpc != 4 && d->n_coarse_dpc != 10 && d->n_coarse_dpc != 20)
-    return mg_fail(TMF_EINVAL, "coarse space must be P1, P2 or P3 (4/10/20 DoFs per cell)");
-  if (d->n_fine_dpc <= d->n_coarse_dpc || d->n_fine_dpc > 35)
-    return mg_fail(TMF_EINVAL, "fine space must have more DoFs per cell than the coarse one (<= 35)");
+  if (d->n_coarse_dpc != 4 && d->n_coarse_dpc != 10 && d->n_coarse_dpc != 20 && d->n_coarse_dpc != 35)
+    return mg_fail(TMF_EINVAL, "coarse space must be P1-P4 (4/10/20/35 DoFs per cell)");
+  if (d->n_fine_dpc < d->n_coarse_dpc || d->n_fine_dpc > 35)
+    return mg_fail(TMF_EINVAL, "fine space needs at least as many DoFs per cell as the coarse one (<= 35)");
   if (d->n_fine_dofs <= 0 || d->n_coarse_dofs <= 0 || d->n_fine_dofs >= INT_MAX)
     return mg_fail(TMF_EINVAL, "bad DoF counts");
   const int64_t n = d->n_cells;
@@ -222,8 +226,10 @@ int tmf_prolongate(tmf_transfer* t, const double* xc, double* xf, int add, void*
     prolongate_kernel<4><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
   else if (t->nc == 10)
     prolongate_kernel<10><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
-  else
+  else if (t->nc == 20)
     prolongate_kernel<20><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
+  else
+    prolongate_kernel<35><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
   MG_CUDA(cudaGetLastError());
   return TMF_OK;
 }
@@ -241,8 +247,10 @@ int tmf_restrict(tmf_transfer* t, const double* rf, double* rc, void* stream) {
     restrict_kernel<4><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
   else if (t->nc == 10)
     restrict_kernel<10><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
-  else
+  else if (t->nc == 20)
     restrict_kernel<20><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
+  else
+    restrict_kernel<35><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
   MG_CUDA(cudaGetLastError());
   return TMF_OK;
 }

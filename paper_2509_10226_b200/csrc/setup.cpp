@@ -203,3 +203,46 @@ extern "C" int tmf_build_cg_dofs(int64_t n_cells, const int32_t* cells, int64_t 
   *n_scalar_dofs = n_scalar;
   return TMF_OK;
 }
+
+// Greedy distance-1 colouring of the face-adjacency graph of the cells (cells in order, each
+// gets the smallest colour not used by an already coloured face neighbour) -- the cell-level
+// analogue of the reference's batch colouring (dofmap.py:269-292).  Used to probe the exact
+// diagonal of DG operators: cells of one colour share no face, so one apply per
+// (colour, local DoF) reads their diagonal entries (multigrid.py: dg_diagonal).
+extern "C" int tmf_color_cells(int64_t n_cells, int64_t n_interior_faces, const int32_t* interior_faces,
+                               int32_t* colors, int32_t* n_colors) {
+  if (n_cells < 0 || n_interior_faces < 0 || !colors || !n_colors || (n_interior_faces && !interior_faces))
+    return TMF_EINVAL;
+  std::vector<int64_t> start(n_cells + 1, 0);
+  for (int64_t f = 0; f < n_interior_faces; ++f) {
+    const int32_t a = interior_faces[5 * f], b = interior_faces[5 * f + 2];
+    if (a < 0 || a >= n_cells || b < 0 || b >= n_cells) return TMF_EINVAL;
+    start[a + 1]++;
+    start[b + 1]++;
+  }
+  for (int64_t e = 0; e < n_cells; ++e) start[e + 1] += start[e];
+  std::vector<int32_t> adj(start[n_cells]);
+  {
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    for (int64_t f = 0; f < n_interior_faces; ++f) {
+      const int32_t a = interior_faces[5 * f], b = interior_faces[5 * f + 2];
+      adj[fill[a]++] = b;
+      adj[fill[b]++] = a;
+    }
+  }
+  int32_t nc = 0;
+  for (int64_t e = 0; e < n_cells; ++e) colors[e] = -1;
+  for (int64_t e = 0; e < n_cells; ++e) {
+    uint64_t used = 0;
+    for (int64_t k = start[e]; k < start[e + 1]; ++k) {
+      const int32_t c = colors[adj[k]];
+      if (c >= 0 && c < 64) used |= 1ull << c;
+    }
+    int32_t c = 0;
+    while (c < 64 && (used >> c & 1)) ++c;
+    colors[e] = c;   // a cell has <= 4 face neighbours, so c <= 4
+    if (c + 1 > nc) nc = c + 1;
+  }
+  *n_colors = nc;
+  return TMF_OK;
+}

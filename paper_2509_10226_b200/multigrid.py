@@ -13,6 +13,9 @@ the fp64 p-multigrid part of it, built on the B200 operator apply:
   [lambda_max / smoothing_range, lambda_max] (Saad, Iterative Methods, Alg. 12.1;
   fused update ``tmf_chebyshev_step``); lambda_max of D^-1 A from a short Lanczos
   (Jacobi-PCG coefficients) times 1.1;
+* optional DG finest level (``fine_operator``) over the CG levels via a c-transfer (DG p ->
+  CG p, "transferred to an auxiliary continuous space"), smoothed with the
+  exact DG diagonal probed by colouring (:func:`dg_diagonal`);
 * coarse level (P1): ``coarse_iterations`` native Jacobi-PCG iterations (``tmf_pcg``);
 * outer loop: flexible (Polak-Ribiere) PCG, since a fixed-count inner CG makes the
   V-cycle slightly nonlinear.
@@ -36,7 +39,8 @@ from . import dofmap as D
 from . import quadrature as Q
 from .geometry import GeometryData
 
-__all__ = ["interpolation_matrix", "Transfer", "PMultigrid", "chebyshev_coefficients"]
+__all__ = ["interpolation_matrix", "Transfer", "PMultigrid", "chebyshev_coefficients", "color_cells",
+           "dg_diagonal", "n10"]
 
 
 def interpolation_matrix(p_fine: int, p_coarse: int) -> np.ndarray:
@@ -48,6 +52,45 @@ def interpolation_matrix(p_fine: int, p_coarse: int) -> np.ndarray:
     P = B.lagrange_values(p_coarse, nodes)
     P[np.abs(P) < 1e-13] = 0.0
     return np.ascontiguousarray(P)
+
+
+def color_cells(mesh):
+    """Greedy face-adjacency colouring of the cells (``tmf_color_cells``): (colors, n_colors)."""
+    f = np.ascontiguousarray(mesh.interior_faces, dtype=np.int32)
+    col = np.empty(mesh.n_cells, dtype=np.int32)
+    nc = C.c_int32()
+    rc = _lib.lib().tmf_color_cells(mesh.n_cells, len(f), _lib.ptr(f, C.c_int32), _lib.ptr(col, C.c_int32),
+                                    C.byref(nc))
+    if rc != _lib.TMF_OK:
+        raise ValueError("bad interior-face table")
+    return col, int(nc.value)
+
+
+def dg_diagonal(A, mesh, stream: int = 0):
+    """Exact diagonal of a DG operator (a device tensor): cells of one colour share no face,
+    so applying A to the indicator of local DoF j on all cells of a colour returns their
+    diagonal entries at those positions (n_colours x n_dofs_per_cell applies)."""
+    import torch
+
+    N = A.dofmap.n_dofs_per_cell
+    nc_ = int(A.dofmap.n_components)
+    col, ncol = color_cells(mesh)
+    dev = torch.device(f"cuda:{A.config.device}")
+    n = A.n_global_dofs
+    diag = torch.empty(n, dtype=torch.float64, device=dev)
+    u = torch.zeros(n, dtype=torch.float64, device=dev)
+    y = torch.empty_like(u)
+    st = stream or torch.cuda.current_stream(dev).cuda_stream
+    for c in range(ncol):
+        cells = torch.from_numpy(np.nonzero(col == c)[0].astype(np.int64)).to(dev)
+        for j in range(N):
+            for k in range(nc_):
+                idx = (cells * N + j) * nc_ + k
+                u.zero_()
+                u[idx] = 1.0
+                A.apply_into(u.data_ptr(), y.data_ptr(), st)
+                diag[idx] = y[idx]
+    return diag
 
 
 def chebyshev_coefficients(lmax: float, smoothing_range: float, degree: int):
@@ -75,7 +118,12 @@ class Transfer:
     def __init__(self, fine_dm, coarse_dm, device: int = 0):
         if fine_dm.n_cells != coarse_dm.n_cells:
             raise ValueError("fine and coarse dof maps must live on the same mesh")
-        self.P = interpolation_matrix(fine_dm.degree, coarse_dm.degree)
+        if fine_dm.space == "dg" and coarse_dm.space == "cg" and fine_dm.degree == coarse_dm.degree:
+            self.P = np.eye(fine_dm.n_dofs_per_cell)          # c-transfer: DG p -> CG p
+        elif fine_dm.space == "cg" and coarse_dm.space == "cg":
+            self.P = interpolation_matrix(fine_dm.degree, coarse_dm.degree)
+        else:
+            raise ValueError("transfers are CG p -> CG q < p, or DG p -> CG p")
         fd = np.ascontiguousarray(fine_dm.cell_dofs, dtype=np.int32)
         cd = np.ascontiguousarray(coarse_dm.cell_dofs, dtype=np.int32)
         fm = np.ascontiguousarray(fine_dm.dirichlet_mask, dtype=np.uint8)
@@ -130,11 +178,16 @@ class _Level:
 
 
 class PMultigrid:
-    """p-multigrid V-cycle on CG Laplace (homogeneous Dirichlet on ``dirichlet_ids``)."""
+    """p-multigrid V-cycle on CG Laplace (homogeneous Dirichlet on ``dirichlet_ids``).
+
+    ``fine_operator``: a DG operator (DgSipgOperator / HelmholtzOperator / KappaHelmholtzOperator
+    of degree ``degrees[0]``, weak Dirichlet on ``dirichlet_ids``) to put on top of the CG levels
+    through a c-transfer (the paper's cp-MG); its smoother uses the exact
+    diagonal probed by :func:`dg_diagonal`."""
 
     def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 2,
                  smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
-                 lmax=None, config=None, seed: int = 0):
+                 lmax=None, config=None, seed: int = 0, fine_operator=None):
         import torch
 
         from . import operator as op
@@ -148,18 +201,29 @@ class PMultigrid:
         self.smoothing_degree, self.smoothing_range = int(smoothing_degree), float(smoothing_range)
         self.coarse_iterations = int(coarse_iterations)
         self.levels: list[_Level] = []
-        for i, p in enumerate(degrees):
-            cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
-            bas = B.tabulate_basis(p, cr, fr)
-            geo = GeometryData("affine", cr, fr, None, None, None, None)
-            dm = D.build_dof_map(mesh, p, "cg", 1, tuple(dirichlet_ids))
-            A = op.CgPoissonOperator(mesh, dm, geo, bas, self.config)
-            dinv = 1.0 / A.diagonal()
+        specs = [("cg", p) for p in degrees]
+        if fine_operator is not None:
+            if fine_operator.dofmap.space != "dg" or fine_operator.dofmap.degree != degrees[0]:
+                raise ValueError("fine_operator must be a DG operator of degree degrees[0]")
+            if int(fine_operator.dofmap.n_components) != 1:
+                raise ValueError("fine_operator must be scalar")
+            specs.insert(0, ("dg", degrees[0]))
+        for i, (space, p) in enumerate(specs):
+            if space == "dg":
+                A, dm = fine_operator, fine_operator.dofmap
+                dinv = 1.0 / dg_diagonal(A, mesh)
+            else:
+                cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+                bas = B.tabulate_basis(p, cr, fr)
+                geo = GeometryData("affine", cr, fr, None, None, None, None)
+                dm = D.build_dof_map(mesh, p, "cg", 1, tuple(dirichlet_ids))
+                A = op.CgPoissonOperator(mesh, dm, geo, bas, self.config)
+                dinv = 1.0 / A.diagonal()
             lv = _Level(p, dm, A, dinv, 0.0, [])
             n = dm.n_global_dofs
             lv.x, lv.b, lv.r, lv.d, lv.ax = (torch.zeros(n, dtype=torch.float64, device=self.device)
                                              for _ in range(5))
-            if i < len(degrees) - 1:
+            if i < len(specs) - 1:
                 given = None if lmax is None else float(lmax[i])
                 lv.lmax = given if given is not None else 1.1 * self.estimate_lmax(lv, eig_iterations, seed)
                 lv.coeffs = chebyshev_coefficients(lv.lmax, self.smoothing_range, self.smoothing_degree)
@@ -290,4 +354,18 @@ class PMultigrid:
         for t in self.transfers:
             t.close()
         for lv in self.levels:
-            lv.A.close()
+            if lv.dm.space == "cg":   # a caller's fine operator stays open
+                lv.A.close()
+
+
+def n10(hist) -> float:
+    """Fractional iteration count to reduce the residual by 1e10 ([Fehn2019]):
+    linear interpolation of log10 ||r|| between the bracketing iterations."""
+    h = np.log10(np.asarray(hist, dtype=float) / float(hist[0]))
+    hit = np.nonzero(h <= -10.0)[0]
+    if not len(hit):
+        raise ValueError("the residual was not reduced by ten orders of magnitude")
+    k = int(hit[0])
+    if k == 0:
+        return 0.0
+    return float(k - 1 + (h[k - 1] + 10.0) / (h[k - 1] - h[k]))

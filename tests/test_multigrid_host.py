@@ -93,3 +93,31 @@ def test_oracle_multigrid_pcg_converges_fast():
     assert rel_l2(levels[0]["apply"](x), b) <= 1e-7
     _, hj = ref_apply.jacobi_pcg(levels[0]["apply"], levels[0]["diag"], b, len(hist) - 1)
     assert hj[-1] > 100 * hist[-1]
+
+
+def test_color_cells_is_a_proper_colouring():
+    from paper_2509_10226_b200.multigrid import color_cells
+
+    m = M.kuhn_cube_mesh(5, seed=0)
+    col, nc = color_cells(m)
+    f = m.interior_faces
+    assert np.all(col[f[:, 0]] != col[f[:, 2]])
+    assert 2 <= nc <= 5 and col.min() == 0 and col.max() == nc - 1
+    # greedy in cell order: every cell's colour is the smallest not used by an earlier neighbour
+    nbr = [[] for _ in range(m.n_cells)]
+    for a, b in zip(f[:, 0], f[:, 2]):
+        nbr[a].append(b)
+        nbr[b].append(a)
+    for e in range(m.n_cells):
+        used = {col[x] for x in nbr[e] if x < e}
+        assert col[e] == min(set(range(6)) - used)
+
+
+def test_n10_metric():
+    from paper_2509_10226_b200.multigrid import n10
+
+    assert n10(10.0 ** -np.arange(12)) == pytest.approx(10.0)        # 10x per iteration
+    h = [1.0, 1e-4, 1e-8, 1e-12]                                        # 1e-10 reached mid-way
+    assert n10(h) == pytest.approx(2.5)
+    with pytest.raises(ValueError):
+        n10([1.0, 1e-3])

@@ -243,6 +243,54 @@ def mg(n=128, degrees=(3, 2, 1), tol=1e-8):
     mg_.close()
 
 
+def mgdg(n=64, p=3, tol=1e-8):
+    """cp-multigrid (DG p -> CG p -> ... -> CG 1) flexible PCG vs Jacobi-PCG on the C3 problem
+    (DG-SIPG P3, weak Dirichlet on all sides, RHS uniform[-1,1]): iterations / time to tol."""
+    import torch
+
+    from paper_2509_10226_b200 import operator as op
+    from paper_2509_10226_b200.multigrid import PMultigrid, n10
+    from paper_2509_10226_b200.solvers import pcg_loop
+
+    m, dm, geo, bas, ts = setup(n, p, "dg", True)
+    t0 = time.time()
+    A = op.DgSipgOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n), dirichlet_ids=range(6))
+    mg_ = PMultigrid(m, tuple(range(p, 0, -1)), fine_operator=A, coarse_iterations=30)
+    setup_mg = time.time() - t0
+    nd = dm.n_global_dofs
+    bt = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, nd)).cuda()
+    mg_.solve(bt, tol=1e-2, maxiter=2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, hist = mg_.solve(bt, tol=tol, maxiter=300)
+    e1.record()
+    e1.synchronize()
+    t_mg = e0.elapsed_time(e1)
+    true_res = float(torch.linalg.vector_norm(A.apply(x) - bt) / torch.linalg.vector_norm(bt))
+    diag = 1.0 / mg_.levels[0].dinv
+    jit = 3000
+    e0.record()
+    _, hj = pcg_loop(lambda v, out: A.apply_into(v.data_ptr(), out.data_ptr(),
+                                                 torch.cuda.current_stream().cuda_stream), diag, bt, jit)
+    e1.record()
+    e1.synchronize()
+    t_j = e0.elapsed_time(e1)
+    hit = np.nonzero(hj <= tol * hj[0])[0]
+    kj = int(hit[0]) if len(hit) else None
+    print(json.dumps({"config": f"cp-multigrid PCG vs Jacobi-PCG, DG-SIPG P{p} {n}^3x6 reordered, weak Dirichlet, "
+                      f"tol {tol}", "ndof": nd, "levels": ["dg%d" % p] + ["cg%d" % lv.p for lv in mg_.levels[1:]],
+                      "lmax": [round(lv.lmax, 4) for lv in mg_.levels[:-1]],
+                      "mg_iterations": len(hist) - 1, "mg_solve_ms": round(t_mg, 2),
+                      "mg_true_rel_residual": true_res,
+                      "jacobi_iterations_to_tol": kj, "jacobi_ms_per_iteration": round(t_j / jit, 4),
+                      "jacobi_rel_residual_after_%d" % jit: float(hj[-1] / hj[0]),
+                      "jacobi_ms_to_tol": round(t_j / jit * kj, 2) if kj else None,
+                      "speedup_time_to_tol": round(t_j / jit * kj / t_mg, 2) if kj else None,
+                      "setup_s": round(ts, 1), "mg_setup_s": round(setup_mg, 1)}), flush=True)
+    mg_.close()
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["c1", "c2", "c3", "c4", "c5"])
@@ -252,4 +300,4 @@ if __name__ == "__main__":
     a = ap.parse_args()
     for c in a.configs:
         {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5),
-         "csr": csr, "mg": lambda: mg(a.n5)}[c]()
+         "csr": csr, "mg": lambda: mg(a.n5), "mgdg": lambda: mgdg(a.n3)}[c]()
