@@ -249,7 +249,11 @@ class PMultigrid:
         for _ in range(iters):
             lv.A.apply_into(p.data_ptr(), q.data_ptr(), self._st())
             pq = float(p @ q)
-            if pq <= 0.0 or rz <= 0.0:
+            if pq <= 0.0:
+                # SPEC.md:514 "indefiniteness detected (p^T A p <= 0)"
+                raise ValueError(f"level P{lv.p} ({lv.dm.space}) is not positive definite: p.Ap = {pq:.3e} "
+                                 f"after {len(alphas)} Lanczos steps (DG: penalty too small for the mesh?)")
+            if rz <= 0.0:
                 break
             a = rz / pq
             r -= a * q
@@ -339,7 +343,10 @@ class PMultigrid:
             if hist[-1] <= stop:
                 break
             A.apply_into(p.data_ptr(), q.data_ptr(), st)
-            alpha = rz / float(p @ q)
+            pq = float(p @ q)
+            if pq <= 0.0:
+                raise ValueError(f"indefinite operator or preconditioner: p.Ap = {pq:.3e}")
+            alpha = rz / pq
             x.add_(p, alpha=alpha)
             r.add_(q, alpha=-alpha)
             hist.append(float(torch.linalg.vector_norm(r)))

@@ -217,3 +217,18 @@ def test_dg_cp_multigrid_matches_oracle_and_converges():
     _, hj = pcg_loop(lambda v, out: out.copy_(A.apply(v)), 1.0 / mg.levels[0].dinv, bt, 3 * len(hist))
     assert hj[-1] > 1e2 * hist[-1]
     assert n10(hist) < len(hist)
+
+
+def test_indefinite_operator_is_reported():
+    """cg_solve reports indefiniteness (p.Ap <= 0); a DG-SIPG penalty far below the
+    coercivity threshold makes the operator indefinite and the hierarchy set-up raises."""
+    from paper_2509_10226_b200 import operator as op
+    from paper_2509_10226_b200.multigrid import PMultigrid
+
+    m, dm, A, _ = _dg_problem(3, 2)
+    sipg = op.baseline_sipg_tau(m, 2, 1.0 / 3)
+    sipg.tau_interior *= 1e-3
+    sipg.tau_boundary *= 1e-3
+    B = op.DgSipgOperator(m, dm, A.geo, A.basis, sipg, dirichlet_ids=range(6))
+    with pytest.raises(ValueError, match="positive definite"):
+        PMultigrid(m, (2, 1), fine_operator=B, eig_iterations=60)
