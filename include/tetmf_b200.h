@@ -78,7 +78,8 @@ typedef struct tmf_plan_desc {
   double mass_scale;           /* Helmholtz mass coefficient                          */
   double diffusivity;          /* Laplace/SIPG scale (nu)                             */
   int32_t device;              /* CUDA device ordinal                                 */
-  int32_t flags;               /* bits 0-3 / 4-7: cell / face kernel tuning variant;
+  int32_t flags;               /* bit 20: also build the fp32 mirror (tmf_apply_f32);
+                                  bits 0-3 / 4-7: cell / face kernel tuning variant;
                                   8-11 face chunk/8; 12 concurrent DG; 13-14 cell engine
                                   (0 by degree, 1 DMMA quadrature points, 2 DFMA,
                                   3 DMMA reference tensor); 15-16 CG
@@ -251,6 +252,16 @@ int tmf_chebyshev_step(int64_t n, const double* ax, const double* b, const doubl
                        double* d, double c1, double c2, void* stream);
 int tmf_vec_axpby(int64_t n, double alpha, const double* x, double beta, const double* y, double* out,
                   void* stream);
+/* Single-precision mirrors for a mixed-precision V-cycle (the paper's fp32 multigrid with an
+ * fp64 outer CG).  tmf_apply_f32: y = A u in fp32 for a scalar CG Laplace
+ * plan created with flags bit 20 (modal cell form, fp32 FFMA, identity Dirichlet rows). */
+int tmf_apply_f32(tmf_plan* plan, const float* u, float* y, void* stream);
+int tmf_prolongate_f32(tmf_transfer* t, const float* xc, float* xf, int add, void* stream);
+int tmf_restrict_f32(tmf_transfer* t, const float* rf, float* rc, void* stream);
+int tmf_chebyshev_step_f32(int64_t n, const float* ax, const float* b, const float* dinv, float* x,
+                           float* d, float c1, float c2, void* stream);
+int tmf_vec_axpby_f32(int64_t n, float alpha, const float* x, float beta, const float* y, float* out,
+                      void* stream);
 
 const char* tmf_last_error(void);
 const char* tmf_version(void);

@@ -103,6 +103,11 @@ def lib():
         L.tmf_restrict.argtypes = [_v, _v, _v, _v]
         L.tmf_chebyshev_step.argtypes = [C.c_int64, _v, _v, _v, _v, _v, C.c_double, C.c_double, _v]
         L.tmf_vec_axpby.argtypes = [C.c_int64, C.c_double, _v, C.c_double, _v, _v, _v]
+        L.tmf_apply_f32.argtypes = [_v, _v, _v, _v]
+        L.tmf_prolongate_f32.argtypes = [_v, _v, _v, C.c_int, _v]
+        L.tmf_restrict_f32.argtypes = [_v, _v, _v, _v]
+        L.tmf_chebyshev_step_f32.argtypes = [C.c_int64, _v, _v, _v, _v, _v, C.c_float, C.c_float, _v]
+        L.tmf_vec_axpby_f32.argtypes = [C.c_int64, C.c_float, _v, C.c_float, _v, _v, _v]
         L.tmf_last_error.restype = C.c_char_p
         L.tmf_version.restype = C.c_char_p
         for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
@@ -111,7 +116,8 @@ def lib():
                      "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction",
                      "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle", "tmf_ipc_open_handle",
                      "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create", "tmf_transfer_destroy", "tmf_prolongate",
-                     "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby"):
+                     "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby", "tmf_apply_f32", "tmf_prolongate_f32",
+                     "tmf_restrict_f32", "tmf_chebyshev_step_f32", "tmf_vec_axpby_f32"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -122,7 +128,8 @@ EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_app
             "tmf_build_faces", "tmf_build_cg_dofs", "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update",
             "tmf_pcg_direction", "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle",
             "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create", "tmf_transfer_destroy",
-            "tmf_prolongate", "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby", "tmf_last_error",
+            "tmf_prolongate", "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby", "tmf_apply_f32",
+            "tmf_prolongate_f32", "tmf_restrict_f32", "tmf_chebyshev_step_f32", "tmf_vec_axpby_f32", "tmf_last_error",
             "tmf_version")
 
 

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/tetmf_b200.h"
+#include "cell_f32_kernel.cuh"
 #include "cell_kernel.cuh"
 #include "face_kernel.cuh"
 #include "launch.h"
@@ -479,6 +480,11 @@ struct tmf_plan {
   double* bf_geo = nullptr;
   int64_t n_bf_batches = 0, n_bf_chunks = 0;
   // staging for host applies / solver scratch
+  // fp32 mirror for the mixed-precision multigrid (flags bit 20, CG Laplace): modal rows
+  // E'[m][k][0..NP) as float4 and per-cell G as 8 floats (cell_f32_kernel.cuh)
+  float4* f32_rows = nullptr;
+  float* f32_geo = nullptr;
+  int f32_M = 0;
   double* stage_u = nullptr;
   double* stage_y = nullptr;
   double* pcg_buf = nullptr;
@@ -547,7 +553,7 @@ struct tmf_plan {
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
-                    (void*)pmeta, (void*)prec,
+                    (void*)pmeta, (void*)prec, (void*)f32_rows, (void*)f32_geo,
                     (void*)peer_u_tab, (void*)peer_y_tab, (void*)ghost_rank, (void*)ghost_index})
       if (p) cudaFree(p);
   }
@@ -985,6 +991,27 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     if ((rc = upload(&P->diag_S, S.data(), S.size(), &total))) return bail(rc);
   }
 
+  // fp32 mirror (flags bit 20): the modal rows of the reference tables and G in fp32
+  if ((d->flags >> 20) & 1) {
+    if (dg || P->mass || P->nc != 1 || P->kind != TMF_CG_LAPLACE)
+      return bail(fail(TMF_EINVAL, "the fp32 mirror is for scalar CG Laplace plans only"));
+    const int N = P->N, p = P->degree, M = p * (p + 1) * (p + 2) / 6, NP = (N + 3) & ~3;
+    std::vector<double> E;
+    if (!build_modal_cell_tables(N, P->Q, M, d->grad_matrix, d->cell_weights, E))
+      return bail(fail(TMF_EINVAL, "fp32 mirror: gradient tables without the P_{p-1} rank structure"));
+    std::vector<float> rows((size_t)M * 3 * NP, 0.0f);
+    for (int m = 0; m < M; ++m)
+      for (int k = 0; k < 3; ++k)
+        for (int j = 0; j < N; ++j) rows[((size_t)m * 3 + k) * NP + j] = (float)E[(size_t)(3 * m + k) * N + j];
+    TMF_CUDA(cudaMalloc(&P->f32_rows, rows.size() * sizeof(float)));
+    TMF_CUDA(cudaMemcpy(P->f32_rows, rows.data(), rows.size() * sizeof(float), cudaMemcpyHostToDevice));
+    TMF_CUDA(cudaMalloc(&P->f32_geo, sizeof(float) * 8 * P->n_cells));
+    total += rows.size() * sizeof(float) + sizeof(float) * 8 * P->n_cells;
+    tmf::geo_to_f32_kernel<<<P->n_sm * 8, 256>>>(P->cell_geo, P->f32_geo, 8 * P->n_cells);
+    TMF_CUDA(cudaGetLastError());
+    P->f32_M = M;
+  }
+
   // face tables -> fragments per (lf, code) in the face frame, face batches
   if (faces) {
     const int N = P->N, QF = P->QF;
@@ -1315,6 +1342,32 @@ int tmf_apply(tmf_plan* P, const double* u, double* y, void* stream) {
   if (P->peer.u && u != P->peer_self_u) return fail(TMF_EINVAL, "u must be this rank's registered buffer");
   TMF_CUDA(cudaSetDevice(P->dev));
   return launch_apply(P, u, y, (cudaStream_t)stream, nullptr);
+}
+
+int tmf_apply_f32(tmf_plan* P, const float* u, float* y, void* stream) {
+  if (!P || !u || !y) return fail(TMF_EINVAL, "null argument");
+  if (u == y) return fail(TMF_EINVAL, "u and y must not alias");
+  if (!P->f32_rows) return fail(TMF_EINVAL, "plan was created without the fp32 mirror (flags bit 20)");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  const cudaStream_t st = (cudaStream_t)stream;
+  TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * P->n_global, st));
+  const int block = 256;
+  int64_t grid = (P->n_cells + block - 1) / block;
+  if (grid > (int64_t)P->n_sm * 8) grid = (int64_t)P->n_sm * 8;
+  const float4* g4 = reinterpret_cast<const float4*>(P->f32_geo);
+  switch (P->N) {
+    case 4: tmf::cell_f32_kernel<4, 1, block><<<(unsigned)grid, block, 0, st>>>(u, y, P->dofs, g4, P->f32_rows, P->n_cells); break;
+    case 10: tmf::cell_f32_kernel<10, 4, block><<<(unsigned)grid, block, 0, st>>>(u, y, P->dofs, g4, P->f32_rows, P->n_cells); break;
+    case 20: tmf::cell_f32_kernel<20, 10, block><<<(unsigned)grid, block, 0, st>>>(u, y, P->dofs, g4, P->f32_rows, P->n_cells); break;
+    case 35: tmf::cell_f32_kernel<35, 20, block><<<(unsigned)grid, block, 0, st>>>(u, y, P->dofs, g4, P->f32_rows, P->n_cells); break;
+    default: return fail(TMF_EINVAL, "fp32 mirror: unsupported degree");
+  }
+  TMF_CUDA(cudaGetLastError());
+  if (P->n_fix) {
+    tmf::fixup_f32_kernel<<<P->n_sm * 4, 256, 0, st>>>(u, y, P->fix_list, P->n_fix);
+    TMF_CUDA(cudaGetLastError());
+  }
+  return TMF_OK;
 }
 
 int tmf_apply_host(tmf_plan* P, const double* u_host, double* y_host) {

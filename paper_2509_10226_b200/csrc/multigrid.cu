@@ -43,29 +43,30 @@ int mg_fail(int code, const std::string& m) { return tmf_internal_set_error(code
 
 // fdofs: fine DoF id (owned, free), ~id (owned, Dirichlet) or kNotOwned
 // cdofs: coarse DoF id, or ~id for a coarse Dirichlet DoF
-template <int NC>
+template <int NC, typename T>
 __global__ void prolongate_kernel(const int* __restrict__ fdofs, const int* __restrict__ cdofs,
-                                  const double* __restrict__ Pg, int nf, int64_t n_cells,
-                                  const double* __restrict__ xc, double* __restrict__ xf, int add) {
-  extern __shared__ double sP[];
+                                  const T* __restrict__ Pg, int nf, int64_t n_cells,
+                                  const T* __restrict__ xc, T* __restrict__ xf, int add) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sP = reinterpret_cast<T*>(smraw);
   for (int i = threadIdx.x; i < nf * NC; i += blockDim.x) sP[i] = Pg[i];
   __syncthreads();
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells;
        c += (int64_t)gridDim.x * blockDim.x) {
-    double v[NC];
+    T v[NC];
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       const int g = __ldg(cdofs + c * NC + j);
-      v[j] = g >= 0 ? __ldg(xc + g) : 0.0;
+      v[j] = g >= 0 ? __ldg(xc + g) : T(0);
     }
     for (int i = 0; i < nf; ++i) {
       const int f = __ldg(fdofs + c * nf + i);
       if (f == kNotOwned) continue;
       if (f < 0) {
-        if (!add) xf[~f] = 0.0;
+        if (!add) xf[~f] = T(0);
         continue;
       }
-      double s = 0.0;
+      T s = T(0);
 #pragma unroll
       for (int j = 0; j < NC; ++j) s = fma(sP[i * NC + j], v[j], s);
       xf[f] = add ? xf[f] + s : s;
@@ -73,53 +74,56 @@ __global__ void prolongate_kernel(const int* __restrict__ fdofs, const int* __re
   }
 }
 
-template <int NC>
+template <int NC, typename T>
 __global__ void restrict_kernel(const int* __restrict__ fdofs, const int* __restrict__ cdofs,
-                                const double* __restrict__ Pg, int nf, int64_t n_cells,
-                                const double* __restrict__ rf, double* __restrict__ rc) {
-  extern __shared__ double sP[];
+                                const T* __restrict__ Pg, int nf, int64_t n_cells,
+                                const T* __restrict__ rf, T* __restrict__ rc) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sP = reinterpret_cast<T*>(smraw);
   for (int i = threadIdx.x; i < nf * NC; i += blockDim.x) sP[i] = Pg[i];
   __syncthreads();
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells;
        c += (int64_t)gridDim.x * blockDim.x) {
-    double acc[NC];
+    T acc[NC];
 #pragma unroll
-    for (int j = 0; j < NC; ++j) acc[j] = 0.0;
+    for (int j = 0; j < NC; ++j) acc[j] = T(0);
     for (int i = 0; i < nf; ++i) {
       const int f = __ldg(fdofs + c * nf + i);
       if (f < 0) continue;   // not owned, or Dirichlet
-      const double r = __ldg(rf + f);
+      const T r = __ldg(rf + f);
 #pragma unroll
       for (int j = 0; j < NC; ++j) acc[j] = fma(sP[i * NC + j], r, acc[j]);
     }
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       const int g = __ldg(cdofs + c * NC + j);
-      if (g >= 0 && acc[j] != 0.0) atomicAdd(rc + g, acc[j]);
+      if (g >= 0 && acc[j] != T(0)) atomicAdd(rc + g, acc[j]);
     }
   }
 }
 
 // first == 1 (x = 0 on entry, ax unused):  d = c2 D^-1 b;  x = d
 // otherwise:                               d = c1 d + c2 D^-1 (b - ax);  x += d
-__global__ void chebyshev_kernel(int64_t n, const double* __restrict__ ax, const double* __restrict__ b,
-                                 const double* __restrict__ dinv, double* __restrict__ x,
-                                 double* __restrict__ d, double c1, double c2, int first) {
+template <typename T>
+__global__ void chebyshev_kernel(int64_t n, const T* __restrict__ ax, const T* __restrict__ b,
+                                 const T* __restrict__ dinv, T* __restrict__ x,
+                                 T* __restrict__ d, T c1, T c2, int first) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (first) {
-      const double di = c2 * dinv[i] * b[i];
+      const T di = c2 * dinv[i] * b[i];
       d[i] = di;
       x[i] = di;
     } else {
-      const double di = c1 * d[i] + c2 * dinv[i] * (b[i] - ax[i]);
+      const T di = c1 * d[i] + c2 * dinv[i] * (b[i] - ax[i]);
       d[i] = di;
       x[i] += di;
     }
   }
 }
 
-__global__ void axpby_kernel(int64_t n, double alpha, const double* __restrict__ x, double beta,
-                             const double* __restrict__ y, double* __restrict__ out) {
+template <typename T>
+__global__ void axpby_kernel(int64_t n, T alpha, const T* __restrict__ x, T beta,
+                             const T* __restrict__ y, T* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = alpha * x[i] + beta * y[i];
 }
@@ -141,6 +145,7 @@ struct tmf_transfer {
   int* fdofs = nullptr;
   int* cdofs = nullptr;
   double* P = nullptr;
+  float* P32 = nullptr;
 };
 
 extern "C" {
@@ -196,6 +201,9 @@ int tmf_transfer_create(const tmf_transfer_desc* d, tmf_transfer** out) {
   if (e == cudaSuccess) e = cudaMemcpy(t->fdofs, f.data(), f.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(t->cdofs, c.data(), c.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(t->P, d->interp, (size_t)nf * nc * sizeof(double), cudaMemcpyHostToDevice);
+  std::vector<float> p32(d->interp, d->interp + (size_t)nf * nc);
+  if (e == cudaSuccess) e = cudaMalloc(&t->P32, p32.size() * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpy(t->P32, p32.data(), p32.size() * sizeof(float), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     tmf_transfer_destroy(t);
     return mg_fail(TMF_ECUDA, std::string("transfer upload: ") + cudaGetErrorString(e));
@@ -210,70 +218,108 @@ int tmf_transfer_destroy(tmf_transfer* t) {
   cudaFree(t->fdofs);
   cudaFree(t->cdofs);
   cudaFree(t->P);
+  cudaFree(t->P32);
   delete t;
   return TMF_OK;
 }
 
-int tmf_prolongate(tmf_transfer* t, const double* xc, double* xf, int add, void* stream) {
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+int prolongate_t(tmf_transfer* t, const T* Pd, const T* xc, T* xf, int add, void* stream) {
   if (!t || !xc || !xf) return mg_fail(TMF_EINVAL, "null argument");
   MG_CUDA(cudaSetDevice(t->device));
   const cudaStream_t st = (cudaStream_t)stream;
   const int block = 256;
   int64_t grid = (t->n_cells + block - 1) / block;
   if (grid > (int64_t)t->sms * 16) grid = (int64_t)t->sms * 16;
-  const size_t smem = (size_t)t->nf * t->nc * sizeof(double);
-  if (t->nc == 4)
-    prolongate_kernel<4><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
-  else if (t->nc == 10)
-    prolongate_kernel<10><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
-  else if (t->nc == 20)
-    prolongate_kernel<20><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
-  else
-    prolongate_kernel<35><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, xc, xf, add);
+  const size_t smem = (size_t)t->nf * t->nc * sizeof(T);
+  const unsigned g = (unsigned)grid;
+  switch (t->nc) {
+    case 4: prolongate_kernel<4, T><<<g, block, smem, st>>>(t->fdofs, t->cdofs, Pd, t->nf, t->n_cells, xc, xf, add); break;
+    case 10: prolongate_kernel<10, T><<<g, block, smem, st>>>(t->fdofs, t->cdofs, Pd, t->nf, t->n_cells, xc, xf, add); break;
+    case 20: prolongate_kernel<20, T><<<g, block, smem, st>>>(t->fdofs, t->cdofs, Pd, t->nf, t->n_cells, xc, xf, add); break;
+    default: prolongate_kernel<35, T><<<g, block, smem, st>>>(t->fdofs, t->cdofs, Pd, t->nf, t->n_cells, xc, xf, add);
+  }
   MG_CUDA(cudaGetLastError());
   return TMF_OK;
 }
 
-int tmf_restrict(tmf_transfer* t, const double* rf, double* rc, void* stream) {
+template <typename T>
+int restrict_t(tmf_transfer* t, const T* Pd, const T* rf, T* rc, void* stream) {
   if (!t || !rf || !rc) return mg_fail(TMF_EINVAL, "null argument");
   MG_CUDA(cudaSetDevice(t->device));
   const cudaStream_t st = (cudaStream_t)stream;
-  MG_CUDA(cudaMemsetAsync(rc, 0, t->n_coarse * sizeof(double), st));
+  MG_CUDA(cudaMemsetAsync(rc, 0, t->n_coarse * sizeof(T), st));
   const int block = 256;
   int64_t grid = (t->n_cells + block - 1) / block;
   if (grid > (int64_t)t->sms * 16) grid = (int64_t)t->sms * 16;
-  const size_t smem = (size_t)t->nf * t->nc * sizeof(double);
-  if (t->nc == 4)
-    restrict_kernel<4><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
-  else if (t->nc == 10)
-    restrict_kernel<10><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
-  else if (t->nc == 20)
-    restrict_kernel<20><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
-  else
-    restrict_kernel<35><<<(unsigned)grid, block, smem, st>>>(t->fdofs, t->cdofs, t->P, t->nf, t->n_cells, rf, rc);
+  const size_t smem = (size_t)t->nf * t->nc * sizeof(T);
+  const unsigned g = (unsigned)grid;
+  switch (t->nc) {
+    case 4: restrict_kernel<4, T><<<g, block, smem, st>>>(t->fdofs, t->cdofs, Pd, t->nf, t->n_cells, rf, rc); break;
+    case 10: restrict_kernel<10, T><<<g, block, smem, st>>>(t->fdofs, t->cdofs, Pd, t->nf, t->n_cells, rf, rc); break;
+    case 20: restrict_kernel<20, T><<<g, block, smem, st>>>(t->fdofs, t->cdofs, Pd, t->nf, t->n_cells, rf, rc); break;
+    default: restrict_kernel<35, T><<<g, block, smem, st>>>(t->fdofs, t->cdofs, Pd, t->nf, t->n_cells, rf, rc);
+  }
   MG_CUDA(cudaGetLastError());
   return TMF_OK;
 }
 
-int tmf_chebyshev_step(int64_t n, const double* ax, const double* b, const double* dinv, double* x,
-                       double* d, double c1, double c2, void* stream) {
+template <typename T>
+int chebyshev_t(int64_t n, const T* ax, const T* b, const T* dinv, T* x, T* d, T c1, T c2, void* stream) {
   if (n < 0 || !b || !dinv || !x || !d) return mg_fail(TMF_EINVAL, "bad argument");
   int dev = 0;
   MG_CUDA(cudaGetDevice(&dev));
-  chebyshev_kernel<<<sm_count(dev) * 4, 512, 0, (cudaStream_t)stream>>>(n, ax, b, dinv, x, d, c1, c2,
-                                                                         ax == nullptr ? 1 : 0);
+  chebyshev_kernel<T><<<sm_count(dev) * 4, 512, 0, (cudaStream_t)stream>>>(n, ax, b, dinv, x, d, c1, c2,
+                                                                            ax == nullptr ? 1 : 0);
   MG_CUDA(cudaGetLastError());
   return TMF_OK;
 }
 
-int tmf_vec_axpby(int64_t n, double alpha, const double* x, double beta, const double* y, double* out,
-                  void* stream) {
+template <typename T>
+int axpby_t(int64_t n, T alpha, const T* x, T beta, const T* y, T* out, void* stream) {
   if (n < 0 || !x || !y || !out) return mg_fail(TMF_EINVAL, "bad argument");
   int dev = 0;
   MG_CUDA(cudaGetDevice(&dev));
-  axpby_kernel<<<sm_count(dev) * 4, 512, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y, out);
+  axpby_kernel<T><<<sm_count(dev) * 4, 512, 0, (cudaStream_t)stream>>>(n, alpha, x, beta, y, out);
   MG_CUDA(cudaGetLastError());
   return TMF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tmf_prolongate(tmf_transfer* t, const double* xc, double* xf, int add, void* stream) {
+  return prolongate_t<double>(t, t ? t->P : nullptr, xc, xf, add, stream);
+}
+int tmf_restrict(tmf_transfer* t, const double* rf, double* rc, void* stream) {
+  return restrict_t<double>(t, t ? t->P : nullptr, rf, rc, stream);
+}
+int tmf_prolongate_f32(tmf_transfer* t, const float* xc, float* xf, int add, void* stream) {
+  return prolongate_t<float>(t, t ? t->P32 : nullptr, xc, xf, add, stream);
+}
+int tmf_restrict_f32(tmf_transfer* t, const float* rf, float* rc, void* stream) {
+  return restrict_t<float>(t, t ? t->P32 : nullptr, rf, rc, stream);
+}
+int tmf_chebyshev_step(int64_t n, const double* ax, const double* b, const double* dinv, double* x,
+                       double* d, double c1, double c2, void* stream) {
+  return chebyshev_t<double>(n, ax, b, dinv, x, d, c1, c2, stream);
+}
+int tmf_chebyshev_step_f32(int64_t n, const float* ax, const float* b, const float* dinv, float* x,
+                           float* d, float c1, float c2, void* stream) {
+  return chebyshev_t<float>(n, ax, b, dinv, x, d, c1, c2, stream);
+}
+int tmf_vec_axpby(int64_t n, double alpha, const double* x, double beta, const double* y, double* out,
+                  void* stream) {
+  return axpby_t<double>(n, alpha, x, beta, y, out, stream);
+}
+int tmf_vec_axpby_f32(int64_t n, float alpha, const float* x, float beta, const float* y, float* out,
+                      void* stream) {
+  return axpby_t<float>(n, alpha, x, beta, y, out, stream);
 }
 
 }  // extern "C"

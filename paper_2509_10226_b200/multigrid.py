@@ -20,8 +20,11 @@ the fp64 p-multigrid part of it, built on the B200 operator apply:
 * outer loop: flexible (Polak-Ribiere) PCG, since a fixed-count inner CG makes the
   V-cycle slightly nonlinear.
 
-Not built (out of scope this round): fp32 levels (mixed precision), h-coarsening
-below P1, Chebyshev on the coarse level.  No CPU fallback: every vector operation
+``precision="mixed"``: the whole V-cycle in fp32 (``tmf_apply_f32``: the modal cell form on
+FFMA, fp32 transfers / Chebyshev steps / coarse Jacobi-PCG) inside the fp64 flexible PCG,
+as the paper does ("the multigrid V-cycle runs in single precision").
+
+Not built (out of scope this round): h-coarsening below P1, Chebyshev on the coarse level.  No CPU fallback: every vector operation
 is a native kernel or a device tensor op; the CPU restatement is
 ``oracle/ref_multigrid.py`` (tests only).
 """
@@ -143,12 +146,22 @@ class Transfer:
         self.n_fine, self.n_coarse = fine_dm.n_scalar_dofs, coarse_dm.n_scalar_dofs
 
     def prolongate(self, xc, xf, add: bool = False, stream: int = 0):
-        """xf = P xc (add: xf += P xc), device tensors."""
-        _lib.check(_lib.lib().tmf_prolongate(self._t, _vp(xc), _vp(xf), int(bool(add)), C.c_void_p(stream)))
+        """xf = P xc (add: xf += P xc), device tensors (both float64 or both float32)."""
+        import torch
+
+        f = _lib.lib().tmf_prolongate_f32 if xc.dtype == torch.float32 else _lib.lib().tmf_prolongate
+        if xf.dtype != xc.dtype:
+            raise ValueError("prolongate: mixed dtypes")
+        _lib.check(f(self._t, _vp(xc), _vp(xf), int(bool(add)), C.c_void_p(stream)))
 
     def restrict(self, rf, rc, stream: int = 0):
-        """rc = P^T rf, device tensors."""
-        _lib.check(_lib.lib().tmf_restrict(self._t, _vp(rf), _vp(rc), C.c_void_p(stream)))
+        """rc = P^T rf, device tensors (both float64 or both float32)."""
+        import torch
+
+        f = _lib.lib().tmf_restrict_f32 if rf.dtype == torch.float32 else _lib.lib().tmf_restrict
+        if rc.dtype != rf.dtype:
+            raise ValueError("restrict: mixed dtypes")
+        _lib.check(f(self._t, _vp(rf), _vp(rc), C.c_void_p(stream)))
 
     def close(self):
         if self._t:
@@ -187,15 +200,24 @@ class PMultigrid:
 
     def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 2,
                  smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
-                 lmax=None, config=None, seed: int = 0, fine_operator=None):
+                 lmax=None, config=None, seed: int = 0, fine_operator=None, precision: str = "f64"):
         import torch
 
         from . import operator as op
 
+        if precision not in ("f64", "mixed"):
+            raise ValueError("precision must be 'f64' or 'mixed' (fp32 V-cycle, fp64 outer CG)")
+        if precision == "mixed" and fine_operator is not None:
+            raise ValueError("the mixed-precision V-cycle has fp32 operators for the CG levels only")
+        self.mixed = precision == "mixed"
         degrees = tuple(int(p) for p in degrees)
         if len(degrees) < 2 or any(a <= b for a, b in zip(degrees, degrees[1:])):
             raise ValueError("degrees must be strictly decreasing, at least two levels")
         self.config = config or op.OperatorConfig()
+        if self.mixed:
+            import dataclasses
+
+            self.config = dataclasses.replace(self.config, f32_mirror=True)
         dev = int(self.config.device)
         self.device = torch.device(f"cuda:{dev}")
         self.smoothing_degree, self.smoothing_range = int(smoothing_degree), float(smoothing_range)
@@ -221,13 +243,16 @@ class PMultigrid:
                 dinv = 1.0 / A.diagonal()
             lv = _Level(p, dm, A, dinv, 0.0, [])
             n = dm.n_global_dofs
-            lv.x, lv.b, lv.r, lv.d, lv.ax = (torch.zeros(n, dtype=torch.float64, device=self.device)
-                                             for _ in range(5))
+            vt = torch.float32 if self.mixed else torch.float64
+            lv.x, lv.b, lv.r, lv.d, lv.ax = (torch.zeros(n, dtype=vt, device=self.device) for _ in range(5))
             if i < len(specs) - 1:
                 given = None if lmax is None else float(lmax[i])
                 lv.lmax = given if given is not None else 1.1 * self.estimate_lmax(lv, eig_iterations, seed)
                 lv.coeffs = chebyshev_coefficients(lv.lmax, self.smoothing_range, self.smoothing_degree)
             self.levels.append(lv)
+        if self.mixed:   # the fp64 diagonals served the eigenvalue estimates; the cycle runs in fp32
+            for lv in self.levels:
+                lv.dinv = lv.dinv.to(torch.float32)
         self.transfers = [Transfer(self.levels[i].dm, self.levels[i + 1].dm, dev)
                           for i in range(len(self.levels) - 1)]
         self.n_global_dofs = self.levels[0].dm.n_global_dofs
@@ -278,33 +303,67 @@ class PMultigrid:
         return torch.cuda.current_stream().cuda_stream
 
     # ------------------------------------------------------------------ cycle
+    def _apply(self, lv, x, y, st):
+        if self.mixed:
+            lv.A.apply_f32(x, out=y, stream=st)
+        else:
+            lv.A.apply_into(x.data_ptr(), y.data_ptr(), st)
+
     def _smooth(self, lv, first: bool):
         """Chebyshev-Jacobi on A x = b (lv.x, lv.b); first: x = 0 on entry."""
         L = _lib.lib()
-        st = C.c_void_p(self._st())
+        stp = self._st()
+        st = C.c_void_p(stp)
         n = lv.dm.n_global_dofs
+        step = L.tmf_chebyshev_step_f32 if self.mixed else L.tmf_chebyshev_step
         for k, (c1, c2) in enumerate(lv.coeffs):
             if k == 0 and first:
-                _lib.check(L.tmf_chebyshev_step(n, None, _vp(lv.b), _vp(lv.dinv), _vp(lv.x), _vp(lv.d),
-                                                c1, c2, st))
+                _lib.check(step(n, None, _vp(lv.b), _vp(lv.dinv), _vp(lv.x), _vp(lv.d), c1, c2, st))
                 continue
-            lv.A.apply_into(lv.x.data_ptr(), lv.ax.data_ptr(), self._st())
-            _lib.check(L.tmf_chebyshev_step(n, _vp(lv.ax), _vp(lv.b), _vp(lv.dinv), _vp(lv.x), _vp(lv.d),
-                                            c1, c2, st))
+            self._apply(lv, lv.x, lv.ax, stp)
+            _lib.check(step(n, _vp(lv.ax), _vp(lv.b), _vp(lv.dinv), _vp(lv.x), _vp(lv.d), c1, c2, st))
+
+    def _coarse_f32(self, lv):
+        """fp32 Jacobi-PCG (x0 = 0, fixed iteration count) with the scalars on the device."""
+        import torch
+
+        st = self._st()
+        x, b, dinv, q = lv.x, lv.b, lv.dinv, lv.ax
+        x.zero_()
+        r = b.clone()
+        z = r * dinv
+        p = z.clone()
+        rz = torch.dot(r, z)
+        zero = torch.zeros((), dtype=torch.float32, device=self.device)
+        for _ in range(self.coarse_iterations):
+            self._apply(lv, p, q, st)
+            pq = torch.dot(p, q)
+            alpha = torch.where(pq != 0, rz / pq, zero)
+            x.add_(alpha * p)
+            r.sub_(alpha * q)
+            torch.mul(r, dinv, out=z)
+            rz_new = torch.dot(r, z)
+            beta = torch.where(rz != 0, rz_new / rz, zero)
+            p = z + beta * p
+            rz = rz_new
 
     def _cycle(self, i: int):
         from .solvers import jacobi_pcg
 
         lv = self.levels[i]
         if i == len(self.levels) - 1:
-            x, _ = jacobi_pcg(lv.A, lv.b, self.coarse_iterations)
-            lv.x.copy_(x)
+            if self.mixed:
+                self._coarse_f32(lv)
+            else:
+                x, _ = jacobi_pcg(lv.A, lv.b, self.coarse_iterations)
+                lv.x.copy_(x)
             return
         st = self._st()
+        L = _lib.lib()
         self._smooth(lv, first=True)
-        lv.A.apply_into(lv.x.data_ptr(), lv.ax.data_ptr(), st)
-        _lib.check(_lib.lib().tmf_vec_axpby(lv.dm.n_global_dofs, 1.0, _vp(lv.b), -1.0, _vp(lv.ax), _vp(lv.r),
-                                            C.c_void_p(st)))
+        self._apply(lv, lv.x, lv.ax, st)
+        axpby = L.tmf_vec_axpby_f32 if self.mixed else L.tmf_vec_axpby
+        _lib.check(axpby(lv.dm.n_global_dofs, 1.0, _vp(lv.b), -1.0, _vp(lv.ax), _vp(lv.r), C.c_void_p(st)))
         nxt = self.levels[i + 1]
         self.transfers[i].restrict(lv.r, nxt.b, st)
         self._cycle(i + 1)
@@ -312,14 +371,13 @@ class PMultigrid:
         self._smooth(lv, first=False)
 
     def vcycle(self, r, out=None):
-        """z = V r (one V-cycle from a zero initial guess); device tensors."""
-        import torch
-
+        """z = V r (one V-cycle from a zero initial guess); device tensors.  Mixed precision:
+        r is rounded to fp32, the cycle runs in fp32 and z is returned in r's dtype."""
         lv = self.levels[0]
         lv.b.copy_(r)
         self._cycle(0)
         if out is None:
-            return lv.x.clone()
+            return lv.x.to(r.dtype, copy=True)
         out.copy_(lv.x)
         return out
 

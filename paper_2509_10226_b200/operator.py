@@ -62,6 +62,7 @@ class OperatorConfig:
     #                              reference tensor) | modal (points loop on the M = dim P_{p-1} exact modes)
     cell_patches: str = "auto"   # B200 CG warp-patch assembly: auto (= off, measured slower) | off | on
     face_engine: str = "auto"    # B200 faces: auto (modal at P2-P4) | quadrature (points) | tensor (interior) | modal
+    f32_mirror: bool = False     # B200 CG Laplace: also build the fp32 apply (apply_f32; mixed-precision multigrid)
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -199,7 +200,8 @@ class _B200Operator:
             ((_ENGINES[getattr(self.config, "cell_engine", "auto")] & 3) << 13) | \
             ((_ENGINES[getattr(self.config, "cell_engine", "auto")] >> 2) << 19) | \
             (_PATCHES[getattr(self.config, "cell_patches", "auto")] << 15) | \
-            (_FACE_ENGINES[getattr(self.config, "face_engine", "auto")] << 17)
+            (_FACE_ENGINES[getattr(self.config, "face_engine", "auto")] << 17) | \
+            ((1 if getattr(self.config, "f32_mirror", False) else 0) << 20)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))
@@ -276,6 +278,20 @@ class _B200Operator:
         """Raw device-pointer apply (y overwritten), ordered on ``stream``."""
         _lib.check(_lib.lib().tmf_apply(self._plan, C.c_void_p(u_ptr), C.c_void_p(y_ptr), C.c_void_p(stream)))
         self._count()
+
+    def apply_f32(self, u, out=None, stream: int | None = None):
+        """y = A u in single precision (CUDA float32 tensors; plans built with
+        ``OperatorConfig(f32_mirror=True)``): the mixed-precision V-cycle's operator."""
+        import torch
+
+        self._check_length(u)
+        if u.dtype != torch.float32 or not u.is_cuda:
+            raise ValueError("apply_f32 needs a CUDA float32 tensor")
+        y = torch.empty_like(u) if out is None else out
+        st = torch.cuda.current_stream(u.device).cuda_stream if stream is None else stream
+        _lib.check(_lib.lib().tmf_apply_f32(self._plan, C.c_void_p(u.data_ptr()), C.c_void_p(y.data_ptr()),
+                                            C.c_void_p(st)))
+        return y
 
     def timed(self, u_ptr: int, y_ptr: int, stream: int = 0, reps: int = 1):
         """(total, cell, face, fixup) ms per apply from CUDA events on ``stream``."""

@@ -232,3 +232,104 @@ def test_indefinite_operator_is_reported():
     B = op.DgSipgOperator(m, dm, A.geo, A.basis, sipg, dirichlet_ids=range(6))
     with pytest.raises(ValueError, match="positive definite"):
         PMultigrid(m, (2, 1), fine_operator=B, eig_iterations=60)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("dirichlet", [False, True])
+def test_apply_f32_matches_fp64(p, dirichlet):
+    """fp32 mirror of the CG Laplace apply (modal form on FFMA) vs the fp64 apply and the oracle."""
+    import torch
+
+    from paper_2509_10226_b200 import basis as B, mesh as M, operator as op, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+
+    m = M.kuhn_cube_mesh(4, seed=0)
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    geo = GeometryData("affine", cr, fr, None, None, None, None)
+    dm = _dm(m, p, tuple(range(6)) if dirichlet else ())
+    A = op.CgPoissonOperator(m, dm, geo, bas, op.OperatorConfig(f32_mirror=True))
+    u = np.random.default_rng(2).uniform(-1, 1, dm.n_global_dofs)
+    y64 = A.apply(u)
+    y32 = A.apply_f32(torch.from_numpy(u).float().cuda()).double().cpu().numpy()
+    assert rel_l2(y32, y64) <= 2e-6
+    yr = ref_apply.cg_apply(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask, bas.grad_matrix, cr.weights, u)
+    assert rel_l2(y64, yr) <= 1e-12
+    if dirichlet:
+        assert np.array_equal(y32[dm.dirichlet_mask], u.astype(np.float32).astype(np.float64)[dm.dirichlet_mask])
+
+
+def test_apply_f32_needs_the_mirror():
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200 import basis as B, operator as op, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+
+    m = M.kuhn_cube_mesh(2, seed=0)
+    cr, fr = Q.make_cell_quadrature(2), Q.make_face_quadrature(2)
+    bas = B.tabulate_basis(2, cr, fr)
+    geo = GeometryData("affine", cr, fr, None, None, None, None)
+    dm = _dm(m, 2, ())
+    A = op.CgPoissonOperator(m, dm, geo, bas)
+    with pytest.raises(ValueError, match="fp32 mirror"):
+        A.apply_f32(torch.zeros(dm.n_global_dofs, dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        A.apply_f32(torch.zeros(dm.n_global_dofs, dtype=torch.float64, device="cuda"))
+    from paper_2509_10226_b200 import dofmap as D
+
+    ddm = D.build_dof_map(m, 2, "dg")
+    with pytest.raises(ValueError, match="fp32 mirror"):
+        op.DgSipgOperator(m, ddm, geo, bas, op.baseline_sipg_tau(m, 2, 0.5), op.OperatorConfig(f32_mirror=True))
+
+
+def test_transfers_f32_match_fp64():
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import Transfer
+
+    m = M.kuhn_cube_mesh(4, seed=0)
+    dmf, dmc = _dm(m, 3, tuple(range(6))), _dm(m, 1, tuple(range(6)))
+    T = Transfer(dmf, dmc)
+    rng = np.random.default_rng(4)
+    xc = torch.from_numpy(rng.uniform(-1, 1, dmc.n_scalar_dofs)).cuda()
+    rf = torch.from_numpy(rng.uniform(-1, 1, dmf.n_scalar_dofs)).cuda()
+    xf64, xf32 = torch.empty(dmf.n_scalar_dofs, dtype=torch.float64, device="cuda"), \
+        torch.empty(dmf.n_scalar_dofs, dtype=torch.float32, device="cuda")
+    T.prolongate(xc, xf64)
+    T.prolongate(xc.float(), xf32)
+    assert rel_l2(xf32.double().cpu().numpy(), xf64.cpu().numpy()) <= 1e-6
+    rc64, rc32 = torch.empty(dmc.n_scalar_dofs, dtype=torch.float64, device="cuda"), \
+        torch.empty(dmc.n_scalar_dofs, dtype=torch.float32, device="cuda")
+    T.restrict(rf, rc64)
+    T.restrict(rf.float(), rc32)
+    assert rel_l2(rc32.double().cpu().numpy(), rc64.cpu().numpy()) <= 1e-6
+    with pytest.raises(ValueError):
+        T.restrict(rf, rc32)
+
+
+def test_mixed_precision_multigrid_converges_like_fp64():
+    """fp32 V-cycle inside the fp64 flexible PCG reaches 1e-10 (far below fp32 round-off) in
+    about the fp64 iteration count."""
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import PMultigrid
+
+    m = M.kuhn_cube_mesh(6, seed=0)
+    mg64 = PMultigrid(m, (3, 2, 1), coarse_iterations=30)
+    mg32 = PMultigrid(m, (3, 2, 1), coarse_iterations=30, precision="mixed")
+    assert mg32.levels[0].x.dtype == torch.float32
+    dm = mg64.levels[0].dm
+    b = np.where(dm.dirichlet_mask, 0.0, np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs))
+    bt = torch.from_numpy(b).cuda()
+    x64, h64 = mg64.solve(bt, tol=1e-10, maxiter=60)
+    x32, h32 = mg32.solve(bt, tol=1e-10, maxiter=60)
+    assert h32[-1] <= 1e-10 * h32[0]
+    assert len(h32) <= len(h64) + 3
+    assert rel_l2(x32.cpu().numpy(), x64.cpu().numpy()) <= 1e-8
+    z = mg32.vcycle(bt)
+    assert z.dtype == torch.float64
+    with pytest.raises(ValueError):
+        PMultigrid(m, (2, 1), precision="half")
