@@ -200,7 +200,8 @@ class PMultigrid:
 
     def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 2,
                  smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
-                 lmax=None, config=None, seed: int = 0, fine_operator=None, precision: str = "f64"):
+                 lmax=None, config=None, seed: int = 0, fine_operator=None, precision: str = "f64",
+                 coarse_matrix: bool = False):
         import torch
 
         from . import operator as op
@@ -253,6 +254,18 @@ class PMultigrid:
         if self.mixed:   # the fp64 diagonals served the eigenvalue estimates; the cycle runs in fp32
             for lv in self.levels:
                 lv.dinv = lv.dinv.to(torch.float32)
+        # matrix-based coarse level (the paper switches to the assembled operator where it is
+        # faster): P1 on the fine mesh has 6 cells per DoF, so its CSR SpMV
+        # (cuSPARSE) moves far fewer bytes than the matrix-free cell loop
+        self.coarse_csr = None
+        if coarse_matrix:
+            from .sparse import assemble_cg_csr
+
+            lv = self.levels[-1]
+            cr, fr = Q.make_cell_quadrature(lv.p), Q.make_face_quadrature(lv.p)
+            A = assemble_cg_csr(mesh, lv.dm, GeometryData("affine", cr, fr, None, None, None, None),
+                                B.tabulate_basis(lv.p, cr, fr), device=self.device)
+            self.coarse_csr = A.to(torch.float32) if self.mixed else A
         self.transfers = [Transfer(self.levels[i].dm, self.levels[i + 1].dm, dev)
                           for i in range(len(self.levels) - 1)]
         self.n_global_dofs = self.levels[0].dm.n_global_dofs
@@ -323,8 +336,9 @@ class PMultigrid:
             self._apply(lv, lv.x, lv.ax, stp)
             _lib.check(step(n, _vp(lv.ax), _vp(lv.b), _vp(lv.dinv), _vp(lv.x), _vp(lv.d), c1, c2, st))
 
-    def _coarse_f32(self, lv):
-        """fp32 Jacobi-PCG (x0 = 0, fixed iteration count) with the scalars on the device."""
+    def _coarse_pcg(self, lv):
+        """Jacobi-PCG in the cycle's precision (x0 = 0, fixed iteration count) with the scalars
+        on the device; the operator is the matrix-free apply or the assembled coarse matrix."""
         import torch
 
         st = self._st()
@@ -334,9 +348,12 @@ class PMultigrid:
         z = r * dinv
         p = z.clone()
         rz = torch.dot(r, z)
-        zero = torch.zeros((), dtype=torch.float32, device=self.device)
+        zero = torch.zeros((), dtype=x.dtype, device=self.device)
         for _ in range(self.coarse_iterations):
-            self._apply(lv, p, q, st)
+            if self.coarse_csr is not None:
+                q = (self.coarse_csr @ p.unsqueeze(1)).squeeze(1)
+            else:
+                self._apply(lv, p, q, st)
             pq = torch.dot(p, q)
             alpha = torch.where(pq != 0, rz / pq, zero)
             x.add_(alpha * p)
@@ -352,8 +369,8 @@ class PMultigrid:
 
         lv = self.levels[i]
         if i == len(self.levels) - 1:
-            if self.mixed:
-                self._coarse_f32(lv)
+            if self.mixed or self.coarse_csr is not None:
+                self._coarse_pcg(lv)
             else:
                 x, _ = jacobi_pcg(lv.A, lv.b, self.coarse_iterations)
                 lv.x.copy_(x)

@@ -333,3 +333,26 @@ def test_mixed_precision_multigrid_converges_like_fp64():
     assert z.dtype == torch.float64
     with pytest.raises(ValueError):
         PMultigrid(m, (2, 1), precision="half")
+
+
+@pytest.mark.parametrize("precision", ["f64", "mixed"])
+def test_matrix_based_coarse_level(precision):
+    """Assembled (cuSPARSE) P1 coarse level: same V-cycle as the matrix-free one up to the
+    coarse solver's round-off, same convergence."""
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import PMultigrid
+
+    m = M.kuhn_cube_mesh(5, seed=0)
+    a = PMultigrid(m, (3, 1), coarse_iterations=20, precision=precision)
+    b_ = PMultigrid(m, (3, 1), coarse_iterations=20, precision=precision, coarse_matrix=True)
+    dm = a.levels[0].dm
+    r = torch.from_numpy(np.where(dm.dirichlet_mask, 0.0,
+                                  np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs))).cuda()
+    za, zb = a.vcycle(r), b_.vcycle(r)
+    tol = 1e-10 if precision == "f64" else 1e-4
+    assert rel_l2(zb.cpu().numpy(), za.cpu().numpy()) <= tol
+    _, ha = a.solve(r, tol=1e-10, maxiter=60)
+    _, hb = b_.solve(r, tol=1e-10, maxiter=60)
+    assert hb[-1] <= 1e-10 * hb[0] and abs(len(ha) - len(hb)) <= 2

@@ -185,7 +185,7 @@ def csr(n=48):
         torch.cuda.empty_cache()
 
 
-def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64"):
+def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False):
     """p-multigrid flexible PCG vs Jacobi-PCG on the C5 problem (CG P3, homogeneous
     Dirichlet, RHS uniform[-1,1]): iterations and device time to ||r|| <= tol ||b||."""
     import torch
@@ -198,7 +198,7 @@ def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64"):
 
     t0 = time.time()
     m = reorder_mesh(M.kuhn_cube_mesh(n, seed=0))
-    mg_ = PMultigrid(m, degrees, coarse_iterations=30, precision=precision)
+    mg_ = PMultigrid(m, degrees, coarse_iterations=30, precision=precision, coarse_matrix=coarse_matrix)
     setup = time.time() - t0
     dm = mg_.levels[0].dm
     nd = dm.n_global_dofs
@@ -234,7 +234,8 @@ def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64"):
                       "precision": "fp32 V-cycle, fp64 outer CG" if precision == "mixed" else "fp64",
                       "ndof": nd, "levels": list(degrees), "lmax": [round(lv.lmax, 4) for lv in mg_.levels[:-1]],
                       "smoother": f"Chebyshev-Jacobi degree {mg_.smoothing_degree}, range {mg_.smoothing_range}",
-                      "coarse": f"P1 Jacobi-PCG {mg_.coarse_iterations} iterations",
+                      "coarse": f"P1 Jacobi-PCG {mg_.coarse_iterations} iterations"
+                      + (" on the assembled CSR matrix (cuSPARSE)" if coarse_matrix else " matrix-free"),
                       "mg_iterations": len(hist) - 1, "mg_solve_ms": round(t_mg, 2), "vcycle_ms": round(t_v, 3),
                       "mg_true_rel_residual": true_res,
                       "jacobi_iterations_to_tol": kj, "jacobi_ms_per_iteration": round(t_j / jit, 4),
@@ -303,7 +304,8 @@ if __name__ == "__main__":
     ap.add_argument("--n5", type=int, default=128)
     ap.add_argument("--tau-scale", type=float, default=1.0)
     ap.add_argument("--precision", default="f64", choices=["f64", "mixed"])
+    ap.add_argument("--coarse-matrix", action="store_true")
     a = ap.parse_args()
     for c in a.configs:
         {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5),
-         "csr": csr, "mg": lambda: mg(a.n5, precision=a.precision), "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale)}[c]()
+         "csr": csr, "mg": lambda: mg(a.n5, precision=a.precision, coarse_matrix=a.coarse_matrix), "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale)}[c]()
