@@ -10,10 +10,13 @@ from paper_2509_10226_b200.reorder import reorder_mesh
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 m = reorder_mesh(M.kuhn_cube_mesh(n, seed=0))
 for spec in sys.argv[2:]:
-    lev, sdeg, ci = spec.split(":")
+    parts = spec.split(":")
+    lev, sdeg, ci = parts[:3]
+    prec = parts[3] if len(parts) > 3 else "f64"
+    cm = len(parts) > 4 and parts[4] == "csr"
     degs = tuple(int(c) for c in lev)
     t0 = time.time()
-    mg = PMultigrid(m, degs, smoothing_degree=int(sdeg), coarse_iterations=int(ci))
+    mg = PMultigrid(m, degs, smoothing_degree=int(sdeg), coarse_iterations=int(ci), precision=prec, coarse_matrix=cm)
     setup = time.time() - t0
     dm = mg.levels[0].dm
     b = np.where(dm.dirichlet_mask, 0.0, np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs))
@@ -25,7 +28,7 @@ for spec in sys.argv[2:]:
     x, hist = mg.solve(bt, tol=1e-8, maxiter=200)
     e1.record()
     e1.synchronize()
-    print(json.dumps({"n": n, "levels": degs, "smoothing_degree": int(sdeg), "coarse_iterations": int(ci),
+    print(json.dumps({"n": n, "levels": degs, "precision": prec, "coarse_matrix": cm, "smoothing_degree": int(sdeg), "coarse_iterations": int(ci),
                       "iterations": len(hist) - 1, "solve_ms": round(e0.elapsed_time(e1), 2),
                       "final_rel": float(hist[-1] / hist[0]), "setup_s": round(setup, 1)}), flush=True)
     mg.close()
