@@ -243,6 +243,19 @@ typedef struct tmf_transfer_desc {
   int32_t device;
 } tmf_transfer_desc;
 int tmf_transfer_create(const tmf_transfer_desc* desc, tmf_transfer** out);
+/* h-coarsening onto a non-nested coarse mesh (P1 -> P1): fine DoF i takes the coarse values at
+ * coarse_index[4i..4i+3] with weights[4i..4i+3] (the barycentric coordinates of the fine node in
+ * the coarse cell containing it).  tmf_prolongate / tmf_restrict (and the _f32 forms) apply it. */
+typedef struct tmf_point_transfer_desc {
+  int64_t n_fine_dofs, n_coarse_dofs;
+  int32_t entries_per_row;                   /* 4                                       */
+  const int32_t* coarse_index;               /* host (n_fine_dofs, 4)                   */
+  const double* weights;                     /* host (n_fine_dofs, 4)                   */
+  const uint8_t* fine_dirichlet;             /* host (n_fine_dofs) or NULL              */
+  const uint8_t* coarse_dirichlet;           /* host (n_coarse_dofs) or NULL            */
+  int32_t device;
+} tmf_point_transfer_desc;
+int tmf_transfer_create_points(const tmf_point_transfer_desc* desc, tmf_transfer** out);
 int tmf_transfer_destroy(tmf_transfer* t);
 int tmf_prolongate(tmf_transfer* t, const double* xc, double* xf, int add, void* stream);
 int tmf_restrict(tmf_transfer* t, const double* rf, double* rc, void* stream);

@@ -47,6 +47,14 @@ class TransferDesc(C.Structure):
     ]
 
 
+class PointTransferDesc(C.Structure):
+    _fields_ = [
+        ("n_fine_dofs", C.c_int64), ("n_coarse_dofs", C.c_int64), ("entries_per_row", C.c_int32),
+        ("coarse_index", _ip), ("weights", _dp), ("fine_dirichlet", _bp), ("coarse_dirichlet", _bp),
+        ("device", C.c_int32),
+    ]
+
+
 class PlanInfo(C.Structure):
     _fields_ = [
         ("n_global_dofs", C.c_int64), ("flops_alg", C.c_double), ("bytes_alg", C.c_double),
@@ -99,6 +107,7 @@ def lib():
         L.tmf_color_cells.argtypes = [C.c_int64, C.c_int64, _ip, _ip, _ip]
         L.tmf_transfer_create.argtypes = [C.POINTER(TransferDesc), C.POINTER(C.c_void_p)]
         L.tmf_transfer_destroy.argtypes = [_v]
+        L.tmf_transfer_create_points.argtypes = [C.POINTER(PointTransferDesc), C.POINTER(C.c_void_p)]
         L.tmf_prolongate.argtypes = [_v, _v, _v, C.c_int, _v]
         L.tmf_restrict.argtypes = [_v, _v, _v, _v]
         L.tmf_chebyshev_step.argtypes = [C.c_int64, _v, _v, _v, _v, _v, C.c_double, C.c_double, _v]
@@ -115,7 +124,8 @@ def lib():
                      "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs",
                      "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction",
                      "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle", "tmf_ipc_open_handle",
-                     "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create", "tmf_transfer_destroy", "tmf_prolongate",
+                     "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create", "tmf_transfer_create_points",
+                     "tmf_transfer_destroy", "tmf_prolongate",
                      "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby", "tmf_apply_f32", "tmf_prolongate_f32",
                      "tmf_restrict_f32", "tmf_chebyshev_step_f32", "tmf_vec_axpby_f32"):
             getattr(L, name).restype = C.c_int
@@ -127,7 +137,8 @@ EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_app
             "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
             "tmf_build_faces", "tmf_build_cg_dofs", "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update",
             "tmf_pcg_direction", "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle",
-            "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create", "tmf_transfer_destroy",
+            "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create",
+            "tmf_transfer_create_points", "tmf_transfer_destroy",
             "tmf_prolongate", "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby", "tmf_apply_f32",
             "tmf_prolongate_f32", "tmf_restrict_f32", "tmf_chebyshev_step_f32", "tmf_vec_axpby_f32", "tmf_last_error",
             "tmf_version")

@@ -128,6 +128,46 @@ __global__ void axpby_kernel(int64_t n, T alpha, const T* __restrict__ x, T beta
     out[i] = alpha * x[i] + beta * y[i];
 }
 
+// Point transfers (h-coarsening onto a non-nested coarse mesh): fine row i has K coarse
+// entries (idx[i*K + k], w[i*K + k]); fine rows ~i < 0 are Dirichlet (0 / untouched),
+// coarse entries ~c < 0 are Dirichlet columns (skipped).
+template <int K, typename T>
+__global__ void point_prolongate_kernel(const int* __restrict__ rows, const int* __restrict__ idx,
+                                        const T* __restrict__ w, int64_t n, const T* __restrict__ xc,
+                                        T* __restrict__ xf, int add) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int f = rows[i];
+    if (f < 0) {
+      if (!add) xf[~f] = T(0);
+      continue;
+    }
+    T s = T(0);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = __ldg(idx + i * K + k);
+      if (c >= 0) s = fma(__ldg(w + i * K + k), __ldg(xc + c), s);
+    }
+    xf[f] = add ? xf[f] + s : s;
+  }
+}
+
+template <int K, typename T>
+__global__ void point_restrict_kernel(const int* __restrict__ rows, const int* __restrict__ idx,
+                                      const T* __restrict__ w, int64_t n, const T* __restrict__ rf,
+                                      T* __restrict__ rc) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int f = rows[i];
+    if (f < 0) continue;
+    const T r = __ldg(rf + f);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = __ldg(idx + i * K + k);
+      const T v = __ldg(w + i * K + k) * r;
+      if (c >= 0 && v != T(0)) atomicAdd(rc + c, v);
+    }
+  }
+}
+
 int sm_count(int dev) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -146,6 +186,10 @@ struct tmf_transfer {
   int* cdofs = nullptr;
   double* P = nullptr;
   float* P32 = nullptr;
+  // point mode (tmf_transfer_create_points): n_cells = fine rows, nc = entries per row
+  bool points = false;
+  double* W = nullptr;
+  float* W32 = nullptr;
 };
 
 extern "C" {
@@ -219,6 +263,8 @@ int tmf_transfer_destroy(tmf_transfer* t) {
   cudaFree(t->cdofs);
   cudaFree(t->P);
   cudaFree(t->P32);
+  cudaFree(t->W);
+  cudaFree(t->W32);
   delete t;
   return TMF_OK;
 }
@@ -235,6 +281,11 @@ int prolongate_t(tmf_transfer* t, const T* Pd, const T* xc, T* xf, int add, void
   const int block = 256;
   int64_t grid = (t->n_cells + block - 1) / block;
   if (grid > (int64_t)t->sms * 16) grid = (int64_t)t->sms * 16;
+  if (t->points) {
+    point_prolongate_kernel<4, T><<<(unsigned)grid, block, 0, st>>>(t->fdofs, t->cdofs, Pd, t->n_cells, xc, xf, add);
+    MG_CUDA(cudaGetLastError());
+    return TMF_OK;
+  }
   const size_t smem = (size_t)t->nf * t->nc * sizeof(T);
   const unsigned g = (unsigned)grid;
   switch (t->nc) {
@@ -256,6 +307,11 @@ int restrict_t(tmf_transfer* t, const T* Pd, const T* rf, T* rc, void* stream) {
   const int block = 256;
   int64_t grid = (t->n_cells + block - 1) / block;
   if (grid > (int64_t)t->sms * 16) grid = (int64_t)t->sms * 16;
+  if (t->points) {
+    point_restrict_kernel<4, T><<<(unsigned)grid, block, 0, st>>>(t->fdofs, t->cdofs, Pd, t->n_cells, rf, rc);
+    MG_CUDA(cudaGetLastError());
+    return TMF_OK;
+  }
   const size_t smem = (size_t)t->nf * t->nc * sizeof(T);
   const unsigned g = (unsigned)grid;
   switch (t->nc) {
@@ -294,16 +350,61 @@ int axpby_t(int64_t n, T alpha, const T* x, T beta, const T* y, T* out, void* st
 extern "C" {
 
 int tmf_prolongate(tmf_transfer* t, const double* xc, double* xf, int add, void* stream) {
-  return prolongate_t<double>(t, t ? t->P : nullptr, xc, xf, add, stream);
+  return prolongate_t<double>(t, t ? (t->points ? t->W : t->P) : nullptr, xc, xf, add, stream);
 }
 int tmf_restrict(tmf_transfer* t, const double* rf, double* rc, void* stream) {
-  return restrict_t<double>(t, t ? t->P : nullptr, rf, rc, stream);
+  return restrict_t<double>(t, t ? (t->points ? t->W : t->P) : nullptr, rf, rc, stream);
 }
 int tmf_prolongate_f32(tmf_transfer* t, const float* xc, float* xf, int add, void* stream) {
-  return prolongate_t<float>(t, t ? t->P32 : nullptr, xc, xf, add, stream);
+  return prolongate_t<float>(t, t ? (t->points ? t->W32 : t->P32) : nullptr, xc, xf, add, stream);
 }
 int tmf_restrict_f32(tmf_transfer* t, const float* rf, float* rc, void* stream) {
-  return restrict_t<float>(t, t ? t->P32 : nullptr, rf, rc, stream);
+  return restrict_t<float>(t, t ? (t->points ? t->W32 : t->P32) : nullptr, rf, rc, stream);
+}
+
+int tmf_transfer_create_points(const tmf_point_transfer_desc* d, tmf_transfer** out) {
+  if (!d || !out) return mg_fail(TMF_EINVAL, "null descriptor/output");
+  *out = nullptr;
+  if (d->n_fine_dofs <= 0 || d->n_coarse_dofs <= 0 || d->n_fine_dofs >= INT_MAX || d->n_coarse_dofs >= INT_MAX)
+    return mg_fail(TMF_EINVAL, "bad DoF counts");
+  if (d->entries_per_row != 4) return mg_fail(TMF_EINVAL, "point transfers take 4 coarse entries per fine row");
+  if (!d->coarse_index || !d->weights) return mg_fail(TMF_EINVAL, "missing coarse indices / weights");
+  const int64_t n = d->n_fine_dofs;
+  std::vector<int> rows(n), idx(n * 4);
+  std::vector<float> w32(n * 4);
+  for (int64_t i = 0; i < n; ++i) {
+    rows[i] = (d->fine_dirichlet && d->fine_dirichlet[i]) ? ~(int)i : (int)i;
+    for (int k = 0; k < 4; ++k) {
+      const int c = d->coarse_index[i * 4 + k];
+      if (c < 0 || c >= d->n_coarse_dofs) return mg_fail(TMF_EINVAL, "coarse index out of range");
+      idx[i * 4 + k] = (d->coarse_dirichlet && d->coarse_dirichlet[c]) ? ~c : c;
+      w32[i * 4 + k] = (float)d->weights[i * 4 + k];
+    }
+  }
+  MG_CUDA(cudaSetDevice(d->device));
+  auto* t = new tmf_transfer();
+  t->points = true;
+  t->device = d->device;
+  t->sms = sm_count(d->device);
+  t->n_cells = n;
+  t->nf = 1;
+  t->nc = 4;
+  t->n_fine = n;
+  t->n_coarse = d->n_coarse_dofs;
+  cudaError_t e = cudaMalloc(&t->fdofs, n * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&t->cdofs, n * 4 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&t->W, n * 4 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&t->W32, n * 4 * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpy(t->fdofs, rows.data(), n * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(t->cdofs, idx.data(), n * 4 * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(t->W, d->weights, n * 4 * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(t->W32, w32.data(), n * 4 * sizeof(float), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    tmf_transfer_destroy(t);
+    return mg_fail(TMF_ECUDA, std::string("point transfer upload: ") + cudaGetErrorString(e));
+  }
+  *out = t;
+  return TMF_OK;
 }
 int tmf_chebyshev_step(int64_t n, const double* ax, const double* b, const double* dinv, double* x,
                        double* d, double c1, double c2, void* stream) {

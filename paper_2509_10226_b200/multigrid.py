@@ -24,7 +24,12 @@ the fp64 p-multigrid part of it, built on the B200 operator apply:
 FFMA, fp32 transfers / Chebyshev steps / coarse Jacobi-PCG) inside the fp64 flexible PCG,
 as the paper does ("the multigrid V-cycle runs in single precision").
 
-Not built (out of scope this round): h-coarsening below P1, Chebyshev on the coarse level.  No CPU fallback: every vector operation
+``h_coarse=(n1, n2, ...)``: h-levels below the fine-mesh P1 level on unjittered Kuhn meshes of
+the unit cube with n1 > n2 > ... cubes per side (non-nested: the BASELINE meshes are jittered, not
+refinements), linked by point transfers (``tmf_transfer_create_points``: each fine vertex takes
+the coarse P1 function at its position).
+
+Not built (out of scope this round): Chebyshev on the coarse level, refinement genealogies.  No CPU fallback: every vector operation
 is a native kernel or a device tensor op; the CPU restatement is
 ``oracle/ref_multigrid.py`` (tests only).
 """
@@ -42,7 +47,8 @@ from . import dofmap as D
 from . import quadrature as Q
 from .geometry import GeometryData
 
-__all__ = ["interpolation_matrix", "Transfer", "PMultigrid", "chebyshev_coefficients", "color_cells",
+__all__ = ["interpolation_matrix", "Transfer", "PointTransfer", "kuhn_point_weights", "PMultigrid",
+           "chebyshev_coefficients", "color_cells",
            "dg_diagonal", "n10"]
 
 
@@ -175,6 +181,52 @@ class Transfer:
             pass
 
 
+def kuhn_point_weights(points: np.ndarray, n_coarse: int):
+    """(idx (n, 4) int32, w (n, 4)): for each point of [0,1]^3, the 4 vertices of the cell of
+    the unjittered, unpermuted Kuhn mesh ``mesh.kuhn_cube_mesh(n_coarse, jitter=0,
+    permute=False)`` containing it and its barycentric coordinates there.  In the cube with
+    origin c and local coordinates t, sorted t_a >= t_b >= t_c, the Kuhn cell is
+    (c, c + e_a, c + e_a + e_b, c + 1) with weights (1 - t_a, t_a - t_b, t_b - t_c, t_c)."""
+    x = np.clip(np.asarray(points, dtype=np.float64), 0.0, 1.0) * n_coarse
+    c = np.minimum(np.floor(x), n_coarse - 1).astype(np.int64)
+    t = x - c
+    order = np.argsort(-t, axis=1, kind="stable")
+    ts = np.take_along_axis(t, order, axis=1)
+    w = np.stack([1.0 - ts[:, 0], ts[:, 0] - ts[:, 1], ts[:, 1] - ts[:, 2], ts[:, 2]], axis=1)
+    corners = np.zeros((len(x), 4, 3), dtype=np.int64)
+    corners[:, 0] = c
+    for k in range(3):
+        corners[:, k + 1] = corners[:, k]
+        np.add.at(corners[:, k + 1], (np.arange(len(x)), order[:, k]), 1)
+    m = n_coarse + 1
+    idx = (corners[..., 0] * m + corners[..., 1]) * m + corners[..., 2]
+    return idx.astype(np.int32), w
+
+
+class PointTransfer(Transfer):
+    """P1 -> P1 transfer onto a non-nested, coarser Kuhn mesh of the unit cube (h-coarsening):
+    each fine DoF (= fine vertex) takes the coarse P1 function at its position."""
+
+    def __init__(self, fine_mesh, fine_dm, coarse_n: int, coarse_dm, device: int = 0):
+        if fine_dm.degree != 1 or coarse_dm.degree != 1 or fine_dm.space != "cg":
+            raise ValueError("h-transfers link P1 CG spaces")
+        idx, w = kuhn_point_weights(fine_mesh.vertices, coarse_n)
+        self.P = None
+        self.index, self.weights = idx, np.ascontiguousarray(w)
+        fm = np.ascontiguousarray(fine_dm.dirichlet_mask, dtype=np.uint8)
+        cm = np.ascontiguousarray(coarse_dm.dirichlet_mask, dtype=np.uint8)
+        d = _lib.PointTransferDesc()
+        d.n_fine_dofs, d.n_coarse_dofs, d.entries_per_row = fine_dm.n_scalar_dofs, coarse_dm.n_scalar_dofs, 4
+        d.coarse_index = _lib.ptr(self.index, C.c_int32)
+        d.weights = _lib.ptr(self.weights, C.c_double)
+        d.fine_dirichlet = _lib.ptr(fm, C.c_uint8) if fm.any() else _lib.ptr(None, C.c_uint8)
+        d.coarse_dirichlet = _lib.ptr(cm, C.c_uint8) if cm.any() else _lib.ptr(None, C.c_uint8)
+        d.device = int(device)
+        self._t = C.c_void_p()
+        _lib.check(_lib.lib().tmf_transfer_create_points(C.byref(d), C.byref(self._t)))
+        self.n_fine, self.n_coarse = fine_dm.n_scalar_dofs, coarse_dm.n_scalar_dofs
+
+
 @dataclass
 class _Level:
     p: int
@@ -188,6 +240,8 @@ class _Level:
     r: object = None
     d: object = None
     ax: object = None
+    csr: object = None      # assembled operator (cuSPARSE) used instead of the matrix-free apply
+    mesh: object = None
 
 
 class PMultigrid:
@@ -201,7 +255,7 @@ class PMultigrid:
     def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 2,
                  smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
                  lmax=None, config=None, seed: int = 0, fine_operator=None, precision: str = "f64",
-                 coarse_matrix: bool = False):
+                 coarse_matrix: bool = False, h_coarse=()):
         import torch
 
         from . import operator as op
@@ -224,14 +278,22 @@ class PMultigrid:
         self.smoothing_degree, self.smoothing_range = int(smoothing_degree), float(smoothing_range)
         self.coarse_iterations = int(coarse_iterations)
         self.levels: list[_Level] = []
-        specs = [("cg", p) for p in degrees]
+        from . import mesh as M
+
+        h_coarse = tuple(int(n) for n in h_coarse)
+        if h_coarse and degrees[-1] != 1:
+            raise ValueError("h-coarsening continues from a P1 level: degrees must end with 1")
+        specs = [("cg", p, mesh) for p in degrees]
+        specs += [("cg", 1, M.kuhn_cube_mesh(n, jitter=0.0, permute=False)) for n in h_coarse]
+        self.p1_fine_level = len(degrees) - 1
         if fine_operator is not None:
             if fine_operator.dofmap.space != "dg" or fine_operator.dofmap.degree != degrees[0]:
                 raise ValueError("fine_operator must be a DG operator of degree degrees[0]")
             if int(fine_operator.dofmap.n_components) != 1:
                 raise ValueError("fine_operator must be scalar")
-            specs.insert(0, ("dg", degrees[0]))
-        for i, (space, p) in enumerate(specs):
+            specs.insert(0, ("dg", degrees[0], mesh))
+            self.p1_fine_level += 1
+        for i, (space, p, lmesh) in enumerate(specs):
             if space == "dg":
                 A, dm = fine_operator, fine_operator.dofmap
                 dinv = 1.0 / dg_diagonal(A, mesh)
@@ -239,10 +301,11 @@ class PMultigrid:
                 cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
                 bas = B.tabulate_basis(p, cr, fr)
                 geo = GeometryData("affine", cr, fr, None, None, None, None)
-                dm = D.build_dof_map(mesh, p, "cg", 1, tuple(dirichlet_ids))
-                A = op.CgPoissonOperator(mesh, dm, geo, bas, self.config)
+                dm = D.build_dof_map(lmesh, p, "cg", 1, tuple(dirichlet_ids))
+                A = op.CgPoissonOperator(lmesh, dm, geo, bas, self.config)
                 dinv = 1.0 / A.diagonal()
             lv = _Level(p, dm, A, dinv, 0.0, [])
+            lv.mesh = lmesh
             n = dm.n_global_dofs
             vt = torch.float32 if self.mixed else torch.float64
             lv.x, lv.b, lv.r, lv.d, lv.ax = (torch.zeros(n, dtype=vt, device=self.device) for _ in range(5))
@@ -254,20 +317,26 @@ class PMultigrid:
         if self.mixed:   # the fp64 diagonals served the eigenvalue estimates; the cycle runs in fp32
             for lv in self.levels:
                 lv.dinv = lv.dinv.to(torch.float32)
-        # matrix-based coarse level (the paper switches to the assembled operator where it is
-        # faster): P1 on the fine mesh has 6 cells per DoF, so its CSR SpMV
+        # matrix-based P1 level on the fine mesh (the paper switches to the assembled operator
+        # where it is faster): P1 there has 6 cells per DoF, so its CSR SpMV
         # (cuSPARSE) moves far fewer bytes than the matrix-free cell loop
         self.coarse_csr = None
         if coarse_matrix:
             from .sparse import assemble_cg_csr
 
-            lv = self.levels[-1]
+            lv = self.levels[self.p1_fine_level]
             cr, fr = Q.make_cell_quadrature(lv.p), Q.make_face_quadrature(lv.p)
-            A = assemble_cg_csr(mesh, lv.dm, GeometryData("affine", cr, fr, None, None, None, None),
+            A = assemble_cg_csr(lv.mesh, lv.dm, GeometryData("affine", cr, fr, None, None, None, None),
                                 B.tabulate_basis(lv.p, cr, fr), device=self.device)
-            self.coarse_csr = A.to(torch.float32) if self.mixed else A
-        self.transfers = [Transfer(self.levels[i].dm, self.levels[i + 1].dm, dev)
-                          for i in range(len(self.levels) - 1)]
+            lv.csr = A.to(torch.float32) if self.mixed else A
+            self.coarse_csr = lv.csr
+        self.transfers = []
+        for i in range(len(self.levels) - 1):
+            f, c = self.levels[i], self.levels[i + 1]
+            if f.mesh is c.mesh:
+                self.transfers.append(Transfer(f.dm, c.dm, dev))
+            else:
+                self.transfers.append(PointTransfer(f.mesh, f.dm, h_coarse[i - self.p1_fine_level], c.dm, dev))
         self.n_global_dofs = self.levels[0].dm.n_global_dofs
 
     # ------------------------------------------------------------------ setup
@@ -317,7 +386,9 @@ class PMultigrid:
 
     # ------------------------------------------------------------------ cycle
     def _apply(self, lv, x, y, st):
-        if self.mixed:
+        if lv.csr is not None:
+            y.copy_((lv.csr @ x.unsqueeze(1)).squeeze(1))
+        elif self.mixed:
             lv.A.apply_f32(x, out=y, stream=st)
         else:
             lv.A.apply_into(x.data_ptr(), y.data_ptr(), st)
@@ -350,10 +421,7 @@ class PMultigrid:
         rz = torch.dot(r, z)
         zero = torch.zeros((), dtype=x.dtype, device=self.device)
         for _ in range(self.coarse_iterations):
-            if self.coarse_csr is not None:
-                q = (self.coarse_csr @ p.unsqueeze(1)).squeeze(1)
-            else:
-                self._apply(lv, p, q, st)
+            self._apply(lv, p, q, st)
             pq = torch.dot(p, q)
             alpha = torch.where(pq != 0, rz / pq, zero)
             x.add_(alpha * p)
@@ -369,7 +437,7 @@ class PMultigrid:
 
         lv = self.levels[i]
         if i == len(self.levels) - 1:
-            if self.mixed or self.coarse_csr is not None:
+            if self.mixed or lv.csr is not None:
                 self._coarse_pcg(lv)
             else:
                 x, _ = jacobi_pcg(lv.A, lv.b, self.coarse_iterations)

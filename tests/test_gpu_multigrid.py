@@ -356,3 +356,59 @@ def test_matrix_based_coarse_level(precision):
     _, ha = a.solve(r, tol=1e-10, maxiter=60)
     _, hb = b_.solve(r, tol=1e-10, maxiter=60)
     assert hb[-1] <= 1e-10 * hb[0] and abs(len(ha) - len(hb)) <= 2
+
+
+@pytest.mark.parametrize("dirichlet", [False, True])
+def test_point_transfer_matches_oracle(dirichlet):
+    import scipy.sparse as sp
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import PointTransfer
+
+    mf = M.kuhn_cube_mesh(6, seed=0)
+    mc = M.kuhn_cube_mesh(3, jitter=0.0, permute=False)
+    dids = tuple(range(6)) if dirichlet else ()
+    dmf, dmc = _dm(mf, 1, dids), _dm(mc, 1, dids)
+    T = PointTransfer(mf, dmf, 3, dmc)
+    nf_, nc_ = dmf.n_scalar_dofs, dmc.n_scalar_dofs
+    rows = np.repeat(np.arange(nf_), 4)
+    w = T.weights.ravel().copy()
+    keep = np.ones_like(w, dtype=bool)
+    if dirichlet:
+        keep &= ~dmf.dirichlet_mask[rows] & ~dmc.dirichlet_mask[T.index.ravel()]
+    Pg = sp.csr_matrix((w[keep], (rows[keep], T.index.ravel()[keep])), shape=(nf_, nc_))
+    rng = np.random.default_rng(6)
+    xc, rf = rng.uniform(-1, 1, nc_), rng.uniform(-1, 1, nf_)
+    for dt, tol in ((torch.float64, 1e-14), (torch.float32, 1e-6)):
+        xf = torch.empty(nf_, dtype=dt, device="cuda")
+        T.prolongate(torch.from_numpy(xc).to("cuda", dt), xf)
+        assert rel_l2(xf.double().cpu().numpy(), Pg @ xc) <= tol
+        rc = torch.empty(nc_, dtype=dt, device="cuda")
+        T.restrict(torch.from_numpy(rf).to("cuda", dt), rc)
+        assert rel_l2(rc.double().cpu().numpy(), Pg.T @ rf) <= tol
+
+
+@pytest.mark.parametrize("precision", ["f64", "mixed"])
+def test_hp_multigrid_mesh_independent_iterations(precision):
+    """SPEC.md:549 (mesh-independent iterations): p-levels then h-levels down to a 2^3 Kuhn
+    mesh; the iteration count to 1e-10 stays within 3 across three refinements."""
+    import torch
+
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.multigrid import PMultigrid, n10
+
+    its = []
+    for n, hc in ((8, (4, 2)), (16, (8, 4, 2)), (24, (12, 6, 3))):
+        m = M.kuhn_cube_mesh(n, seed=0)
+        mg = PMultigrid(m, (2, 1), h_coarse=hc, coarse_iterations=40, precision=precision)
+        assert [lv.dm.n_scalar_dofs for lv in mg.levels][-1] == (hc[-1] + 1) ** 3
+        dm = mg.levels[0].dm
+        b = torch.from_numpy(np.where(dm.dirichlet_mask, 0.0,
+                                      np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs))).cuda()
+        x, hist = mg.solve(b, tol=1e-10, maxiter=80)
+        assert hist[-1] <= 1e-10 * hist[0]
+        assert rel_l2(mg.levels[0].A.apply(x).cpu().numpy(), b.cpu().numpy()) <= 1e-9
+        its.append(n10(hist))
+        mg.close()
+    assert max(its) - min(its) <= 3.0, its

@@ -121,3 +121,22 @@ def test_n10_metric():
     assert n10(h) == pytest.approx(2.5)
     with pytest.raises(ValueError):
         n10([1.0, 1e-3])
+
+
+@pytest.mark.parametrize("nf,nc", [(7, 4), (8, 4), (16, 8), (5, 2)])
+def test_kuhn_point_weights_locate_and_interpolate(nf, nc):
+    """h-transfer weights: each fine vertex lies in a real cell of the coarse Kuhn mesh, with
+    nonnegative barycentric weights summing to 1 that reproduce linear functions exactly."""
+    from paper_2509_10226_b200.multigrid import kuhn_point_weights
+
+    mc = M.kuhn_cube_mesh(nc, jitter=0.0, permute=False)
+    mf = M.kuhn_cube_mesh(nf, seed=3)
+    idx, w = kuhn_point_weights(mf.vertices, nc)
+    assert w.min() >= -1e-15 and np.allclose(w.sum(axis=1), 1.0, atol=1e-15)
+    f = lambda x: 1.0 + 2.0 * x[:, 0] - 3.0 * x[:, 1] + 0.5 * x[:, 2]  # noqa: E731
+    assert np.abs((w * f(mc.vertices)[idx]).sum(axis=1) - f(mf.vertices)).max() <= 1e-14
+    cells = {tuple(sorted(c)) for c in mc.cells.tolist()}
+    assert all(tuple(sorted(r)) in cells for r in idx.tolist())
+    # a fine vertex that coincides with a coarse vertex maps onto it alone
+    idx2, w2 = kuhn_point_weights(mc.vertices, nc)
+    assert np.allclose(np.take_along_axis(w2, np.argmax(w2, axis=1)[:, None], 1), 1.0)

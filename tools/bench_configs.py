@@ -185,7 +185,7 @@ def csr(n=48):
         torch.cuda.empty_cache()
 
 
-def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False):
+def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False, h_coarse=(), coarse_iterations=30):
     """p-multigrid flexible PCG vs Jacobi-PCG on the C5 problem (CG P3, homogeneous
     Dirichlet, RHS uniform[-1,1]): iterations and device time to ||r|| <= tol ||b||."""
     import torch
@@ -198,7 +198,8 @@ def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False)
 
     t0 = time.time()
     m = reorder_mesh(M.kuhn_cube_mesh(n, seed=0))
-    mg_ = PMultigrid(m, degrees, coarse_iterations=30, precision=precision, coarse_matrix=coarse_matrix)
+    mg_ = PMultigrid(m, degrees, coarse_iterations=coarse_iterations, precision=precision,
+                     coarse_matrix=coarse_matrix, h_coarse=h_coarse)
     setup = time.time() - t0
     dm = mg_.levels[0].dm
     nd = dm.n_global_dofs
@@ -234,8 +235,9 @@ def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False)
                       "precision": "fp32 V-cycle, fp64 outer CG" if precision == "mixed" else "fp64",
                       "ndof": nd, "levels": list(degrees), "lmax": [round(lv.lmax, 4) for lv in mg_.levels[:-1]],
                       "smoother": f"Chebyshev-Jacobi degree {mg_.smoothing_degree}, range {mg_.smoothing_range}",
-                      "coarse": f"P1 Jacobi-PCG {mg_.coarse_iterations} iterations"
-                      + (" on the assembled CSR matrix (cuSPARSE)" if coarse_matrix else " matrix-free"),
+                      "p1_fine_level": "assembled CSR (cuSPARSE)" if coarse_matrix else "matrix-free",
+                      "h_levels": list(h_coarse),
+                      "coarse": f"Jacobi-PCG {mg_.coarse_iterations} iterations on {mg_.levels[-1].dm.n_scalar_dofs} DoFs",
                       "mg_iterations": len(hist) - 1, "mg_solve_ms": round(t_mg, 2), "vcycle_ms": round(t_v, 3),
                       "mg_true_rel_residual": true_res,
                       "jacobi_iterations_to_tol": kj, "jacobi_ms_per_iteration": round(t_j / jit, 4),
@@ -305,7 +307,11 @@ if __name__ == "__main__":
     ap.add_argument("--tau-scale", type=float, default=1.0)
     ap.add_argument("--precision", default="f64", choices=["f64", "mixed"])
     ap.add_argument("--coarse-matrix", action="store_true")
+    ap.add_argument("--h-coarse", default="", help="comma-separated coarse Kuhn sizes, e.g. 64,32,16,8")
+    ap.add_argument("--coarse-iterations", type=int, default=30)
     a = ap.parse_args()
     for c in a.configs:
         {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5),
-         "csr": csr, "mg": lambda: mg(a.n5, precision=a.precision, coarse_matrix=a.coarse_matrix), "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale)}[c]()
+         "csr": csr, "mg": lambda: mg(a.n5, precision=a.precision, coarse_matrix=a.coarse_matrix,
+                         h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v),
+                         coarse_iterations=a.coarse_iterations), "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale)}[c]()
