@@ -423,11 +423,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
                 if (PEER)
                   atomicAdd(peer_dst(a.peer, a.y, g, a.nc, comp), yacc[m][nj][i]);
                 else
-#if defined(TMF_EXP_SCATTER) && TMF_EXP_SCATTER == 1
-                  a.y[g * a.nc + comp] = yacc[m][nj][i];  // timing experiment only: wrong sums
-#else
                   atomicAdd(a.y + g * a.nc + comp, yacc[m][nj][i]);
-#endif
               }
             }
           }

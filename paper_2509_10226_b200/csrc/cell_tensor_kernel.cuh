@@ -186,11 +186,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
             if (PEER)
               atomicAdd(peer_dst(a.peer, a.y, g, a.nc, comp), yv[m]);
             else
-#if defined(TMF_EXP_SCATTER) && TMF_EXP_SCATTER == 1
-              a.y[(int64_t)g * a.nc + comp] = yv[m];  // timing experiment only: wrong sums
-#else
               atomicAdd(a.y + (int64_t)g * a.nc + comp, yv[m]);
-#endif
           }
         }
       }

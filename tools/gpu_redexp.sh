@@ -1,4 +1,5 @@
 # timing experiment: CG cell kernels with the fp64 RED scatter replaced by plain stores
+# NOTE: needs the TMF_EXP_SCATTER switch that was removed from the kernels after this experiment (see profiles/r01/red_scatter_experiments.json "how")
 set -x
 Q="cg:1:48 cgv:1:48 cg:2:48 cgv:2:48 cg:3:48 cgv:3:48 cg:4:48 cgv:4:48"
 timeout 600 python tools/quick_bench.py $Q > gpurun_out/redexp_base.jsonl 2> gpurun_out/redexp_base.err
