@@ -255,7 +255,7 @@ class PMultigrid:
     def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 2,
                  smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
                  lmax=None, config=None, seed: int = 0, fine_operator=None, precision: str = "f64",
-                 coarse_matrix: bool = False, h_coarse=()):
+                 coarse_matrix: bool = False, h_coarse=(), fine_smoothing_degree: int | None = None):
         import torch
 
         from . import operator as op
@@ -312,7 +312,10 @@ class PMultigrid:
             if i < len(specs) - 1:
                 given = None if lmax is None else float(lmax[i])
                 lv.lmax = given if given is not None else 1.1 * self.estimate_lmax(lv, eig_iterations, seed)
-                lv.coeffs = chebyshev_coefficients(lv.lmax, self.smoothing_range, self.smoothing_degree)
+                deg = self.smoothing_degree
+                if space == "dg" and fine_smoothing_degree is not None:
+                    deg = int(fine_smoothing_degree)   # the DG level sets the cp-MG rate
+                lv.coeffs = chebyshev_coefficients(lv.lmax, self.smoothing_range, deg)
             self.levels.append(lv)
         if self.mixed:   # the fp64 diagonals served the eigenvalue estimates; the cycle runs in fp32
             for lv in self.levels:

@@ -247,7 +247,7 @@ def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False,
     mg_.close()
 
 
-def mgdg(n=64, p=3, tol=1e-8, tau_scale=1.0, h_coarse=(), precision="f64"):
+def mgdg(n=64, p=3, tol=1e-8, tau_scale=1.0, h_coarse=(), precision="f64", fine_smoothing_degree=None):
     """cp-multigrid (DG p -> CG p -> ... -> CG 1) flexible PCG vs Jacobi-PCG on the C3 problem
     (DG-SIPG P3, weak Dirichlet on all sides, RHS uniform[-1,1]): iterations / time to tol."""
     import torch
@@ -263,7 +263,7 @@ def mgdg(n=64, p=3, tol=1e-8, tau_scale=1.0, h_coarse=(), precision="f64"):
     sipg.tau_boundary *= tau_scale
     A = op.DgSipgOperator(m, dm, geo, bas, sipg, dirichlet_ids=range(6))
     mg_ = PMultigrid(m, tuple(range(p, 0, -1)), fine_operator=A, coarse_iterations=50 if h_coarse else 30,
-                     h_coarse=h_coarse)
+                     h_coarse=h_coarse, fine_smoothing_degree=fine_smoothing_degree)
     setup_mg = time.time() - t0
     nd = dm.n_global_dofs
     bt = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, nd)).cuda()
@@ -287,7 +287,8 @@ def mgdg(n=64, p=3, tol=1e-8, tau_scale=1.0, h_coarse=(), precision="f64"):
     hit = np.nonzero(hj <= tol * hj[0])[0]
     kj = int(hit[0]) if len(hit) else None
     print(json.dumps({"config": f"cp-multigrid PCG vs Jacobi-PCG, DG-SIPG P{p} {n}^3x6 reordered, weak Dirichlet, "
-                      f"tol {tol}", "tau": f"{tau_scale} x 2.5 (p+1)^2 / h", "h_levels": list(h_coarse), "ndof": nd, "levels": ["dg%d" % p] + ["cg%d" % lv.p for lv in mg_.levels[1:]],
+                      f"tol {tol}", "tau": f"{tau_scale} x 2.5 (p+1)^2 / h", "h_levels": list(h_coarse),
+                      "dg_smoothing_degree": len(mg_.levels[0].coeffs), "ndof": nd, "levels": ["dg%d" % p] + ["cg%d" % lv.p for lv in mg_.levels[1:]],
                       "lmax": [round(lv.lmax, 4) for lv in mg_.levels[:-1]],
                       "mg_iterations": len(hist) - 1, "mg_solve_ms": round(t_mg, 2),
                       "mg_true_rel_residual": true_res,
@@ -310,10 +311,12 @@ if __name__ == "__main__":
     ap.add_argument("--coarse-matrix", action="store_true")
     ap.add_argument("--h-coarse", default="", help="comma-separated coarse Kuhn sizes, e.g. 64,32,16,8")
     ap.add_argument("--coarse-iterations", type=int, default=30)
+    ap.add_argument("--dg-smoothing-degree", type=int, default=None)
     a = ap.parse_args()
     for c in a.configs:
         {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5),
          "csr": csr, "mg": lambda: mg(a.n5, precision=a.precision, coarse_matrix=a.coarse_matrix,
                          h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v),
                          coarse_iterations=a.coarse_iterations), "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale,
-                             h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v))}[c]()
+                             h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v),
+                             fine_smoothing_degree=a.dg_smoothing_degree)}[c]()
