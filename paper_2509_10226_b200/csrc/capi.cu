@@ -474,6 +474,7 @@ struct tmf_plan {
   double* if_tau = nullptr;
   double* if_geo = nullptr;
   int64_t n_if_batches = 0, n_if_chunks = 0;
+  int64_t face_blocked_grid = 0;   // > 0: window-major chunk runs for the blocked default kernel
   int4* bf_chunks = nullptr;
   int* bf_cm = nullptr;
   double* bf_tau = nullptr;
@@ -578,6 +579,40 @@ void push_chunks(std::vector<int4>& out, int cm, int cp, int64_t first, int64_t 
     out.push_back(make_int4(cm, cp, (int)(first + b), (int)std::min<int64_t>(chunk, count - b)));
 }
 
+// Window-major layout of the chunk list for the blocked face kernel (each CTA takes a
+// contiguous run of per = n / G chunks): run k is the concatenation of CTA k's contiguous
+// share of every window, shares balanced to within one chunk (padding chunks of zero
+// batches, with the previous chunk's signature so they cost no restaging, even the runs
+// out).  All CTAs then sweep the windows in step, so the live u / y of a window stay in L2
+// instead of every CTA streaming its own region of the mesh (DRAM 3x the algorithmic
+// bytes with plain contiguous runs, profiles/r01/ncu_prof_face_modal_d3_w32k.json).
+std::vector<int4> window_major_runs(const std::vector<int4>& chunks, const std::vector<int64_t>& cwin, int64_t G) {
+  std::vector<std::vector<int4>> run(G);
+  int64_t off = 0;
+  for (size_t s = 0; s < chunks.size();) {
+    size_t e = s;
+    while (e < chunks.size() && cwin[e] == cwin[s]) ++e;
+    const int64_t c = (int64_t)(e - s), base = c / G, extra = c % G;
+    size_t pos = s;
+    for (int64_t k = 0; k < G; ++k) {
+      const int64_t len = base + (((k - off) % G + G) % G < extra ? 1 : 0);
+      for (int64_t i = 0; i < len; ++i) run[k].push_back(chunks[pos++]);
+    }
+    off = (off + extra) % G;
+    s = e;
+  }
+  size_t L = 0;
+  for (const auto& r : run) L = std::max(L, r.size());
+  std::vector<int4> out;
+  out.reserve(L * G);
+  for (const auto& r : run) {
+    for (const auto& c : r) out.push_back(c);
+    const int4 last = r.empty() ? chunks[0] : r.back();
+    for (size_t i = r.size(); i < L; ++i) out.push_back(make_int4(last.x, last.y, 0, 0));
+  }
+  return out;
+}
+
 int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* total) {
   const int64_t nif = d->n_interior_faces, nbf = d->n_boundary_faces;
   // interior: stable sort by signature (lf-, lf+, code); faces keep their
@@ -599,6 +634,7 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   }
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sig(a) < sig(b); });
   std::vector<int4> chunks;
+  std::vector<int64_t> cwin;   // window of each chunk
   std::vector<int> cm, cp;
   std::vector<double> tau;
   int64_t nb = 0;
@@ -609,6 +645,7 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
     const int32_t* r0 = d->interior_faces + 5 * order[s];
     const int64_t nbatch = (e - s + 7) / 8;
     push_chunks(chunks, r0[1] * 6, r0[3] * 6 + r0[4], nb, nbatch, chunk);
+    cwin.resize(chunks.size(), r0[0] / kFaceWindow);
     for (int64_t k = 0; k < nbatch * 8; ++k) {
       if (s + k < e) {
         const int64_t f = order[s + k];
@@ -626,6 +663,8 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
     s = e;
   }
   P->n_if_batches = nb;
+  if (P->face_blocked_grid > 0 && P->nc == 1 && (int64_t)chunks.size() > P->face_blocked_grid)
+    chunks = window_major_runs(chunks, cwin, P->face_blocked_grid);
   P->n_if_chunks = (int64_t)chunks.size();
   int rc;
   if ((rc = upload(&P->if_chunks, chunks.data(), chunks.size(), total))) return rc;
@@ -1151,6 +1190,10 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       if ((rc = upload(&P->face_tfrags, tf.data(), tf.size(), &total))) return bail(rc);
     }
     const int chunk = ((d->flags >> 8) & 0xF) ? 8 * ((d->flags >> 8) & 0xF) : fi.chunk;
+    // window-major runs only for the default blocked kernel the launcher will pick (P4's
+    // default is the asynchronous-ring kernel with its own grid; tuning variants may deal
+    // chunks round-robin; the tensor engine has its own kernel)
+    if (P->face_variant == 0 && N != 35 && fe != 2 && !((d->flags >> 21) & 1)) P->face_blocked_grid = fi.blocked_grid;
     if ((rc = build_face_batches(P, d, chunk, &total))) return bail(rc);
     // per-face geometry, computed once on the device (64 B per face slot)
     for (int bnd = 0; bnd < 2; ++bnd) {

@@ -21,6 +21,11 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
     info->nfrag = S::NFRAG;
     info->chunk = S::CHUNK;
     info->dmma_per_batch = BND ? (S::NB1 + S::NB2) : 2 * (S::NB1 + S::NB2);
+    info->blocked_grid = 0;
+    if (BLOCKED && !TPF) {
+      int ps = 0;
+      if (blocks_per_sm(kern, BLOCK, SMEM, &ps) == cudaSuccess) info->blocked_grid = n_sm * (ps < 1 ? 1 : ps);
+    }
     return cudaSuccess;
   }
   int per_sm = 0;

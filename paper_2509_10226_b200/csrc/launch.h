@@ -30,6 +30,7 @@ struct FaceLaunchInfo {
   int grid = 0;
   int tnfrag = 0;           // reference-tensor interior-face kernel: fragments per signature
   int tdmma_per_batch = 0;  //   and its DMMAs per 8-face batch (0: no tensor kernel)
+  int blocked_grid = 0;     // interior default kernel deals contiguous chunk runs: its grid size
 };
 
 // info != nullptr: only fill the launch description (no launch).

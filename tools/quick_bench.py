@@ -5,7 +5,7 @@ import numpy as np
 import torch
 from paper_2509_10226_b200 import mesh as M, dofmap as D, basis as B, quadrature as Q, geometry as G, operator as op
 
-def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto", face="auto"):
+def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto", face="auto", runs="window"):
     reordered = kind[-1] in "rv"
     suffix = kind[-1] if reordered else ""
     t0 = time.time()
@@ -23,13 +23,13 @@ def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto", face="aut
     elif kind == "dg":
         dm = D.build_dof_map(m, p, "dg")
         A = op.DgSipgOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n),
-                              op.OperatorConfig(kernel_variant=variant & 0xF, face_variant=(variant >> 4) & 0xF, face_chunk=((variant >> 8) & 0xF) * 8, concurrent_dg=bool(variant >> 12), cell_engine=engine, face_engine=face),
+                              op.OperatorConfig(kernel_variant=variant & 0xF, face_variant=(variant >> 4) & 0xF, face_chunk=((variant >> 8) & 0xF) * 8, concurrent_dg=bool(variant >> 12), cell_engine=engine, face_engine=face, face_runs=runs),
                               dirichlet_ids=range(6))
     else:
         dm = D.build_dof_map(m, p, "dg")
         kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
         A = op.KappaHelmholtzOperator(m, dm, geo, bas, op.baseline_sipg_tau(m, p, 1.0 / n), kap, 1.0,
-                                      op.OperatorConfig(kernel_variant=variant & 0xF, face_variant=(variant >> 4) & 0xF, face_chunk=((variant >> 8) & 0xF) * 8, concurrent_dg=bool(variant >> 12), cell_engine=engine, face_engine=face),
+                                      op.OperatorConfig(kernel_variant=variant & 0xF, face_variant=(variant >> 4) & 0xF, face_chunk=((variant >> 8) & 0xF) * 8, concurrent_dg=bool(variant >> 12), cell_engine=engine, face_engine=face, face_runs=runs),
                                       dirichlet_ids=range(6))
     setup = time.time() - t0
     nd = A.n_global_dofs
@@ -42,7 +42,7 @@ def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto", face="aut
     gdofs = nd / (ms[0] * 1e-3) / 1e9
     tf_alg = info["flops_alg"] / (ms[0] * 1e-3) / 1e12
     tf_iss = info["flops_issued"] / (ms[0] * 1e-3) / 1e12
-    print(json.dumps(dict(kind=kind + suffix, p=p, n=n, variant=variant, engine=engine, face=face, patch_cells=A.info['patch_cells'], patch_ratio=round(A.info['patch_ratio'], 3), ndof=nd, setup_s=round(setup, 1), ms=[round(x, 4) for x in ms],
+    print(json.dumps(dict(kind=kind + suffix, p=p, n=n, variant=variant, engine=engine, face=face, runs=runs, patch_cells=A.info['patch_cells'], patch_ratio=round(A.info['patch_ratio'], 3), ndof=nd, setup_s=round(setup, 1), ms=[round(x, 4) for x in ms],
                           gdofs=round(gdofs, 3), tflops_alg=round(tf_alg, 2), tflops_issued=round(tf_iss, 2),
                           frac_fp64=round(tf_alg / 37.1, 3))), flush=True)
 
@@ -51,4 +51,4 @@ if __name__ == "__main__":
         parts = spec.split(":")
         run(parts[0], int(parts[1]), int(parts[2]), variant=int(parts[3]) if len(parts) > 3 else 0,
             engine=parts[4] if len(parts) > 4 else "auto", patches=parts[5] if len(parts) > 5 else "auto",
-            face=parts[6] if len(parts) > 6 else "auto")
+            face=parts[6] if len(parts) > 6 else "auto", runs=parts[7] if len(parts) > 7 else "window")
