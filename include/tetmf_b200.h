@@ -79,7 +79,7 @@ typedef struct tmf_plan_desc {
   double diffusivity;          /* Laplace/SIPG scale (nu)                             */
   int32_t device;              /* CUDA device ordinal                                 */
   int32_t flags;               /* bit 20: also build the fp32 mirror (tmf_apply_f32);
-                                  bit 21: plain contiguous face-chunk runs (default: window-major);
+                                  bit 21: window-major face-chunk runs (default: plain contiguous runs);
                                   bits 0-3 / 4-7: cell / face kernel tuning variant;
                                   8-11 face chunk/8; 12 concurrent DG; 13-14 cell engine
                                   (0 by degree, 1 DMMA quadrature points, 2 DFMA,

@@ -1193,7 +1193,10 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     // window-major runs only for the default blocked kernel the launcher will pick (P4's
     // default is the asynchronous-ring kernel with its own grid; tuning variants may deal
     // chunks round-robin; the tensor engine has its own kernel)
-    if (P->face_variant == 0 && N != 35 && fe != 2 && !((d->flags >> 21) & 1)) P->face_blocked_grid = fi.blocked_grid;
+    // (opt-in, flags bit 21: measured at C3 64^3 -- DRAM per launch 2.94 -> 1.56 GB but the face
+    // kernel 0.890 -> 0.924 ms, since a CTA then restages its tables for almost every chunk;
+    // the kernel is DMMA/latency-bound, not DRAM-bound)
+    if (P->face_variant == 0 && N != 35 && fe != 2 && ((d->flags >> 21) & 1)) P->face_blocked_grid = fi.blocked_grid;
     if ((rc = build_face_batches(P, d, chunk, &total))) return bail(rc);
     // per-face geometry, computed once on the device (64 B per face slot)
     for (int bnd = 0; bnd < 2; ++bnd) {

@@ -63,7 +63,7 @@ class OperatorConfig:
     cell_patches: str = "auto"   # B200 CG warp-patch assembly: auto (= off, measured slower) | off | on
     face_engine: str = "auto"    # B200 faces: auto (modal at P2-P4) | quadrature (points) | tensor (interior) | modal
     f32_mirror: bool = False     # B200 CG Laplace: also build the fp32 apply (apply_f32; mixed-precision multigrid)
-    face_runs: str = "window"    # B200 DG faces, blocked kernel: "window" (window-major CTA runs) | "plain"
+    face_runs: str = "plain"     # B200 DG faces, blocked kernel: "plain" (contiguous CTA runs) | "window" (window-major; measured slower)
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -205,7 +205,7 @@ class _B200Operator:
             (_PATCHES[getattr(self.config, "cell_patches", "auto")] << 15) | \
             (_FACE_ENGINES[getattr(self.config, "face_engine", "auto")] << 17) | \
             ((1 if getattr(self.config, "f32_mirror", False) else 0) << 20) | \
-            ((1 if getattr(self.config, "face_runs", "window") == "plain" else 0) << 21)
+            ((1 if getattr(self.config, "face_runs", "plain") == "window" else 0) << 21)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))

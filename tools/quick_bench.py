@@ -5,7 +5,7 @@ import numpy as np
 import torch
 from paper_2509_10226_b200 import mesh as M, dofmap as D, basis as B, quadrature as Q, geometry as G, operator as op
 
-def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto", face="auto", runs="window"):
+def run(kind, p, n, reps=20, variant=0, engine="auto", patches="auto", face="auto", runs="plain"):
     reordered = kind[-1] in "rv"
     suffix = kind[-1] if reordered else ""
     t0 = time.time()
@@ -51,4 +51,4 @@ if __name__ == "__main__":
         parts = spec.split(":")
         run(parts[0], int(parts[1]), int(parts[2]), variant=int(parts[3]) if len(parts) > 3 else 0,
             engine=parts[4] if len(parts) > 4 else "auto", patches=parts[5] if len(parts) > 5 else "auto",
-            face=parts[6] if len(parts) > 6 else "auto", runs=parts[7] if len(parts) > 7 else "window")
+            face=parts[6] if len(parts) > 6 else "auto", runs=parts[7] if len(parts) > 7 else "plain")
