@@ -14,9 +14,11 @@ for spec in sys.argv[2:]:
     lev, sdeg, ci = parts[:3]
     prec = parts[3] if len(parts) > 3 else "f64"
     cm = len(parts) > 4 and parts[4] == "csr"
+    hc = tuple(int(v) for v in parts[5].split("-")) if len(parts) > 5 and parts[5] else ()
     degs = tuple(int(c) for c in lev)
     t0 = time.time()
-    mg = PMultigrid(m, degs, smoothing_degree=int(sdeg), coarse_iterations=int(ci), precision=prec, coarse_matrix=cm)
+    mg = PMultigrid(m, degs, smoothing_degree=int(sdeg), coarse_iterations=int(ci), precision=prec, coarse_matrix=cm,
+                    h_coarse=hc)
     setup = time.time() - t0
     dm = mg.levels[0].dm
     b = np.where(dm.dirichlet_mask, 0.0, np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs))
@@ -28,7 +30,7 @@ for spec in sys.argv[2:]:
     x, hist = mg.solve(bt, tol=1e-8, maxiter=200)
     e1.record()
     e1.synchronize()
-    print(json.dumps({"n": n, "levels": degs, "precision": prec, "coarse_matrix": cm, "smoothing_degree": int(sdeg), "coarse_iterations": int(ci),
+    print(json.dumps({"n": n, "levels": degs, "precision": prec, "coarse_matrix": cm, "h_levels": hc, "smoothing_degree": int(sdeg), "coarse_iterations": int(ci),
                       "iterations": len(hist) - 1, "solve_ms": round(e0.elapsed_time(e1), 2),
                       "final_rel": float(hist[-1] / hist[0]), "setup_s": round(setup, 1)}), flush=True)
     mg.close()
