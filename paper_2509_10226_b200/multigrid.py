@@ -255,7 +255,8 @@ class PMultigrid:
     def __init__(self, mesh, degrees=(3, 2, 1), dirichlet_ids=tuple(range(6)), smoothing_degree: int = 2,
                  smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
                  lmax=None, config=None, seed: int = 0, fine_operator=None, precision: str = "f64",
-                 coarse_matrix: bool = False, h_coarse=(), fine_smoothing_degree: int | None = None):
+                 coarse_matrix: bool = False, h_coarse=(), fine_smoothing_degree: int | None = None,
+                 graph: bool = True):
         import torch
 
         from . import operator as op
@@ -265,6 +266,10 @@ class PMultigrid:
         if precision == "mixed" and fine_operator is not None:
             raise ValueError("the mixed-precision V-cycle has fp32 operators for the CG levels only")
         self.mixed = precision == "mixed"
+        # CUDA-graph replay of the V-cycle: needs device-side scalars everywhere (the mixed
+        # cycle's coarse PCG); the fp64 cycle's native coarse PCG syncs with the host
+        self.use_graph = bool(graph) and self.mixed
+        self._graph, self._graph_failed = None, False
         degrees = tuple(int(p) for p in degrees)
         if len(degrees) < 2 or any(a <= b for a, b in zip(degrees, degrees[1:])):
             raise ValueError("degrees must be strictly decreasing, at least two levels")
@@ -459,12 +464,41 @@ class PMultigrid:
         self.transfers[i].prolongate(nxt.x, lv.x, add=True, stream=st)
         self._smooth(lv, first=False)
 
+    def _capture(self):
+        """Capture the whole V-cycle (every level's kernels, the coarse PCG with device scalars)
+        into one CUDA graph: its hundreds of small launches on the coarse levels would
+        otherwise be host-bound.  Returns None where capture is not possible."""
+        import torch
+
+        lv = self.levels[0]
+        try:
+            s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(s):
+                for _ in range(2):   # warm-up (allocator, cuSPARSE workspaces) off the capture
+                    self._cycle(0)
+            torch.cuda.current_stream(self.device).wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._cycle(0)
+            return g
+        except Exception:   # noqa: BLE001 -- eager cycles instead
+            torch.cuda.synchronize(self.device)
+            return None
+
     def vcycle(self, r, out=None):
         """z = V r (one V-cycle from a zero initial guess); device tensors.  Mixed precision:
-        r is rounded to fp32, the cycle runs in fp32 and z is returned in r's dtype."""
+        r is rounded to fp32, the cycle runs in fp32 and z is returned in r's dtype.  With
+        ``graph=True`` (mixed precision) the cycle is replayed from a captured CUDA graph."""
         lv = self.levels[0]
         lv.b.copy_(r)
-        self._cycle(0)
+        if self.use_graph and self._graph is None and not self._graph_failed:
+            self._graph = self._capture()
+            self._graph_failed = self._graph is None
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self._cycle(0)
         if out is None:
             return lv.x.to(r.dtype, copy=True)
         out.copy_(lv.x)
