@@ -185,7 +185,8 @@ def csr(n=48):
         torch.cuda.empty_cache()
 
 
-def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False, h_coarse=(), coarse_iterations=30):
+def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False, h_coarse=(), coarse_iterations=30,
+       smoothing_degree=2):
     """p-multigrid flexible PCG vs Jacobi-PCG on the C5 problem (CG P3, homogeneous
     Dirichlet, RHS uniform[-1,1]): iterations and device time to ||r|| <= tol ||b||."""
     import torch
@@ -199,7 +200,7 @@ def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False,
     t0 = time.time()
     m = reorder_mesh(M.kuhn_cube_mesh(n, seed=0))
     mg_ = PMultigrid(m, degrees, coarse_iterations=coarse_iterations, precision=precision,
-                     coarse_matrix=coarse_matrix, h_coarse=h_coarse)
+                     coarse_matrix=coarse_matrix, h_coarse=h_coarse, smoothing_degree=smoothing_degree)
     setup = time.time() - t0
     dm = mg_.levels[0].dm
     nd = dm.n_global_dofs
@@ -312,11 +313,18 @@ if __name__ == "__main__":
     ap.add_argument("--h-coarse", default="", help="comma-separated coarse Kuhn sizes, e.g. 64,32,16,8")
     ap.add_argument("--coarse-iterations", type=int, default=30)
     ap.add_argument("--dg-smoothing-degree", type=int, default=None)
+    ap.add_argument("--smoothing-degree", type=int, default=2)
+    ap.add_argument("--best", action="store_true",
+                    help="mg: the fastest measured hierarchy (fp32 V-cycle in a CUDA graph, CSR P1 level, "
+                         "h-levels n/2..n/16, Chebyshev degree 3, 10 coarse iterations)")
     a = ap.parse_args()
     for c in a.configs:
         {"c1": c1, "c2": c2, "c3": lambda: c3(a.n3), "c4": lambda: c4(a.n4), "c5": lambda: c5(a.n5),
-         "csr": csr, "mg": lambda: mg(a.n5, precision=a.precision, coarse_matrix=a.coarse_matrix,
-                         h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v),
-                         coarse_iterations=a.coarse_iterations), "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale,
+         "csr": csr, "mg": (lambda: mg(a.n5, precision="mixed", coarse_matrix=True,
+                          h_coarse=tuple(a.n5 // 2 ** k for k in range(1, 5) if a.n5 // 2 ** k >= 2),
+                          coarse_iterations=10, smoothing_degree=3)) if a.best else
+              (lambda: mg(a.n5, precision=a.precision, coarse_matrix=a.coarse_matrix,
+                          h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v),
+                          coarse_iterations=a.coarse_iterations, smoothing_degree=a.smoothing_degree)), "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale,
                              h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v),
                              fine_smoothing_degree=a.dg_smoothing_degree)}[c]()
