@@ -225,6 +225,7 @@ static cudaError_t launch_cell_t(const CellArgs& a, int n_sm, cudaStream_t st, C
     if (variant == 5) return launch_cell_v<N, Q, MASS, DG, DB, 0, 1, false, false, false, false, 3>(a, n_sm, st, info);
     if (variant == 6) return launch_cell_v<N, Q, MASS, DG, DB, 0, 1, false, false, false, false, 2>(a, n_sm, st, info);
     if (variant == 7) return launch_cell_v<N, Q, MASS, DG, DB, 0, 1, false, false, false, false, 4>(a, n_sm, st, info);
+    if (variant == 9) return launch_cell_v<N, Q, MASS, DG, 1024, 0, 1>(a, n_sm, st, info);   // 64 registers, 32 warps
   }
   if (!DG && !MASS) {
     if (variant == 1) return launch_cell_v<N, Q, MASS, DG, BLOCK, 2, 1>(a, n_sm, st, info);
