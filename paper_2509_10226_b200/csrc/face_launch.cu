@@ -40,6 +40,25 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
   return cudaGetLastError();
 }
 
+// Interior faces, MB batches per warp iteration (face_mb_kernel)
+template <int N, int QF, int MB, int MINB, bool BLOCKED>
+static cudaError_t launch_face_mb(const FaceArgs& a, int n_sm, cudaStream_t st) {
+  using S = FaceShape<N, QF>;
+  constexpr int SMEM = 2 * S::NFRAG * 32 * 8;
+  auto kern = face_mb_kernel<N, QF, MB, MINB, 256, BLOCKED>;
+  if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaError_t e = blocks_per_sm(kern, 256, SMEM, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t work = a.n_chunks * a.nc;
+  if (work == 0) return cudaSuccess;
+  int64_t blocks = (int64_t)n_sm * per_sm;
+  if (blocks > work) blocks = work;
+  kern<<<(unsigned)blocks, 256, SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
 // Reference-tensor interior-face kernel (face_tensor_kernel.cuh)
 template <int N, int BLOCK, int MINB, bool PF>
 static cudaError_t launch_face_x(const FaceArgs& a, int n_sm, cudaStream_t st) {
@@ -120,11 +139,14 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
   if (variant == 8) return launch_face_v<N, QF, BND, 1, 6, 128>(a, n_sm, st, info);
   if (variant == 9) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
   if (variant == 10) return launch_face_v<N, QF, BND, 2, 2, 256, true>(a, n_sm, st, info);
-  // round-robin chunks (all CTAs march through the chunk list together, keeping the
-  // live u / y in L2) + cp.async prefetch of the next chunk's tables: measured
-  // 5-15 % slower than the blocked default at C3 / C4 sizes (barrier per chunk)
-  if (variant == 11) return launch_face_v<N, QF, BND, 1, 3, 256, false, true>(a, n_sm, st, info);
-  if (variant == 12) return launch_face_v<N, QF, BND, 2, 2, 256, false, true>(a, n_sm, st, info);
+  // (variants 11 / 12 were round-robin chunks + cp.async table prefetch, TPF: measured 5-15 %
+  // slower than the blocked default at C3 / C4 sizes; they now select the two-batch kernel)
+  if constexpr (!BND) {
+    if (!info && a.peer.u == nullptr && (variant == 11 || variant == 12)) {
+      if (variant == 11) return launch_face_mb<N, QF, 2, 2, false>(a, n_sm, st);
+      return launch_face_mb<N, QF, 2, 2, true>(a, n_sm, st);
+    }
+  }
   if constexpr (!BND) {   // asynchronous gather ring (no peers)
     if (!info && a.peer.u == nullptr && variant >= 13) {
       cudaError_t e = cudaErrorNotSupported;
