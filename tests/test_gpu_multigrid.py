@@ -436,3 +436,32 @@ def test_graph_replayed_vcycle_matches_eager():
     assert rel_l2(z2.cpu().numpy(), 2.0 * z0.cpu().numpy()) <= 1e-4
     _, h = graph.solve(r, tol=1e-10, maxiter=60)
     assert h[-1] <= 1e-10 * h[0]
+
+
+def test_transfer_c_abi_rejects_bad_input():
+    """C-ABI argument checks of the transfer entry points (TMF_EINVAL -> ValueError)."""
+    import ctypes as C
+
+    from paper_2509_10226_b200 import _lib
+
+    L = _lib.lib()
+    fd = np.zeros((1, 10), np.int32)
+    cd = np.zeros((1, 4), np.int32)
+    P = np.zeros((10, 4))
+    d = _lib.TransferDesc()
+    d.n_cells, d.n_fine_dpc, d.n_coarse_dpc, d.n_fine_dofs, d.n_coarse_dofs = 1, 10, 4, 1, 1
+    d.fine_cell_dofs, d.coarse_cell_dofs = _lib.ptr(fd, C.c_int32), _lib.ptr(cd, C.c_int32)
+    d.interp = _lib.ptr(P, C.c_double)
+    t = C.c_void_p()
+    fd[0, 3] = 7                                     # fine DoF out of range
+    with pytest.raises(ValueError, match="out of range"):
+        _lib.check(L.tmf_transfer_create(C.byref(d), C.byref(t)))
+    d.n_coarse_dpc = 5                               # unsupported coarse space
+    with pytest.raises(ValueError):
+        _lib.check(L.tmf_transfer_create(C.byref(d), C.byref(t)))
+    pd = _lib.PointTransferDesc()
+    pd.n_fine_dofs, pd.n_coarse_dofs, pd.entries_per_row = 1, 1, 3
+    with pytest.raises(ValueError):
+        _lib.check(L.tmf_transfer_create_points(C.byref(pd), C.byref(t)))
+    with pytest.raises(ValueError):
+        _lib.check(L.tmf_prolongate(None, None, None, 0, None))

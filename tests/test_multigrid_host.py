@@ -140,3 +140,16 @@ def test_kuhn_point_weights_locate_and_interpolate(nf, nc):
     # a fine vertex that coincides with a coarse vertex maps onto it alone
     idx2, w2 = kuhn_point_weights(mc.vertices, nc)
     assert np.allclose(np.take_along_axis(w2, np.argmax(w2, axis=1)[:, None], 1), 1.0)
+
+
+def test_color_cells_rejects_bad_faces():
+    from paper_2509_10226_b200.multigrid import color_cells
+
+    m = M.kuhn_cube_mesh(2, seed=0)
+    bad = type("Mesh", (), {"n_cells": m.n_cells, "interior_faces": m.interior_faces.copy()})()
+    bad.interior_faces[0, 2] = m.n_cells + 5
+    with pytest.raises(ValueError):
+        color_cells(bad)
+    empty = type("Mesh", (), {"n_cells": 1, "interior_faces": np.zeros((0, 5), np.int32)})()
+    col, nc = color_cells(empty)
+    assert nc == 1 and col.tolist() == [0]
