@@ -159,10 +159,13 @@ def cell_loop(u, y, gidx, Eg, jit, jxw, Ev=None, mass_jxw=None, mass_scale=0.0,
 
 # ------------------------------------------------------------------ operators
 def cg_apply(vertices, cells, cell_dofs, dirichlet_mask, grad_matrix, weights, u,
-             batch_cells=None):
-    """CgPoissonOperator.apply (operator.py:320-331)."""
+             batch_cells=None, kappa=None):
+    """CgPoissonOperator.apply (operator.py:320-331); ``kappa``: per-cell coefficient of the
+    stiffness term ("multiply the stiffness part by kappa_e")."""
     u = np.asarray(u, dtype=np.float64)
     jit, jxw, _ = affine_cell_geometry(vertices, cells, weights)
+    if kappa is not None:
+        jxw = jxw * np.asarray(kappa, dtype=np.float64)[:, None]
     gidx = cell_dofs.astype(np.int64).copy()
     if dirichlet_mask is not None and dirichlet_mask.any():
         gidx[dirichlet_mask[gidx]] = -1
@@ -253,10 +256,12 @@ def dg_apply(vertices, cells, n_dpc, interior_faces, boundary_faces, dirichlet_i
     return y
 
 
-def cg_diagonal(vertices, cells, cell_dofs, dirichlet_mask, grad_matrix, weights, n_dofs):
+def cg_diagonal(vertices, cells, cell_dofs, dirichlet_mask, grad_matrix, weights, n_dofs, kappa=None):
     """Diagonal of the CG operator (identity on Dirichlet rows): the matrix-free
     equivalent of sparse.assemble(...).diagonal() (sparse.py:237-243)."""
     jit, jxw, _ = affine_cell_geometry(vertices, cells, weights)
+    if kappa is not None:
+        jxw = jxw * np.asarray(kappa, dtype=np.float64)[:, None]
     nq = grad_matrix.shape[0] // 3
     g3 = grad_matrix.reshape(nq, 3, -1)
     B = np.einsum("eij,qja->eqia", jit, g3)

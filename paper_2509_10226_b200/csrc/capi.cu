@@ -1486,7 +1486,7 @@ int tmf_diagonal(tmf_plan* P, double* diag, void* stream) {
   TMF_CUDA(cudaSetDevice(P->dev));
   cudaStream_t st = (cudaStream_t)stream;
   TMF_CUDA(cudaMemsetAsync(diag, 0, sizeof(double) * P->n_global, st));
-  tmf::DiagArgs a{diag, P->dofs, P->cells, P->verts, P->diag_S, P->n_cells, P->N, P->nc};
+  tmf::DiagArgs a{diag, P->dofs, P->cells, P->verts, P->diag_S, P->n_cells, P->N, P->nc, P->cell_geo};
   tmf::diag_kernel<<<P->n_sm * 8, 256, 0, st>>>(a);
   TMF_CUDA(cudaGetLastError());
   if (P->n_fix) {

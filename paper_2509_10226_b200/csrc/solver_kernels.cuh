@@ -21,6 +21,7 @@ struct DiagArgs {
   const double* __restrict__ verts;
   const double* __restrict__ S;    // (6, n_dpc): 00,01,02,11,12,22
   int64_t n_cells;
+  const double* __restrict__ cgeo = nullptr;  // plan geometry (G scaled by any per-cell kappa)
   int n_dpc;
   int nc;
 };
@@ -28,14 +29,19 @@ struct DiagArgs {
 __global__ void diag_kernel(DiagArgs a) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.n_cells;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int vid[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) vid[i] = __ldg(a.cells + 4 * e + i);
-    Affine g;
-    affine_from_vertices(load_vertex(a.verts, vid[0]), load_vertex(a.verts, vid[1]),
-                         load_vertex(a.verts, vid[2]), load_vertex(a.verts, vid[3]), g);
     double G[6];
-    stiffness_metric(g, 1.0, G);
+    if (a.cgeo) {   // the apply's own metric (includes the stiffness scale and per-cell kappa)
+#pragma unroll
+      for (int i = 0; i < 6; ++i) G[i] = __ldg(a.cgeo + 8 * e + i);
+    } else {
+      int vid[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) vid[i] = __ldg(a.cells + 4 * e + i);
+      Affine g;
+      affine_from_vertices(load_vertex(a.verts, vid[0]), load_vertex(a.verts, vid[1]),
+                           load_vertex(a.verts, vid[2]), load_vertex(a.verts, vid[3]), g);
+      stiffness_metric(g, 1.0, G);
+    }
     const int n = a.n_dpc;
     for (int j = 0; j < n; ++j) {
       const int dof = __ldg(a.dofs + e * n + j);

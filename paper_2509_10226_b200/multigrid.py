@@ -247,6 +247,8 @@ class _Level:
 class PMultigrid:
     """p-multigrid V-cycle on CG Laplace (homogeneous Dirichlet on ``dirichlet_ids``).
 
+    ``kappa``: per-cell coefficient of the CG levels' Laplacians (with a KappaHelmholtzOperator
+    on top: the C4 operator's auxiliary CG space).
     ``fine_operator``: a DG operator (DgSipgOperator / HelmholtzOperator / KappaHelmholtzOperator
     of degree ``degrees[0]``, weak Dirichlet on ``dirichlet_ids``) to put on top of the CG levels
     through a c-transfer (the paper's cp-MG); its smoother uses the exact
@@ -256,7 +258,7 @@ class PMultigrid:
                  smoothing_range: float = 15.0, coarse_iterations: int = 30, eig_iterations: int = 15,
                  lmax=None, config=None, seed: int = 0, fine_operator=None, precision: str = "f64",
                  coarse_matrix: bool = False, h_coarse=(), fine_smoothing_degree: int | None = None,
-                 graph: bool = True):
+                 graph: bool = True, kappa=None):
         import torch
 
         from . import operator as op
@@ -286,6 +288,8 @@ class PMultigrid:
         from . import mesh as M
 
         h_coarse = tuple(int(n) for n in h_coarse)
+        if kappa is not None and h_coarse:
+            raise ValueError("a per-cell kappa lives on the fine mesh: no h-levels with kappa")
         if h_coarse and degrees[-1] != 1:
             raise ValueError("h-coarsening continues from a P1 level: degrees must end with 1")
         specs = [("cg", p, mesh) for p in degrees]
@@ -307,7 +311,7 @@ class PMultigrid:
                 bas = B.tabulate_basis(p, cr, fr)
                 geo = GeometryData("affine", cr, fr, None, None, None, None)
                 dm = D.build_dof_map(lmesh, p, "cg", 1, tuple(dirichlet_ids))
-                A = op.CgPoissonOperator(lmesh, dm, geo, bas, self.config)
+                A = op.CgPoissonOperator(lmesh, dm, geo, bas, self.config, kappa=kappa)
                 dinv = 1.0 / A.diagonal()
             lv = _Level(p, dm, A, dinv, 0.0, [])
             lv.mesh = lmesh
@@ -336,7 +340,7 @@ class PMultigrid:
             lv = self.levels[self.p1_fine_level]
             cr, fr = Q.make_cell_quadrature(lv.p), Q.make_face_quadrature(lv.p)
             A = assemble_cg_csr(lv.mesh, lv.dm, GeometryData("affine", cr, fr, None, None, None, None),
-                                B.tabulate_basis(lv.p, cr, fr), device=self.device)
+                                B.tabulate_basis(lv.p, cr, fr), device=self.device, kappa=kappa)
             lv.csr = A.to(torch.float32) if self.mixed else A
             self.coarse_csr = lv.csr
         self.transfers = []

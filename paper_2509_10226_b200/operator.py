@@ -310,10 +310,12 @@ class CgPoissonOperator(_B200Operator):
 
     _kind = _lib.TMF_CG_LAPLACE
 
-    def __init__(self, mesh, dofmap, geometry, basis, config=None):
+    def __init__(self, mesh, dofmap, geometry, basis, config=None, kappa=None):
+        """``kappa`` (B200 extension, keyword only in practice): per-cell coefficient of the
+        Laplacian, -div(kappa grad u); None = the reference operator."""
         if dofmap.space != "cg":
             raise ValueError("CG operator needs a CG dof map")
-        super().__init__(mesh, dofmap, geometry, basis, config)
+        super().__init__(mesh, dofmap, geometry, basis, config, kappa=kappa)
 
     def diagonal(self, stream: int = 0):
         """Matrix-free diag(A) as a CUDA tensor (identity on Dirichlet rows)."""

@@ -29,8 +29,9 @@ def _metric(vertices, cells):
     return G
 
 
-def assemble_cg_csr(mesh, dofmap, geometry, basis, device="cuda"):
-    """torch sparse CSR matrix (fp64, on ``device``) of the CG Laplace operator."""
+def assemble_cg_csr(mesh, dofmap, geometry, basis, device="cuda", kappa=None):
+    """torch sparse CSR matrix (fp64, on ``device``) of the CG Laplace operator
+    (``kappa``: per-cell coefficient, -div(kappa grad u))."""
     import torch
 
     nq = len(geometry.cell_rule.weights)
@@ -38,7 +39,10 @@ def assemble_cg_csr(mesh, dofmap, geometry, basis, device="cuda"):
     w = np.asarray(geometry.cell_rule.weights)
     Eg = np.asarray(basis.grad_matrix).reshape(nq, 3, nd)
     S = np.einsum("q,qka,qlb->klab", w, Eg, Eg).reshape(9, nd * nd)            # (9, nd^2)
-    G = torch.from_numpy(_metric(mesh.vertices, mesh.cells).reshape(-1, 9)).to(device)
+    Gn = _metric(mesh.vertices, mesh.cells).reshape(-1, 9)
+    if kappa is not None:
+        Gn = Gn * np.asarray(kappa, dtype=np.float64)[:, None]
+    G = torch.from_numpy(Gn).to(device)
     Ke = G @ torch.from_numpy(S).to(device)                                      # (n_cells, nd^2)
     cd = torch.from_numpy(dofmap.cell_dofs.astype(np.int64)).to(device)
     rows = cd[:, :, None].expand(-1, nd, nd).reshape(-1)
