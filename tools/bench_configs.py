@@ -248,7 +248,8 @@ def mg(n=128, degrees=(3, 2, 1), tol=1e-8, precision="f64", coarse_matrix=False,
     mg_.close()
 
 
-def mgdg(n=64, p=3, tol=1e-8, tau_scale=1.0, h_coarse=(), precision="f64", fine_smoothing_degree=None):
+def mgdg(n=64, p=3, tol=1e-8, tau_scale=1.0, h_coarse=(), precision="f64", fine_smoothing_degree=None,
+         helmholtz=False):
     """cp-multigrid (DG p -> CG p -> ... -> CG 1) flexible PCG vs Jacobi-PCG on the C3 problem
     (DG-SIPG P3, weak Dirichlet on all sides, RHS uniform[-1,1]): iterations / time to tol."""
     import torch
@@ -262,9 +263,14 @@ def mgdg(n=64, p=3, tol=1e-8, tau_scale=1.0, h_coarse=(), precision="f64", fine_
     sipg = op.baseline_sipg_tau(m, p, 1.0 / n)
     sipg.tau_interior *= tau_scale
     sipg.tau_boundary *= tau_scale
-    A = op.DgSipgOperator(m, dm, geo, bas, sipg, dirichlet_ids=range(6))
+    kap = None
+    if helmholtz:   # C4: mass + kappa-Laplace, kappa log-uniform in [0.1, 10] (seed 2)
+        kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
+        A = op.KappaHelmholtzOperator(m, dm, geo, bas, sipg, kap, 1.0, dirichlet_ids=range(6))
+    else:
+        A = op.DgSipgOperator(m, dm, geo, bas, sipg, dirichlet_ids=range(6))
     mg_ = PMultigrid(m, tuple(range(p, 0, -1)), fine_operator=A, coarse_iterations=50 if h_coarse else 30,
-                     h_coarse=h_coarse, fine_smoothing_degree=fine_smoothing_degree)
+                     h_coarse=h_coarse, fine_smoothing_degree=fine_smoothing_degree, kappa=kap)
     setup_mg = time.time() - t0
     nd = dm.n_global_dofs
     bt = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, nd)).cuda()
@@ -287,7 +293,8 @@ def mgdg(n=64, p=3, tol=1e-8, tau_scale=1.0, h_coarse=(), precision="f64", fine_
     t_j = e0.elapsed_time(e1)
     hit = np.nonzero(hj <= tol * hj[0])[0]
     kj = int(hit[0]) if len(hit) else None
-    print(json.dumps({"config": f"cp-multigrid PCG vs Jacobi-PCG, DG-SIPG P{p} {n}^3x6 reordered, weak Dirichlet, "
+    what = "DG kappa-Helmholtz (C4 operator)" if helmholtz else "DG-SIPG"
+    print(json.dumps({"config": f"cp-multigrid PCG vs Jacobi-PCG, {what} P{p} {n}^3x6 reordered, weak Dirichlet, "
                       f"tol {tol}", "tau": f"{tau_scale} x 2.5 (p+1)^2 / h", "h_levels": list(h_coarse),
                       "dg_smoothing_degree": len(mg_.levels[0].coeffs), "ndof": nd, "levels": ["dg%d" % p] + ["cg%d" % lv.p for lv in mg_.levels[1:]],
                       "lmax": [round(lv.lmax, 4) for lv in mg_.levels[:-1]],
@@ -325,6 +332,7 @@ if __name__ == "__main__":
                           coarse_iterations=10, smoothing_degree=3)) if a.best else
               (lambda: mg(a.n5, precision=a.precision, coarse_matrix=a.coarse_matrix,
                           h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v),
-                          coarse_iterations=a.coarse_iterations, smoothing_degree=a.smoothing_degree)), "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale,
+                          coarse_iterations=a.coarse_iterations, smoothing_degree=a.smoothing_degree)), "mgc4": lambda: mgdg(a.n4, p=2, tau_scale=a.tau_scale, helmholtz=True),
+         "mgdg": lambda: mgdg(a.n3, tau_scale=a.tau_scale,
                              h_coarse=tuple(int(v) for v in a.h_coarse.split(",") if v),
                              fine_smoothing_degree=a.dg_smoothing_degree)}[c]()
