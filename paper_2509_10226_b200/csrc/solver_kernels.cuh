@@ -21,9 +21,9 @@ struct DiagArgs {
   const double* __restrict__ verts;
   const double* __restrict__ S;    // (6, n_dpc): 00,01,02,11,12,22
   int64_t n_cells;
-  const double* __restrict__ cgeo = nullptr;  // plan geometry (G scaled by any per-cell kappa)
   int n_dpc;
   int nc;
+  const double* __restrict__ cgeo = nullptr;  // plan geometry (G scaled by any per-cell kappa)
 };
 
 __global__ void diag_kernel(DiagArgs a) {
