@@ -224,6 +224,43 @@ def cpu_reference(args, sample_s, workers=None):
 
 
 # ----------------------------------------------------------------- GPU arm
+def measure_link(problems, reps):
+    """Pinned host <-> device copy rates of this box, measured live on the largest plan's
+    vectors (H2D alone, D2H alone, both at once on two streams), and the lower bound they put
+    on one e2e step: every plan's u goes up and its y comes down, a plan's D2H cannot start
+    before its own H2D has finished, so a step takes at least max((H + D) / duplex,
+    (H + s_max) / min(h2d, d2h)) whatever the order (two-stage flow shop, equal job sizes)."""
+    import torch
+
+    big = max(problems, key=lambda pr: pr["ndof"])
+    nbytes = 8 * big["ndof"]
+    dev_u = torch.empty(big["ndof"], dtype=torch.float64, device="cuda")
+    dev_y = big["y"][: big["ndof"]]
+    s_up, s_dn = torch.cuda.Stream(), torch.cuda.Stream()
+    reps = max(3, reps)
+
+    def rate(up, dn):
+        dev_u.copy_(big["u_pin"], non_blocking=True)   # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            if up:
+                with torch.cuda.stream(s_up):
+                    dev_u.copy_(big["u_pin"], non_blocking=True)
+            if dn:
+                with torch.cuda.stream(s_dn):
+                    big["y_pin"].copy_(dev_y, non_blocking=True)
+        torch.cuda.synchronize()
+        return (up + dn) * nbytes * reps / (time.perf_counter() - t0) / 1e9
+
+    h2d, d2h, duplex = rate(True, False), rate(False, True), rate(True, True)
+    tot = sum(8 * pr["ndof"] for pr in problems)
+    bound_s = max(2 * tot / (duplex * 1e9), (tot + nbytes) / (min(h2d, d2h) * 1e9))
+    del dev_u
+    return {"h2d_GBs": round(h2d, 1), "d2h_GBs": round(d2h, 1), "duplex_GBs": round(duplex, 1),
+            "step_bound_ms": round(bound_s * 1e3, 3)}
+
+
 def gpu_bench(args, rank, world):
     import torch
 
@@ -384,6 +421,8 @@ def gpu_bench(args, rank, world):
     y0 = pr0["y"][: pr0["ndof"]].cpu()
     err = float(torch.linalg.vector_norm(y0 - pr0["y_pin"]) / torch.linalg.vector_norm(pr0["y_pin"]))
 
+    link = measure_link(problems, args.steps) if (world == 1 and not args.dist) else None
+
     per = {}
     for pr in problems:
         key = f"p{pr['p']}{'_reordered' if pr['reorder'] else ''}"
@@ -445,7 +484,7 @@ def gpu_bench(args, rank, world):
                                          "(tmf_plan_info.flops_engine: modal 12 M N + 18 M + N per cell, M = dim "
                                          "P_(p-1), N = DoFs per cell; reference tensor 12 N^2 + 13 N) / CUDA-event "
                                          "kernel time"},
-                gpu_launches=n_kern, parity_rel_l2=err,
+                gpu_launches=n_kern, parity_rel_l2=err, link=link,
                 h2d=sum(8 * pr["ndof"] for pr in problems), d2h=sum(8 * pr["ndof"] for pr in problems))
 
 
@@ -534,7 +573,11 @@ def main():
                 "per_degree": r["per"], "roofline": r["roofline"], "cpu_baseline": cpu,
                 "quadrature_engine": r["quadrature_engine"],
                 "e2e": {"value": round(e2e_val, 4), "unit": unit, "h2d_bytes_per_step": r["h2d"],
-                        "d2h_bytes_per_step": r["d2h"], "path": "Operator.apply_host_async(pinned host u, y) -> tmf_apply_host_async, one stream per plan, largest first"},
+                        "d2h_bytes_per_step": r["d2h"], "path": "Operator.apply_host_async(pinned host u, y) -> tmf_apply_host_async, one stream per plan, largest first",
+                        "ms_per_step": round(e2e_s / args.steps * 1e3, 3),
+                        # the box's PCIe link measured live; frac = link lower bound / measured step
+                        "link": None if r["link"] is None else dict(
+                            r["link"], frac=round(r["link"]["step_bound_ms"] / (e2e_s / args.steps * 1e3), 3))},
                 "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "parity_e2e_vs_timed_rel_l2": r["parity_rel_l2"]}
         emit(line)
     if world > 1 or args.dist:
