@@ -394,14 +394,19 @@ def gpu_bench(args, rank, world):
     e2e_order = sorted(problems, key=lambda pr: -pr["ndof"]) if os.environ.get("TMF_E2E_ORDER", "desc") == "desc" \
         else list(problems)
     streams = [torch.cuda.Stream() for _ in range(n_streams)]
+    e2e_multi = os.environ.get("TMF_E2E_PATH", "streams") == "multi"
 
     def e2e_step():
         if world == 1 and not args.dist:
             # public C-ABI with host buffers; the plans' H2D / kernels / D2H are
             # pipelined on one stream per plan, so the H2D and D2H copy engines and the
             # SMs work on different plans at the same time
-            for i, pr in enumerate(e2e_order):
-                pr["A"].apply_host_async(pr["u_pin"], pr["y_pin"], streams[i % len(streams)].cuda_stream)
+            if e2e_multi:
+                op.apply_host_multi([pr["A"] for pr in e2e_order], [pr["u_pin"] for pr in e2e_order],
+                                    [pr["y_pin"] for pr in e2e_order], streams[0].cuda_stream)
+            else:
+                for i, pr in enumerate(e2e_order):
+                    pr["A"].apply_host_async(pr["u_pin"], pr["y_pin"], streams[i % len(streams)].cuda_stream)
             torch.cuda.synchronize()
             return
         for pr in problems:   # host -> device, partitioned apply (NCCL halo), device -> host

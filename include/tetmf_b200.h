@@ -140,6 +140,17 @@ int tmf_apply_host(tmf_plan* plan, const double* u_host, double* y_host);
  * against each other's kernels. */
 int tmf_apply_host_async(tmf_plan* plan, const double* u_host, double* y_host, void* stream);
 
+/* Several plans' host applies as one pipeline, asynchronous on `stream`: the
+ * uploads of u_hosts[0..n) run back to back in that order on one copy stream,
+ * the kernels on one compute stream (plan i's kernels wait only for plan i's
+ * upload), the downloads on the other copy direction (plan i's download waits
+ * only for plan i's kernels); `stream` is ordered before and after the whole
+ * pipeline.  Same results as n tmf_apply_host_async calls (the reference has no
+ * batched call; it replaces the caller's loop over operator.apply(u) calls,
+ * operator.py:320-331).  All plans on one device; host buffers pinned. */
+int tmf_apply_host_multi(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
+                         void* stream);
+
 /* Per-stage timing of `reps` back-to-back applies (device pointers), CUDA
  * events on `stream`: out_ms[0] = total, out_ms[1..] = per kernel class
  * (cell, face, fixup).  For the bench only. */

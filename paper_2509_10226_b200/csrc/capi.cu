@@ -11,6 +11,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -1445,6 +1446,75 @@ int tmf_apply_host_async(tmf_plan* P, const double* u_host, double* y_host, void
   int rc = launch_apply(P, P->stage_u, P->stage_y, st, nullptr);
   if (rc) return rc;
   TMF_CUDA(cudaMemcpyAsync(y_host, P->stage_y, bytes, cudaMemcpyDeviceToHost, st));
+  return TMF_OK;
+}
+
+// Several plans' host applies as one three-stage pipeline: every upload on one copy stream
+// in the caller's order, the kernels on one compute stream (each waits for its own upload),
+// every download on a second copy stream (each waits for its own kernels).  Per-plan
+// streams would let the copy engine interleave all uploads, so the first kernel (and the
+// first download) would wait for most of the uploads instead of one.
+namespace {
+struct HostPipe {
+  cudaStream_t up = nullptr, comp = nullptr, down = nullptr;
+};
+HostPipe g_pipe[64];
+std::mutex g_pipe_mu;
+}  // namespace
+
+int tmf_apply_host_multi(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
+                         void* stream) {
+  if (n < 0 || (n > 0 && (!plans || !u_hosts || !y_hosts))) return fail(TMF_EINVAL, "null argument");
+  if (n == 0) return TMF_OK;
+  for (int i = 0; i < n; ++i) {
+    if (!plans[i] || !u_hosts[i] || !y_hosts[i]) return fail(TMF_EINVAL, "null plan or host buffer");
+    if (plans[i]->dev != plans[0]->dev) return fail(TMF_EINVAL, "plans on different devices");
+  }
+  const int dev = plans[0]->dev;
+  if (dev < 0 || dev >= 64) return fail(TMF_EINVAL, "device index out of range");
+  TMF_CUDA(cudaSetDevice(dev));
+  HostPipe pp;
+  {
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    HostPipe& p = g_pipe[dev];
+    if (!p.up) {
+      TMF_CUDA(cudaStreamCreateWithFlags(&p.up, cudaStreamNonBlocking));
+      TMF_CUDA(cudaStreamCreateWithFlags(&p.comp, cudaStreamNonBlocking));
+      TMF_CUDA(cudaStreamCreateWithFlags(&p.down, cudaStreamNonBlocking));
+    }
+    pp = p;
+  }
+  for (int i = 0; i < n; ++i) {
+    tmf_plan* P = plans[i];
+    if (!P->stage_u) {
+      const size_t bytes = sizeof(double) * P->n_global;
+      TMF_CUDA(cudaMalloc(&P->stage_u, bytes));
+      TMF_CUDA(cudaMalloc(&P->stage_y, bytes));
+    }
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t ev;
+  auto link = [&](cudaStream_t from, cudaStream_t to) -> int {
+    TMF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TMF_CUDA(cudaEventRecord(ev, from));
+    TMF_CUDA(cudaStreamWaitEvent(to, ev, 0));
+    TMF_CUDA(cudaEventDestroy(ev));  // released once the wait has been satisfied
+    return TMF_OK;
+  };
+  int rc;
+  // the caller's prior work on `stream` (e.g. writes into the host buffers' sources) comes first
+  if ((rc = link(st, pp.up)) || (rc = link(st, pp.comp)) || (rc = link(st, pp.down))) return rc;
+  for (int i = 0; i < n; ++i) {
+    tmf_plan* P = plans[i];
+    const size_t bytes = sizeof(double) * P->n_global;
+    TMF_CUDA(cudaMemcpyAsync(P->stage_u, u_hosts[i], bytes, cudaMemcpyHostToDevice, pp.up));
+    if ((rc = link(pp.up, pp.comp))) return rc;
+    if ((rc = launch_apply(P, P->stage_u, P->stage_y, pp.comp, nullptr))) return rc;
+    if ((rc = link(pp.comp, pp.down))) return rc;
+    TMF_CUDA(cudaMemcpyAsync(y_hosts[i], P->stage_y, bytes, cudaMemcpyDeviceToHost, pp.down));
+  }
+  // `stream` reaches the end of the pipeline only when every download has landed
+  if ((rc = link(pp.down, st)) || (rc = link(pp.comp, st)) || (rc = link(pp.up, st))) return rc;
   return TMF_OK;
 }
 

@@ -378,3 +378,32 @@ def apply_dg_sipg(config, mesh, dofmap, geometry, basis, sipg, u, dirichlet_ids=
 
 def apply_helmholtz(config, mesh, dofmap, geometry, basis, sipg, coeffs, u, dirichlet_ids=()):
     return HelmholtzOperator(mesh, dofmap, geometry, basis, sipg, coeffs, config, dirichlet_ids).apply(u)
+
+
+def apply_host_multi(operators, u_hosts, y_hosts, stream: int = 0):
+    """y_hosts[i] = operators[i] u_hosts[i] for several operators as one pipelined call
+    (``tmf_apply_host_multi``): uploads back to back in the given order, each plan's
+    kernels as soon as its own upload has landed, downloads overlapping the next plans'
+    uploads.  Enqueued on ``stream`` and returns; the host buffers (pinned tensors or
+    arrays) must outlive the stream work.  Replaces a caller's loop of
+    ``operator.apply(u)`` calls (reference operator.py:320-331)."""
+    ops, us, ys = list(operators), list(u_hosts), list(y_hosts)
+    if not (len(ops) == len(us) == len(ys)):
+        raise ValueError("operators, u_hosts and y_hosts differ in length")
+
+    def ptr(t):
+        return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+
+    for A, u, y in zip(ops, us, ys):
+        for t in (u, y):
+            n = t.numel() if hasattr(t, "numel") else len(t)
+            if n != A.n_global_dofs:
+                raise ValueError("host buffer length does not match the operator size")
+    n = len(ops)
+    arr = C.c_void_p * max(n, 1)
+    plans = arr(*[A._plan.value for A in ops])
+    up = arr(*[ptr(u) for u in us])
+    yp = arr(*[ptr(y) for y in ys])
+    _lib.check(_lib.lib().tmf_apply_host_multi(plans, up, yp, n, C.c_void_p(stream)))
+    for A in ops:
+        A._count()

@@ -46,6 +46,33 @@ def test_out_buffer_and_async_host_path():
     assert rel_l2(y_pin.numpy(), g["y"]) <= 1e-12
 
 
+def test_host_multi_pipeline_matches_goldens():
+    """tmf_apply_host_multi: CG and DG plans (mixed sizes, one plan twice) in one pipelined
+    call give the golden results; a length mismatch or an empty list is handled."""
+    import torch
+
+    from paper_2509_10226_b200 import operator as op
+
+    names = ["cg_p2_n8_gm_dir", "dg_p3_n3_gm_dir", "cg_p4_n3_gm", "helmk_p2_n3_gm_dir"]
+    gs = [load_golden(n) for n in names]
+    ops = [operator_from_fixture(g) for g in gs]
+    ops.append(ops[0])
+    gs.append(gs[0])
+    us = [torch.from_numpy(np.ascontiguousarray(g["u"])).pin_memory() for g in gs]
+    ys = [torch.full_like(u, np.nan).pin_memory() for u in us]
+    s = torch.cuda.Stream()
+    op.apply_host_multi(ops, us, ys, s.cuda_stream)
+    s.synchronize()
+    for g, y in zip(gs, ys):
+        assert rel_l2(y.numpy(), g["y"]) <= 1e-12
+    assert ops[0].n_applies == 2
+    op.apply_host_multi([], [], [], s.cuda_stream)
+    with pytest.raises(ValueError, match="does not match"):
+        op.apply_host_multi(ops[:1], us[1:2], ys[1:2])
+    with pytest.raises(ValueError, match="differ in length"):
+        op.apply_host_multi(ops[:2], us[:1], ys[:2])
+
+
 def test_wrong_space_and_missing_faces():
     from paper_2509_10226_b200 import operator as op
 
