@@ -519,7 +519,12 @@ def main():
         val, cores, detail = cpu_reference(args, args.cpu_sample_s)
         line = {"impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
-                "data": "synthetic", "config": {"workload": workload},
+                "data": "synthetic",
+                # same workload as the b200 arm at this world size; the bounded CPU sample is drawn
+                # from the 48^3 mesh (the per-DoF rate of the batched loop does not depend on size)
+                "config": {"workload": workload,
+                           "global_mesh": f"{args.n if world == 1 else int(round(args.n * world ** (1.0 / 3.0)))}^3 x 6",
+                           "sample_mesh": f"{args.n}^3 x 6"},
                 "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "port",
                                  "sample": f"oracle port of the reference batched NumPy loop (16-cell batches), "
                                            f"~{args.cpu_sample_s}s per worker per degree, extrapolated per DoF",
