@@ -1462,13 +1462,34 @@ HostPipe g_pipe[64];
 std::mutex g_pipe_mu;
 }  // namespace
 
-int tmf_apply_host_multi(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
-                         void* stream) {
+// sched (nb blocks, CG plans only): cell_split[nb+1], u_end[nb] (u[0, u_end[k]) has landed before
+// block k's cells run), y_end[nb] (y[0, y_end[k]) is final after block k), fix_split[nb+1]
+// (Dirichlet list entries block k writes; the list is ascending).  Built on the host from the
+// DoF map (operator.host_schedule); on a locality-ordered mesh block k's kernels overlap block
+// k+1's upload and block k's download overlaps both.
+static int host_pipeline(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
+                         const int* nblocks, const int64_t* const* sched, void* stream) {
   if (n < 0 || (n > 0 && (!plans || !u_hosts || !y_hosts))) return fail(TMF_EINVAL, "null argument");
   if (n == 0) return TMF_OK;
   for (int i = 0; i < n; ++i) {
     if (!plans[i] || !u_hosts[i] || !y_hosts[i]) return fail(TMF_EINVAL, "null plan or host buffer");
     if (plans[i]->dev != plans[0]->dev) return fail(TMF_EINVAL, "plans on different devices");
+    const int nb = nblocks ? nblocks[i] : 0;
+    if (nb < 0 || (nb > 0 && (!sched || !sched[i]))) return fail(TMF_EINVAL, "bad block schedule");
+    if (nb > 0) {
+      const tmf_plan* P = plans[i];
+      if (P->dg || P->peer.u) return fail(TMF_EINVAL, "block schedules are for single-GPU CG plans");
+      const int64_t* cs = sched[i];
+      const int64_t *ue = cs + nb + 1, *ye = ue + nb, *fs = ye + nb;
+      if (cs[0] != 0 || cs[nb] != P->n_cells || fs[0] != 0 || fs[nb] != P->n_fix)
+        return fail(TMF_EINVAL, "block schedule does not cover the plan");
+      for (int k = 0; k < nb; ++k)
+        if (cs[k + 1] < cs[k] || fs[k + 1] < fs[k] || ue[k] < 0 || ue[k] > P->n_global || ye[k] < 0 ||
+            ye[k] > ue[k] || (k && (ue[k] < ue[k - 1] || ye[k] < ye[k - 1])))
+          return fail(TMF_EINVAL, "block schedule is not monotone");
+      if (ue[nb - 1] != P->n_global || ye[nb - 1] != P->n_global)
+        return fail(TMF_EINVAL, "block schedule does not cover the plan");
+    }
   }
   const int dev = plans[0]->dev;
   if (dev < 0 || dev >= 64) return fail(TMF_EINVAL, "device index out of range");
@@ -1506,16 +1527,52 @@ int tmf_apply_host_multi(tmf_plan* const* plans, const double* const* u_hosts, d
   if ((rc = link(st, pp.up)) || (rc = link(st, pp.comp)) || (rc = link(st, pp.down))) return rc;
   for (int i = 0; i < n; ++i) {
     tmf_plan* P = plans[i];
-    const size_t bytes = sizeof(double) * P->n_global;
-    TMF_CUDA(cudaMemcpyAsync(P->stage_u, u_hosts[i], bytes, cudaMemcpyHostToDevice, pp.up));
-    if ((rc = link(pp.up, pp.comp))) return rc;
-    if ((rc = launch_apply(P, P->stage_u, P->stage_y, pp.comp, nullptr))) return rc;
-    if ((rc = link(pp.comp, pp.down))) return rc;
-    TMF_CUDA(cudaMemcpyAsync(y_hosts[i], P->stage_y, bytes, cudaMemcpyDeviceToHost, pp.down));
+    const int nb = nblocks ? nblocks[i] : 0;
+    if (nb == 0) {
+      const size_t bytes = sizeof(double) * P->n_global;
+      TMF_CUDA(cudaMemcpyAsync(P->stage_u, u_hosts[i], bytes, cudaMemcpyHostToDevice, pp.up));
+      if ((rc = link(pp.up, pp.comp))) return rc;
+      if ((rc = launch_apply(P, P->stage_u, P->stage_y, pp.comp, nullptr))) return rc;
+      if ((rc = link(pp.comp, pp.down))) return rc;
+      TMF_CUDA(cudaMemcpyAsync(y_hosts[i], P->stage_y, bytes, cudaMemcpyDeviceToHost, pp.down));
+      continue;
+    }
+    const int64_t* cs = sched[i];
+    const int64_t *ue = cs + nb + 1, *ye = ue + nb, *fs = ye + nb;
+    TMF_CUDA(cudaMemsetAsync(P->stage_y, 0, sizeof(double) * P->n_global, pp.comp));
+    int64_t u0 = 0, y0 = 0;
+    for (int k = 0; k < nb; ++k) {
+      if (ue[k] > u0)
+        TMF_CUDA(cudaMemcpyAsync(P->stage_u + u0, u_hosts[i] + u0, sizeof(double) * (ue[k] - u0),
+                                 cudaMemcpyHostToDevice, pp.up));
+      u0 = ue[k];
+      if ((rc = link(pp.up, pp.comp))) return rc;
+      if ((rc = tmf_apply_stages(P, P->stage_u, P->stage_y, TMF_STAGE_CELLS, cs[k], cs[k + 1], pp.comp)))
+        return rc;
+      if (fs[k + 1] > fs[k])
+        TMF_CUDA(tmf::launch_fixup(P->stage_u, P->stage_y, P->fix_list + fs[k], fs[k + 1] - fs[k], P->n_sm,
+                                   pp.comp));
+      if (ye[k] > y0) {
+        if ((rc = link(pp.comp, pp.down))) return rc;
+        TMF_CUDA(cudaMemcpyAsync(y_hosts[i] + y0, P->stage_y + y0, sizeof(double) * (ye[k] - y0),
+                                 cudaMemcpyDeviceToHost, pp.down));
+      }
+      y0 = ye[k];
+    }
   }
   // `stream` reaches the end of the pipeline only when every download has landed
   if ((rc = link(pp.down, st)) || (rc = link(pp.comp, st)) || (rc = link(pp.up, st))) return rc;
   return TMF_OK;
+}
+
+int tmf_apply_host_multi(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
+                         void* stream) {
+  return host_pipeline(plans, u_hosts, y_hosts, n, nullptr, nullptr, stream);
+}
+
+int tmf_apply_host_multi_blocks(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts,
+                                int n, const int* nblocks, const int64_t* const* schedules, void* stream) {
+  return host_pipeline(plans, u_hosts, y_hosts, n, nblocks, schedules, stream);
 }
 
 int tmf_apply_timed(tmf_plan* P, const double* u, double* y, void* stream, int reps, double* out_ms,

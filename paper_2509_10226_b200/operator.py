@@ -271,6 +271,31 @@ class _B200Operator:
         _lib.check(_lib.lib().tmf_apply_host_async(self._plan, C.c_void_p(up), C.c_void_p(yp), C.c_void_p(stream)))
         self._count()
 
+    def host_schedule(self, n_blocks: int, align: int = 256) -> np.ndarray:
+        """Block schedule of a streamed host apply (``tmf_apply_host_multi_blocks``): cells
+        split into ~n_blocks ranges (multiples of ``align``); block k needs the u prefix up to
+        the largest DoF its cells (and earlier ones) touch, and after it every DoF below the
+        smallest DoF of the later cells is final.  Packed int64
+        [cell_split(nb+1), u_end(nb), y_end(nb), fix_split(nb+1)]."""
+        if self.dofmap.space != "cg":
+            raise ValueError("block schedules are for CG operators")
+        cd = np.asarray(self.dofmap.cell_dofs, dtype=np.int64)
+        n, nc, ng = len(cd), int(getattr(self.dofmap, "n_components", 1)), int(self.n_global_dofs)
+        cuts = np.unique(np.clip((np.linspace(0, n, max(1, n_blocks) + 1) // align).astype(np.int64) * align, 0, n))
+        cuts = np.unique(np.concatenate([[0], cuts, [n]]))
+        nb = len(cuts) - 1
+        pmax = np.maximum.accumulate(cd.max(axis=1))
+        smin = np.minimum.accumulate(cd.min(axis=1)[::-1])[::-1]
+        ue = (pmax[cuts[1:] - 1] + 1) * nc
+        ye = np.append(smin[cuts[1:-1]] * nc, ng)
+        ue[-1] = ng
+        ye = np.minimum(ye, ue)
+        mask = np.asarray(self.dofmap.dirichlet_mask, dtype=bool)
+        fix = (np.nonzero(mask)[0][:, None] * nc + np.arange(nc)[None, :]).ravel()
+        fs = np.concatenate([[0], np.searchsorted(fix, ye, side="left")])
+        fs[-1] = len(fix)
+        return np.ascontiguousarray(np.concatenate([cuts, ue, ye, fs]).astype(np.int64)), nb
+
     def apply_stages(self, u_ptr: int, y_ptr: int, stages: int, cell_begin: int = 0, cell_end: int | None = None,
                      stream: int = 0):
         """Part of the apply (``_lib.STAGE_*`` bits) on cells [cell_begin, cell_end)."""
@@ -380,13 +405,15 @@ def apply_helmholtz(config, mesh, dofmap, geometry, basis, sipg, coeffs, u, diri
     return HelmholtzOperator(mesh, dofmap, geometry, basis, sipg, coeffs, config, dirichlet_ids).apply(u)
 
 
-def apply_host_multi(operators, u_hosts, y_hosts, stream: int = 0):
+def apply_host_multi(operators, u_hosts, y_hosts, stream: int = 0, schedules=None):
     """y_hosts[i] = operators[i] u_hosts[i] for several operators as one pipelined call
     (``tmf_apply_host_multi``): uploads back to back in the given order, each plan's
     kernels as soon as its own upload has landed, downloads overlapping the next plans'
     uploads.  Enqueued on ``stream`` and returns; the host buffers (pinned tensors or
     arrays) must outlive the stream work.  Replaces a caller's loop of
-    ``operator.apply(u)`` calls (reference operator.py:320-331)."""
+    ``operator.apply(u)`` calls (reference operator.py:320-331).  ``schedules``: one
+    ``host_schedule(n_blocks)`` result (or None = whole plan) per operator, streaming CG plans
+    in cell blocks (``tmf_apply_host_multi_blocks``; read during the call)."""
     ops, us, ys = list(operators), list(u_hosts), list(y_hosts)
     if not (len(ops) == len(us) == len(ys)):
         raise ValueError("operators, u_hosts and y_hosts differ in length")
@@ -404,6 +431,13 @@ def apply_host_multi(operators, u_hosts, y_hosts, stream: int = 0):
     plans = arr(*[A._plan.value for A in ops])
     up = arr(*[ptr(u) for u in us])
     yp = arr(*[ptr(y) for y in ys])
-    _lib.check(_lib.lib().tmf_apply_host_multi(plans, up, yp, n, C.c_void_p(stream)))
+    if schedules is None:
+        _lib.check(_lib.lib().tmf_apply_host_multi(plans, up, yp, n, C.c_void_p(stream)))
+    else:
+        if len(schedules) != n:
+            raise ValueError("one schedule (or None) per operator")
+        nbs = (C.c_int * max(n, 1))(*[0 if sc is None else int(sc[1]) for sc in schedules])
+        sp = arr(*[None if sc is None else sc[0].ctypes.data for sc in schedules])
+        _lib.check(_lib.lib().tmf_apply_host_multi_blocks(plans, up, yp, n, nbs, sp, C.c_void_p(stream)))
     for A in ops:
         A._count()
