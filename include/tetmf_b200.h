@@ -147,22 +147,11 @@ int tmf_apply_host_async(tmf_plan* plan, const double* u_host, double* y_host, v
  * only for plan i's kernels); `stream` is ordered before and after the whole
  * pipeline.  Same results as n tmf_apply_host_async calls (the reference has no
  * batched call; it replaces the caller's loop over operator.apply(u) calls,
- * operator.py:320-331).  All plans on one device; host buffers pinned. */
+ * operator.py:320-331).  All plans on one device; host buffers pinned.  A plan may
+ * appear more than once (its entries run in order: each waits for the previous
+ * download of that plan's staging buffers); plans with peers are rejected. */
 int tmf_apply_host_multi(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
                          void* stream);
-
-/* The same pipeline with plans streamed in cell blocks (single-GPU CG plans;
- * nblocks[i] = 0 runs plan i whole).  schedules[i] packs, for nb = nblocks[i]:
- * cell_split[nb+1] (0 .. n_cells), u_end[nb] (the prefix u[0, u_end[k]) is
- * uploaded before block k's cells run; non-decreasing, last = n_global_dofs),
- * y_end[nb] (y[0, y_end[k]) is final after block k and is downloaded then;
- * y_end[k] <= u_end[k], last = n_global_dofs) and fix_split[nb+1] (the
- * ascending Dirichlet list's entries block k writes: those in
- * [y_end[k-1], y_end[k])).  Built from the DoF map by the Python
- * `_B200Operator.host_schedule`; on a locality-ordered mesh a block's kernels
- * and download overlap the next blocks' uploads.  Same results as tmf_apply. */
-int tmf_apply_host_multi_blocks(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts,
-                                int n, const int* nblocks, const int64_t* const* schedules, void* stream);
 
 /* Per-stage timing of `reps` back-to-back applies (device pointers), CUDA
  * events on `stream`: out_ms[0] = total, out_ms[1..] = per kernel class

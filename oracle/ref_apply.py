@@ -120,17 +120,22 @@ def _cell_batches(n_cells, lane_width, cells_per_lane):
 
 
 def cell_loop(u, y, gidx, Eg, jit, jxw, Ev=None, mass_jxw=None, mass_scale=0.0,
-              stiff_scale=1.0, batch_cells=None, max_batches=None):
+              stiff_scale=1.0, batch_cells=None, max_batches=None, chunk=None):
     """operator.py:255-278 over batches of cells.
 
     gidx: (N, n_dpc) gather indices (-1 = masked).  jxw: stiffness JxW (N, n_q)
     (already scaled by any per-cell coefficient); mass_jxw: unscaled JxW for
     the mass term.  ``batch_cells`` = columns per batch (None: one batch of all
-    cells).  Returns the number of batches run.
+    cells).  ``chunk``: process contiguous ranges of this many cells instead (bounded
+    memory at full BASELINE sizes; the sum is the same up to rounding order).  Returns
+    the number of batches run.
     """
     n = len(gidx)
     nq = Eg.shape[0] // 3
-    if batch_cells is None:
+    if chunk is not None:
+        batches = ((np.arange(c0, min(n, c0 + chunk)), np.ones(min(n, c0 + chunk) - c0, bool))
+                   for c0 in range(0, n, chunk))
+    elif batch_cells is None:
         batches = [(np.arange(n), np.ones(n, bool))]
     else:
         W = 4
@@ -159,7 +164,7 @@ def cell_loop(u, y, gidx, Eg, jit, jxw, Ev=None, mass_jxw=None, mass_scale=0.0,
 
 # ------------------------------------------------------------------ operators
 def cg_apply(vertices, cells, cell_dofs, dirichlet_mask, grad_matrix, weights, u,
-             batch_cells=None, kappa=None):
+             batch_cells=None, kappa=None, chunk=None):
     """CgPoissonOperator.apply (operator.py:320-331); ``kappa``: per-cell coefficient of the
     stiffness term ("multiply the stiffness part by kappa_e")."""
     u = np.asarray(u, dtype=np.float64)
@@ -170,7 +175,7 @@ def cg_apply(vertices, cells, cell_dofs, dirichlet_mask, grad_matrix, weights, u
     if dirichlet_mask is not None and dirichlet_mask.any():
         gidx[dirichlet_mask[gidx]] = -1
     y = np.zeros(len(u))
-    cell_loop(u, y, gidx, grad_matrix, jit, jxw, batch_cells=batch_cells)
+    cell_loop(u, y, gidx, grad_matrix, jit, jxw, batch_cells=batch_cells, chunk=chunk)
     if dirichlet_mask is not None and dirichlet_mask.any():
         y[dirichlet_mask] = u[dirichlet_mask]
     return y
@@ -234,7 +239,7 @@ def _face_loop(u, y, vertices, cells, n_dpc, interior_faces, boundary_faces, dir
 
 def dg_apply(vertices, cells, n_dpc, interior_faces, boundary_faces, dirichlet_ids,
              value_matrix, grad_matrix, weights, face_values, face_grads, face_weights,
-             tau_i, tau_b, u, kappa=None, mass_scale=0.0, stiff_scale=1.0, n_components=1):
+             tau_i, tau_b, u, kappa=None, mass_scale=0.0, stiff_scale=1.0, n_components=1, chunk=None):
     """DgSipgOperator.apply (operator.py:456-466), HelmholtzOperator.apply
     (operator.py:481-493; 3 interleaved components, constant coefficients) and
     the scalar per-cell-kappa Helmholtz of BASELINE config 4 (SURVEY §8c-3:
@@ -248,7 +253,7 @@ def dg_apply(vertices, cells, n_dpc, interior_faces, boundary_faces, dirichlet_i
     for comp in range(nc):
         gidx = (np.arange(n)[:, None] * n_dpc + np.arange(n_dpc)[None, :]) * nc + comp
         cell_loop(u, y, gidx, grad_matrix, jit, sjxw_cells, value_matrix, jxw,
-                  mass_scale, stiff_scale)
+                  mass_scale, stiff_scale, chunk=chunk)
         if stiff_scale != 0.0:
             _face_loop(u, y, vertices, cells, n_dpc, interior_faces, boundary_faces,
                        dirichlet_ids, face_values, face_grads, face_weights, tau_i, tau_b,

@@ -86,9 +86,6 @@ def lib():
         L.tmf_apply_host_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.tmf_apply_host_multi.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                            C.c_int, C.c_void_p]
-        L.tmf_apply_host_multi_blocks.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
-                                                  C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_int),
-                                                  C.POINTER(C.c_void_p), C.c_void_p]
         L.tmf_apply_timed.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_int]
         L.tmf_diagonal.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.tmf_pcg.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp, C.c_void_p]
@@ -125,7 +122,7 @@ def lib():
         L.tmf_last_error.restype = C.c_char_p
         L.tmf_version.restype = C.c_char_p
         for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
-                     "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_host_multi", "tmf_apply_host_multi_blocks", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg",
+                     "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_host_multi", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg",
                      "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs",
                      "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update", "tmf_pcg_direction",
                      "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle", "tmf_ipc_open_handle",
@@ -139,7 +136,7 @@ def lib():
 
 
 EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
-            "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_host_multi", "tmf_apply_host_multi_blocks", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
+            "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_host_multi", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg", "tmf_hierarchical_reorder",
             "tmf_build_faces", "tmf_build_cg_dofs", "tmf_vec_dot", "tmf_pcg_init", "tmf_pcg_update",
             "tmf_pcg_direction", "tmf_plan_set_peers", "tmf_alloc", "tmf_free", "tmf_ipc_get_handle",
             "tmf_ipc_open_handle", "tmf_ipc_close_handle", "tmf_color_cells", "tmf_transfer_create",

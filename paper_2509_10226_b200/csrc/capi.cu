@@ -434,6 +434,7 @@ struct tmf_plan {
   bool concurrent = false;  // DG: cell and face kernels run concurrently (flags bit 12)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_stage = nullptr;   // end of the last staged (host-buffer) apply
   int face_variant = 0;  // (desc.flags >> 4) & 0xF: face-kernel tuning variant
   bool dg = false, mass = false, faces = false;
   int64_t n_cells = 0, n_verts = 0, n_scalar = 0, n_global = 0;
@@ -551,6 +552,7 @@ struct tmf_plan {
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_stage) cudaEventDestroy(ev_stage);
     for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)face_tfrags, (void*)cells,
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
@@ -1417,18 +1419,34 @@ int tmf_apply_f32(tmf_plan* P, const float* u, float* y, void* stream) {
   return TMF_OK;
 }
 
+// Host-buffer applies stage u / y in per-plan device buffers.  ev_stage marks the end of the
+// plan's last staged apply (its download): every staged apply waits for it before it uploads
+// into stage_u (an earlier kernel may still read it) and records it after its download, so two
+// staged applies of one plan on any streams (or twice in one pipeline call) are ordered.
+static int ensure_staging(tmf_plan* P) {
+  if (P->peer.u)
+    return fail(TMF_EINVAL, "a plan with peers applies on its registered buffers (tmf_apply / "
+                            "tmf_apply_stages), not through host staging");
+  if (!P->stage_u) {
+    const size_t bytes = sizeof(double) * P->n_global;
+    TMF_CUDA(cudaMalloc(&P->stage_u, bytes));
+    TMF_CUDA(cudaMalloc(&P->stage_y, bytes));
+    TMF_CUDA(cudaEventCreateWithFlags(&P->ev_stage, cudaEventDisableTiming));
+  }
+  return TMF_OK;
+}
+
 int tmf_apply_host(tmf_plan* P, const double* u_host, double* y_host) {
   if (!P || !u_host || !y_host) return fail(TMF_EINVAL, "null argument");
   TMF_CUDA(cudaSetDevice(P->dev));
+  if (int rc = ensure_staging(P)) return rc;
   const size_t bytes = sizeof(double) * P->n_global;
-  if (!P->stage_u) {
-    TMF_CUDA(cudaMalloc(&P->stage_u, bytes));
-    TMF_CUDA(cudaMalloc(&P->stage_y, bytes));
-  }
+  TMF_CUDA(cudaStreamWaitEvent(0, P->ev_stage, 0));
   TMF_CUDA(cudaMemcpyAsync(P->stage_u, u_host, bytes, cudaMemcpyHostToDevice, 0));
   int rc = launch_apply(P, P->stage_u, P->stage_y, 0, nullptr);
   if (rc) return rc;
   TMF_CUDA(cudaMemcpyAsync(y_host, P->stage_y, bytes, cudaMemcpyDeviceToHost, 0));
+  TMF_CUDA(cudaEventRecord(P->ev_stage, 0));
   TMF_CUDA(cudaStreamSynchronize(0));
   return TMF_OK;
 }
@@ -1436,16 +1454,15 @@ int tmf_apply_host(tmf_plan* P, const double* u_host, double* y_host) {
 int tmf_apply_host_async(tmf_plan* P, const double* u_host, double* y_host, void* stream) {
   if (!P || !u_host || !y_host) return fail(TMF_EINVAL, "null argument");
   TMF_CUDA(cudaSetDevice(P->dev));
+  if (int rc = ensure_staging(P)) return rc;
   const size_t bytes = sizeof(double) * P->n_global;
-  if (!P->stage_u) {
-    TMF_CUDA(cudaMalloc(&P->stage_u, bytes));
-    TMF_CUDA(cudaMalloc(&P->stage_y, bytes));
-  }
   cudaStream_t st = (cudaStream_t)stream;
+  TMF_CUDA(cudaStreamWaitEvent(st, P->ev_stage, 0));
   TMF_CUDA(cudaMemcpyAsync(P->stage_u, u_host, bytes, cudaMemcpyHostToDevice, st));
   int rc = launch_apply(P, P->stage_u, P->stage_y, st, nullptr);
   if (rc) return rc;
   TMF_CUDA(cudaMemcpyAsync(y_host, P->stage_y, bytes, cudaMemcpyDeviceToHost, st));
+  TMF_CUDA(cudaEventRecord(P->ev_stage, st));
   return TMF_OK;
 }
 
@@ -1453,7 +1470,8 @@ int tmf_apply_host_async(tmf_plan* P, const double* u_host, double* y_host, void
 // in the caller's order, the kernels on one compute stream (each waits for its own upload),
 // every download on a second copy stream (each waits for its own kernels).  Per-plan
 // streams would let the copy engine interleave all uploads, so the first kernel (and the
-// first download) would wait for most of the uploads instead of one.
+// first download) would wait for most of the uploads instead of one.  The pipeline streams
+// are shared per device, so concurrent callers are serialised for the (short) enqueue.
 namespace {
 struct HostPipe {
   cudaStream_t up = nullptr, comp = nullptr, down = nullptr;
@@ -1462,117 +1480,63 @@ HostPipe g_pipe[64];
 std::mutex g_pipe_mu;
 }  // namespace
 
-// sched (nb blocks, CG plans only): cell_split[nb+1], u_end[nb] (u[0, u_end[k]) has landed before
-// block k's cells run), y_end[nb] (y[0, y_end[k]) is final after block k), fix_split[nb+1]
-// (Dirichlet list entries block k writes; the list is ascending).  Built on the host from the
-// DoF map (operator.host_schedule); on a locality-ordered mesh block k's kernels overlap block
-// k+1's upload and block k's download overlaps both.
-static int host_pipeline(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
-                         const int* nblocks, const int64_t* const* sched, void* stream) {
+int tmf_apply_host_multi(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
+                         void* stream) {
   if (n < 0 || (n > 0 && (!plans || !u_hosts || !y_hosts))) return fail(TMF_EINVAL, "null argument");
   if (n == 0) return TMF_OK;
   for (int i = 0; i < n; ++i) {
     if (!plans[i] || !u_hosts[i] || !y_hosts[i]) return fail(TMF_EINVAL, "null plan or host buffer");
     if (plans[i]->dev != plans[0]->dev) return fail(TMF_EINVAL, "plans on different devices");
-    const int nb = nblocks ? nblocks[i] : 0;
-    if (nb < 0 || (nb > 0 && (!sched || !sched[i]))) return fail(TMF_EINVAL, "bad block schedule");
-    if (nb > 0) {
-      const tmf_plan* P = plans[i];
-      if (P->dg || P->peer.u) return fail(TMF_EINVAL, "block schedules are for single-GPU CG plans");
-      const int64_t* cs = sched[i];
-      const int64_t *ue = cs + nb + 1, *ye = ue + nb, *fs = ye + nb;
-      if (cs[0] != 0 || cs[nb] != P->n_cells || fs[0] != 0 || fs[nb] != P->n_fix)
-        return fail(TMF_EINVAL, "block schedule does not cover the plan");
-      for (int k = 0; k < nb; ++k)
-        if (cs[k + 1] < cs[k] || fs[k + 1] < fs[k] || ue[k] < 0 || ue[k] > P->n_global || ye[k] < 0 ||
-            ye[k] > ue[k] || (k && (ue[k] < ue[k - 1] || ye[k] < ye[k - 1])))
-          return fail(TMF_EINVAL, "block schedule is not monotone");
-      if (ue[nb - 1] != P->n_global || ye[nb - 1] != P->n_global)
-        return fail(TMF_EINVAL, "block schedule does not cover the plan");
-    }
+    if (plans[i]->peer.u) return fail(TMF_EINVAL, "a plan with peers cannot take host buffers");
   }
   const int dev = plans[0]->dev;
   if (dev < 0 || dev >= 64) return fail(TMF_EINVAL, "device index out of range");
   TMF_CUDA(cudaSetDevice(dev));
-  HostPipe pp;
-  {
-    std::lock_guard<std::mutex> lk(g_pipe_mu);
-    HostPipe& p = g_pipe[dev];
-    if (!p.up) {
-      TMF_CUDA(cudaStreamCreateWithFlags(&p.up, cudaStreamNonBlocking));
-      TMF_CUDA(cudaStreamCreateWithFlags(&p.comp, cudaStreamNonBlocking));
-      TMF_CUDA(cudaStreamCreateWithFlags(&p.down, cudaStreamNonBlocking));
-    }
-    pp = p;
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  HostPipe& pp = g_pipe[dev];
+  if (!pp.up) {
+    TMF_CUDA(cudaStreamCreateWithFlags(&pp.up, cudaStreamNonBlocking));
+    TMF_CUDA(cudaStreamCreateWithFlags(&pp.comp, cudaStreamNonBlocking));
+    TMF_CUDA(cudaStreamCreateWithFlags(&pp.down, cudaStreamNonBlocking));
   }
-  for (int i = 0; i < n; ++i) {
-    tmf_plan* P = plans[i];
-    if (!P->stage_u) {
-      const size_t bytes = sizeof(double) * P->n_global;
-      TMF_CUDA(cudaMalloc(&P->stage_u, bytes));
-      TMF_CUDA(cudaMalloc(&P->stage_y, bytes));
-    }
-  }
+  for (int i = 0; i < n; ++i)
+    if (int rc = ensure_staging(plans[i])) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaEvent_t ev;
   auto link = [&](cudaStream_t from, cudaStream_t to) -> int {
+    cudaEvent_t ev;
     TMF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     TMF_CUDA(cudaEventRecord(ev, from));
     TMF_CUDA(cudaStreamWaitEvent(to, ev, 0));
     TMF_CUDA(cudaEventDestroy(ev));  // released once the wait has been satisfied
     return TMF_OK;
   };
-  int rc;
   // the caller's prior work on `stream` (e.g. writes into the host buffers' sources) comes first
+  int rc = 0;
   if ((rc = link(st, pp.up)) || (rc = link(st, pp.comp)) || (rc = link(st, pp.down))) return rc;
-  for (int i = 0; i < n; ++i) {
+  for (int i = 0; i < n && !rc; ++i) {
     tmf_plan* P = plans[i];
-    const int nb = nblocks ? nblocks[i] : 0;
-    if (nb == 0) {
-      const size_t bytes = sizeof(double) * P->n_global;
-      TMF_CUDA(cudaMemcpyAsync(P->stage_u, u_hosts[i], bytes, cudaMemcpyHostToDevice, pp.up));
-      if ((rc = link(pp.up, pp.comp))) return rc;
-      if ((rc = launch_apply(P, P->stage_u, P->stage_y, pp.comp, nullptr))) return rc;
-      if ((rc = link(pp.comp, pp.down))) return rc;
-      TMF_CUDA(cudaMemcpyAsync(y_hosts[i], P->stage_y, bytes, cudaMemcpyDeviceToHost, pp.down));
-      continue;
+    const size_t bytes = sizeof(double) * P->n_global;
+    // the plan's previous staged apply (an earlier list entry, or another call) has downloaded
+    if ((rc = cudaStreamWaitEvent(pp.up, P->ev_stage, 0) == cudaSuccess ? 0 : fail(TMF_ECUDA, "event wait")))
+      break;
+    if (cudaMemcpyAsync(P->stage_u, u_hosts[i], bytes, cudaMemcpyHostToDevice, pp.up) != cudaSuccess) {
+      rc = fail(TMF_ECUDA, "upload failed");
+      break;
     }
-    const int64_t* cs = sched[i];
-    const int64_t *ue = cs + nb + 1, *ye = ue + nb, *fs = ye + nb;
-    TMF_CUDA(cudaMemsetAsync(P->stage_y, 0, sizeof(double) * P->n_global, pp.comp));
-    int64_t u0 = 0, y0 = 0;
-    for (int k = 0; k < nb; ++k) {
-      if (ue[k] > u0)
-        TMF_CUDA(cudaMemcpyAsync(P->stage_u + u0, u_hosts[i] + u0, sizeof(double) * (ue[k] - u0),
-                                 cudaMemcpyHostToDevice, pp.up));
-      u0 = ue[k];
-      if ((rc = link(pp.up, pp.comp))) return rc;
-      if ((rc = tmf_apply_stages(P, P->stage_u, P->stage_y, TMF_STAGE_CELLS, cs[k], cs[k + 1], pp.comp)))
-        return rc;
-      if (fs[k + 1] > fs[k])
-        TMF_CUDA(tmf::launch_fixup(P->stage_u, P->stage_y, P->fix_list + fs[k], fs[k + 1] - fs[k], P->n_sm,
-                                   pp.comp));
-      if (ye[k] > y0) {
-        if ((rc = link(pp.comp, pp.down))) return rc;
-        TMF_CUDA(cudaMemcpyAsync(y_hosts[i] + y0, P->stage_y + y0, sizeof(double) * (ye[k] - y0),
-                                 cudaMemcpyDeviceToHost, pp.down));
-      }
-      y0 = ye[k];
+    if ((rc = link(pp.up, pp.comp))) break;
+    if ((rc = launch_apply(P, P->stage_u, P->stage_y, pp.comp, nullptr))) break;
+    if ((rc = link(pp.comp, pp.down))) break;
+    if (cudaMemcpyAsync(y_hosts[i], P->stage_y, bytes, cudaMemcpyDeviceToHost, pp.down) != cudaSuccess ||
+        cudaEventRecord(P->ev_stage, pp.down) != cudaSuccess) {
+      rc = fail(TMF_ECUDA, "download failed");
+      break;
     }
   }
-  // `stream` reaches the end of the pipeline only when every download has landed
-  if ((rc = link(pp.down, st)) || (rc = link(pp.comp, st)) || (rc = link(pp.up, st))) return rc;
-  return TMF_OK;
-}
-
-int tmf_apply_host_multi(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts, int n,
-                         void* stream) {
-  return host_pipeline(plans, u_hosts, y_hosts, n, nullptr, nullptr, stream);
-}
-
-int tmf_apply_host_multi_blocks(tmf_plan* const* plans, const double* const* u_hosts, double* const* y_hosts,
-                                int n, const int* nblocks, const int64_t* const* schedules, void* stream) {
-  return host_pipeline(plans, u_hosts, y_hosts, n, nblocks, schedules, stream);
+  // `stream` reaches the end of the pipeline only when every download has landed -- also
+  // after an error, so the caller can tell when the copies touching its buffers are done
+  int rl = 0;
+  if ((rl = link(pp.down, st)) || (rl = link(pp.comp, st)) || (rl = link(pp.up, st))) return rc ? rc : rl;
+  return rc;
 }
 
 int tmf_apply_timed(tmf_plan* P, const double* u, double* y, void* stream, int reps, double* out_ms,
@@ -1626,6 +1590,9 @@ int tmf_diagonal(tmf_plan* P, double* diag, void* stream) {
 int tmf_pcg(tmf_plan* P, const double* b, double* x, int iters, double* res_norms, void* stream) {
   if (!P || !b || !x || iters < 0) return fail(TMF_EINVAL, "bad argument");
   if (P->dg) return fail(TMF_EINVAL, "PCG is implemented for the CG operator");
+  if (P->peer.u)
+    return fail(TMF_EINVAL, "tmf_pcg is the single-GPU solver; a plan with peers needs the multi-rank "
+                            "loop (tmf_apply_stages + tmf_pcg_* with cross-rank reductions)");
   TMF_CUDA(cudaSetDevice(P->dev));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = P->n_global;

@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .counters import FlopCounters
+from .counters import FlopCounters, reference_apply_counts
 
 __all__ = ["OperatorConfig", "SipgConfig", "HelmholtzCoefficients", "CgPoissonOperator",
            "DgSipgOperator", "HelmholtzOperator", "KappaHelmholtzOperator", "compute_sipg_tau",
@@ -140,6 +140,26 @@ class _B200Operator:
             raise ValueError("the B200 operators need the mesh: geometry is recomputed from vertices")
         self.mesh, self.dofmap, self.geo, self.basis = mesh, dofmap, geometry, basis
         self.config = config or OperatorConfig()
+        # geometry.py:139-142: unknown modes and affine-on-curved are errors in the reference.  The
+        # kernels recompute the AFFINE map of every cell from its 4 vertices, which is the
+        # reference's per-point geometry too whenever the cells are straight (its quadratic
+        # geometry nodes are then the affine midpoints, geometry.py:77-83); curved cells have no
+        # B200 path and are rejected instead of silently linearised.
+        mode = getattr(geometry, "mode", "affine")
+        if mode not in ("affine", "per_point"):
+            raise ValueError(f"unknown geometry mode {mode!r}")
+        if getattr(mesh, "is_curved", False) or getattr(mesh, "geometry_nodes", None) is not None:
+            if mode == "affine":
+                raise ValueError("affine geometry requested for a curved mesh; use per-point mode")
+            raise ValueError("curved (per-point) geometry is not supported by the B200 operators: "
+                             "the kernels use the affine map of each cell's vertices")
+        if self.config.batching == "components" and int(dofmap.n_components) != 3:
+            raise ValueError("components batching requires a 3-component space")   # operator.py:197-198
+        self.precision = self.config.precision
+        if self.precision == "f32" and (self._kind != _lib.TMF_CG_LAPLACE or int(dofmap.n_components) != 1
+                                        or kappa is not None):
+            raise ValueError("precision='f32' is implemented for the scalar CG Laplace operator only on "
+                             "the B200 path (DG / Helmholtz run in f64)")
         self.counters = FlopCounters()
         self.n_applies = 0
         self.dirichlet_ids = frozenset(int(b) for b in dirichlet_ids)
@@ -204,12 +224,17 @@ class _B200Operator:
             ((_ENGINES[getattr(self.config, "cell_engine", "auto")] >> 2) << 19) | \
             (_PATCHES[getattr(self.config, "cell_patches", "auto")] << 15) | \
             (_FACE_ENGINES[getattr(self.config, "face_engine", "auto")] << 17) | \
-            ((1 if getattr(self.config, "f32_mirror", False) else 0) << 20) | \
+            ((1 if (getattr(self.config, "f32_mirror", False) or self.precision == "f32") else 0) << 20) | \
             ((1 if getattr(self.config, "face_runs", "plain") == "window" else 0) << 21)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))
         self.info = {f: getattr(info, f) for f, _ in info._fields_}
+        # the reference's per-apply counter increments (operator.py:227-248, 416-437)
+        self._apply_counts = reference_apply_counts(
+            self.config, dofmap, d.n_q, int(d.n_qf), interior_faces=getattr(mesh, "interior_faces", None),
+            boundary_faces=getattr(mesh, "boundary_faces", None), dirichlet_ids=self.dirichlet_ids,
+            mass_scale=mass_scale, diffusivity=diffusivity, affine=mode == "affine", faces=sipg is not None)
 
     # -- lifecycle
     def close(self):
@@ -232,15 +257,17 @@ class _B200Operator:
             raise ValueError(f"vector length {len(u)} does not match {self.n_global_dofs} DoFs")
 
     def _count(self):
-        self.counters.add("total_flops_alg", int(self.info["flops_alg"]))
-        self.counters.add("vector_bytes", 24 * self.n_global_dofs)
+        self.counters.add_all(self._apply_counts)
         self.n_applies += 1
 
     # -- apply
     def apply(self, u, out=None):
         """y = A u.  NumPy in -> fresh NumPy out (or ``out``, e.g. a pinned buffer);
-        CUDA tensor in -> CUDA tensor out."""
+        CUDA tensor in -> CUDA tensor out.  ``precision="f32"`` (CG Laplace) computes in
+        single precision and returns float32, as the reference does (operator.py:323-324)."""
         self._check_length(u)
+        if self.precision == "f32":
+            return self._apply_single(u, out)
         if type(u).__module__.startswith("torch"):
             import torch
 
@@ -259,42 +286,32 @@ class _B200Operator:
         self._count()
         return y
 
+    def _apply_single(self, u, out=None):
+        import torch
+
+        if type(u).__module__.startswith("torch") and u.is_cuda:
+            ut = u.to(torch.float32).contiguous()
+            y = torch.empty_like(ut)
+            self.apply_f32(ut, out=y)
+            self._count()
+            return y
+        un = np.ascontiguousarray(u.detach().cpu().numpy() if hasattr(u, "detach") else u, dtype=np.float32)
+        ut = torch.from_numpy(un).to(torch.device("cuda", int(self.config.device)))
+        yt = self.apply_f32(ut)
+        y = yt.cpu().numpy()
+        self._count()
+        if out is not None:
+            out[...] = y
+            return out
+        return y
+
     def apply_host_async(self, u_host, y_host, stream: int = 0):
         """Enqueue H2D(u), apply, D2H(y) on ``stream`` and return (pinned host arrays
         or tensors; they must outlive the stream work)."""
-        for t in (u_host, y_host):
-            n = t.numel() if hasattr(t, "numel") else len(t)
-            if n != self.n_global_dofs:
-                raise ValueError("host buffer length does not match the operator size")
-        up = u_host.data_ptr() if hasattr(u_host, "data_ptr") else u_host.ctypes.data
-        yp = y_host.data_ptr() if hasattr(y_host, "data_ptr") else y_host.ctypes.data
+        up = _host_buffer(u_host, self.n_global_dofs)
+        yp = _host_buffer(y_host, self.n_global_dofs)
         _lib.check(_lib.lib().tmf_apply_host_async(self._plan, C.c_void_p(up), C.c_void_p(yp), C.c_void_p(stream)))
         self._count()
-
-    def host_schedule(self, n_blocks: int, align: int = 256) -> np.ndarray:
-        """Block schedule of a streamed host apply (``tmf_apply_host_multi_blocks``): cells
-        split into ~n_blocks ranges (multiples of ``align``); block k needs the u prefix up to
-        the largest DoF its cells (and earlier ones) touch, and after it every DoF below the
-        smallest DoF of the later cells is final.  Packed int64
-        [cell_split(nb+1), u_end(nb), y_end(nb), fix_split(nb+1)]."""
-        if self.dofmap.space != "cg":
-            raise ValueError("block schedules are for CG operators")
-        cd = np.asarray(self.dofmap.cell_dofs, dtype=np.int64)
-        n, nc, ng = len(cd), int(getattr(self.dofmap, "n_components", 1)), int(self.n_global_dofs)
-        cuts = np.unique(np.clip((np.linspace(0, n, max(1, n_blocks) + 1) // align).astype(np.int64) * align, 0, n))
-        cuts = np.unique(np.concatenate([[0], cuts, [n]]))
-        nb = len(cuts) - 1
-        pmax = np.maximum.accumulate(cd.max(axis=1))
-        smin = np.minimum.accumulate(cd.min(axis=1)[::-1])[::-1]
-        ue = (pmax[cuts[1:] - 1] + 1) * nc
-        ye = np.append(smin[cuts[1:-1]] * nc, ng)
-        ue[-1] = ng
-        ye = np.minimum(ye, ue)
-        mask = np.asarray(self.dofmap.dirichlet_mask, dtype=bool)
-        fix = (np.nonzero(mask)[0][:, None] * nc + np.arange(nc)[None, :]).ravel()
-        fs = np.concatenate([[0], np.searchsorted(fix, ye, side="left")])
-        fs[-1] = len(fix)
-        return np.ascontiguousarray(np.concatenate([cuts, ue, ye, fs]).astype(np.int64)), nb
 
     def apply_stages(self, u_ptr: int, y_ptr: int, stages: int, cell_begin: int = 0, cell_end: int | None = None,
                      stream: int = 0):
@@ -405,39 +422,35 @@ def apply_helmholtz(config, mesh, dofmap, geometry, basis, sipg, coeffs, u, diri
     return HelmholtzOperator(mesh, dofmap, geometry, basis, sipg, coeffs, config, dirichlet_ids).apply(u)
 
 
-def apply_host_multi(operators, u_hosts, y_hosts, stream: int = 0, schedules=None):
+def _host_buffer(t, n: int) -> int:
+    """Address of a host (CPU) float64 C-contiguous buffer of n entries (ideally pinned)."""
+    if hasattr(t, "data_ptr"):
+        import torch
+
+        if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != n:
+            raise ValueError("host buffers must be contiguous float64 CPU tensors of the operator size")
+        return t.data_ptr()
+    a = np.asarray(t)
+    if a.dtype != np.float64 or not a.flags.c_contiguous or a.size != n or a is not t:
+        raise ValueError("host buffers must be contiguous float64 arrays of the operator size")
+    return a.ctypes.data
+
+
+def apply_host_multi(operators, u_hosts, y_hosts, stream: int = 0):
     """y_hosts[i] = operators[i] u_hosts[i] for several operators as one pipelined call
     (``tmf_apply_host_multi``): uploads back to back in the given order, each plan's
     kernels as soon as its own upload has landed, downloads overlapping the next plans'
     uploads.  Enqueued on ``stream`` and returns; the host buffers (pinned tensors or
     arrays) must outlive the stream work.  Replaces a caller's loop of
-    ``operator.apply(u)`` calls (reference operator.py:320-331).  ``schedules``: one
-    ``host_schedule(n_blocks)`` result (or None = whole plan) per operator, streaming CG plans
-    in cell blocks (``tmf_apply_host_multi_blocks``; read during the call)."""
+    ``operator.apply(u)`` calls (reference operator.py:320-331)."""
     ops, us, ys = list(operators), list(u_hosts), list(y_hosts)
     if not (len(ops) == len(us) == len(ys)):
         raise ValueError("operators, u_hosts and y_hosts differ in length")
-
-    def ptr(t):
-        return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
-
-    for A, u, y in zip(ops, us, ys):
-        for t in (u, y):
-            n = t.numel() if hasattr(t, "numel") else len(t)
-            if n != A.n_global_dofs:
-                raise ValueError("host buffer length does not match the operator size")
     n = len(ops)
     arr = C.c_void_p * max(n, 1)
     plans = arr(*[A._plan.value for A in ops])
-    up = arr(*[ptr(u) for u in us])
-    yp = arr(*[ptr(y) for y in ys])
-    if schedules is None:
-        _lib.check(_lib.lib().tmf_apply_host_multi(plans, up, yp, n, C.c_void_p(stream)))
-    else:
-        if len(schedules) != n:
-            raise ValueError("one schedule (or None) per operator")
-        nbs = (C.c_int * max(n, 1))(*[0 if sc is None else int(sc[1]) for sc in schedules])
-        sp = arr(*[None if sc is None else sc[0].ctypes.data for sc in schedules])
-        _lib.check(_lib.lib().tmf_apply_host_multi_blocks(plans, up, yp, n, nbs, sp, C.c_void_p(stream)))
+    up = arr(*[_host_buffer(u, A.n_global_dofs) for A, u in zip(ops, us)])
+    yp = arr(*[_host_buffer(y, A.n_global_dofs) for A, y in zip(ops, ys)])
+    _lib.check(_lib.lib().tmf_apply_host_multi(plans, up, yp, n, C.c_void_p(stream)))
     for A in ops:
         A._count()

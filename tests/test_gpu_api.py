@@ -26,7 +26,10 @@ def test_torch_cuda_tensor_roundtrip_and_counters():
     assert rel_l2(y.cpu().numpy(), g["y"]) <= 1e-12
     y2 = A.apply(g["u"])
     assert A.n_applies == 2
-    assert A.counters.total_flops == 2 * int(A.info["flops_alg"])
+    assert A.counters.total_flops == 2 * A._apply_counts["cell_interp_flops"] + 2 * (
+        A._apply_counts["cell_qpoint_flops"] + A._apply_counts["cell_sum_flops"]
+        + A._apply_counts["face_interp_flops"] + A._apply_counts["face_qpoint_flops"])
+    assert A.counters["vector_bytes"] == 2 * 24 * A.n_global_dofs
     assert rel_l2(y2, g["y"]) <= 1e-12
 
 
@@ -66,22 +69,16 @@ def test_host_multi_pipeline_matches_goldens():
     for g, y in zip(gs, ys):
         assert rel_l2(y.numpy(), g["y"]) <= 1e-12
     assert ops[0].n_applies == 2
-    # the same plans streamed in cell blocks (CG plans; DG and Helmholtz whole)
-    for y in ys:
-        y.fill_(np.nan)
-    scheds = [A.host_schedule(5, align=32) if A.dofmap.space == "cg" else None for A in ops]
-    assert scheds[0][1] > 1
-    op.apply_host_multi(ops, us, ys, s.cuda_stream, schedules=scheds)
-    s.synchronize()
-    for g, y in zip(gs, ys):
-        assert rel_l2(y.numpy(), g["y"]) <= 1e-12
-    bad = (scheds[0][0].copy(), scheds[0][1])
-    bad[0][0] = 1
-    with pytest.raises(Exception, match="schedule"):
-        op.apply_host_multi(ops[:1], us[:1], ys[:1], s.cuda_stream, schedules=[bad])
     op.apply_host_multi([], [], [], s.cuda_stream)
-    with pytest.raises(ValueError, match="does not match"):
+    with pytest.raises(ValueError, match="operator size"):
         op.apply_host_multi(ops[:1], us[1:2], ys[1:2])
+    # host buffers must be float64, contiguous, on the host
+    with pytest.raises(ValueError, match="host buffers"):
+        op.apply_host_multi(ops[:1], [us[0].float()], ys[:1])
+    with pytest.raises(ValueError, match="host buffers"):
+        op.apply_host_multi(ops[:1], [us[0].cuda()], ys[:1])
+    with pytest.raises(ValueError, match="host buffers"):
+        ops[0].apply_host_async(us[0], ys[0][::1].cuda(), s.cuda_stream)
     with pytest.raises(ValueError, match="differ in length"):
         op.apply_host_multi(ops[:2], us[:1], ys[:2])
 
@@ -243,28 +240,84 @@ def test_c_abi_demo_runs():
     assert "PASS" in r.stdout
 
 
-@pytest.mark.parametrize("p", [1, 3])
-def test_host_blocks_on_reordered_mesh_match_device_apply(p):
-    """Streamed host apply (many narrow blocks on a hierarchically reordered mesh, Dirichlet
-    rows) equals the device-resident apply bit for bit up to the RED order (1e-14)."""
+def test_host_multi_same_plan_adjacent_different_inputs():
+    """one plan twice in a row with DIFFERENT inputs, and the plan's
+    async host apply on another stream right after: the staging buffers are ordered by the
+    plan's stage event, so every output is its own input's apply."""
     import torch
 
-    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, operator as op, quadrature as Q
-    from paper_2509_10226_b200.geometry import GeometryData
-    from paper_2509_10226_b200.reorder import reorder_mesh
+    from paper_2509_10226_b200 import operator as op
 
-    m = reorder_mesh(M.kuhn_cube_mesh(16, seed=3))
-    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
-    bas = B.tabulate_basis(p, cr, fr)
-    dm = D.build_dof_map(m, p, "cg")
-    A = op.CgPoissonOperator(m, dm, GeometryData("affine", cr, fr, None, None, None, None), bas,
-                             op.OperatorConfig(device=0))
-    u = np.random.default_rng(5).uniform(-1, 1, A.n_global_dofs)
-    y_ref = A.apply(u)
-    u_pin = torch.from_numpy(u).pin_memory()
-    y_pin = torch.full_like(u_pin, np.nan).pin_memory()
-    sched = A.host_schedule(24, align=64)
-    assert sched[1] >= 16
-    op.apply_host_multi([A], [u_pin], [y_pin], 0, schedules=[sched])
-    torch.cuda.synchronize()
-    assert rel_l2(y_pin.numpy(), y_ref) <= 1e-14
+    g = load_golden("cg_p2_n8_gm_dir")
+    A = operator_from_fixture(g)
+    rng = np.random.default_rng(9)
+    us = [torch.from_numpy(rng.uniform(-1, 1, A.n_global_dofs)).pin_memory() for _ in range(3)]
+    ys = [torch.full_like(u, np.nan).pin_memory() for u in us]
+    refs = [A.apply(u.numpy()) for u in us]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        for y in ys:
+            y.fill_(np.nan)
+        op.apply_host_multi([A, A], us[:2], ys[:2], s1.cuda_stream)
+        A.apply_host_async(us[2], ys[2], s2.cuda_stream)
+        torch.cuda.synchronize()
+        for y, r in zip(ys, refs):
+            assert rel_l2(y.numpy(), r) <= 1e-14
+
+
+def test_counters_follow_reference_batching():
+    """Row a23: the reference counter categories, per apply, from the reference's batching
+    (the values themselves are pinned against the real reference in tests/test_counters.py)."""
+    from paper_2509_10226_b200 import operator as op
+    from paper_2509_10226_b200.counters import reference_apply_counts
+
+    g = load_golden("dg_p3_n3_gm_dir")
+    mesh, dofmap, geo, basis = fixture_objects(g)
+    sipg = op.SipgConfig(1.0, g["tau_i"], g["tau_b"])
+    cfg = op.OperatorConfig(kernel_stage="ref", lane_width=8)
+    A = op.DgSipgOperator(mesh, dofmap, geo, basis, sipg, cfg, dirichlet_ids=range(6))
+    A.apply(g["u"])
+    inc = reference_apply_counts(cfg, dofmap, len(geo.cell_rule.weights), len(geo.face_rule.weights),
+                                 interior_faces=mesh.interior_faces, boundary_faces=mesh.boundary_faces,
+                                 dirichlet_ids=range(6), faces=True)
+    d = A.counters.as_dict()
+    assert all(d[k] == v for k, v in inc.items())
+    assert d["face_interp_flops"] > 0 and d["index_bytes"] > 0 and d["geometry_bytes"] > 0
+
+
+def test_geometry_mode_and_precision_boundary():
+    """geometry.py:139-142 (unknown mode, affine on curved), per-point geometry of straight
+    cells (= the affine map), precision="f32" (CG: float32 result; DG: rejected)."""
+    from types import SimpleNamespace as NS
+
+    import torch
+
+    from paper_2509_10226_b200 import operator as op
+
+    g = load_golden("cg_p2_n8_gm_dir")
+    mesh, dofmap, geo, basis = fixture_objects(g)
+    geo.mode = "bogus"
+    with pytest.raises(ValueError, match="unknown geometry mode"):
+        op.CgPoissonOperator(mesh, dofmap, geo, basis)
+    geo.mode = "affine"
+    curved = NS(**vars(mesh), geometry_nodes=np.zeros((len(g["cells"]), 10, 3)), is_curved=True)
+    with pytest.raises(ValueError, match="curved"):
+        op.CgPoissonOperator(curved, dofmap, geo, basis)
+    geo.mode = "per_point"
+    with pytest.raises(ValueError, match="curved"):
+        op.CgPoissonOperator(curved, dofmap, geo, basis)
+    A = op.CgPoissonOperator(mesh, dofmap, geo, basis)          # straight cells: same operator
+    assert rel_l2(A.apply(g["u"]), g["y"]) <= 1e-12
+    assert A.counters["geometry_bytes"] > 0
+    geo.mode = "affine"
+    A32 = op.CgPoissonOperator(mesh, dofmap, geo, basis, op.OperatorConfig(precision="f32"))
+    y32 = A32.apply(g["u"])
+    assert y32.dtype == np.float32
+    assert rel_l2(y32.astype(np.float64), g["y"]) <= 1e-5
+    yt = A32.apply(torch.from_numpy(g["u"]).cuda())
+    assert yt.dtype == torch.float32 and rel_l2(yt.cpu().double().numpy(), g["y"]) <= 1e-5
+    gd = load_golden("dg_p2_n3_gm_dir")
+    mesh, dofmap, geo, basis = fixture_objects(gd)
+    with pytest.raises(ValueError, match="f32"):
+        op.DgSipgOperator(mesh, dofmap, geo, basis, op.SipgConfig(1.0, gd["tau_i"], gd["tau_b"]),
+                          op.OperatorConfig(precision="f32"))

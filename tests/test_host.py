@@ -250,37 +250,3 @@ def test_vertex_renumbering_is_a_permutation_of_the_operator(p):
     assert np.linalg.norm(y2[new_of_old] - y1) <= 1e-13 * np.linalg.norm(y1)
     with pytest.raises(ValueError):
         M.apply_vertex_permutation(m, np.zeros(m.n_vertices, dtype=np.int64))
-
-
-@pytest.mark.parametrize("p,reorder", [(1, True), (2, True), (3, False)])
-def test_host_block_schedule_invariants(p, reorder):
-    """_B200Operator.host_schedule (the streamed host apply's plan): every DoF a block's cells
-    touch is inside its uploaded u prefix, every DoF a later block touches lies at or above its
-    final y prefix, and each Dirichlet row is written by the block that finalises it."""
-    from types import SimpleNamespace
-
-    from paper_2509_10226_b200 import operator as op
-
-    m = M.kuhn_cube_mesh(6, seed=0)
-    if reorder:
-        m = R.reorder_mesh(m)
-    dm = D.build_dof_map(m, p, "cg")
-    fake = SimpleNamespace(dofmap=dm, n_global_dofs=dm.n_global_dofs)
-    sched, nb = op._B200Operator.host_schedule(fake, 8, align=64)
-    cuts, ue, ye, fs = sched[: nb + 1], sched[nb + 1: 2 * nb + 1], sched[2 * nb + 1: 3 * nb + 1], sched[3 * nb + 1:]
-    assert len(fs) == nb + 1 and cuts[0] == 0 and cuts[-1] == len(m.cells) and np.all(np.diff(cuts) > 0)
-    assert ue[-1] == ye[-1] == dm.n_global_dofs and np.all(ye <= ue)
-    assert np.all(np.diff(ue) >= 0) and np.all(np.diff(ye) >= 0)
-    cd = np.asarray(dm.cell_dofs)
-    fix = np.nonzero(np.asarray(dm.dirichlet_mask, dtype=bool))[0]
-    assert fs[0] == 0 and fs[-1] == len(fix)
-    lo = 0
-    for k in range(nb):
-        assert cd[: cuts[k + 1]].max() < ue[k]
-        if cuts[k + 1] < len(m.cells):
-            assert cd[cuts[k + 1]:].min() >= ye[k]
-        f = fix[fs[k]: fs[k + 1]]
-        assert np.all((f >= lo) & (f < ye[k]))
-        lo = ye[k]
-    if reorder:   # locality: half the cells need well under the whole vector
-        assert ue[nb // 2 - 1] < 0.8 * dm.n_global_dofs
