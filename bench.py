@@ -43,9 +43,9 @@ sys.path.insert(0, ROOT)
 FP64_PEAK_TFLOPS = 37.1   # measured: DMMA m8n8k4 on this pool's B200 (profiles/r01_fp64_peak.json)
 FP64_PEAK_SOURCE = "profiles/r01_fp64_peak.json (mma.sync m8n8k4 f64 microbench on B200, 1965 MHz)"
 DEGREES = (1, 2, 3, 4)
-ENGINE_NAMES = {1: "dmma-quadrature", 2: "dfma-quadrature", 3: "dmma-reference-tensor",
+ENGINE_NAMES = {1: "dmma-quadrature", 3: "dmma-reference-tensor",
                 4: "dmma-modal (point kernel on M = dim P_(p-1) exact modes)"}
-KERNEL_NAMES = {1: "cell_apply_kernel (n_q points)", 2: "cell_dfma_kernel", 3: "cell_tensor_kernel",
+KERNEL_NAMES = {1: "cell_apply_kernel (n_q points)", 3: "cell_tensor_kernel",
                 4: "cell_apply_kernel (modal tables)"}
 N_MESH = 48
 

@@ -78,19 +78,15 @@ typedef struct tmf_plan_desc {
   double mass_scale;           /* Helmholtz mass coefficient                          */
   double diffusivity;          /* Laplace/SIPG scale (nu)                             */
   int32_t device;              /* CUDA device ordinal                                 */
-  int32_t flags;               /* bit 20: also build the fp32 mirror (tmf_apply_f32);
-                                  bit 21: window-major face-chunk runs (default: plain contiguous runs);
-                                  bits 0-3 / 4-7: cell / face kernel tuning variant;
-                                  8-11 face chunk/8; 12 concurrent DG; 13-14 cell engine
-                                  (0 by degree, 1 DMMA quadrature points, 2 DFMA,
-                                  3 DMMA reference tensor); 15-16 CG
-                                  patch-local assembly (0 auto, 1 off, 2 on); 17-18
-                                  face engine (0 by degree, 1 quadrature points,
-                                  2 reference tensor (interior faces), 3 modal: the
-                                  point loop on NF exact unit-weight face modes);
-                                  19: cell engine bit 2
-                                  (4 = modal: the point kernel on M = dim P_{p-1}
-                                  unit-weight modes)                                   */
+  int32_t flags;               /* bits 8-11: face batches per CTA chunk / 8 (0 = 32);
+                                  13-14 + 19 (bit 2): cell engine (0 by degree,
+                                  1 DMMA quadrature points, 3 DMMA reference tensor,
+                                  4 modal: the point kernel on M = dim P_{p-1}
+                                  unit-weight modes); 15-16: CG block assembly (0 auto,
+                                  1 off, 2 on); 17-18 face engine (0 by degree,
+                                  1 quadrature points, 3 modal: the point loop on NF
+                                  exact unit-weight face modes); 20: also build the
+                                  fp32 mirror (tmf_apply_f32).  Other bits: reserved. */
 } tmf_plan_desc;
 
 typedef struct tmf_plan_info {
@@ -101,15 +97,14 @@ typedef struct tmf_plan_info {
   int32_t kernels_per_apply;   /* kernel launches per tmf_apply                       */
   int32_t n_face_batches;      /* signature-uniform 8-face batches (DG)               */
   int64_t device_bytes;        /* device memory held by the plan                      */
-  int32_t patch_cells;         /* CG patch-local assembly: cells per patch (0 = off)  */
-  double patch_ratio;          /* unique patch DoFs / unmasked cell-DoF slots (CG)    */
-  int32_t cell_engine;         /* cell kernel in use: 1 DMMA quadrature points, 2 DFMA,
+  int32_t block_cells;         /* CG block assembly: cells per block (0 = off)         */
+  double block_ratio;          /* unique block DoFs / cell-DoF slots (CG block assembly) */
+  int32_t cell_engine;         /* cell kernel in use: 1 DMMA quadrature points,
                                   3 DMMA reference tensor (affine precontraction),
                                   4 modal (point kernel on M exact unit-weight modes) */
   double flops_engine;         /* useful flops per apply of the algorithm the engines
                                   run (= flops_alg except for the tensor engines)      */
-  int32_t face_engine;         /* faces: 1 quadrature points, 2 reference tensor,
-                                  3 modal (0: no faces)                                */
+  int32_t face_engine;         /* faces: 1 quadrature points, 3 modal (0: no faces)   */
 } tmf_plan_info;
 
 int tmf_plan_create(const tmf_plan_desc* desc, tmf_plan** out);

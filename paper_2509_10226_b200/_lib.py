@@ -59,8 +59,8 @@ class PlanInfo(C.Structure):
     _fields_ = [
         ("n_global_dofs", C.c_int64), ("flops_alg", C.c_double), ("bytes_alg", C.c_double),
         ("flops_issued", C.c_double), ("kernels_per_apply", C.c_int32),
-        ("n_face_batches", C.c_int32), ("device_bytes", C.c_int64), ("patch_cells", C.c_int32),
-        ("patch_ratio", C.c_double), ("cell_engine", C.c_int32), ("flops_engine", C.c_double),
+        ("n_face_batches", C.c_int32), ("device_bytes", C.c_int64), ("block_cells", C.c_int32),
+        ("block_ratio", C.c_double), ("cell_engine", C.c_int32), ("flops_engine", C.c_double),
         ("face_engine", C.c_int32),
     ]
 

@@ -128,92 +128,6 @@ void build_tensor_fragments(int N, int Q, bool mass, FG Eg, FV Ev, const double*
         }
 }
 
-// Reference-tensor interior-face tables (face_tensor_kernel.cuh), one per signature
-// sig = lf- * 24 + lf+ * 6 + code.  Tables of one side: Ev(lf, code, c, q, a) = component
-// c (0 value, 1..3 face-frame derivative) at point q of the DoF at gather position a
-// (face DoFs first).  With <x, y> = sum_q w_q x(q) y(q) and slots (0 s tau, 1 hm0,
-// 2 hm1, 3 hp0, 4 hp1, 5 zero, 6 hm2, 7 hp2), the point loop of face_kernel.cuh is
-//   s tau: [m,m] <m0,m0>  [m,p] -<m0,p0>  [p,m] -<p0,m0>  [p,p] <p0,p0>
-//   hm_k:  [m,m] -<m0,mk'> - <mk',m0>  [m,p] <mk',p0>  [p,m] <p0,mk'>
-//   hp_k:  [m,p] -<m0,pk'>  [p,m] -<pk',m0>  [p,p] <p0,pk'> + <pk',p0>      (k' = k + 1)
-// ([out side, in side]).  Inputs/outputs are ordered [-F | +F] (region F) and
-// [-I | +I] (region I); the fragments hold the blocks the kernel multiplies, and every
-// dropped block is checked to vanish (nodal basis).
-template <typename F>
-int build_face_tensor_fragments(int N, int NF, int QF, F Ev, const double* w, std::vector<double>& out) {
-  const int NI = N - NF, KF = (2 * NF + 3) / 4, KI = (2 * NI + 3) / 4;
-  double dropped = 0.0, kept = 0.0;
-  for (int lfm = 0; lfm < 4; ++lfm)
-    for (int lfp = 0; lfp < 4; ++lfp)
-      for (int code = 0; code < 6; ++code) {
-        // side 0 = minus (lf-, code 0), side 1 = plus (lf+, code)
-        const int lf[2] = {lfm, lfp}, cd[2] = {0, code};
-        auto E = [&](int side, int c, int q, int a) { return Ev(lf[side], cd[side], c, q, a); };
-        auto IP = [&](int so, int co, int ao, int si, int ci, int ai) {
-          long double acc = 0.0L;
-          for (int q = 0; q < QF; ++q) acc += (long double)w[q] * E(so, co, q, ao) * E(si, ci, q, ai);
-          return (double)acc;
-        };
-        auto T = [&](int slot, int so, int ao, int si, int ai) -> double {
-          if (slot == 5) return 0.0;
-          if (slot == 0) return (so == si ? 1.0 : -1.0) * IP(so, 0, ao, si, 0, ai);
-          const bool hm = slot == 1 || slot == 2 || slot == 6;
-          const int k1 = (slot == 1 || slot == 3) ? 1 : (slot == 2 || slot == 4) ? 2 : 3;
-          if (hm) {
-            if (so == 0 && si == 0) return -IP(0, 0, ao, 0, k1, ai) - IP(0, k1, ao, 0, 0, ai);
-            if (so == 0 && si == 1) return IP(0, k1, ao, 1, 0, ai);
-            if (so == 1 && si == 0) return IP(1, 0, ao, 0, k1, ai);
-            return 0.0;
-          }
-          if (so == 1 && si == 1) return IP(1, 0, ao, 1, k1, ai) + IP(1, k1, ao, 1, 0, ai);
-          if (so == 0 && si == 1) return -IP(0, 0, ao, 1, k1, ai);
-          if (so == 1 && si == 0) return -IP(1, k1, ao, 0, 0, ai);
-          return 0.0;
-        };
-        // region index -> (side, gather position); -1 = padding
-        auto regF = [&](int x, int& side, int& a) {
-          if (x >= 2 * NF) return false;
-          side = x >= NF;
-          a = x - side * NF;
-          return true;
-        };
-        auto regI = [&](int x, int& side, int& a) {
-          if (x >= 2 * NI) return false;
-          side = x >= NI;
-          a = NF + x - side * NI;
-          return true;
-        };
-        auto frag = [&](bool outF, int ib, int p, bool inF, int kk) {
-          for (int lane = 0; lane < 32; ++lane) {
-            const int n = lane >> 2, slot = 2 * p + (n & 1);
-            int so, ao, si, ai;
-            const bool ok = (outF ? regF(4 * ib + (n >> 1), so, ao) : regI(4 * ib + (n >> 1), so, ao)) &&
-                            (inF ? regF(4 * kk + (lane & 3), si, ai) : regI(4 * kk + (lane & 3), si, ai));
-            out.push_back(ok ? T(slot, so, ao, si, ai) : 0.0);
-          }
-        };
-        for (int ib = 0; ib < KF; ++ib) {
-          for (int p = 0; p < 4; ++p)
-            for (int kk = 0; kk < KF; ++kk) frag(true, ib, p, true, kk);
-          for (int kk = 0; kk < KI; ++kk) frag(true, ib, 3, false, kk);
-        }
-        for (int ib = 0; ib < KI; ++ib)
-          for (int kk = 0; kk < KF; ++kk) frag(false, ib, 3, true, kk);
-        // the dropped blocks must vanish: slots 0-5 between F and I, everything I x I
-        for (int so = 0; so < 2; ++so)
-          for (int si = 0; si < 2; ++si)
-            for (int slot = 0; slot < 8; ++slot)
-              for (int ao = 0; ao < N; ++ao)
-                for (int ai = 0; ai < N; ++ai) {
-                  const bool fo = ao < NF, fi = ai < NF;
-                  const double v = std::fabs(T(slot, so, ao, si, ai));
-                  const bool keep = (fo && fi) || ((fo != fi) && slot >= 6);
-                  (keep ? kept : dropped) = std::max(keep ? kept : dropped, v);
-                }
-      }
-  return dropped <= 1e-12 * std::max(kept, 1.0) ? TMF_OK : TMF_EINVAL;
-}
-
 // Symmetric eigendecomposition by cyclic Jacobi rotations in long double (small n):
 // A (n x n, row-major, destroyed) -> eigenvalues lam (descending) and eigenvectors V
 // (column m of V belongs to lam[m]).
@@ -297,104 +211,6 @@ bool build_modal_cell_tables(int N, int Q, int M, const double* Gm, const double
   return true;
 }
 
-// CG warp-patch records (cell_patch_kernel.cuh) for patches of CH = 32 consecutive
-// cells; contribution slots are j*CH + cl.  Two parallel passes over the patches
-// (sizes, then fill at the prefix-summed offsets); per patch the (DoF, slot) pairs
-// are sorted, so unique DoFs are ascending (coalesced u gathers and REDs) and every
-// DoF's incidences are contiguous.  G is filled in on the device afterwards.
-struct PatchTables {
-  std::vector<int4> meta;         // {record offset (16 B), nu, incidences, record size (16 B)}
-  std::vector<uint4> rec;         // records
-  int numax = 0, recmax = 0;
-  int64_t slots = 0, unique = 0;
-};
-
-void build_patches(const int* enc, int64_t n_cells, int N, int CH, PatchTables& T) {
-  const int NP = (N + 1) & ~1, NW = NP / 2;
-  const int geo_b = 6 * CH * 8, lid_b = NW * CH * 4;
-  const int64_t np = (n_cells + CH - 1) / CH;
-  std::vector<int> nu(np), ninc(np);
-  auto keys_of = [&](int64_t p, std::vector<uint32_t>& k) {
-    k.clear();
-    const int64_t c0 = p * CH, c1 = std::min<int64_t>(n_cells, c0 + CH);
-    for (int64_t c = c0; c < c1; ++c)
-      for (int j = 0; j < N; ++j) {
-        const int g = enc[c * N + j];
-        if (g >= 0) k.push_back((uint32_t)(j * CH + (c - c0)));
-      }
-    std::sort(k.begin(), k.end(), [&](uint32_t x, uint32_t y) {
-      const int gx = enc[(p * CH + x % CH) * N + x / CH], gy = enc[(p * CH + y % CH) * N + y / CH];
-      return gx != gy ? gx < gy : x < y;
-    });
-  };
-  auto dof = [&](int64_t p, uint32_t x) { return enc[(p * CH + x % CH) * N + x / CH]; };
-  const int nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  auto parallel = [&](auto&& body) {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t)
-      th.emplace_back([&, t] {
-        std::vector<uint32_t> k;
-        for (int64_t p = t; p < np; p += nt) body(p, k);
-      });
-    for (auto& x : th) x.join();
-  };
-  parallel([&](int64_t p, std::vector<uint32_t>& k) {
-    keys_of(p, k);
-    int u = 0;
-    for (size_t i = 0; i < k.size(); ++i) u += (i == 0 || dof(p, k[i]) != dof(p, k[i - 1]));
-    nu[p] = u;
-    ninc[p] = (int)k.size();
-  });
-  auto r4 = [](int64_t x) { return (x + 3) & ~(int64_t)3; };
-  auto r8 = [](int64_t x) { return (x + 7) & ~(int64_t)7; };
-  T.meta.resize(np);
-  int64_t at = 0;   // 16-byte units
-  for (int64_t p = 0; p < np; ++p) {
-    const int64_t bytes = geo_b + lid_b + 4 * r4(nu[p]) + 2 * r8(nu[p] + 1) + 2 * r8(ninc[p]);
-    T.meta[p] = make_int4((int)at, nu[p], ninc[p], (int)(bytes / 16));
-    at += bytes / 16;
-    T.numax = std::max(T.numax, (nu[p] + 1) & ~1);
-    T.recmax = std::max<int>(T.recmax, (int)bytes);
-    T.slots += ninc[p];
-    T.unique += nu[p];
-  }
-  T.rec.assign(at, make_uint4(0, 0, 0, 0));
-  parallel([&](int64_t p, std::vector<uint32_t>& k) {
-    keys_of(p, k);
-    const int4 m = T.meta[p];
-    unsigned char* r = reinterpret_cast<unsigned char*>(T.rec.data() + m.x);
-    uint16_t* lid = reinterpret_cast<uint16_t*>(r + geo_b);
-    std::fill(lid, lid + 2 * NW * CH, (uint16_t)0xFFFF);
-    int* pd = reinterpret_cast<int*>(r + geo_b + lid_b);
-    uint16_t* off = reinterpret_cast<uint16_t*>(pd + r4(m.y));
-    uint16_t* pos = off + r8(m.y + 1);
-    int u = -1;
-    for (size_t i = 0; i < k.size(); ++i) {
-      const int g = dof(p, k[i]);
-      if (i == 0 || g != dof(p, k[i - 1])) {
-        ++u;
-        pd[u] = g;
-        off[u] = (uint16_t)i;
-      }
-      pos[i] = (uint16_t)k[i];
-      const int j = k[i] / CH, cl = k[i] % CH;
-      lid[2 * ((j / 2) * CH + cl) + (j & 1)] = (uint16_t)u;   // little-endian halves of word j/2
-    }
-    off[m.y] = (uint16_t)k.size();
-  });
-}
-
-// Point-major rows for the DFMA cell kernel (cell_dfma_kernel.cuh), row length
-// NP = N rounded up to even:  T1[q][c][j] = E_c(q, j),  T2[q][c][j] = w_q E_c(q, j)
-template <typename F>
-void build_point_rows(int N, int Q, int NC, F E, const double* w, std::vector<double>& out) {
-  const int NP = (N + 1) & ~1;
-  for (int t = 0; t < 2; ++t)
-    for (int q = 0; q < Q; ++q)
-      for (int c = 0; c < NC; ++c)
-        for (int j = 0; j < NP; ++j) out.push_back(j < N ? (t ? w[q] : 1.0) * E(c, q, j) : 0.0);
-}
-
 // Face tables in the face frame (see face_kernel.cuh), for one (lf, code) combo.
 // Components c: 0 = value, 1..3 = D_i = a_i . grad (a_0, a_1 tangent, a_2 transversal);
 // columns are DoFs in the gather order perm (face DoFs first).  Point groups of 4:
@@ -425,17 +241,12 @@ void build_face_fragments(int N, int NF, int Q, F E, const double* w, std::vecto
 struct tmf_plan {
   int dev = 0, n_sm = 0;
   int kind = 0, degree = 0, N = 0, Q = 0, QF = 0, nc = 1;
-  int variant = 0;       // desc.flags & 0xF: cell-kernel tuning variant (0 = default)
   int engine = 0;        // (desc.flags >> 13) & 3 (| 4 via bit 19): cell engine 0 = by degree,
-                         // 1 = DMMA points, 2 = DFMA, 3 = reference tensor, 4 = modal
+                         // 1 = DMMA points, 3 = reference tensor, 4 = modal
   int kengine = 0;       // engine handed to the launcher (modal runs the point kernel: 1)
   int Qk = 0;            // "points" of the cell kernel (n_q, or M for the modal tables)
   int QFk = 0;           // "points" of the face kernel (n_qf, or NF for the modal face tables)
-  bool concurrent = false;  // DG: cell and face kernels run concurrently (flags bit 12)
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_stage = nullptr;   // end of the last staged (host-buffer) apply
-  int face_variant = 0;  // (desc.flags >> 4) & 0xF: face-kernel tuning variant
   bool dg = false, mass = false, faces = false;
   int64_t n_cells = 0, n_verts = 0, n_scalar = 0, n_global = 0;
   double mass_scale = 0.0, stiff_scale = 1.0;
@@ -446,21 +257,12 @@ struct tmf_plan {
   double* cell_frags = nullptr;
   double* cell_geo = nullptr;
   double* face_frags = nullptr;
-  double* face_tfrags = nullptr;   // reference-tensor interior-face tables (96 signatures)
-  std::vector<double> p1_tab;      // P1: constant gradients a[3][4] + sum of weights (13)
-  int face_engine = 0;             // (desc.flags >> 17) & 3: 0 by degree, 1 quadrature points, 2 tensor
+  int face_engine = 0;             // (desc.flags >> 17) & 3: 0 by degree, 1 quadrature points, 3 modal
   int* face_perm = nullptr;
   int* cells = nullptr;
   int* dofs = nullptr;
   int* fix_list = nullptr;
   int64_t n_fix = 0;
-  // CG patch-local assembly (CellArgs): built when the cell order has locality
-  int patches = 0;       // (desc.flags >> 15) & 3: 0 = auto (locality ratio), 1 = off, 2 = on
-  bool local = false;
-  int numax = 0, recmax = 0;
-  double patch_ratio = 1.0;   // unique patch DoFs / unmasked cell-DoF slots
-  int4* pmeta = nullptr;
-  uint4* prec = nullptr;
   // multi-GPU peer-memory ghost access (tmf_plan_set_peers)
   tmf::PeerArgs peer{};
   const double** peer_u_tab = nullptr;   // device arrays of device pointers
@@ -476,7 +278,6 @@ struct tmf_plan {
   double* if_tau = nullptr;
   double* if_geo = nullptr;
   int64_t n_if_batches = 0, n_if_chunks = 0;
-  int64_t face_blocked_grid = 0;   // > 0: window-major chunk runs for the blocked default kernel
   int4* bf_chunks = nullptr;
   int* bf_cm = nullptr;
   double* bf_tau = nullptr;
@@ -505,16 +306,9 @@ struct tmf_plan {
     a.dofs = dg ? nullptr : dofs + c0 * N;
     a.cgeo = cell_geo + 8 * c0;
     a.frags = cell_frags;
-    a.hP1 = p1_tab.empty() ? nullptr : p1_tab.data();
     a.n_cells = c1 - c0;
     a.nc = nc;
     if (!dg && with_peer) a.peer = peer;   // CG ghost DoFs over peer memory (DG: the face kernel's ghost cells)
-    if (local && c0 == 0 && c1 == n_cells) {
-      a.pmeta = pmeta;
-      a.prec = prec;
-      a.numax = numax;
-      a.recmax = recmax;
-    }
     return a;
   }
   tmf::FaceArgs face_args(const double* u, double* y, bool boundary) const {
@@ -531,7 +325,6 @@ struct tmf_plan {
     a.n_dpc = N;
     a.nc = nc;
     a.peer = peer;
-    a.tfrags = face_tfrags;   // the launcher uses the tensor kernel for interior faces when set
     return a;
   }
   tmf::FaceGeoArgs face_geo_args(bool boundary) const {
@@ -549,15 +342,12 @@ struct tmf_plan {
     return a;
   }
   ~tmf_plan() {
-    if (side) cudaStreamDestroy(side);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
     if (ev_stage) cudaEventDestroy(ev_stage);
-    for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)face_tfrags, (void*)cells,
+    for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
-                    (void*)pmeta, (void*)prec, (void*)f32_rows, (void*)f32_geo,
+                    (void*)f32_rows, (void*)f32_geo,
                     (void*)peer_u_tab, (void*)peer_y_tab, (void*)ghost_rank, (void*)ghost_index})
       if (p) cudaFree(p);
   }
@@ -567,53 +357,15 @@ namespace {
 
 int n_dofs_per_cell(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
 
-#ifdef TMF_EXP_FACE_WINDOW_ENV   // tuning experiment only (tools/gpu_window.sh)
-const int64_t kFaceWindow = getenv("TMF_FACE_WINDOW") ? atoll(getenv("TMF_FACE_WINDOW")) : 32768;
-#else
-// measured (tools/gpu_window.sh, profiles/r01/face_window_sweep.json): 512 / 2048 / 8192 / 32768 /
-// 131072 minus cells per window -> DG P3 64^3 faces 1.224 / 1.045 / 0.930 / 0.889 / 0.888 ms,
-// Helmholtz P2 96^3 1.576 / 1.459 / 1.406 / 1.392 / 1.412 ms (longer signature runs, fewer chunks)
+// measured (profiles/r01/face_window_sweep.json): 512 / 2048 / 8192 / 32768 / 131072 minus
+// cells per window -> DG P3 64^3 faces 1.224 / 1.045 / 0.930 / 0.889 / 0.888 ms, Helmholtz
+// P2 96^3 1.576 / 1.459 / 1.406 / 1.392 / 1.412 ms (longer signature runs, fewer chunks)
 constexpr int64_t kFaceWindow = 32768;
-#endif
 
 // Split [first, first+count) batches of one signature into CTA chunks.
 void push_chunks(std::vector<int4>& out, int cm, int cp, int64_t first, int64_t count, int chunk) {
   for (int64_t b = 0; b < count; b += chunk)
     out.push_back(make_int4(cm, cp, (int)(first + b), (int)std::min<int64_t>(chunk, count - b)));
-}
-
-// Window-major layout of the chunk list for the blocked face kernel (each CTA takes a
-// contiguous run of per = n / G chunks): run k is the concatenation of CTA k's contiguous
-// share of every window, shares balanced to within one chunk (padding chunks of zero
-// batches, with the previous chunk's signature so they cost no restaging, even the runs
-// out).  All CTAs then sweep the windows in step, so the live u / y of a window stay in L2
-// instead of every CTA streaming its own region of the mesh (DRAM 3x the algorithmic
-// bytes with plain contiguous runs, profiles/r01/ncu_prof_face_modal_d3_w32k.json).
-std::vector<int4> window_major_runs(const std::vector<int4>& chunks, const std::vector<int64_t>& cwin, int64_t G) {
-  std::vector<std::vector<int4>> run(G);
-  int64_t off = 0;
-  for (size_t s = 0; s < chunks.size();) {
-    size_t e = s;
-    while (e < chunks.size() && cwin[e] == cwin[s]) ++e;
-    const int64_t c = (int64_t)(e - s), base = c / G, extra = c % G;
-    size_t pos = s;
-    for (int64_t k = 0; k < G; ++k) {
-      const int64_t len = base + (((k - off) % G + G) % G < extra ? 1 : 0);
-      for (int64_t i = 0; i < len; ++i) run[k].push_back(chunks[pos++]);
-    }
-    off = (off + extra) % G;
-    s = e;
-  }
-  size_t L = 0;
-  for (const auto& r : run) L = std::max(L, r.size());
-  std::vector<int4> out;
-  out.reserve(L * G);
-  for (const auto& r : run) {
-    for (const auto& c : r) out.push_back(c);
-    const int4 last = r.empty() ? chunks[0] : r.back();
-    for (size_t i = r.size(); i < L; ++i) out.push_back(make_int4(last.x, last.y, 0, 0));
-  }
-  return out;
 }
 
 int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* total) {
@@ -637,7 +389,6 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   }
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sig(a) < sig(b); });
   std::vector<int4> chunks;
-  std::vector<int64_t> cwin;   // window of each chunk
   std::vector<int> cm, cp;
   std::vector<double> tau;
   int64_t nb = 0;
@@ -648,7 +399,6 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
     const int32_t* r0 = d->interior_faces + 5 * order[s];
     const int64_t nbatch = (e - s + 7) / 8;
     push_chunks(chunks, r0[1] * 6, r0[3] * 6 + r0[4], nb, nbatch, chunk);
-    cwin.resize(chunks.size(), r0[0] / kFaceWindow);
     for (int64_t k = 0; k < nbatch * 8; ++k) {
       if (s + k < e) {
         const int64_t f = order[s + k];
@@ -666,8 +416,6 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
     s = e;
   }
   P->n_if_batches = nb;
-  if (P->face_blocked_grid > 0 && P->nc == 1 && (int64_t)chunks.size() > P->face_blocked_grid)
-    chunks = window_major_runs(chunks, cwin, P->face_blocked_grid);
   P->n_if_chunks = (int64_t)chunks.size();
   int rc;
   if ((rc = upload(&P->if_chunks, chunks.data(), chunks.size(), total))) return rc;
@@ -729,46 +477,19 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
                  bool y_zeroed = false, double* energy = nullptr) {
   bool ok = true;
   if (ev) TMF_CUDA(cudaEventRecord(ev[0], st));
-  if (P->dg && P->faces && P->concurrent) {
-    // DG with concurrent kernels: y = 0, then the face kernels (stream st) and the cell
-    // kernel (side stream) both accumulate with RED and fill each other's idle pipe slots
-    if (!P->side) {
-      TMF_CUDA(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
-      TMF_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
-      TMF_CUDA(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
-    }
-    TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
-    TMF_CUDA(cudaEventRecord(P->ev_fork, st));
-    TMF_CUDA(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
-    tmf::CellArgs ca = P->cell_args(u, y);
-    ca.accumulate = 1;
-    TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, ca, P->n_sm, P->side, nullptr, &ok, P->variant, P->kengine));
-    if (ev) TMF_CUDA(cudaEventRecord(ev[1], st));
-    TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
-                              P->face_variant));
-    TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
-                              P->face_variant));
-    TMF_CUDA(cudaEventRecord(P->ev_join, P->side));
-    TMF_CUDA(cudaStreamWaitEvent(st, P->ev_join, 0));
-    if (ev) TMF_CUDA(cudaEventRecord(ev[2], st));
-    if (ev) TMF_CUDA(cudaEventRecord(ev[3], st));
-    return TMF_OK;
-  }
   if (!P->dg && !y_zeroed) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
   {
     tmf::CellArgs ca = P->cell_args(u, y);
     ca.energy = energy;
-    TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, ca, P->n_sm, st, nullptr, &ok, P->variant, P->kengine));
+    TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, ca, P->n_sm, st, nullptr, &ok, P->kengine));
   }
   // stage events only between kernels that exist (an event record between two empty
   // stages still costs ~3 us of GPU time, which would inflate the measured apply)
   const bool fix = !P->dg && P->n_fix;
   if (ev && (P->faces || fix)) TMF_CUDA(cudaEventRecord(ev[1], st));
   if (P->faces) {
-    TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
-                              P->face_variant));
-    TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
-                              P->face_variant));
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok));
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok));
   }
   if (ev && P->faces && fix) TMF_CUDA(cudaEventRecord(ev[2], st));
   if (fix) TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st, energy));
@@ -798,20 +519,18 @@ int tmf_apply_stages(tmf_plan* P, const double* u, double* y, int stages, int64_
       const int64_t m = std::min(std::max(P->n_peer_free, cell_begin), cell_end);
       if (m > cell_begin)
         TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, P->cell_args(u, y, cell_begin, m, false), P->n_sm,
-                                  st, nullptr, &ok, P->variant, P->kengine));
+                                  st, nullptr, &ok, P->kengine));
       if (cell_end > m)
         TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, P->cell_args(u, y, m, cell_end), P->n_sm, st,
-                                  nullptr, &ok, P->variant, P->kengine));
+                                  nullptr, &ok, P->kengine));
     } else {
       TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, P->cell_args(u, y, cell_begin, cell_end), P->n_sm,
-                                st, nullptr, &ok, P->variant, P->kengine));
+                                st, nullptr, &ok, P->kengine));
     }
   }
   if ((stages & TMF_STAGE_FACES) && P->faces) {
-    TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok,
-                              P->face_variant));
-    TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok,
-                              P->face_variant));
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok));
+    TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok));
   }
   if ((stages & TMF_STAGE_FIXUP) && !P->dg && P->n_fix)
     TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st));
@@ -871,14 +590,11 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     P->n_sm = sms;
   }
   P->kind = d->operator_kind;
-  P->variant = d->flags & 0xF;
   P->engine = ((d->flags >> 13) & 3) | (((d->flags >> 19) & 1) << 2);
-  P->patches = (d->flags >> 15) & 3;
-  // warp patches use the DFMA point-major tables (also for their global-kernel fallback)
-  if (P->patches == 2 && d->operator_kind == TMF_CG_LAPLACE && d->n_dofs_per_cell <= 20) P->engine = 2;
-  P->face_variant = (d->flags >> 4) & 0xF;
+  if (P->engine == 2) return bail(fail(TMF_EINVAL, "cell engine 2 (DFMA) was removed: use auto, dmma, tensor or modal"));
   P->face_engine = (d->flags >> 17) & 3;
-  P->concurrent = (d->flags >> 12) & 1;
+  if (P->face_engine == 2)
+    return bail(fail(TMF_EINVAL, "face engine 2 (reference tensor) was removed: use auto, quadrature or modal"));
   P->degree = d->degree;
   P->N = d->n_dofs_per_cell;
   P->Q = d->n_q;
@@ -936,7 +652,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     tmf::CellArgs dummy{};
     dummy.n_cells = P->n_cells;
     dummy.nc = P->nc;
-    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok, P->variant, P->kengine));
+    TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok, P->kengine));
     if (!ok) return bail(fail(TMF_EINVAL, "unsupported (n_dofs_per_cell, n_q) = (" +
                                               std::to_string(N) + ", " + std::to_string(Q) + ")"));
     const int NC = P->mass ? 4 : 3;
@@ -949,29 +665,12 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       build_tensor_fragments(
           N, Q, P->mass, [&](int k, int q, int j) { return Gm[(3 * q + k) * N + j]; },
           [&](int q, int j) { return V[q * N + j]; }, W, fr);
-    else if (ci.table == 0)
-      build_fragments(N, Q, NC, E, W, fr);
     else
-      build_point_rows(N, Q, NC, E, W, fr);
+      build_fragments(N, Q, NC, E, W, fr);
     if ((int)fr.size() != ci.frag_doubles) return bail(fail(TMF_EINVAL, "internal: fragment size"));
     if ((rc = upload(&P->cell_frags, fr.data(), fr.size(), &total))) return bail(rc);
     P->info.flops_issued = ci.flops_issued;
-    P->info.cell_engine = eng == 4 ? 4 : ci.table == 2 ? 3 : ci.table == 1 ? 2 : 1;
-    if (N == 4 && ci.table == 2) {
-      // P1: point-independent gradients -> the one-point collapse of cell_p1_thread_kernel
-      bool constant = true;
-      for (int q = 1; q < Q && constant; ++q)
-        for (int r = 0; r < 12; ++r)
-          if (std::fabs(Gm[3 * q * N + r] - Gm[r]) > 1e-13) constant = false;
-      if (constant) {
-        P->p1_tab.assign(13, 0.0);
-        for (int k = 0; k < 3; ++k)
-          for (int i = 0; i < 4; ++i) P->p1_tab[4 * k + i] = Gm[k * N + i];
-        long double ws = 0.0L;
-        for (int q = 0; q < Q; ++q) ws += d->cell_weights[q];
-        P->p1_tab[12] = (double)ws;
-      }
-    }
+    P->info.cell_engine = eng == 4 ? 4 : ci.table == 2 ? 3 : 1;
   }
 
   // per-cell geometry (G, mass factor), computed once on the device
@@ -991,29 +690,6 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       enc[i] = (d->dirichlet_mask && d->dirichlet_mask[g]) ? ~g : g;
     }
     if ((rc = upload(&P->dofs, enc.data(), enc.size(), &total))) return bail(rc);
-    // patch-local assembly when the launcher supports it and the cell order has locality
-    tmf::CellLaunchInfo ci;
-    bool ok = true;
-    tmf::CellArgs dummy{};
-    dummy.n_cells = P->n_cells;
-    dummy.nc = P->nc;
-    TMF_CUDA(tmf::launch_cell(P->N, P->Qk, false, false, dummy, P->n_sm, 0, &ci, &ok, P->variant, P->kengine));
-    if (P->patches == 2 && ci.patch_cells > 0) {
-      PatchTables T;
-      build_patches(enc.data(), P->n_cells, P->N, ci.patch_cells, T);
-      P->patch_ratio = T.slots ? (double)T.unique / (double)T.slots : 1.0;
-      P->info.patch_ratio = P->patch_ratio;
-      if (P->patches == 2) {   // opt-in: measured slower than the DMMA kernel
-        P->local = true;
-        P->numax = T.numax;
-        P->recmax = T.recmax;
-        P->info.patch_cells = ci.patch_cells;
-        if ((rc = upload(&P->pmeta, T.meta.data(), T.meta.size(), &total))) return bail(rc);
-        if ((rc = upload(&P->prec, T.rec.data(), T.rec.size(), &total))) return bail(rc);
-        TMF_CUDA(tmf::launch_patch_geometry(P->cell_geo, P->pmeta, P->prec, P->n_cells, ci.patch_cells,
-                                            P->n_sm, 0));
-      }
-    }
     std::vector<int> fix;
     if (d->dirichlet_mask)
       for (int64_t g = 0; g < d->n_scalar_dofs; ++g)
@@ -1160,46 +836,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
                                               std::to_string(N) + ", " + std::to_string(QF) + ")"));
     if ((int64_t)fr.size() != 24LL * fi.nfrag * 32) return bail(fail(TMF_EINVAL, "internal: face fragments"));
     if ((rc = upload(&P->face_frags, fr.data(), fr.size(), &total))) return bail(rc);
-    // reference-tensor interior-face tables (face engine 2; DMMAs per 8 faces 48 / 150 / 416
-    // at P2-P4 vs 60 / 170 / 432 for the n_qf-point loop and 40 / 102 / 192 for the modal
-    // one; measured faces P2 96^3 Helmholtz 1.89 -> 1.77 ms, P3 64^3 1.34 -> 1.14 ms, P4
-    // 48^3 1.71 -> 1.31 ms against the n_qf-point loop)
-    if (fe == 2 && d->n_interior_faces > 0) {
-      std::vector<double> tf;
-      tf.reserve((size_t)96 * fi.tnfrag * 32);
-      const double* Fv = d->face_values;
-      const double* Fg = d->face_grads;
-      std::vector<std::array<std::array<double, 3>, 3>> frame(4);
-      for (int lf = 0; lf < 4; ++lf) {
-        const double R[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
-        const int fvv[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
-        for (int k = 0; k < 3; ++k) {
-          frame[lf][0][k] = R[fvv[lf][1]][k] - R[fvv[lf][0]][k];
-          frame[lf][1][k] = R[fvv[lf][2]][k] - R[fvv[lf][0]][k];
-          frame[lf][2][k] = R[lf][k] - R[fvv[lf][0]][k];
-        }
-      }
-      auto Ev = [&](int lf, int code, int c, int q, int a) -> double {
-        const int jj = perm[lf * N + a];
-        const size_t t = (size_t)(lf * 6 + code);
-        if (c == 0) return Fv[(t * QF + q) * N + jj];
-        const auto& av = frame[lf][c - 1];
-        const double* g = Fg + t * 3 * QF * N;
-        return av[0] * g[(3 * q) * N + jj] + av[1] * g[(3 * q + 1) * N + jj] + av[2] * g[(3 * q + 2) * N + jj];
-      };
-      if (build_face_tensor_fragments(N, NF, QF, Ev, d->face_weights, tf) != TMF_OK)
-        return bail(fail(TMF_EINVAL, "face tables are not those of a nodal basis (tensor face form)"));
-      if ((int64_t)tf.size() != 96LL * fi.tnfrag * 32) return bail(fail(TMF_EINVAL, "internal: tensor face fragments"));
-      if ((rc = upload(&P->face_tfrags, tf.data(), tf.size(), &total))) return bail(rc);
-    }
     const int chunk = ((d->flags >> 8) & 0xF) ? 8 * ((d->flags >> 8) & 0xF) : fi.chunk;
-    // window-major runs only for the default blocked kernel the launcher will pick (P4's
-    // default is the asynchronous-ring kernel with its own grid; tuning variants may deal
-    // chunks round-robin; the tensor engine has its own kernel)
-    // (opt-in, flags bit 21: measured at C3 64^3 -- DRAM per launch 2.94 -> 1.56 GB but the face
-    // kernel 0.890 -> 0.924 ms, since a CTA then restages its tables for almost every chunk;
-    // the kernel is DMMA/latency-bound, not DRAM-bound)
-    if (P->face_variant == 0 && N != 35 && fe != 2 && ((d->flags >> 21) & 1)) P->face_blocked_grid = fi.blocked_grid;
     if ((rc = build_face_batches(P, d, chunk, &total))) return bail(rc);
     // per-face geometry, computed once on the device (64 B per face slot)
     for (int bnd = 0; bnd < 2; ++bnd) {
@@ -1211,8 +848,8 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       TMF_CUDA(tmf::launch_face_geometry(bnd != 0, P->face_geo_args(bnd != 0), P->n_sm, 0));
     }
     P->info.n_face_batches = (int32_t)(P->n_if_batches + P->n_bf_batches);
-    P->info.face_engine = P->face_tfrags ? 2 : P->face_engine;
-    P->info.flops_issued += (double)P->nc * (P->n_if_batches * (P->face_tfrags ? fi.tdmma_per_batch : fi.dmma_per_batch) +
+    P->info.face_engine = P->face_engine;
+    P->info.flops_issued += (double)P->nc * (P->n_if_batches * fi.dmma_per_batch +
                                              P->n_bf_batches * fi.dmma_per_batch / 2) * 512.0;
   }
 
@@ -1253,13 +890,6 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       fe -= (double)d->n_interior_faces * (32.0 * nqf * nd + 26.0 * nqf) + (double)nbf_dir * (16.0 * nqf * nd + 13.0 * nqf);
       fe += (double)d->n_interior_faces * (32.0 * NFm * nd + 26.0 * NFm) + (double)nbf_dir * (16.0 * NFm * nd + 13.0 * NFm);
     }
-    if (faces && P->face_tfrags) {
-      // tensor face form: the nonzero blocks (F x F: s tau full, each m~ coefficient 3/4 of
-      // it; F x I and I x F: the transversal pair) plus the per-output contraction
-      const double NF = (P->degree + 1) * (P->degree + 2) / 2, NI = nd - NF;
-      fe -= (double)d->n_interior_faces * (32.0 * nqf * nd + 26.0 * nqf);
-      fe += (double)d->n_interior_faces * (2.0 * (22.0 * NF * NF + 8.0 * NF * NI) + 2.0 * (14.0 * NF + 4.0 * NI));
-    }
     P->info.flops_engine = fe * P->nc;
     double b = 16.0 * (double)P->n_global + 24.0 * (double)P->n_verts;
     if (!dg)
@@ -1299,8 +929,6 @@ int tmf_plan_set_peers(tmf_plan* P, int32_t n_ranks, const uint64_t* peer_u, con
       (n_ghost && (!ghost_rank || !ghost_index)) || n_peer_free_cells < 0 || n_peer_free_cells > P->n_cells)
     return fail(TMF_EINVAL, "bad peer description");
   if (!P->dg && !peer_y) return fail(TMF_EINVAL, "a CG plan needs the peers' y buffers (ghost RED)");
-  if (P->engine == 2 || P->local)
-    return fail(TMF_EINVAL, "peer-memory ghosts need the DMMA cell engine (no DFMA engine / patches)");
   const int64_t n_entries = P->dg ? P->n_cells : P->n_scalar;
   if (n_own + n_ghost != n_entries)
     return fail(TMF_EINVAL, "n_own + n_ghost must equal the plan's local " +
@@ -1548,8 +1176,8 @@ int tmf_apply_timed(tmf_plan* P, const double* u, double* y, void* stream, int r
   for (auto& e : ev) TMF_CUDA(cudaEventCreate(&e));
   double acc[4] = {0, 0, 0, 0};
   // which stage events launch_apply records (see there): ev[0] and ev[3] always
-  const bool fix = !P->dg && P->n_fix, conc = P->dg && P->faces && P->concurrent;
-  const bool e1 = conc || P->faces || fix, e2 = conc || (P->faces && fix);
+  const bool fix = !P->dg && P->n_fix;
+  const bool e1 = P->faces || fix, e2 = P->faces && fix;
   for (int r = 0; r < reps; ++r) {
     int rc = launch_apply(P, u, y, st, ev);
     if (rc) return rc;
@@ -1559,7 +1187,7 @@ int tmf_apply_timed(tmf_plan* P, const double* u, double* y, void* stream, int r
     // cell | faces | fixup; a stage without its closing event ends at ev[3]
     const cudaEvent_t end_cell = e1 ? ev[1] : ev[3];
     cudaEventElapsedTime(&a, ev[0], end_cell);
-    if (P->faces || conc) cudaEventElapsedTime(&b, end_cell, e2 ? ev[2] : ev[3]);
+    if (P->faces) cudaEventElapsedTime(&b, end_cell, e2 ? ev[2] : ev[3]);
     if (fix) cudaEventElapsedTime(&c, e2 ? ev[2] : end_cell, ev[3]);
     acc[0] += t;
     acc[1] += a;
@@ -1607,7 +1235,7 @@ int tmf_pcg(tmf_plan* P, const double* b, double* x, int iters, double* res_norm
   const int grid = P->n_sm * 4, blk = 512;
   // fused iteration when the element energies are available (tensor cell engine, plain
   // single-GPU plan): apply(+p.Ap) -> residual -> step (x, p, q = 0)
-  const bool fused = (P->info.cell_engine == 3 || P->info.cell_engine == 4) && !P->local && !P->peer.u && !P->dg;
+  const bool fused = (P->info.cell_engine == 3 || P->info.cell_engine == 4) && !P->peer.u && !P->dg;
   if (fused) {
     tmf::pcg_init_fused_kernel<<<grid, blk, 0, st>>>(b, dg, x, r, z, p, q, n, rz, rr);
     TMF_CUDA(cudaGetLastError());

@@ -40,18 +40,8 @@ struct CellArgs {
   const double* __restrict__ frags;  // B1 then B2 fragments (global; staged to smem)
   int64_t n_cells;
   int nc;                          // interleaved components
-  int accumulate;                  // DG: add into y (concurrent face kernel) instead of storing
-  // CG warp-patch-local assembly (cell_patch_kernel.cuh): patches of 32
-  // consecutive cells, one 16-byte aligned record each in prec; pmeta[p] =
-  // {record offset (16 B units), unique DoFs nu, incidences, record size (16 B)}
-  const int4* __restrict__ pmeta = nullptr;
-  const void* __restrict__ prec = nullptr;
-  int numax = 0;                   // max unique DoFs of a patch (even)
-  int recmax = 0;                  // max record bytes (multiple of 16)
   PeerArgs peer;                   // multi-GPU: ghost DoFs read / scattered over peer memory
-  double* energy = nullptr;        // CG tensor engine: += sum_e u_e^T A_e u_e (PCG's p.Ap)
-  const double* hP1 = nullptr;     // HOST: P1 constant gradients a[3][4] and sum of weights (13
-                                   // doubles, launcher only: a kernel parameter of the P1 kernel)
+  double* energy = nullptr;        // CG tensor / modal engines: += sum_e u_e^T A_e u_e (PCG's p.Ap)
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the
@@ -113,22 +103,17 @@ struct CellShape {
   static constexpr int MT = (KK + 2 * NJ) <= 7 ? 2 : 1;
 };
 
-// MT_: tiles per warp iteration (0 = CellShape default); MINB: min CTAs/SM hint;
-// PF: software-prefetch the next super-tile's gathered u and geometry (indices 2 ahead)
-// BLK: each warp takes a contiguous run of super-tiles instead of a grid-strided set
-// SKEW: issue GEMM1 of the next point tile before the D action of the current one
 // PEER: ghost DoFs through peer memory (multi-GPU, CellArgs::peer); a separate
 // instantiation so the single-GPU kernel carries no ghost test (it costs 10-20 %)
 // AS: asynchronous gather pipeline with AS stages -- each warp cp.async's the gathered u
 // (8-byte copies, zero-filled for masked DoFs) and the 64-byte geometry records of the
 // super-tile AS-1 ahead into its own shared-memory ring, so AS-1 tiles' loads are in
-// flight without holding registers (the register-prefetch PF variant spills)
-template <int N, int Q, bool MASS, bool DG, int BLOCK, int MT_ = 0, int MINB = 1, bool PF = false,
-          bool BLK = false, bool SKEW = false, bool PEER = false, int AS = 0>
-__global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
+// flight without holding registers (measured: pays at P4 only)
+template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0>
+__global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
   using S = CellShape<N, Q, MASS>;
-  constexpr int MT = MT_ ? MT_ : S::MT;
-  static_assert(AS == 0 || (!PF && !PEER), "the async ring replaces PF; no peer gathers");
+  constexpr int MT = S::MT;
+  static_assert(AS == 0 || !PEER, "the async ring has no peer gathers");
   extern __shared__ __align__(16) double smem[];
   {
     const double2* src = reinterpret_cast<const double2*>(a.frags);
@@ -150,11 +135,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
   // Index prefetch: the DoF indices of the warp's next super-tile are loaded
   // while the current one computes, so each start pays one memory round trip
   // (u and the per-cell geometry, issued together) instead of two.
-  const int64_t gw = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
-  const int64_t per = (nst + nwarps - 1) / nwarps;
-  int64_t st = BLK ? gw * per : gw;
-  const int64_t st_end = BLK ? (st + per < nst ? st + per : nst) : nst;
-  const int64_t step = BLK ? 1 : nwarps;
+  int64_t st = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+  const int64_t step = nwarps;
   int nidx[MT][S::KK];
   auto load_indices = [&](int64_t t) {
     const int cmp = a.nc == 1 ? 0 : (int)(t / cst);
@@ -227,17 +209,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
       load_indices(st + (s + 1) * step);
     }
   }
-  double pav[MT][S::KK], pG[MT][6], pmdet[MT];
   // sum over the lane's points of g . (G g) = u_e^T A_e u_e when the point weights are 1:
   // compiled for the modal tables only (fewer "points" than DoFs), CG; CellArgs::energy
   constexpr bool EN = !DG && Q < N;
   double en = 0.0;
-  if (PF) {
-    load_data(st, pav, pG, pmdet);
-    load_indices(st + step);
-  }
 
-  for (; st < st_end; st += step) {
+  for (; st < nst; st += step) {
     const int comp = a.nc == 1 ? 0 : (int)(st / cst);
     int64_t cell[MT];
     bool valid[MT];
@@ -269,17 +246,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
         mdet[m] = MASS ? gg[6] : 0.0;
       }
       slot = slot + 1 == AS ? 0 : slot + 1;
-    } else if (PF) {
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-#pragma unroll
-        for (int kk = 0; kk < S::KK; ++kk) av[m][kk] = pav[m][kk];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) G[m][i] = pG[m][i];
-        mdet[m] = pmdet[m];
-      }
-      load_data(st + step, pav, pG, pmdet);
-      load_indices(st + 2 * step);
     } else {
       load_data(st, av, G, mdet);
       load_indices(st + step);
@@ -369,36 +335,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
         }
     };
     double vg[MT][2][2];
-    if (SKEW) {
-      // skewed software pipeline: GEMM1 of point tile t+1 is issued before the D
-      // action of tile t, so the FP64-pipe D action overlaps tensor work in flight
-      double va[MT][S::NC][2], vb[MT][S::NC][2];
-      if (S::T > 0) gemm1(0, va);
-      else if (S::GRP) gemm1g(vg);
 #pragma unroll
-      for (int t = 0; t < S::T; ++t) {
-        if (t % 2 == 0) {
-          if (t + 1 < S::T) gemm1(t + 1, vb);
-          else if (S::GRP) gemm1g(vg);
-          daction_gemm2(t, va);
-        } else {
-          if (t + 1 < S::T) gemm1(t + 1, va);
-          else if (S::GRP) gemm1g(vg);
-          daction_gemm2(t, vb);
-        }
-      }
-      if (S::GRP) dgemm2g(vg);
-    } else {
-#pragma unroll
-      for (int t = 0; t < S::T; ++t) {
-        double v[MT][S::NC][2];
-        gemm1(t, v);
-        daction_gemm2(t, v);
-      }
-      if (S::GRP) {
-        gemm1g(vg);
-        dgemm2g(vg);
-      }
+    for (int t = 0; t < S::T; ++t) {
+      double v[MT][S::NC][2];
+      gemm1(t, v);
+      daction_gemm2(t, v);
+    }
+    if (S::GRP) {
+      gemm1g(vg);
+      dgemm2g(vg);
     }
 
     // ---- scatter / store: lane owns DoFs 8nj + 2q4 + {0,1}
@@ -412,11 +357,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_apply_kernel(CellArgs a) {
           const int j = 8 * nj + 2 * q4 + i;
           if (j < N) {
             if (DG) {
-              double* dst = a.y + (cell[m] * N + j) * a.nc + comp;
-              if (a.accumulate)
-                atomicAdd(dst, yacc[m][nj][i]);
-              else
-                *dst = yacc[m][nj][i];
+              a.y[(cell[m] * N + j) * a.nc + comp] = yacc[m][nj][i];
             } else {
               const int64_t g = __ldg(a.dofs + cell[m] * N + j);
               if (g >= 0) {

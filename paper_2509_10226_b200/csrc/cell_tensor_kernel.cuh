@@ -41,10 +41,7 @@ struct TensorShape {
 };
 
 // MT: 8-cell tiles per warp iteration (they share every B-fragment load)
-// PF: software pipeline one super-tile deeper -- the next super-tile's gathered u and
-// geometry are loaded while this one computes (indices two ahead); for the low degrees,
-// whose few DMMAs cannot hide a memory round trip per tile
-template <int N, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PEER = false, bool PF = false>
+template <int N, bool MASS, bool DG, int BLOCK, int MT, int MINB, bool PEER = false>
 __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
   using S = TensorShape<N, MASS>;
   constexpr int KK = S::KK, NP = S::NP;
@@ -107,13 +104,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
       mdet[m] = MASS ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
     }
   };
-  int pidx[MT][KK];
-  double pav[MT][KK], pG[MT][6], pmdet[MT];
   double en = 0.0;   // sum of u_i y_i over the lane's outputs (element energies, CG)
-  if (PF) {
-    load_data(st, pidx, pav, pG, pmdet);
-    load_indices(st + step);
-  }
 
   for (; st < nst; st += step) {
     const int comp = a.nc == 1 ? 0 : (int)(st / cst);
@@ -122,24 +113,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
     double av[MT][KK], G[MT][6], mdet[MT];
 #pragma unroll
     for (int m = 0; m < MT; ++m) cell[m] = ((st - (int64_t)comp * cst) * MT + m) * 8 + cs;
-    if (PF) {
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-#pragma unroll
-        for (int kk = 0; kk < KK; ++kk) {
-          idx[m][kk] = pidx[m][kk];
-          av[m][kk] = pav[m][kk];
-        }
-#pragma unroll
-        for (int i = 0; i < 6; ++i) G[m][i] = pG[m][i];
-        mdet[m] = pmdet[m];
-      }
-      load_data(st + step, pidx, pav, pG, pmdet);
-      load_indices(st + 2 * step);
-    } else {
-      load_data(st, idx, av, G, mdet);
-      load_indices(st + step);
-    }
+    load_data(st, idx, av, G, mdet);
+    load_indices(st + step);
 
     // one i-block at a time: GEMM columns (ib, kl), contraction, then its scatter/store
     // (the lane owns DoF 4 ib + q4 of cell cs, whose index it gathered for k-step ib)
@@ -174,11 +149,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
       for (int m = 0; m < MT; ++m) {
         if (j >= N || cell[m] >= a.n_cells) continue;
         if (DG) {
-          double* dst = a.y + (cell[m] * N + j) * a.nc + comp;
-          if (a.accumulate)
-            atomicAdd(dst, yv[m]);
-          else
-            *dst = yv[m];
+          a.y[(cell[m] * N + j) * a.nc + comp] = yv[m];
         } else {
           const int g = idx[m][ib];
           en = fma(av[m][ib], yv[m], en);   // av = u at this DoF (0 when masked)
@@ -198,77 +169,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
     if (lane == 0) atomicAdd(a.energy, en);
   }
   if (PEER && a.peer.y != nullptr) __threadfence_system();
-}
-
-// ---- P1, thread per cell.  Linear basis functions have constant gradients, so the
-// reference's point loop collapses to one point: with a_k[i] = d_k phi_i (the same at
-// every quadrature point) and W = sum_q w_q,
-//     y_e = W A^T G_e A u_e,     A = [a_k[i]] (3 x 4)
-// i.e. 12 + 9 + 12 = 33 FMAs per cell (the 6 x 4 x 4 reference tensor has rank one per
-// coefficient).  A and W (13 doubles, checked constant over the points on the host) are a
-// kernel parameter, so they sit in registers; each thread issues its own cell's index
-// (one 16-byte load), geometry and u loads, so a warp has 32 cells' loads in flight
-// instead of the tile kernel's 8.  Measured (tools/gpu_p1.sh, gpu_p1b.sh): no faster than the
-// tile kernel (48^3 reordered 29-30 us vs 32; 96^3 155 vs 142 us) -- both are bound by the
-// scatter: with the REDs removed (timing experiment) the same kernel takes 21 / 81 us, i.e.
-// the fp64 REDs to L2 cost ~3.5 ns per 1000 (~290 G REDs/s), and without them the 64 B/cell
-// geometry + 16 B/cell index stream is DRAM-bound.  Kept as kernel variant 7 (P1 CG/DG).
-struct P1Tab {
-  double a[3][4];   // a[k][i] = d phi_i / d xi_k
-  double w;         // sum of the quadrature weights
-};
-
-template <bool DG, int BLOCK, int MINB>
-__global__ void __launch_bounds__(BLOCK, MINB) cell_p1_thread_kernel(CellArgs a, const P1Tab T) {
-  const int64_t total = a.n_cells * a.nc;
-  double en = 0.0;
-  for (int64_t t = (int64_t)blockIdx.x * BLOCK + threadIdx.x; t < total; t += (int64_t)gridDim.x * BLOCK) {
-    const int comp = a.nc == 1 ? 0 : (int)(t / a.n_cells);
-    const int64_t c = t - (int64_t)comp * a.n_cells;
-    int idx[4];
-    if (DG) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) idx[j] = (int)(c * 4 + j);
-    } else {
-      const int4 v = __ldg(reinterpret_cast<const int4*>(a.dofs) + c);
-      idx[0] = v.x; idx[1] = v.y; idx[2] = v.z; idx[3] = v.w;
-    }
-    double u[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) u[j] = idx[j] >= 0 ? __ldg(a.u + (int64_t)idx[j] * a.nc + comp) : 0.0;
-    const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * c);
-    const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
-    double g[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) s = fma(T.a[k][j], u[j], s);
-      g[k] = s * T.w;
-    }
-    const double d0 = g01.x * g[0] + g01.y * g[1] + g23.x * g[2];
-    const double d1 = g01.y * g[0] + g23.y * g[1] + g45.x * g[2];
-    const double d2 = g23.x * g[0] + g45.x * g[1] + g45.y * g[2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const double yi = fma(T.a[0][i], d0, fma(T.a[1][i], d1, T.a[2][i] * d2));
-      if (DG) {
-        double* dst = a.y + (c * 4 + i) * a.nc + comp;
-        if (a.accumulate)
-          atomicAdd(dst, yi);
-        else
-          *dst = yi;
-      } else if (idx[i] >= 0) {
-        en = fma(u[i], yi, en);
-        atomicAdd(a.y + (int64_t)idx[i] * a.nc + comp, yi);
-      }
-    }
-  }
-  if (!DG && a.energy != nullptr) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) en += __shfl_xor_sync(0xffffffffu, en, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(a.energy, en);
-  }
 }
 
 }  // namespace tmf

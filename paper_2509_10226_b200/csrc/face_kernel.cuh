@@ -54,8 +54,6 @@ struct FaceArgs {
   int n_dpc;
   int nc;
   PeerArgs peer;                      // multi-GPU: ghost cells' u read from their owner (n_own = cells)
-  const double* __restrict__ tfrags = nullptr;   // interior faces, reference-tensor form
-                                                 // (face_tensor_kernel.cuh): 96 signature tables
 };
 
 // Per-face geometry, computed once at plan creation by face_geometry_kernel and
@@ -218,15 +216,10 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 // BLOCKED: each CTA takes a contiguous run of chunks (consecutive chunks of one
 // (window, signature) group share their tables, so restaging and both barriers are
 // skipped); otherwise chunks are dealt round-robin.
-// TPF (with !BLOCKED): chunks are dealt round-robin, so all CTAs march through the
-// (window, signature)-sorted chunk list together and the live set of u / y stays in
-// L2; the next chunk's tables are prefetched with cp.async into a second shared
-// buffer while the current chunk computes (one barrier per chunk, no load latency).
 template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool TPF = false, bool PEER = false>
+          bool PEER = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
-  constexpr int TAB = (BOUNDARY ? 1 : 2) * S::NFRAG * 32;   // doubles per staged table set
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
   const int fs = lane >> 2;
@@ -243,56 +236,24 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     return __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
   };
-  auto stage_async = [&](int4 c, double* d) {
-    const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)c.x * S::NFRAG * 32);
-    for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(d + 2 * i)),
-                   "l"(s0 + i) : "memory");
-    if (!BOUNDARY) {
-      const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)c.y * S::NFRAG * 32);
-      for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n"
-                     ::"r"((uint32_t)__cvta_generic_to_shared(d + S::NFRAG * 32 + 2 * i)), "l"(s1 + i) : "memory");
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
   int cur_x = -1, cur_y = -2;
-  int buf = 0;   // TPF: staged table set in use
-  if (TPF && w0 < w1) {
-    stage_async(chunk_at(w0), smem);
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();
-  }
   for (int64_t w = w0; w < w1; w += wstep) {
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     const int4 ch = chunk_at(w);
-    bool next_restage = false;
-    if (TPF) {
-      // prefetch the next chunk's tables when its signature differs
-      if (w + wstep < w1) {
-        const int4 nx = chunk_at(w + wstep);
-        next_restage = nx.x != ch.x || nx.y != ch.y;
-        if (next_restage) stage_async(nx, smem + (buf ^ 1) * TAB);
-      }
-    } else {
-      const bool restage = ch.x != cur_x || ch.y != cur_y;
+    if (ch.x != cur_x || ch.y != cur_y) {
       cur_x = ch.x;
       cur_y = ch.y;
-      if (restage) {
-        __syncthreads();  // previous chunk's warps are done with the staged tables
-        {
-          const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.x * S::NFRAG * 32);
-          double2* d = reinterpret_cast<double2*>(smem);
-          for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[i] = __ldg(s0 + i);
-          if (!BOUNDARY) {
-            const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.y * S::NFRAG * 32);
-            for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[S::NFRAG * 16 + i] = __ldg(s1 + i);
-          }
-        }
-        __syncthreads();
+      __syncthreads();  // previous chunk's warps are done with the staged tables
+      const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.x * S::NFRAG * 32);
+      double2* d = reinterpret_cast<double2*>(smem);
+      for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[i] = __ldg(s0 + i);
+      if (!BOUNDARY) {
+        const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.y * S::NFRAG * 32);
+        for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) d[S::NFRAG * 16 + i] = __ldg(s1 + i);
       }
+      __syncthreads();
     }
-    const double* Fm = smem + (TPF ? buf * TAB : 0);
+    const double* Fm = smem;
     const double* Fp = Fm + S::NFRAG * 32;
     const int* perm_m = a.perm + (ch.x / 6) * N;                  // gather order, minus side
     const int* perm_p = a.perm + (BOUNDARY ? 0 : ch.y / 6) * N;   // plus side
@@ -430,172 +391,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
           }
       }
     }
-    if (TPF) {
-      if (next_restage) asm volatile("cp.async.wait_all;\n" ::: "memory");
-      __syncthreads();   // the chunk's warps are done with buffer buf; the next tables landed
-      if (next_restage) buf ^= 1;
-    }
   }
 }
 
 
-// Interior faces, MB batches (8-face M-tiles) per warp iteration: the records, geometry and
-// gathered u of all MB batches are loaded together (MB x the memory-level parallelism of the
-// one-batch loop) and every staged B fragment feeds 2 MB DMMAs (both sides of MB batches).
-// Same tables, signatures and chunk dealing (BLOCKED runs or round-robin) as
-// face_apply_kernel; no cross-iteration prefetch.
-template <int N, int QF, int MB, int MINB = 2, int BLOCK = 256, bool BLOCKED = false>
-__global__ void __launch_bounds__(BLOCK, MINB) face_mb_kernel(FaceArgs a) {
-  using S = FaceShape<N, QF>;
-  extern __shared__ __align__(16) double smem[];
-  const int lane = threadIdx.x & 31;
-  const int fs = lane >> 2;
-  const int q4 = lane & 3;
-  const int warp = threadIdx.x >> 5;
-  const int nwb = blockDim.x >> 5;
-  const int64_t nwork = a.n_chunks * a.nc;
-  const int64_t per = (nwork + gridDim.x - 1) / gridDim.x;
-  const int64_t w0 = BLOCKED ? blockIdx.x * per : blockIdx.x;
-  const int64_t w1 = BLOCKED ? (w0 + per < nwork ? w0 + per : nwork) : nwork;
-  const int64_t wstep = BLOCKED ? 1 : gridDim.x;
-  int cur_x = -1, cur_y = -2;
-  for (int64_t w = w0; w < w1; w += wstep) {
-    const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
-    const int4 ch = __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
-    if (ch.x != cur_x || ch.y != cur_y) {
-      cur_x = ch.x;
-      cur_y = ch.y;
-      __syncthreads();
-      const double2* s0 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.x * S::NFRAG * 32);
-      const double2* s1 = reinterpret_cast<const double2*>(a.frags + (int64_t)ch.y * S::NFRAG * 32);
-      double2* d = reinterpret_cast<double2*>(smem);
-      for (int i = threadIdx.x; i < S::NFRAG * 16; i += blockDim.x) {
-        d[i] = __ldg(s0 + i);
-        d[S::NFRAG * 16 + i] = __ldg(s1 + i);
-      }
-      __syncthreads();
-    }
-    const double* Fm = smem;
-    const double* Fp = smem + S::NFRAG * 32;
-    const int* perm_m = a.perm + (ch.x / 6) * N;
-    const int* perm_p = a.perm + (ch.y / 6) * N;
-    for (int bi = warp; bi < ch.w; bi += nwb * MB) {
-      int cm[MB], cp[MB];
-      double am[MB][S::KK], ap[MB][S::KK], gg[MB][8];
-#pragma unroll
-      for (int t = 0; t < MB; ++t) {
-        const int b = bi + t * nwb;
-        cm[t] = cp[t] = -1;
-        if (b < ch.w) {
-          const int64_t slot = ((int64_t)ch.z + b) * 8 + fs;
-          cm[t] = __ldg(a.cm + slot);
-          cp[t] = __ldg(a.cp + slot);
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < MB; ++t) {
-        const int b = bi + t * nwb;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) gg[t][i] = 0.0;
-        if (b < ch.w) {
-          const double2* gp = reinterpret_cast<const double2*>(a.geo + (((int64_t)ch.z + b) * 8 + fs) * 8);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const double2 v = __ldg(gp + i);
-            gg[t][2 * i] = v.x;
-            gg[t][2 * i + 1] = v.y;
-          }
-        }
-#pragma unroll
-        for (int kk = 0; kk < S::KK; ++kk) {
-          const int j = 4 * kk + q4;
-          am[t][kk] = 0.0;
-          ap[t][kk] = 0.0;
-          if (cm[t] >= 0 && j < N) {
-            am[t][kk] = __ldg(a.u + ((int64_t)cm[t] * N + __ldg(perm_m + j)) * a.nc + comp);
-            ap[t][kk] = __ldg(a.u + ((int64_t)cp[t] * N + __ldg(perm_p + j)) * a.nc + comp);
-          }
-        }
-      }
-      double ym[MB][S::NJ][2], yp[MB][S::NJ][2];
-#pragma unroll
-      for (int t = 0; t < MB; ++t)
-#pragma unroll
-        for (int nj = 0; nj < S::NJ; ++nj) ym[t][nj][0] = ym[t][nj][1] = yp[t][nj][0] = yp[t][nj][1] = 0.0;
-#pragma unroll
-      for (int g = 0; g < S::G; ++g) {
-        double vm[MB][2][2], vp[MB][2][2];
-#pragma unroll
-        for (int t = 0; t < MB; ++t)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) vm[t][h][0] = vm[t][h][1] = vp[t][h][0] = vp[t][h][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < S::KK; ++kk)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (h == 0 && kk >= S::KKF) continue;
-            const int f = S::b1(g, h, kk) * 32 + lane;
-            const double bm = Fm[f], bp = Fp[f];
-#pragma unroll
-            for (int t = 0; t < MB; ++t) {
-              dmma(vm[t][h], am[t][kk], bm);
-              dmma(vp[t][h], ap[t][kk], bp);
-            }
-          }
-        double qm[MB][4], qp[MB][4];
-#pragma unroll
-        for (int t = 0; t < MB; ++t) {
-          const double nj = vp[t][0][0] - vm[t][0][0];   // -[[u]]
-          double qv = -gg[t][6] * nj;
-          qv = fma(-gg[t][0], vm[t][0][1], qv);
-          qv = fma(-gg[t][1], vm[t][1][0], qv);
-          qv = fma(-gg[t][2], vm[t][1][1], qv);
-          qv = fma(-gg[t][3], vp[t][0][1], qv);
-          qv = fma(-gg[t][4], vp[t][1][0], qv);
-          qv = fma(-gg[t][5], vp[t][1][1], qv);
-          qm[t][0] = qv;
-          qp[t][0] = -qv;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            qm[t][1 + k] = nj * gg[t][k];
-            qp[t][1 + k] = nj * gg[t][3 + k];
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int nj = 0; nj < S::NJ; ++nj) {
-            if (c < 3 && nj >= S::NJF) continue;
-            const int f = S::b2(g, c, nj) * 32 + lane;
-            const double bm = Fm[f], bp = Fp[f];
-#pragma unroll
-            for (int t = 0; t < MB; ++t) {
-              dmma(ym[t][nj], qm[t][c], bm);
-              dmma(yp[t][nj], qp[t][c], bp);
-            }
-          }
-      }
-#pragma unroll
-      for (int t = 0; t < MB; ++t) {
-        if (cm[t] < 0) continue;
-#pragma unroll
-        for (int nj = 0; nj < S::NJ; ++nj)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int j = 8 * nj + 2 * q4 + i;
-            if (j < N) {
-              atomicAdd(a.y + ((int64_t)cm[t] * N + __ldg(perm_m + j)) * a.nc + comp, ym[t][nj][i]);
-              atomicAdd(a.y + ((int64_t)cp[t] * N + __ldg(perm_p + j)) * a.nc + comp, yp[t][nj][i]);
-            }
-          }
-      }
-    }
-  }
-}
 
-}  // namespace tmf
 
-namespace tmf {
 
 // Interior faces with an asynchronous gather ring (the face-kernel analogue of the cell
 // kernel's AS pipeline).  Each warp walks its batches of the CTA's chunks as one flat

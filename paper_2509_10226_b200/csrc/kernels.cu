@@ -8,32 +8,32 @@
 namespace tmf {
 
 cudaError_t cell_dispatch_4_4(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_4_5(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_10_14(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_10_15(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_20_35(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_4_1(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_10_4(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_20_10(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_35_20(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 cudaError_t cell_dispatch_35_70(bool mass, bool dg, const CellArgs& a, int n_sm, cudaStream_t st,
-                              CellLaunchInfo* info, int variant, int engine);
+                              CellLaunchInfo* info, int engine);
 
 cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& a, int n_sm,
-                        cudaStream_t st, CellLaunchInfo* info, bool* supported, int variant, int engine) {
+                        cudaStream_t st, CellLaunchInfo* info, bool* supported, int engine) {
   *supported = true;
 #define TMF_CELL(NN, QQ)   \
   if (n_dpc == NN && n_q == QQ) \
-    return cell_dispatch_##NN##_##QQ(mass, dg, a, n_sm, st, info, variant, engine);
+    return cell_dispatch_##NN##_##QQ(mass, dg, a, n_sm, st, info, engine);
   TMF_CELL(4, 4)
   TMF_CELL(4, 5)
   TMF_CELL(10, 14)
@@ -51,25 +51,6 @@ cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& 
 
 cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st) {
   cell_geometry_kernel<<<n_sm * 8, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-// G into the warp-patch records (cell_patch_kernel.cuh): record p starts with
-// G component-major, geo[i*CH + cl] = cgeo[(p*CH + cl)*8 + i] (0 past the last cell)
-static __global__ void patch_geometry_kernel(const double* __restrict__ cgeo, const int4* __restrict__ pmeta,
-                                             double* __restrict__ prec, int64_t n_cells, int CH) {
-  const int64_t n = (n_cells + CH - 1) / CH * CH;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = c / CH, cl = c - p * CH;
-    double* geo = prec + (int64_t)pmeta[p].x * 2;   // 16-byte units
-#pragma unroll
-    for (int i = 0; i < 6; ++i) geo[i * CH + cl] = c < n_cells ? cgeo[c * 8 + i] : 0.0;
-  }
-}
-
-cudaError_t launch_patch_geometry(const double* cgeo, const int4* pmeta, void* prec, int64_t n_cells,
-                                  int CH, int n_sm, cudaStream_t st) {
-  patch_geometry_kernel<<<n_sm * 8, 256, 0, st>>>(cgeo, pmeta, static_cast<double*>(prec), n_cells, CH);
   return cudaGetLastError();
 }
 

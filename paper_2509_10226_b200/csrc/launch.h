@@ -17,10 +17,9 @@ struct CellLaunchInfo {
   int grid = 0;
   int smem = 0;
   int frag_doubles = 0;
-  int table = 0;             // 0 = DMMA lane fragments, 1 = point-major DFMA rows,
+  int table = 0;             // 0 = DMMA lane fragments (cell_kernel.cuh),
                              // 2 = reference-tensor fragments (cell_tensor_kernel.cuh)
   double flops_issued = 0;   // FP64 FMA*2 issued per launch (padding included)
-  int patch_cells = 0;       // CG patch-local assembly: cells per patch (0 = not supported)
 };
 
 struct FaceLaunchInfo {
@@ -28,21 +27,15 @@ struct FaceLaunchInfo {
   int chunk = 0;            // batches per CTA chunk
   int dmma_per_batch = 0;
   int grid = 0;
-  int tnfrag = 0;           // reference-tensor interior-face kernel: fragments per signature
-  int tdmma_per_batch = 0;  //   and its DMMAs per 8-face batch (0: no tensor kernel)
-  int blocked_grid = 0;     // interior default kernel deals contiguous chunk runs: its grid size
 };
 
 // info != nullptr: only fill the launch description (no launch).
 cudaError_t launch_cell(int n_dpc, int n_q, bool mass, bool dg, const CellArgs& a, int n_sm,
-                        cudaStream_t st, CellLaunchInfo* info, bool* supported, int variant = 0,
-                        int engine = 0);
+                        cudaStream_t st, CellLaunchInfo* info, bool* supported, int engine);
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
-                        cudaStream_t st, FaceLaunchInfo* info, bool* supported, int variant = 0);
+                        cudaStream_t st, FaceLaunchInfo* info, bool* supported);
 cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st);
-cudaError_t launch_patch_geometry(const double* cgeo, const int4* pmeta, void* prec, int64_t n_cells,
-                                  int CH, int n_sm, cudaStream_t st);
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
                          cudaStream_t st, double* energy = nullptr);
 

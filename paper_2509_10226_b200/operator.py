@@ -35,9 +35,9 @@ __all__ = ["OperatorConfig", "SipgConfig", "HelmholtzCoefficients", "CgPoissonOp
            "baseline_sipg_tau", "apply_cg_poisson", "apply_dg_sipg", "apply_helmholtz"]
 
 _STAGES = ("ref", "data", "mm", "sched")
-_ENGINES = {"auto": 0, "dmma": 1, "dfma": 2, "tensor": 3, "modal": 4}
-_PATCHES = {"auto": 0, "off": 1, "on": 2}
-_FACE_ENGINES = {"auto": 0, "quadrature": 1, "tensor": 2, "modal": 3}
+_ENGINES = {"auto": 0, "dmma": 1, "tensor": 3, "modal": 4}
+_BLOCKS = {"auto": 0, "off": 1, "on": 2}
+_FACE_ENGINES = {"auto": 0, "quadrature": 1, "modal": 3}
 
 
 @dataclass(frozen=True)
@@ -54,16 +54,12 @@ class OperatorConfig:
     threads: int = 1
     backend: str = "auto"
     device: int = 0
-    kernel_variant: int = 0     # B200 cell-kernel tuning variant (0 = default)
-    face_variant: int = 0       # B200 face-kernel tuning variant (0 = default)
-    face_chunk: int = 0         # 8-face batches per CTA chunk, multiple of 8 up to 120 (0 = default 32)
-    concurrent_dg: bool = False  # DG: run the cell and face kernels concurrently (accumulating)
-    cell_engine: str = "auto"    # B200 cell kernel: auto | dmma (quadrature points) | dfma | tensor (affine
+    face_chunk: int = 0          # 8-face batches per CTA chunk, multiple of 8 up to 120 (0 = default 32)
+    cell_engine: str = "auto"    # B200 cell kernel: auto | dmma (quadrature points) | tensor (affine
     #                              reference tensor) | modal (points loop on the M = dim P_{p-1} exact modes)
-    cell_patches: str = "auto"   # B200 CG warp-patch assembly: auto (= off, measured slower) | off | on
-    face_engine: str = "auto"    # B200 faces: auto (modal at P2-P4) | quadrature (points) | tensor (interior) | modal
+    cell_blocks: str = "auto"    # B200 CG block assembly (low degrees on locality-ordered meshes): auto | off | on
+    face_engine: str = "auto"    # B200 faces: auto (modal at P2-P4) | quadrature (points) | modal
     f32_mirror: bool = False     # B200 CG Laplace: also build the fp32 apply (apply_f32; mixed-precision multigrid)
-    face_runs: str = "plain"     # B200 DG faces, blocked kernel: "plain" (contiguous CTA runs) | "window" (window-major; measured slower)
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -74,10 +70,8 @@ class OperatorConfig:
             raise ValueError(f"unknown precision {self.precision!r}")
         if self.cell_engine not in _ENGINES:
             raise ValueError(f"unknown cell engine {self.cell_engine!r}")
-        if self.cell_patches not in _PATCHES:
-            raise ValueError(f"unknown cell patch mode {self.cell_patches!r}")
-        if self.face_runs not in ("window", "plain"):
-            raise ValueError(f"unknown face run layout {self.face_runs!r}")
+        if self.cell_blocks not in _BLOCKS:
+            raise ValueError(f"unknown cell block mode {self.cell_blocks!r}")
         if self.face_engine not in _FACE_ENGINES:
             raise ValueError(f"unknown face engine {self.face_engine!r}")
         if self.backend not in ("auto", "compiled", "python", "b200"):
@@ -216,16 +210,12 @@ class _B200Operator:
         d.mass_scale = float(mass_scale)
         d.diffusivity = float(diffusivity)
         d.device = int(self.config.device)
-        d.flags = (int(getattr(self.config, "kernel_variant", 0)) & 0xF) | \
-            ((int(getattr(self.config, "face_variant", 0)) & 0xF) << 4) | \
-            ((int(getattr(self.config, "face_chunk", 0)) // 8 & 0xF) << 8) | \
-            ((1 if getattr(self.config, "concurrent_dg", False) else 0) << 12) | \
-            ((_ENGINES[getattr(self.config, "cell_engine", "auto")] & 3) << 13) | \
-            ((_ENGINES[getattr(self.config, "cell_engine", "auto")] >> 2) << 19) | \
-            (_PATCHES[getattr(self.config, "cell_patches", "auto")] << 15) | \
+        eng = _ENGINES[getattr(self.config, "cell_engine", "auto")]
+        d.flags = ((int(getattr(self.config, "face_chunk", 0)) // 8 & 0xF) << 8) | \
+            ((eng & 3) << 13) | ((eng >> 2) << 19) | \
+            (_BLOCKS[getattr(self.config, "cell_blocks", "auto")] << 15) | \
             (_FACE_ENGINES[getattr(self.config, "face_engine", "auto")] << 17) | \
-            ((1 if (getattr(self.config, "f32_mirror", False) or self.precision == "f32") else 0) << 20) | \
-            ((1 if getattr(self.config, "face_runs", "plain") == "window" else 0) << 21)
+            ((1 if (getattr(self.config, "f32_mirror", False) or self.precision == "f32") else 0) << 20)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))

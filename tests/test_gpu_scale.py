@@ -134,22 +134,3 @@ def test_oracle_parity_16cubed_dg_p2():
                              bas.face_values, bas.face_grads, geo.face_rule.weights, sipg.tau_interior,
                              sipg.tau_boundary, u)
     assert rel_l2(y, ref) <= 1e-12
-
-
-@pytest.mark.parametrize("p", [1, 2, 3])
-def test_patch_local_assembly_on_reordered_mesh(p):
-    """Warp-patch assembly (opt-in) on a reordered mesh: the patches have locality
-    (ratio < 0.6) and the result matches the oracle and the global-atomic kernel."""
-    from oracle import ref_apply
-    from paper_2509_10226_b200 import operator as op
-
-    m, dm, geo, bas = _setup(12, p, "cg", True, (0, 3))
-    u = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
-    A = op.CgPoissonOperator(m, dm, geo, bas, op.OperatorConfig(cell_patches="on"))
-    assert A.info["patch_cells"] > 0 and A.info["patch_ratio"] < 0.6
-    B = op.CgPoissonOperator(m, dm, geo, bas, op.OperatorConfig(cell_engine="dfma", cell_patches="off"))
-    assert B.info["patch_cells"] == 0
-    ref = ref_apply.cg_apply(m.vertices, m.cells, dm.cell_dofs, dm.dirichlet_mask, bas.grad_matrix,
-                             geo.cell_rule.weights, u)
-    assert rel_l2(A.apply(u), ref) <= 1e-12
-    assert rel_l2(B.apply(u), ref) <= 1e-12
