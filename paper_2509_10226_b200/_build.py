@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtetmf_b200.so")
 BUILD = os.path.join(HERE, "csrc", "_obj")
-SOURCES = ["kernels.cu", "cell_p1.cu", "cell_p2.cu", "cell_p3.cu", "cell_p4.cu", "face_launch.cu", "capi.cu", "multigrid.cu",
+SOURCES = ["kernels.cu", "cell_p1.cu", "cell_p2.cu", "cell_p3.cu", "cell_p4.cu", "face_launch.cu", "cell_block.cu", "capi.cu", "multigrid.cu",
            "reorder.cpp", "setup.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

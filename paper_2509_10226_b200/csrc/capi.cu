@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/tetmf_b200.h"
+#include "cell_block_kernel.cuh"
 #include "cell_f32_kernel.cuh"
 #include "cell_kernel.cuh"
 #include "face_kernel.cuh"
@@ -263,6 +264,19 @@ struct tmf_plan {
   int* dofs = nullptr;
   int* fix_list = nullptr;
   int64_t n_fix = 0;
+  // CG block assembly (cell_block_kernel.cuh; flags bits 15-16: 0 auto, 1 off, 2 on)
+  int blocks_mode = 0;
+  int blk_B = 0;                   // cells per block (0: off)
+  int64_t blk_n = 0;               // blocks
+  int blk_numax = 0, blk_nvmax = 0;
+  std::vector<double> blk_tab;     // modal table E'(k, m, j) at [(3 m + k) N + j] (kernel parameter)
+  int* blk_off = nullptr;
+  int* blk_nv = nullptr;
+  int* blk_uniq = nullptr;
+  uint16_t* blk_loc = nullptr;
+  uint16_t* blk_inc = nullptr;
+  uint16_t* blk_ioff = nullptr;
+  double* blk_kappa = nullptr;
   // multi-GPU peer-memory ghost access (tmf_plan_set_peers)
   tmf::PeerArgs peer{};
   const double** peer_u_tab = nullptr;   // device arrays of device pointers
@@ -311,6 +325,26 @@ struct tmf_plan {
     if (!dg && with_peer) a.peer = peer;   // CG ghost DoFs over peer memory (DG: the face kernel's ghost cells)
     return a;
   }
+  tmf::BlockArgs block_args(const double* u, double* y, double* energy) const {
+    tmf::BlockArgs a{};
+    a.u = u;
+    a.y = y;
+    a.verts = verts;
+    a.kappa = blk_kappa;
+    a.boff = blk_off;
+    a.bnv = blk_nv;
+    a.uniq = blk_uniq;
+    a.loc = blk_loc;
+    a.inc = blk_inc;
+    a.ioff = blk_ioff;
+    a.n_cells = n_cells;
+    a.n_blocks = blk_n;
+    a.numax = blk_numax;
+    a.nvmax = blk_nvmax;
+    a.scale = stiff_scale;
+    a.energy = energy;
+    return a;
+  }
   tmf::FaceArgs face_args(const double* u, double* y, bool boundary) const {
     tmf::FaceArgs a{};
     a.u = u;
@@ -347,7 +381,8 @@ struct tmf_plan {
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
-                    (void*)f32_rows, (void*)f32_geo,
+                    (void*)f32_rows, (void*)f32_geo, (void*)blk_off, (void*)blk_nv, (void*)blk_uniq,
+                    (void*)blk_loc, (void*)blk_inc, (void*)blk_ioff, (void*)blk_kappa,
                     (void*)peer_u_tab, (void*)peer_y_tab, (void*)ghost_rank, (void*)ghost_index})
       if (p) cudaFree(p);
   }
@@ -471,6 +506,123 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   return TMF_OK;
 }
 
+// CG block assembly tables (cell_block_kernel.cuh).  Cells are taken in Morton order of
+// their centroids (a locality order of the plan's own; the input numbering of cells and
+// DoFs is unchanged, the sum over cells does not depend on the order) and cut into blocks
+// of B.  Per block: its unique global DoFs sorted ascending (so the vertex DoFs, ids <
+// n_vertices in the reference numbering, come first), each slot's local index (u16), and
+// the slots of every unique DoF (u16 j*B + cl, in slot order) with their offsets.
+// Returns TMF_OK with P->blk_B = 0 when the plan does not qualify (vertex DoFs are not the
+// vertex ids, or a block does not fit in shared memory).
+int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total) {
+  const int N = P->N, NP = (N + 3) & ~3;
+  const int64_t n = P->n_cells;
+  for (int64_t c = 0; c < n; ++c)
+    for (int j = 0; j < 4; ++j)
+      if (d->cell_dofs[c * N + j] != d->cells[c * 4 + j]) return TMF_OK;   // not the reference numbering
+  // Morton order of the centroids (21 bits per axis in the bounding box)
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t v = 0; v < d->n_vertices; ++v)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], d->vertices[3 * v + k]);
+      hi[k] = std::max(hi[k], d->vertices[3 * v + k]);
+    }
+  auto spread = [](uint64_t x) {
+    x &= 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffULL;
+    x = (x | x << 16) & 0x1f0000ff0000ffULL;
+    x = (x | x << 8) & 0x100f00f00f00f00fULL;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+    x = (x | x << 2) & 0x1249249249249249ULL;
+    return x;
+  };
+  std::vector<std::pair<uint64_t, int64_t>> key(n);
+  for (int64_t c = 0; c < n; ++c) {
+    uint64_t code = 0;
+    for (int k = 0; k < 3; ++k) {
+      double x = 0.0;
+      for (int i = 0; i < 4; ++i) x += d->vertices[3 * (int64_t)d->cells[c * 4 + i] + k];
+      const double t = hi[k] > lo[k] ? (0.25 * x - lo[k]) / (hi[k] - lo[k]) : 0.0;
+      code |= spread((uint64_t)std::min(2097151.0, std::max(0.0, t * 2097152.0))) << k;
+    }
+    key[c] = {code, c};
+  }
+  std::sort(key.begin(), key.end());
+  const int64_t nb = (n + B - 1) / B;
+  std::vector<std::vector<int>> uq(nb);
+  std::vector<std::vector<uint16_t>> io(nb);
+  std::vector<int> nvb(nb);
+  std::vector<uint16_t> loc((size_t)n * NP, 0), inc((size_t)nb * B * N + 8, 0);
+  const int nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nth; ++t)
+    pool.emplace_back([&, t]() {
+      std::vector<std::pair<int, int>> pr;   // (global DoF, slot)
+      for (int64_t b = t; b < nb; b += nth) {
+        const int64_t c0 = b * B;
+        const int ncb = (int)std::min<int64_t>(B, n - c0);
+        pr.clear();
+        for (int cl = 0; cl < ncb; ++cl) {
+          const int64_t c = key[c0 + cl].second;
+          for (int j = 0; j < N; ++j) pr.emplace_back(d->cell_dofs[c * N + j], j * B + cl);
+        }
+        std::sort(pr.begin(), pr.end());
+        std::vector<int>& U = uq[b];
+        std::vector<uint16_t>& O = io[b];
+        uint16_t* I = inc.data() + (size_t)b * B * N;
+        int nv = 0;
+        for (size_t k = 0; k < pr.size(); ++k) {
+          if (k == 0 || pr[k].first != pr[k - 1].first) {
+            const int g = pr[k].first;
+            U.push_back(d->dirichlet_mask && d->dirichlet_mask[g] ? ~g : g);
+            O.push_back((uint16_t)k);
+            if (g < d->n_vertices) ++nv;
+          }
+          I[k] = (uint16_t)pr[k].second;
+          const int slot = pr[k].second, j = slot / B, cl = slot % B;
+          loc[(size_t)(c0 + cl) * NP + j] = (uint16_t)(U.size() - 1);
+        }
+        O.push_back((uint16_t)pr.size());
+        nvb[b] = nv;
+      }
+    });
+  for (auto& th : pool) th.join();
+  std::vector<int> off(nb + 1, 0), uniq;
+  std::vector<uint16_t> ioff;
+  int numax = 0, nvmax = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    off[b + 1] = off[b] + (int)uq[b].size();
+    numax = std::max(numax, (int)uq[b].size());
+    nvmax = std::max(nvmax, nvb[b]);
+  }
+  if (numax > 65535 || tmf::block_smem_bytes(N, B, numax, nvmax) > 227 * 1024) return TMF_OK;
+  uniq.reserve(off[nb]);
+  ioff.reserve(off[nb] + nb);
+  for (int64_t b = 0; b < nb; ++b) {
+    uniq.insert(uniq.end(), uq[b].begin(), uq[b].end());
+    ioff.insert(ioff.end(), io[b].begin(), io[b].end());
+  }
+  int rc;
+  if ((rc = upload(&P->blk_off, off.data(), off.size(), total))) return rc;
+  if ((rc = upload(&P->blk_nv, nvb.data(), nvb.size(), total))) return rc;
+  if ((rc = upload(&P->blk_uniq, uniq.data(), uniq.size(), total))) return rc;
+  if ((rc = upload(&P->blk_loc, loc.data(), loc.size(), total))) return rc;
+  if ((rc = upload(&P->blk_inc, inc.data(), inc.size(), total))) return rc;
+  if ((rc = upload(&P->blk_ioff, ioff.data(), ioff.size(), total))) return rc;
+  if (d->kappa) {
+    std::vector<double> kp(n);
+    for (int64_t i = 0; i < n; ++i) kp[i] = d->kappa[key[i].second];
+    if ((rc = upload(&P->blk_kappa, kp.data(), kp.size(), total))) return rc;
+  }
+  P->blk_B = B;
+  P->blk_n = nb;
+  P->blk_numax = numax;
+  P->blk_nvmax = nvmax;
+  P->info.block_cells = B;
+  P->info.block_ratio = (double)off[nb] / ((double)n * N);
+  return TMF_OK;
+}
+
 // y_zeroed: the caller already cleared y (CG); energy: += sum_e u_e^T A_e u_e + the identity
 // rows' u_i^2 (= u.Au when the tensor cell engine runs; PCG's fused p.Ap)
 int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaEvent_t* ev,
@@ -478,7 +630,9 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
   bool ok = true;
   if (ev) TMF_CUDA(cudaEventRecord(ev[0], st));
   if (!P->dg && !y_zeroed) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
-  {
+  if (P->blk_B && !P->peer.u) {
+    TMF_CUDA(tmf::launch_cell_block(P->N, P->block_args(u, y, energy), P->blk_tab.data(), st));
+  } else {
     tmf::CellArgs ca = P->cell_args(u, y);
     ca.energy = energy;
     TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, ca, P->n_sm, st, nullptr, &ok, P->kengine));
@@ -690,6 +844,24 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       enc[i] = (d->dirichlet_mask && d->dirichlet_mask[g]) ? ~g : g;
     }
     if ((rc = upload(&P->dofs, enc.data(), enc.size(), &total))) return bail(rc);
+    // block assembly for the scalar Laplace at P1-P3 (flags bits 15-16: 0 auto = on, 1 off, 2 on);
+    // the tile kernels stay built for the multi-GPU stages (peer ghosts, cell ranges)
+    P->blocks_mode = (d->flags >> 15) & 3;
+    const int Bc = tmf::block_cells_for(P->N);
+    const int req_engine = ((d->flags >> 13) & 3) | (((d->flags >> 19) & 1) << 2);
+    // auto: P1 only (48^3: 28 vs 31-33 us per apply for the tensor tile kernel; at P2 the modal
+    // tile kernel is as fast or faster, 54-63 vs 59-67 us; profiles/r02/block_assembly.jsonl)
+    const bool want = P->blocks_mode == 2 || (P->blocks_mode == 0 && req_engine == 0 && P->N == 4);
+    if (want && Bc > 0 && P->nc == 1 && !P->mass && (req_engine == 0 || req_engine == 4)) {
+      const int p = P->degree, M = p * (p + 1) * (p + 2) / 6;
+      if (build_modal_cell_tables(P->N, P->Q, M, d->grad_matrix, d->cell_weights, P->blk_tab)) {
+        if ((rc = build_blocks(P, d, Bc, &total))) return bail(rc);
+        if (P->blk_B) P->info.cell_engine = 5;
+      }
+    }
+    if (P->blocks_mode == 2 && !P->blk_B)
+      return bail(fail(TMF_EINVAL, "block assembly requested but the plan does not qualify (scalar CG "
+                                   "Laplace at P1-P3 with the reference DoF numbering, modal or auto engine)"));
     std::vector<int> fix;
     if (d->dirichlet_mask)
       for (int64_t g = 0; g < d->n_scalar_dofs; ++g)
@@ -878,9 +1050,9 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       fe -= nce * (12.0 * nq * nd + 33.0 * nq);
       fe += nce * (12.0 * nd * nd + 12.0 * nd);
       if (P->mass) fe += nce * (2.0 * nd * nd + 2.0 * nd) - nce * (4.0 * nq * nd + 5.0 * nq + nd);
-    } else if (P->info.cell_engine == 4) {
+    } else if (P->info.cell_engine == 4 || P->info.cell_engine == 5) {
       // the point loop on M unit-weight modes: 12 M N (both GEMMs) + 18 M (G action)
-      const double M = P->Qk;
+      const double M = P->degree * (P->degree + 1) * (P->degree + 2) / 6;
       fe -= nce * (12.0 * nq * nd + 33.0 * nq);
       fe += nce * (12.0 * M * nd + 18.0 * M);
     }
@@ -1235,7 +1407,7 @@ int tmf_pcg(tmf_plan* P, const double* b, double* x, int iters, double* res_norm
   const int grid = P->n_sm * 4, blk = 512;
   // fused iteration when the element energies are available (tensor cell engine, plain
   // single-GPU plan): apply(+p.Ap) -> residual -> step (x, p, q = 0)
-  const bool fused = (P->info.cell_engine == 3 || P->info.cell_engine == 4) && !P->peer.u && !P->dg;
+  const bool fused = P->info.cell_engine >= 3 && !P->peer.u && !P->dg;
   if (fused) {
     tmf::pcg_init_fused_kernel<<<grid, blk, 0, st>>>(b, dg, x, r, z, p, q, n, rz, rr);
     TMF_CUDA(cudaGetLastError());

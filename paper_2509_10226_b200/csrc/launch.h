@@ -9,6 +9,7 @@ struct CellArgs;
 struct FaceArgs;
 struct FaceGeoArgs;
 struct CellGeoArgs;
+struct BlockArgs;
 
 struct CellLaunchInfo {
   int dmma_per_tile = 0;
@@ -36,6 +37,10 @@ cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, i
                         cudaStream_t st, FaceLaunchInfo* info, bool* supported);
 cudaError_t launch_face_geometry(bool boundary, const FaceGeoArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st);
+// CG block assembly (cell_block_kernel.cuh): cells per block for n_dpc (0 = no kernel),
+// and the launch (host_tab: the M x 3 x n_dpc modal table, passed as a kernel parameter)
+int block_cells_for(int n_dpc);
+cudaError_t launch_cell_block(int n_dpc, const BlockArgs& a, const double* host_tab, cudaStream_t st);
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
                          cudaStream_t st, double* energy = nullptr);
 

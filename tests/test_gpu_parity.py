@@ -52,9 +52,11 @@ def test_gpu_cell_engines_match_golden(name, engine):
 
 
 def test_gpu_default_engines():
-    """auto: modal tables for Laplace cell terms at P2-P4, the reference tensor at P1 and
-    for Helmholtz; modal faces at P2-P4, the point loop at P1."""
-    for name, cell, face in [("cg_p1_n3_gm_dir2", 3, 0), ("cg_p2_n8_gm", 4, 0), ("cg_p4_n3_gm", 4, 0),
+    """auto: block assembly (5) for scalar CG Laplace at P1, modal tables for the other
+    Laplace cell terms at P2-P4, the reference tensor at P1 and for Helmholtz; modal faces
+    at P2-P4, the point loop at P1."""
+    for name, cell, face in [("cg_p1_n3_gm_dir2", 5, 0), ("cg_p2_n8_gm", 4, 0), ("cg_p3_n4_ref_dir", 4, 0),
+                             ("cg_p4_n3_gm", 4, 0), ("cg3_p2_n3_ref_dir", 4, 0),
                              ("dg_p1_n3_gm_dir", 3, 1), ("dg_p3_n3_gm_dir", 4, 3), ("helmk_p2_n3_gm_dir", 3, 3)]:
         A = operator_from_fixture(load_golden(name))
         assert A.info["cell_engine"] == cell, name
@@ -76,3 +78,18 @@ def test_gpu_face_engines_match_golden(name, engine):
         assert A.info["face_engine"] == FACE_CODE[engine]
     err = rel_l2(A.apply(g["u"]), g["y"])
     assert err <= TOL, f"{name}/{engine}: rel L2 {err:.3e}"
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("cg") if ("_p1_" in n or "_p2_" in n)
+                                  and not n.startswith("cg3")])
+def test_gpu_block_assembly_matches_golden(name):
+    """CG block assembly (cell_block_kernel.cuh) on and off against every scalar CG golden
+    P1-P2 (Dirichlet and pure Neumann, reference and GM rules)."""
+    g = load_golden(name)
+    on = operator_from_fixture(g, cell_blocks="on")
+    off = operator_from_fixture(g, cell_blocks="off")
+    assert on.info["cell_engine"] == 5 and on.info["block_cells"] > 0
+    assert off.info["cell_engine"] != 5 and off.info["block_cells"] == 0
+    for A in (on, off):
+        err = rel_l2(A.apply(g["u"]), g["y"])
+        assert err <= TOL, f"{name}: rel L2 {err:.3e}"
