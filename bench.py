@@ -1,27 +1,33 @@
 """Benchmark of the B200 matrix-free operator apply (driver contract: one JSON line).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Workload (BASELINE.json configs[1], "C2"): CG Laplace operator apply, degree
-sweep P1..P4, fp64, on the 48^3 x 6 = 663,552-cell jittered, randomly permuted
-Kuhn mesh (seed 0), Grundmann-Moller quadrature exact to 2p, u ~ U[-1,1]
-(seed 1).  One *step* = one apply at each degree, on the unordered mesh and on
-the hierarchically reordered mesh (8 applies); ``value`` = DoFs processed /
-device time (GDoF/s).  Inputs and plans are resident in HBM before timing;
-L2 is flushed (256 MiB write) before every apply, outside the timed events.
+Workload (BASELINE.json configs[1], "C2"): CG Laplace operator apply, degree sweep
+P1..P4, fp64, on the 48^3 x 6 = 663,552-cell jittered, randomly permuted Kuhn mesh
+(seed 0), Grundmann-Moller quadrature exact to 2p, u ~ U[-1,1] (seed 1).  One *step*
+= one apply at each degree on the unordered mesh and on the hierarchically reordered
+mesh (8 applies, 22,536,008 DoFs); ``value`` = DoFs per step / device time (GDoF/s).
 
-``e2e`` times the same step through the public API with host buffers
-(``Operator.apply(numpy)`` -> ``tmf_apply_host``: pinned H2D of u, apply, D2H
-of y), wall clock.  ``--impl reference`` times the CPU oracle port of the
-reference's batched NumPy loop (oracle/ref_apply.py; the reference package
-itself cannot travel to the GPU box) with one worker process per host core
-on a bounded sample of batches of the same workload, extrapolated per DoF.
+B200 arm (default).  Inputs and plans are resident in HBM before timing; L2 is
+flushed (256 MiB write) before every apply, outside the timed events; every apply
+is timed with CUDA events on its launch stream (tmf_apply_timed), clocks sampled by
+NVML during the timed region.  ``e2e`` = the same step through the public API with
+pinned host buffers (H2D + apply + D2H per plan, one stream per plan).  ``roofline``
+= the dominant kernel against the measured FP64 DMMA peak, with SURVEY §8(d)'s
+algorithmic flops and bytes and the engine's own flops.
+``c4_strong`` (every N) = BASELINE config 4, the DG kappa-Helmholtz P2 apply on the
+128^3 x 6 mesh partitioned over the N ranks (strong scaling, fixed mesh).
 
-Multi-GPU (torchrun, N>1): ``scaling: "weak"``.  The global mesh grows to
-round(48 N^(1/3))^3 x 6 cells, is split by recursive coordinate bisection into
-N subdomains (paper_2509_10226_b200.distributed), and every apply runs the
-forward NCCL halo, the local B200 kernel and the reverse (additive) halo;
-``value`` = global DoFs per step / max-over-ranks step time.
+Reference arm (``--impl reference``): the reference's CPU path, i.e. the oracle port
+of its batched NumPy cell loop (kernel_stage "mm": 16-cell lane-major batches,
+operator.py:255-278, oracle/ref_apply.py), on every host core (one worker process
+per core on disjoint batch ranges), each step a bounded sample of the same 8 applies;
+its whole workload is built by the oracle (oracle/ref_mesh.py, ref_reorder.py) and
+the reference's own tables (tests/golden fixtures) -- no product code, no GPU.
+
+Multi-GPU (torchrun, N > 1): ``value`` is C2 weak scaling -- the global mesh grows
+to round(48 N^(1/3))^3 x 6 and is split by recursive coordinate bisection; every
+apply gathers / scatters ghost DoFs over NVLink (peer memory) or the NCCL halo.
 """
 
 from __future__ import annotations
@@ -41,13 +47,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.1   # measured: DMMA m8n8k4 on this pool's B200 (profiles/r01_fp64_peak.json)
-FP64_PEAK_SOURCE = "profiles/r01_fp64_peak.json (mma.sync m8n8k4 f64 microbench on B200, 1965 MHz)"
+FP64_PEAK_SOURCE = ("measured DMMA m8n8k4 f64 microbenchmark, B200 at 1965 MHz (profiles/r01_fp64_peak.json; "
+                    "MEASURED_PEAKS.json has no FP64 entry)")
+HBM_GBS = 6547.2          # MEASURED_PEAKS.json hbm_gbs
 DEGREES = (1, 2, 3, 4)
-ENGINE_NAMES = {1: "dmma-quadrature", 3: "dmma-reference-tensor",
-                4: "dmma-modal (point kernel on M = dim P_(p-1) exact modes)"}
-KERNEL_NAMES = {1: "cell_apply_kernel (n_q points)", 3: "cell_tensor_kernel",
-                4: "cell_apply_kernel (modal tables)"}
 N_MESH = 48
+ENGINE_NAMES = {1: "dmma n_q-point loop", 3: "dmma reference tensor", 4: "dmma modal (point loop on M exact modes)",
+                5: "block assembly (modal, DFMA, Morton cell blocks)"}
+KERNEL_NAMES = {1: "cell_apply_kernel (n_q points)", 3: "cell_tensor_kernel", 4: "cell_apply_kernel (modal tables)",
+                5: "cell_block_kernel"}
+METRIC = "operator-apply GDoF/s (fp64), CG Laplace P1-P4 sweep"
+UNIT = "GDoF/s"
 
 
 def parse():
@@ -56,63 +66,29 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2"])
     ap.add_argument("--n", type=int, default=N_MESH)
-    ap.add_argument("--no-reorder", action="store_true")
-    ap.add_argument("--cpu-sample-s", type=float, default=2.5)
+    ap.add_argument("--cpu-step-s", type=float, default=1.5, help="reference arm: wall seconds per sampled step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (e.g. under ncu)")
-    ap.add_argument("--dist", action="store_true", help="use the partitioned (NCCL) path even at world size 1")
-    ap.add_argument("--no-quadrature", action="store_true", help="skip the quadrature-point engine comparison")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-quadrature", action="store_true", help="skip the n_q-point engine comparison")
+    ap.add_argument("--c4-n", type=int, default=128, help="c4_strong mesh (0 = skip)")
+    ap.add_argument("--dist", action="store_true", help="partitioned code path even at world size 1")
     return ap.parse_args()
 
 
-# ----------------------------------------------------------------- workload
-_MESHES = {}
+def global_n(args, world):
+    return args.n if world == 1 else int(round(args.n * world ** (1.0 / 3.0)))
 
 
-def build_problem(n, p, reorder):
-    """Mesh (cached per (n, reorder): the reordering and the partition are shared by
-    all degrees), DoF map, tables."""
-    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, quadrature as Q
-    from paper_2509_10226_b200.geometry import GeometryData
-
-    key = (n, reorder)
-    if key not in _MESHES:
-        m = M.kuhn_cube_mesh(n, seed=0)
-        if reorder:
-            from paper_2509_10226_b200.reorder import reorder_mesh
-
-            m = reorder_mesh(m)   # hierarchical cell order + first-touch vertex numbering
-        _MESHES[key] = m
-    m = _MESHES[key]
-    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
-    bas = B.tabulate_basis(p, cr, fr)
-    dm = D.build_dof_map(m, p, "cg")
-    geo = GeometryData("affine", cr, fr, None, None, None, None)
-    return m, dm, geo, bas
-
-
-_PARTS = {}
-
-
-def partition_of(m, world):
-    from paper_2509_10226_b200.distributed import partition_cells
-
-    key = (id(m), world)
-    if key not in _PARTS:
-        _PARTS[key] = partition_cells(m, world)
-    return _PARTS[key]
-
-
-def variants(args):
-    vs = [False]
-    if not args.no_reorder:
-        try:
-            import paper_2509_10226_b200.reorder  # noqa: F401
-            vs.append(True)
-        except ImportError:
-            pass
-    return vs
+def shared_config(args, world):
+    """The config dict both arms print (same keys and values at a given world size)."""
+    n = global_n(args, world)
+    return {"workload": f"C2: CG Laplace apply, P1-P4 sweep, {n}^3x6 jittered permuted Kuhn tets, GM quadrature "
+                        f"exact to 2p, fp64, unordered + hierarchically reordered (8 applies per step)",
+            "global_mesh": f"{n}^3 x 6", "degrees": list(DEGREES), "orderings": ["unordered", "reordered"],
+            "seeds": {"mesh": 0, "u": 1},
+            "parallelism": "single GPU" if world == 1 else
+            f"{world}-way RCB domain decomposition, weak scaling (~{args.n}^3 x 6 cells per GPU)"}
 
 
 # ----------------------------------------------------------------- clocks
@@ -163,73 +139,131 @@ class ClockSampler:
                 "reasons": [v for k, v in self.NAMES.items() if self.reasons & k], "samples": len(self.samples)}
 
 
-# ----------------------------------------------------------------- reference arm / cpu baseline
-def _cpu_worker(args):
-    p, n, b0, b1, reorder = args
+# ----------------------------------------------------------------- reference arm (oracle only)
+_REF = {}
+
+
+def reference_workload(n):
+    """The C2 problems built by the oracle alone (mesh, reordering, DoF maps) with the
+    reference's own GM tables (tests/golden fixtures made by the real reference)."""
+    from oracle import ref_apply, ref_mesh, ref_reorder
+
+    v, c, fi, fb = ref_mesh.kuhn_mesh(n, seed=0)
+    c2, fi2, fb2 = ref_mesh.permute_cells(c, fb, ref_reorder.hierarchical_reorder(len(c), fi))
+    v3, c3, _, _ = ref_mesh.first_touch_vertices(v, c2, fb2)
+    probs = []
+    for reorder, (verts, cells) in ((False, (v, c)), (True, (v3, c3))):
+        for p in DEGREES:
+            g = np.load(os.path.join(ROOT, "tests", "golden", f"cg_p{p}_n3_gm{'_dir2' if p < 4 else ''}.npz"))
+            Eg, w = g["grad_matrix"], g["cell_weights"]
+            cd, ns = ref_mesh.cg_dofs(cells, len(verts), p)
+            jit, jxw, _ = ref_apply.affine_cell_geometry(verts, cells, w)
+            probs.append(dict(p=p, reorder=reorder, cd=cd.astype(np.int64), ndof=ns, Eg=Eg, jit=jit, jxw=jxw,
+                              u=np.random.default_rng(1).uniform(-1, 1, ns)))
+    return probs
+
+
+def _ref_batches(pr, b0, b1):
+    """operator.py:255-278 with kernel_stage "mm" (W = 4 lanes x 4 cells, 16-column
+    batches, lane-major slots) over batches [b0, b1): gather, E U, D, E^T V, scatter."""
     from oracle import ref_apply
 
-    m, dm, geo, bas, jit, jxw = _CPU_CACHE[(p, reorder)]
-    gidx = dm.cell_dofs.astype(np.int64)
-    u = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
-    y = np.zeros_like(u)
-    ids, act = ref_apply._cell_batches(m.n_cells, 4, 4)
-    t0 = time.perf_counter()
+    ids, act = pr["ids"], pr["act"]
+    y = pr["y"]
     for b in range(b0, b1):
         sub = ids[b]
-        idx = gidx[sub].T.copy()
+        idx = pr["cd"][sub].T.copy()
         idx[:, ~act[b]] = -1
-        U = ref_apply.gather(u, idx)
-        G = (bas.grad_matrix @ U).reshape(-1, 3, U.shape[1])
-        Dd = ref_apply.d_action_affine(G, jit[sub], jxw[sub])
-        R = bas.grad_matrix.T @ Dd.reshape(-1, U.shape[1])
-        ref_apply.scatter_add(y, idx, R)
-    return time.perf_counter() - t0, b1 - b0
+        U = ref_apply.gather(pr["u"], idx)
+        G = (pr["Eg"] @ U).reshape(-1, 3, U.shape[1])
+        D = ref_apply.d_action_affine(G, pr["jit"][sub], pr["jxw"][sub])
+        ref_apply.scatter_add(y, idx, pr["Eg"].T @ D.reshape(-1, U.shape[1]))
+    return b1 - b0
 
 
-_CPU_CACHE = {}
+def _ref_worker(ranges):
+    """One worker's share of one step: per problem a disjoint range of batches."""
+    return [_ref_batches(_REF["probs"][i], b0, b1) for i, (b0, b1) in enumerate(ranges)]
 
 
-def cpu_reference(args, sample_s, workers=None):
-    """Time the oracle port of the reference's batched NumPy loop (kernel_stage "mm":
-    W=4 lanes x 4 cells per batch, operator.py:77-87) on all host cores; returns the
-    aggregate GDoF/s over the P1..P4 sweep, extrapolated from a bounded sample."""
+def reference_arm(args, steps, warmup, step_s, workers=None):
+    """Times the reference CPU path on all host cores.  Returns a dict with value (GDoF/s of
+    DoF-equivalents: each problem counts N_dof x sampled batches / all batches), ms_per_step,
+    cores and the sample description."""
     import multiprocessing as mp
 
-    workers = workers or os.cpu_count() or 1
-    tot_dofs, tot_time, detail = 0.0, 0.0, {}
-    for reorder in variants(args):
-        for p in DEGREES:
-            from oracle import ref_apply
+    from oracle import ref_apply
 
-            m, dm, geo, bas = build_problem(args.n, p, reorder)
-            jit, jxw, _ = ref_apply.affine_cell_geometry(m.vertices, m.cells, geo.cell_rule.weights)
-            _CPU_CACHE[(p, reorder)] = (m, dm, geo, bas, jit, jxw)
-            n_batches = (m.n_cells + 15) // 16
-            # calibrate batches/second on one worker, then give each worker ~sample_s
-            dt, nb = _cpu_worker((p, args.n, 0, 20, reorder))
-            per = max(1, int(sample_s * nb / dt))
-            chunks = [(p, args.n, (w * per) % n_batches, min(n_batches, (w * per) % n_batches + per), reorder)
-                      for w in range(workers)]
-            ctx = mp.get_context("fork")
-            with ctx.Pool(workers) as pool:
-                res = pool.map(_cpu_worker, chunks)
-            wall = max(r[0] for r in res)                # concurrent loops: slowest worker
-            done = sum(r[1] for r in res)
-            t_full = wall * n_batches / done            # extrapolated apply time, all cores
-            tot_dofs += dm.n_global_dofs
-            tot_time += t_full
-            detail[f"p{p}{'_reordered' if reorder else ''}"] = {
-                "gdofs": dm.n_global_dofs / t_full / 1e9, "batches_sampled": done, "n_batches": n_batches}
-    return tot_dofs / tot_time / 1e9, workers, detail
+    t0 = time.time()
+    if "probs" not in _REF:
+        probs = reference_workload(args.n)
+        for pr in probs:
+            pr["ids"], pr["act"] = ref_apply._cell_batches(len(pr["cd"]), 4, 4)
+            pr["nb"] = len(pr["ids"])
+            pr["y"] = np.zeros(pr["ndof"])
+        _REF["probs"] = probs
+    probs = _REF["probs"]
+    setup_s = time.time() - t0
+    workers = workers or os.cpu_count() or 1
+    # calibrate batches per second of one worker per problem, then size every worker's range so
+    # a step takes ~step_s of wall time (each worker runs all 8 problems' ranges back to back)
+    rate = []
+    for pr in probs:
+        _ref_batches(pr, 0, 4)
+        t = time.perf_counter()
+        _ref_batches(pr, 4, 24)
+        rate.append(20 / (time.perf_counter() - t))
+    share = step_s / len(probs)
+    per = [max(1, int(r * share)) for r in rate]
+    ctx = mp.get_context("fork")
+    t_steps, dofs = [], 0.0
+    with ctx.Pool(workers) as pool:
+        for k in range(warmup + steps):
+            tasks = []
+            for w in range(workers):
+                rg = []
+                for pr, q in zip(probs, per):
+                    span = max(1, pr["nb"] - q)
+                    b0 = ((k * workers + w) * q) % span
+                    rg.append((b0, min(pr["nb"], b0 + q)))
+                tasks.append(rg)
+            t = time.perf_counter()
+            res = pool.map(_ref_worker, tasks)
+            dt = time.perf_counter() - t
+            if k >= warmup:
+                t_steps.append(dt)
+                dofs += sum(pr["ndof"] * sum(r[i] for r in res) / pr["nb"] for i, pr in enumerate(probs))
+    total = float(np.sum(t_steps))
+    return {"value": dofs / total / 1e9, "ms_per_step": total / len(t_steps) * 1e3, "cores": workers,
+            "setup_s": round(setup_s, 1), "batches_per_worker_per_problem": per,
+            "sample": (f"per step: {workers} worker processes, each a disjoint range of 16-cell batches of every "
+                       f"one of the 8 C2 applies (~{step_s:.1f} s wall); DoF-equivalents = N_dof x sampled "
+                       f"batches / all batches; oracle-built workload, reference GM tables")}
 
 
 # ----------------------------------------------------------------- GPU arm
+def build_problem(n, p, reorder, cache={}):
+    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+
+    key = (n, reorder)
+    if key not in cache:
+        m = M.kuhn_cube_mesh(n, seed=0)
+        if reorder:
+            from paper_2509_10226_b200.reorder import reorder_mesh
+
+            m = reorder_mesh(m)   # hierarchical cell order + first-touch vertex numbering
+        cache[key] = m
+    m = cache[key]
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    dm = D.build_dof_map(m, p, "cg")
+    return m, dm, GeometryData("affine", cr, fr, None, None, None, None), bas
+
+
 def measure_link(problems, reps):
-    """Pinned host <-> device copy rates of this box, measured live on the largest plan's
-    vectors (H2D alone, D2H alone, both at once on two streams), and the lower bound they put
-    on one e2e step: every plan's u goes up and its y comes down, a plan's D2H cannot start
-    before its own H2D has finished, so a step takes at least max((H + D) / duplex,
-    (H + s_max) / min(h2d, d2h)) whatever the order (two-stage flow shop, equal job sizes)."""
+    """Pinned host <-> device copy rates of this box on the largest plan's vectors, and the
+    lower bound they put on one e2e step."""
     import torch
 
     big = max(problems, key=lambda pr: pr["ndof"])
@@ -240,7 +274,7 @@ def measure_link(problems, reps):
     reps = max(3, reps)
 
     def rate(up, dn):
-        dev_u.copy_(big["u_pin"], non_blocking=True)   # warm
+        dev_u.copy_(big["u_pin"], non_blocking=True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(reps):
@@ -256,9 +290,23 @@ def measure_link(problems, reps):
     h2d, d2h, duplex = rate(True, False), rate(False, True), rate(True, True)
     tot = sum(8 * pr["ndof"] for pr in problems)
     bound_s = max(2 * tot / (duplex * 1e9), (tot + nbytes) / (min(h2d, d2h) * 1e9))
-    del dev_u
     return {"h2d_GBs": round(h2d, 1), "d2h_GBs": round(d2h, 1), "duplex_GBs": round(duplex, 1),
             "step_bound_ms": round(bound_s * 1e3, 3)}
+
+
+def committed_traffic(key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the cell kernel of problem
+    ``key`` from the ncu --set full capture committed under profiles/ (tools/capture_roofline.sh)."""
+    path = os.path.join(ROOT, "profiles", "r02", "ncu_dominant.json")
+    try:
+        rec = json.load(open(path))
+    except (OSError, ValueError):
+        return None, None
+    for r in rec.get("kernels", []):
+        if r.get("key") == key:
+            return r.get("dram_bytes_per_launch"), {"file": "profiles/r02/ncu_dominant.json",
+                                                    "ncu_kernel": r.get("kernel"), "commit": rec.get("commit")}
+    return None, None
 
 
 def gpu_bench(args, rank, world):
@@ -270,28 +318,23 @@ def gpu_bench(args, rank, world):
     torch.cuda.set_device(dev)
     cfg = op.OperatorConfig(device=dev)
     st = torch.cuda.current_stream().cuda_stream
-    # weak scaling: each rank keeps ~n^3 x 6 cells (global mesh grows with the world size)
-    n_glob = args.n if world == 1 else int(round(args.n * world ** (1.0 / 3.0)))
-    # multi-GPU transport: "p2p" = ghost DoFs read / RED-scattered by the cell kernel in
-    # the owner's buffers over NVLink (CUDA IPC), "nccl" = NCCL halo exchange
+    n_glob = global_n(args, world)
+    dist_path = world > 1 or args.dist
     transport = os.environ.get("TMF_TRANSPORT", "p2p")
     problems = []
-    for reorder in variants(args):
+    for reorder in (False, True):
         for p in DEGREES:
             m, dm, geo, bas = build_problem(n_glob, p, reorder)
             u_glob = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
-            if world == 1 and not args.dist:
-                A = op.CgPoissonOperator(m, dm, geo, bas, cfg)
+            if not dist_path:
+                A = local = op.CgPoissonOperator(m, dm, geo, bas, cfg)
                 ids = None
-                local = A
             else:
-                from paper_2509_10226_b200.distributed import DistributedCgOperator
+                from paper_2509_10226_b200.distributed import DistributedCgOperator, partition_cells
 
-                A = DistributedCgOperator(m, dm, geo, bas, rank, world, part=partition_of(m, world),
+                A = DistributedCgOperator(m, dm, geo, bas, rank, world, part=partition_cells(m, world),
                                           transport=transport)
                 if transport == "p2p":
-                    # CUDA-IPC mapping of the peers' buffers; if any rank cannot map them,
-                    # every rank falls back to the NCCL halo transport
                     ok = 1.0
                     try:
                         A.connect_ipc()
@@ -304,35 +347,29 @@ def gpu_bench(args, rank, world):
                     if float(flag[0]) < 1.0:
                         transport = "nccl"
                         for q in problems:
-                            if q["ids"] is not None:
-                                q["A"].set_transport("nccl")
+                            q["A"].set_transport("nccl")
                         A.set_transport("nccl")
-                ids = A.owned_global_ids
-                local = A.local_op
+                ids, local = A.owned_global_ids, A.local_op
             u_host = u_glob if ids is None else u_glob[ids]
             u = torch.from_numpy(np.ascontiguousarray(u_host)).cuda()
-            if ids is not None and transport == "p2p" and A.transport == "p2p":
-                # the registered (peer-visible) local buffers, used in place
+            if ids is not None and transport == "p2p":
                 A.bufs.u[: len(u_host)].copy_(u)
                 u, y = A.bufs.u, A.bufs.y
             elif ids is not None:
-                # rank-local layout (owned DoFs, then ghost slots): the partitioned apply
-                # works on these vectors in place (no owned <-> local copies)
                 ul = torch.zeros(A.n_local, dtype=torch.float64, device="cuda")
                 ul[: len(u_host)] = u
-                u = ul
-                y = torch.empty_like(u)
+                u, y = ul, torch.empty_like(ul)
             else:
                 y = torch.empty_like(u)
             u_pin = torch.from_numpy(np.ascontiguousarray(u_host)).pin_memory()
             y_pin = torch.empty_like(u_pin).pin_memory()
             problems.append(dict(p=p, reorder=reorder, A=A, local=local, u=u, y=y, u_pin=u_pin, y_pin=y_pin,
-                                 ndof=len(u_host), ndof_global=dm.n_global_dofs, ids=ids))
+                                 ndof=len(u_host), ndof_global=dm.n_global_dofs, ids=ids,
+                                 key=f"p{p}{'_reordered' if reorder else ''}"))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    # self-check of the peer-memory transport against the NCCL halo path (same plans)
     p2p_check = None
-    if (world > 1 or args.dist) and transport == "p2p":
+    if dist_path and transport == "p2p":
         err = 0.0
         for pr in problems:
             A, n = pr["A"], pr["ndof"]
@@ -352,7 +389,7 @@ def gpu_bench(args, rank, world):
 
     def timed_apply(pr):
         """(total, cell-kernel) ms of one apply, CUDA events on the launch stream."""
-        if world == 1 and not args.dist:
+        if not dist_path:
             ms = pr["A"].timed(pr["u"].data_ptr(), pr["y"].data_ptr(), st, 1)
             return float(ms[0]), float(ms[1])
         A = pr["A"]
@@ -386,95 +423,73 @@ def gpu_bench(args, rank, world):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     total_ms = sum(ms[0] for _, ms in rec)
-    dofs = sum(pr["ndof"] for pr, _ in rec)   # owned DoFs of this rank
 
     # e2e through the public API with host (pinned) buffers
-    n_streams = int(os.environ.get("TMF_E2E_STREAMS", "8"))
-    # largest plans first: the D2H of the big vectors starts as early as possible
-    e2e_order = sorted(problems, key=lambda pr: -pr["ndof"]) if os.environ.get("TMF_E2E_ORDER", "desc") == "desc" \
-        else list(problems)
-    streams = [torch.cuda.Stream() for _ in range(n_streams)]
-    e2e_path = os.environ.get("TMF_E2E_PATH", "streams")
-    e2e_multi = e2e_path in ("multi", "blocks")
-    e2e_sched = None
-    if e2e_path == "blocks":
-        # reordered plans streamed in cell blocks (their cells touch narrow DoF windows), each
-        # ahead of its unordered twin; schedules built here, outside the timed region
-        nblk = int(os.environ.get("TMF_E2E_BLOCKS", "16"))
-        e2e_order = sorted(problems, key=lambda pr: (-pr["ndof"], not pr["reorder"]))
-        e2e_sched = [pr["A"].host_schedule(nblk) if pr["reorder"] else None for pr in e2e_order]
+    e2e_s, link, parity = None, None, None
+    if not args.no_e2e:
+        order = sorted(problems, key=lambda pr: -pr["ndof"])
+        streams = [torch.cuda.Stream() for _ in problems]
 
-    def e2e_step():
-        if world == 1 and not args.dist:
-            # public C-ABI with host buffers; the plans' H2D / kernels / D2H are
-            # pipelined on one stream per plan, so the H2D and D2H copy engines and the
-            # SMs work on different plans at the same time
-            if e2e_multi:
-                op.apply_host_multi([pr["A"] for pr in e2e_order], [pr["u_pin"] for pr in e2e_order],
-                                    [pr["y_pin"] for pr in e2e_order], streams[0].cuda_stream,
-                                    schedules=e2e_sched)
+        def e2e_step():
+            if not dist_path:
+                for i, pr in enumerate(order):
+                    pr["A"].apply_host_async(pr["u_pin"], pr["y_pin"], streams[i].cuda_stream)
             else:
-                for i, pr in enumerate(e2e_order):
-                    pr["A"].apply_host_async(pr["u_pin"], pr["y_pin"], streams[i % len(streams)].cuda_stream)
+                for pr in problems:
+                    pr["y_pin"].copy_(pr["A"].apply(pr["u_pin"].cuda(non_blocking=True)), non_blocking=True)
             torch.cuda.synchronize()
-            return
-        for pr in problems:   # host -> device, partitioned apply (NCCL halo), device -> host
-            u = pr["u_pin"].cuda(non_blocking=True)
-            pr["y_pin"].copy_(pr["A"].apply(u), non_blocking=True)
-        torch.cuda.synchronize()
-    e2e_step()
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
+
         e2e_step()
-    e2e_s = time.perf_counter() - t0
-
-    # parity spot check of the timed path against the e2e path (P2, unordered)
-    pr0 = problems[1]
-    y0 = pr0["y"][: pr0["ndof"]].cpu()
-    err = float(torch.linalg.vector_norm(y0 - pr0["y_pin"]) / torch.linalg.vector_norm(pr0["y_pin"]))
-
-    link = measure_link(problems, args.steps) if (world == 1 and not args.dist) else None
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        e2e_s = time.perf_counter() - t0
+        pr0 = problems[1]
+        y0 = pr0["y"][: pr0["ndof"]].cpu()
+        parity = float(torch.linalg.vector_norm(y0 - pr0["y_pin"]) / torch.linalg.vector_norm(pr0["y_pin"]))
+        link = measure_link(problems, args.steps) if not dist_path else None
 
     per = {}
     for pr in problems:
-        key = f"p{pr['p']}{'_reordered' if pr['reorder'] else ''}"
         ms = np.array([m for q, m in rec if q is pr])
-        t = ms[:, 0].mean()
-        tc = ms[:, 1].mean()
+        t, tc = float(ms[:, 0].mean()), float(ms[:, 1].mean())
         info = pr["local"].info
-        per[key] = {"ndof": pr["ndof"], "ms": round(float(t), 4), "gdofs": round(pr["ndof"] / t / 1e6, 3),
-                    "cell_kernel_ms": round(float(tc), 4), "cell_engine": ENGINE_NAMES.get(info["cell_engine"]),
-                    # useful flops of the algorithm the kernel runs (reference tensor: 12 N^2 + 12 N + N per cell)
-                    "tflops_engine": round(info["flops_engine"] / tc / 1e9, 2),
-                    "frac_fp64": round(info["flops_engine"] / tc / 1e9 / FP64_PEAK_TFLOPS, 3),
-                    # the reference counter formula (quadrature-point loop, operator.py:227-242) / the same time:
-                    # the rate the reference's own algorithm would need to match this time (> peak possible)
-                    "tflops_ref_formula": round(info["flops_alg"] / tc / 1e9, 2)}
-    # dominant kernel = the cell kernel of the slowest apply
-    dom = max(problems, key=lambda q: per[f"p{q['p']}{'_reordered' if q['reorder'] else ''}"]["cell_kernel_ms"])
-    dk = f"p{dom['p']}{'_reordered' if dom['reorder'] else ''}"
-    tc = per[dk]["cell_kernel_ms"]
-    achieved = dom["local"].info["flops_engine"] / tc / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("cell_kernel_p4", {}).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    n_kern = sum(pr["local"].info["kernels_per_apply"] for pr in problems) * args.steps
-
-    # the paper's own algorithm (quadrature-point DMMA engine) on the reordered meshes, timed the
-    # same way after the main timed region (reported beside it, not part of ``value``)
+        per[pr["key"]] = {
+            "ndof": pr["ndof"], "ms": round(t, 4), "gdofs": round(pr["ndof"] / t / 1e6, 3),
+            "cell_kernel_ms": round(tc, 4), "cell_engine": ENGINE_NAMES.get(info["cell_engine"]),
+            "tflops_engine": round(info["flops_engine"] / tc / 1e9, 2),
+            "frac_engine": round(info["flops_engine"] / tc / 1e9 / FP64_PEAK_TFLOPS, 3),
+            "tflops_alg": round(info["flops_alg"] / tc / 1e9, 2),
+            "frac_alg": round(info["flops_alg"] / tc / 1e9 / FP64_PEAK_TFLOPS, 3),
+            "hbm_frac_alg": round(info["bytes_alg"] / (tc * 1e-3) / (HBM_GBS * 1e9), 3)}
+    dom = max(problems, key=lambda q: per[q["key"]]["cell_kernel_ms"])
+    info = dom["local"].info
+    tc = per[dom["key"]]["cell_kernel_ms"]
+    traffic, traffic_src = committed_traffic(dom["key"])
+    fe, fa = info["flops_engine"] / tc / 1e9, info["flops_alg"] / tc / 1e9
+    roofline = {
+        "bound": "tensor", "kernel": f"{KERNEL_NAMES.get(info['cell_engine'])} ({dom['key']})", "unit": "TFLOP/s",
+        "achieved": round(fe, 3), "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
+        "frac": round(fe / FP64_PEAK_TFLOPS, 4), "frac_engine": round(fe / FP64_PEAK_TFLOPS, 4),
+        "frac_alg": round(fa / FP64_PEAK_TFLOPS, 4),
+        "flops_engine": info["flops_engine"], "flops_alg": info["flops_alg"], "bytes_alg": info["bytes_alg"],
+        "hbm_frac_alg": round(info["bytes_alg"] / (tc * 1e-3) / (HBM_GBS * 1e9), 4),
+        "kernel_ms": tc, "traffic": traffic, "traffic_source": traffic_src,
+        "note": ("frac = frac_engine: the kernel's useful flops (the exact rank-M modal refactorisation of the "
+                 "reference's point sums, DESIGN §4) / CUDA-event kernel time / FP64 peak.  frac_alg uses SURVEY "
+                 "§8(d)'s F_alg (the reference's n_q-point counter formula), which the modal form does not "
+                 "execute: it exceeds 1 because the same apply needs 3.6x fewer flops.  bytes_alg is §8(d)'s "
+                 "compulsory HBM traffic; every config is FP64-bound")}
+    kernels = sum(pr["local"].info["kernels_per_apply"] for pr in problems) * args.steps
     quad = None
-    if world == 1 and not args.dist and not args.no_quadrature:
+    if not dist_path and not args.no_quadrature:
         quad = {}
         for pr in problems:
-            if not pr["reorder"] and len(variants(args)) > 1:
+            if not pr["reorder"]:
                 continue
-            m, dm, geo, bas = build_problem(n_glob, pr["p"], pr["reorder"])
+            m, dm, geo, bas = build_problem(n_glob, pr["p"], True)
             Aq = op.CgPoissonOperator(m, dm, geo, bas, op.OperatorConfig(device=dev, cell_engine="dmma"))
             Aq.timed(pr["u"].data_ptr(), pr["y"].data_ptr(), st, 2)
             tq = []
@@ -482,40 +497,83 @@ def gpu_bench(args, rank, world):
                 flush.fill_(1.0)
                 tq.append(Aq.timed(pr["u"].data_ptr(), pr["y"].data_ptr(), st, 1))
             tq = np.array(tq)
-            t, tc = float(tq[:, 0].mean()), float(tq[:, 1].mean())
+            t, tcq = float(tq[:, 0].mean()), float(tq[:, 1].mean())
             quad[f"p{pr['p']}"] = {"ms": round(t, 4), "gdofs": round(pr["ndof"] / t / 1e6, 3),
-                                   "cell_kernel_ms": round(tc, 4),
-                                   "frac_fp64": round(Aq.info["flops_alg"] / tc / 1e9 / FP64_PEAK_TFLOPS, 3)}
+                                   "frac_alg": round(Aq.info["flops_alg"] / tcq / 1e9 / FP64_PEAK_TFLOPS, 3)}
             del Aq
-    dofs_global = sum(pr["ndof_global"] for pr, _ in rec)
-    return dict(total_ms=total_ms, dofs=dofs, dofs_global=dofs_global, n_glob=n_glob, e2e_s=e2e_s, per=per, clocks=clk.summary(),
-                transport=transport, p2p_check=p2p_check, quadrature_engine=quad,
-                roofline={"bound": "tensor", "kernel": f"{KERNEL_NAMES.get(dom['local'].info['cell_engine'])} ({dk})",
-                          "achieved": round(achieved, 3),
-                          "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE, "unit": "TFLOP/s",
-                          "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
-                          "algorithmic": "useful flops of the algorithm the cell engine runs, per launch "
-                                         "(tmf_plan_info.flops_engine: modal 12 M N + 18 M + N per cell, M = dim "
-                                         "P_(p-1), N = DoFs per cell; reference tensor 12 N^2 + 13 N) / CUDA-event "
-                                         "kernel time"},
-                gpu_launches=n_kern, parity_rel_l2=err, link=link,
-                e2e_desc={"streams": "Operator.apply_host_async(pinned host u, y) -> tmf_apply_host_async, one stream "
-                                     "per plan, largest first",
-                          "multi": "operator.apply_host_multi -> tmf_apply_host_multi (upload / compute / download "
-                                   "pipeline), largest first",
-                          "blocks": "operator.apply_host_multi(schedules) -> tmf_apply_host_multi_blocks: reordered "
-                                    "plans streamed in cell blocks, each ahead of its unordered twin, largest first"
-                          }.get(e2e_path, e2e_path) if (world == 1 and not args.dist) else
-                "host -> device, partitioned apply, device -> host",
-                h2d=sum(8 * pr["ndof"] for pr in problems), d2h=sum(8 * pr["ndof"] for pr in problems))
+    out = dict(total_ms=total_ms, dofs_global=sum(pr["ndof_global"] for pr, _ in rec), e2e_s=e2e_s, per=per,
+               clocks=clk.summary(), transport=transport, p2p_check=p2p_check, quadrature_engine=quad,
+               roofline=roofline, gpu_launches=kernels, parity=parity, link=link,
+               h2d=sum(8 * pr["ndof"] for pr in problems), d2h=sum(8 * pr["ndof"] for pr in problems))
+    for pr in problems:
+        pr.clear()
+    torch.cuda.empty_cache()
+    return out
+
+
+def c4_strong(args, rank, world):
+    """BASELINE config 4 at a FIXED mesh over the N ranks (strong scaling): DG kappa-Helmholtz
+    P2 on the reordered args.c4_n^3 x 6 mesh, partitioned by RCB, every apply with its ghost
+    exchange; apply time = max over ranks of the CUDA-event mean, L2 flushed before each."""
+    import torch
+
+    from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, operator as op, quadrature as Q
+    from paper_2509_10226_b200 import distributed as DD
+    from paper_2509_10226_b200.geometry import GeometryData
+    from paper_2509_10226_b200.reorder import hierarchical_reorder
+
+    t0 = time.time()
+    n, p = args.c4_n, 2
+    m = M.kuhn_cube_mesh(n, seed=0)
+    m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    geo = GeometryData("affine", cr, fr, None, None, None, None)
+    dm = D.build_dof_map(m, p, "dg")
+    kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
+    sipg = op.baseline_sipg_tau(m, p, 1.0 / n)
+    transport = os.environ.get("TMF_TRANSPORT", "p2p") if world > 1 else "nccl"
+    A = DD.DistributedDgOperator(m, dm, geo, bas, sipg, rank, world, kind="helmholtz", dirichlet_ids=range(6),
+                                 kappa=kap, part=DD.partition_cells(m, world), transport=transport)
+    if transport == "p2p":
+        A.connect_ipc()
+    ids = A.owned_global_ids()
+    ng = dm.n_global_dofs
+    del m, kap
+    setup_s = time.time() - t0
+    u = torch.from_numpy(np.ascontiguousarray(np.random.default_rng(1).uniform(-1, 1, ng)[ids])).cuda()
+    y = torch.empty_like(u)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        A.apply(u, out=y)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ts = []
+    for _ in range(max(5, args.steps)):
+        flush.fill_(1.0)
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        A.apply(u, out=y)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t[0])
+    return {"config": f"C4: DG kappa-Helmholtz P2 apply, {n}^3 x 6 reordered mesh, {world}-way RCB partition",
+            "scaling": "strong", "ndof": ng, "ms_per_apply": round(ms, 4), "value": round(ng / ms / 1e6, 3),
+            "unit": UNIT, "transport": transport, "setup_s_rank0": round(setup_s, 1)}
 
 
 _STDOUT_FD = None
 
 
 def emit(line):
-    """The one JSON line, on the real stdout (everything else -- e.g. the NCCL version
-    banner that libnccl prints on fd 1 -- was redirected to stderr)."""
+    """The one JSON line, on the real stdout (NCCL and library banners go to stderr)."""
     os.write(_STDOUT_FD if _STDOUT_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 
@@ -527,85 +585,81 @@ def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    workload = (f"CG Laplace apply, P1-P4 sweep, {args.n}^3x6 jittered permuted Kuhn tets, GM quadrature 2p, "
-                f"fp64, unordered{'' if args.no_reorder else ' + hierarchically reordered'}")
-    metric, unit = "operator-apply GDoF/s (fp64), CG Laplace P1-P4 sweep", "GDoF/s"
+    config = shared_config(args, world)
     if args.impl == "reference":
         if rank != 0:
             return
-        val, cores, detail = cpu_reference(args, args.cpu_sample_s)
-        line = {"impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
-                "data": "synthetic",
-                # same workload as the b200 arm at this world size; the bounded CPU sample is drawn
-                # from the 48^3 mesh (the per-DoF rate of the batched loop does not depend on size)
-                "config": {"workload": workload,
-                           "global_mesh": f"{args.n if world == 1 else int(round(args.n * world ** (1.0 / 3.0)))}^3 x 6",
-                           "sample_mesh": f"{args.n}^3 x 6"},
-                "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "port",
-                                 "sample": f"oracle port of the reference batched NumPy loop (16-cell batches), "
-                                           f"~{args.cpu_sample_s}s per worker per degree, extrapolated per DoF",
-                                 "detail": detail},
-                "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        emit(line)
+        r = reference_arm(args, args.steps, args.warmup, args.cpu_step_s)
+        emit({"impl": "reference", "metric": METRIC, "value": round(r["value"], 6), "unit": UNIT,
+              "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+              "ms_per_step": round(r["ms_per_step"], 3), "higher_is_better": True, "scaling": "weak",
+              "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+              "cpu_baseline": {"value": round(r["value"], 6), "unit": UNIT, "cores": r["cores"], "kind": "port",
+                               "sample": r["sample"], "setup_s": r["setup_s"]},
+              "e2e": {"value": round(r["value"], 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                      "d2h_bytes_per_step": 0},
+              "gpu_launches": 0})
         return
 
+    comm = None
     if world > 1 or args.dist:
         import torch
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29561")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator size / NVLS choice in the stderr log
         dev = int(os.environ.get("LOCAL_RANK", "0"))
         torch.cuda.set_device(dev)
-        # eager communicator init + a collective first: batch_isend_irecv requires that all
-        # ranks take part in the first NCCL call, and halo peers are a subset of the ranks
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", dev))
         dist.barrier()
+        comm = {"backend": "nccl", "world_size": dist.get_world_size(),
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
     r = gpu_bench(args, rank, world)
-    total_ms = r["total_ms"]
+    total_ms, e2e_s = r["total_ms"], r["e2e_s"]
     if world > 1:
         import torch
         import torch.distributed as dist
 
-        t = torch.tensor([total_ms, r["e2e_s"]], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms, e2e_s or 0.0], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_s = float(t[0]), float(t[1])
-    else:
-        e2e_s = r["e2e_s"]
-    value = r["dofs_global"] / (total_ms * 1e-3) / 1e9
-    e2e_val = r["dofs_global"] / e2e_s / 1e9
+        total_ms, e2e_s = float(t[0]), (float(t[1]) if e2e_s is not None else None)
+    c4 = None
+    if args.c4_n > 0:
+        try:
+            c4 = c4_strong(args, rank, world)
+        except Exception as e:  # reported beside the C2 value, not required for it
+            c4 = {"error": str(e)[:300]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            v, cores, detail = cpu_reference(args, min(args.cpu_sample_s, 1.5))
-            cpu = {"value": v, "unit": unit, "cores": cores, "kind": "port",
-                   "sample": "oracle port of the reference batched NumPy loop, ~1.5 s per worker per degree, "
-                             "extrapolated per DoF", "detail": detail}
+            c = reference_arm(args, 3, 1, min(args.cpu_step_s, 1.5))
+            cpu = {"value": round(c["value"], 6), "unit": UNIT, "cores": c["cores"], "kind": "port",
+                   "sample": c["sample"], "ms_per_step": round(c["ms_per_step"], 3)}
         except Exception as e:  # the CPU baseline is reported, not required for the GPU number
-            cpu = {"value": None, "error": str(e)[:200]}
+            cpu = {"value": None, "error": str(e)[:300]}
     if rank == 0:
-        line = {"metric": metric, "value": round(value, 4), "unit": unit, "n_gpus": world, "steps": args.steps,
+        value = r["dofs_global"] / (total_ms * 1e-3) / 1e9
+        config = dict(config, l2="flushed (256 MiB write) before every apply",
+                      transport=r["transport"] if (world > 1 or args.dist) else None,
+                      p2p_vs_nccl_rel_l2=r["p2p_check"])
+        line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload, "l2": "flushed (256 MiB write) before every apply",
-                           "global_mesh": f"{r['n_glob']}^3 x 6",
-                           "parallelism": (f"{world}-way RCB domain decomposition, "
-                                           + ("ghost DoFs gathered / RED-scattered by the cell kernel in peer "
-                                              "memory (NVLink, CUDA IPC)" if r["transport"] == "p2p" else "NCCL halo")
-                                           + f" (weak scaling: ~{args.n}^3 x 6 cells per GPU)")
-                           if (world > 1 or args.dist) else "single GPU",
-                           "transport": r["transport"] if (world > 1 or args.dist) else None,
-                           "p2p_vs_nccl_rel_l2": r["p2p_check"]},
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
                 "per_degree": r["per"], "roofline": r["roofline"], "cpu_baseline": cpu,
-                "quadrature_engine": r["quadrature_engine"],
-                "e2e": {"value": round(e2e_val, 4), "unit": unit, "h2d_bytes_per_step": r["h2d"],
-                        "d2h_bytes_per_step": r["d2h"], "path": r["e2e_desc"],
-                        "ms_per_step": round(e2e_s / args.steps * 1e3, 3),
-                        # the box's PCIe link measured live; frac = link lower bound / measured step
-                        "link": None if r["link"] is None else dict(
-                            r["link"], frac=round(r["link"]["step_bound_ms"] / (e2e_s / args.steps * 1e3), 3))},
-                "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "parity_e2e_vs_timed_rel_l2": r["parity_rel_l2"]}
+                "quadrature_engine": r["quadrature_engine"], "c4_strong": c4,
+                "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "comm": comm}
+        if e2e_s is not None:
+            ms_e2e = e2e_s / args.steps * 1e3
+            line["e2e"] = {"value": round(r["dofs_global"] / e2e_s / 1e9, 4), "unit": UNIT,
+                           "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
+                           "path": "Operator.apply_host_async(pinned host u, y) -> tmf_apply_host_async, one "
+                                   "stream per plan, largest first" if world == 1 else
+                                   "host -> device, partitioned apply, device -> host",
+                           "ms_per_step": round(ms_e2e, 3),
+                           "link": None if r["link"] is None else
+                           dict(r["link"], frac=round(r["link"]["step_bound_ms"] / ms_e2e, 3)),
+                           "parity_vs_timed_rel_l2": r["parity"]}
         emit(line)
     if world > 1 or args.dist:
         import torch.distributed as dist
