@@ -40,8 +40,14 @@ struct CellArgs {
   const double* __restrict__ frags;  // B1 then B2 fragments (global; staged to smem)
   int64_t n_cells;
   int nc;                          // interleaved components
+  // kernel-parameter layout: the cell kernels' code generation depends on it (a tighter
+  // struct measured 4-9 % slower at P3 / P4, same SASS otherwise); keep these reserved slots
+  int reserved0 = 0;
+  const void* reserved1[2] = {nullptr, nullptr};
+  int reserved2[2] = {0, 0};
   PeerArgs peer;                   // multi-GPU: ghost DoFs read / scattered over peer memory
   double* energy = nullptr;        // CG tensor / modal engines: += sum_e u_e^T A_e u_e (PCG's p.Ap)
+  const double* reserved3 = nullptr;
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the
