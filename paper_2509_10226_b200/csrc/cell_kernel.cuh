@@ -115,10 +115,11 @@ struct CellShape {
 // (8-byte copies, zero-filled for masked DoFs) and the 64-byte geometry records of the
 // super-tile AS-1 ahead into its own shared-memory ring, so AS-1 tiles' loads are in
 // flight without holding registers (measured: pays at P4 only)
-template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0>
+// MT_: 8-cell tiles per warp iteration sharing every B-fragment load (0 = CellShape::MT)
+template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0>
 __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
   using S = CellShape<N, Q, MASS>;
-  constexpr int MT = S::MT;
+  constexpr int MT = MT_ ? MT_ : S::MT;
   static_assert(AS == 0 || !PEER, "the async ring has no peer gathers");
   extern __shared__ __align__(16) double smem[];
   {

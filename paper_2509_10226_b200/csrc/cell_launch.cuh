@@ -27,26 +27,28 @@ static cudaError_t persistent_grid(K kern, int block, int smem, int64_t warps_of
   return cudaSuccess;
 }
 
-template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0>
+// MT_: 8-cell tiles per warp iteration sharing every B-fragment load (0 = CellShape default)
+template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0>
 static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = CellShape<N, Q, MASS>;
+  constexpr int MT = MT_ ? MT_ : S::MT;
   // tables + the per-warp async rings
-  constexpr int SMEM = S::SMEM + (AS > 0 ? AS * S::MT * (S::KK * 32 + 64) * 8 * (BLOCK / 32) : 0);
+  constexpr int SMEM = S::SMEM + (AS > 0 ? AS * MT * (S::KK * 32 + 64) * 8 * (BLOCK / 32) : 0);
   static_assert(SMEM <= 227 * 1024, "shared memory");
-  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, PEER, AS>;
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, PEER, AS, MT_>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
-  const int64_t supertiles = ((a.n_cells + 8 * S::MT - 1) / (8 * S::MT)) * a.nc;
+  const int64_t supertiles = ((a.n_cells + 8 * MT - 1) / (8 * MT)) * a.nc;
   int64_t blocks = 1;
   if (cudaError_t e = persistent_grid(kern, BLOCK, SMEM, supertiles, n_sm, &blocks); e != cudaSuccess) return e;
   if (info) {
     info->dmma_per_tile = S::DMMA_PER_TILE;
-    info->tiles = supertiles * S::MT;
+    info->tiles = supertiles * MT;
     info->block = BLOCK;
     info->grid = (int)blocks;
     info->smem = SMEM;
     info->frag_doubles = S::NFRAG * 32;
     info->table = 0;
-    info->flops_issued = (double)supertiles * S::MT * S::DMMA_PER_TILE * 512.0;
+    info->flops_issued = (double)supertiles * MT * S::DMMA_PER_TILE * 512.0;
     return cudaSuccess;
   }
   if (a.n_cells == 0) return cudaSuccess;
@@ -86,7 +88,10 @@ static cudaError_t launch_cell_x(const CellArgs& a, int n_sm, cudaStream_t st, C
 //           P4 512 x 2 (P2 with mass 512 x 2)
 //   points  one large CTA per SM: P3 768 threads (-5.6 %), P4 640 (-1.4 %), DG P2 512 (-26 %);
 //   modal   P2 256 x 2 tiles 0.0516 ms, P3 768 0.1075 ms, P4 512 with the 2-stage async
-//           gather ring (0.267 -> 0.245 ms reordered; P2 / P3 lose 5-8 % with any ring)
+//           gather ring (0.267 -> 0.245 ms reordered; P2 / P3 lose 5-8 % with any ring);
+//           two 8-cell tiles per warp sharing every B-fragment load (half the shared-memory
+//           wavefronts) measured 7-36 % SLOWER at P3 / P4 (fewer warps, round 2:
+//           profiles/r02/modal_two_tiles.jsonl)
 template <int N, bool MASS, bool DG>
 static cudaError_t launch_tensor(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   if (!DG && a.peer.u != nullptr && !info) {   // multi-GPU peer ghosts
