@@ -18,6 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtetmf_b200.so")
+LIB_DEBUG = os.path.join(HERE, "libtetmf_b200_debug.so")   # -DTMF_DEBUG_CHECKS (common.cuh)
 BUILD = os.path.join(HERE, "csrc", "_obj")
 SOURCES = ["kernels.cu", "cell_p1.cu", "cell_p2.cu", "cell_p3.cu", "cell_p4.cu", "face_launch.cu", "cell_block.cu", "capi.cu", "multigrid.cu",
            "reorder.cpp", "setup.cpp"]
@@ -40,17 +41,21 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, debug: bool = False) -> str:
+    """Compile the library (``debug``: the bounds-checking variant libtetmf_b200_debug.so)."""
+    obj_dir = BUILD + ("_debug" if debug else "")
+    lib = LIB_DEBUG if debug else LIB
+    flags = FLAGS + (["-DTMF_DEBUG_CHECKS"] if debug else [])
+    os.makedirs(obj_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "tetmf_b200.h"))
     objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+        o = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [nvcc(), *ARCH, *flags, "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)
@@ -65,10 +70,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for log in ex.map(run, jobs):
             if verbose and log:
                 print(log, file=sys.stderr)
-    if force or jobs or _stale(LIB, objs):
-        run([nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
-    return LIB
+    if force or jobs or _stale(lib, objs):
+        run([nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart"])
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv))
+    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv, debug="--debug" in sys.argv))

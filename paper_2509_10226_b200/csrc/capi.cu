@@ -248,6 +248,7 @@ struct tmf_plan {
   int Qk = 0;            // "points" of the cell kernel (n_q, or M for the modal tables)
   int QFk = 0;           // "points" of the face kernel (n_qf, or NF for the modal face tables)
   cudaEvent_t ev_stage = nullptr;   // end of the last staged (host-buffer) apply
+  int* dbg_flag = nullptr;          // TMF_DEBUG_CHECKS builds: device check flags (common.cuh)
   bool dg = false, mass = false, faces = false;
   int64_t n_cells = 0, n_verts = 0, n_scalar = 0, n_global = 0;
   double mass_scale = 0.0, stiff_scale = 1.0;
@@ -323,6 +324,11 @@ struct tmf_plan {
     a.n_cells = c1 - c0;
     a.nc = nc;
     if (!dg && with_peer) a.peer = peer;   // CG ghost DoFs over peer memory (DG: the face kernel's ghost cells)
+#ifdef TMF_DEBUG_CHECKS
+    a.dbg_n_dofs = dg ? (c1 - c0) * N * nc : n_global;
+    a.dbg_n_cells = c1 - c0;
+    a.dbg_flag = dbg_flag;
+#endif
     return a;
   }
   tmf::BlockArgs block_args(const double* u, double* y, double* energy) const {
@@ -343,6 +349,11 @@ struct tmf_plan {
     a.nvmax = blk_nvmax;
     a.scale = stiff_scale;
     a.energy = energy;
+#ifdef TMF_DEBUG_CHECKS
+    a.dbg_n_dofs = n_global;
+    a.dbg_n_cells = n_cells;
+    a.dbg_flag = dbg_flag;
+#endif
     return a;
   }
   tmf::FaceArgs face_args(const double* u, double* y, bool boundary) const {
@@ -359,6 +370,11 @@ struct tmf_plan {
     a.n_dpc = N;
     a.nc = nc;
     a.peer = peer;
+#ifdef TMF_DEBUG_CHECKS
+    a.dbg_n_dofs = n_global;
+    a.dbg_n_cells = n_cells;
+    a.dbg_flag = dbg_flag;
+#endif
     return a;
   }
   tmf::FaceGeoArgs face_geo_args(bool boundary) const {
@@ -382,7 +398,7 @@ struct tmf_plan {
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
                     (void*)f32_rows, (void*)f32_geo, (void*)blk_off, (void*)blk_nv, (void*)blk_uniq,
-                    (void*)blk_loc, (void*)blk_inc, (void*)blk_ioff, (void*)blk_kappa,
+                    (void*)blk_loc, (void*)blk_inc, (void*)blk_ioff, (void*)blk_kappa, (void*)dbg_flag,
                     (void*)peer_u_tab, (void*)peer_y_tab, (void*)ghost_rank, (void*)ghost_index})
       if (p) cudaFree(p);
   }
@@ -623,6 +639,21 @@ int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total) {
   return TMF_OK;
 }
 
+#ifdef TMF_DEBUG_CHECKS
+// Debug build: wait for the apply and report any index the kernels found out of range.
+int debug_flag_check(tmf_plan* P, cudaStream_t st) {
+  TMF_CUDA(cudaStreamSynchronize(st));
+  int flag = 0;
+  TMF_CUDA(cudaMemcpy(&flag, P->dbg_flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {
+    TMF_CUDA(cudaMemset(P->dbg_flag, 0, sizeof(int)));
+    return fail(TMF_ECUDA, "debug bounds check failed in a kernel: flags " + std::to_string(flag) +
+                               " (1 DoF index, 2 cell, 4 face position, 8 block-local index, 16 block slots)");
+  }
+  return TMF_OK;
+}
+#endif
+
 // y_zeroed: the caller already cleared y (CG); energy: += sum_e u_e^T A_e u_e + the identity
 // rows' u_i^2 (= u.Au when the tensor cell engine runs; PCG's fused p.Ap)
 int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaEvent_t* ev,
@@ -648,6 +679,9 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
   if (ev && P->faces && fix) TMF_CUDA(cudaEventRecord(ev[2], st));
   if (fix) TMF_CUDA(tmf::launch_fixup(u, y, P->fix_list, P->n_fix, P->n_sm, st, energy));
   if (ev) TMF_CUDA(cudaEventRecord(ev[3], st));
+#ifdef TMF_DEBUG_CHECKS
+  if (int rc = debug_flag_check(P, st)) return rc;
+#endif
   return TMF_OK;
 }
 
@@ -695,7 +729,11 @@ const char* tmf_last_error(void) { return g_err.c_str(); }
 
 // error reporting for the other C-ABI translation units (multigrid.cu); not in the header
 int tmf_internal_set_error(int code, const char* msg) { return fail(code, msg); }
-const char* tmf_version(void) { return "tetmf_b200 0.1 (sm_100a, fp64 DMMA)"; }
+#ifdef TMF_DEBUG_CHECKS
+const char* tmf_version(void) { return "tetmf_b200 0.2 (sm_100a, fp64 DMMA) DEBUG-CHECKS"; }
+#else
+const char* tmf_version(void) { return "tetmf_b200 0.2 (sm_100a, fp64 DMMA)"; }
+#endif
 
 int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   if (!d || !out) return fail(TMF_EINVAL, "null descriptor/output");
@@ -737,6 +775,10 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     delete P;
     return rc;
   };
+#ifdef TMF_DEBUG_CHECKS
+  TMF_CUDA(cudaMalloc(&P->dbg_flag, sizeof(int)));
+  TMF_CUDA(cudaMemset(P->dbg_flag, 0, sizeof(int)));
+#endif
   P->dev = d->device;
   {
     int sms = 0;

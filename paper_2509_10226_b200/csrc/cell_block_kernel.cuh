@@ -54,6 +54,7 @@ struct BlockArgs {
   int numax, nvmax;                     // largest block: unique DoFs / vertex DoFs
   double scale;                         // stiff_scale
   double* energy;                       // += sum_e u_e^T A_e u_e (PCG's fused p.Ap), or nullptr
+  TMF_DBG_FIELDS
 };
 
 template <int N>
@@ -107,6 +108,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_block_kernel(BlockArgs a, co
     const int e0 = __ldg(a.uniq + off + i0);
     const int e1 = i1 < nu ? __ldg(a.uniq + off + i1) : -1;
     const int g0 = e0 < 0 ? ~e0 : e0, g1 = e1 < 0 ? ~e1 : e1;
+    TMF_CHECK(a, g0 < a.dbg_n_dofs && (i1 >= nu || g1 < a.dbg_n_dofs), TMF_DBG_DOF);
+    TMF_CHECK(a, nu <= a.numax && nv <= a.nvmax && nv <= nu, TMF_DBG_LOCAL);
     const double u0 = e0 < 0 ? 0.0 : __ldg(a.u + g0);
     const double u1 = e1 < 0 ? 0.0 : __ldg(a.u + g1);
     double x0[3], x1[3];
@@ -155,6 +158,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_block_kernel(BlockArgs a, co
       l[4 * q + 2] = (uint16_t)(v.y & 0xFFFFu);
       l[4 * q + 3] = (uint16_t)(v.y >> 16);
     }
+#pragma unroll
+    for (int j = 0; j < N; ++j) TMF_CHECK(a, l[j] < nu && (j >= 4 || l[j] < nv), TMF_DBG_LOCAL);
     Vec3 x[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = Vec3{xs[3 * l[i]], xs[3 * l[i] + 1], xs[3 * l[i] + 2]};
@@ -196,7 +201,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_block_kernel(BlockArgs a, co
     const int e = __ldg(a.uniq + off + i);
     if (e < 0) continue;
     double s = 0.0;
-    for (int k = sioff[i]; k < sioff[i + 1]; ++k) s += R[sinc[k]];
+    TMF_CHECK(a, sioff[i] <= sioff[i + 1] && sioff[i + 1] <= ncb * N && e < a.dbg_n_dofs, TMF_DBG_SLOT);
+    for (int k = sioff[i]; k < sioff[i + 1]; ++k) {
+      TMF_CHECK(a, sinc[k] < N * B && (int)(sinc[k] % B) < ncb, TMF_DBG_SLOT);
+      s += R[sinc[k]];
+    }
     atomicAdd(a.y + e, s);
   }
   if (a.energy != nullptr) {

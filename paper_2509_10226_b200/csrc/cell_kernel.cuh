@@ -48,6 +48,7 @@ struct CellArgs {
   PeerArgs peer;                   // multi-GPU: ghost DoFs read / scattered over peer memory
   double* energy = nullptr;        // CG tensor / modal engines: += sum_e u_e^T A_e u_e (PCG's p.Ap)
   const double* reserved3 = nullptr;
+  TMF_DBG_FIELDS
 };
 
 // Per-cell geometry, computed once per plan by cell_geometry_kernel (the
@@ -169,6 +170,8 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
 #pragma unroll
       for (int kk = 0; kk < S::KK; ++kk) {
         const int g = nidx[m][kk];
+        TMF_CHECK(a, g < 0 || (int64_t)g * a.nc + cmp < a.dbg_n_dofs, TMF_DBG_DOF);
+        TMF_CHECK(a, !ok || c < a.dbg_n_cells, TMF_DBG_CELL);
         if (PEER)
           av[m][kk] = (g >= 0) ? __ldg(peer_src(a.peer, a.u, g, a.nc, cmp)) : 0.0;
         else
@@ -194,6 +197,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
 #pragma unroll
       for (int kk = 0; kk < S::KK; ++kk) {
         const int g = nidx[m][kk];
+        TMF_CHECK(a, g < 0 || (int64_t)g * a.nc + cmp < a.dbg_n_dofs, TMF_DBG_DOF);
         const double* src = g >= 0 ? a.u + (int64_t)g * a.nc + cmp : a.u;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(r + (m * S::KK + kk) * 32 + lane)),
@@ -364,9 +368,11 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
           const int j = 8 * nj + 2 * q4 + i;
           if (j < N) {
             if (DG) {
+              TMF_CHECK(a, (cell[m] * N + j) * a.nc + comp < a.dbg_n_dofs, TMF_DBG_DOF);
               a.y[(cell[m] * N + j) * a.nc + comp] = yacc[m][nj][i];
             } else {
               const int64_t g = __ldg(a.dofs + cell[m] * N + j);
+              TMF_CHECK(a, g < 0 || g * a.nc + comp < a.dbg_n_dofs, TMF_DBG_DOF);
               if (g >= 0) {
                 if (PEER)
                   atomicAdd(peer_dst(a.peer, a.y, g, a.nc, comp), yacc[m][nj][i]);

@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
 #pragma unroll
       for (int kk = 0; kk < KK; ++kk) {
         const int g = ix[m][kk] = nidx[m][kk];
+        TMF_CHECK(a, g < 0 || (int64_t)g * a.nc + cmp < a.dbg_n_dofs, TMF_DBG_DOF);
+        TMF_CHECK(a, !ok || c < a.dbg_n_cells, TMF_DBG_CELL);
         if (PEER)
           av[m][kk] = (g >= 0) ? __ldg(peer_src(a.peer, a.u, g, a.nc, cmp)) : 0.0;
         else
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
       for (int m = 0; m < MT; ++m) {
         if (j >= N || cell[m] >= a.n_cells) continue;
         if (DG) {
+          TMF_CHECK(a, (cell[m] * N + j) * a.nc + comp < a.dbg_n_dofs, TMF_DBG_DOF);
           a.y[(cell[m] * N + j) * a.nc + comp] = yv[m];
         } else {
           const int g = idx[m][ib];

@@ -11,6 +11,35 @@
 
 namespace tmf {
 
+// Debug build (-DTMF_DEBUG_CHECKS, libtetmf_b200_debug.so): the kernels test every global
+// index they derive (gathered / scattered DoFs, cells, face DoF positions, block-local
+// indices and slot lists) against the plan's sizes and OR a code into a device flag that
+// the C-ABI reads after each apply -- the memcheck substitute on this pool, where
+// compute-sanitizer is closed.  Release builds: the fields and checks do not exist (same
+// SASS).
+#ifdef TMF_DEBUG_CHECKS
+#define TMF_DBG_FIELDS \
+  int64_t dbg_n_dofs = 0;  /* vector entries (global / local layout) */ \
+  int64_t dbg_n_cells = 0; \
+  int* dbg_flag = nullptr;
+#define TMF_CHECK(args, cond, code)                                       \
+  do {                                                                    \
+    if (!(cond) && (args).dbg_flag != nullptr) atomicOr((args).dbg_flag, (code)); \
+  } while (0)
+#else
+#define TMF_DBG_FIELDS
+#define TMF_CHECK(args, cond, code) \
+  do {                              \
+  } while (0)
+#endif
+enum : int {
+  TMF_DBG_DOF = 1,        // gathered / scattered vector index out of range
+  TMF_DBG_CELL = 2,       // cell index out of range
+  TMF_DBG_PERM = 4,       // face gather position out of range
+  TMF_DBG_LOCAL = 8,      // block-local DoF index >= the block's unique DoFs
+  TMF_DBG_SLOT = 16,      // block slot list / offsets inconsistent
+};
+
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])

@@ -54,6 +54,7 @@ struct FaceArgs {
   int n_dpc;
   int nc;
   PeerArgs peer;                      // multi-GPU: ghost cells' u read from their owner (n_own = cells)
+  TMF_DBG_FIELDS
 };
 
 // Per-face geometry, computed once at plan creation by face_geometry_kernel and
@@ -291,6 +292,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
         nam[kk] = 0.0;
         nap[kk] = 0.0;
         if (n_cm >= 0 && j < N) {
+          TMF_CHECK(a, n_cm < a.dbg_n_cells && __ldg(perm_m + j) < N, TMF_DBG_CELL);
+          TMF_CHECK(a, BOUNDARY || (n_cp >= 0 && (PEER || n_cp < a.dbg_n_cells) && __ldg(perm_p + j) < N),
+                    TMF_DBG_CELL);
           nam[kk] = __ldg(a.u + ((int64_t)n_cm * N + __ldg(perm_m + j)) * a.nc + comp);
           if (!BOUNDARY) {
             // DG ghost cell (partitioned apply): its u is read from the owner rank
@@ -475,6 +479,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
       for (int kk = 0; kk < S::KK; ++kk) {
         const int j = 4 * kk + q4;
         const bool ok = rcm >= 0 && j < N;
+        TMF_CHECK(a, !ok || (rcm < a.dbg_n_cells && rcp >= 0 && rcp < a.dbg_n_cells && pm[j] < N && pp[j] < N),
+                  TMF_DBG_CELL);
         const double* sm = ok ? a.u + ((int64_t)rcm * N + pm[j]) * a.nc + comp : a.u;
         const double* sp = ok ? a.u + ((int64_t)rcp * N + pp[j]) * a.nc + comp : a.u;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(

@@ -89,16 +89,19 @@ def dg_diagonal(A, mesh, stream: int = 0):
     diag = torch.empty(n, dtype=torch.float64, device=dev)
     u = torch.zeros(n, dtype=torch.float64, device=dev)
     y = torch.empty_like(u)
-    st = stream or torch.cuda.current_stream(dev).cuda_stream
-    for c in range(ncol):
-        cells = torch.from_numpy(np.nonzero(col == c)[0].astype(np.int64)).to(dev)
-        for j in range(N):
-            for k in range(nc_):
-                idx = (cells * N + j) * nc_ + k
-                u.zero_()
-                u[idx] = 1.0
-                A.apply_into(u.data_ptr(), y.data_ptr(), st)
-                diag[idx] = y[idx]
+    # every probe (torch writes of u, the apply, torch reads of y) runs on ONE stream: the
+    # caller's ``stream`` if given (made torch's current stream for the loop), else torch's own
+    ext = torch.cuda.ExternalStream(stream, device=dev) if stream else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(ext):
+        for c in range(ncol):
+            cells = torch.from_numpy(np.nonzero(col == c)[0].astype(np.int64)).to(dev)
+            for j in range(N):
+                for k in range(nc_):
+                    idx = (cells * N + j) * nc_ + k
+                    u.zero_()
+                    u[idx] = 1.0
+                    A.apply_into(u.data_ptr(), y.data_ptr(), ext.cuda_stream)
+                    diag[idx] = y[idx]
     return diag
 
 
