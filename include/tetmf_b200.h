@@ -111,6 +111,11 @@ int tmf_plan_create(const tmf_plan_desc* desc, tmf_plan** out);
 int tmf_plan_destroy(tmf_plan* plan);
 int tmf_plan_get_info(const tmf_plan* plan, tmf_plan_info* info);
 
+/* Test hook of the bounds-checking build (libtetmf_b200_debug.so, -DTMF_DEBUG_CHECKS):
+ * overwrite the device copy of one CG cell-DoF slot (to show the kernels' range checks
+ * fire).  The release library returns TMF_EINVAL. */
+int tmf_debug_poke_dof(tmf_plan* plan, int64_t slot, int32_t value);
+
 /* y = A u on device pointers (length n_global_dofs), ordered on `stream`
  * (a cudaStream_t, NULL = legacy default stream).  y is overwritten. */
 int tmf_apply(tmf_plan* plan, const double* u, double* y, void* stream);

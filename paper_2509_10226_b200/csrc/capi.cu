@@ -1218,6 +1218,22 @@ int tmf_plan_destroy(tmf_plan* plan) {
   return TMF_OK;
 }
 
+int tmf_debug_poke_dof(tmf_plan* P, int64_t slot, int32_t value) {
+#ifdef TMF_DEBUG_CHECKS
+  if (!P || P->dg || slot < 0 || slot >= P->n_cells * P->N) return fail(TMF_EINVAL, "bad poke");
+  TMF_CUDA(cudaSetDevice(P->dev));
+  TMF_CUDA(cudaMemcpy(P->dofs + slot, &value, sizeof(int32_t), cudaMemcpyHostToDevice));
+  // the block-assembly tables are derived at plan creation: take the tile kernel from now on
+  P->blk_B = 0;
+  return TMF_OK;
+#else
+  (void)P;
+  (void)slot;
+  (void)value;
+  return fail(TMF_EINVAL, "tmf_debug_poke_dof needs the TMF_DEBUG_CHECKS build (libtetmf_b200_debug.so)");
+#endif
+}
+
 int tmf_plan_get_info(const tmf_plan* plan, tmf_plan_info* info) {
   if (!plan || !info) return fail(TMF_EINVAL, "null plan/info");
   *info = plan->info;
