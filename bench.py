@@ -640,12 +640,14 @@ def main():
             cpu = {"value": None, "error": str(e)[:300]}
     if rank == 0:
         value = r["dofs_global"] / (total_ms * 1e-3) / 1e9
-        config = dict(config, l2="flushed (256 MiB write) before every apply",
-                      transport=r["transport"] if (world > 1 or args.dist) else None,
-                      p2p_vs_nccl_rel_l2=r["p2p_check"])
+        timing = {"l2": "flushed (256 MiB write) before every apply (inputs are L2-sized at P1)",
+                  "events": "CUDA events on the launch stream around each apply (tmf_apply_timed)",
+                  "transport": r["transport"] if (world > 1 or args.dist) else None,
+                  "p2p_vs_nccl_rel_l2": r["p2p_check"]}
         line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "timing": timing,
                 "per_degree": r["per"], "roofline": r["roofline"], "cpu_baseline": cpu,
                 "quadrature_engine": r["quadrature_engine"], "c4_strong": c4,
                 "gpu_launches": r["gpu_launches"], "clocks": r["clocks"], "comm": comm}
