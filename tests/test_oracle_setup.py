@@ -56,3 +56,13 @@ def test_bench_workload_matches_product_setup(p):
     cd, ns = ref_mesh.cg_dofs(c3, len(v3), p)
     dm = D.build_dof_map(m, p, "cg")
     assert ns == dm.n_scalar_dofs and np.array_equal(cd, dm.cell_dofs)
+
+
+def test_reorder_bit_exact_at_bench_size():
+    """The product's C++ hierarchical reordering equals the oracle's restatement on the 48^3
+    C2 mesh the bench reorders (663,552 cells)."""
+    from paper_2509_10226_b200 import mesh as M
+    from paper_2509_10226_b200.reorder import hierarchical_reorder
+
+    m = M.kuhn_cube_mesh(48, seed=0)
+    assert np.array_equal(hierarchical_reorder(m), ref_reorder.hierarchical_reorder(m.n_cells, m.interior_faces))
