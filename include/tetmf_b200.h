@@ -86,7 +86,10 @@ typedef struct tmf_plan_desc {
                                   1 off, 2 on); 17-18 face engine (0 by degree,
                                   1 quadrature points, 3 modal: the point loop on NF
                                   exact unit-weight face modes); 20: also build the
-                                  fp32 mirror (tmf_apply_f32).  Other bits: reserved. */
+                                  fp32 mirror (tmf_apply_f32); 22-23 CG cell traversal
+                                  order (0 auto: Morton when the given order has no
+                                  locality, 1 the given order, 2 Morton; u / y keep the
+                                  caller's numbering either way).  Other bits: reserved. */
 } tmf_plan_desc;
 
 typedef struct tmf_plan_info {
@@ -105,6 +108,8 @@ typedef struct tmf_plan_info {
   double flops_engine;         /* useful flops per apply of the algorithm the engines
                                   run (= flops_alg except for the tensor engines)      */
   int32_t face_engine;         /* faces: 1 quadrature points, 3 modal (0: no faces)   */
+  int32_t cell_order;          /* CG cell traversal: 1 the caller's order, 2 Morton order of the
+                                  centroids (0: DG, always the caller's)              */
 } tmf_plan_info;
 
 int tmf_plan_create(const tmf_plan_desc* desc, tmf_plan** out);

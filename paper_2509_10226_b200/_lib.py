@@ -63,7 +63,7 @@ class PlanInfo(C.Structure):
         ("flops_issued", C.c_double), ("kernels_per_apply", C.c_int32),
         ("n_face_batches", C.c_int32), ("device_bytes", C.c_int64), ("block_cells", C.c_int32),
         ("block_ratio", C.c_double), ("cell_engine", C.c_int32), ("flops_engine", C.c_double),
-        ("face_engine", C.c_int32),
+        ("face_engine", C.c_int32), ("cell_order", C.c_int32),
     ]
 
 

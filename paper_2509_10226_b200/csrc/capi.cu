@@ -265,6 +265,9 @@ struct tmf_plan {
   int* dofs = nullptr;
   int* fix_list = nullptr;
   int64_t n_fix = 0;
+  // CG traversal order (flags bits 22-23: 0 auto, 1 input, 2 Morton): the tile kernels walk the
+  // plan's per-cell arrays in this order; u / y keep the caller's numbering
+  bool cell_perm = false;
   // CG block assembly (cell_block_kernel.cuh; flags bits 15-16: 0 auto, 1 off, 2 on)
   int blocks_mode = 0;
   int blk_B = 0;                   // cells per block (0: off)
@@ -522,21 +525,10 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   return TMF_OK;
 }
 
-// CG block assembly tables (cell_block_kernel.cuh).  Cells are taken in Morton order of
-// their centroids (a locality order of the plan's own; the input numbering of cells and
-// DoFs is unchanged, the sum over cells does not depend on the order) and cut into blocks
-// of B.  Per block: its unique global DoFs sorted ascending (so the vertex DoFs, ids <
-// n_vertices in the reference numbering, come first), each slot's local index (u16), and
-// the slots of every unique DoF (u16 j*B + cl, in slot order) with their offsets.
-// Returns TMF_OK with P->blk_B = 0 when the plan does not qualify (vertex DoFs are not the
-// vertex ids, or a block does not fit in shared memory).
-int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total) {
-  const int N = P->N, NP = (N + 3) & ~3;
-  const int64_t n = P->n_cells;
-  for (int64_t c = 0; c < n; ++c)
-    for (int j = 0; j < 4; ++j)
-      if (d->cell_dofs[c * N + j] != d->cells[c * 4 + j]) return TMF_OK;   // not the reference numbering
-  // Morton order of the centroids (21 bits per axis in the bounding box)
+// Cells in Morton order of their centroids (21 bits per axis in the vertices' bounding box),
+// ties by cell id: the plans' locality traversal order (a permutation of 0..n-1).
+std::vector<int64_t> morton_order(const tmf_plan_desc* d) {
+  const int64_t n = d->n_cells;
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
   for (int64_t v = 0; v < d->n_vertices; ++v)
     for (int k = 0; k < 3; ++k) {
@@ -564,6 +556,43 @@ int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total) {
     key[c] = {code, c};
   }
   std::sort(key.begin(), key.end());
+  std::vector<int64_t> order(n);
+  for (int64_t i = 0; i < n; ++i) order[i] = key[i].second;
+  return order;
+}
+
+// Mean distance between the centroids of consecutive cells of an order (a locality measure).
+double consecutive_distance(const tmf_plan_desc* d, const int64_t* order) {
+  const int64_t n = d->n_cells;
+  if (n < 2) return 0.0;
+  double acc = 0.0, prev[3] = {0, 0, 0};
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t c = order ? order[i] : i;
+    double x[3] = {0, 0, 0};
+    for (int k = 0; k < 3; ++k)
+      for (int j = 0; j < 4; ++j) x[k] += 0.25 * d->vertices[3 * (int64_t)d->cells[c * 4 + j] + k];
+    if (i) acc += std::sqrt((x[0] - prev[0]) * (x[0] - prev[0]) + (x[1] - prev[1]) * (x[1] - prev[1]) +
+                            (x[2] - prev[2]) * (x[2] - prev[2]));
+    for (int k = 0; k < 3; ++k) prev[k] = x[k];
+  }
+  return acc / (double)(n - 1);
+}
+
+// CG block assembly tables (cell_block_kernel.cuh).  Cells are taken in Morton order of
+// their centroids (a locality order of the plan's own; the input numbering of cells and
+// DoFs is unchanged, the sum over cells does not depend on the order) and cut into blocks
+// of B.  Per block: its unique global DoFs sorted ascending (so the vertex DoFs, ids <
+// n_vertices in the reference numbering, come first), each slot's local index (u16), and
+// the slots of every unique DoF (u16 j*B + cl, in slot order) with their offsets.
+// Returns TMF_OK with P->blk_B = 0 when the plan does not qualify (vertex DoFs are not the
+// vertex ids, or a block does not fit in shared memory).
+int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total) {
+  const int N = P->N, NP = (N + 3) & ~3;
+  const int64_t n = P->n_cells;
+  for (int64_t c = 0; c < n; ++c)
+    for (int j = 0; j < 4; ++j)
+      if (d->cell_dofs[c * N + j] != d->cells[c * 4 + j]) return TMF_OK;   // not the reference numbering
+  const std::vector<int64_t> order = morton_order(d);
   const int64_t nb = (n + B - 1) / B;
   std::vector<std::vector<int>> uq(nb);
   std::vector<std::vector<uint16_t>> io(nb);
@@ -579,7 +608,7 @@ int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total) {
         const int ncb = (int)std::min<int64_t>(B, n - c0);
         pr.clear();
         for (int cl = 0; cl < ncb; ++cl) {
-          const int64_t c = key[c0 + cl].second;
+          const int64_t c = order[c0 + cl];
           for (int j = 0; j < N; ++j) pr.emplace_back(d->cell_dofs[c * N + j], j * B + cl);
         }
         std::sort(pr.begin(), pr.end());
@@ -627,7 +656,7 @@ int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total) {
   if ((rc = upload(&P->blk_ioff, ioff.data(), ioff.size(), total))) return rc;
   if (d->kappa) {
     std::vector<double> kp(n);
-    for (int64_t i = 0; i < n; ++i) kp[i] = d->kappa[key[i].second];
+    for (int64_t i = 0; i < n; ++i) kp[i] = d->kappa[order[i]];
     if ((rc = upload(&P->blk_kappa, kp.data(), kp.size(), total))) return rc;
   }
   P->blk_B = B;
@@ -694,6 +723,9 @@ int tmf_apply_stages(tmf_plan* P, const double* u, double* y, int stages, int64_
   if (!P || !u || !y) return fail(TMF_EINVAL, "null argument");
   if (cell_begin < 0 || cell_end > P->n_cells || cell_begin > cell_end)
     return fail(TMF_EINVAL, "bad cell range");
+  if (P->cell_perm && (stages & TMF_STAGE_CELLS) && cell_end > cell_begin && (cell_begin != 0 || cell_end != P->n_cells))
+    return fail(TMF_EINVAL, "the plan traverses cells in its own (Morton) order: cell ranges need the caller's "
+                            "order (flags bits 22-23 = 1, OperatorConfig(cell_order='input'))");
   if (P->peer.u && (u != P->peer_self_u || (!P->dg && y != P->peer_self_y)))
     return fail(TMF_EINVAL, "with peers, u (and y for CG) must be this rank's registered buffers");
   TMF_CUDA(cudaSetDevice(P->dev));
@@ -814,8 +846,38 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   size_t total = 0;
   int rc;
   if ((rc = upload(&P->verts, d->vertices, 3 * d->n_vertices, &total))) return bail(rc);
-  if ((rc = upload(&P->cells, d->cells, 4 * d->n_cells, &total))) return bail(rc);
-  if (d->kappa && (rc = upload(&P->kappa, d->kappa, d->n_cells, &total))) return bail(rc);
+  // CG traversal order: auto takes the Morton order of the centroids when the caller's cell
+  // order has no locality (mean centroid distance of consecutive cells > 2x the Morton order's:
+  // a randomly permuted mesh), keeps the caller's order otherwise (a locality-ordered mesh is
+  // as fast or faster, its DoF numbering following it; profiles/r02/cell_order.jsonl)
+  std::vector<int64_t> order;
+  {
+    const int mode = (d->flags >> 22) & 3;
+    if (!dg && mode != 1) {
+      order = morton_order(d);
+      if (mode == 0 && !(consecutive_distance(d, nullptr) > 2.0 * consecutive_distance(d, order.data())))
+        order.clear();
+    }
+    P->cell_perm = !order.empty();
+    P->info.cell_order = dg ? 0 : (P->cell_perm ? 2 : 1);
+  }
+  std::vector<int32_t> cells_p;
+  std::vector<double> kappa_p;
+  const int32_t* cells_in = d->cells;
+  const double* kappa_in = d->kappa;
+  if (P->cell_perm) {
+    cells_p.resize((size_t)4 * d->n_cells);
+    for (int64_t i = 0; i < d->n_cells; ++i)
+      for (int k = 0; k < 4; ++k) cells_p[4 * i + k] = d->cells[4 * order[i] + k];
+    cells_in = cells_p.data();
+    if (d->kappa) {
+      kappa_p.resize(d->n_cells);
+      for (int64_t i = 0; i < d->n_cells; ++i) kappa_p[i] = d->kappa[order[i]];
+      kappa_in = kappa_p.data();
+    }
+  }
+  if ((rc = upload(&P->cells, cells_in, 4 * d->n_cells, &total))) return bail(rc);
+  if (kappa_in && (rc = upload(&P->kappa, kappa_in, d->n_cells, &total))) return bail(rc);
 
   // cell tables -> fragments
   {
@@ -881,7 +943,8 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   if (!dg) {
     std::vector<int> enc((size_t)d->n_cells * P->N);
     for (int64_t i = 0; i < (int64_t)enc.size(); ++i) {
-      const int g = d->cell_dofs[i];
+      const int64_t c = P->cell_perm ? order[i / P->N] : i / P->N;
+      const int g = d->cell_dofs[c * P->N + i % P->N];
       if (g < 0 || g >= d->n_scalar_dofs) return bail(fail(TMF_EINVAL, "cell dof out of range"));
       enc[i] = (d->dirichlet_mask && d->dirichlet_mask[g]) ? ~g : g;
     }
@@ -1127,6 +1190,8 @@ int tmf_plan_set_peers(tmf_plan* P, int32_t n_ranks, const uint64_t* peer_u, con
                        int32_t self_rank, int64_t n_own, int64_t n_ghost, const int32_t* ghost_rank,
                        const int32_t* ghost_index, int64_t n_peer_free_cells) {
   if (!P) return fail(TMF_EINVAL, "null plan");
+  if (P->cell_perm)
+    return fail(TMF_EINVAL, "peers need the caller's cell order (OperatorConfig(cell_order='input'))");
   TMF_CUDA(cudaSetDevice(P->dev));
   for (void* q : {(void*)P->peer_u_tab, (void*)P->peer_y_tab, (void*)P->ghost_rank, (void*)P->ghost_index})
     if (q) cudaFree(q);

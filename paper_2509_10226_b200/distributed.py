@@ -547,8 +547,9 @@ class DistributedCgOperator(_PeerTransport):
         ldm = DoFMap("cg", dofmap.degree, 1, n_local, self.sub.cell_dofs, self.sub.dirichlet_mask)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         if local_factory is None:
+            # the halo overlap runs cell RANGES (interior cells first): the caller's order
             op = CgPoissonOperator(self.sub.mesh, ldm, geometry, basis,
-                                   OperatorConfig(device=self.device.index or 0))
+                                   OperatorConfig(device=self.device.index or 0, cell_order="input"))
             self.local_op = op
 
             def local(u, y):

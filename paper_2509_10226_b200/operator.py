@@ -37,6 +37,7 @@ __all__ = ["OperatorConfig", "SipgConfig", "HelmholtzCoefficients", "CgPoissonOp
 _STAGES = ("ref", "data", "mm", "sched")
 _ENGINES = {"auto": 0, "dmma": 1, "tensor": 3, "modal": 4}
 _BLOCKS = {"auto": 0, "off": 1, "on": 2}
+_ORDERS = {"auto": 0, "input": 1, "morton": 2}
 _FACE_ENGINES = {"auto": 0, "quadrature": 1, "modal": 3}
 
 
@@ -60,6 +61,7 @@ class OperatorConfig:
     cell_blocks: str = "auto"    # B200 CG block assembly (low degrees on locality-ordered meshes): auto | off | on
     face_engine: str = "auto"    # B200 faces: auto (modal at P2-P4) | quadrature (points) | modal
     f32_mirror: bool = False     # B200 CG Laplace: also build the fp32 apply (apply_f32; mixed-precision multigrid)
+    cell_order: str = "auto"     # B200 CG traversal: auto (Morton when the mesh order has no locality) | input | morton
 
     def __post_init__(self):
         if self.kernel_stage not in _STAGES:
@@ -72,6 +74,8 @@ class OperatorConfig:
             raise ValueError(f"unknown cell engine {self.cell_engine!r}")
         if self.cell_blocks not in _BLOCKS:
             raise ValueError(f"unknown cell block mode {self.cell_blocks!r}")
+        if self.cell_order not in _ORDERS:
+            raise ValueError(f"unknown cell order {self.cell_order!r}")
         if self.face_engine not in _FACE_ENGINES:
             raise ValueError(f"unknown face engine {self.face_engine!r}")
         if self.backend not in ("auto", "compiled", "python", "b200"):
@@ -215,7 +219,8 @@ class _B200Operator:
             ((eng & 3) << 13) | ((eng >> 2) << 19) | \
             (_BLOCKS[getattr(self.config, "cell_blocks", "auto")] << 15) | \
             (_FACE_ENGINES[getattr(self.config, "face_engine", "auto")] << 17) | \
-            ((1 if (getattr(self.config, "f32_mirror", False) or self.precision == "f32") else 0) << 20)
+            ((1 if (getattr(self.config, "f32_mirror", False) or self.precision == "f32") else 0) << 20) | \
+            (_ORDERS[getattr(self.config, "cell_order", "auto")] << 22)
         _lib.check(_lib.lib().tmf_plan_create(C.byref(d), C.byref(self._plan)))
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().tmf_plan_get_info(self._plan, C.byref(info)))

@@ -93,3 +93,42 @@ def test_gpu_block_assembly_matches_golden(name):
     for A in (on, off):
         err = rel_l2(A.apply(g["u"]), g["y"])
         assert err <= TOL, f"{name}: rel L2 {err:.3e}"
+
+
+@pytest.mark.parametrize("order", ["input", "morton"])
+@pytest.mark.parametrize("name", [n for n in golden_names("cg")])
+def test_gpu_cell_traversal_order_matches_golden(name, order):
+    """CG plans traverse cells in the caller's order or in the Morton order of the centroids
+    (OperatorConfig.cell_order); u / y keep the caller's numbering, results are the same."""
+    g = load_golden(name)
+    A = operator_from_fixture(g, cell_order=order)
+    assert A.info["cell_order"] == {"input": 1, "morton": 2}[order]
+    err = rel_l2(A.apply(g["u"]), g["y"])
+    assert err <= TOL, f"{name}/{order}: rel L2 {err:.3e}"
+
+
+def test_gpu_cell_order_auto_and_ranges():
+    """auto picks Morton for a randomly permuted mesh and keeps a locality-ordered one; a
+    Morton plan refuses partial cell ranges (the multi-GPU stages need the caller's order)."""
+    import torch
+
+    from paper_2509_10226_b200 import _lib, basis as B, dofmap as D, mesh as M, operator as op, quadrature as Q
+    from paper_2509_10226_b200.geometry import GeometryData
+    from paper_2509_10226_b200.reorder import reorder_mesh
+
+    p = 2
+    cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
+    bas = B.tabulate_basis(p, cr, fr)
+    geo = GeometryData("affine", cr, fr, None, None, None, None)
+    m = M.kuhn_cube_mesh(10, seed=0)
+    A = op.CgPoissonOperator(m, D.build_dof_map(m, p, "cg"), geo, bas)
+    assert A.info["cell_order"] == 2
+    mr = reorder_mesh(m)
+    assert op.CgPoissonOperator(mr, D.build_dof_map(mr, p, "cg"), geo, bas).info["cell_order"] == 1
+    u = torch.rand(A.n_global_dofs, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(u)
+    with pytest.raises(ValueError, match="cell ranges"):
+        A.apply_stages(u.data_ptr(), y.data_ptr(), _lib.STAGE_CELLS, 0, 10)
+    A.apply_stages(u.data_ptr(), y.data_ptr(), _lib.STAGE_ZERO | _lib.STAGE_CELLS | _lib.STAGE_FIXUP)
+    torch.cuda.synchronize()
+    assert rel_l2(y.cpu().numpy(), A.apply(u).cpu().numpy()) <= 1e-14
