@@ -281,11 +281,6 @@ struct tmf_plan {
   uint16_t* blk_inc = nullptr;
   uint16_t* blk_ioff = nullptr;
   double* blk_kappa = nullptr;
-  bool blk_pipe = false;           // the pipelined block-DMMA kernel (flags bits 15-16 = 3)
-  int4* blk_head = nullptr;        //   per block {uniq offset, nu, nv, ioff offset}, 16-B aligned segments
-  int* blk_uniq2 = nullptr;
-  uint16_t* blk_ioff2 = nullptr;
-  double* blk_frags = nullptr;     //   modal DMMA fragments of blk_tab
   // multi-GPU peer-memory ghost access (tmf_plan_set_peers)
   tmf::PeerArgs peer{};
   const double** peer_u_tab = nullptr;   // device arrays of device pointers
@@ -364,31 +359,6 @@ struct tmf_plan {
 #endif
     return a;
   }
-  tmf::BpipeArgs bpipe_args(const double* u, double* y, double* energy) const {
-    tmf::BpipeArgs a{};
-    a.u = u;
-    a.y = y;
-    a.verts = verts;
-    a.kappa = blk_kappa;
-    a.frags = blk_frags;
-    a.head = blk_head;
-    a.uniq = blk_uniq2;
-    a.loc = blk_loc;
-    a.inc = blk_inc;
-    a.ioff = blk_ioff2;
-    a.n_cells = n_cells;
-    a.n_blocks = blk_n;
-    a.numax = blk_numax;
-    a.nvmax = blk_nvmax;
-    a.scale = stiff_scale;
-    a.energy = energy;
-#ifdef TMF_DEBUG_CHECKS
-    a.dbg_n_dofs = n_global;
-    a.dbg_n_cells = n_cells;
-    a.dbg_flag = dbg_flag;
-#endif
-    return a;
-  }
   tmf::FaceArgs face_args(const double* u, double* y, bool boundary) const {
     tmf::FaceArgs a{};
     a.u = u;
@@ -432,7 +402,6 @@ struct tmf_plan {
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
                     (void*)f32_rows, (void*)f32_geo, (void*)blk_off, (void*)blk_nv, (void*)blk_uniq,
                     (void*)blk_loc, (void*)blk_inc, (void*)blk_ioff, (void*)blk_kappa, (void*)dbg_flag,
-                    (void*)blk_head, (void*)blk_uniq2, (void*)blk_ioff2, (void*)blk_frags,
                     (void*)peer_u_tab, (void*)peer_y_tab, (void*)ghost_rank, (void*)ghost_index})
       if (p) cudaFree(p);
   }
@@ -617,7 +586,7 @@ double consecutive_distance(const tmf_plan_desc* d, const int64_t* order) {
 // the slots of every unique DoF (u16 j*B + cl, in slot order) with their offsets.
 // Returns TMF_OK with P->blk_B = 0 when the plan does not qualify (vertex DoFs are not the
 // vertex ids, or a block does not fit in shared memory).
-int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total, bool pipe) {
+int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total) {
   const int N = P->N, NP = (N + 3) & ~3;
   const int64_t n = P->n_cells;
   for (int64_t c = 0; c < n; ++c)
@@ -628,7 +597,7 @@ int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total, bool
   std::vector<std::vector<int>> uq(nb);
   std::vector<std::vector<uint16_t>> io(nb);
   std::vector<int> nvb(nb);
-  std::vector<uint16_t> loc((size_t)n * NP + 16, 0), inc((size_t)nb * B * N + 16, 0);
+  std::vector<uint16_t> loc((size_t)n * NP, 0), inc((size_t)nb * B * N + 8, 0);
   const int nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
   std::vector<std::thread> pool;
   for (int t = 0; t < nth; ++t)
@@ -671,9 +640,7 @@ int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total, bool
     numax = std::max(numax, (int)uq[b].size());
     nvmax = std::max(nvmax, nvb[b]);
   }
-  if (numax > 65535) return TMF_OK;
-  if (!pipe && tmf::block_smem_bytes(N, B, numax, nvmax) > 227 * 1024) return TMF_OK;
-  if (pipe && tmf::pipe_smem_bytes(N, numax, nvmax) > 227 * 1024) return TMF_OK;
+  if (numax > 65535 || tmf::block_smem_bytes(N, B, numax, nvmax) > 227 * 1024) return TMF_OK;
   uniq.reserve(off[nb]);
   ioff.reserve(off[nb] + nb);
   for (int64_t b = 0; b < nb; ++b) {
@@ -687,30 +654,6 @@ int build_blocks(tmf_plan* P, const tmf_plan_desc* d, int B, size_t* total, bool
   if ((rc = upload(&P->blk_loc, loc.data(), loc.size(), total))) return rc;
   if ((rc = upload(&P->blk_inc, inc.data(), inc.size(), total))) return rc;
   if ((rc = upload(&P->blk_ioff, ioff.data(), ioff.size(), total))) return rc;
-  if (pipe) {
-    // per-block segments starting 16-byte aligned (the kernel's copies are 16-byte cp.async)
-    std::vector<int4> head(nb);
-    std::vector<int> uq2;
-    std::vector<uint16_t> io2;
-    for (int64_t b = 0; b < nb; ++b) {
-      head[b] = make_int4((int)uq2.size(), (int)uq[b].size(), nvb[b], (int)io2.size());
-      uq2.insert(uq2.end(), uq[b].begin(), uq[b].end());
-      uq2.resize((uq2.size() + 3) & ~(size_t)3, 0);
-      io2.insert(io2.end(), io[b].begin(), io[b].end());
-      io2.resize((io2.size() + 7) & ~(size_t)7, 0);
-    }
-    uq2.resize(uq2.size() + 4, 0);
-    io2.resize(io2.size() + 8, 0);
-    if ((rc = upload(&P->blk_head, head.data(), head.size(), total))) return rc;
-    if ((rc = upload(&P->blk_uniq2, uq2.data(), uq2.size(), total))) return rc;
-    if ((rc = upload(&P->blk_ioff2, io2.data(), io2.size(), total))) return rc;
-    const int p = P->degree, M = p * (p + 1) * (p + 2) / 6;
-    std::vector<double> ones(M, 1.0), fr;
-    const std::vector<double>& E = P->blk_tab;
-    build_fragments(N, M, 3, [&](int c, int q, int j) { return E[(size_t)(3 * q + c) * N + j]; }, ones.data(), fr);
-    if ((rc = upload(&P->blk_frags, fr.data(), fr.size(), total))) return rc;
-    P->blk_pipe = true;
-  }
   if (d->kappa) {
     std::vector<double> kp(n);
     for (int64_t i = 0; i < n; ++i) kp[i] = d->kappa[order[i]];
@@ -747,9 +690,7 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
   bool ok = true;
   if (ev) TMF_CUDA(cudaEventRecord(ev[0], st));
   if (!P->dg && !y_zeroed) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
-  if (P->blk_B && !P->peer.u && P->blk_pipe) {
-    TMF_CUDA(tmf::launch_cell_bpipe(P->N, P->bpipe_args(u, y, energy), P->n_sm, st));
-  } else if (P->blk_B && !P->peer.u) {
+  if (P->blk_B && !P->peer.u) {
     TMF_CUDA(tmf::launch_cell_block(P->N, P->block_args(u, y, energy), P->blk_tab.data(), st));
   } else {
     tmf::CellArgs ca = P->cell_args(u, y);
@@ -1010,24 +951,20 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     if ((rc = upload(&P->dofs, enc.data(), enc.size(), &total))) return bail(rc);
     // block assembly for the scalar Laplace at P1-P3 (flags bits 15-16: 0 auto = on, 1 off, 2 on);
     // the tile kernels stay built for the multi-GPU stages (peer ghosts, cell ranges)
-    // modes: 0 auto, 1 off, 2 thread-per-cell block kernel (P1-P2), 3 pipelined block-DMMA
-    // kernel (P1-P3)
     P->blocks_mode = (d->flags >> 15) & 3;
+    const int Bc = tmf::block_cells_for(P->N);
     const int req_engine = ((d->flags >> 13) & 3) | (((d->flags >> 19) & 1) << 2);
     // auto: P1 only (48^3: 28 vs 31-33 us per apply for the tensor tile kernel; at P2 the modal
     // tile kernel is as fast or faster, 54-63 vs 59-67 us; profiles/r02/block_assembly.jsonl)
-    int mode = P->blocks_mode;
-    if (mode == 0) mode = (req_engine == 0 && P->N == 4) ? 2 : 1;
-    const bool pipe = mode == 3;
-    const int Bc = pipe ? tmf::pipe_cells_for(P->N) : mode == 2 ? tmf::block_cells_for(P->N) : 0;
-    if (Bc > 0 && P->nc == 1 && !P->mass && (req_engine == 0 || req_engine == 4)) {
+    const bool want = P->blocks_mode == 2 || (P->blocks_mode == 0 && req_engine == 0 && P->N == 4);
+    if (want && Bc > 0 && P->nc == 1 && !P->mass && (req_engine == 0 || req_engine == 4)) {
       const int p = P->degree, M = p * (p + 1) * (p + 2) / 6;
       if (build_modal_cell_tables(P->N, P->Q, M, d->grad_matrix, d->cell_weights, P->blk_tab)) {
-        if ((rc = build_blocks(P, d, Bc, &total, pipe))) return bail(rc);
-        if (P->blk_B) P->info.cell_engine = pipe ? 6 : 5;
+        if ((rc = build_blocks(P, d, Bc, &total))) return bail(rc);
+        if (P->blk_B) P->info.cell_engine = 5;
       }
     }
-    if (P->blocks_mode >= 2 && !P->blk_B)
+    if (P->blocks_mode == 2 && !P->blk_B)
       return bail(fail(TMF_EINVAL, "block assembly requested but the plan does not qualify (scalar CG "
                                    "Laplace at P1-P3 with the reference DoF numbering, modal or auto engine)"));
     std::vector<int> fix;
@@ -1218,7 +1155,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       fe -= nce * (12.0 * nq * nd + 33.0 * nq);
       fe += nce * (12.0 * nd * nd + 12.0 * nd);
       if (P->mass) fe += nce * (2.0 * nd * nd + 2.0 * nd) - nce * (4.0 * nq * nd + 5.0 * nq + nd);
-    } else if (P->info.cell_engine >= 4) {
+    } else if (P->info.cell_engine == 4 || P->info.cell_engine == 5) {
       // the point loop on M unit-weight modes: 12 M N (both GEMMs) + 18 M (G action)
       const double M = P->degree * (P->degree + 1) * (P->degree + 2) / 6;
       fe -= nce * (12.0 * nq * nd + 33.0 * nq);
@@ -1353,7 +1290,6 @@ int tmf_debug_poke_dof(tmf_plan* P, int64_t slot, int32_t value) {
   TMF_CUDA(cudaMemcpy(P->dofs + slot, &value, sizeof(int32_t), cudaMemcpyHostToDevice));
   // the block-assembly tables are derived at plan creation: take the tile kernel from now on
   P->blk_B = 0;
-  P->blk_pipe = false;
   return TMF_OK;
 #else
   (void)P;

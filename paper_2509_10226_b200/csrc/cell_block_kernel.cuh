@@ -29,7 +29,6 @@
 #pragma once
 #include <cstdint>
 
-#include "cell_kernel.cuh"
 #include "common.cuh"
 
 namespace tmf {
@@ -213,341 +212,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_block_kernel(BlockArgs a, co
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) en += __shfl_xor_sync(0xffffffffu, en, o);
     if ((threadIdx.x & 31) == 0 && en != 0.0) atomicAdd(a.energy, en);
-  }
-}
-
-
-// ===================================================================================
-// Pipelined block assembly on FP64 tensor cores: cell_bpipe_kernel
-//
-// The same three phases as cell_block_kernel (unique-DoF gather, per-cell work, per-DoF
-// reduction + one RED), with the per-cell work done by the modal DMMA tile of
-// cell_kernel.cuh (8 cells per warp tile, A fragments read from the block's staged u,
-// G from a per-block shared array), and the block's global loads PIPELINED across the
-// blocks a persistent CTA walks:
-//   contiguous data (unique DoFs, local indices, slot lists, offsets) of block k+2 and the
-//   indirect gathers (u, vertex coordinates) of block k+1 are in flight, as cp.async
-//   groups, while block k computes -- 3 stages of contiguous data, 2 of gathered data.
-// Host layout (capi.cu build_blocks): per block a header {uniq offset, nu, nv, ioff offset}
-// whose segments start 16-byte aligned, so every contiguous copy is 16-byte cp.async.
-// ===================================================================================
-
-struct BpipeLayout {
-  int numax, nvmax, B, N, NP, NFRAG;
-  // byte offsets in dynamic shared memory
-  __host__ __device__ static int r16(int x) { return (x + 15) & ~15; }
-  __host__ __device__ int frag_bytes() const { return NFRAG * 32 * 8; }
-  __host__ __device__ int rstride() const { return B + 2; }   // doubles per R row (bank spread)
-  __host__ __device__ int r_bytes() const { return N * rstride() * 8; }
-  __host__ __device__ int g_bytes() const { return B * 6 * 8; }
-  __host__ __device__ int gath_bytes() const { return r16((numax + 3 * nvmax) * 8); }
-  __host__ __device__ int uq_bytes() const { return r16(numax * 4); }
-  __host__ __device__ int loc_bytes() const { return r16(B * NP * 2); }
-  __host__ __device__ int inc_bytes() const { return r16(B * N * 2); }
-  __host__ __device__ int io_bytes() const { return r16((numax + 1) * 2); }
-  __host__ __device__ int cont_bytes() const { return uq_bytes() + loc_bytes() + inc_bytes() + io_bytes(); }
-  __host__ __device__ int off_r() const { return frag_bytes(); }
-  __host__ __device__ int off_g() const { return off_r() + r_bytes(); }
-  __host__ __device__ int off_gath(int s) const { return off_g() + g_bytes() + s * gath_bytes(); }
-  __host__ __device__ int off_cont(int s) const { return off_gath(2) + s * cont_bytes(); }
-  __host__ __device__ int total() const { return off_cont(3); }
-};
-
-struct BpipeArgs {
-  const double* __restrict__ u;
-  double* __restrict__ y;
-  const double* __restrict__ verts;
-  const double* __restrict__ kappa;     // per processed cell (plan order), or nullptr
-  const double* __restrict__ frags;     // modal DMMA fragments (CellShape<N, M, false> layout)
-  const int4* __restrict__ head;        // (n_blocks): {uniq offset, nu, nv, ioff offset}, offsets 16-B aligned
-  const int* __restrict__ uniq;         // global DoF, ~g for Dirichlet DoFs
-  const uint16_t* __restrict__ loc;     // (n_cells, NP) local DoF index per slot, processing order
-  const uint16_t* __restrict__ inc;     // block b's B*N slot ids (j*B + cl), grouped by unique DoF
-  const uint16_t* __restrict__ ioff;    // block b: nu_b + 1 offsets into its slot list
-  int64_t n_cells;
-  int64_t n_blocks;
-  int numax, nvmax;
-  double scale;
-  double* energy;
-  TMF_DBG_FIELDS
-};
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(ok ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-template <int N, int M, int BLOCK, int B>
-__global__ void __launch_bounds__(BLOCK, 1) cell_bpipe_kernel(BpipeArgs a) {
-  using S = CellShape<N, M, false>;
-  constexpr int NP = BlockShape<N>::NP;
-  constexpr int MT = S::MT;
-  constexpr int NT = B / 8;                   // 8-cell tiles per block
-  constexpr int NW = BLOCK / 32;
-  static_assert(B % 8 == 0 && (B & (B - 1)) == 0, "block size");
-  extern __shared__ __align__(16) unsigned char sm[];
-  const BpipeLayout L{a.numax, a.nvmax, B, N, NP, S::NFRAG};
-  double* sF = reinterpret_cast<double*>(sm);
-  double* sR = reinterpret_cast<double*>(sm + L.off_r());
-  double* sG = reinterpret_cast<double*>(sm + L.off_g());
-  constexpr int RS = B + 2;
-  {
-    const double2* src = reinterpret_cast<const double2*>(a.frags);
-    double2* dst = reinterpret_cast<double2*>(sF);
-    for (int i = threadIdx.x; i < S::NFRAG * 16; i += BLOCK) dst[i] = __ldg(src + i);
-  }
-  const double* sB1 = sF;
-  const double* sB2 = sF + S::NB1 * 32;
-  auto cont_uq = [&](int s) { return reinterpret_cast<int*>(sm + L.off_cont(s)); };
-  auto cont_loc = [&](int s) { return reinterpret_cast<uint16_t*>(sm + L.off_cont(s) + L.uq_bytes()); };
-  auto cont_inc = [&](int s) {
-    return reinterpret_cast<uint16_t*>(sm + L.off_cont(s) + L.uq_bytes() + L.loc_bytes());
-  };
-  auto cont_io = [&](int s) {
-    return reinterpret_cast<uint16_t*>(sm + L.off_cont(s) + L.uq_bytes() + L.loc_bytes() + L.inc_bytes());
-  };
-  auto gath_u = [&](int s) { return reinterpret_cast<double*>(sm + L.off_gath(s)); };
-  auto gath_x = [&](int s) { return reinterpret_cast<double*>(sm + L.off_gath(s)) + a.numax; };
-
-  // contiguous data of block b into stage s (16-byte copies; the host pads every segment)
-  auto issue_cont = [&](int64_t b, int s) {
-    const int4 h = __ldg(a.head + b);
-    const int64_t c0 = b * B;
-    const int ncb = (int)(a.n_cells - c0 < B ? a.n_cells - c0 : B);
-    const int nu = h.y;
-    {
-      const int n16 = (nu + 3) / 4;
-      const int4* src = reinterpret_cast<const int4*>(a.uniq + h.x);
-      int4* dst = reinterpret_cast<int4*>(cont_uq(s));
-      for (int i = threadIdx.x; i < n16; i += BLOCK) cp_async16(dst + i, src + i);
-    }
-    {
-      const int n16 = (ncb * NP * 2 + 15) / 16;
-      const int4* src = reinterpret_cast<const int4*>(a.loc + c0 * NP);
-      int4* dst = reinterpret_cast<int4*>(cont_loc(s));
-      for (int i = threadIdx.x; i < n16; i += BLOCK) cp_async16(dst + i, src + i);
-    }
-    {
-      const int n16 = (ncb * N * 2 + 15) / 16;
-      const int4* src = reinterpret_cast<const int4*>(a.inc + b * (int64_t)B * N);
-      int4* dst = reinterpret_cast<int4*>(cont_inc(s));
-      for (int i = threadIdx.x; i < n16; i += BLOCK) cp_async16(dst + i, src + i);
-    }
-    {
-      const int n16 = ((nu + 1) * 2 + 15) / 16;
-      const int4* src = reinterpret_cast<const int4*>(a.ioff + h.w);
-      int4* dst = reinterpret_cast<int4*>(cont_io(s));
-      for (int i = threadIdx.x; i < n16; i += BLOCK) cp_async16(dst + i, src + i);
-    }
-  };
-  // indirect gathers of block b (its unique DoFs in contiguous stage sc) into gather stage sg
-  auto issue_gath = [&](int64_t b, int sc, int sg) {
-    const int4 h = __ldg(a.head + b);
-    const int* uq = cont_uq(sc);
-    double* us = gath_u(sg);
-    double* xs = gath_x(sg);
-    for (int i = threadIdx.x; i < h.y; i += BLOCK) {
-      const int e = uq[i];
-      const int g = e < 0 ? ~e : e;
-      TMF_CHECK(a, g < a.dbg_n_dofs && h.y <= a.numax && h.z <= a.nvmax, TMF_DBG_DOF);
-      cp_async8(us + i, a.u + g, e >= 0);
-      if (i < h.z) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) cp_async8(xs + 3 * i + k, a.verts + 3 * (int64_t)g + k, true);
-      }
-    }
-  };
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int cs = lane >> 2, q4 = lane & 3;
-  double en = 0.0;
-  const int64_t b0 = blockIdx.x, bstep = gridDim.x;
-  // prologue: contiguous data of the first two blocks, the gathers of the first
-  if (b0 < a.n_blocks) issue_cont(b0, 0);
-  cp_commit();
-  if (b0 + bstep < a.n_blocks) issue_cont(b0 + bstep, 1);
-  cp_commit();
-  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-  __syncthreads();
-  if (b0 < a.n_blocks) issue_gath(b0, 0, 0);
-  cp_commit();
-
-  int k = 0;
-  for (int64_t b = b0; b < a.n_blocks; b += bstep, ++k) {
-    const int sc = k % 3, sg = k & 1;
-    cp_wait_all();       // this block's gathers and the next block's contiguous data
-    __syncthreads();
-    if (b + bstep < a.n_blocks) issue_gath(b + bstep, (k + 1) % 3, sg ^ 1);
-    cp_commit();
-    if (b + 2 * bstep < a.n_blocks) issue_cont(b + 2 * bstep, (k + 2) % 3);
-    cp_commit();
-
-    const int4 h = __ldg(a.head + b);
-    const int64_t c0 = b * B;
-    const int ncb = (int)(a.n_cells - c0 < B ? a.n_cells - c0 : B);
-    const uint16_t* loc = cont_loc(sc);
-    const double* us = gath_u(sg);
-    const double* xs = gath_x(sg);
-
-    // ---- geometry: G per cell from its 4 staged vertices
-    for (int cl = threadIdx.x; cl < ncb; cl += BLOCK) {
-      const uint16_t* l = loc + cl * NP;
-      Vec3 x[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        TMF_CHECK(a, l[i] < h.z, TMF_DBG_LOCAL);
-        x[i] = Vec3{xs[3 * l[i]], xs[3 * l[i] + 1], xs[3 * l[i] + 2]};
-      }
-      Affine g;
-      affine_from_vertices(x[0], x[1], x[2], x[3], g);
-      double G[6];
-      stiffness_metric(g, a.kappa ? a.scale * __ldg(a.kappa + c0 + cl) : a.scale, G);
-      double2* o = reinterpret_cast<double2*>(sG + 6 * cl);
-      o[0] = make_double2(G[0], G[1]);
-      o[1] = make_double2(G[2], G[3]);
-      o[2] = make_double2(G[4], G[5]);
-    }
-    __syncthreads();
-
-    // ---- DMMA tiles: 8 cells per warp tile, MT tiles per warp iteration
-    for (int st = warp; st * MT < NT; st += NW) {
-      int cell[MT];
-      bool valid[MT];
-      double av[MT][S::KK], G[MT][6];
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        cell[m] = (st * MT + m) * 8 + cs;
-        valid[m] = (st * MT + m) < NT && cell[m] < ncb;
-        const int cl = valid[m] ? cell[m] : 0;
-#pragma unroll
-        for (int kk = 0; kk < S::KK; ++kk) {
-          const int j = 4 * kk + q4;
-          double v = 0.0;
-          if (valid[m] && j < N) {
-            const int li = loc[cl * NP + j];
-            TMF_CHECK(a, li < h.y, TMF_DBG_LOCAL);
-            v = us[li];
-          }
-          av[m][kk] = v;
-        }
-        const double2* gp = reinterpret_cast<const double2*>(sG + 6 * cl);
-        const double2 g01 = gp[0], g23 = gp[1], g45 = gp[2];
-        G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
-        G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
-      }
-      double yacc[MT][S::NJ][2];
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-#pragma unroll
-        for (int nj = 0; nj < S::NJ; ++nj) yacc[m][nj][0] = yacc[m][nj][1] = 0.0;
-      auto dact = [&](int m, double g0, double g1, double g2, double& d0, double& d1, double& d2) {
-        d0 = G[m][0] * g0 + G[m][1] * g1 + G[m][2] * g2;
-        d1 = G[m][1] * g0 + G[m][3] * g1 + G[m][4] * g2;
-        d2 = G[m][2] * g0 + G[m][4] * g1 + G[m][5] * g2;
-        en = fma(g0, d0, fma(g1, d1, fma(g2, d2, en)));
-      };
-#pragma unroll
-      for (int t = 0; t < S::T; ++t) {
-        double v[MT][3][2];
-#pragma unroll
-        for (int m = 0; m < MT; ++m)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) v[m][c][0] = v[m][c][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < S::KK; ++kk)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const double bb = sB1[((t * 3 + c) * S::KK + kk) * 32 + lane];
-#pragma unroll
-            for (int m = 0; m < MT; ++m) dmma(v[m][c], av[m][kk], bb);
-          }
-        double d[MT][3][2];
-#pragma unroll
-        for (int m = 0; m < MT; ++m)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) dact(m, v[m][0][i], v[m][1][i], v[m][2][i], d[m][0][i], d[m][1][i], d[m][2][i]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int nj = 0; nj < S::NJ; ++nj) {
-              const double bb = sB2[(((t * 3 + c) * 2 + i) * S::NJ + nj) * 32 + lane];
-#pragma unroll
-              for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][c][i], bb);
-            }
-      }
-      if (S::GRP) {
-        double v[MT][2][2];
-#pragma unroll
-        for (int m = 0; m < MT; ++m) v[m][0][0] = v[m][0][1] = v[m][1][0] = v[m][1][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < S::KK; ++kk)
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const double bb = sB1[(S::NB1T + hh * S::KK + kk) * 32 + lane];
-#pragma unroll
-            for (int m = 0; m < MT; ++m) dmma(v[m][hh], av[m][kk], bb);
-          }
-        double d[MT][3];
-#pragma unroll
-        for (int m = 0; m < MT; ++m) dact(m, v[m][0][0], v[m][0][1], v[m][1][0], d[m][0], d[m][1], d[m][2]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int nj = 0; nj < S::NJ; ++nj) {
-            const double bb = sB2[(S::NB2T + c * S::NJ + nj) * 32 + lane];
-#pragma unroll
-            for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][c], bb);
-          }
-      }
-      // lane owns output DoFs 8nj + 2q4 + {0,1} of its cell: to the slot array
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        if (!valid[m]) continue;
-#pragma unroll
-        for (int nj = 0; nj < S::NJ; ++nj)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int j = 8 * nj + 2 * q4 + i;
-            if (j < N) sR[j * RS + cell[m]] = yacc[m][nj][i];
-          }
-      }
-    }
-    __syncthreads();
-
-    // ---- one thread per unique DoF: its slots in list order, one RED
-    {
-      const int* uq = cont_uq(sc);
-      const uint16_t* sinc = cont_inc(sc);
-      const uint16_t* sio = cont_io(sc);
-      for (int i = threadIdx.x; i < h.y; i += BLOCK) {
-        const int e = uq[i];
-        if (e < 0) continue;
-        double s = 0.0;
-        TMF_CHECK(a, sio[i] <= sio[i + 1] && sio[i + 1] <= ncb * N, TMF_DBG_SLOT);
-        for (int q = sio[i]; q < sio[i + 1]; ++q) {
-          const int slot = sinc[q];
-          TMF_CHECK(a, slot < N * B && (slot & (B - 1)) < ncb, TMF_DBG_SLOT);
-          s += sR[(slot / B) * RS + (slot & (B - 1))];
-        }
-        atomicAdd(a.y + e, s);
-      }
-    }
-    __syncthreads();     // stage sc / sg, sG and sR are free for the next blocks
-  }
-  cp_wait_all();
-  if (a.energy != nullptr) {
-    // DMMA lanes accumulate two points' g.(G g) per 8-point tile once; the geometry threads none
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) en += __shfl_xor_sync(0xffffffffu, en, o);
-    if (lane == 0 && en != 0.0) atomicAdd(a.energy, en);
   }
 }
 

@@ -10,7 +10,6 @@ struct FaceArgs;
 struct FaceGeoArgs;
 struct CellGeoArgs;
 struct BlockArgs;
-struct BpipeArgs;
 
 struct CellLaunchInfo {
   int dmma_per_tile = 0;
@@ -42,10 +41,6 @@ cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st
 // and the launch (host_tab: the M x 3 x n_dpc modal table, passed as a kernel parameter)
 int block_cells_for(int n_dpc);
 cudaError_t launch_cell_block(int n_dpc, const BlockArgs& a, const double* host_tab, cudaStream_t st);
-// pipelined block-DMMA variant (cell_bpipe_kernel): cells per block, shared memory, launch
-int pipe_cells_for(int n_dpc);
-size_t pipe_smem_bytes(int n_dpc, int numax, int nvmax);
-cudaError_t launch_cell_bpipe(int n_dpc, const BpipeArgs& a, int n_sm, cudaStream_t st);
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
                          cudaStream_t st, double* energy = nullptr);
 

@@ -132,14 +132,3 @@ def test_gpu_cell_order_auto_and_ranges():
     A.apply_stages(u.data_ptr(), y.data_ptr(), _lib.STAGE_ZERO | _lib.STAGE_CELLS | _lib.STAGE_FIXUP)
     torch.cuda.synchronize()
     assert rel_l2(y.cpu().numpy(), A.apply(u).cpu().numpy()) <= 1e-14
-
-
-@pytest.mark.parametrize("name", [n for n in golden_names("cg") if "_p4_" not in n and not n.startswith("cg3")])
-def test_gpu_pipelined_block_kernel_matches_golden(name):
-    """The pipelined block-DMMA kernel (cell_bpipe_kernel, OperatorConfig(cell_blocks='pipe'))
-    against every scalar CG golden P1-P3."""
-    g = load_golden(name)
-    A = operator_from_fixture(g, cell_blocks="pipe")
-    assert A.info["cell_engine"] == 6 and A.info["block_cells"] > 0
-    err = rel_l2(A.apply(g["u"]), g["y"])
-    assert err <= TOL, f"{name}: rel L2 {err:.3e}"
