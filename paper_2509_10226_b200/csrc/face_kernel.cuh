@@ -217,11 +217,19 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 // BLOCKED: each CTA takes a contiguous run of chunks (consecutive chunks of one
 // (window, signature) group share their tables, so restaging and both barriers are
 // skipped); otherwise chunks are dealt round-robin.
+// RESIDENT: all 24 (lf, code) tables are staged once per CTA, so a chunk never restages
+// and the warps never wait for each other (small tables: P1 / P2 modal faces)
 template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool PEER = false>
+          bool PEER = false, bool RESIDENT = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   using S = FaceShape<N, QF>;
   extern __shared__ __align__(16) double smem[];
+  if (RESIDENT) {
+    const double2* src = reinterpret_cast<const double2*>(a.frags);
+    double2* dst = reinterpret_cast<double2*>(smem);
+    for (int i = threadIdx.x; i < 24 * S::NFRAG * 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int fs = lane >> 2;
   const int q4 = lane & 3;
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   for (int64_t w = w0; w < w1; w += wstep) {
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     const int4 ch = chunk_at(w);
-    if (ch.x != cur_x || ch.y != cur_y) {
+    if (!RESIDENT && (ch.x != cur_x || ch.y != cur_y)) {
       cur_x = ch.x;
       cur_y = ch.y;
       __syncthreads();  // previous chunk's warps are done with the staged tables
@@ -254,8 +262,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
       }
       __syncthreads();
     }
-    const double* Fm = smem;
-    const double* Fp = Fm + S::NFRAG * 32;
+    const double* Fm = RESIDENT ? smem + (int64_t)ch.x * S::NFRAG * 32 : smem;
+    const double* Fp = RESIDENT ? smem + (int64_t)(BOUNDARY ? 0 : ch.y) * S::NFRAG * 32 : Fm + S::NFRAG * 32;
     const int* perm_m = a.perm + (ch.x / 6) * N;                  // gather order, minus side
     const int* perm_p = a.perm + (BOUNDARY ? 0 : ch.y / 6) * N;   // plus side
 

@@ -10,11 +10,12 @@
 namespace tmf {
 
 template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool PEER = false>
+          bool PEER = false, bool RESIDENT = false>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShape<N, QF>;
-  constexpr int SMEM = (BND ? 1 : 2) * S::NFRAG * 32 * 8;
-  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, PEER>;
+  constexpr int SMEM = RESIDENT ? 24 * S::NFRAG * 32 * 8 : (BND ? 1 : 2) * S::NFRAG * 32 * 8;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, PEER, RESIDENT>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   if (info) {
     info->nfrag = S::NFRAG;
@@ -76,6 +77,12 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
       cudaError_t e = launch_face_a<N, QF, 3, 2>(a, n_sm, st);
       if (e != cudaErrorNotSupported) return e;
     }
+  }
+  // P2 modal interior faces: all 24 (lf, code) tables resident in shared memory (123 KB), one
+  // 512-thread CTA per SM, no restaging and no barriers between chunks: faces -6 to -7 % at
+  // 64^3 / 96^3 against the restaging 3-CTA kernel (round 2, profiles/r02/face_resident.jsonl)
+  if constexpr (!BND && N == 10 && QF < 10) {
+    if (!info && a.peer.u == nullptr) return launch_face_v<N, QF, BND, 1, 1, 512, false, false, true>(a, n_sm, st, info);
   }
   if (N == 10 && QF < 10) return launch_face_v<N, QF, BND, 1, 3>(a, n_sm, st, info);
   if (N <= 10) return launch_face_v<N, QF, BND, 1, 3, 256, true>(a, n_sm, st, info);
