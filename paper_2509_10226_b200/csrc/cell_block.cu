@@ -42,16 +42,8 @@ static cudaError_t launch_block_n(const BlockArgs& a, const double* tab, cudaStr
   auto kern = cell_block_kernel<N, C::M, C::BLOCK, C::CPT, C::MINB>;
   const size_t smem = block_smem_bytes(N, B, a.numax, a.nvmax);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  if (cudaError_t e = opt_in_smem(kern, 227 * 1024); e != cudaSuccess) return e;
-  {
-    static bool carve = false;   // the whole unified L1/shared array as shared memory
-    if (!carve) {
-      if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-          e != cudaSuccess)
-        return e;
-      carve = true;
-    }
-  }
+  // the whole unified L1 / shared array as shared memory (several CTAs per SM)
+  if (cudaError_t e = opt_in_smem(kern, 227 * 1024, true); e != cudaSuccess) return e;
   if (a.n_blocks == 0) return cudaSuccess;
   kern<<<(unsigned)a.n_blocks, C::BLOCK, smem, st>>>(a, T);
   return cudaGetLastError();

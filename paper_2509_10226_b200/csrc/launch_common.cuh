@@ -10,8 +10,9 @@ namespace tmf {
 // Dynamic shared memory above 48 KB needs a per-kernel, per-DEVICE opt-in; remember
 // which (kernel, device) pairs have been configured (kernels sharing a signature share
 // a function-pointer type, so the key is the pointer itself).
+// carveout100: also prefer the whole unified L1 / shared array as shared memory (block kernels)
 template <typename K>
-static cudaError_t opt_in_smem(K kern, int bytes) {
+static cudaError_t opt_in_smem(K kern, int bytes, bool carveout100 = false) {
   static std::mutex mu;
   static std::unordered_map<const void*, unsigned long long> done;  // bit d = device d (< 64)
   int dev = 0;
@@ -23,6 +24,11 @@ static cudaError_t opt_in_smem(K kern, int bytes) {
   if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       e != cudaSuccess)
     return e;
+  if (carveout100) {
+    if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e != cudaSuccess)
+      return e;
+  }
   mask |= bit;
   return cudaSuccess;
 }
