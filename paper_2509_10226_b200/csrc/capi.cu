@@ -237,6 +237,35 @@ void build_face_fragments(int N, int NF, int Q, F E, const double* w, std::vecto
         }
 }
 
+// Fragments of the split-mode modal face layout (face_kernel.cuh, HierShape): E(c, m, j) is
+// the modal table (component c of mode m at gather position j), unit weights.
+template <int N, class F>
+void build_face_fragments_hier(F E, std::vector<double>& out) {
+  using S = tmf::HierShape<N>;
+  auto val = [&](int q, int s, int r, int j) {
+    if (s < 0 || j >= N) return 0.0;
+    const int m = S::item_mode(q, s, r);
+    return m < 0 ? 0.0 : E(S::item_comp(q, s, r), m, j);
+  };
+  for (int t = 0; t < S::NTF; ++t)
+    for (int kk = 0; kk < S::KKF; ++kk)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int n = lane >> 2, q = n >> 1, i = n & 1;
+        out.push_back(val(q, S::tf_s(t, i), S::tf_r(t, i), 4 * kk + (lane & 3)));
+      }
+  for (int d = 0; d < S::NTD; ++d)
+    for (int kk = 0; kk < S::KK; ++kk)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int n = lane >> 2, q = n >> 1, i = n & 1;
+        out.push_back(val(q, S::td_s(d, i), S::td_r(d, i), 4 * kk + (lane & 3)));
+      }
+  for (int r3 = 0; r3 < 2; ++r3)          // face-only items first, then the D2 items (HierShape::b2)
+    for (int s = 0; s < S::NS; ++s)
+      for (int r = (r3 ? 3 : 0); r < (r3 ? 4 : 3); ++r)
+        for (int nj = 0; nj < (r < 3 ? S::NJF : S::NJ); ++nj)
+          for (int lane = 0; lane < 32; ++lane) out.push_back(val(lane & 3, s, r, 8 * nj + (lane >> 2)));
+}
+
 }  // namespace
 
 struct tmf_plan {
@@ -259,7 +288,9 @@ struct tmf_plan {
   double* cell_frags = nullptr;
   double* cell_geo = nullptr;
   double* face_frags = nullptr;
-  int face_engine = 0;             // (desc.flags >> 17) & 3: 0 by degree, 1 quadrature points, 3 modal
+  double* face_frags_h = nullptr;  // interior faces, split-mode modal layout (face engine 3)
+  int face_engine = 0;             // (desc.flags >> 17) & 3: 0 by degree, 1 quadrature points,
+                                   // 2 modal in the flat layout, 3 modal in the split-mode layout
   int* face_perm = nullptr;
   int* cells = nullptr;
   int* dofs = nullptr;
@@ -363,7 +394,8 @@ struct tmf_plan {
     tmf::FaceArgs a{};
     a.u = u;
     a.y = y;
-    a.frags = face_frags;
+    a.frags = (!boundary && face_frags_h) ? face_frags_h : face_frags;
+    a.hier = (!boundary && face_frags_h) ? 1 : 0;
     a.chunks = boundary ? bf_chunks : if_chunks;
     a.cm = boundary ? bf_cm : if_cm;
     a.cp = boundary ? nullptr : if_cp;
@@ -396,7 +428,7 @@ struct tmf_plan {
   }
   ~tmf_plan() {
     if (ev_stage) cudaEventDestroy(ev_stage);
-    for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)cells,
+    for (void* p : {(void*)verts, (void*)kappa, (void*)cell_frags, (void*)face_frags, (void*)face_frags_h, (void*)cells,
                     (void*)dofs, (void*)fix_list, (void*)if_chunks, (void*)if_cm, (void*)if_cp,
                     (void*)if_tau, (void*)bf_chunks, (void*)bf_cm, (void*)bf_tau, (void*)stage_u,
                     (void*)stage_y, (void*)pcg_buf, (void*)diag, (void*)diag_S, (void*)if_geo, (void*)bf_geo, (void*)cell_geo, (void*)face_perm,
@@ -821,8 +853,6 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   P->engine = ((d->flags >> 13) & 3) | (((d->flags >> 19) & 1) << 2);
   if (P->engine == 2) return bail(fail(TMF_EINVAL, "cell engine 2 (DFMA) was removed: use auto, dmma, tensor or modal"));
   P->face_engine = (d->flags >> 17) & 3;
-  if (P->face_engine == 2)
-    return bail(fail(TMF_EINVAL, "face engine 2 (reference tensor) was removed: use auto, quadrature or modal"));
   P->degree = d->degree;
   P->N = d->n_dofs_per_cell;
   P->Q = d->n_q;
@@ -1031,50 +1061,85 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     int fe = P->face_engine;
     if (fe == 0) fe = N >= 10 ? 3 : 1;
     P->face_engine = fe;
-    // modal face tables (face engine 3): every face integrand is a product of two P_p
+    // modal face tables (face engines 2 / 3): every face integrand is a product of two P_p
     // polynomials on the face (values in P_p, derivatives in P_{p-1}), so NF = dim P_p
-    // orthonormal modes integrate it exactly.  psi = V_F L^-T from the Cholesky factor of
-    // the Gram matrix of the face-DoF traces (lf 0, code 0; every (lf, code) table is
-    // indexed by the same reference-triangle points), and each table is projected:
-    //   E'(c, m, j) = sum_q w_q psi_m(q) E(c, q, j),  unit weights.
+    // orthonormal modes integrate it exactly:  E'(c, m, j) = sum_q w_q psi_m(q) E(c, q, j), unit
+    // weights.  The modes are degree-ordered: psi_0..psi_{MD-1} span P_{p-1} (MD = dim P_{p-1}),
+    // the rest complete P_p.  They come from the tables alone (lf 0, code 0; every (lf, code)
+    // table is indexed by the same reference-triangle points): pivoted Gram-Schmidt in the
+    // w-inner product, first over the tangential derivatives of the face traces (their span is
+    // P_{p-1} at the points), then over the traces themselves.  Derivative components then
+    // have no coefficient on the modes >= MD, which the split-mode layout (engine 3) leaves out.
     std::vector<double> proj;   // (NF, QF): w_q psi_m(q)
     int QK = QF;
-    if (fe == 3) {
-      std::vector<long double> H((size_t)NF * NF, 0.0L), L((size_t)NF * NF, 0.0L);
+    const int MD = P->degree * (P->degree + 1) / 2;
+    if (fe == 3 || fe == 2) {
       const double* Fv0 = d->face_values;
-      for (int a = 0; a < NF; ++a)
-        for (int b = 0; b < NF; ++b) {
-          long double acc = 0.0L;
-          for (int q = 0; q < QF; ++q)
-            acc += (long double)d->face_weights[q] * Fv0[q * N + perm[a]] * Fv0[q * N + perm[b]];
-          H[(size_t)a * NF + b] = acc;
+      const double* Fg0 = d->face_grads;
+      const double fr0[2][3] = {{-1.0, 1.0, 0.0}, {-1.0, 0.0, 1.0}};   // lf 0 frame tangents (R2-R1, R3-R1)
+      std::vector<std::vector<long double>> cand;
+      for (int t = 0; t < 2; ++t)
+        for (int a = 0; a < NF; ++a) {
+          std::vector<long double> v(QF);
+          for (int q = 0; q < QF; ++q) {
+            long double acc = 0.0L;
+            for (int k = 0; k < 3; ++k) acc += (long double)fr0[t][k] * Fg0[(size_t)(3 * q + k) * N + perm[a]];
+            v[q] = acc;
+          }
+          cand.push_back(std::move(v));
         }
-      for (int j = 0; j < NF; ++j) {
-        long double dj = H[(size_t)j * NF + j];
-        for (int k = 0; k < j; ++k) dj -= L[(size_t)j * NF + k] * L[(size_t)j * NF + k];
-        if (!(dj > 1e-20L)) return bail(fail(TMF_EINVAL, "modal face engine: face traces are not a basis of P_p"));
-        L[(size_t)j * NF + j] = std::sqrt(dj);
-        for (int i = j + 1; i < NF; ++i) {
-          long double v = H[(size_t)i * NF + j];
-          for (int k = 0; k < j; ++k) v -= L[(size_t)i * NF + k] * L[(size_t)j * NF + k];
-          L[(size_t)i * NF + j] = v / L[(size_t)j * NF + j];
-        }
+      const size_t n_der = cand.size();
+      for (int a = 0; a < NF; ++a) {
+        std::vector<long double> v(QF);
+        for (int q = 0; q < QF; ++q) v[q] = Fv0[(size_t)q * N + perm[a]];
+        cand.push_back(std::move(v));
       }
+      auto dot = [&](const std::vector<long double>& x, const std::vector<long double>& y) {
+        long double acc = 0.0L;
+        for (int q = 0; q < QF; ++q) acc += (long double)d->face_weights[q] * x[q] * y[q];
+        return acc;
+      };
+      std::vector<std::vector<long double>> psi;
+      auto sweep = [&](size_t c0, size_t c1, int want) {   // greedy: largest residual first
+        long double scale0 = 0.0L;
+        for (size_t c = c0; c < c1; ++c) scale0 = std::max(scale0, dot(cand[c], cand[c]));
+        for (int it = 0; it < want; ++it) {
+          size_t best = c0;
+          long double nb = -1.0L;
+          for (size_t c = c0; c < c1; ++c) {
+            const long double nn = dot(cand[c], cand[c]);
+            if (nn > nb) nb = nn, best = c;
+          }
+          if (!(nb > 1e-20L * scale0) || !(nb > 0.0L)) return false;
+          std::vector<long double> v = cand[best];
+          for (int rep = 0; rep < 2; ++rep)                 // re-orthogonalise against all modes
+            for (const auto& ps : psi) {
+              const long double c = dot(v, ps);
+              for (int q = 0; q < QF; ++q) v[q] -= c * ps[q];
+            }
+          const long double nv = std::sqrt(dot(v, v));
+          for (int q = 0; q < QF; ++q) v[q] /= nv;
+          psi.push_back(v);
+          for (size_t c = c0; c < cand.size(); ++c) {       // deflate the remaining candidates
+            const long double cc = dot(cand[c], v);
+            for (int q = 0; q < QF; ++q) cand[c][q] -= cc * v[q];
+          }
+        }
+        long double rest = 0.0L;                            // the span must be exhausted
+        for (size_t c = c0; c < c1; ++c) rest = std::max(rest, dot(cand[c], cand[c]));
+        return rest <= 1e-22L * std::max(scale0, 1.0L);
+      };
+      if (!sweep(0, n_der, MD) || !sweep(n_der, cand.size(), NF - MD))
+        return bail(fail(TMF_EINVAL, "modal face engine: face traces are not a nodal basis of P_p"));
       proj.assign((size_t)NF * QF, 0.0);
-      for (int q = 0; q < QF; ++q) {   // X = L^-1 V_F^T column by column (forward substitution)
-        std::vector<long double> x(NF);
-        for (int m = 0; m < NF; ++m) {
-          long double v = Fv0[q * N + perm[m]];
-          for (int k = 0; k < m; ++k) v -= L[(size_t)m * NF + k] * x[k];
-          x[m] = v / L[(size_t)m * NF + m];
-          proj[(size_t)m * QF + q] = (double)((long double)d->face_weights[q] * x[m]);
-        }
-      }
+      for (int m = 0; m < NF; ++m)
+        for (int q = 0; q < QF; ++q) proj[(size_t)m * QF + q] = (double)((long double)d->face_weights[q] * psi[m][q]);
       QK = NF;
     }
     P->QFk = QK;
     std::vector<double> ones(QK, 1.0);
-    std::vector<double> fr;
+    std::vector<double> fr, frh;
+    double lost = 0.0, kept = 0.0;   // derivative coefficients on the value-only modes (must vanish)
     for (int lf = 0; lf < 4; ++lf) {
       const double R[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
       const int fvv[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
@@ -1094,16 +1159,32 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
           const double* av = a[c - 1];
           return av[0] * Fg[(3 * q) * N + jj] + av[1] * Fg[(3 * q + 1) * N + jj] + av[2] * Fg[(3 * q + 2) * N + jj];
         };
-        if (fe == 3)
-          build_face_fragments(N, NF, QK, [&](int c, int m, int j) {
-            long double acc = 0.0L;
-            for (int q = 0; q < QF; ++q) acc += (long double)proj[(size_t)m * QF + q] * Ept(c, q, j);
-            return (double)acc;
-          }, ones.data(), fr);
-        else
+        if (fe == 3 || fe == 2) {
+          std::vector<double> Em((size_t)4 * NF * N);   // modal table (c, m, j)
+          for (int c = 0; c < 4; ++c)
+            for (int m = 0; m < NF; ++m)
+              for (int j = 0; j < N; ++j) {
+                long double acc = 0.0L;
+                for (int q = 0; q < QF; ++q) acc += (long double)proj[(size_t)m * QF + q] * Ept(c, q, j);
+                Em[((size_t)c * NF + m) * N + j] = (double)acc;
+                if (c > 0) (m >= MD ? lost : kept) = std::max(m >= MD ? lost : kept, std::fabs((double)acc));
+              }
+          auto Emod = [&](int c, int m, int j) { return Em[((size_t)c * NF + m) * N + j]; };
+          build_face_fragments(N, NF, QK, Emod, ones.data(), fr);
+          if (fe == 3) {
+            if (N == 4) build_face_fragments_hier<4>(Emod, frh);
+            else if (N == 10) build_face_fragments_hier<10>(Emod, frh);
+            else if (N == 20) build_face_fragments_hier<20>(Emod, frh);
+            else if (N == 35) build_face_fragments_hier<35>(Emod, frh);
+            else return bail(fail(TMF_EINVAL, "modal face engine: unsupported n_dofs_per_cell"));
+          }
+        } else {
           build_face_fragments(N, NF, QF, Ept, d->face_weights, fr);
+        }
       }
     }
+    if (fe == 3 && !(lost <= 1e-11 * std::max(kept, 1.0)))
+      return bail(fail(TMF_EINVAL, "modal face engine: derivative tables are not of degree p-1 on the face"));
     tmf::FaceLaunchInfo fi;
     bool ok = true;
     tmf::FaceArgs dummy{};
@@ -1113,6 +1194,14 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
                                               std::to_string(N) + ", " + std::to_string(QF) + ")"));
     if ((int64_t)fr.size() != 24LL * fi.nfrag * 32) return bail(fail(TMF_EINVAL, "internal: face fragments"));
     if ((rc = upload(&P->face_frags, fr.data(), fr.size(), &total))) return bail(rc);
+    const int dmma_boundary = fi.dmma_per_batch / 2;
+    if (fe == 3) {   // interior faces: the split-mode layout (the boundary kernel keeps the flat one)
+      dummy.hier = 1;
+      TMF_CUDA(tmf::launch_face(N, QK, false, dummy, P->n_sm, 0, &fi, &ok));
+      if (!ok || (int64_t)frh.size() != 24LL * fi.nfrag * 32)
+        return bail(fail(TMF_EINVAL, "internal: split-mode face fragments"));
+      if ((rc = upload(&P->face_frags_h, frh.data(), frh.size(), &total))) return bail(rc);
+    }
     const int chunk = ((d->flags >> 8) & 0xF) ? 8 * ((d->flags >> 8) & 0xF) : fi.chunk;
     if ((rc = build_face_batches(P, d, chunk, &total))) return bail(rc);
     // per-face geometry, computed once on the device (64 B per face slot)
@@ -1126,8 +1215,8 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     }
     P->info.n_face_batches = (int32_t)(P->n_if_batches + P->n_bf_batches);
     P->info.face_engine = P->face_engine;
-    P->info.flops_issued += (double)P->nc * (P->n_if_batches * fi.dmma_per_batch +
-                                             P->n_bf_batches * fi.dmma_per_batch / 2) * 512.0;
+    P->info.flops_issued += (double)P->nc * (P->n_if_batches * (double)fi.dmma_per_batch +
+                                             P->n_bf_batches * (double)dmma_boundary) * 512.0;
   }
 
   // algorithmic flops / bytes (reference counters)
@@ -1161,11 +1250,19 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       fe -= nce * (12.0 * nq * nd + 33.0 * nq);
       fe += nce * (12.0 * M * nd + 18.0 * M);
     }
-    if (faces && P->face_engine == 3) {
+    if (faces && (P->face_engine == 3 || P->face_engine == 2)) {
       // modal face tables: the point loop on NF unit-weight modes instead of n_qf points
       const double NFm = P->QFk;
       fe -= (double)d->n_interior_faces * (32.0 * nqf * nd + 26.0 * nqf) + (double)nbf_dir * (16.0 * nqf * nd + 13.0 * nqf);
-      fe += (double)d->n_interior_faces * (32.0 * NFm * nd + 26.0 * NFm) + (double)nbf_dir * (16.0 * NFm * nd + 13.0 * NFm);
+      double fi_face = 32.0 * NFm * nd + 26.0 * NFm;
+      if (P->face_engine == 3) {
+        // split-mode layout: values and tangential derivatives on the NF face DoFs only, the
+        // derivatives on MD = dim P_{p-1} modes, the transversal one on all DoFs; two GEMMs on
+        // two sides (x 8 flops per table entry), 26 flops per full mode, 6 per value-only mode
+        const double MDm = P->degree * (P->degree + 1) / 2;
+        fi_face = 8.0 * (NFm * NFm + 2.0 * MDm * NFm + MDm * nd) + 26.0 * MDm + 6.0 * (NFm - MDm);
+      }
+      fe += (double)d->n_interior_faces * fi_face + (double)nbf_dir * (16.0 * NFm * nd + 13.0 * NFm);
     }
     P->info.flops_engine = fe * P->nc;
     double b = 16.0 * (double)P->n_global + 24.0 * (double)P->n_verts;

@@ -54,6 +54,7 @@ struct FaceArgs {
   int n_dpc;
   int nc;
   PeerArgs peer;                      // multi-GPU: ghost cells' u read from their owner (n_own = cells)
+  int hier = 0;                       // host-side: frags hold the split-mode layout (HierShape) -> HIER kernels
   TMF_DBG_FIELDS
 };
 
@@ -93,6 +94,162 @@ struct FaceShape {
     return NB1 + g * B2G + (c < 3 ? c * NJF + nj : 3 * NJF + nj);
   }
 };
+
+// Split-mode layout of the modal interior-face kernel (HIER).  With a degree-ordered
+// orthonormal basis psi_0.. of P_p on the face (the first MD = dim P_{p-1} modes span
+// P_{p-1}), the derivative components of every trace are polynomials of degree p-1, so they
+// only have MD modal coefficients; the NVO = p+1 modes of exact degree p carry a value only,
+// and their share of the face term is linear: qv_m = -s tau (V+_m - V-_m).
+//
+// Each lane (q = lane&3) owns NS "quad slots" of four registers per side.  Quad slot
+// idx = 4 s + q is
+//   * full   (idx < MD):  (V, D0, D1, D2) of mode idx        -> (qv, qg0, qg1, qg2)
+//   * triple (idx >= MD): V of modes MD + 3 (idx-MD) + {0,1,2} -> their three qv, and 0
+// (triples only occur in the last slot row).  GEMM1 n-tiles pair the lane's registers:
+// face-only entries e = 3 s + r (r < 3: V, D0, D1 need the NF face DoFs = KKF k-steps),
+// then the D2 entries (all N DoFs, KK k-steps; an odd NS leaves a spare column that takes
+// the last face-only entry).  GEMM2 k-steps: one per (s, r), NJF n-tiles for r < 3, NJ for
+// the transversal derivative.  DMMAs per 8-face batch (both sides): 20 / 64 / 134 at
+// P2 / P3 / P4 against 40 / 102 / 192 for the flat 4-components-per-mode layout.
+template <int N>
+struct HierShape {
+  static constexpr int P = N == 4 ? 1 : N == 10 ? 2 : N == 20 ? 3 : 4;
+  static constexpr int NF = (P + 1) * (P + 2) / 2;   // value modes = DoFs on a face
+  static constexpr int MD = P * (P + 1) / 2;         // derivative modes
+  static constexpr int NVO = NF - MD;                // value-only modes
+  static constexpr int NTRI = (NVO + 2) / 3;
+  static constexpr int NS = (MD + NTRI + 3) / 4;     // quad slots per lane
+  static_assert(4 * (NS - 1) <= MD, "triple slots must sit in the last slot row");
+  static constexpr int KK = (N + 3) / 4;
+  static constexpr int KKF = (NF + 3) / 4;
+  static constexpr int NJ = (N + 7) / 8;
+  static constexpr int NJF = (NF + 7) / 8;
+  static constexpr int NTF = (3 * NS) / 2;           // face-only GEMM1 tiles
+  static constexpr int NTD = (NS + 1) / 2;           // GEMM1 tiles with the D2 entries
+  static constexpr int NB1 = NTF * KKF + NTD * KK;
+  static constexpr int NB2 = 3 * NS * NJF + NS * NJ;
+  static constexpr int NFRAG = NB1 + NB2;            // per (lf, code) combo
+  static constexpr int CHUNK = 32;
+  __host__ __device__ static constexpr int b1f(int t, int kk) { return t * KKF + kk; }
+  __host__ __device__ static constexpr int b1d(int d, int kk) { return NTF * KKF + d * KK + kk; }
+  __host__ __device__ static constexpr int b2(int s, int r, int nj) {
+    return NB1 + (r < 3 ? (s * 3 + r) * NJF + nj : 3 * NS * NJF + s * NJ + nj);
+  }
+  // register (s, r) of column i of face-only tile t / D2 tile d; s < 0: empty column
+  __host__ __device__ static constexpr int tf_s(int t, int i) { return (2 * t + i) / 3; }
+  __host__ __device__ static constexpr int tf_r(int t, int i) { return (2 * t + i) % 3; }
+  __host__ __device__ static constexpr int td_s(int d, int i) {
+    return i == 0 ? 2 * d : (2 * d + 1 < NS ? 2 * d + 1 : ((3 * NS) % 2 ? (3 * NS - 1) / 3 : -1));
+  }
+  __host__ __device__ static constexpr int td_r(int d, int i) {
+    return (i == 0 || 2 * d + 1 < NS) ? 3 : (3 * NS - 1) % 3;
+  }
+  // (component, mode) held by register (s, r) of lane slot q: mode < 0 = empty
+  __host__ __device__ static constexpr int item_mode(int q, int s, int r) {
+    const int idx = 4 * s + q;
+    if (idx < MD) return idx;
+    const int m = MD + 3 * (idx - MD) + r;
+    return (r < 3 && m < NF) ? m : -1;
+  }
+  __host__ __device__ static constexpr int item_comp(int q, int s, int r) { return 4 * s + q < MD ? r : 0; }
+};
+
+// Either layout behind the names the kernels use
+template <int N, int QF, bool HIER>
+struct FaceShapeSel : FaceShape<N, QF> {};
+template <int N, int QF>
+struct FaceShapeSel<N, QF, true> : HierShape<N> {};
+
+// Interior-face arithmetic of one 8-face batch in the split-mode layout: GEMM1 of both
+// sides, the modal face_qpoint (numpy_backend.py:91-105 on modes), GEMM2 of both sides.
+template <int N>
+__device__ __forceinline__ void face_hier_core(const double (&am)[HierShape<N>::KK], const double (&ap)[HierShape<N>::KK],
+                                               const double (&hm)[3], const double (&hp)[3], double stau,
+                                               const double* __restrict__ Fm, const double* __restrict__ Fp,
+                                               int lane, double (&ym)[HierShape<N>::NJ][2],
+                                               double (&yp)[HierShape<N>::NJ][2]) {
+  using S = HierShape<N>;
+  const int q4 = lane & 3;
+  double vm[S::NS][4], vp[S::NS][4];
+#pragma unroll
+  for (int s = 0; s < S::NS; ++s)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) vm[s][r] = vp[s][r] = 0.0;
+#pragma unroll
+  for (int t = 0; t < S::NTF; ++t) {
+    double cm[2] = {0.0, 0.0}, cp[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kk = 0; kk < S::KKF; ++kk) {
+      const int f = S::b1f(t, kk) * 32 + lane;
+      dmma(cm, am[kk], Fm[f]);
+      dmma(cp, ap[kk], Fp[f]);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      vm[S::tf_s(t, i)][S::tf_r(t, i)] = cm[i];
+      vp[S::tf_s(t, i)][S::tf_r(t, i)] = cp[i];
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < S::NTD; ++d) {
+    double cm[2] = {0.0, 0.0}, cp[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kk = 0; kk < S::KK; ++kk) {
+      const int f = S::b1d(d, kk) * 32 + lane;
+      dmma(cm, am[kk], Fm[f]);
+      dmma(cp, ap[kk], Fp[f]);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      if (S::td_s(d, i) >= 0) {
+        vm[S::td_s(d, i)][S::td_r(d, i)] = cm[i];
+        vp[S::td_s(d, i)][S::td_r(d, i)] = cp[i];
+      }
+  }
+#pragma unroll
+  for (int s = 0; s < S::NS; ++s) {
+    const bool may_tri = 4 * s + 3 >= S::MD;            // compile time per unrolled s
+    const bool tri = may_tri && (4 * s + q4 >= S::MD);
+    const double d0 = vp[s][0] - vm[s][0];              // -[[u]] of the slot's (first) mode
+    double hmf[3], hpf[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      hmf[k] = tri ? 0.0 : hm[k];
+      hpf[k] = tri ? 0.0 : hp[k];
+    }
+    double qv = -stau * d0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      qv = fma(-hmf[k], vm[s][1 + k], qv);
+      qv = fma(-hpf[k], vp[s][1 + k], qv);
+    }
+    double om[4], op[4];
+    om[0] = qv;
+    op[0] = -qv;
+    if (may_tri) {
+      const double t1 = stau * (vp[s][1] - vm[s][1]), t2 = stau * (vp[s][2] - vm[s][2]);
+      om[1] = tri ? -t1 : d0 * hm[0];
+      om[2] = tri ? -t2 : d0 * hm[1];
+      op[1] = tri ? t1 : d0 * hp[0];
+      op[2] = tri ? t2 : d0 * hp[1];
+    } else {
+      om[1] = d0 * hm[0];
+      om[2] = d0 * hm[1];
+      op[1] = d0 * hp[0];
+      op[2] = d0 * hp[1];
+    }
+    om[3] = d0 * hmf[2];
+    op[3] = d0 * hpf[2];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int nj = 0; nj < (r < 3 ? S::NJF : S::NJ); ++nj) {
+        const int f = S::b2(s, r, nj) * 32 + lane;
+        dmma(ym[nj], om[r], Fm[f]);
+        dmma(yp[nj], op[r], Fp[f]);
+      }
+  }
+}
 
 // A_lf^-1 for the face frame (reference vertices (0,0,0),(1,0,0),(0,1,0),(0,0,1)).
 __host__ __device__ inline void face_frame_inverse(int lf, double (&Ai)[3][3]) {
@@ -219,10 +376,12 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 // skipped); otherwise chunks are dealt round-robin.
 // RESIDENT: all 24 (lf, code) tables are staged once per CTA, so a chunk never restages
 // and the warps never wait for each other (small tables: P1 / P2 modal faces)
+// HIER: the split-mode modal layout (HierShape, interior faces only; QF is not used)
 template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool PEER = false, bool RESIDENT = false>
+          bool PEER = false, bool RESIDENT = false, bool HIER = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
-  using S = FaceShape<N, QF>;
+  static_assert(!HIER || !BOUNDARY, "the split-mode layout is for interior faces");
+  using S = FaceShapeSel<N, QF, HIER>;
   extern __shared__ __align__(16) double smem[];
   if (RESIDENT) {
     const double2* src = reinterpret_cast<const double2*>(a.frags);
@@ -340,6 +499,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
 #pragma unroll
       for (int nj = 0; nj < S::NJ; ++nj) ym[nj][0] = ym[nj][1] = yp[nj][0] = yp[nj][1] = 0.0;
 
+      if constexpr (HIER) {
+        face_hier_core<N>(am, ap, hm, hp, stau, Fm, Fp, lane, ym, yp);
+      } else {
 #pragma unroll
       for (int g = 0; g < S::G; ++g) {
         double vm[2][2], vp[2][2];  // [h][i] = component 2h+i of point 4g+q4
@@ -389,6 +551,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
             if (!BOUNDARY) dmma(yp[nj], qp[c], Fp[f]);
           }
       }
+      }
 
       if (c_m >= 0) {
 #pragma unroll
@@ -418,9 +581,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
 // and the cell ids of the batch after that are loaded into registers, so AS-1 batches'
 // gathers are in flight while the DMMAs of the current one run.  The chunk loop (table
 // restaging and its barriers) is unchanged; round-robin or blocked chunk runs.
-template <int N, int QF, int AS, int MINB = 2, int BLOCK = 256, bool BLOCKED = false>
+template <int N, int QF, int AS, int MINB = 2, int BLOCK = 256, bool BLOCKED = false, bool HIER = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
-  using S = FaceShape<N, QF>;
+  using S = FaceShapeSel<N, QF, HIER>;
   constexpr int SLOT = 2 * S::KK * 32 + 64 + 16;   // am, ap, geometry (8 x 8), cell ids (8 x 2 ints)
   extern __shared__ __align__(16) double smem[];
   double* tabs = smem;                                        // two staged tables
@@ -568,6 +731,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
       double ym[S::NJ][2], yp[S::NJ][2];
 #pragma unroll
       for (int nj = 0; nj < S::NJ; ++nj) ym[nj][0] = ym[nj][1] = yp[nj][0] = yp[nj][1] = 0.0;
+      if constexpr (HIER) {
+        face_hier_core<N>(am, ap, hm, hp, stau, Fm, Fp, lane, ym, yp);
+      } else {
 #pragma unroll
       for (int g = 0; g < S::G; ++g) {
         double vm[2][2], vp[2][2];
@@ -607,6 +773,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
             dmma(ym[nj2], qm[c], Fm[f]);
             dmma(yp[nj2], qp[c], Fp[f]);
           }
+      }
       }
       if (c_m >= 0) {
 #pragma unroll

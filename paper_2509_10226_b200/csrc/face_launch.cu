@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "face_kernel.cuh"
 #include "launch.h"
@@ -10,12 +11,12 @@
 namespace tmf {
 
 template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool PEER = false, bool RESIDENT = false>
+          bool PEER = false, bool RESIDENT = false, bool HIER = false>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
-  using S = FaceShape<N, QF>;
+  using S = FaceShapeSel<N, QF, HIER>;
   constexpr int SMEM = RESIDENT ? 24 * S::NFRAG * 32 * 8 : (BND ? 1 : 2) * S::NFRAG * 32 * 8;
   static_assert(SMEM <= 227 * 1024, "shared memory");
-  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, PEER, RESIDENT>;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, PEER, RESIDENT, HIER>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   if (info) {
     info->nfrag = S::NFRAG;
@@ -36,15 +37,15 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
 }
 
 // interior faces with the asynchronous gather ring (face_async_kernel), blocked chunk runs
-template <int N, int QF, int AS, int MINB, int BLOCK = 256>
+template <int N, int QF, int AS, int MINB, int BLOCK = 256, bool HIER = false>
 static cudaError_t launch_face_a(const FaceArgs& a, int n_sm, cudaStream_t st) {
-  using S = FaceShape<N, QF>;
+  using S = FaceShapeSel<N, QF, HIER>;
   constexpr int SLOT = 2 * S::KK * 32 + 64 + 16;
   constexpr int SMEM = (2 * S::NFRAG * 32 + (4 * N + 1) / 2 + (BLOCK / 32) * AS * SLOT) * 8;
   if constexpr (SMEM > 227 * 1024) {
     return cudaErrorNotSupported;   // tables + rings do not fit (n_qf-point P4): caller falls back
   } else {
-    auto kern = face_async_kernel<N, QF, AS, MINB, BLOCK, true>;
+    auto kern = face_async_kernel<N, QF, AS, MINB, BLOCK, true, HIER>;
     if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
     int per_sm = 0;
     cudaError_t e = blocks_per_sm(kern, BLOCK, SMEM, &per_sm);
@@ -66,6 +67,43 @@ static cudaError_t launch_face_a(const FaceArgs& a, int n_sm, cudaStream_t st) {
 // chunks with record prefetch at 3 CTAs/SM (Helmholtz 96^3 1.55 ms vs 1.90 blocked); P4
 // interior faces take the 3-stage asynchronous gather ring (DG 48^3 1.05 -> 0.85 ms; P2 / P3
 // gain nothing from it).
+// Split-mode modal layout (HierShape), interior faces.  TMF_FACE_VARIANT (environment,
+// experiments only) picks another CTA shape / pipeline.
+template <int N>
+static cudaError_t launch_face_h(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
+  constexpr int QF = HierShape<N>::NF;
+  static const int variant = [] {
+    const char* e = std::getenv("TMF_FACE_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (info) return launch_face_v<N, QF, false, 1, 2, 256, false, false, false, true>(a, n_sm, st, info);
+  if (a.peer.u != nullptr) {
+    if (N <= 10) return launch_face_v<N, QF, false, 1, 3, 256, true, true, false, true>(a, n_sm, st, info);
+    return launch_face_v<N, QF, false, 2, 2, 256, true, true, false, true>(a, n_sm, st, info);
+  }
+  if constexpr (N == 35) {
+    if (variant == 1) return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true>(a, n_sm, st, info);
+    if (variant == 2) return launch_face_a<N, QF, 2, 2, 256, true>(a, n_sm, st);
+    return launch_face_a<N, QF, 3, 2, 256, true>(a, n_sm, st);
+  } else if constexpr (N == 20) {
+    if (variant == 1) return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 2) return launch_face_v<N, QF, false, 2, 1, 512, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 3) return launch_face_v<N, QF, false, 1, 1, 768, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 4) return launch_face_a<N, QF, 3, 2, 256, true>(a, n_sm, st);
+    if (variant == 5) return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
+    return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true>(a, n_sm, st, info);
+  } else if constexpr (N == 10) {
+    if (variant == 1) return launch_face_v<N, QF, false, 1, 2, 512, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 2) return launch_face_v<N, QF, false, 2, 1, 512, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 3) return launch_face_v<N, QF, false, 1, 3, 256, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 4) return launch_face_v<N, QF, false, 1, 1, 1024, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 5) return launch_face_a<N, QF, 3, 3, 256, true>(a, n_sm, st);
+    return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true>(a, n_sm, st, info);
+  } else {
+    return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
+  }
+}
+
 template <int N, int QF, bool BND>
 static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   if (!BND && a.peer.u != nullptr && !info) {   // multi-GPU: plus-side ghost cells from peer memory
@@ -92,6 +130,14 @@ static cudaError_t launch_face_t(const FaceArgs& a, int n_sm, cudaStream_t st, F
 cudaError_t launch_face(int n_dpc, int n_qf, bool boundary, const FaceArgs& a, int n_sm,
                         cudaStream_t st, FaceLaunchInfo* info, bool* supported) {
   *supported = true;
+  if (a.hier && !boundary) {
+    if (n_dpc == 4) return launch_face_h<4>(a, n_sm, st, info);
+    if (n_dpc == 10) return launch_face_h<10>(a, n_sm, st, info);
+    if (n_dpc == 20) return launch_face_h<20>(a, n_sm, st, info);
+    if (n_dpc == 35) return launch_face_h<35>(a, n_sm, st, info);
+    *supported = false;
+    return cudaSuccess;
+  }
 #define TMF_FACE(NN, QQ)                                                          \
   if (n_dpc == NN && n_qf == QQ) {                                                \
     if (boundary) return launch_face_t<NN, QQ, true>(a, n_sm, st, info);          \

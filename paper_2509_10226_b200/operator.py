@@ -38,7 +38,7 @@ _STAGES = ("ref", "data", "mm", "sched")
 _ENGINES = {"auto": 0, "dmma": 1, "tensor": 3, "modal": 4}
 _BLOCKS = {"auto": 0, "off": 1, "on": 2}
 _ORDERS = {"auto": 0, "input": 1, "morton": 2}
-_FACE_ENGINES = {"auto": 0, "quadrature": 1, "modal": 3}
+_FACE_ENGINES = {"auto": 0, "quadrature": 1, "modal_flat": 2, "modal": 3}
 
 
 @dataclass(frozen=True)
@@ -59,7 +59,7 @@ class OperatorConfig:
     cell_engine: str = "auto"    # B200 cell kernel: auto | dmma (quadrature points) | tensor (affine
     #                              reference tensor) | modal (points loop on the M = dim P_{p-1} exact modes)
     cell_blocks: str = "auto"    # B200 CG block assembly (low degrees on locality-ordered meshes): auto | off | on
-    face_engine: str = "auto"    # B200 faces: auto (modal at P2-P4) | quadrature (points) | modal
+    face_engine: str = "auto"    # B200 faces: auto (modal at P2-P4) | quadrature (points) | modal | modal_flat
     f32_mirror: bool = False     # B200 CG Laplace: also build the fp32 apply (apply_f32; mixed-precision multigrid)
     cell_order: str = "auto"     # B200 CG traversal: auto (Morton when the mesh order has no locality) | input | morton
 

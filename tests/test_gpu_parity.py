@@ -63,10 +63,10 @@ def test_gpu_default_engines():
         assert A.info["face_engine"] == face, name
 
 
-FACE_CODE = {"quadrature": 1, "modal": 3}
+FACE_CODE = {"quadrature": 1, "modal_flat": 2, "modal": 3}
 
 
-@pytest.mark.parametrize("engine", ["quadrature", "modal"])
+@pytest.mark.parametrize("engine", ["quadrature", "modal_flat", "modal"])
 @pytest.mark.parametrize("name", [n for n in golden_names() if n.startswith(("dg", "helm"))])
 def test_gpu_face_engines_match_golden(name, engine):
     """Faces: the n_qf-point loop (face_kernel.cuh) and the point loop on NF exact face

@@ -3,7 +3,7 @@
     python tools/loop_bench.py cg:2:48:r:auto:auto [dg:3:64:r:auto:auto ...]
 
 spec = kind (cg | dg | helmk) : degree : n (n^3 x 6 Kuhn mesh) : u (unordered) | r
-(reorder_mesh) : cell engine : cell blocks.  Prints one JSON line per spec: the apply
+(reorder_mesh) : cell engine : cell blocks [: face engine].  Prints one JSON line per spec: the apply
 time per tmf_apply_timed with a 256 MiB L2 flush before every apply (the bench's
 protocol, CUDA events on the launch stream), its cell / face split, and back-to-back
 "hot" applies.
@@ -24,7 +24,9 @@ def build(spec):
     from paper_2509_10226_b200.geometry import GeometryData
     from paper_2509_10226_b200.reorder import reorder_mesh
 
-    kind, p, n, order, eng, blocks = spec.split(":")
+    parts = spec.split(":")
+    kind, p, n, order, eng, blocks = parts[:6]
+    face = parts[6] if len(parts) > 6 else "auto"
     p, n = int(p), int(n)
     if (n, order) not in _MESH:
         m = M.kuhn_cube_mesh(n, seed=0)
@@ -33,7 +35,7 @@ def build(spec):
     cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
     bas = B.tabulate_basis(p, cr, fr)
     geo = GeometryData("affine", cr, fr, None, None, None, None)
-    cfg = op.OperatorConfig(cell_engine=eng, cell_blocks=blocks)
+    cfg = op.OperatorConfig(cell_engine=eng, cell_blocks=blocks, face_engine=face)
     if kind == "cg":
         dm = D.build_dof_map(m, p, "cg")
         A = op.CgPoissonOperator(m, dm, geo, bas, cfg)
