@@ -56,11 +56,15 @@ int upload(T** dst, const T* src, size_t n, size_t* total) {
 // (CellShape::GRP) with components padded to 4:
 //   B1g[h][kk][lane] = E_{2h + (n&1)}(8T + (n>>1), 4kk + (lane&3)),  n = lane>>2
 //   B2g[c][nj][lane] = w_q E_c(q = 8T + (lane&3), 8nj + (lane>>2))
+// a remainder of 1..2 points is one pair group (CellShape::PAIR), columns (point, component):
+//   B1p[kk][lane] = E_{n&3}(8T + (n>>2), 4kk + (lane&3)),  n = lane>>2
+//   B2p[i][nj][lane] = w_q E_{2(k&1)+i}(q = 8T + (k>>1), 8nj + (lane>>2)),  k = lane&3
 template <typename F>
 void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<double>& out) {
   const int KK = (N + 3) / 4, NJ = (N + 7) / 8, R = Q % 8;
-  const bool grp = R >= 1 && R <= 4;
-  const int T = grp ? Q / 8 : (Q + 7) / 8;
+  const bool pair = R >= 1 && R <= 2;
+  const bool grp = R >= 3 && R <= 4;
+  const int T = (grp || pair) ? Q / 8 : (Q + 7) / 8;
   for (int t = 0; t < T; ++t)
     for (int c = 0; c < NC; ++c)
       for (int kk = 0; kk < KK; ++kk)
@@ -75,6 +79,12 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
           const int n = lane >> 2, c = 2 * h + (n & 1), q = 8 * T + (n >> 1), j = 4 * kk + (lane & 3);
           out.push_back(q < Q && j < N && c < NC ? E(c, q, j) : 0.0);
         }
+  if (pair)
+    for (int kk = 0; kk < KK; ++kk)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int n = lane >> 2, c = n & 3, q = 8 * T + (n >> 2), j = 4 * kk + (lane & 3);
+        out.push_back(q < Q && j < N && c < NC ? E(c, q, j) : 0.0);
+      }
   for (int t = 0; t < T; ++t)
     for (int c = 0; c < NC; ++c)
       for (int i = 0; i < 2; ++i)
@@ -89,6 +99,13 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
         for (int lane = 0; lane < 32; ++lane) {
           const int q = 8 * T + (lane & 3), j = 8 * nj + (lane >> 2);
           out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
+        }
+  if (pair)
+    for (int i = 0; i < 2; ++i)
+      for (int nj = 0; nj < NJ; ++nj)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int k = lane & 3, c = 2 * (k & 1) + i, q = 8 * T + (k >> 1), j = 8 * nj + (lane >> 2);
+          out.push_back(q < Q && j < N && c < NC ? w[q] * E(c, q, j) : 0.0);
         }
 }
 
@@ -327,6 +344,7 @@ struct tmf_plan {
   double* if_tau = nullptr;
   double* if_geo = nullptr;
   int64_t n_if_batches = 0, n_if_chunks = 0;
+  int face_run = 0;   // chunk-run length of the interior-face CTA walk (face_kernel.cuh ChunkWalk)
   int4* bf_chunks = nullptr;
   int* bf_cm = nullptr;
   double* bf_tau = nullptr;
@@ -396,6 +414,7 @@ struct tmf_plan {
     a.y = y;
     a.frags = (!boundary && face_frags_h) ? face_frags_h : face_frags;
     a.hier = (!boundary && face_frags_h) ? 1 : 0;
+    a.run = boundary ? 0 : face_run;
     a.chunks = boundary ? bf_chunks : if_chunks;
     a.cm = boundary ? bf_cm : if_cm;
     a.cp = boundary ? nullptr : if_cp;
@@ -503,6 +522,24 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   }
   P->n_if_batches = nb;
   P->n_if_chunks = (int64_t)chunks.size();
+  // CTA walk of the interior faces (face_kernel.cuh ChunkWalk).  P3: runs of 2 chunks dealt
+  // round-robin, so the CTAs sweep the windows together and the faces of a cell find its
+  // u / y rows in L2 -- measured (profiles/r02/face_runs.jsonl) DG P3 64^3 faces 0.841 ->
+  // 0.755 ms reordered, 0.929 -> 0.776 ms unordered; on the permuted 48^3 mesh +3 %, so small
+  // meshes without locality keep one contiguous run per CTA.  P4's 3-stage ring kernel is
+  // slower with any run length (larger tables to restage: 40^3 0.424 -> 0.459 ms); P2's
+  // resident-table kernel already deals chunks round-robin.  TMF_FACE_RUN (environment,
+  // experiments) overrides.
+  {
+    int64_t near = 0;
+    for (int64_t f = 0; f < nif; ++f) {
+      const int32_t* r = d->interior_faces + 5 * f;
+      if (r[0] / kFaceWindow == r[2] / kFaceWindow) ++near;
+    }
+    const bool local = nif > 0 && 2 * near >= nif;
+    P->face_run = (P->N == 20 && d->n_cells > 2 * kFaceWindow && (local || d->n_cells >= (1 << 20))) ? 2 : 0;
+    if (const char* e = std::getenv("TMF_FACE_RUN")) P->face_run = std::atoi(e);
+  }
   int rc;
   if ((rc = upload(&P->if_chunks, chunks.data(), chunks.size(), total))) return rc;
   if ((rc = upload(&P->if_cm, cm.data(), cm.size(), total))) return rc;

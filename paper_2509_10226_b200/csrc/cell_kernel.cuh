@@ -95,13 +95,18 @@ struct CellShape {
   // group (GEMM1 columns (point, component) with components padded to 4, the
   // face-kernel layout), which takes 2 KK + NC NJ DMMAs instead of the
   // NC KK + 2 NC NJ of an 8-point tile (P3, n_q 35: 165 -> 151 per tile).
+  // A remainder of 1..2 points goes to one 2-point pair group: ONE 8-column GEMM1 tile
+  // with columns (point, component padded to 4); a lane holds two components of its
+  // point and gets the others from its neighbour lane with one shuffle each, so the
+  // pair takes KK + 2 NJ DMMAs (modal P3, 10 modes: 52 -> 44 per tile).
   static constexpr int R = Q % 8;
-  static constexpr bool GRP = R >= 1 && R <= 4;
-  static constexpr int T = GRP ? Q / 8 : (Q + 7) / 8;
+  static constexpr bool PAIR = R >= 1 && R <= 2;
+  static constexpr bool GRP = R >= 3 && R <= 4;
+  static constexpr int T = (GRP || PAIR) ? Q / 8 : (Q + 7) / 8;
   static constexpr int NB1T = T * NC * KK;   // GEMM1 fragments of the 8-point tiles
   static constexpr int NB2T = T * NC * 2 * NJ;
-  static constexpr int NB1 = NB1T + (GRP ? 2 * KK : 0);
-  static constexpr int NB2 = NB2T + (GRP ? NC * NJ : 0);
+  static constexpr int NB1 = NB1T + (GRP ? 2 * KK : 0) + (PAIR ? KK : 0);
+  static constexpr int NB2 = NB2T + (GRP ? NC * NJ : 0) + (PAIR ? 2 * NJ : 0);
   static constexpr int NFRAG = NB1 + NB2;
   static constexpr int SMEM = NFRAG * 32 * 8;
   static constexpr int DMMA_PER_TILE = NB1 + NB2;
@@ -131,8 +136,10 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
   __syncthreads();
   const double* sB1 = smem;
   const double* sB2 = smem + S::NB1 * 32;
-
   const int lane = threadIdx.x & 31;
+  auto B1 = [&](int f) -> double { return sB1[f * 32 + lane]; };
+  auto B2 = [&](int f) -> double { return sB2[f * 32 + lane]; };
+
   const int cs = lane >> 2;  // cell slot in the tile
   const int q4 = lane & 3;
   const int64_t ctiles = (a.n_cells + 7) / 8;
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       for (int kk = 0; kk < S::KK; ++kk) {
 #pragma unroll
         for (int c = 0; c < S::NC; ++c) {
-          const double b = sB1[((t * S::NC + c) * S::KK + kk) * 32 + lane];
+          const double b = B1((t * S::NC + c) * S::KK + kk);
 #pragma unroll
           for (int m = 0; m < MT; ++m) dmma(v[m][c], av[m][kk], b);
         }
@@ -304,7 +311,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
         for (int i = 0; i < 2; ++i)
 #pragma unroll
           for (int nj = 0; nj < S::NJ; ++nj) {
-            const double b = sB2[(((t * S::NC + c) * 2 + i) * S::NJ + nj) * 32 + lane];
+            const double b = B2(((t * S::NC + c) * 2 + i) * S::NJ + nj);
 #pragma unroll
             for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][c][i], b);
           }
@@ -317,7 +324,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       for (int kk = 0; kk < S::KK; ++kk)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const double b = sB1[(S::NB1T + h * S::KK + kk) * 32 + lane];
+          const double b = B1(S::NB1T + h * S::KK + kk);
 #pragma unroll
           for (int m = 0; m < MT; ++m) dmma(v[m][h], av[m][kk], b);
         }
@@ -340,9 +347,53 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       for (int c = 0; c < S::NC; ++c)
 #pragma unroll
         for (int nj = 0; nj < S::NJ; ++nj) {
-          const double b = sB2[(S::NB2T + c * S::NJ + nj) * 32 + lane];
+          const double b = B2(S::NB2T + c * S::NJ + nj);
 #pragma unroll
           for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][c], b);
+        }
+    };
+    // remainder pair group: lane owns components 2(q4&1) + {0,1} of point 8T + (q4>>1)
+    auto gemm1p = [&](double (&v)[MT][2]) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m) v[m][0] = v[m][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < S::KK; ++kk) {
+        const double b = B1(S::NB1T + kk);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) dmma(v[m], av[m][kk], b);
+      }
+    };
+    auto dgemm2p = [&](const double (&v)[MT][2]) {
+      double d[MT][2];
+      const bool odd = (q4 & 1) != 0;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const double x0 = __shfl_xor_sync(0xffffffffu, v[m][0], 1);
+        const double x1 = __shfl_xor_sync(0xffffffffu, v[m][1], 1);
+        if (MASS) {
+          // components (value, g0 | g1, g2): even lanes integrate value and d0, odd lanes d1 and d2
+          const double val = odd ? x0 : v[m][0], g0 = odd ? x1 : v[m][1];
+          const double g1 = odd ? v[m][0] : x0, g2 = odd ? v[m][1] : x1;
+          const double a0 = odd ? G[m][1] : 0.0, a1 = odd ? G[m][3] : 0.0, a2 = odd ? G[m][4] : 0.0;
+          const double b0 = odd ? G[m][2] : G[m][0], b1 = odd ? G[m][4] : G[m][1], b2 = odd ? G[m][5] : G[m][2];
+          d[m][0] = odd ? a0 * g0 + a1 * g1 + a2 * g2 : mdet[m] * val;
+          d[m][1] = b0 * g0 + b1 * g1 + b2 * g2;
+        } else {
+          // components (g0, g1 | g2, pad): even lanes integrate d0 and d1, odd lanes d2
+          const double g0 = odd ? x0 : v[m][0], g1 = odd ? x1 : v[m][1], g2 = odd ? v[m][0] : x0;
+          const double a0 = odd ? G[m][2] : G[m][0], a1 = odd ? G[m][4] : G[m][1], a2 = odd ? G[m][5] : G[m][2];
+          d[m][0] = a0 * g0 + a1 * g1 + a2 * g2;
+          d[m][1] = odd ? 0.0 : G[m][1] * g0 + G[m][3] * g1 + G[m][4] * g2;
+          if (EN) en = odd ? fma(g2, d[m][0], en) : fma(g0, d[m][0], fma(g1, d[m][1], en));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int nj = 0; nj < S::NJ; ++nj) {
+          const double b = B2(S::NB2T + i * S::NJ + nj);
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], d[m][i], b);
         }
     };
     double vg[MT][2][2];
@@ -355,6 +406,11 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
     if (S::GRP) {
       gemm1g(vg);
       dgemm2g(vg);
+    }
+    if (S::PAIR) {
+      double vp[MT][2];
+      gemm1p(vp);
+      dgemm2p(vp);
     }
 
     // ---- scatter / store: lane owns DoFs 8nj + 2q4 + {0,1}

@@ -55,7 +55,33 @@ struct FaceArgs {
   int nc;
   PeerArgs peer;                      // multi-GPU: ghost cells' u read from their owner (n_own = cells)
   int hier = 0;                       // host-side: frags hold the split-mode layout (HierShape) -> HIER kernels
+  int run = 0;                        // BLOCKED kernels: chunk-run length of the CTA walk (ChunkWalk), 0 = one run per CTA
   TMF_DBG_FIELDS
+};
+
+// Which chunks a CTA takes, in which order (work item w = component * n_chunks + chunk):
+//   round-robin (not BLOCKED): w = blockIdx + i * grid;
+//   BLOCKED, run 0: one contiguous run per CTA -- consecutive chunks of a (window,
+//     signature) group share their tables, so restaging and its barriers are skipped;
+//   BLOCKED, run R: runs of R consecutive chunks dealt round-robin, so all CTAs advance
+//     through the window-sorted face list together and the four faces of a cell find its
+//     u / y rows in L2 (DG P3 64^3 reordered: faces -10 %), while a run still shares tables.
+struct ChunkWalk {
+  int64_t nwork, nit, per;
+  int run;
+  bool blocked;
+  __device__ ChunkWalk(int64_t nwork_, bool blocked_, int run_) : nwork(nwork_), run(run_), blocked(blocked_) {
+    per = (nwork + gridDim.x - 1) / gridDim.x;
+    if (!blocked) nit = per;
+    else if (run <= 0) nit = per;
+    else nit = ((nwork + run - 1) / run + gridDim.x - 1) / gridDim.x * run;
+  }
+  // work item of this CTA's iteration i (>= nwork: none)
+  __device__ int64_t at(int64_t i) const {
+    if (!blocked) return blockIdx.x + i * gridDim.x;
+    if (run <= 0) return (int64_t)blockIdx.x * per + i;
+    return ((i / run) * gridDim.x + blockIdx.x) * run + i % run;
+  }
 };
 
 // Per-face geometry, computed once at plan creation by face_geometry_kernel and
@@ -396,16 +422,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   const int nwb = blockDim.x >> 5;
 
   const int64_t nwork = a.n_chunks * a.nc;
-  const int64_t per = (nwork + gridDim.x - 1) / gridDim.x;
-  const int64_t w0 = BLOCKED ? blockIdx.x * per : blockIdx.x;
-  const int64_t w1 = BLOCKED ? (w0 + per < nwork ? w0 + per : nwork) : nwork;
-  const int64_t wstep = BLOCKED ? 1 : gridDim.x;
+  const ChunkWalk walk(nwork, BLOCKED, a.run);
   auto chunk_at = [&](int64_t w) {
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     return __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
   };
   int cur_x = -1, cur_y = -2;
-  for (int64_t w = w0; w < w1; w += wstep) {
+  for (int64_t it = 0; it < walk.nit; ++it) {
+    const int64_t w = walk.at(it);
+    if (w >= nwork) continue;
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     const int4 ch = chunk_at(w);
     if (!RESIDENT && (ch.x != cur_x || ch.y != cur_y)) {
@@ -598,42 +623,41 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
   const int warp = threadIdx.x >> 5;
 
   const int64_t nwork = a.n_chunks * a.nc;
-  const int64_t per = (nwork + gridDim.x - 1) / gridDim.x;
-  const int64_t w0 = BLOCKED ? blockIdx.x * per : blockIdx.x;
-  const int64_t w1 = BLOCKED ? (w0 + per < nwork ? w0 + per : nwork) : nwork;
-  const int64_t wstep = BLOCKED ? 1 : gridDim.x;
+  const ChunkWalk walk(nwork, BLOCKED, a.run);
   auto chunk_at = [&](int64_t w) {
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     return __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
   };
-  // flat per-warp item sequence (chunk w, batch bi); w >= w1 = past the end
+  // flat per-warp item sequence (walk iteration i -> chunk w, batch bi); i >= nit = past the end
   struct Item {
-    int64_t w;
+    int64_t i, w;
     int bi;
     int4 ch;
   };
-  auto first_from = [&](int64_t w) {
-    Item it{w, warp, make_int4(0, 0, 0, 0)};
-    for (; it.w < w1; it.w += wstep) {
+  auto first_from = [&](int64_t i) {
+    Item it{i, 0, warp, make_int4(0, 0, 0, 0)};
+    for (; it.i < walk.nit; ++it.i) {
+      it.w = walk.at(it.i);
+      if (it.w >= nwork) continue;
       it.ch = chunk_at(it.w);
       if (warp < it.ch.w) break;
     }
     return it;
   };
   auto advance = [&](Item it) {
-    if (it.w >= w1) return it;
+    if (it.i >= walk.nit) return it;
     if (it.bi + NW < it.ch.w) {
       it.bi += NW;
       return it;
     }
-    return first_from(it.w + wstep);
+    return first_from(it.i + 1);
   };
-  Item iss = first_from(w0);    // next item to issue
+  Item iss = first_from(0);     // next item to issue
   Item rec = iss;               // item whose cell ids are in (rcm, rcp)
   int rcm = -1, rcp = -1;
   auto load_rec = [&]() {
     rcm = rcp = -1;
-    if (rec.w < w1) {
+    if (rec.i < walk.nit) {
       const int64_t slot = ((int64_t)rec.ch.z + rec.bi) * 8 + fs;
       rcm = __ldg(a.cm + slot);
       rcp = __ldg(a.cp + slot);
@@ -642,7 +666,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
   int islot = 0;
   auto issue = [&]() {   // gathers of item iss (cell ids rcm / rcp) into ring slot islot
     double* r = ring + islot * SLOT;
-    if (iss.w < w1) {
+    if (iss.i < walk.nit) {
       const int comp = a.nc == 1 ? 0 : (int)(iss.w / a.n_chunks);
       const int* pm = sperm + (iss.ch.x / 6) * N;
       const int* pp = sperm + (iss.ch.y / 6) * N;
@@ -684,7 +708,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
   }
   int cslot = 0;
   int cur_x = -1, cur_y = -2;
-  for (int64_t w = w0; w < w1; w += wstep) {
+  for (int64_t wi = 0; wi < walk.nit; ++wi) {
+    const int64_t w = walk.at(wi);
+    if (w >= nwork) continue;
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     const int4 ch = chunk_at(w);
     if (ch.x != cur_x || ch.y != cur_y) {
