@@ -12,9 +12,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# TMF_LIB=debug loads the bounds-checking build (libtetmf_b200_debug.so, _build.py --debug)
-LIB_PATH = os.path.join(_HERE, "libtetmf_b200_debug.so" if os.environ.get("TMF_LIB") == "debug"
-                        else "libtetmf_b200.so")
+# TMF_LIB=debug loads the bounds-checking build (libtetmf_b200_debug.so, _build.py --debug);
+# TMF_LIB=<name> any other in-tree build libtetmf_b200_<name>.so (developer A/B measurements)
+_VARIANT = os.environ.get("TMF_LIB", "")
+LIB_PATH = os.path.join(_HERE, f"libtetmf_b200_{_VARIANT}.so" if _VARIANT else "libtetmf_b200.so")
 
 TMF_OK, TMF_EINVAL, TMF_ECUDA = 0, 1, 2
 TMF_CG_LAPLACE, TMF_DG_SIPG, TMF_DG_HELMHOLTZ = 0, 1, 2

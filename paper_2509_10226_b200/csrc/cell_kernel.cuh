@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
               TMF_CHECK(a, g < 0 || g * a.nc + comp < a.dbg_n_dofs, TMF_DBG_DOF);
               if (g >= 0) {
                 if (PEER)
-                  atomicAdd(peer_dst(a.peer, a.y, g, a.nc, comp), yacc[m][nj][i]);
+                  peer_red_add(peer_dst(a.peer, a.y, g, a.nc, comp), yacc[m][nj][i]);
                 else
                   atomicAdd(a.y + g * a.nc + comp, yacc[m][nj][i]);
               }

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
           en = fma(av[m][ib], yv[m], en);   // av = u at this DoF (0 when masked)
           if (g >= 0) {
             if (PEER)
-              atomicAdd(peer_dst(a.peer, a.y, g, a.nc, comp), yv[m]);
+              peer_red_add(peer_dst(a.peer, a.y, g, a.nc, comp), yv[m]);
             else
               atomicAdd(a.y + (int64_t)g * a.nc + comp, yv[m]);
           }

@@ -76,6 +76,15 @@ __device__ __forceinline__ double* peer_dst(const PeerArgs& p, double* y, int64_
   return y + e * nc + comp;
 }
 
+// Scatter-add into a (possibly peer-mapped) y entry.  The destination pointer comes out of
+// a table, so atomicAdd compiles to the GENERIC returning atomic (ATOM.E.ADD.F64 plus the
+// shared-memory CAS fallback, cuobjdump) and the warp waits for the old value; the address
+// is always global memory, so issue the result-less global RED, system scope because other
+// GPUs add into the same entries over NVLink.
+__device__ __forceinline__ void peer_red_add(double* dst, double v) {
+  asm volatile("red.relaxed.sys.global.add.f64 [%0], %1;\n" ::"l"(dst), "d"(v) : "memory");
+}
+
 struct Vec3 {
   double x, y, z;
 };
