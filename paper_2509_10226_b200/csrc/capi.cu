@@ -958,10 +958,12 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     // and 42 / 151 / 513 for the n_q-point loop), the reference tensor otherwise (P1, mass)
     std::vector<double> modal, ones;
     int eng = P->engine;
-    if (eng == 0) eng = (!P->mass && N >= 10) ? 4 : 3;
+    if (eng == 0) eng = N >= 10 ? 4 : 3;
+    const bool modal_mass = eng == 4 && P->mass;   // mass term as a separate GEMM (MM kernels)
     if (eng == 4) {
       const int p = P->degree, M = p * (p + 1) * (p + 2) / 6;
-      if (P->mass) return bail(fail(TMF_EINVAL, "the modal cell engine has no mass term (Helmholtz: use tensor)"));
+      if (P->mass && (!P->dg || N < 10))
+        return bail(fail(TMF_EINVAL, "the modal cell engine with a mass term is built for DG at P2-P4"));
       if (!build_modal_cell_tables(N, Q, M, Gm, W, modal))
         return bail(fail(TMF_EINVAL, "modal cell engine: gradient tables without the P_{p-1} rank structure"));
       Gm = modal.data();
@@ -980,9 +982,9 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
     TMF_CUDA(tmf::launch_cell(N, Q, P->mass, P->dg, dummy, P->n_sm, 0, &ci, &ok, P->kengine));
     if (!ok) return bail(fail(TMF_EINVAL, "unsupported (n_dofs_per_cell, n_q) = (" +
                                               std::to_string(N) + ", " + std::to_string(Q) + ")"));
-    const int NC = P->mass ? 4 : 3;
+    const int NC = (P->mass && !modal_mass) ? 4 : 3;
     auto E = [&](int c, int q, int j) {
-      if (P->mass) return c == 0 ? V[q * N + j] : Gm[(3 * q + c - 1) * N + j];
+      if (NC == 4) return c == 0 ? V[q * N + j] : Gm[(3 * q + c - 1) * N + j];
       return Gm[(3 * q + c) * N + j];
     };
     std::vector<double> fr;
@@ -992,6 +994,21 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
           [&](int q, int j) { return V[q * N + j]; }, W, fr);
     else
       build_fragments(N, Q, NC, E, W, fr);
+    if (modal_mass) {
+      // B3[kk][nj][lane] = M(4kk + (lane&3), 8nj + (lane>>2)), M = sum_q w_q phi_i phi_j over the
+      // plan's n_q-point rule (the reference's mass_action, numpy_backend.py:79-88), long double
+      const int KK = (N + 3) / 4, NJ = (N + 7) / 8;
+      for (int kk = 0; kk < KK; ++kk)
+        for (int nj = 0; nj < NJ; ++nj)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int i = 4 * kk + (lane & 3), j = 8 * nj + (lane >> 2);
+            long double acc = 0.0L;
+            if (i < N && j < N)
+              for (int q = 0; q < P->Q; ++q)
+                acc += (long double)d->cell_weights[q] * (long double)V[q * N + i] * (long double)V[q * N + j];
+            fr.push_back((double)acc);
+          }
+    }
     if ((int)fr.size() != ci.frag_doubles) return bail(fail(TMF_EINVAL, "internal: fragment size"));
     if ((rc = upload(&P->cell_frags, fr.data(), fr.size(), &total))) return bail(rc);
     P->info.flops_issued = ci.flops_issued;
@@ -1286,6 +1303,8 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       const double M = P->degree * (P->degree + 1) * (P->degree + 2) / 6;
       fe -= nce * (12.0 * nq * nd + 33.0 * nq);
       fe += nce * (12.0 * M * nd + 18.0 * M);
+      // the mass term as one N x N GEMM and a row scaling
+      if (P->mass) fe += nce * (2.0 * nd * nd + 2.0 * nd) - nce * (4.0 * nq * nd + 5.0 * nq + nd);
     }
     if (faces && (P->face_engine == 3 || P->face_engine == 2)) {
       // modal face tables: the point loop on NF unit-weight modes instead of n_qf points

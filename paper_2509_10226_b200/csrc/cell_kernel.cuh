@@ -86,7 +86,9 @@ static __global__ void cell_geometry_kernel(CellGeoArgs a) {
   }
 }
 
-template <int N, int Q, bool MASS>
+// MM: the mass term as its own GEMM (modal Helmholtz): Y += diag(m_e) U M with the exact
+// reference mass matrix M = sum_q w_q phi_i phi_j as KK x NJ more table fragments
+template <int N, int Q, bool MASS, bool MM = false>
 struct CellShape {
   static constexpr int KK = (N + 3) / 4;     // GEMM1 k-steps (DoFs)
   static constexpr int NJ = (N + 7) / 8;     // GEMM2 n-tiles (DoFs)
@@ -107,9 +109,10 @@ struct CellShape {
   static constexpr int NB2T = T * NC * 2 * NJ;
   static constexpr int NB1 = NB1T + (GRP ? 2 * KK : 0) + (PAIR ? KK : 0);
   static constexpr int NB2 = NB2T + (GRP ? NC * NJ : 0) + (PAIR ? 2 * NJ : 0);
-  static constexpr int NFRAG = NB1 + NB2;
+  static constexpr int NB3 = MM ? KK * NJ : 0;   // mass-matrix fragments
+  static constexpr int NFRAG = NB1 + NB2 + NB3;
   static constexpr int SMEM = NFRAG * 32 * 8;
-  static constexpr int DMMA_PER_TILE = NB1 + NB2;
+  static constexpr int DMMA_PER_TILE = NB1 + NB2 + NB3;
   // tiles per warp iteration: two independent 8-cell tiles share every B
   // fragment load (half the LDS traffic) and double the DMMA chains in flight
   static constexpr int MT = (KK + 2 * NJ) <= 7 ? 2 : 1;
@@ -122,9 +125,11 @@ struct CellShape {
 // super-tile AS-1 ahead into its own shared-memory ring, so AS-1 tiles' loads are in
 // flight without holding registers (measured: pays at P4 only)
 // MT_: 8-cell tiles per warp iteration sharing every B-fragment load (0 = CellShape::MT)
-template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0>
+// MM: mass term as a separate GEMM on the gathered u (CellShape; Helmholtz on the modal tables)
+template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0, bool MM = false>
 __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
-  using S = CellShape<N, Q, MASS>;
+  static_assert(!(MASS && MM), "the mass term is either in the point loop or a separate GEMM");
+  using S = CellShape<N, Q, MASS, MM>;
   constexpr int MT = MT_ ? MT_ : S::MT;
   static_assert(AS == 0 || !PEER, "the async ring has no peer gathers");
   extern __shared__ __align__(16) double smem[];
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
       G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
       G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
-      mdet[m] = MASS ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
+      mdet[m] = (MASS || MM) ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
     }
   };
   // async ring: per stage MT x (KK x 32 gathered u, then 8 cells x 8 geometry doubles)
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
         const double* gg = r + MT * S::KK * 32 + m * 64 + cs * 8;
 #pragma unroll
         for (int i = 0; i < 6; ++i) G[m][i] = gg[i];
-        mdet[m] = MASS ? gg[6] : 0.0;
+        mdet[m] = (MASS || MM) ? gg[6] : 0.0;
       }
       slot = slot + 1 == AS ? 0 : slot + 1;
     } else {
@@ -274,6 +279,24 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
     for (int m = 0; m < MT; ++m)
 #pragma unroll
       for (int nj = 0; nj < S::NJ; ++nj) yacc[m][nj][0] = yacc[m][nj][1] = 0.0;
+    if (MM) {
+      // mass term: (U M) rows scaled by the cell's m_e = mass_scale det J (operator.py:86-88)
+#pragma unroll
+      for (int kk = 0; kk < S::KK; ++kk)
+#pragma unroll
+        for (int nj = 0; nj < S::NJ; ++nj) {
+          const double b = sB2[(S::NB2 + kk * S::NJ + nj) * 32 + lane];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) dmma(yacc[m][nj], av[m][kk], b);
+        }
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int nj = 0; nj < S::NJ; ++nj) {
+          yacc[m][nj][0] *= mdet[m];
+          yacc[m][nj][1] *= mdet[m];
+        }
+    }
 
     auto gemm1 = [&](int t, double (&v)[MT][S::NC][2]) {
 #pragma unroll

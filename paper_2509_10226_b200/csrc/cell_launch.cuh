@@ -28,14 +28,14 @@ static cudaError_t persistent_grid(K kern, int block, int smem, int64_t warps_of
 }
 
 // MT_: 8-cell tiles per warp iteration sharing every B-fragment load (0 = CellShape default)
-template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0>
+template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0, bool MM = false>
 static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
-  using S = CellShape<N, Q, MASS>;
+  using S = CellShape<N, Q, MASS, MM>;
   constexpr int MT = MT_ ? MT_ : S::MT;
   // tables + the per-warp async rings
   constexpr int SMEM = S::SMEM + (AS > 0 ? AS * MT * (S::KK * 32 + 64) * 8 * (BLOCK / 32) : 0);
   static_assert(SMEM <= 227 * 1024, "shared memory");
-  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, PEER, AS, MT_>;
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, PEER, AS, MT_, MM>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   const int64_t supertiles = ((a.n_cells + 8 * MT - 1) / (8 * MT)) * a.nc;
   int64_t blocks = 1;
@@ -133,6 +133,14 @@ static cudaError_t cell_engine_launch(bool mass, bool dg, const CellArgs& a, int
     return launch_tensor<N, false, true>(a, n_sm, st, info);
   }
   if (!dg) return launch_points<N, Q, false, false>(a, n_sm, st, info);
+  if constexpr (Q < N && N >= 10) {
+    // Helmholtz on the modal tables: the mass term as its own GEMM (cell_kernel.cuh MM)
+    if (mass) {
+      if (N == 10) return launch_cell_v<N, Q, false, true, 512, false, 0, 0, true>(a, n_sm, st, info);
+      if (N == 20) return launch_cell_v<N, Q, false, true, 768, false, 0, 0, true>(a, n_sm, st, info);
+      return launch_cell_v<N, Q, false, true, 512, false, 0, 0, true>(a, n_sm, st, info);
+    }
+  }
   if (mass) return launch_points<N, Q, true, true>(a, n_sm, st, info);
   return launch_points<N, Q, false, true>(a, n_sm, st, info);
 }

@@ -38,10 +38,10 @@ ENGINE_CODE = {"dmma": 1, "tensor": 3, "modal": 4}
 def test_gpu_cell_engines_match_golden(name, engine):
     """Every cell engine against every golden, P4 included: the quadrature-point loop (the
     reference's algorithm), the reference tensor (point sum precontracted per plan) and
-    the modal tables (the point loop on M = dim P_{p-1} exact unit-weight modes; Laplace
-    cell terms only -- Helmholtz plans refuse it)."""
+    the modal tables (the point loop on M = dim P_{p-1} exact unit-weight modes; for
+    Helmholtz at P2-P4 the mass term is a separate GEMM, P1 Helmholtz plans refuse it)."""
     g = load_golden(name)
-    if engine == "modal" and str(g["kind"]).startswith("helm"):
+    if engine == "modal" and str(g["kind"]).startswith("helm") and "_p1_" in name:
         with pytest.raises(ValueError, match="modal"):
             operator_from_fixture(g, cell_engine=engine)
         return
@@ -53,11 +53,12 @@ def test_gpu_cell_engines_match_golden(name, engine):
 
 def test_gpu_default_engines():
     """auto: block assembly (5) for scalar CG Laplace at P1, modal tables for the other
-    Laplace cell terms at P2-P4, the reference tensor at P1 and for Helmholtz; modal faces
-    at P2-P4, the point loop at P1."""
+    cell terms at P2-P4 (Helmholtz: plus the mass GEMM), the reference tensor for DG at P1;
+    modal faces at P2-P4, the point loop at P1."""
     for name, cell, face in [("cg_p1_n3_gm_dir2", 5, 0), ("cg_p2_n8_gm", 4, 0), ("cg_p3_n4_ref_dir", 4, 0),
                              ("cg_p4_n3_gm", 4, 0), ("cg3_p2_n3_ref_dir", 4, 0),
-                             ("dg_p1_n3_gm_dir", 3, 1), ("dg_p3_n3_gm_dir", 4, 3), ("helmk_p2_n3_gm_dir", 3, 3)]:
+                             ("dg_p1_n3_gm_dir", 3, 1), ("dg_p3_n3_gm_dir", 4, 3), ("helmk_p2_n3_gm_dir", 4, 3),
+                             ("helm3_p2_n2_gm_none", 4, 3), ("helmk_p1_n3_ref_dir", 3, 1)]:
         A = operator_from_fixture(load_golden(name))
         assert A.info["cell_engine"] == cell, name
         assert A.info["face_engine"] == face, name

@@ -142,6 +142,26 @@ def test_c4_kappa_helmholtz_p2_64cubed_value_parity():
     assert rel_l2(y, ref) <= 1e-12
 
 
+@pytest.mark.parametrize("engine", ["modal", "tensor"])
+@pytest.mark.parametrize("p,n", [(2, 12), (3, 8), (4, 6)])
+def test_kappa_helmholtz_cell_engines_vs_oracle(p, n, engine):
+    """kappa-Helmholtz at P2-P4 (no reference golden above P2): the modal cell engine with the
+    mass term as its own GEMM, and the reference tensor, against the oracle."""
+    from paper_2509_10226_b200 import dofmap as D, operator as op
+
+    m = _mesh(n, True)
+    geo, bas = _tables(p)
+    dm = D.build_dof_map(m, p, "dg")
+    sipg = op.baseline_sipg_tau(m, p, 1.0 / n)
+    kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
+    u = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
+    A = op.KappaHelmholtzOperator(m, dm, geo, bas, sipg, kap, 0.7, op.OperatorConfig(cell_engine=engine),
+                                  dirichlet_ids=(0, 2, 5))
+    assert A.info["cell_engine"] == {"modal": 4, "tensor": 3}[engine]
+    ref = _dg_oracle(m, dm, geo, bas, sipg, (0, 2, 5), u, kappa=kap, mass_scale=0.7)
+    assert rel_l2(A.apply(u), ref) <= 1e-12
+
+
 def test_c5_jacobi_pcg_p3_24cubed_history():
     """C5's solver (CG P3, homogeneous Dirichlet, RHS U[-1,1] zero on constrained rows,
     100 Jacobi-PCG iterations) against the oracle PCG on the oracle apply."""
