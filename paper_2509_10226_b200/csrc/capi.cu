@@ -309,6 +309,7 @@ struct tmf_plan {
   int face_engine = 0;             // (desc.flags >> 17) & 3: 0 by degree, 1 quadrature points,
                                    // 2 modal in the flat layout, 3 modal in the split-mode layout
   int* face_perm = nullptr;
+  std::vector<int> face_perm_h;   // host copy (FaceArgs::permc)
   int* cells = nullptr;
   int* dofs = nullptr;
   int* fix_list = nullptr;
@@ -420,6 +421,7 @@ struct tmf_plan {
     a.cp = boundary ? nullptr : if_cp;
     a.geo = boundary ? bf_geo : if_geo;
     a.perm = face_perm;
+    for (size_t i = 0; i < face_perm_h.size() && i < sizeof(a.permc) / sizeof(int); ++i) a.permc[i] = face_perm_h[i];
     a.n_chunks = boundary ? n_bf_chunks : n_if_chunks;
     a.n_dpc = N;
     a.nc = nc;
@@ -1111,6 +1113,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       std::copy(on.begin(), on.end(), perm.begin() + lf * N);
     }
     if ((rc = upload(&P->face_perm, perm.data(), perm.size(), &total))) return bail(rc);
+    P->face_perm_h.assign(perm.begin(), perm.end());
     // face engine by default: modal at P2-P4, the point loop at P1 (decided by measurement)
     int fe = P->face_engine;
     if (fe == 0) fe = N >= 10 ? 3 : 1;

@@ -56,6 +56,9 @@ struct FaceArgs {
   PeerArgs peer;                      // multi-GPU: ghost cells' u read from their owner (n_own = cells)
   int hier = 0;                       // host-side: frags hold the split-mode layout (HierShape) -> HIER kernels
   int run = 0;                        // BLOCKED kernels: chunk-run length of the CTA walk (ChunkWalk), 0 = one run per CTA
+  // the (4, n_dpc) gather orders again, as a kernel parameter: face_apply_kernel reads them
+  // from the constant bank (LDC), off the L1 data pipe its gathers and REDs saturate
+  int permc[4 * 35] = {};
   TMF_DBG_FIELDS
 };
 
@@ -448,8 +451,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
     }
     const double* Fm = RESIDENT ? smem + (int64_t)ch.x * S::NFRAG * 32 : smem;
     const double* Fp = RESIDENT ? smem + (int64_t)(BOUNDARY ? 0 : ch.y) * S::NFRAG * 32 : Fm + S::NFRAG * 32;
-    const int* perm_m = a.perm + (ch.x / 6) * N;                  // gather order, minus side
-    const int* perm_p = a.perm + (BOUNDARY ? 0 : ch.y / 6) * N;   // plus side
+    const int pm0 = (ch.x / 6) * N;                  // gather order, minus side
+    const int pp0 = (BOUNDARY ? 0 : ch.y / 6) * N;   // plus side
 
     // Software pipeline over the warp's batches.  PF 2: the next batch's face
     // record, geometry and gathered u are loaded while the current batch
@@ -484,18 +487,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
         nam[kk] = 0.0;
         nap[kk] = 0.0;
         if (n_cm >= 0 && j < N) {
-          TMF_CHECK(a, n_cm < a.dbg_n_cells && __ldg(perm_m + j) < N, TMF_DBG_CELL);
-          TMF_CHECK(a, BOUNDARY || (n_cp >= 0 && (PEER || n_cp < a.dbg_n_cells) && __ldg(perm_p + j) < N),
+          TMF_CHECK(a, n_cm < a.dbg_n_cells && a.permc[pm0 + j] < N, TMF_DBG_CELL);
+          TMF_CHECK(a, BOUNDARY || (n_cp >= 0 && (PEER || n_cp < a.dbg_n_cells) && a.permc[pp0 + j] < N),
                     TMF_DBG_CELL);
-          nam[kk] = __ldg(a.u + ((int64_t)n_cm * N + __ldg(perm_m + j)) * a.nc + comp);
+          nam[kk] = __ldg(a.u + ((int64_t)n_cm * N + a.permc[pm0 + j]) * a.nc + comp);
           if (!BOUNDARY) {
             // DG ghost cell (partitioned apply): its u is read from the owner rank
             if (PEER && n_cp >= a.peer.n_own) {
               const int64_t gc = n_cp - a.peer.n_own;
               nap[kk] = __ldg(a.peer.u[__ldg(a.peer.rank + gc)] +
-                              ((int64_t)__ldg(a.peer.idx + gc) * N + __ldg(perm_p + j)) * a.nc + comp);
+                              ((int64_t)__ldg(a.peer.idx + gc) * N + a.permc[pp0 + j]) * a.nc + comp);
             } else {
-              nap[kk] = __ldg(a.u + ((int64_t)n_cp * N + __ldg(perm_p + j)) * a.nc + comp);
+              nap[kk] = __ldg(a.u + ((int64_t)n_cp * N + a.permc[pp0 + j]) * a.nc + comp);
             }
           }
         }
@@ -585,8 +588,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
           for (int i = 0; i < 2; ++i) {
             const int j = 8 * nj + 2 * q4 + i;
             if (j < N) {
-              atomicAdd(a.y + ((int64_t)c_m * N + __ldg(perm_m + j)) * a.nc + comp, ym[nj][i]);
-              if (!BOUNDARY) atomicAdd(a.y + ((int64_t)c_p * N + __ldg(perm_p + j)) * a.nc + comp, yp[nj][i]);
+              atomicAdd(a.y + ((int64_t)c_m * N + a.permc[pm0 + j]) * a.nc + comp, ym[nj][i]);
+              if (!BOUNDARY) atomicAdd(a.y + ((int64_t)c_p * N + a.permc[pp0 + j]) * a.nc + comp, yp[nj][i]);
             }
           }
       }

@@ -98,6 +98,9 @@ static cudaError_t launch_face_h(const FaceArgs& a, int n_sm, cudaStream_t st, F
     if (variant == 3) return launch_face_v<N, QF, false, 1, 3, 256, false, false, true, true>(a, n_sm, st, info);
     if (variant == 4) return launch_face_v<N, QF, false, 1, 1, 1024, false, false, true, true>(a, n_sm, st, info);
     if (variant == 5) return launch_face_a<N, QF, 3, 3, 256, true>(a, n_sm, st);
+    if (variant == 6) return launch_face_v<N, QF, false, 1, 1, 768, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 7) return launch_face_v<N, QF, false, 1, 1, 640, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 8) return launch_face_v<N, QF, false, 0, 1, 768, false, false, true, true>(a, n_sm, st, info);
     return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true>(a, n_sm, st, info);
   } else {
     return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
