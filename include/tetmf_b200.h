@@ -121,6 +121,13 @@ int tmf_plan_get_info(const tmf_plan* plan, tmf_plan_info* info);
  * fire).  The release library returns TMF_EINVAL. */
 int tmf_debug_poke_dof(tmf_plan* plan, int64_t slot, int32_t value);
 
+/* Test hook (host only, no GPU): the order in which CTA `block` of a `grid`-CTA face launch
+ * visits the `n_work` face chunks (face_kernel.cuh ChunkWalk: round-robin, one contiguous run
+ * per CTA, or runs of `run` chunks dealt round-robin).  Writes the visited work items to
+ * out[0..*n_out) (capacity `cap`); entries >= n_work are skipped as the kernel skips them. */
+int tmf_debug_chunk_walk(int64_t n_work, int64_t grid, int64_t block, int blocked, int run,
+                         int64_t* out, int64_t cap, int64_t* n_out);
+
 /* y = A u on device pointers (length n_global_dofs), ordered on `stream`
  * (a cudaStream_t, NULL = legacy default stream).  y is overwritten. */
 int tmf_apply(tmf_plan* plan, const double* u, double* y, void* stream);

@@ -125,6 +125,8 @@ def lib():
         L.tmf_last_error.restype = C.c_char_p
         L.tmf_version.restype = C.c_char_p
         L.tmf_debug_poke_dof.argtypes = [C.c_void_p, C.c_int64, C.c_int32]
+        L.tmf_debug_chunk_walk.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, _v, C.c_int64, _v]
+        L.tmf_debug_chunk_walk.restype = C.c_int
         for name in ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_apply",
                      "tmf_apply_host", "tmf_apply_host_async", "tmf_apply_host_multi", "tmf_apply_stages", "tmf_apply_timed", "tmf_diagonal", "tmf_pcg",
                      "tmf_hierarchical_reorder", "tmf_build_faces", "tmf_build_cg_dofs",
@@ -147,7 +149,7 @@ EXPORTED = ("tmf_plan_create", "tmf_plan_destroy", "tmf_plan_get_info", "tmf_app
             "tmf_transfer_create_points", "tmf_transfer_destroy",
             "tmf_prolongate", "tmf_restrict", "tmf_chebyshev_step", "tmf_vec_axpby", "tmf_apply_f32",
             "tmf_prolongate_f32", "tmf_restrict_f32", "tmf_chebyshev_step_f32", "tmf_vec_axpby_f32", "tmf_last_error",
-            "tmf_version", "tmf_debug_poke_dof")
+            "tmf_version", "tmf_debug_poke_dof", "tmf_debug_chunk_walk")
 
 
 def check(rc: int) -> None:

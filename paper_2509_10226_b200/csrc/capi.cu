@@ -1439,6 +1439,21 @@ int tmf_plan_destroy(tmf_plan* plan) {
   return TMF_OK;
 }
 
+int tmf_debug_chunk_walk(int64_t n_work, int64_t grid, int64_t block, int blocked, int run, int64_t* out,
+                         int64_t cap, int64_t* n_out) {
+  if (n_work < 0 || grid < 1 || block < 0 || block >= grid || !out || !n_out) return fail(TMF_EINVAL, "bad argument");
+  const tmf::ChunkWalk walk(n_work, blocked != 0, run, grid, block);
+  int64_t n = 0;
+  for (int64_t i = 0; i < walk.nit; ++i) {
+    const int64_t w = walk.at(i);
+    if (w >= n_work) continue;
+    if (n >= cap) return fail(TMF_EINVAL, "output capacity");
+    out[n++] = w;
+  }
+  *n_out = n;
+  return TMF_OK;
+}
+
 int tmf_debug_poke_dof(tmf_plan* P, int64_t slot, int32_t value) {
 #ifdef TMF_DEBUG_CHECKS
   if (!P || P->dg || slot < 0 || slot >= P->n_cells * P->N) return fail(TMF_EINVAL, "bad poke");

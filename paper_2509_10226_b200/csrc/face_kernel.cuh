@@ -71,19 +71,20 @@ struct FaceArgs {
 //     u / y rows in L2 (DG P3 64^3 reordered: faces -10 %), while a run still shares tables.
 struct ChunkWalk {
   int64_t nwork, nit, per;
+  int64_t grid, block;   // CTAs of the launch, this CTA
   int run;
   bool blocked;
-  __device__ ChunkWalk(int64_t nwork_, bool blocked_, int run_) : nwork(nwork_), run(run_), blocked(blocked_) {
-    per = (nwork + gridDim.x - 1) / gridDim.x;
-    if (!blocked) nit = per;
-    else if (run <= 0) nit = per;
-    else nit = ((nwork + run - 1) / run + gridDim.x - 1) / gridDim.x * run;
+  __host__ __device__ ChunkWalk(int64_t nwork_, bool blocked_, int run_, int64_t grid_, int64_t block_)
+      : nwork(nwork_), grid(grid_), block(block_), run(run_), blocked(blocked_) {
+    per = (nwork + grid - 1) / grid;
+    if (!blocked || run <= 0) nit = per;
+    else nit = ((nwork + run - 1) / run + grid - 1) / grid * run;
   }
   // work item of this CTA's iteration i (>= nwork: none)
-  __device__ int64_t at(int64_t i) const {
-    if (!blocked) return blockIdx.x + i * gridDim.x;
-    if (run <= 0) return (int64_t)blockIdx.x * per + i;
-    return ((i / run) * gridDim.x + blockIdx.x) * run + i % run;
+  __host__ __device__ int64_t at(int64_t i) const {
+    if (!blocked) return block + i * grid;
+    if (run <= 0) return block * per + i;
+    return ((i / run) * grid + block) * run + i % run;
   }
 };
 
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   const int nwb = blockDim.x >> 5;
 
   const int64_t nwork = a.n_chunks * a.nc;
-  const ChunkWalk walk(nwork, BLOCKED, a.run);
+  const ChunkWalk walk(nwork, BLOCKED, a.run, gridDim.x, blockIdx.x);
   auto chunk_at = [&](int64_t w) {
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     return __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));
@@ -626,7 +627,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
   const int warp = threadIdx.x >> 5;
 
   const int64_t nwork = a.n_chunks * a.nc;
-  const ChunkWalk walk(nwork, BLOCKED, a.run);
+  const ChunkWalk walk(nwork, BLOCKED, a.run, gridDim.x, blockIdx.x);
   auto chunk_at = [&](int64_t w) {
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     return __ldg(a.chunks + (w - (int64_t)comp * a.n_chunks));

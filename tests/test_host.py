@@ -37,6 +37,28 @@ def test_plan_create_rejects_bad_descriptors():
         _lib.check(_lib.lib().tmf_plan_create(ctypes.byref(d), ctypes.byref(plan)))
 
 
+@pytest.mark.parametrize("blocked,run", [(0, 0), (1, 0), (1, 1), (1, 2), (1, 8)])
+@pytest.mark.parametrize("n_work,grid", [(0, 4), (1, 296), (295, 296), (296, 296), (1000, 296), (12345, 148), (37, 5)])
+def test_face_chunk_walk_visits_every_chunk_once(n_work, grid, blocked, run):
+    """The CTA walks of the face kernels (face_kernel.cuh ChunkWalk, through the host test
+    hook): over all CTAs every chunk exactly once; blocked runs are consecutive chunks."""
+    L = _lib.lib()
+    seen = []
+    for b in range(grid):
+        out = (ctypes.c_int64 * (n_work + 1))()
+        n = ctypes.c_int64()
+        _lib.check(L.tmf_debug_chunk_walk(n_work, grid, b, blocked, run, out, n_work + 1, ctypes.byref(n)))
+        w = list(out[: n.value])
+        if blocked and run == 0:
+            assert w == list(range(w[0], w[0] + len(w))) if w else True
+        if blocked and run > 0:
+            for k in range(0, len(w), run):   # each run: consecutive chunks starting at a multiple of run
+                r = w[k:k + run]
+                assert r[0] % run == 0 and r == list(range(r[0], r[0] + len(r)))
+        seen += w
+    assert sorted(seen) == list(range(n_work))
+
+
 # ------------------------------------------------------------------ mesh / faces
 @pytest.mark.parametrize("n,seed", [(1, 0), (2, 5), (3, 1)])
 def test_build_faces_matches_oracle(n, seed):
