@@ -242,23 +242,53 @@ def reference_arm(args, steps, warmup, step_s, workers=None):
 
 
 # ----------------------------------------------------------------- GPU arm
-def build_problem(n, p, reorder, cache={}):
+_MESH_FIELDS = ("vertices", "cells", "interior_faces", "boundary_faces")
+
+
+def build_problem(n, p, reorder, cache={}, ns=None):
+    """The C2 problem (mesh, CG DoF map, tables).  ``ns`` (a distributed.NodeShared, N > 1): the
+    global mesh and DoF maps are built by the node's first rank only and mapped read-only by
+    the others, instead of every rank building the whole global problem."""
     from paper_2509_10226_b200 import basis as B, dofmap as D, mesh as M, quadrature as Q
     from paper_2509_10226_b200.geometry import GeometryData
 
-    key = (n, reorder)
-    if key not in cache:
+    def make_mesh():
         m = M.kuhn_cube_mesh(n, seed=0)
         if reorder:
             from paper_2509_10226_b200.reorder import reorder_mesh
 
             m = reorder_mesh(m)   # hierarchical cell order + first-touch vertex numbering
-        cache[key] = m
+        return m
+
+    key = (n, reorder)
+    if key not in cache:
+        if ns is None:
+            cache[key] = make_mesh()
+        else:
+            a = ns.get(f"mesh_{n}_{int(reorder)}", lambda: {k: getattr(make_mesh(), k) for k in _MESH_FIELDS})
+            cache[key] = M.TetMesh(*(a[k] for k in _MESH_FIELDS))
     m = cache[key]
     cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
     bas = B.tabulate_basis(p, cr, fr)
-    dm = D.build_dof_map(m, p, "cg")
+    if ns is None:
+        dm = D.build_dof_map(m, p, "cg")
+    else:
+        def make_dofs():
+            d = D.build_dof_map(m, p, "cg")
+            return {"cell_dofs": d.cell_dofs, "dirichlet_mask": d.dirichlet_mask}
+
+        a = ns.get(f"cg_{n}_{int(reorder)}_{p}", make_dofs)
+        dm = D.DoFMap("cg", p, 1, len(a["dirichlet_mask"]), a["cell_dofs"], a["dirichlet_mask"])
     return m, dm, GeometryData("affine", cr, fr, None, None, None, None), bas
+
+
+def node_shared(world):
+    """distributed.NodeShared for this job when it has more than one rank (else None)."""
+    if world <= 1:
+        return None
+    from paper_2509_10226_b200.distributed import NodeShared
+
+    return NodeShared(int(os.environ.get("LOCAL_RANK", "0")), NodeShared.job_token())
 
 
 def measure_link(problems, reps):
@@ -322,18 +352,25 @@ def gpu_bench(args, rank, world):
     dist_path = world > 1 or args.dist
     transport = os.environ.get("TMF_TRANSPORT", "p2p")
     problems = []
+    ns = node_shared(world)
     for reorder in (False, True):
         for p in DEGREES:
-            m, dm, geo, bas = build_problem(n_glob, p, reorder)
-            u_glob = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
+            m, dm, geo, bas = build_problem(n_glob, p, reorder, ns=ns)
+            ng = dm.n_global_dofs
+
+            def make_u():
+                return {"u": np.random.default_rng(1).uniform(-1, 1, ng)}
+
+            u_glob = make_u()["u"] if ns is None else ns.get(f"u_{ng}", make_u)["u"]
             if not dist_path:
                 A = local = op.CgPoissonOperator(m, dm, geo, bas, cfg)
                 ids = None
             else:
                 from paper_2509_10226_b200.distributed import DistributedCgOperator, partition_cells
 
-                A = DistributedCgOperator(m, dm, geo, bas, rank, world, part=partition_cells(m, world),
-                                          transport=transport)
+                part = (partition_cells(m, world) if ns is None else
+                        ns.get(f"part_{n_glob}_{int(reorder)}", lambda: {"part": partition_cells(m, world)})["part"])
+                A = DistributedCgOperator(m, dm, geo, bas, rank, world, part=part, transport=transport)
                 if transport == "p2p":
                     ok = 1.0
                     try:
@@ -366,6 +403,10 @@ def gpu_bench(args, rank, world):
             problems.append(dict(p=p, reorder=reorder, A=A, local=local, u=u, y=y, u_pin=u_pin, y_pin=y_pin,
                                  ndof=len(u_host), ndof_global=dm.n_global_dofs, ids=ids,
                                  key=f"p{p}{'_reordered' if reorder else ''}"))
+    if ns is not None:   # every rank has extracted its subdomains: drop the shared global arrays
+        del m, dm, u_glob
+        torch.distributed.barrier()
+        ns.close()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     p2p_check = None
@@ -524,24 +565,39 @@ def c4_strong(args, rank, world):
 
     t0 = time.time()
     n, p = args.c4_n, 2
-    m = M.kuhn_cube_mesh(n, seed=0)
-    m = M.apply_cell_permutation(m, hierarchical_reorder(m))
+
+    def make_global():
+        # the global mesh, its partition, kappa and the input vector: built by the node's first
+        # rank only when there are several (distributed.NodeShared), mapped by the others
+        g = M.kuhn_cube_mesh(n, seed=0)
+        g = M.apply_cell_permutation(g, hierarchical_reorder(g))
+        out = {k: getattr(g, k) for k in _MESH_FIELDS}
+        out["part"] = DD.partition_cells(g, world)
+        out["kappa"] = 10.0 ** np.random.default_rng(2).uniform(-1, 1, g.n_cells)
+        out["u"] = np.random.default_rng(1).uniform(-1, 1, g.n_cells * 10)   # P2 DG: 10 DoFs per cell
+        return out
+
+    ns = node_shared(world)
+    a = make_global() if ns is None else ns.get(f"c4_{n}", make_global)
+    m = M.TetMesh(*(a[k] for k in _MESH_FIELDS))
     cr, fr = Q.make_cell_quadrature(p), Q.make_face_quadrature(p)
     bas = B.tabulate_basis(p, cr, fr)
     geo = GeometryData("affine", cr, fr, None, None, None, None)
     dm = D.build_dof_map(m, p, "dg")
-    kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
     sipg = op.baseline_sipg_tau(m, p, 1.0 / n)
     transport = os.environ.get("TMF_TRANSPORT", "p2p") if world > 1 else "nccl"
     A = DD.DistributedDgOperator(m, dm, geo, bas, sipg, rank, world, kind="helmholtz", dirichlet_ids=range(6),
-                                 kappa=kap, part=DD.partition_cells(m, world), transport=transport)
+                                 kappa=a["kappa"], part=a["part"], transport=transport)
     if transport == "p2p":
         A.connect_ipc()
     ids = A.owned_global_ids()
     ng = dm.n_global_dofs
-    del m, kap
+    u = torch.from_numpy(np.ascontiguousarray(a["u"][ids])).cuda()
+    del m, a
+    if ns is not None:
+        torch.distributed.barrier()
+        ns.close()
     setup_s = time.time() - t0
-    u = torch.from_numpy(np.ascontiguousarray(np.random.default_rng(1).uniform(-1, 1, ng)[ids])).cuda()
     y = torch.empty_like(u)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     for _ in range(3):

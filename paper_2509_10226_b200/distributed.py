@@ -35,7 +35,81 @@ from .mesh import TetMesh, build_faces
 from .reference import FACE_VERTICES_ARR
 
 __all__ = ["partition_cells", "CgSubdomain", "DgSubdomain", "build_cg_subdomain",
-           "build_dg_subdomain", "HaloExchange"]
+           "build_dg_subdomain", "HaloExchange", "NodeShared"]
+
+
+class NodeShared:
+    """Global setup arrays built ONCE per node and mapped read-only by the other ranks.
+
+    The subdomain builders need the global mesh, DoF map and partition (the reference's
+    first-encounter DoF numbering is a global construction).  With one process per GPU,
+    every rank building them itself costs world x the host time and memory (a 128^3 mesh
+    and its DoF maps are several GB).  ``get(tag, build)``: the node's first rank calls
+    ``build() -> {name: ndarray}`` and publishes the arrays as ``.npy`` files under
+    ``/dev/shm`` (atomic rename); the other ranks wait for the directory and
+    ``np.load(..., mmap_mode="r")`` them, so the pages are shared.  ``token`` must be the
+    same on all ranks of one job and unique to it (``NodeShared.job_token()`` broadcasts
+    one); ``close()`` on the publishing rank removes the files (mapped pages stay valid).
+    """
+
+    def __init__(self, local_rank: int, token: str, root: str = "/dev/shm", timeout_s: float = 7200.0):
+        import os
+
+        self.publisher = int(local_rank) == 0
+        self.dir = os.path.join(root, f"tmf_b200_{token}")
+        self.timeout_s = timeout_s
+        self._cache = {}
+        if self.publisher:
+            os.makedirs(self.dir, exist_ok=True)
+
+    @staticmethod
+    def job_token(group=None) -> str:
+        """A token unique to this job, agreed by all ranks (torch.distributed must be up;
+        without it: a token private to this process)."""
+        import os
+        import time
+
+        tok = [f"{os.getpid()}_{time.time_ns()}"]
+        try:
+            import torch.distributed as dist
+
+            if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+                dist.broadcast_object_list(tok, src=0, group=group)
+        except ImportError:
+            pass
+        return tok[0]
+
+    def get(self, tag: str, build):
+        import os
+        import time
+
+        if tag in self._cache:
+            return self._cache[tag]
+        d = os.path.join(self.dir, tag)
+        if self.publisher:
+            arrays = {k: np.ascontiguousarray(v) for k, v in build().items()}
+            tmp = d + ".tmp"
+            os.makedirs(tmp, exist_ok=True)
+            for k, a in arrays.items():
+                np.save(os.path.join(tmp, k + ".npy"), a)
+            os.rename(tmp, d)
+            self._cache[tag] = arrays
+            return arrays
+        t0 = time.time()
+        while not os.path.isdir(d):
+            if time.time() - t0 > self.timeout_s:
+                raise TimeoutError(f"NodeShared: {d} was not published within {self.timeout_s} s")
+            time.sleep(0.05)
+        self._cache[tag] = {f[:-4]: np.load(os.path.join(d, f), mmap_mode="r") for f in sorted(os.listdir(d))
+                            if f.endswith(".npy")}
+        return self._cache[tag]
+
+    def close(self):
+        import shutil
+
+        self._cache = {}
+        if self.publisher:
+            shutil.rmtree(self.dir, ignore_errors=True)
 
 
 def partition_cells(mesh: TetMesh, k: int) -> np.ndarray:

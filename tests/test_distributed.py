@@ -97,11 +97,36 @@ def _worker(rank, world, port, kind, n, p, q):
         from paper_2509_10226_b200 import distributed as DD
         from paper_2509_10226_b200.solvers import pcg_loop
 
-        m, dm, geo, bas, sipg, dids = _problem(kind, n, p)
+        shared = kind.endswith("_shared")
+        kind = kind.replace("_shared", "")
+        if shared:
+            # global setup built by rank 0 only and mapped read-only by the others (NodeShared)
+            from paper_2509_10226_b200.dofmap import DoFMap
+            from paper_2509_10226_b200.mesh import TetMesh
+
+            ns = DD.NodeShared(rank, DD.NodeShared.job_token())
+
+            def build():
+                assert rank == 0, "only the node's first rank builds"
+                m0, dm0 = _problem(kind, n, p)[:2]
+                return {"vertices": m0.vertices, "cells": m0.cells, "interior_faces": m0.interior_faces,
+                        "boundary_faces": m0.boundary_faces, "cell_dofs": dm0.cell_dofs,
+                        "dirichlet_mask": dm0.dirichlet_mask, "part": DD.partition_cells(m0, world)}
+
+            a = ns.get("problem", build)
+            if rank != 0:
+                assert not a["cells"].flags.writeable   # mapped, not copied
+            _, _, geo, bas, sipg, dids = _problem(kind, 2, p)   # tables only (tiny mesh)
+            m = TetMesh(a["vertices"], a["cells"], a["interior_faces"], a["boundary_faces"])
+            dm = DoFMap("cg", p, 1, len(a["dirichlet_mask"]), a["cell_dofs"], a["dirichlet_mask"])
+            part = a["part"]
+        else:
+            m, dm, geo, bas, sipg, dids = _problem(kind, n, p)
+            part = None
         u = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
         out = {}
         if kind.startswith("cg"):
-            A = DD.DistributedCgOperator(m, dm, geo, bas, rank, world, device="cpu",
+            A = DD.DistributedCgOperator(m, dm, geo, bas, rank, world, part=part, device="cpu",
                                          local_factory=_cg_local_factory)
             ids = A.owned_global_ids
             y = A.apply(torch.from_numpy(u[ids])).numpy()
@@ -140,6 +165,9 @@ def _worker(rank, world, port, kind, n, p, q):
             assert np.array_equal(yl[: A.n_owned].numpy(), y)
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
+        if shared:
+            dist.barrier()
+            ns.close()
         if rank == 0:
             q.put(gathered)
     finally:
@@ -171,11 +199,12 @@ def _assemble(parts, key, n):
 
 
 @pytest.mark.parametrize("kind,world,n,p", [("cg", 2, 4, 2), ("cg_dir", 2, 4, 3), ("cg_dir", 4, 4, 1),
-                                            ("dg", 2, 3, 2), ("helm", 4, 3, 1)])
+                                            ("dg", 2, 3, 2), ("helm", 4, 3, 1), ("cg_shared", 2, 4, 2)])
 def test_partitioned_apply_matches_global(kind, world, n, p):
     from oracle import ref_apply
 
     parts = _run(kind, world, n, p)
+    kind = kind.replace("_shared", "")   # same problem, global setup published by rank 0 (NodeShared)
     m, dm, geo, bas, sipg, dids = _problem(kind, n, p)
     u = np.random.default_rng(1).uniform(-1, 1, dm.n_global_dofs)
     y = _assemble(parts, "apply", dm.n_global_dofs)
@@ -263,3 +292,50 @@ def test_ghost_owner_maps_point_at_the_owners_entries():
                 sel = s.ghost_owner == o
                 assert np.all(s.ghost_index[sel] < dsubs[o].n_owned_cells)
                 assert np.array_equal(dsubs[o].cell_l2g[s.ghost_index[sel]], gh[sel])
+
+
+def _bench_shared_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+
+        ns = bench.node_shared(world)
+        assert ns is not None and ns.publisher == (rank == 0)
+        ok = True
+        for reorder in (False, True):
+            for p in (1, 3):
+                m, dm, _, _ = bench.build_problem(5, p, reorder, cache={}, ns=ns)
+                m0, dm0, _, _ = bench.build_problem(5, p, reorder, cache={})
+                ok &= all(np.array_equal(getattr(m, k), getattr(m0, k)) for k in bench._MESH_FIELDS)
+                ok &= np.array_equal(dm.cell_dofs, dm0.cell_dofs) and np.array_equal(dm.dirichlet_mask, dm0.dirichlet_mask)
+                ok &= dm.n_global_dofs == dm0.n_global_dofs
+                if rank != 0:
+                    ok &= not m.cells.flags.writeable and not dm.cell_dofs.flags.writeable
+        shared_dir = ns.dir
+        dist.barrier()
+        ns.close()
+        dist.barrier()
+        res = [None] * world
+        dist.all_gather_object(res, (bool(ok), os.path.isdir(shared_dir)))
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_builds_the_global_problem_once_per_node():
+    """bench.py at N > 1: the global mesh / DoF maps come from the node's first rank through
+    distributed.NodeShared, bit-identical to a rank's own build, and are removed afterwards."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_shared_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res == [(True, False), (True, False)]
