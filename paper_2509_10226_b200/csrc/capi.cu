@@ -59,6 +59,11 @@ int upload(T** dst, const T* src, size_t n, size_t* total) {
 // a remainder of 1..2 points is one pair group (CellShape::PAIR), columns (point, component):
 //   B1p[kk][lane] = E_{n&3}(8T + (n>>2), 4kk + (lane&3)),  n = lane>>2
 //   B2p[i][nj][lane] = w_q E_{2(k&1)+i}(q = 8T + (k>>1), 8nj + (lane>>2)),  k = lane&3
+// GEMM2-type fragments (B2, B2g, B2p and the mass fragments): column n = lane>>2 of n-tile nj
+// is DoF col_dof(nj, n) = 4(2nj + (n&1)) + (n>>1), so a lane's accumulators are the DoFs
+// 4kk + (lane&3) it gathered (cell_kernel.cuh: the scatter reuses the gather's indices).
+inline int col_dof(int nj, int n) { return 4 * (2 * nj + (n & 1)) + (n >> 1); }
+
 template <typename F>
 void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<double>& out) {
   const int KK = (N + 3) / 4, NJ = (N + 7) / 8, R = Q % 8;
@@ -90,21 +95,21 @@ void build_fragments(int N, int Q, int NC, F E, const double* w, std::vector<dou
       for (int i = 0; i < 2; ++i)
         for (int nj = 0; nj < NJ; ++nj)
           for (int lane = 0; lane < 32; ++lane) {
-            const int q = 8 * t + 2 * (lane & 3) + i, j = 8 * nj + (lane >> 2);
+            const int q = 8 * t + 2 * (lane & 3) + i, j = col_dof(nj, lane >> 2);
             out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
           }
   if (grp)
     for (int c = 0; c < NC; ++c)
       for (int nj = 0; nj < NJ; ++nj)
         for (int lane = 0; lane < 32; ++lane) {
-          const int q = 8 * T + (lane & 3), j = 8 * nj + (lane >> 2);
+          const int q = 8 * T + (lane & 3), j = col_dof(nj, lane >> 2);
           out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
         }
   if (pair)
     for (int i = 0; i < 2; ++i)
       for (int nj = 0; nj < NJ; ++nj)
         for (int lane = 0; lane < 32; ++lane) {
-          const int k = lane & 3, c = 2 * (k & 1) + i, q = 8 * T + (k >> 1), j = 8 * nj + (lane >> 2);
+          const int k = lane & 3, c = 2 * (k & 1) + i, q = 8 * T + (k >> 1), j = col_dof(nj, lane >> 2);
           out.push_back(q < Q && j < N && c < NC ? w[q] * E(c, q, j) : 0.0);
         }
 }
@@ -1003,7 +1008,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
       for (int kk = 0; kk < KK; ++kk)
         for (int nj = 0; nj < NJ; ++nj)
           for (int lane = 0; lane < 32; ++lane) {
-            const int i = 4 * kk + (lane & 3), j = 8 * nj + (lane >> 2);
+            const int i = 4 * kk + (lane & 3), j = col_dof(nj, lane >> 2);
             long double acc = 0.0L;
             if (i < N && j < N)
               for (int q = 0; q < P->Q; ++q)

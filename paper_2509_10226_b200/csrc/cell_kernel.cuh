@@ -16,6 +16,10 @@
 //   GEMM2  Y^T[8, N] += D^T[8, (t,c,i,lane&3)] . Ew[(t,c,i,k), N]
 //          the C fragment of GEMM1 *is* the A fragment of GEMM2 once the K
 //          index of GEMM2 is ordered (t, c, i, lane&3): no shuffles, no smem.
+//          GEMM2's output columns are ordered so that column 2q+i of n-tile nj is
+//          DoF 4(2nj+i)+q: a lane ends up with the results of exactly the DoFs
+//          4kk + (lane&3) whose u it gathered, and scatters them through the index
+//          registers of the gather (no second index load).
 //
 // Both B operands are constant tables, pre-swizzled on the host into
 // lane-major fragments (frag[f][lane]) and staged once per CTA in shared
@@ -196,8 +200,9 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       mdet[m] = (MASS || MM) ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
     }
   };
-  // async ring: per stage MT x (KK x 32 gathered u, then 8 cells x 8 geometry doubles)
-  constexpr int STAGE = MT * (S::KK * 32 + 64);
+  // async ring: per stage MT x (KK x 32 gathered u, 8 cells x 8 geometry doubles, and the
+  // KK x 32 gather indices as ints, read back by the scatter)
+  constexpr int STAGE = MT * (S::KK * 32 + 64 + S::KK * 16);
   double* ring = smem + S::NFRAG * 32 + (threadIdx.x >> 5) * (AS > 0 ? AS : 1) * STAGE;
   auto issue = [&](int64_t t, int slot) {
     double* r = ring + slot * STAGE;
@@ -214,6 +219,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(r + (m * S::KK + kk) * 32 + lane)),
                      "l"(src), "r"(g >= 0 ? 8 : 0) : "memory");
+        if (!DG) reinterpret_cast<int*>(r + MT * (S::KK * 32 + 64))[(m * S::KK + kk) * 32 + lane] = g;
       }
       // lane copies 16-byte piece q4 of its cell's 64-byte geometry record
       const double* gsrc = a.cgeo + 8 * (ok ? c : 0) + 2 * q4;
@@ -249,6 +255,8 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       cell[m] = ((st - (int64_t)comp * cst) * MT + m) * 8 + cs;
       valid[m] = cell[m] < a.n_cells;
     }
+    int cidx[MT][S::KK];               // this tile's gather indices (CG scatter; AS: in the ring slot)
+    const int* ridx = nullptr;
     if (AS > 0) {
       // refill the slot of tile st + (AS-1) step (the slot the previous tile was read
       // from: every lane has its values in registers), then wait for this tile's group
@@ -268,9 +276,16 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
         for (int i = 0; i < 6; ++i) G[m][i] = gg[i];
         mdet[m] = (MASS || MM) ? gg[6] : 0.0;
       }
+      ridx = reinterpret_cast<const int*>(r + MT * (S::KK * 32 + 64));   // refilled only next iteration
       slot = slot + 1 == AS ? 0 : slot + 1;
     } else {
       load_data(st, av, G, mdet);
+      if (!DG) {
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int kk = 0; kk < S::KK; ++kk) cidx[m][kk] = nidx[m][kk];
+      }
       load_indices(st + step);
     }
 
@@ -387,21 +402,14 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       }
     };
     auto dgemm2p = [&](const double (&v)[MT][2]) {
+      static_assert(!(S::PAIR && MASS), "no rule with a mass term in the point loop leaves a 1-2 point remainder");
       double d[MT][2];
       const bool odd = (q4 & 1) != 0;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         const double x0 = __shfl_xor_sync(0xffffffffu, v[m][0], 1);
         const double x1 = __shfl_xor_sync(0xffffffffu, v[m][1], 1);
-        if (MASS) {
-          // components (value, g0 | g1, g2): even lanes integrate value and d0, odd lanes d1 and d2
-          const double val = odd ? x0 : v[m][0], g0 = odd ? x1 : v[m][1];
-          const double g1 = odd ? v[m][0] : x0, g2 = odd ? v[m][1] : x1;
-          const double a0 = odd ? G[m][1] : 0.0, a1 = odd ? G[m][3] : 0.0, a2 = odd ? G[m][4] : 0.0;
-          const double b0 = odd ? G[m][2] : G[m][0], b1 = odd ? G[m][4] : G[m][1], b2 = odd ? G[m][5] : G[m][2];
-          d[m][0] = odd ? a0 * g0 + a1 * g1 + a2 * g2 : mdet[m] * val;
-          d[m][1] = b0 * g0 + b1 * g1 + b2 * g2;
-        } else {
+        {
           // components (g0, g1 | g2, pad): even lanes integrate d0 and d1, odd lanes d2
           const double g0 = odd ? x0 : v[m][0], g1 = odd ? x1 : v[m][1], g2 = odd ? v[m][0] : x0;
           const double a0 = odd ? G[m][2] : G[m][0], a1 = odd ? G[m][4] : G[m][1], a2 = odd ? G[m][5] : G[m][2];
@@ -436,7 +444,8 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       dgemm2p(vp);
     }
 
-    // ---- scatter / store: lane owns DoFs 8nj + 2q4 + {0,1}
+    // ---- scatter / store: accumulator (nj, i) of a lane is DoF 4(2nj+i) + q4, the DoF of
+    // its gather k-step kk = 2nj+i
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
       if (!valid[m]) continue;
@@ -444,13 +453,16 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       for (int nj = 0; nj < S::NJ; ++nj)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const int j = 8 * nj + 2 * q4 + i;
+          constexpr int KKc = S::KK;
+          const int kk = 2 * nj + i;
+          if (kk >= KKc) continue;
+          const int j = 4 * kk + q4;
           if (j < N) {
             if (DG) {
               TMF_CHECK(a, (cell[m] * N + j) * a.nc + comp < a.dbg_n_dofs, TMF_DBG_DOF);
               a.y[(cell[m] * N + j) * a.nc + comp] = yacc[m][nj][i];
             } else {
-              const int64_t g = __ldg(a.dofs + cell[m] * N + j);
+              const int64_t g = AS > 0 ? ridx[(m * S::KK + kk) * 32 + lane] : cidx[m][kk < KKc ? kk : 0];
               TMF_CHECK(a, g < 0 || g * a.nc + comp < a.dbg_n_dofs, TMF_DBG_DOF);
               if (g >= 0) {
                 if (PEER)

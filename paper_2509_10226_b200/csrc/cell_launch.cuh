@@ -33,7 +33,7 @@ static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, C
   using S = CellShape<N, Q, MASS, MM>;
   constexpr int MT = MT_ ? MT_ : S::MT;
   // tables + the per-warp async rings
-  constexpr int SMEM = S::SMEM + (AS > 0 ? AS * MT * (S::KK * 32 + 64) * 8 * (BLOCK / 32) : 0);
+  constexpr int SMEM = S::SMEM + (AS > 0 ? AS * MT * (S::KK * 32 + 64 + S::KK * 16) * 8 * (BLOCK / 32) : 0);
   static_assert(SMEM <= 227 * 1024, "shared memory");
   auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, PEER, AS, MT_, MM>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
@@ -133,16 +133,23 @@ static cudaError_t cell_engine_launch(bool mass, bool dg, const CellArgs& a, int
     return launch_tensor<N, false, true>(a, n_sm, st, info);
   }
   if (!dg) return launch_points<N, Q, false, false>(a, n_sm, st, info);
-  if constexpr (Q < N && N >= 10) {
-    // Helmholtz on the modal tables: the mass term as its own GEMM (cell_kernel.cuh MM)
+  if constexpr (Q < N) {
+    // Helmholtz on the modal tables: the mass term as its own GEMM (cell_kernel.cuh MM); the
+    // plan refuses modal + mass at P1, and no kernel with the mass term in a modal point loop exists
     if (mass) {
-      if (N == 10) return launch_cell_v<N, Q, false, true, 512, false, 0, 0, true>(a, n_sm, st, info);
-      if (N == 20) return launch_cell_v<N, Q, false, true, 768, false, 0, 0, true>(a, n_sm, st, info);
-      return launch_cell_v<N, Q, false, true, 512, false, 0, 0, true>(a, n_sm, st, info);
+      if constexpr (N >= 10) {
+        if (N == 10) return launch_cell_v<N, Q, false, true, 512, false, 0, 0, true>(a, n_sm, st, info);
+        if (N == 20) return launch_cell_v<N, Q, false, true, 768, false, 0, 0, true>(a, n_sm, st, info);
+        return launch_cell_v<N, Q, false, true, 512, false, 0, 0, true>(a, n_sm, st, info);
+      } else {
+        return cudaErrorInvalidValue;
+      }
     }
+    return launch_points<N, Q, false, true>(a, n_sm, st, info);
+  } else {
+    if (mass) return launch_points<N, Q, true, true>(a, n_sm, st, info);
+    return launch_points<N, Q, false, true>(a, n_sm, st, info);
   }
-  if (mass) return launch_points<N, Q, true, true>(a, n_sm, st, info);
-  return launch_points<N, Q, false, true>(a, n_sm, st, info);
 }
 
 #define TMF_CELL_TU(NN, QQ)                                                                        \
