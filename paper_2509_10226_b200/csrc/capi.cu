@@ -254,7 +254,7 @@ void build_face_fragments(int N, int NF, int Q, F E, const double* w, std::vecto
     for (int c = 0; c < 4; ++c)
       for (int nj = 0; nj < (c < 3 ? NJF : NJ); ++nj)
         for (int lane = 0; lane < 32; ++lane) {
-          const int q = 4 * g + (lane & 3), j = 8 * nj + (lane >> 2);
+          const int q = 4 * g + (lane & 3), j = col_dof(nj, lane >> 2);   // the lane order of the gather
           out.push_back(q < Q && j < N ? w[q] * E(c, q, j) : 0.0);
         }
 }
@@ -285,7 +285,7 @@ void build_face_fragments_hier(F E, std::vector<double>& out) {
     for (int s = 0; s < S::NS; ++s)
       for (int r = (r3 ? 3 : 0); r < (r3 ? 4 : 3); ++r)
         for (int nj = 0; nj < (r < 3 ? S::NJF : S::NJ); ++nj)
-          for (int lane = 0; lane < 32; ++lane) out.push_back(val(lane & 3, s, r, 8 * nj + (lane >> 2)));
+          for (int lane = 0; lane < 32; ++lane) out.push_back(val(lane & 3, s, r, col_dof(nj, lane >> 2)));
 }
 
 }  // namespace

@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
         for (int nj = 0; nj < S::NJ; ++nj)
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            const int j = 8 * nj + 2 * q4 + i;
+            const int j = 4 * (2 * nj + i) + q4;   // GEMM2 columns in the gather's lane order (capi.cu col_dof)
             if (j < N) {
               atomicAdd(a.y + ((int64_t)c_m * N + a.permc[pm0 + j]) * a.nc + comp, ym[nj][i]);
               if (!BOUNDARY) atomicAdd(a.y + ((int64_t)c_p * N + a.permc[pp0 + j]) * a.nc + comp, yp[nj][i]);
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
         for (int nj = 0; nj < S::NJ; ++nj)
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            const int j = 8 * nj + 2 * q4 + i;
+            const int j = 4 * (2 * nj + i) + q4;   // GEMM2 columns in the gather's lane order (capi.cu col_dof)
             if (j < N) {
               atomicAdd(a.y + ((int64_t)c_m * N + perm_m[j]) * a.nc + comp, ym[nj][i]);
               atomicAdd(a.y + ((int64_t)c_p * N + perm_p[j]) * a.nc + comp, yp[nj][i]);
