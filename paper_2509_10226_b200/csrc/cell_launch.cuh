@@ -118,6 +118,8 @@ static cudaError_t launch_points(const CellArgs& a, int n_sm, cudaStream_t st, C
   if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768>(a, n_sm, st, info);
   if constexpr (N == 35 && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, false, 2>(a, n_sm, st, info);
   if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640>(a, n_sm, st, info);
+  // DG P2 on the modal tables: 3-stage gather ring (cells -23 % at 64^3: the rows stream from HBM)
+  if constexpr (N == 10 && DG && !MASS && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, false, 3>(a, n_sm, st, info);
   if (N == 10 && DG) return launch_cell_v<N, Q, MASS, DG, 512>(a, n_sm, st, info);
   return launch_cell_v<N, Q, MASS, DG, BLOCK>(a, n_sm, st, info);
 }
@@ -138,7 +140,9 @@ static cudaError_t cell_engine_launch(bool mass, bool dg, const CellArgs& a, int
     // plan refuses modal + mass at P1, and no kernel with the mass term in a modal point loop exists
     if (mass) {
       if constexpr (N >= 10) {
-        if (N == 10) return launch_cell_v<N, Q, false, true, 512, false, 0, 0, true>(a, n_sm, st, info);
+        // P2: 3-stage gather ring, two 256-thread CTAs per SM (DG rows stream from HBM; cells
+        // -19 % at 96^3, profiles/r02/dg_cell_ring.jsonl; P3 gains nothing from a ring)
+        if (N == 10) return launch_cell_v<N, Q, false, true, 256, false, 3, 0, true>(a, n_sm, st, info);
         if (N == 20) return launch_cell_v<N, Q, false, true, 768, false, 0, 0, true>(a, n_sm, st, info);
         return launch_cell_v<N, Q, false, true, 512, false, 0, 0, true>(a, n_sm, st, info);
       } else {
