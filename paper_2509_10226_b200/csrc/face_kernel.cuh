@@ -407,12 +407,19 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 // RESIDENT: all 24 (lf, code) tables are staged once per CTA, so a chunk never restages
 // and the warps never wait for each other (small tables: P1 / P2 modal faces)
 // HIER: the split-mode modal layout (HierShape, interior faces only; QF is not used)
+// SG: the batch's 8 face records (64 B each) are staged through a per-warp shared-memory
+// slot with ONE coalesced 16-byte cp.async per lane and read back as broadcast LDS.64s,
+// instead of four LDG.128s per lane that every lane of a face repeats (32 -> 15 L1
+// wavefronts per batch, 8 fewer registers in the prefetch state)
 template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool PEER = false, bool RESIDENT = false, bool HIER = false>
+          bool PEER = false, bool RESIDENT = false, bool HIER = false, bool SG = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   static_assert(!HIER || !BOUNDARY, "the split-mode layout is for interior faces");
   using S = FaceShapeSel<N, QF, HIER>;
   extern __shared__ __align__(16) double smem[];
+  // staged geometry: two 64-double slots per warp behind the tables
+  double* sgeo = smem + (RESIDENT ? 24 : (BOUNDARY ? 1 : 2)) * S::NFRAG * 32 + (threadIdx.x >> 5) * 128;
+  int gslot = 0;
   if (RESIDENT) {
     const double2* src = reinterpret_cast<const double2*>(a.frags);
     double2* dst = reinterpret_cast<double2*>(smem);
@@ -472,7 +479,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
       }
     };
     auto fetch_data = [&](int bi) {
-      if (bi < ch.w) {
+      if (SG) {
+        if (bi < ch.w)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(sgeo + (gslot ^ 1) * 64 + 2 * lane)),
+                       "l"(a.geo + ((int64_t)ch.z + bi) * 64 + 2 * lane) : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        gslot ^= 1;
+      } else if (bi < ch.w) {
         const int64_t slot = ((int64_t)ch.z + bi) * 8 + fs;
         const double2* gp = reinterpret_cast<const double2*>(a.geo + slot * 8);
 #pragma unroll
@@ -517,6 +531,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
       for (int kk = 0; kk < S::KK; ++kk) {
         am[kk] = nam[kk];
         ap[kk] = nap[kk];
+      }
+      if (SG) {
+        // the slot filled by this batch's fetch_data (PF 2: one iteration ago)
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        const double* g8 = sgeo + gslot * 64 + fs * 8;
+#pragma unroll
+        for (int i = 0; i < 7; ++i) ng[i] = g8[i];
+        // (this slot is refilled two fetches from now, after the next batch's __syncwarp)
       }
       const double hm[3] = {ng[0], ng[1], ng[2]};   // s m~- / 2   (boundary: s m~)
       const double hp[3] = {ng[3], ng[4], ng[5]};   // s m~+ / 2

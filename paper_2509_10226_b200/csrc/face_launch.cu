@@ -11,12 +11,13 @@
 namespace tmf {
 
 template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool PEER = false, bool RESIDENT = false, bool HIER = false>
+          bool PEER = false, bool RESIDENT = false, bool HIER = false, bool SG = false>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShapeSel<N, QF, HIER>;
-  constexpr int SMEM = RESIDENT ? 24 * S::NFRAG * 32 * 8 : (BND ? 1 : 2) * S::NFRAG * 32 * 8;
+  constexpr int SMEM = (RESIDENT ? 24 * S::NFRAG * 32 * 8 : (BND ? 1 : 2) * S::NFRAG * 32 * 8) +
+                       (SG ? (BLOCK / 32) * 128 * 8 : 0);   // + the per-warp staged face records
   static_assert(SMEM <= 227 * 1024, "shared memory");
-  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, PEER, RESIDENT, HIER>;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, PEER, RESIDENT, HIER, SG>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   if (info) {
     info->nfrag = S::NFRAG;
@@ -91,6 +92,8 @@ static cudaError_t launch_face_h(const FaceArgs& a, int n_sm, cudaStream_t st, F
     if (variant == 3) return launch_face_v<N, QF, false, 1, 1, 768, false, false, true, true>(a, n_sm, st, info);
     if (variant == 4) return launch_face_a<N, QF, 3, 2, 256, true>(a, n_sm, st);
     if (variant == 5) return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
+    if (variant == 10) return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 11) return launch_face_v<N, QF, false, 2, 3, 256, true, false, false, true, true>(a, n_sm, st, info);
     return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true>(a, n_sm, st, info);
   } else if constexpr (N == 10) {
     if (variant == 1) return launch_face_v<N, QF, false, 1, 2, 512, false, false, true, true>(a, n_sm, st, info);
@@ -101,6 +104,9 @@ static cudaError_t launch_face_h(const FaceArgs& a, int n_sm, cudaStream_t st, F
     if (variant == 6) return launch_face_v<N, QF, false, 1, 1, 768, false, false, true, true>(a, n_sm, st, info);
     if (variant == 7) return launch_face_v<N, QF, false, 1, 1, 640, false, false, true, true>(a, n_sm, st, info);
     if (variant == 8) return launch_face_v<N, QF, false, 0, 1, 768, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 10) return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true, true>(a, n_sm, st, info);
+    if (variant == 11) return launch_face_v<N, QF, false, 2, 1, 512, false, false, true, true, true>(a, n_sm, st, info);
+    if (variant == 12) return launch_face_v<N, QF, false, 1, 1, 640, false, false, true, true, true>(a, n_sm, st, info);
     return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true>(a, n_sm, st, info);
   } else {
     return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
