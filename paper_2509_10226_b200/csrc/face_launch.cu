@@ -92,9 +92,9 @@ static cudaError_t launch_face_h(const FaceArgs& a, int n_sm, cudaStream_t st, F
     if (variant == 3) return launch_face_v<N, QF, false, 1, 1, 768, false, false, true, true>(a, n_sm, st, info);
     if (variant == 4) return launch_face_a<N, QF, 3, 2, 256, true>(a, n_sm, st);
     if (variant == 5) return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
-    if (variant == 10) return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true, true>(a, n_sm, st, info);
-    if (variant == 11) return launch_face_v<N, QF, false, 2, 3, 256, true, false, false, true, true>(a, n_sm, st, info);
-    return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true>(a, n_sm, st, info);
+    if (variant == 10) return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true>(a, n_sm, st, info);
+    // default: full prefetch, face records staged through shared memory (SG: faces -1.9 %)
+    return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true, true>(a, n_sm, st, info);
   } else if constexpr (N == 10) {
     if (variant == 1) return launch_face_v<N, QF, false, 1, 2, 512, false, false, true, true>(a, n_sm, st, info);
     if (variant == 2) return launch_face_v<N, QF, false, 2, 1, 512, false, false, true, true>(a, n_sm, st, info);
@@ -104,9 +104,6 @@ static cudaError_t launch_face_h(const FaceArgs& a, int n_sm, cudaStream_t st, F
     if (variant == 6) return launch_face_v<N, QF, false, 1, 1, 768, false, false, true, true>(a, n_sm, st, info);
     if (variant == 7) return launch_face_v<N, QF, false, 1, 1, 640, false, false, true, true>(a, n_sm, st, info);
     if (variant == 8) return launch_face_v<N, QF, false, 0, 1, 768, false, false, true, true>(a, n_sm, st, info);
-    if (variant == 10) return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true, true>(a, n_sm, st, info);
-    if (variant == 11) return launch_face_v<N, QF, false, 2, 1, 512, false, false, true, true, true>(a, n_sm, st, info);
-    if (variant == 12) return launch_face_v<N, QF, false, 1, 1, 640, false, false, true, true, true>(a, n_sm, st, info);
     return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true>(a, n_sm, st, info);
   } else {
     return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
