@@ -192,12 +192,13 @@ struct FaceShapeSel<N, QF, true> : HierShape<N> {};
 
 // Interior-face arithmetic of one 8-face batch in the split-mode layout: GEMM1 of both
 // sides, the modal face_qpoint (numpy_backend.py:91-105 on modes), GEMM2 of both sides.
-template <int N>
-__device__ __forceinline__ void face_hier_core(const double (&am)[HierShape<N>::KK], const double (&ap)[HierShape<N>::KK],
-                                               const double (&hm)[3], const double (&hp)[3], double stau,
-                                               const double* __restrict__ Fm, const double* __restrict__ Fp,
-                                               int lane, double (&ym)[HierShape<N>::NJ][2],
-                                               double (&yp)[HierShape<N>::NJ][2]) {
+// Bm(f) / Bp(f): fragment f of the minus / plus table for this lane (shared memory, or
+// registers loaded once per chunk: face_apply_kernel RT)
+template <int N, class TM, class TP>
+__device__ __forceinline__ void face_hier_core_t(const double (&am)[HierShape<N>::KK], const double (&ap)[HierShape<N>::KK],
+                                                 const double (&hm)[3], const double (&hp)[3], double stau,
+                                                 TM Bm, TP Bp, int lane, double (&ym)[HierShape<N>::NJ][2],
+                                                 double (&yp)[HierShape<N>::NJ][2]) {
   using S = HierShape<N>;
   const int q4 = lane & 3;
   double vm[S::NS][4], vp[S::NS][4];
@@ -210,9 +211,8 @@ __device__ __forceinline__ void face_hier_core(const double (&am)[HierShape<N>::
     double cm[2] = {0.0, 0.0}, cp[2] = {0.0, 0.0};
 #pragma unroll
     for (int kk = 0; kk < S::KKF; ++kk) {
-      const int f = S::b1f(t, kk) * 32 + lane;
-      dmma(cm, am[kk], Fm[f]);
-      dmma(cp, ap[kk], Fp[f]);
+      dmma(cm, am[kk], Bm(S::b1f(t, kk)));
+      dmma(cp, ap[kk], Bp(S::b1f(t, kk)));
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -225,9 +225,8 @@ __device__ __forceinline__ void face_hier_core(const double (&am)[HierShape<N>::
     double cm[2] = {0.0, 0.0}, cp[2] = {0.0, 0.0};
 #pragma unroll
     for (int kk = 0; kk < S::KK; ++kk) {
-      const int f = S::b1d(d, kk) * 32 + lane;
-      dmma(cm, am[kk], Fm[f]);
-      dmma(cp, ap[kk], Fp[f]);
+      dmma(cm, am[kk], Bm(S::b1d(d, kk)));
+      dmma(cp, ap[kk], Bp(S::b1d(d, kk)));
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -274,11 +273,21 @@ __device__ __forceinline__ void face_hier_core(const double (&am)[HierShape<N>::
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int nj = 0; nj < (r < 3 ? S::NJF : S::NJ); ++nj) {
-        const int f = S::b2(s, r, nj) * 32 + lane;
-        dmma(ym[nj], om[r], Fm[f]);
-        dmma(yp[nj], op[r], Fp[f]);
+        dmma(ym[nj], om[r], Bm(S::b2(s, r, nj)));
+        dmma(yp[nj], op[r], Bp(S::b2(s, r, nj)));
       }
   }
+}
+
+template <int N>
+__device__ __forceinline__ void face_hier_core(const double (&am)[HierShape<N>::KK], const double (&ap)[HierShape<N>::KK],
+                                               const double (&hm)[3], const double (&hp)[3], double stau,
+                                               const double* __restrict__ Fm, const double* __restrict__ Fp,
+                                               int lane, double (&ym)[HierShape<N>::NJ][2],
+                                               double (&yp)[HierShape<N>::NJ][2]) {
+  face_hier_core_t<N>(
+      am, ap, hm, hp, stau, [&](int f) { return Fm[f * 32 + lane]; }, [&](int f) { return Fp[f * 32 + lane]; },
+      lane, ym, yp);
 }
 
 // A_lf^-1 for the face frame (reference vertices (0,0,0),(1,0,0),(0,1,0),(0,0,1)).
@@ -412,13 +421,17 @@ __global__ void face_geometry_kernel(FaceGeoArgs a) {
 // instead of four LDG.128s per lane that every lane of a face repeats (32 -> 15 L1
 // wavefronts per batch, 8 fewer registers in the prefetch state)
 template <int N, int QF, bool BOUNDARY, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool PEER = false, bool RESIDENT = false, bool HIER = false, bool SG = false>
+          bool PEER = false, bool RESIDENT = false, bool HIER = false, bool SG = false, bool RT = false>
 __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
   static_assert(!HIER || !BOUNDARY, "the split-mode layout is for interior faces");
+  // RT: both tables' fragments of a chunk are loaded into registers once and serve all of the
+  // warp's batches in the chunk (small tables: split-mode P2, 2 x 10 fragments)
+  static_assert(!RT || HIER, "register tables are for the split-mode layout");
   using S = FaceShapeSel<N, QF, HIER>;
   extern __shared__ __align__(16) double smem[];
   // staged geometry: two 64-double slots per warp behind the tables
-  double* sgeo = smem + (RESIDENT ? 24 : (BOUNDARY ? 1 : 2)) * S::NFRAG * 32 + (threadIdx.x >> 5) * 128;
+  double* sgeo = smem + ((RT && !RESIDENT) ? 0 : (RESIDENT ? 24 : (BOUNDARY ? 1 : 2))) * S::NFRAG * 32 +
+                 (threadIdx.x >> 5) * 128;
   int gslot = 0;
   if (RESIDENT) {
     const double2* src = reinterpret_cast<const double2*>(a.frags);
@@ -444,7 +457,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
     if (w >= nwork) continue;
     const int comp = a.nc == 1 ? 0 : (int)(w / a.n_chunks);
     const int4 ch = chunk_at(w);
-    if (!RESIDENT && (ch.x != cur_x || ch.y != cur_y)) {
+    // RT without RESIDENT: the register tables are loaded straight from global memory (L1 / L2
+    // hold the 24 small tables), nothing is staged and the CTA needs no table shared memory
+    constexpr bool GT = RT && !RESIDENT;
+    if (!RESIDENT && !GT && (ch.x != cur_x || ch.y != cur_y)) {
       cur_x = ch.x;
       cur_y = ch.y;
       __syncthreads();  // previous chunk's warps are done with the staged tables
@@ -457,8 +473,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
       }
       __syncthreads();
     }
-    const double* Fm = RESIDENT ? smem + (int64_t)ch.x * S::NFRAG * 32 : smem;
-    const double* Fp = RESIDENT ? smem + (int64_t)(BOUNDARY ? 0 : ch.y) * S::NFRAG * 32 : Fm + S::NFRAG * 32;
+    const double* Fm = GT ? a.frags + (int64_t)ch.x * S::NFRAG * 32
+                          : RESIDENT ? smem + (int64_t)ch.x * S::NFRAG * 32 : smem;
+    const double* Fp = GT ? a.frags + (int64_t)(BOUNDARY ? 0 : ch.y) * S::NFRAG * 32
+                          : RESIDENT ? smem + (int64_t)(BOUNDARY ? 0 : ch.y) * S::NFRAG * 32 : Fm + S::NFRAG * 32;
     const int pm0 = (ch.x / 6) * N;                  // gather order, minus side
     const int pp0 = (BOUNDARY ? 0 : ch.y / 6) * N;   // plus side
 
@@ -519,6 +537,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
         }
       }
     };
+    double bm[RT ? S::NFRAG : 1], bp[RT ? S::NFRAG : 1];
+    if (RT && warp < ch.w) {
+#pragma unroll
+      for (int f = 0; f < S::NFRAG; ++f) {
+        bm[f] = GT ? __ldg(Fm + f * 32 + lane) : Fm[f * 32 + lane];
+        bp[f] = GT ? __ldg(Fp + f * 32 + lane) : Fp[f * 32 + lane];
+      }
+    }
     if (PF >= 1) fetch_rec(warp);
     if (PF == 2) fetch_data(warp);
 
@@ -551,7 +577,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
 #pragma unroll
       for (int nj = 0; nj < S::NJ; ++nj) ym[nj][0] = ym[nj][1] = yp[nj][0] = yp[nj][1] = 0.0;
 
-      if constexpr (HIER) {
+      if constexpr (HIER && RT) {
+        face_hier_core_t<N>(
+            am, ap, hm, hp, stau, [&](int f) { return bm[f]; }, [&](int f) { return bp[f]; }, lane, ym, yp);
+      } else if constexpr (HIER) {
         face_hier_core<N>(am, ap, hm, hp, stau, Fm, Fp, lane, ym, yp);
       } else {
 #pragma unroll

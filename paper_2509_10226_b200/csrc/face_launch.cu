@@ -11,13 +11,13 @@
 namespace tmf {
 
 template <int N, int QF, bool BND, int PF = 2, int MINB = 2, int BLOCK = 256, bool BLOCKED = false,
-          bool PEER = false, bool RESIDENT = false, bool HIER = false, bool SG = false>
+          bool PEER = false, bool RESIDENT = false, bool HIER = false, bool SG = false, bool RT = false>
 static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, FaceLaunchInfo* info) {
   using S = FaceShapeSel<N, QF, HIER>;
-  constexpr int SMEM = (RESIDENT ? 24 * S::NFRAG * 32 * 8 : (BND ? 1 : 2) * S::NFRAG * 32 * 8) +
+  constexpr int SMEM = ((RT && !RESIDENT) ? 0 : RESIDENT ? 24 * S::NFRAG * 32 * 8 : (BND ? 1 : 2) * S::NFRAG * 32 * 8) +
                        (SG ? (BLOCK / 32) * 128 * 8 : 0);   // + the per-warp staged face records
   static_assert(SMEM <= 227 * 1024, "shared memory");
-  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, PEER, RESIDENT, HIER, SG>;
+  auto kern = face_apply_kernel<N, QF, BND, PF, MINB, BLOCK, BLOCKED, PEER, RESIDENT, HIER, SG, RT>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   if (info) {
     info->nfrag = S::NFRAG;
@@ -96,15 +96,14 @@ static cudaError_t launch_face_h(const FaceArgs& a, int n_sm, cudaStream_t st, F
     // default: full prefetch, face records staged through shared memory (SG: faces -1.9 %)
     return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true, true>(a, n_sm, st, info);
   } else if constexpr (N == 10) {
-    if (variant == 1) return launch_face_v<N, QF, false, 1, 2, 512, false, false, true, true>(a, n_sm, st, info);
-    if (variant == 2) return launch_face_v<N, QF, false, 2, 1, 512, false, false, true, true>(a, n_sm, st, info);
-    if (variant == 3) return launch_face_v<N, QF, false, 1, 3, 256, false, false, true, true>(a, n_sm, st, info);
-    if (variant == 4) return launch_face_v<N, QF, false, 1, 1, 1024, false, false, true, true>(a, n_sm, st, info);
-    if (variant == 5) return launch_face_a<N, QF, 3, 3, 256, true>(a, n_sm, st);
-    if (variant == 6) return launch_face_v<N, QF, false, 1, 1, 768, false, false, true, true>(a, n_sm, st, info);
-    if (variant == 7) return launch_face_v<N, QF, false, 1, 1, 640, false, false, true, true>(a, n_sm, st, info);
-    if (variant == 8) return launch_face_v<N, QF, false, 0, 1, 768, false, false, true, true>(a, n_sm, st, info);
-    return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true>(a, n_sm, st, info);
+    // P2: both tables of a chunk (2 x 10 fragments) live in REGISTERS, loaded once per chunk from
+    // global memory (no table shared memory, no barriers); small CTAs (2 warps, 8 per SM) so a
+    // warp serves 16 batches per table load; face records staged through shared memory.
+    // kappa-Helmholtz P2 96^3 faces 1.032 -> 0.895 ms (-13 %) against round 2's resident-table
+    // 512-thread kernel (variant 1), profiles/r02/face_register_tables.jsonl
+    if (variant == 1) return launch_face_v<N, QF, false, 1, 1, 512, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 2) return launch_face_v<N, QF, false, 1, 4, 128, false, false, false, true, true, true>(a, n_sm, st, info);
+    return launch_face_v<N, QF, false, 1, 8, 64, false, false, false, true, true, true>(a, n_sm, st, info);
   } else {
     return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
   }
