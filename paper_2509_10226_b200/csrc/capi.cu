@@ -529,14 +529,15 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
   }
   P->n_if_batches = nb;
   P->n_if_chunks = (int64_t)chunks.size();
-  // CTA walk of the interior faces (face_kernel.cuh ChunkWalk).  P3: runs of 2 chunks dealt
+  // CTA walk of the interior faces (face_kernel.cuh ChunkWalk).  P3: short chunk runs dealt
   // round-robin, so the CTAs sweep the windows together and the faces of a cell find its
-  // u / y rows in L2 -- measured (profiles/r02/face_runs.jsonl) DG P3 64^3 faces 0.841 ->
-  // 0.755 ms reordered, 0.929 -> 0.776 ms unordered; on the permuted 48^3 mesh +3 %, so small
-  // meshes without locality keep one contiguous run per CTA.  P4's 3-stage ring kernel is
-  // slower with any run length (larger tables to restage: 40^3 0.424 -> 0.459 ms); P2's
-  // resident-table kernel already deals chunks round-robin.  TMF_FACE_RUN (environment,
-  // experiments) overrides.
+  // u / y rows in L2 -- runs of 2 when the numbering has locality (consecutive chunks share
+  // their tables), single chunks when it has not.  Measured with the 128-thread CTAs
+  // (profiles/r02/face_runs.jsonl), DG P3 64^3 faces, run 0 (one contiguous run per CTA, round
+  // 1) / 1 / 2 / 3: reordered 0.84 (256-thread CTAs) / 0.642 / 0.631 / 0.640 ms, unordered
+  // 0.93 / 0.664 / 0.685 / 0.752 ms.  P4's 3-stage ring kernel is slower with any run length
+  // (larger tables to restage: 40^3 0.424 -> 0.459 ms); P2's register-table kernel deals chunks
+  // round-robin.  TMF_FACE_RUN (environment, experiments) overrides.
   {
     int64_t near = 0;
     for (int64_t f = 0; f < nif; ++f) {
@@ -544,7 +545,7 @@ int build_face_batches(tmf_plan* P, const tmf_plan_desc* d, int chunk, size_t* t
       if (r[0] / kFaceWindow == r[2] / kFaceWindow) ++near;
     }
     const bool local = nif > 0 && 2 * near >= nif;
-    P->face_run = (P->N == 20 && d->n_cells > 2 * kFaceWindow && (local || d->n_cells >= (1 << 20))) ? 2 : 0;
+    P->face_run = P->N == 20 ? (local ? 2 : 1) : 0;
     if (const char* e = std::getenv("TMF_FACE_RUN")) P->face_run = std::atoi(e);
   }
   int rc;

@@ -93,8 +93,12 @@ static cudaError_t launch_face_h(const FaceArgs& a, int n_sm, cudaStream_t st, F
     if (variant == 4) return launch_face_a<N, QF, 3, 2, 256, true>(a, n_sm, st);
     if (variant == 5) return launch_face_v<N, QF, false, 1, 3, 256, true, false, false, true>(a, n_sm, st, info);
     if (variant == 10) return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true>(a, n_sm, st, info);
-    // default: full prefetch, face records staged through shared memory (SG: faces -1.9 %)
-    return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 11) return launch_face_v<N, QF, false, 2, 2, 256, true, false, false, true, true>(a, n_sm, st, info);
+    if (variant == 12) return launch_face_v<N, QF, false, 2, 8, 64, true, false, false, true, true>(a, n_sm, st, info);
+    // default: full prefetch, face records staged through shared memory (SG: faces -1.9 %), four
+    // 128-thread CTAs per SM instead of two of 256 (fewer warps wait at each table restage:
+    // DG P3 64^3 faces 0.677 -> 0.631 ms, profiles/r02/face_runs.jsonl)
+    return launch_face_v<N, QF, false, 2, 4, 128, true, false, false, true, true>(a, n_sm, st, info);
   } else if constexpr (N == 10) {
     // P2: both tables of a chunk (2 x 10 fragments) live in REGISTERS, loaded once per chunk from
     // global memory (no table shared memory, no barriers); small CTAs (2 warps, 8 per SM) so a
