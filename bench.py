@@ -286,9 +286,13 @@ def node_shared(world):
     """distributed.NodeShared for this job when it has more than one rank (else None)."""
     if world <= 1:
         return None
+    import atexit
+
     from paper_2509_10226_b200.distributed import NodeShared
 
-    return NodeShared(int(os.environ.get("LOCAL_RANK", "0")), NodeShared.job_token())
+    ns = NodeShared(int(os.environ.get("LOCAL_RANK", "0")), NodeShared.job_token())
+    atexit.register(ns.close)   # a failed run must not leave GBs under /dev/shm
+    return ns
 
 
 def measure_link(problems, reps):
