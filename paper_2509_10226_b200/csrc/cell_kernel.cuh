@@ -130,8 +130,13 @@ struct CellShape {
 // flight without holding registers (measured: pays at P4 only)
 // MT_: 8-cell tiles per warp iteration sharing every B-fragment load (0 = CellShape::MT)
 // MM: mass term as a separate GEMM on the gathered u (CellShape; Helmholtz on the modal tables)
-template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0, bool MM = false>
+// GS (kernels without the ring): the geometry records of the NEXT super-tile are staged one
+// iteration ahead into a per-warp shared-memory slot (one coalesced 16-byte cp.async per lane)
+// and read back as broadcast LDS.64s, instead of three LDG.128s per lane at the tile start
+template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0, bool MM = false,
+          bool GS = false>
 __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
+  static_assert(!GS || AS == 0, "the ring stages the geometry itself");
   static_assert(!(MASS && MM), "the mass term is either in the point loop or a separate GEMM");
   using S = CellShape<N, Q, MASS, MM>;
   constexpr int MT = MT_ ? MT_ : S::MT;
@@ -193,12 +198,30 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
         else
           av[m][kk] = (g >= 0) ? __ldg(a.u + (int64_t)g * a.nc + cmp) : 0.0;
       }
-      const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * (ok ? c : 0));
-      const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
-      G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
-      G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
-      mdet[m] = (MASS || MM) ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
+      if (!GS) {
+        const double2* gp = reinterpret_cast<const double2*>(a.cgeo + 8 * (ok ? c : 0));
+        const double2 g01 = __ldg(gp), g23 = __ldg(gp + 1), g45 = __ldg(gp + 2);
+        G[m][0] = g01.x; G[m][1] = g01.y; G[m][2] = g23.x;
+        G[m][3] = g23.y; G[m][4] = g45.x; G[m][5] = g45.y;
+        mdet[m] = (MASS || MM) ? __ldg(a.cgeo + 8 * (ok ? c : 0) + 6) : 0.0;
+      }
     }
+  };
+  // GS: two slots of MT x 64 doubles per warp behind the tables
+  double* sgeo = smem + S::NFRAG * 32 + (threadIdx.x >> 5) * 2 * MT * 64;
+  int gslot = 0;
+  auto stage_geo = [&](int64_t t) {   // records of super-tile t into the other slot
+    const int cmp = a.nc == 1 ? 0 : (int)(t / cst);
+    gslot ^= 1;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const int64_t c = ((t - (int64_t)cmp * cst) * MT + m) * 8 + cs;
+      const bool ok = t < nst && c < a.n_cells;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(sgeo + (gslot * MT + m) * 64 + cs * 8 + 2 * q4)),
+                   "l"(a.cgeo + 8 * (ok ? c : 0) + 2 * q4), "r"(ok ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   // async ring: per stage MT x (KK x 32 gathered u, 8 cells x 8 geometry doubles, and the
   // KK x 32 gather indices as ints, read back by the scatter)
@@ -229,6 +252,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
     }
   };
   load_indices(st);
+  if (GS) stage_geo(st);
   int slot = 0;
   if (AS > 0) {
 #pragma unroll
@@ -280,6 +304,18 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
       slot = slot + 1 == AS ? 0 : slot + 1;
     } else {
       load_data(st, av, G, mdet);
+      if (GS) {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const double* gg = sgeo + (gslot * MT + m) * 64 + cs * 8;
+#pragma unroll
+          for (int i = 0; i < 6; ++i) G[m][i] = gg[i];
+          mdet[m] = (MASS || MM) ? gg[6] : 0.0;
+        }
+        stage_geo(st + step);   // the other slot: read two iterations ago
+      }
       if (!DG) {
 #pragma unroll
         for (int m = 0; m < MT; ++m)

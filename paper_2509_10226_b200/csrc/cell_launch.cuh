@@ -28,14 +28,16 @@ static cudaError_t persistent_grid(K kern, int block, int smem, int64_t warps_of
 }
 
 // MT_: 8-cell tiles per warp iteration sharing every B-fragment load (0 = CellShape default)
-template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0, bool MM = false>
+template <int N, int Q, bool MASS, bool DG, int BLOCK, bool PEER = false, int AS = 0, int MT_ = 0, bool MM = false,
+          bool GS = false>
 static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, CellLaunchInfo* info) {
   using S = CellShape<N, Q, MASS, MM>;
   constexpr int MT = MT_ ? MT_ : S::MT;
   // tables + the per-warp async rings
-  constexpr int SMEM = S::SMEM + (AS > 0 ? AS * MT * (S::KK * 32 + 64 + S::KK * 16) * 8 * (BLOCK / 32) : 0);
+  constexpr int SMEM = S::SMEM + (AS > 0 ? AS * MT * (S::KK * 32 + 64 + S::KK * 16) * 8 * (BLOCK / 32) : 0) +
+                       (GS ? 2 * MT * 64 * 8 * (BLOCK / 32) : 0);
   static_assert(SMEM <= 227 * 1024, "shared memory");
-  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, PEER, AS, MT_, MM>;
+  auto kern = cell_apply_kernel<N, Q, MASS, DG, BLOCK, PEER, AS, MT_, MM, GS>;
   if (cudaError_t e = opt_in_smem(kern, SMEM); e != cudaSuccess) return e;
   const int64_t supertiles = ((a.n_cells + 8 * MT - 1) / (8 * MT)) * a.nc;
   int64_t blocks = 1;
@@ -115,6 +117,10 @@ static cudaError_t launch_points(const CellArgs& a, int n_sm, cudaStream_t st, C
     if (N == 35) return launch_cell_v<N, Q, MASS, DG, 640, true>(a, n_sm, st, info);
     return launch_cell_v<N, Q, MASS, DG, BLOCK, true>(a, n_sm, st, info);
   }
+  // CG P3 on the modal tables: geometry records staged one tile ahead through shared memory
+  // (GS), 640 threads -- 48^3 0.108 / 0.110 -> 0.104 / 0.106 ms, 96^3 0.728 -> 0.672 ms
+  // (profiles/r02/cell_kernel_experiments.jsonl); DG P3 and CG P2 are slower with it
+  if constexpr (N == 20 && !MASS && !DG && Q < N) return launch_cell_v<N, Q, MASS, DG, 640, false, 0, 0, false, true>(a, n_sm, st, info);
   if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768>(a, n_sm, st, info);
   if constexpr (N == 35 && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, false, 2>(a, n_sm, st, info);
   if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640>(a, n_sm, st, info);
