@@ -117,10 +117,16 @@ static cudaError_t launch_points(const CellArgs& a, int n_sm, cudaStream_t st, C
     if (N == 35) return launch_cell_v<N, Q, MASS, DG, 640, true>(a, n_sm, st, info);
     return launch_cell_v<N, Q, MASS, DG, BLOCK, true>(a, n_sm, st, info);
   }
-  // CG P3 on the modal tables: geometry records staged one tile ahead through shared memory
-  // (GS), 640 threads -- 48^3 0.108 / 0.110 -> 0.104 / 0.106 ms, 96^3 0.728 -> 0.672 ms
-  // (profiles/r02/cell_kernel_experiments.jsonl); DG P3 and CG P2 are slower with it
-  if constexpr (N == 20 && !MASS && !DG && Q < N) return launch_cell_v<N, Q, MASS, DG, 640, false, 0, 0, false, true>(a, n_sm, st, info);
+  // CG P3 on the modal tables.  Up to ~1 M cells (vectors and indices L2-resident): the 2-stage
+  // gather ring, 768 threads; larger meshes: no ring, geometry records staged one tile ahead
+  // through shared memory (GS), 640 threads.  48^3 reordered 0.108 -> 0.100 ms (ring; GS 0.103),
+  // 96^3 0.728 -> 0.672 ms (GS; ring 0.693): profiles/r02/cell_kernel_experiments.jsonl.  (Before
+  // the scatter reused the gather's indices the ring lost 5-8 % at P3.)  DG P3 and CG P2 are
+  // slower with either.
+  if constexpr (N == 20 && !MASS && !DG && Q < N) {
+    if (a.n_cells <= 1000000) return launch_cell_v<N, Q, MASS, DG, 768, false, 2>(a, n_sm, st, info);
+    return launch_cell_v<N, Q, MASS, DG, 640, false, 0, 0, false, true>(a, n_sm, st, info);
+  }
   if (N == 20 && !MASS) return launch_cell_v<N, Q, MASS, DG, 768>(a, n_sm, st, info);
   if constexpr (N == 35 && Q < N) return launch_cell_v<N, Q, MASS, DG, 512, false, 2>(a, n_sm, st, info);
   if (N == 35 && !DG) return launch_cell_v<N, Q, MASS, DG, 640>(a, n_sm, st, info);
