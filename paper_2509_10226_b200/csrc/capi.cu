@@ -760,19 +760,41 @@ int debug_flag_check(tmf_plan* P, cudaStream_t st) {
 }
 #endif
 
+// TMF_PDL=0 (read once): cudaMemsetAsync + a plain cell-kernel launch instead of the clear
+// kernel with its programmatic dependent (launch_apply)
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TMF_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // y_zeroed: the caller already cleared y (CG); energy: += sum_e u_e^T A_e u_e + the identity
 // rows' u_i^2 (= u.Au when the tensor cell engine runs; PCG's fused p.Ap)
 int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaEvent_t* ev,
                  bool y_zeroed = false, double* energy = nullptr) {
   bool ok = true;
   if (ev) TMF_CUDA(cudaEventRecord(ev[0], st));
-  if (!P->dg && !y_zeroed) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
-  if (P->blk_B && !P->peer.u) {
-    TMF_CUDA(tmf::launch_cell_block(P->N, P->block_args(u, y, energy), P->blk_tab.data(), st));
-  } else {
-    tmf::CellArgs ca = P->cell_args(u, y);
-    ca.energy = energy;
-    TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, ca, P->n_sm, st, nullptr, &ok, P->kengine));
+  // CG: y is cleared by a kernel that releases its dependents at once, and the cell kernel is
+  // launched as its programmatic dependent (its launch, table staging and first gathers
+  // overlap the clear; it waits before its first RED).  TMF_PDL=0: cudaMemsetAsync + plain launch.
+  const bool pdl = pdl_enabled() && !P->dg && !y_zeroed && P->n_cells > 0;
+  if (pdl) TMF_CUDA(tmf::launch_zero(y, P->n_global, P->n_sm, st));
+  else if (!P->dg && !y_zeroed) TMF_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * P->n_global, st));
+  struct PdlScope {
+    explicit PdlScope(bool on) { tmf::tl_pdl = on; }
+    ~PdlScope() { tmf::tl_pdl = false; }
+  };
+  {
+    PdlScope scope(pdl);
+    if (P->blk_B && !P->peer.u) {
+      TMF_CUDA(tmf::launch_cell_block(P->N, P->block_args(u, y, energy), P->blk_tab.data(), st));
+    } else {
+      tmf::CellArgs ca = P->cell_args(u, y);
+      ca.energy = energy;
+      TMF_CUDA(tmf::launch_cell(P->N, P->Qk, P->mass, P->dg, ca, P->n_sm, st, nullptr, &ok, P->kengine));
+    }
   }
   // stage events only between kernels that exist (an event record between two empty
   // stages still costs ~3 us of GPU time, which would inflate the measured apply)
@@ -1340,7 +1362,7 @@ int tmf_plan_create(const tmf_plan_desc* d, tmf_plan** out) {
   }
   P->info.n_global_dofs = P->n_global;
   P->info.kernels_per_apply = 1 + (faces ? ((P->n_if_batches ? 1 : 0) + (P->n_bf_batches ? 1 : 0)) : 0) +
-                              ((!dg && P->n_fix) ? 1 : 0);
+                              ((!dg && P->n_fix) ? 1 : 0) + ((!dg && pdl_enabled()) ? 1 : 0);   // + the y clear kernel
   P->dev_bytes = total;
   P->info.device_bytes = (int64_t)total;
   TMF_CUDA(cudaDeviceSynchronize());

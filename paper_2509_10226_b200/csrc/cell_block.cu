@@ -45,8 +45,7 @@ static cudaError_t launch_block_n(const BlockArgs& a, const double* tab, cudaStr
   // the whole unified L1 / shared array as shared memory (several CTAs per SM)
   if (cudaError_t e = opt_in_smem(kern, 227 * 1024, true); e != cudaSuccess) return e;
   if (a.n_blocks == 0) return cudaSuccess;
-  kern<<<(unsigned)a.n_blocks, C::BLOCK, smem, st>>>(a, T);
-  return cudaGetLastError();
+  return launch_kernel(kern, (unsigned)a.n_blocks, C::BLOCK, smem, st, a, T);
 }
 
 cudaError_t launch_cell_block(int n_dpc, const BlockArgs& a, const double* host_tab, cudaStream_t st) {

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_block_kernel(BlockArgs a, co
 #pragma unroll
     for (int j = 0; j < N; ++j) R[j * B + cl] = yy[j];
   }
+  pdl_wait_prior_grid();   // y cleared (common.cuh); phases 1-2 do not touch y
   __syncthreads();
 
   // ---- phase 3: one thread per unique DoF, its slots summed in list order, one RED

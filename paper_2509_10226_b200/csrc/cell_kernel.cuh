@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(BLOCK, 1) cell_apply_kernel(CellArgs a) {
   constexpr bool EN = !DG && Q < N;
   double en = 0.0;
 
+  if (!DG) pdl_wait_prior_grid();   // y cleared (common.cuh); nothing above touches y
   for (; st < nst; st += step) {
     const int comp = a.nc == 1 ? 0 : (int)(st / cst);
     int64_t cell[MT];

@@ -54,8 +54,7 @@ static cudaError_t launch_cell_v(const CellArgs& a, int n_sm, cudaStream_t st, C
     return cudaSuccess;
   }
   if (a.n_cells == 0) return cudaSuccess;
-  kern<<<(unsigned)blocks, BLOCK, SMEM, st>>>(a);
-  return cudaGetLastError();
+  return launch_kernel(kern, (unsigned)blocks, BLOCK, SMEM, st, a);
 }
 
 // Reference-tensor engine (cell_tensor_kernel.cuh)
@@ -80,8 +79,7 @@ static cudaError_t launch_cell_x(const CellArgs& a, int n_sm, cudaStream_t st, C
     return cudaSuccess;
   }
   if (a.n_cells == 0) return cudaSuccess;
-  kern<<<(unsigned)blocks, BLOCK, S::SMEM, st>>>(a);
-  return cudaGetLastError();
+  return launch_kernel(kern, (unsigned)blocks, BLOCK, S::SMEM, st, a);
 }
 
 // Per-degree CTA shapes, measured on 48^3 (CG reordered) / 64^3 (DG) meshes in round 1

@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) cell_tensor_kernel(CellArgs a) {
   };
   double en = 0.0;   // sum of u_i y_i over the lane's outputs (element energies, CG)
 
+  if (!DG) pdl_wait_prior_grid();   // y cleared (common.cuh); nothing above touches y
   for (; st < nst; st += step) {
     const int comp = a.nc == 1 ? 0 : (int)(st / cst);
     int64_t cell[MT];

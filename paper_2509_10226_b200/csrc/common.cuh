@@ -32,6 +32,14 @@ namespace tmf {
   do {                              \
   } while (0)
 #endif
+// Programmatic dependent launch (launch_apply): the CG apply clears y with zero_y_kernel, which
+// lets its dependents start at once; the cell kernel, launched with programmatic stream
+// serialization, stages its tables and issues its first index / gather loads meanwhile and
+// waits here -- before its first RED into y -- for the clear to complete and be visible.
+// Without the launch attribute the wait returns immediately.
+__device__ __forceinline__ void pdl_wait_prior_grid() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 enum : int {
   TMF_DBG_DOF = 1,        // gathered / scattered vector index out of range
   TMF_DBG_CELL = 2,       // cell index out of range

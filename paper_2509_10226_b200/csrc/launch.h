@@ -41,6 +41,11 @@ cudaError_t launch_cell_geometry(const CellGeoArgs& a, int n_sm, cudaStream_t st
 // and the launch (host_tab: the M x 3 x n_dpc modal table, passed as a kernel parameter)
 int block_cells_for(int n_dpc);
 cudaError_t launch_cell_block(int n_dpc, const BlockArgs& a, const double* host_tab, cudaStream_t st);
+// Clear y ahead of a CG cell kernel (zero_y_kernel: releases its dependents at once).  While
+// tl_pdl is set on the calling thread the cell launchers launch with programmatic stream
+// serialization, so the kernel's prologue overlaps the clear (common.cuh pdl_wait_prior_grid).
+extern thread_local bool tl_pdl;
+cudaError_t launch_zero(double* y, int64_t n, int n_sm, cudaStream_t st);
 cudaError_t launch_fixup(const double* u, double* y, const int* list, int64_t n, int n_sm,
                          cudaStream_t st, double* energy = nullptr);
 

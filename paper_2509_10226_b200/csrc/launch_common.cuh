@@ -5,6 +5,8 @@
 #include <mutex>
 #include <unordered_map>
 
+#include "launch.h"
+
 namespace tmf {
 
 // Dynamic shared memory above 48 KB needs a per-kernel, per-DEVICE opt-in; remember
@@ -71,6 +73,27 @@ static cudaError_t blocks_per_sm(K kern, int block, size_t smem, int* out) {
   cache[key] = per_sm;
   *out = per_sm;
   return cudaSuccess;
+}
+
+// Launch, as a programmatic dependent of the stream's previous kernel when tl_pdl is set
+template <typename... KA, typename... A>
+static cudaError_t launch_kernel(void (*kern)(KA...), unsigned grid, int block, size_t smem, cudaStream_t st,
+                                 const A&... args) {
+  if (!tl_pdl) {
+    kern<<<grid, block, smem, st>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 }  // namespace tmf

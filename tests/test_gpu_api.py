@@ -321,3 +321,44 @@ def test_geometry_mode_and_precision_boundary():
     with pytest.raises(ValueError, match="f32"):
         op.DgSipgOperator(mesh, dofmap, geo, basis, op.SipgConfig(1.0, gd["tau_i"], gd["tau_b"]),
                           op.OperatorConfig(precision="f32"))
+
+
+@pytest.mark.parametrize("name", ["cg_p1_n4_ref", "cg_p2_n8_gm_dir", "cg_p3_n4_ref_dir", "cg_p4_n3_gm_dir"])
+def test_y_clear_kernel_unaligned_and_stale_output(name):
+    """The CG apply clears y with its own kernel (16-byte stores behind an 8-byte head / tail) and
+    launches the cell kernel as its programmatic dependent: a y that starts 8 bytes off a 16-byte
+    boundary and holds stale values must come out the same, with the neighbouring entries untouched."""
+    import torch
+
+    g = load_golden(name)
+    A = operator_from_fixture(g)
+    n = A.n_global_dofs
+    u = torch.from_numpy(g["u"]).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    for off in (0, 1):
+        buf = torch.full((n + 4,), 7.5, dtype=torch.float64, device="cuda")
+        y = buf[off + 1: off + 1 + n]
+        for _ in range(3):   # repeated applies: the clear must not race the previous apply's REDs
+            A.apply_into(u.data_ptr(), y.data_ptr(), st)
+        torch.cuda.synchronize()
+        assert rel_l2(y.cpu().numpy(), g["y"]) <= 1e-12
+        assert float(buf[off]) == 7.5 and float(buf[off + 1 + n]) == 7.5
+
+
+def test_plain_launch_path_matches(tmp_path):
+    """TMF_PDL=0 (cudaMemsetAsync + plain launch) gives the same y as the default dependent launch."""
+    import os
+    import subprocess
+    import sys
+
+    g = load_golden("cg_p2_n8_gm_dir")
+    y_pdl = operator_from_fixture(g).apply(g["u"])
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r);"
+            "from conftest import load_golden; from helpers import operator_from_fixture;"
+            "g = load_golden('cg_p2_n8_gm_dir'); np.save(%r, operator_from_fixture(g).apply(g['u']))"
+            % (root, os.path.join(root, "tests"), str(tmp_path / "y.npy")))
+    subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, TMF_PDL="0"), timeout=300)
+    y_plain = np.load(tmp_path / "y.npy")
+    assert rel_l2(y_plain, g["y"]) <= 1e-12
+    assert rel_l2(y_plain, y_pdl) <= 1e-14
