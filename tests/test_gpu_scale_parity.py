@@ -189,3 +189,37 @@ def test_c5_jacobi_pcg_p3_24cubed_history():
     assert np.allclose(hist, hr, rtol=1e-6, atol=0)
     assert rel_l2(x.cpu().numpy(), xr) <= 1e-6
     assert hist[-1] < 1e-2 * hist[0]
+
+
+@pytest.mark.parametrize("kind", ["dg", "helmk"])
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_dg_cell_kernels_are_bitwise_repeatable(p, kind):
+    """Race smoke test (no racecheck on this pool, DESIGN 3.3): the DG cell kernels store their
+    rows (no REDs), so repeated launches must agree BIT FOR BIT; a race in the per-warp cp.async
+    gather rings (DG P2 / P4, Helmholtz P2) or the staged tables would show up as run-to-run
+    differences.  24^3 x 6 cells: several tiles per warp, the rings wrap."""
+    import torch
+
+    from paper_2509_10226_b200 import _lib, dofmap as D, operator as op
+
+    n = 24
+    m = _mesh(n, True)
+    geo, bas = _tables(p)
+    dm = D.build_dof_map(m, p, "dg")
+    sipg = op.baseline_sipg_tau(m, p, 1.0 / n)
+    if kind == "dg":
+        A = op.DgSipgOperator(m, dm, geo, bas, sipg, dirichlet_ids=range(6))
+    else:
+        kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells)
+        A = op.KappaHelmholtzOperator(m, dm, geo, bas, sipg, kap, 1.0, dirichlet_ids=range(6))
+    u = torch.from_numpy(np.random.default_rng(p).uniform(-1, 1, dm.n_global_dofs)).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    ys = []
+    for _ in range(6):
+        y = torch.full_like(u, float("nan"))
+        A.apply_stages(u.data_ptr(), y.data_ptr(), _lib.STAGE_CELLS, stream=st)
+        torch.cuda.synchronize()
+        ys.append(y)
+    assert bool(torch.isfinite(ys[0]).all())
+    for y in ys[1:]:
+        assert torch.equal(y, ys[0])
