@@ -89,6 +89,7 @@ def shared_config(args, world):
                         f"exact to 2p, fp64, unordered + hierarchically reordered (8 applies per step)",
             "global_mesh": f"{n}^3 x 6", "degrees": list(DEGREES), "orderings": ["unordered", "reordered"],
             "seeds": {"mesh": 0, "u": 1},
+            "l2": "B200 arm: L2 flushed (256 MiB write) before every timed apply; CPU arm: no flush",
             "parallelism": "single GPU" if world == 1 else
             f"{world}-way RCB domain decomposition, weak scaling (~{args.n}^3 x 6 cells per GPU)"}
 
