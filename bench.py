@@ -544,7 +544,10 @@ def gpu_bench(args, rank, world):
                  "reference's point sums, DESIGN §4) / CUDA-event kernel time / FP64 peak.  frac_alg uses SURVEY "
                  "§8(d)'s F_alg (the reference's n_q-point counter formula), which the modal form does not "
                  "execute: it exceeds 1 because the same apply needs 3.6x fewer flops.  bytes_alg is §8(d)'s "
-                 "compulsory HBM traffic; every config is FP64-bound")}
+                 "compulsory HBM traffic; every config is FP64-bound.  kernel_ms = CUDA events around the y-clear kernel "
+                 "and the cell kernel, its programmatic dependent (an event between the two would undo the "
+                 "overlap): the cell kernel alone is ~10 us shorter at P4 (ncu launch list), so frac is a "
+                 "lower bound")}
     kernels = sum(pr["local"].info["kernels_per_apply"] for pr in problems) * args.steps
     quad = None
     if not dist_path and not args.no_quadrature:
