@@ -1,8 +1,10 @@
 """Geometry container mirroring the reference ``GeometryData`` (geometry.py:31-74).
 
-The GPU kernels recompute every geometric factor (J, det J, J^-T, face normals,
-surface JxW, m = J^-1 n) from vertex coordinates on the fly, so the only
-fields the operators read are the quadrature rules.  :func:`build_geometry`
+The plan computes every geometric factor itself from the vertex coordinates, once, at plan
+creation (``cell_geometry_kernel`` / ``face_geometry_kernel``: 64-byte cell records G = det J
+J^-1 J^-T and the mass factor, and the face records; the P1 block kernel recomputes G from
+staged vertices instead), so the only fields the operators read from this container are
+``mode`` (must be "affine") and the quadrature rules.  :func:`build_geometry`
 still fills the affine arrays (vectorised restatement of geometry.py:145-151,
 202-240, with the reference's compact per-face storage) so that code written
 against the reference (e.g. ``compute_sipg_tau``) keeps working.
