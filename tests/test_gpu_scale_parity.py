@@ -263,3 +263,38 @@ def test_three_component_cg_value_parity(p):
     for c in range(3):
         ref = _cg_oracle(m, dm, geo, bas, uc[:, c])
         assert rel_l2(y[:, c], ref) <= 1e-12
+
+
+@pytest.mark.parametrize("p,n", [(1, 24), (2, 24), (3, 24), (4, 24), (1, 48), (4, 48)])
+def test_dependent_launch_clear_is_ordered_before_the_scatter(p, n):
+    """Stress test of the y clear + programmatic dependent cell kernel (DESIGN 4.8): 40 applies
+    back to back into a y refilled with garbage each time.  A RED that landed before the clear
+    would be lost (or a stale value survive): every result must match the oracle-checked first
+    one to RED-order round-off.  24^3: the P1 block kernel's CTAs are all resident while the
+    clear runs (largest overlap); 48^3 P4: the longest clear."""
+    import torch
+
+    from paper_2509_10226_b200 import dofmap as D, operator as op
+
+    m = _mesh(n, True)
+    geo, bas = _tables(p)
+    dm = D.build_dof_map(m, p, "cg")
+    A = op.CgPoissonOperator(m, dm, geo, bas)
+    u = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, dm.n_global_dofs)).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    y0 = torch.empty_like(u)
+    A.apply_into(u.data_ptr(), y0.data_ptr(), st)
+    if n <= 24:
+        ref = _cg_oracle(m, dm, geo, bas, u.cpu().numpy())
+        assert rel_l2(y0.cpu().numpy(), ref) <= 1e-12
+    ys = [torch.empty_like(u) for _ in range(4)]
+    worst = 0.0
+    for r in range(10):
+        for y in ys:
+            y.fill_(1e300 if r % 2 else -7.0)
+        for y in ys:                       # four applies queued back to back
+            A.apply_into(u.data_ptr(), y.data_ptr(), st)
+        torch.cuda.synchronize()
+        for y in ys:
+            worst = max(worst, float(torch.linalg.vector_norm(y - y0) / torch.linalg.vector_norm(y0)))
+    assert worst <= 1e-13
