@@ -801,6 +801,10 @@ int launch_apply(tmf_plan* P, const double* u, double* y, cudaStream_t st, cudaE
   const bool fix = !P->dg && P->n_fix;
   if (ev && (P->faces || fix)) TMF_CUDA(cudaEventRecord(ev[1], st));
   if (P->faces) {
+    // DG: each face kernel is the programmatic dependent of the kernel before it (its CTAs set up
+    // while that one drains; they wait before touching y).  A stage event in between (timed
+    // applies) makes the first one an ordinary launch again.
+    PdlScope scope(pdl_enabled() && P->n_cells > 0);
     TMF_CUDA(tmf::launch_face(P->N, P->QFk, false, P->face_args(u, y, false), P->n_sm, st, nullptr, &ok));
     TMF_CUDA(tmf::launch_face(P->N, P->QFk, true, P->face_args(u, y, true), P->n_sm, st, nullptr, &ok));
   }

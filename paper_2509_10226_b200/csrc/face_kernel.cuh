@@ -439,6 +439,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_apply_kernel(FaceArgs a) {
     for (int i = threadIdx.x; i < 24 * S::NFRAG * 16; i += blockDim.x) dst[i] = __ldg(src + i);
     __syncthreads();
   }
+  // launched as the programmatic dependent of the kernel before it (launch_apply): the CTA and
+  // its resident tables are set up while that kernel drains; its stores / REDs into y are
+  // complete and visible from here on (no-op without the launch attribute)
+  pdl_wait_prior_grid();
   const int lane = threadIdx.x & 31;
   const int fs = lane >> 2;
   const int q4 = lane & 3;
@@ -672,6 +676,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) face_async_kernel(FaceArgs a) {
   constexpr int NW = BLOCK / 32;
   double* ring = smem + 2 * S::NFRAG * 32 + (4 * N + 1) / 2 + (threadIdx.x >> 5) * AS * SLOT;
   for (int i = threadIdx.x; i < 4 * N; i += BLOCK) sperm[i] = __ldg(a.perm + i);
+  pdl_wait_prior_grid();   // see face_apply_kernel
   __syncthreads();   // the prologue's gathers read sperm
   const int lane = threadIdx.x & 31;
   const int fs = lane >> 2;

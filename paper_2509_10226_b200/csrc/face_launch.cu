@@ -33,8 +33,7 @@ static cudaError_t launch_face_v(const FaceArgs& a, int n_sm, cudaStream_t st, F
   if (work == 0) return cudaSuccess;
   int64_t blocks = (int64_t)n_sm * per_sm;
   if (blocks > work) blocks = work;
-  kern<<<(unsigned)blocks, BLOCK, SMEM, st>>>(a);
-  return cudaGetLastError();
+  return launch_kernel(kern, (unsigned)blocks, BLOCK, SMEM, st, a);
 }
 
 // interior faces with the asynchronous gather ring (face_async_kernel), blocked chunk runs
@@ -56,8 +55,7 @@ static cudaError_t launch_face_a(const FaceArgs& a, int n_sm, cudaStream_t st) {
     if (work == 0) return cudaSuccess;
     int64_t blocks = (int64_t)n_sm * per_sm;
     if (blocks > work) blocks = work;
-    kern<<<(unsigned)blocks, BLOCK, SMEM, st>>>(a);
-    return cudaGetLastError();
+    return launch_kernel(kern, (unsigned)blocks, BLOCK, SMEM, st, a);
   }
 }
 

@@ -298,3 +298,42 @@ def test_dependent_launch_clear_is_ordered_before_the_scatter(p, n):
         for y in ys:
             worst = max(worst, float(torch.linalg.vector_norm(y - y0) / torch.linalg.vector_norm(y0)))
     assert worst <= 1e-13
+
+
+@pytest.mark.parametrize("kind,p,n", [("dg", 3, 16), ("helmk", 2, 24), ("dg", 1, 24)])
+def test_dg_dependent_launch_chain_is_ordered(kind, p, n):
+    """The DG face kernels are programmatic dependents of the kernel before them (cell -> interior
+    faces -> boundary faces): queued applies into garbage-filled y must all match the
+    oracle-checked first result to RED-order round-off (a face RED overtaken by the cell kernel's
+    row store would be lost)."""
+    import torch
+
+    from paper_2509_10226_b200 import dofmap as D, operator as op
+
+    m = _mesh(n, True)
+    geo, bas = _tables(p)
+    dm = D.build_dof_map(m, p, "dg")
+    sipg = op.baseline_sipg_tau(m, p, 1.0 / n)
+    kap = 10.0 ** np.random.default_rng(2).uniform(-1, 1, m.n_cells) if kind == "helmk" else None
+    if kind == "dg":
+        A = op.DgSipgOperator(m, dm, geo, bas, sipg, dirichlet_ids=range(6))
+    else:
+        A = op.KappaHelmholtzOperator(m, dm, geo, bas, sipg, kap, 1.0, dirichlet_ids=range(6))
+    un = np.random.default_rng(3).uniform(-1, 1, dm.n_global_dofs)
+    u = torch.from_numpy(un).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    y0 = torch.empty_like(u)
+    A.apply_into(u.data_ptr(), y0.data_ptr(), st)
+    ref = _dg_oracle(m, dm, geo, bas, sipg, range(6), un, kappa=kap, mass_scale=1.0 if kind == "helmk" else 0.0)
+    assert rel_l2(y0.cpu().numpy(), ref) <= 1e-12
+    ys = [torch.empty_like(u) for _ in range(4)]
+    worst = 0.0
+    for r in range(8):
+        for y in ys:
+            y.fill_(1e300 if r % 2 else -7.0)
+        for y in ys:
+            A.apply_into(u.data_ptr(), y.data_ptr(), st)
+        torch.cuda.synchronize()
+        for y in ys:
+            worst = max(worst, float(torch.linalg.vector_norm(y - y0) / torch.linalg.vector_norm(y0)))
+    assert worst <= 1e-13
